@@ -1,0 +1,146 @@
+"""Pins for oracle.cg and oracle.exact: exact solves, library CG, textbook CG invariants."""
+
+import numpy as np
+import pytest
+import scipy.sparse.linalg as spla
+
+from oracle import cg, exact, model
+from synth import make_config, make_patch
+
+
+def rel(a, b):
+    return float(np.linalg.norm(a - b) / np.linalg.norm(b))
+
+
+@pytest.fixture(scope="module")
+def tiny():
+    p = make_config("tiny")[0]
+    G, b = model.problem_system(p)
+    return p, G, b
+
+
+def test_dct_exact_equals_dense_cholesky(tiny):
+    p, G, b = tiny
+    x_dense = exact.dense_solve(G, b)
+    x_dct = exact.problem_dct_exact(p)
+    assert rel(x_dct, x_dense) <= 1e-12
+    assert np.linalg.norm(G @ x_dense - b) <= 1e-12 * np.linalg.norm(b)
+
+
+def test_dense_guard():
+    p = make_patch(6, 9, 3, seed=0)
+    G, b = model.problem_system(p)
+    with pytest.raises(MemoryError):
+        exact.dense_solve(G, b)
+
+
+def test_cg_tiny_matches_exact_and_scipy(tiny):
+    p, G, b = tiny
+    res = cg.cg_hs(G, b, tol=1e-10)
+    assert res.converged
+    x_star = exact.dense_solve(G, b)
+    assert rel(res.x, x_star) <= 1e-8
+    assert np.linalg.norm(b - G @ res.x) <= 1.01e-10 * np.linalg.norm(b) * 1.5
+    # scipy's CG is an independent implementation of the same textbook iteration
+    its = []
+    x_sp, info = spla.cg(G, b, rtol=1e-10, atol=0.0, maxiter=10000,
+                         callback=lambda xk: its.append(1))
+    assert info == 0
+    assert abs(len(its) - res.iterations) <= 1
+    assert rel(res.x, x_sp) <= 1e-9
+    assert len(res.history) == res.iterations
+    assert res.history[-1] <= 1e-10 < res.history[-2]
+
+
+def test_cg_zero_rhs():
+    p = make_patch(3, 9, 3, seed=0)
+    G, b = model.problem_system(p)
+    res = cg.cg_hs(G, np.zeros_like(b))
+    assert res.iterations == 0 and res.converged and not res.x.any()
+    res2 = cg.cg_single_pass(G, np.zeros_like(b))
+    assert res2.iterations == 0 and res2.converged
+
+
+def test_finite_termination_level1():
+    # mN = 8: CG terminates in at most mN iterations
+    p = make_patch(1, 3, 2, seed=2, tau="given", tau_values=[1.0, 3.0])
+    G, b = model.problem_system(p)
+    res = cg.cg_hs(G, b, tol=1e-12)
+    assert res.converged and res.iterations <= 8
+
+
+def test_energy_norm_monotone_and_orthogonality():
+    p = make_patch(2, 9, 3, seed=4)
+    G, b = model.problem_system(p)
+    x_star = exact.dense_solve(G, b)
+    errs, rs = [], []
+
+    def cb(j, x, r):
+        e = x - x_star
+        errs.append(float(e @ (G @ e)))
+        rs.append(r.copy())
+
+    cg.cg_hs(G, b, tol=1e-14, max_iter=200, callback=cb)
+    e0 = float(x_star @ (G @ x_star))
+    seq = [e0] + errs
+    assert all(seq[i + 1] <= seq[i] * (1 + 1e-12) + 1e-300 for i in range(len(seq) - 1))
+    R = [b] + rs[:10]
+    for i in range(len(R)):
+        for j in range(i):
+            c = abs(R[i] @ R[j]) / (np.linalg.norm(R[i]) * np.linalg.norm(R[j]))
+            assert c <= 1e-8
+
+
+def test_linearity(tiny):
+    p, G, b = tiny
+    r1 = cg.cg_hs(G, b, tol=1e-10)
+    r2 = cg.cg_hs(G, 3.5 * b, tol=1e-10)
+    assert r1.iterations == r2.iterations
+    assert rel(r2.x, 3.5 * r1.x) <= 1e-12
+
+
+def test_single_pass_variant_like_hs(tiny):
+    p, G, b = tiny
+    hs = cg.cg_hs(G, b, tol=1e-10)
+    sp1 = cg.cg_single_pass(G, b, tol=1e-10)
+    assert sp1.converged and abs(sp1.iterations - hs.iterations) <= 1
+    assert rel(sp1.x, hs.x) <= 1e-10
+
+
+def test_block_jacobi_precond(tiny):
+    p, G, b = tiny
+    K = cg.block_jacobi_precond(p.level, p.A, p.noise_prec, p.tau, p.kappa2)
+    hs = cg.cg_hs(G, b, tol=1e-10)
+    pc = cg.cg_hs(G, b, tol=1e-10, precond=K)
+    sp1 = cg.cg_single_pass(G, b, tol=1e-10, precond=K)
+    x_star = exact.dense_solve(G, b)
+    assert pc.converged and pc.iterations < hs.iterations
+    assert rel(pc.x, x_star) <= 1e-8
+    assert abs(sp1.iterations - pc.iterations) <= 1 and rel(sp1.x, x_star) <= 1e-8
+
+
+def test_breakdown_detected_on_indefinite():
+    import scipy.sparse as sp
+    G = sp.diags([1.0, -1.0, 2.0]).tocsr()
+    b = np.array([1.0, 1.0, 0.0])
+    assert cg.cg_hs(G, b).status == "breakdown"
+
+
+@pytest.mark.slow
+def test_cg_medium_matches_dct_exact():
+    p = make_config("medium")[0]
+    G, b = model.problem_system(p)
+    res = cg.cg_hs(G, b, tol=1e-10)
+    x_star = exact.problem_dct_exact(p)
+    assert res.converged
+    assert rel(res.x, x_star) <= 1e-8
+
+
+@pytest.mark.parametrize("prior", ["d2"])
+def test_cg_d2_prior_small(prior):
+    p = make_patch(4, 9, 3, seed=9, prior=prior)
+    G, b = model.problem_system(p)
+    res = cg.cg_hs(G, b, tol=1e-10)
+    assert res.converged
+    assert rel(res.x, exact.problem_dct_exact(p)) <= 1e-8
+    assert rel(res.x, exact.dense_solve(G, b)) <= 1e-8

@@ -1,0 +1,78 @@
+"""Pins for oracle.sylvester: Lemma 2, the Kronecker/Sylvester identity, exact solutions."""
+
+import numpy as np
+import pytest
+import scipy.sparse as sp
+
+from oracle import exact, grid, model, sylvester
+from synth import make_config, make_patch
+
+
+def rel(a, b):
+    return float(np.linalg.norm(a - b) / np.linalg.norm(b))
+
+
+def test_lemma2_and_eigen_normalisation():
+    p = make_patch(2, 9, 4, seed=5, tau="loguniform")
+    M, P, rho, W = sylvester.small_factor(p.A, p.noise_prec, p.tau)
+    Shat = M @ np.linalg.inv(P)                       # S^ = A^T T A P^{-1}
+    Pinv = np.linalg.inv(P)
+    # Lemma 2: P^{-1} S^ = S^T P^{-1}
+    assert np.abs(Pinv @ Shat - Shat.T @ Pinv).max() <= 1e-12 * np.abs(Pinv @ Shat).max()
+    assert np.allclose(W.T @ P @ W, np.eye(4), atol=1e-12)
+    assert np.allclose(M @ W, P @ W @ np.diag(rho), atol=1e-9 * np.abs(M).max())
+    assert np.all(np.diff(rho) >= 0) and rho.min() > 0
+    U = P @ W                                          # paper's U: S^ = U R U^{-1}, U^T P^{-1} U = I
+    assert np.allclose(U.T @ Pinv @ U, np.eye(4), atol=1e-12)
+    assert np.allclose(Shat @ U, U @ np.diag(rho), atol=1e-9 * np.abs(Shat).max())
+    for i in range(4):
+        assert W[np.argmax(np.abs(W[:, i])), i] > 0
+
+
+@pytest.mark.parametrize("hits", [None, "random"])
+def test_kronecker_sylvester_identity(hits):
+    # north star: vec(Q0 X P + N_h X M) = (P (x) Q0 + M (x) N_h) vec X = G vec X
+    p = make_patch(3, 9, 4, seed=8, tau="loguniform", hits=hits)
+    G = model.assemble_G(p.level, p.A, p.noise_prec, p.tau, p.kappa2, p.hits)
+    Q0 = model.prior_Q0(p.level, p.kappa2)
+    M = p.A.T @ np.diag(p.noise_prec) @ p.A
+    Nh = sp.diags(np.ones(p.N) if p.hits is None else p.hits.ravel())
+    X = np.random.default_rng(0).standard_normal((p.N, 4))
+    lhs = (Q0 @ X) @ np.diag(p.tau) + (Nh @ X) @ M
+    y = G @ X.T.reshape(-1)
+    assert np.abs(lhs.T.reshape(-1) - y).max() <= 5e-16 * 50 * np.abs(y).max()
+
+
+def test_sylvester_tiny_matches_exact():
+    p = make_config("tiny")[0]
+    res = sylvester.problem_solve(p, tol=1e-10)
+    G, b = model.problem_system(p)
+    x_star = exact.dense_solve(G, b)
+    assert res.converged
+    assert rel(res.x, x_star) <= 1e-8
+    assert rel(res.x, exact.problem_dct_exact(p)) <= 1e-8
+    assert len(res.iterations) == 3 and all(i > 0 for i in res.iterations)
+
+
+def test_sylvester_with_hits_matches_dense():
+    p = make_patch(4, 9, 3, seed=12, hits="random")
+    res = sylvester.problem_solve(p, tol=1e-11)
+    G, b = model.problem_system(p)
+    assert rel(res.x, exact.dense_solve(G, b)) <= 1e-8
+
+
+def test_sylvester_k1_is_single_shifted_system():
+    p = make_patch(3, 4, 1, seed=1, tau="given", tau_values=[3.0])
+    M, P, rho, W = sylvester.small_factor(p.A, p.noise_prec, p.tau)
+    m = float(p.A[:, 0] @ (p.noise_prec * p.A[:, 0]))
+    assert np.isclose(rho[0], m / 3.0) and np.isclose(W[0, 0], 1 / np.sqrt(3.0))
+    res = sylvester.problem_solve(p)
+    G, b = model.problem_system(p)
+    assert rel(res.x, exact.dense_solve(G, b)) <= 1e-8
+
+
+@pytest.mark.slow
+def test_sylvester_medium_matches_dct():
+    p = make_config("medium")[0]
+    res = sylvester.problem_solve(p, tol=1e-10)
+    assert rel(res.x, exact.problem_dct_exact(p)) <= 1e-8
