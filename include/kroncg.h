@@ -1,0 +1,159 @@
+/*
+ * kroncg.h -- C ABI of the B200 (sm_100a, fp64) Krylov solver for the Kronecker-structured
+ * posterior-mean system of arxiv 2204.08057 (Bayesian CMB source separation).
+ *
+ * The operation (PAPER.md = /root/reference/PAPER.md, "P:Lnnn" = line):
+ *   (Q + B^T C B) mu = B^T C Y                                   Eq.(Axb), Eq.(mu*) P:L78-82
+ *   B = A (x) I_N,  C = T (x) N_h,  Q = P (x) Q0
+ * per HEALPix base face ("patch", App. A) of N = 4^level pixels on a 2^level x 2^level
+ * grid with free boundary (reading R2).  In matrix form, with X = reshape(mu, N, k):
+ *   G vec(X) = vec( N_h X M + Q0 X P ),   M = A^T T A,   P = diag(prior_scale),
+ *   b        = vec( N_h Y T A ),
+ *   Q0 = kappa2 I + L  (KCG_PRIOR_LAPLACIAN; BASELINE configs, reading R3/R24),
+ *   L  = graph Laplacian of the 4-neighbour face grid = -D of P:L100-106.
+ *
+ * Routes:
+ *   kron_cg_solve    -- CG applied directly to G (Sec. 3.2), single-pass variant.
+ *   sylvester_solve  -- Sylvester reformulation (Sec. 3.3), small factor diagonalised
+ *                       once (Lemma 2): (Q0 + rho_i N_h) xt_i = ft_i, Ft = F W,
+ *                       X = Xt W^T, all k shifted systems of all patches in ONE batched launch.
+ *
+ * Conventions (all entry points):
+ *   - "_dev" pointers are CUDA device pointers, "_host" pointers are host memory.  Every buffer,
+ *     including the workspace, is owned by the caller; the library never allocates device memory.
+ *   - Layouts are C-contiguous, fp64:
+ *       A_host            [P][n][k]   (A[p][f][c] = mixing of component c into map f)
+ *       noise_prec_host   [P][n]      (T = 1/sigma^2, > 0)
+ *       prior_scale_host  [P][k]      (paper phi_l = config tau_i, > 0)
+ *       kappa2_host       [P]         (>= 0; kappa2 = 0 with hits = 1 still gives SPD G as M SPD)
+ *       hits_dev          [P][side][side] (> 0) or NULL for all ones
+ *       Y                 [P][n][side][side]   row-major pixels idx = y*side + x (reading R1)
+ *       mu / x / y        [P][k][side][side]
+ *   - Calls are stream-ordered on the stream given at create and BLOCKING: they return after the
+ *     report is on the host.  One solve at a time per context (not thread-safe).
+ *   - x0 = 0; a system stops after the first iteration j with ||r_j||_2 <= tol ||b||_2 on the
+ *     recursively updated residual (reading R8); iterations = number of x-updates.
+ *     ||b|| = 0 gives mu = 0 after 0 iterations.  Y is never modified.
+ *   - Errors: KCG_E_ARG (null pointer, tol <= 0, max_iter < 0, non-positive T/phi/hits,
+ *     kappa2 < 0, non-finite scalars), KCG_E_SHAPE / KCG_E_CONFIG (descriptor out of range,
+ *     workspace too small, unsupported combination), KCG_NOT_CONVERGED (max_iter reached: mu
+ *     holds the last iterate; not fatal), KCG_E_BREAKDOWN (p^T G p <= 0 -- G not SPD),
+ *     KCG_E_NONFINITE (NaN/Inf met during the iteration), KCG_E_CUDA (a CUDA call failed;
+ *     kcg_last_error() has the text).
+ */
+#ifndef KRONCG_H
+#define KRONCG_H
+
+#include <stddef.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#if defined(__GNUC__)
+#define KCG_API __attribute__((visibility("default")))
+#else
+#define KCG_API
+#endif
+
+typedef struct kcg_ctx kcg_ctx;
+
+typedef enum {
+  KCG_OK = 0,
+  KCG_NOT_CONVERGED = 1,
+  KCG_E_ARG = 2,
+  KCG_E_SHAPE = 3,
+  KCG_E_CONFIG = 4,
+  KCG_E_NONFINITE = 5,
+  KCG_E_BREAKDOWN = 6,
+  KCG_E_CUDA = 7,
+  KCG_E_NCCL = 8,
+  KCG_E_STATE = 9
+} kcg_status;
+
+enum { KCG_PRIOR_LAPLACIAN = 0, KCG_PRIOR_D2 = 1 };
+enum { KCG_LAYOUT_ROW_MAJOR = 0, KCG_LAYOUT_NESTED = 1 };
+enum { KCG_PRECOND_NONE = 0, KCG_PRECOND_BLOCK_JACOBI = 1 };
+
+/* Problem descriptor (fixed for the life of a context). */
+typedef struct {
+  int level;        /* face grid 2^level x 2^level, N = 4^level; 0 <= level <= 12 (App. A)  */
+  int n_freq;       /* n, number of frequency maps; 1 <= n <= 64                                  */
+  int n_comp;       /* k (paper m), number of sources; 1 <= k <= 8 and k <= n                      */
+  int n_patches;    /* independent faces in this context (1..64)                                  */
+  int prior;        /* KCG_PRIOR_LAPLACIAN (only value supported in this build)                    */
+  int layout;       /* KCG_LAYOUT_ROW_MAJOR (only value supported in this build)                   */
+  int precond;      /* KCG_PRECOND_NONE (the paper's CG) -- only value in this build        */
+  int host_staging; /* 1: workspace also holds Y / mu staging for the *_host entry points          */
+  int history_cap;  /* per-iteration max relative residual recorded on device (0 = off)            */
+} kcg_desc;
+
+/* Solve report, filled on return (host memory). */
+typedef struct {
+  int status;              /* kcg_status of the solve                                        */
+  int converged;           /* 1 if every system converged                                    */
+  int iterations;          /* max over systems                                               */
+  int n_systems;           /* patches (kron) or patches*k (sylvester)                        */
+  int* iterations_per;     /* optional caller array [n_systems] (NULL = skip)                */
+  double rel_residual;     /* max over systems of recursive ||r||/||b||                      */
+  double rel_residual_true;/* max over patches of ||b - G mu||/||b||, recomputed at exit     */
+  double wall_time_s;      /* device time of the whole solve (CUDA events, launching stream)  */
+  double loop_time_s;      /* device time of the persistent CG kernel alone                  */
+  long long system_iterations; /* sum over systems of iterations (+1 start pass each)        */
+  double loop_bytes;       /* algorithmic HBM bytes of the CG kernel: 48*K*N per system-pass  */
+  size_t peak_mem_bytes;   /* workspace bytes                                                */
+  double* history;         /* optional caller array [history_cap] (NULL = skip)               */
+  int history_len;
+} kcg_report;
+
+/* Bytes of device workspace needed for desc (256-byte aligned sub-buffers). 0 on bad desc. */
+KCG_API size_t kron_cg_workspace_size(const kcg_desc* desc);
+
+/* Validate, copy the small parameters to the device, diagonalise M = A^T T A against P
+ * (Lemma 2: eigh(M, P), ascending rho, W^T P W = I, largest-|.| entry of each column positive)
+ * and build the TMA descriptors.  stream: a cudaStream_t (NULL = legacy default stream).     */
+KCG_API kcg_status kron_cg_create(const kcg_desc* desc, const double* A_host, const double* noise_prec_host,
+                          const double* prior_scale_host, const double* kappa2_host,
+                          const double* hits_dev, void* workspace_dev, size_t ws_bytes,
+                          void* stream, kcg_ctx** out);
+
+/* Kronecker route: CG on G (Sec. 3.2).  Y_dev [P][n][N] -> mu_dev [P][k][N].                   */
+KCG_API kcg_status kron_cg_solve(kcg_ctx* ctx, const double* Y_dev, double* mu_dev, double tol,
+                         int max_iter, kcg_report* report);
+
+/* Sylvester route (Sec. 3.3, Lemma 2): k shifted systems per patch, batched.  Per-column stop
+ * ||rt_i|| <= tol ||ft_i|| (reading R15).  report->iterations_per is [P*k].                   */
+KCG_API kcg_status sylvester_solve(kcg_ctx* ctx, const double* Y_dev, double* mu_dev, double tol,
+                           int max_iter, kcg_report* report);
+
+/* Same as above with HOST buffers: copies Y in and mu out through the context's staging buffers
+ * (desc.host_staging = 1), copies included in report->wall_time_s.                            */
+KCG_API kcg_status kron_cg_solve_host(kcg_ctx* ctx, const double* Y_host, double* mu_host, double tol,
+                              int max_iter, kcg_report* report);
+KCG_API kcg_status sylvester_solve_host(kcg_ctx* ctx, const double* Y_host, double* mu_host, double tol,
+                                int max_iter, kcg_report* report);
+
+/* y = G x for all patches (Alg.MatvecQ + Alg.MatvecBCBT fused).  x_dev, y_dev
+ * [P][k][N], must not alias.                                                                  */
+KCG_API kcg_status kron_cg_apply(kcg_ctx* ctx, const double* x_dev, double* y_dev);
+
+/* b = vec(N_h Y T A) for all patches (Eq.(mu*) right-hand side).  b_dev [P][k][N].            */
+KCG_API kcg_status kron_cg_rhs(kcg_ctx* ctx, const double* Y_dev, double* b_dev);
+
+/* The small-factor eigendecomposition computed at create: rho_host [P][k] ascending,
+ * W_host [P][k][k] (W[p][c][i] = entry c of eigenvector i).                                    */
+KCG_API kcg_status sylvester_factor(kcg_ctx* ctx, double* rho_host, double* W_host);
+
+/* Text of the last error on ctx (never NULL). */
+KCG_API const char* kcg_last_error(const kcg_ctx* ctx);
+/* Name of a status code (static string). */
+KCG_API const char* kcg_status_string(int status);
+
+/* Release host-side state.  Does not free the caller's workspace. */
+KCG_API void kron_cg_destroy(kcg_ctx* ctx);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* KRONCG_H */

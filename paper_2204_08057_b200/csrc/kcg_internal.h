@@ -1,0 +1,83 @@
+// Internal declarations shared by the host runtime (kcg_host.cu) and the kernels (kcg_kernels.cu).
+// Not part of the ABI.
+#pragma once
+
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#define KCG_KMAX 8
+#define KCG_NT 512          // threads per CTA of the persistent CG kernel
+#define KCG_TX 64           // tile width (pixels) of the CG kernel
+#define KCG_HALO 2          // single-pass recompute halo for a radius-1 stencil
+
+namespace kcg {
+
+// Compile-time tile height of the persistent kernel for K component planes per system.
+__host__ __device__ constexpr int cg_tile_y(int K) { return K == 1 ? 32 : (K <= 4 ? 16 : 8); }
+
+// Bytes of one pipeline stage (r and p boxes with halo, K planes).
+__host__ __device__ constexpr int cg_stage_bytes(int K) {
+  return 2 * K * (cg_tile_y(K) + 2 * KCG_HALO) * (KCG_TX + 2 * KCG_HALO) * 8;
+}
+
+// Per-system constant parameters of the operator  q_c = h sum_d M[c][d] p_d + tau_c (kappa2 p_c + (L p_c)).
+// Kronecker route: one system per patch, K = k, M = A^T T A, tau = prior scales.
+// Sylvester route: one system per (patch, column i), K = 1, M = [rho_i], tau = [1].
+struct SysParams {
+  double M[KCG_KMAX * KCG_KMAX];  // row-major K x K (compact)
+  double tau[KCG_KMAX];
+  double kappa2;
+  double hits_plane;              // index of the hits plane (patch) as a double (exact)
+};
+
+// Per-system iteration state (kept redundantly in every CTA's shared memory).
+enum { ST_RUNNING = 0, ST_CONVERGED = 1, ST_MAXIT = 2, ST_BREAKDOWN = 3, ST_NONFINITE = 4 };
+struct SysState {
+  double bnorm2;   // ||b||^2
+  double gamma;    // (r, r) of the current residual
+  double alpha;    // step of the next pass
+  double beta;     // p-update coefficient of the next pass
+  double rel;      // last recursive ||r|| / ||b||
+  int iters;       // completed iterations
+  int status;
+  int parity;      // which ping-pong buffer holds the current r, p
+  int pad;
+};
+
+struct CgArgs {
+  const SysParams* params;   // [n_sys]
+  double* x;                 // user solution planes [n_sys*K][side][side]
+  double* rbuf[2];           // internal ping-pong r planes, row pitch `pitch`
+  double* pbuf[2];           // internal ping-pong p planes
+  double* partials;          // [2][n_sys][tiles_per_sys][2]
+  SysState* state_out;       // [n_sys]
+  double* history;           // [history_cap]
+  const double* hits;        // [P][side][side] or nullptr
+  int history_cap;
+  int side, pitch;
+  int n_sys, tiles_x, tiles_y, tiles_per_sys;
+  int max_iter;
+  double tol2;
+};
+
+struct CgMaps {              // TMA descriptors of rbuf[0..1], pbuf[0..1] (box = {TX+4, TY+4, K})
+  CUtensorMap r[2];
+  CUtensorMap p[2];
+};
+
+// ---------------------------------------------------------------- launchers (kcg_kernels.cu)
+// All return cudaError_t of the launch.
+cudaError_t launch_rhs(int K, cudaStream_t s, const double* Y, const double* E, const double* hits,
+                       double* r0, double* p0, double* x, int P, int n, int side, int pitch);
+cudaError_t launch_cg(int K, cudaStream_t s, const CgArgs& a, const CgMaps& m, int grid, size_t smem);
+cudaError_t cg_kernel_config(int K, int n_sys, int* max_grid, size_t* smem);
+cudaError_t launch_apply(int K, cudaStream_t s, const SysParams* params, const double* x, double* y,
+                         const double* hits, int n_sys, int side);
+cudaError_t launch_resid(int K, cudaStream_t s, const SysParams* params, const double* x,
+                         const double* Y, const double* E, const double* hits, double* partials,
+                         double* out, int n_sys, int n, int side);
+cudaError_t launch_backtransform(int K, cudaStream_t s, const double* W, double* x, int P, int side);
+int apply_tiles_per_sys(int side);
+
+}  // namespace kcg

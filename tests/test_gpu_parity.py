@@ -1,0 +1,226 @@
+"""GPU parity: the CUDA path through the C ABI against the oracle (element by element).
+
+Bar (BASELINE.json north_star): relative 2-norm error <= 1e-8 at CG tolerance 1e-10 and
+iteration counts within +-2 of the oracle; operator / right-hand side kernels to 1e-13
+relative (fp64 with a different but exact-arithmetic-equivalent evaluation order).
+"""
+
+import numpy as np
+import pytest
+
+from gpu_util import have_gpu, make_ctx, rel
+from oracle import cg, exact, model, sylvester
+from synth import make_config, make_patch
+
+pytestmark = [pytest.mark.gpu, pytest.mark.skipif(not have_gpu(), reason="needs a CUDA GPU")]
+
+TOL = 1e-10
+
+
+def _np(t):
+    return t.detach().cpu().numpy()
+
+
+# ----------------------------------------------------------------------------- operator kernels
+@pytest.mark.parametrize("level,n,k,hits", [
+    (0, 3, 2, None), (1, 3, 2, "random"), (2, 4, 1, None), (3, 9, 3, "random"),
+    (5, 9, 3, None), (5, 9, 4, "random"), (6, 9, 5, None), (7, 9, 6, "random"),
+    (6, 9, 7, None), (5, 9, 8, "random"), (8, 9, 4, None)])
+def test_apply_matches_assembled_G(level, n, k, hits):
+    import torch
+    ps = [make_patch(level, n, k, seed=40 + s, tau="loguniform", hits=hits) for s in range(2)]
+    ctx, Y = make_ctx(ps)
+    rng = np.random.default_rng(level * 10 + k)
+    x = rng.standard_normal((2, k, ps[0].side, ps[0].side))
+    y = _np(ctx.apply(torch.from_numpy(x).cuda()))
+    for i, p in enumerate(ps):
+        G = model.assemble_G(p.level, p.A, p.noise_prec, p.tau, p.kappa2, p.hits)
+        ref = G @ x[i].reshape(-1)
+        assert np.abs(y[i].reshape(-1) - ref).max() <= 1e-13 * np.abs(ref).max()
+
+
+@pytest.mark.parametrize("level,k,hits", [(0, 1, None), (3, 3, "random"), (6, 4, None), (5, 8, None)])
+def test_rhs_matches_assembled_BtCY(level, k, hits):
+    ps = [make_patch(level, 9, k, seed=3 + s, hits=hits) for s in range(3)]
+    ctx, Y = make_ctx(ps)
+    b = _np(ctx.rhs(Y))
+    for i, p in enumerate(ps):
+        ref = model.assemble_rhs(p.level, p.A, p.noise_prec, p.Y, p.hits)
+        assert np.abs(b[i].reshape(-1) - ref).max() <= 1e-13 * np.abs(ref).max()
+
+
+@pytest.mark.parametrize("k", [1, 2, 4, 6, 8])
+def test_small_factor_matches_scipy_eigh(k):
+    ps = [make_patch(3, 9, k, seed=s, tau="loguniform") for s in range(3)]
+    ctx, _ = make_ctx(ps)
+    rho, W = ctx.factor()
+    for i, p in enumerate(ps):
+        M, P, rho_ref, W_ref = sylvester.small_factor(p.A, p.noise_prec, p.tau)
+        assert np.allclose(rho[i], rho_ref, rtol=1e-11, atol=1e-11 * rho_ref.max())
+        assert np.allclose(W[i], W_ref, rtol=1e-8, atol=1e-10 * np.abs(W_ref).max())
+
+
+# ----------------------------------------------------------------------------- Kronecker CG
+def _check_kron(ps, its_tol=2, err_tol=1e-8):
+    ctx, Y = make_ctx(ps)
+    mu, rep = ctx.solve(Y, tol=TOL)
+    mu = _np(mu)
+    assert rep["converged"], rep
+    for i, p in enumerate(ps):
+        G, b = model.problem_system(p)
+        ref = cg.cg_hs(G, b, tol=TOL)
+        assert ref.converged
+        assert rel(mu[i], ref.x) <= err_tol, (i, rel(mu[i], ref.x))
+        assert abs(rep["iterations_per"][i] - ref.iterations) <= its_tol, \
+            (i, rep["iterations_per"][i], ref.iterations)
+    return ctx, Y, mu, rep
+
+
+def test_kron_tiny():
+    ctx, Y, mu, rep = _check_kron(make_config("tiny"))
+    p = make_config("tiny")[0]
+    assert rel(mu[0], exact.problem_dct_exact(p)) <= 1e-8
+    assert rep["rel_residual"] <= TOL and rep["rel_residual_true"] <= 2 * TOL
+
+
+def test_kron_medium():
+    _check_kron(make_config("medium"))
+
+
+@pytest.mark.parametrize("level,k,hits", [(0, 1, None), (0, 3, None), (1, 2, "random"),
+                                          (2, 3, None), (3, 4, "random"), (4, 5, None),
+                                          (5, 6, "random"), (6, 8, None), (7, 2, None)])
+def test_kron_edge_levels(level, k, hits):
+    ps = [make_patch(level, 9, k, seed=60 + s, tau="loguniform", hits=hits) for s in range(2)]
+    _check_kron(ps)
+
+
+def test_kron_batch_composition_is_bitwise_irrelevant():
+    ps = [make_patch(6, 9, 4, seed=70 + s, tau="loguniform") for s in range(3)]
+    ctx, Y = make_ctx(ps)
+    mu_all, rep_all = ctx.solve(Y, tol=TOL)
+    mu_all = _np(mu_all)
+    for i, p in enumerate(ps):
+        c1, Y1 = make_ctx([p])
+        mu1, rep1 = c1.solve(Y1, tol=TOL)
+        assert np.array_equal(_np(mu1)[0], mu_all[i])
+        assert rep1["iterations_per"][0] == rep_all["iterations_per"][i]
+
+
+def test_kron_deterministic_and_host_entry():
+    import torch
+    ps = [make_patch(7, 9, 3, seed=5, tau="loguniform")]
+    ctx, Y = make_ctx(ps, host_staging=True, history_cap=4096)
+    m1, r1 = ctx.solve(Y, tol=TOL)
+    m2, r2 = ctx.solve(Y, tol=TOL)
+    assert torch.equal(m1, m2) and r1["iterations"] == r2["iterations"]
+    m3, r3 = ctx.solve_host(Y.cpu().pin_memory(), tol=TOL)
+    assert np.array_equal(_np(m1), m3.numpy()) and r3["iterations"] == r1["iterations"]
+    h = r1["history"]
+    assert len(h) == r1["iterations"] and h[-1] <= TOL < h[-2]
+
+
+def test_kron_zero_rhs_and_max_iter():
+    import torch
+    ps = [make_patch(5, 9, 3, seed=1)]
+    ctx, Y = make_ctx(ps)
+    mu, rep = ctx.solve(torch.zeros_like(Y), tol=TOL)
+    assert rep["iterations"] == 0 and rep["converged"] and not mu.any()
+    mu, rep = ctx.solve(Y, tol=TOL, max_iter=7)
+    assert rep["status_name"] == "KCG_NOT_CONVERGED" and rep["iterations"] == 7
+    G, b = model.problem_system(ps[0])
+    ref = cg.cg_hs(G, b, tol=1e-30, max_iter=7)
+    assert rel(_np(mu)[0], ref.x) <= 1e-10
+
+
+def test_kron_nonfinite_input():
+    ps = [make_patch(4, 9, 3, seed=1)]
+    ctx, Y = make_ctx(ps)
+    Y[0, 2, 3, 3] = float("nan")
+    from paper_2204_08057_b200.kroncg import KcgError
+    with pytest.raises(KcgError) as e:
+        ctx.solve(Y, tol=TOL)
+    assert e.value.status == 5
+
+
+def test_kron_planck_full_size():
+    _check_kron(make_config("planck"))
+
+
+def test_kron_fullsky_vs_exact_and_sampled_oracle():
+    import torch
+    ps = make_config("fullsky")
+    ctx, Y = make_ctx(ps)
+    mu, rep = ctx.solve(Y, tol=TOL)
+    mu = _np(mu)
+    assert rep["converged"]
+    for i, p in enumerate(ps):
+        assert rel(mu[i], exact.problem_dct_exact(p)) <= 1e-8, i
+    # iteration counts against the oracle on two patches (the oracle takes ~15 s each)
+    for i in (0, 11):
+        G, b = model.problem_system(ps[i])
+        ref = cg.cg_hs(G, b, tol=TOL)
+        assert abs(rep["iterations_per"][i] - ref.iterations) <= 2
+        assert rel(mu[i], ref.x) <= 1e-8
+    # operator at full size on sampled rows, one by one
+    rng = np.random.default_rng(0)
+    x = rng.standard_normal((12, 4, 1024, 1024))
+    y = _np(ctx.apply(torch.from_numpy(x).cuda()))
+    for i in (0, 5, 11):
+        rows = [(int(rng.integers(4)), int(rng.integers(1024 * 1024))) for _ in range(50)]
+        rows += [(0, 0), (1, 1023), (2, 1024 * 1023), (3, 1024 * 1024 - 1), (0, 1024 * 512 + 1023)]
+        p = ps[i]
+        ref = model.apply_G_rows(p.level, p.A, p.noise_prec, p.tau, p.kappa2, x[i], rows)
+        got = np.array([y[i][l].reshape(-1)[j] for (l, j) in rows])
+        assert np.allclose(got, ref, rtol=1e-13, atol=1e-13 * np.abs(ref).max())
+
+
+def test_kron_stress_vs_exact():
+    p = make_config("stress")[0]
+    ctx, Y = make_ctx([p])
+    mu, rep = ctx.solve(Y, tol=TOL)
+    assert rep["converged"] and rep["rel_residual_true"] <= 5 * TOL
+    assert rel(_np(mu)[0], exact.problem_dct_exact(p)) <= 1e-8
+
+
+# ----------------------------------------------------------------------------- Sylvester route
+def _check_syl(ps, its_tol=2):
+    ctx, Y = make_ctx(ps)
+    mu, rep = ctx.sylvester(Y, tol=TOL)
+    mu = _np(mu)
+    assert rep["converged"], rep
+    k = ps[0].k
+    for i, p in enumerate(ps):
+        ref = sylvester.problem_solve(p, tol=TOL)
+        assert rel(mu[i], ref.x) <= 1e-8, (i, rel(mu[i], ref.x))
+        gits = rep["iterations_per"][i * k:(i + 1) * k]
+        distinct = np.all(np.diff(ref.rho) > 1e-8 * ref.rho.max())
+        if distinct:
+            assert all(abs(a - b) <= its_tol for a, b in zip(gits, ref.iterations)), (gits, ref.iterations)
+    return mu, rep
+
+
+def test_sylvester_tiny_medium():
+    _check_syl(make_config("tiny"))
+    _check_syl(make_config("medium"))
+
+
+@pytest.mark.parametrize("level,k,hits", [(0, 2, None), (1, 1, None), (3, 4, "random"),
+                                          (5, 6, "random"), (6, 8, None)])
+def test_sylvester_edge(level, k, hits):
+    _check_syl([make_patch(level, 9, k, seed=80 + s, tau="loguniform", hits=hits) for s in range(2)])
+
+
+def test_sylvester_planck_and_stress():
+    _check_syl(make_config("planck"))
+    p = make_config("stress")[0]
+    mu, rep = _check_syl([p])
+    assert rel(mu[0], exact.problem_dct_exact(p)) <= 1e-8
+
+
+def test_routes_agree():
+    ps = [make_patch(7, 9, 4, seed=90, tau="loguniform")]
+    ctx, Y = make_ctx(ps)
+    a, _ = ctx.solve(Y, tol=TOL)
+    b, _ = ctx.sylvester(Y, tol=TOL)
+    assert rel(_np(a), _np(b)) <= 1e-8
