@@ -38,15 +38,18 @@ def _stale() -> bool:
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not _stale():
+def build(force: bool = False, verbose: bool = False, defines=(), out: str = None) -> str:
+    """Compile the sources into LIB (or ``out``), with optional -D ``defines`` (experiments)."""
+    LIB = out or globals()["LIB"]
+    if not force and not defines and out is None and not _stale():
         return LIB
     os.makedirs(os.path.dirname(LIB), exist_ok=True)
     nvcc = _nvcc()
     objs = []
     for s in SOURCES:
         obj = os.path.join(os.path.dirname(LIB), s.replace(".cu", ".o"))
-        cmd = [nvcc, *NVCC_FLAGS, "-c", os.path.join(CSRC, s), "-o", obj]
+        obj = obj + "." + str(abs(hash((LIB,) + tuple(defines)))) + ".o"
+        cmd = [nvcc, *NVCC_FLAGS, *[f"-D{d}" for d in defines], "-c", os.path.join(CSRC, s), "-o", obj]
         if verbose:
             print(" ".join(cmd), file=sys.stderr)
         subprocess.run(cmd, check=True)

@@ -481,9 +481,9 @@ kcg_status kron_cg_create(const kcg_desc* d, const double* A_host, const double*
   c->tiles_x_syl = tiles_x(c->side);
   c->tiles_y_syl = tiles_y(c->side, 1);
   int mg = 0;
-  CKC(kcg::cg_kernel_config(k, P, &mg, &c->smem_kron), "cg kernel config (kron)");
+  CKC(kcg::cg_kernel_config(k, hits_dev != nullptr, P, &mg, &c->smem_kron), "cg kernel config (kron)");
   c->grid_kron = std::max(1, std::min(mg, P * c->tiles_x_kron * c->tiles_y_kron));
-  CKC(kcg::cg_kernel_config(1, P * k, &mg, &c->smem_syl), "cg kernel config (sylvester)");
+  CKC(kcg::cg_kernel_config(1, hits_dev != nullptr, P * k, &mg, &c->smem_syl), "cg kernel config (sylvester)");
   c->grid_syl = std::max(1, std::min(mg, P * k * c->tiles_x_syl * c->tiles_y_syl));
   for (int i = 0; i < 4; ++i) CKC(cudaEventCreate(&c->ev[i]), "event create");
 #undef CKC

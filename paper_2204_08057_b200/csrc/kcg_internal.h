@@ -7,15 +7,37 @@
 #include <stdint.h>
 
 #define KCG_KMAX 8
-#define KCG_NT 512          // threads per CTA of the persistent CG kernel
 #define KCG_TX 64           // tile width (pixels) of the CG kernel
 #define KCG_HALO 2          // single-pass recompute halo for a radius-1 stencil
 
 namespace kcg {
 
 // Compile-time tile height of the persistent kernel for K component planes per system.
-__host__ __device__ constexpr int cg_tile_y(int K) { return K == 1 ? 32 : (K <= 4 ? 16 : 8); }
-
+#ifndef KCG_TY_SMALLK
+#define KCG_TY_SMALLK 16    // tile height for 2 <= K <= 4
+#endif
+#ifndef KCG_NT_SMALLK
+#define KCG_NT_SMALLK 512   // threads per CTA for K <= 4
+#endif
+#ifndef KCG_M_IN_REGS
+#define KCG_M_IN_REGS 0     // keep the K x K mixing block in registers (else read from shared)
+#endif
+__host__ __device__ constexpr int cg_tile_y(int K) { return K == 1 ? 32 : (K <= 4 ? KCG_TY_SMALLK : 8); }
+#ifndef KCG_STAGES_SMALLK
+#define KCG_STAGES_SMALLK 2 // TMA pipeline stages per CTA for K <= 4
+#endif
+#ifndef KCG_MINB_SMALLK
+#define KCG_MINB_SMALLK 1   // __launch_bounds__ min blocks per SM for K <= 4
+#endif
+#ifndef KCG_BULK
+#define KCG_BULK 0          // 1: x in / x, r, p out through cp.async.bulk rows (measured slower on B200)
+#endif
+// Threads per CTA of the persistent kernel (warps divide the tile rows).
+__host__ __device__ constexpr int cg_threads(int K) { return K == 1 ? 256 : (K >= 5 ? 256 : KCG_NT_SMALLK); }
+__host__ __device__ constexpr int cg_stages(int K) { return K == 8 ? 1 : (K >= 5 ? 2 : KCG_STAGES_SMALLK); }
+__host__ __device__ constexpr int cg_min_blocks(int K) { return K == 1 ? 2 : (K >= 5 ? 1 : KCG_MINB_SMALLK); }
+// Bytes of the x tile staging buffer (K planes of TY x TX, no halo).
+__host__ __device__ constexpr int cg_xstage_bytes(int K) { return KCG_BULK ? K * cg_tile_y(K) * KCG_TX * 8 : 0; }
 // Bytes of one pipeline stage (r and p boxes with halo, K planes).
 __host__ __device__ constexpr int cg_stage_bytes(int K) {
   return 2 * K * (cg_tile_y(K) + 2 * KCG_HALO) * (KCG_TX + 2 * KCG_HALO) * 8;
@@ -71,7 +93,7 @@ struct CgMaps {              // TMA descriptors of rbuf[0..1], pbuf[0..1] (box =
 cudaError_t launch_rhs(int K, cudaStream_t s, const double* Y, const double* E, const double* hits,
                        double* r0, double* p0, double* x, int P, int n, int side, int pitch);
 cudaError_t launch_cg(int K, cudaStream_t s, const CgArgs& a, const CgMaps& m, int grid, size_t smem);
-cudaError_t cg_kernel_config(int K, int n_sys, int* max_grid, size_t* smem);
+cudaError_t cg_kernel_config(int K, bool hits, int n_sys, int* max_grid, size_t* smem);
 cudaError_t launch_apply(int K, cudaStream_t s, const SysParams* params, const double* x, double* y,
                          const double* hits, int n_sys, int side);
 cudaError_t launch_resid(int K, cudaStream_t s, const SysParams* params, const double* x,

@@ -110,33 +110,331 @@ __global__ void __launch_bounds__(256) rhs_kernel(const double* __restrict__ Y, 
 }
 
 // --------------------------------------------------------------------------- persistent CG
-template <int K>
-__global__ void __launch_bounds__(KCG_NT, 1) cg_persistent_kernel(const CgArgs a, const __grid_constant__ CgMaps maps) {
+// One tile of one system: box = tile + 2-pixel halo, K planes of r and p staged by TMA (zero fill
+// outside the face).  Warp w owns T rows w, w+NW, ...; lane l owns the pixel PAIR at tile columns
+// 2l, 2l+1 (double2 in shared and global memory); horizontal neighbours come from shuffles.
+//   Phase A  p_new = r + beta p                    whole box (elementwise)
+//   Phase B  q = G p_new, r_new = r - alpha q      T rows (pairs) + the 1-pixel ring (scalars)
+//   Phase C  w = G r_new on T; (r,r), (w,r); x += alpha p_new
+// Output: with BULK (face side a multiple of 64) x is brought in and x, r_new, p_new are written
+// back by the bulk-copy engine (cp.async.bulk, 512-byte rows) straight from shared memory, so the
+// SM issues no global loads/stores on the hot path; otherwise plain vector loads/stores.
+// EDGE = the box touches the face border (bounds checks, degree 2/3); interior tiles skip both.
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void bulk_s2g(void* dst, const void* src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(smem_u32(src)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read_all() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+
+struct TileCtx {
+  double* R;          // r box (stage)
+  double* Pp;         // p box (stage)
+  double* xs;         // x tile staging [K][TY][TX] (BULK)
+  const double* Ms;   // M (K*K) then tau (K) of this tile's system, shared
+  int s, y0, x0, par;
+  double alpha, beta, kappa2;
+  const double* hp;   // hits plane or nullptr
+  uint64_t* bar;      // stage mbarrier
+  uint32_t phase;
+  uint64_t* xbar;     // x staging mbarrier
+  uint32_t xphase;
+  double* part_out;
+};
+
+template <int K, bool EDGE, bool HITS, bool BULK>
+__device__ __forceinline__ void cg_tile(const CgArgs& a, const TileCtx& tc, double (*red)[32]) {
+  constexpr int TY = cg_tile_y(K), TX = KCG_TX, H = KCG_HALO;
+  constexpr int BW = TX + 2 * H, BH = TY + 2 * H, PLANE = BW * BH, FIELD = K * PLANE;
+  constexpr int NT = cg_threads(K), NW = NT / 32, RPW = TY / NW;
+  constexpr int RP = 2 * (TX + 2) + 2 * TY;  // ring points
+  static_assert(TX == 64 && RPW * NW == TY, "pair mapping needs TX = 64 and NW | TY");
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int side = a.side;
+  const size_t N = (size_t)side * side;
+  const size_t ps = (size_t)a.pitch * side;
+  double* __restrict__ R = tc.R;
+  double* __restrict__ Pp = tc.Pp;
+  const int s = tc.s, y0 = tc.y0, x0 = tc.x0;
+  const double alpha = tc.alpha, beta = tc.beta, kappa2 = tc.kappa2;
+  const int gx = x0 + 2 * lane;
+
+  if (BULK && warp == 0) {  // x rows of this tile -> xs (completes on xbar)
+    if (lane == 0) mbar_arrive_expect_tx(tc.xbar, K * TY * TX * 8);
+    __syncwarp();
+    for (int rrow = lane; rrow < K * TY; rrow += 32) {
+      const int c = rrow / TY, row = rrow - c * TY;
+      bulk_g2s(tc.xs + (size_t)rrow * TX, a.x + ((size_t)(s * K + c) * side + y0 + row) * side + x0, TX * 8, tc.xbar);
+    }
+  }
+
+  mbar_wait(tc.bar, tc.phase);
+
+  // Phase A
+  {
+    double2* P2 = reinterpret_cast<double2*>(Pp);
+    const double2* R2 = reinterpret_cast<const double2*>(R);
+    if (beta == 0.0) {
+      for (int e = tid; e < FIELD / 2; e += NT) P2[e] = R2[e];
+    } else {
+      for (int e = tid; e < FIELD / 2; e += NT) {
+        const double2 r = R2[e];
+        double2 p = P2[e];
+        p.x = fma(beta, p.x, r.x);
+        p.y = fma(beta, p.y, r.y);
+        P2[e] = p;
+      }
+    }
+  }
+  __syncthreads();
+
+#if KCG_M_IN_REGS
+  double M[K * K];
+#pragma unroll
+  for (int e = 0; e < K * K; ++e) M[e] = tc.Ms[e];
+#else
+  const double* M = tc.Ms;
+#endif
+  double tau[K];
+#pragma unroll
+  for (int c = 0; c < K; ++c) tau[c] = tc.Ms[K * K + c];
+
+  // Phase B1: T rows, pairs
+#pragma unroll
+  for (int j = 0; j < RPW; ++j) {
+    const int gy = y0 + warp + j * NW;
+    const int ly = gy - y0 + H;
+    bool in0 = true, in1 = true;
+    double kd0 = kappa2 + 4.0, kd1 = kappa2 + 4.0;
+    if (EDGE) {
+      in0 = gy < side && gx < side;
+      in1 = gy < side && gx + 1 < side;
+      const double dy = (gy == 0) + (gy == side - 1);
+      kd0 = kappa2 + (4.0 - dy - (gx == 0) - (gx == side - 1));
+      kd1 = kappa2 + (4.0 - dy - (gx + 1 == 0) - (gx + 1 == side - 1));
+    }
+    double h0 = 1.0, h1 = 1.0;
+    if (HITS) {
+      if (in0) h0 = __ldg(tc.hp + (size_t)gy * side + gx);
+      if (in1) h1 = __ldg(tc.hp + (size_t)gy * side + gx + 1);
+    }
+    double2 pc[K];
+#pragma unroll
+    for (int c = 0; c < K; ++c) pc[c] = reinterpret_cast<const double2*>(Pp + c * PLANE + ly * BW)[1 + lane];
+#pragma unroll
+    for (int c = 0; c < K; ++c) {
+      const double* row = Pp + c * PLANE + ly * BW;
+      const double2 up = reinterpret_cast<const double2*>(row - BW)[1 + lane];
+      const double2 dn = reinterpret_cast<const double2*>(row + BW)[1 + lane];
+      const double el = row[H - 1], er = row[H + TX];  // broadcast loads, no branch
+      double left = __shfl_up_sync(0xffffffffu, pc[c].y, 1);
+      double right = __shfl_down_sync(0xffffffffu, pc[c].x, 1);
+      left = lane == 0 ? el : left;
+      right = lane == 31 ? er : right;
+      const double nb0 = (up.x + dn.x) + (left + pc[c].y);
+      const double nb1 = (up.y + dn.y) + (pc[c].x + right);
+      double mix0 = 0.0, mix1 = 0.0;
+#pragma unroll
+      for (int d = 0; d < K; ++d) {
+        mix0 = fma(M[c * K + d], pc[d].x, mix0);
+        mix1 = fma(M[c * K + d], pc[d].y, mix1);
+      }
+      const double q0 = HITS ? fma(h0, mix0, tau[c] * fma(kd0, pc[c].x, -nb0)) : fma(tau[c], fma(kd0, pc[c].x, -nb0), mix0);
+      const double q1 = HITS ? fma(h1, mix1, tau[c] * fma(kd1, pc[c].y, -nb1)) : fma(tau[c], fma(kd1, pc[c].y, -nb1), mix1);
+      double2* rp = reinterpret_cast<double2*>(R + c * PLANE + ly * BW) + 1 + lane;
+      double2 rv = *rp;
+      if (in0) rv.x = fma(-alpha, q0, rv.x);
+      if (in1) rv.y = fma(-alpha, q1, rv.y);
+      *rp = rv;
+    }
+  }
+  // Phase B2: the 1-pixel ring around T (scalars)
+  for (int t = tid; t < RP; t += NT) {
+    int ly, lx;
+    if (t < TX + 2) { ly = H - 1; lx = H - 1 + t; }
+    else if (t < 2 * (TX + 2)) { ly = H + TY; lx = H - 1 + (t - (TX + 2)); }
+    else { const int u = t - 2 * (TX + 2); ly = H + (u >> 1); lx = (u & 1) ? H + TX : H - 1; }
+    const int gyr = y0 - H + ly, gxr = x0 - H + lx;
+    double kd = kappa2 + 4.0;
+    if (EDGE) {
+      if (gyr < 0 || gyr >= side || gxr < 0 || gxr >= side) continue;
+      kd = kappa2 + (4.0 - (gyr == 0) - (gyr == side - 1) - (gxr == 0) - (gxr == side - 1));
+    }
+    const double h = HITS ? __ldg(tc.hp + (size_t)gyr * side + gxr) : 1.0;
+    const int o = ly * BW + lx;
+    double pcs[K];
+#pragma unroll
+    for (int c = 0; c < K; ++c) pcs[c] = Pp[c * PLANE + o];
+#pragma unroll
+    for (int c = 0; c < K; ++c) {
+      const double* pl = Pp + c * PLANE + o;
+      const double nb = (pl[-BW] + pl[BW]) + (pl[-1] + pl[1]);
+      double mix = 0.0;
+#pragma unroll
+      for (int d = 0; d < K; ++d) mix = fma(M[c * K + d], pcs[d], mix);
+      const double q = HITS ? fma(h, mix, tau[c] * fma(kd, pcs[c], -nb)) : fma(tau[c], fma(kd, pcs[c], -nb), mix);
+      R[c * PLANE + o] = fma(-alpha, q, R[c * PLANE + o]);
+    }
+  }
+  __syncthreads();
+  if (BULK) mbar_wait(tc.xbar, tc.xphase);
+
+  // Phase C
+  double rr = 0.0, wr = 0.0;
+#pragma unroll
+  for (int j = 0; j < RPW; ++j) {
+    const int gy = y0 + warp + j * NW;
+    const int ly = gy - y0 + H;
+    bool in0 = true, in1 = true;
+    double kd0 = kappa2 + 4.0, kd1 = kappa2 + 4.0;
+    if (EDGE) {
+      in0 = gy < side && gx < side;
+      in1 = gy < side && gx + 1 < side;
+      const double dy = (gy == 0) + (gy == side - 1);
+      kd0 = kappa2 + (4.0 - dy - (gx == 0) - (gx == side - 1));
+      kd1 = kappa2 + (4.0 - dy - (gx + 1 == 0) - (gx + 1 == side - 1));
+    }
+    double h0 = 1.0, h1 = 1.0;
+    if (HITS) {
+      if (in0) h0 = __ldg(tc.hp + (size_t)gy * side + gx);
+      if (in1) h1 = __ldg(tc.hp + (size_t)gy * side + gx + 1);
+    }
+    double* xp = a.x + ((size_t)s * K * side + gy) * side + gx;
+    double2 xj[K];
+#pragma unroll
+    for (int c = 0; c < K; ++c) {
+      if (BULK) {
+        xj[c] = reinterpret_cast<const double2*>(tc.xs + ((size_t)c * TY + (gy - y0)) * TX)[lane];
+      } else if (!EDGE || (in0 && in1)) {
+        xj[c] = __ldcg(reinterpret_cast<const double2*>(xp + c * N));
+      } else {
+        xj[c].x = in0 ? __ldcg(xp + c * N) : 0.0;
+        xj[c].y = in1 ? __ldcg(xp + c * N + 1) : 0.0;
+      }
+    }
+    double2 rc[K];
+#pragma unroll
+    for (int c = 0; c < K; ++c) rc[c] = reinterpret_cast<const double2*>(R + c * PLANE + ly * BW)[1 + lane];
+    const size_t ro = ((size_t)s * K) * ps + (size_t)gy * a.pitch + gx;
+    double* rout = (tc.par ? a.rbuf[0] : a.rbuf[1]) + ro;  // select, not a dynamic param index
+    double* pout = (tc.par ? a.pbuf[0] : a.pbuf[1]) + ro;
+#pragma unroll
+    for (int c = 0; c < K; ++c) {
+      const double* row = R + c * PLANE + ly * BW;
+      const double2 up = reinterpret_cast<const double2*>(row - BW)[1 + lane];
+      const double2 dn = reinterpret_cast<const double2*>(row + BW)[1 + lane];
+      const double el = row[H - 1], er = row[H + TX];
+      double left = __shfl_up_sync(0xffffffffu, rc[c].y, 1);
+      double right = __shfl_down_sync(0xffffffffu, rc[c].x, 1);
+      left = lane == 0 ? el : left;
+      right = lane == 31 ? er : right;
+      const double nb0 = (up.x + dn.x) + (left + rc[c].y);
+      const double nb1 = (up.y + dn.y) + (rc[c].x + right);
+      double mix0 = 0.0, mix1 = 0.0;
+#pragma unroll
+      for (int d = 0; d < K; ++d) {
+        mix0 = fma(M[c * K + d], rc[d].x, mix0);
+        mix1 = fma(M[c * K + d], rc[d].y, mix1);
+      }
+      const double w0 = HITS ? fma(h0, mix0, tau[c] * fma(kd0, rc[c].x, -nb0)) : fma(tau[c], fma(kd0, rc[c].x, -nb0), mix0);
+      const double w1 = HITS ? fma(h1, mix1, tau[c] * fma(kd1, rc[c].y, -nb1)) : fma(tau[c], fma(kd1, rc[c].y, -nb1), mix1);
+      const double2 pn = reinterpret_cast<const double2*>(Pp + c * PLANE + ly * BW)[1 + lane];
+      double2 xn;
+      xn.x = fma(alpha, pn.x, xj[c].x);
+      xn.y = fma(alpha, pn.y, xj[c].y);
+      if (BULK) {
+        rr = fma(rc[c].x, rc[c].x, rr);
+        wr = fma(w0, rc[c].x, wr);
+        rr = fma(rc[c].y, rc[c].y, rr);
+        wr = fma(w1, rc[c].y, wr);
+        reinterpret_cast<double2*>(tc.xs + ((size_t)c * TY + (gy - y0)) * TX)[lane] = xn;
+      } else if (!EDGE || (in0 && in1)) {
+        rr = fma(rc[c].x, rc[c].x, rr);
+        wr = fma(w0, rc[c].x, wr);
+        rr = fma(rc[c].y, rc[c].y, rr);
+        wr = fma(w1, rc[c].y, wr);
+        *reinterpret_cast<double2*>(xp + c * N) = xn;
+        *reinterpret_cast<double2*>(rout + c * ps) = rc[c];
+        *reinterpret_cast<double2*>(pout + c * ps) = pn;
+      } else {
+        if (in0) {
+          rr = fma(rc[c].x, rc[c].x, rr);
+          wr = fma(w0, rc[c].x, wr);
+          xp[c * N] = xn.x;
+          rout[c * ps] = rc[c].x;
+          pout[c * ps] = pn.x;
+        }
+        if (in1) {
+          rr = fma(rc[c].y, rc[c].y, rr);
+          wr = fma(w1, rc[c].y, wr);
+          xp[c * N + 1] = xn.y;
+          rout[c * ps + 1] = rc[c].y;
+          pout[c * ps + 1] = pn.y;
+        }
+      }
+    }
+  }
+  rr = warp_sum(rr);
+  wr = warp_sum(wr);
+  if (lane == 0) { red[0][warp] = rr; red[1][warp] = wr; }
+  if (BULK) fence_proxy_async_smem();  // x_new in xs and r_new/p_new in the boxes -> async proxy
+  __syncthreads();
+  if (BULK) {  // 3*K*TY rows of 512 bytes, one per thread
+    for (int t = tid; t < 3 * K * TY; t += NT) {
+      const int f = t / (K * TY), rc_ = t - f * (K * TY), c = rc_ / TY, row = rc_ - c * TY;
+      const size_t plane = (size_t)s * K + c;
+      const int gy = y0 + row;
+      if (f == 0) {
+        bulk_s2g(a.x + (plane * side + gy) * side + x0, tc.xs + (size_t)rc_ * TX, TX * 8);
+      } else {
+        double* out = f == 1 ? (tc.par ? a.rbuf[0] : a.rbuf[1]) : (tc.par ? a.pbuf[0] : a.pbuf[1]);
+        const double* src = (f == 1 ? R : Pp) + c * PLANE + (row + H) * BW + H;
+        bulk_s2g(out + plane * ps + (size_t)gy * a.pitch + x0, src, TX * 8);
+      }
+    }
+    bulk_commit();
+  }
+  if (warp == 0) {
+    double v0 = lane < NW ? red[0][lane] : 0.0;
+    double v1 = lane < NW ? red[1][lane] : 0.0;
+    v0 = warp_sum(v0);
+    v1 = warp_sum(v1);
+    if (lane == 0) { tc.part_out[0] = v0; tc.part_out[1] = v1; }
+  }
+}
+
+template <int K, bool HITS>
+__global__ void __launch_bounds__(cg_threads(K), cg_min_blocks(K)) cg_persistent_kernel(const CgArgs a, const __grid_constant__ CgMaps maps) {
   constexpr int TY = cg_tile_y(K), TX = KCG_TX, H = KCG_HALO;
   constexpr int BW = TX + 2 * H, BH = TY + 2 * H;
-  constexpr int PLANE = BW * BH;
-  constexpr int FIELD = K * PLANE;  // doubles of one field box
+  constexpr int FIELD = K * BW * BH;  // doubles of one field box
   constexpr int STAGE_BYTES = 2 * FIELD * 8;
-  constexpr int NW = KCG_NT / 32;
-  constexpr int PTS = TY * TX / KCG_NT;  // T-region points per thread
-  static_assert(PTS >= 1 && TY * TX % KCG_NT == 0, "tile/threads mismatch");
+  constexpr int NT = cg_threads(K), NW = NT / 32, NS = cg_stages(K);
   static_assert(STAGE_BYTES == cg_stage_bytes(K), "stage size");
 
   extern __shared__ __align__(128) unsigned char smem_raw[];
-  SysState* st = reinterpret_cast<SysState*>(smem_raw + 2 * STAGE_BYTES);
+  double* xs = reinterpret_cast<double*>(smem_raw + NS * STAGE_BYTES);
+  SysState* st = reinterpret_cast<SysState*>(smem_raw + NS * STAGE_BYTES + cg_xstage_bytes(K));
   int* act = reinterpret_cast<int*>(st + a.n_sys);
   __shared__ __align__(8) uint64_t mbar[2];
-  __shared__ double red[2][NW];
+  __shared__ __align__(8) uint64_t xbar;
+  __shared__ double red[2][32];
+  __shared__ double Ms[KCG_KMAX * KCG_KMAX + KCG_KMAX];
   __shared__ int s_nact;
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int side = a.side, pitch = a.pitch;
-  const size_t N = (size_t)side * side;
-  const size_t ps = (size_t)pitch * side;
   const int tps = a.tiles_per_sys;
+  const bool bulk = KCG_BULK && (a.side % TX) == 0;  // whole 512-byte rows everywhere
   cg::grid_group grid = cg::this_grid();
 
-  for (int s = tid; s < a.n_sys; s += KCG_NT) {
+  for (int s = tid; s < a.n_sys; s += NT) {
     SysState z;
     z.bnorm2 = 0.0; z.gamma = 0.0; z.alpha = 0.0; z.beta = 0.0; z.rel = 1.0;
     z.iters = 0; z.status = ST_RUNNING; z.parity = 0; z.pad = 0;
@@ -145,24 +443,28 @@ __global__ void __launch_bounds__(KCG_NT, 1) cg_persistent_kernel(const CgArgs a
   if (tid == 0) {
     mbar_init(&mbar[0], 1);
     mbar_init(&mbar[1], 1);
+    mbar_init(&xbar, 1);
     fence_mbar_init();
   }
   __syncthreads();
 
-  uint32_t phase0 = 0, phase1 = 0;
+  uint32_t phase0 = 0, phase1 = 0, xphase = 0;
   int it = -1;  // -1 = start pass (alpha = beta = 0): r, p <- b and (b, b), (G b, b)
 
-  auto issue = [&](int t, int sidx) {
+  // TMA of tile t (index into the active-tile list) into stage sidx; parity flip for speculation
+  auto issue = [&](int t, int sidx, int flip) {
     const int s = act[t / tps];
     const int tile = t - (t / tps) * tps;
     const int ty = tile / a.tiles_x, tx = tile - ty * a.tiles_x;
-    const int par = st[s].parity;
+    const int par = st[s].parity ^ flip;
     double* dst = reinterpret_cast<double*>(smem_raw + sidx * STAGE_BYTES);
     mbar_arrive_expect_tx(&mbar[sidx], STAGE_BYTES);
     tma_load_3d(dst, &maps.r[par], &mbar[sidx], tx * TX - H, ty * TY - H, s * K);
     tma_load_3d(dst + FIELD, &maps.p[par], &mbar[sidx], tx * TX - H, ty * TY - H, s * K);
   };
 
+  int nact_prev = -1;
+  bool spec = false;  // a speculative first TMA of this iteration is in flight in stage 0
   while (true) {
     if (tid == 0) {
       int n = 0;
@@ -172,161 +474,97 @@ __global__ void __launch_bounds__(KCG_NT, 1) cg_persistent_kernel(const CgArgs a
     }
     __syncthreads();
     const int nact = s_nact;
+    if (spec && nact != nact_prev) {  // mis-speculated: drain the stale load before reusing stage 0
+      mbar_wait(&mbar[0], phase0);
+      phase0 ^= 1u;
+      spec = false;
+    }
     if (nact == 0) break;
     const int ntiles = nact * tps;
     const int par_out = (it + 1) & 1;
 
-    int sidx = 0;
-    if ((int)blockIdx.x < ntiles && tid == 0) issue(blockIdx.x, 0);
-    for (int t = blockIdx.x; t < ntiles; t += gridDim.x, sidx ^= 1) {
+    if (!spec && (int)blockIdx.x < ntiles && tid == 0) issue(blockIdx.x, 0, 0);
+    spec = false;
+    int i = 0;
+    for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++i) {
+      const int sidx = NS == 2 ? (i & 1) : 0;
       const int tn = t + gridDim.x;
-      if (tn < ntiles && tid == 0) {
-        fence_proxy_async_smem();
-        issue(tn, sidx ^ 1);
+      if (bulk) bulk_wait_read_all();  // previous tile's bulk stores have read their smem
+      __syncthreads();
+      if (tid == 0) {
+        if (NS == 2 && tn < ntiles) {
+          fence_proxy_async_smem();
+          issue(tn, sidx ^ 1, 0);
+        } else if (NS == 1 && i > 0) {
+          fence_proxy_async_smem();
+          issue(t, 0, 0);
+        }
       }
       const int s = act[t / tps];
       const int tile = t - (t / tps) * tps;
       const int ty = tile / a.tiles_x, tx = tile - ty * a.tiles_x;
-      const int ty0 = ty * TY, tx0 = tx * TX;
       const SysParams* sp = a.params + s;
-      double M[K * K], tau[K];
-#pragma unroll
-      for (int e = 0; e < K * K; ++e) M[e] = __ldg(&sp->M[e]);
-#pragma unroll
-      for (int c = 0; c < K; ++c) tau[c] = __ldg(&sp->tau[c]);
-      const double kappa2 = __ldg(&sp->kappa2);
-      const double* hp = a.hits ? a.hits + (size_t)__ldg(&sp->hits_plane) * N : nullptr;
-      const double alpha = st[s].alpha, beta = st[s].beta;
-      const int par = st[s].parity;
-
-      // prefetch x of this thread's T-region points
-      double xv[PTS][K];
-#pragma unroll
-      for (int j = 0; j < PTS; ++j) {
-        const int pt = tid + j * KCG_NT;
-        const int gy = ty0 + pt / TX, gx = tx0 + pt % TX;
-        const bool in = gy < side && gx < side;
-#pragma unroll
-        for (int c = 0; c < K; ++c)
-          xv[j][c] = in ? __ldcg(a.x + ((size_t)(s * K + c) * side + gy) * side + gx) : 0.0;
+      if (tid < K * K) Ms[tid] = __ldg(&sp->M[tid]);
+      else if (tid < K * K + K) Ms[tid] = __ldg(&sp->tau[tid - K * K]);
+      TileCtx tc;
+      tc.R = reinterpret_cast<double*>(smem_raw + sidx * STAGE_BYTES);
+      tc.Pp = tc.R + FIELD;
+      tc.xs = xs;
+      tc.Ms = Ms;
+      tc.s = s;
+      tc.y0 = ty * TY;
+      tc.x0 = tx * TX;
+      tc.par = st[s].parity;
+      tc.alpha = st[s].alpha;
+      tc.beta = st[s].beta;
+      tc.kappa2 = __ldg(&sp->kappa2);
+      tc.hp = HITS ? a.hits + (size_t)__ldg(&sp->hits_plane) * ((size_t)a.side * a.side) : nullptr;
+      tc.bar = &mbar[sidx];
+      tc.phase = sidx ? phase1 : phase0;
+      tc.xbar = &xbar;
+      tc.xphase = xphase;
+      tc.part_out = a.partials + (((size_t)par_out * a.n_sys + s) * tps + tile) * 2;
+      const bool interior = tc.x0 >= H && tc.x0 + TX + H <= a.side && tc.y0 >= H && tc.y0 + TY + H <= a.side;
+      if (KCG_BULK && bulk) {
+        if (interior) cg_tile<K, false, HITS, true>(a, tc, red);
+        else cg_tile<K, true, HITS, true>(a, tc, red);
+        xphase ^= 1u;
+      } else {
+        if (interior) cg_tile<K, false, HITS, false>(a, tc, red);
+        else cg_tile<K, true, HITS, false>(a, tc, red);
       }
-
-      if (sidx == 0) { mbar_wait(&mbar[0], phase0); phase0 ^= 1u; }
-      else           { mbar_wait(&mbar[1], phase1); phase1 ^= 1u; }
-      double* R = reinterpret_cast<double*>(smem_raw + sidx * STAGE_BYTES);
-      double* Pp = R + FIELD;
-
-      // Phase A: p_new = r + beta p_old on the whole haloed box (zero outside the face).
-      {
-        double2* P2 = reinterpret_cast<double2*>(Pp);
-        const double2* R2 = reinterpret_cast<const double2*>(R);
-        if (beta == 0.0) {
-          for (int e = tid; e < FIELD / 2; e += KCG_NT) P2[e] = R2[e];
-        } else {
-          for (int e = tid; e < FIELD / 2; e += KCG_NT) {
-            const double2 r = R2[e];
-            double2 p = P2[e];
-            p.x = fma(beta, p.x, r.x);
-            p.y = fma(beta, p.y, r.y);
-            P2[e] = p;
-          }
-        }
-      }
-      __syncthreads();
-
-      // Phase B: q = G p_new and r_new = r - alpha q on the tile + 1-pixel ring (in-face only).
-      {
-        constexpr int RW = BW - 2, RH = BH - 2;
-        for (int pt = tid; pt < RW * RH; pt += KCG_NT) {
-          const int ly = pt / RW + 1, lx = pt % RW + 1;
-          const int gy = ty0 - H + ly, gx = tx0 - H + lx;
-          if (gy < 0 || gy >= side || gx < 0 || gx >= side) continue;
-          const double deg = 4.0 - (gy == 0) - (gy == side - 1) - (gx == 0) - (gx == side - 1);
-          const double h = hp ? __ldg(hp + (size_t)gy * side + gx) : 1.0;
-          const int o = ly * BW + lx;
-          double pc[K];
-#pragma unroll
-          for (int c = 0; c < K; ++c) pc[c] = Pp[c * PLANE + o];
-#pragma unroll
-          for (int c = 0; c < K; ++c) {
-            const double* pl = Pp + c * PLANE + o;
-            const double nb = (pl[-BW] + pl[BW]) + (pl[-1] + pl[1]);
-            double mix = 0.0;
-#pragma unroll
-            for (int d = 0; d < K; ++d) mix = fma(M[c * K + d], pc[d], mix);
-            const double q = fma(h, mix, tau[c] * (fma(kappa2 + deg, pc[c], -nb)));
-            R[c * PLANE + o] = fma(-alpha, q, R[c * PLANE + o]);
-          }
-        }
-      }
-      __syncthreads();
-
-      // Phase C: w = G r_new on the tile, partial (r,r), (w,r); x += alpha p; store x, r, p.
-      double rr = 0.0, wr = 0.0;
-#pragma unroll
-      for (int j = 0; j < PTS; ++j) {
-        const int pt = tid + j * KCG_NT;
-        const int ly = pt / TX + H, lx = pt % TX + H;
-        const int gy = ty0 + pt / TX, gx = tx0 + pt % TX;
-        if (gy < side && gx < side) {
-          const double deg = 4.0 - (gy == 0) - (gy == side - 1) - (gx == 0) - (gx == side - 1);
-          const double h = hp ? __ldg(hp + (size_t)gy * side + gx) : 1.0;
-          const int o = ly * BW + lx;
-          double rc[K];
-#pragma unroll
-          for (int c = 0; c < K; ++c) rc[c] = R[c * PLANE + o];
-#pragma unroll
-          for (int c = 0; c < K; ++c) {
-            const double* rl = R + c * PLANE + o;
-            const double nb = (rl[-BW] + rl[BW]) + (rl[-1] + rl[1]);
-            double mix = 0.0;
-#pragma unroll
-            for (int d = 0; d < K; ++d) mix = fma(M[c * K + d], rc[d], mix);
-            const double w = fma(h, mix, tau[c] * (fma(kappa2 + deg, rc[c], -nb)));
-            rr = fma(rc[c], rc[c], rr);
-            wr = fma(w, rc[c], wr);
-            const double pn = Pp[c * PLANE + o];
-            const size_t plane = (size_t)(s * K + c);
-            a.x[(plane * side + gy) * side + gx] = fma(alpha, pn, xv[j][c]);
-            a.rbuf[par ^ 1][plane * ps + (size_t)gy * pitch + gx] = rc[c];
-            a.pbuf[par ^ 1][plane * ps + (size_t)gy * pitch + gx] = pn;
-          }
-        }
-      }
-      rr = warp_sum(rr);
-      wr = warp_sum(wr);
-      if (lane == 0) { red[0][warp] = rr; red[1][warp] = wr; }
-      __syncthreads();
-      if (warp == 0) {
-        double v0 = lane < NW ? red[0][lane] : 0.0;
-        double v1 = lane < NW ? red[1][lane] : 0.0;
-        v0 = warp_sum(v0);
-        v1 = warp_sum(v1);
-        if (lane == 0) {
-          double* dst = a.partials + (((size_t)par_out * a.n_sys + s) * tps + tile) * 2;
-          dst[0] = v0;
-          dst[1] = v1;
-        }
-      }
-      __syncthreads();
+      if (sidx) phase1 ^= 1u; else phase0 ^= 1u;
     }
 
+    if (bulk) bulk_wait_all();  // this iteration's bulk stores are complete
     fence_proxy_async_global();
     grid.sync();
     fence_proxy_async_global();
+    // speculative first load of the next iteration (same active set, flipped parity) overlaps the
+    // reduction below; verified against the new active count at the top of the loop
+    if (it >= 0 && (int)blockIdx.x < ntiles && tid == 0) issue(blockIdx.x, 0, 1);
+    spec = it >= 0 && (int)blockIdx.x < ntiles;
+    nact_prev = nact;
 
     // Per-system reduction of the tile partials (fixed order -> deterministic, independent of the
     // grid size and of which other systems are in the batch), then the CG scalar recurrences.
-    for (int i = warp; i < nact; i += NW) {
-      const int s = act[i];
+    for (int ii = warp; ii < nact; ii += NW) {
+      const int s = act[ii];
       const double* base = a.partials + ((size_t)par_out * a.n_sys + s) * tps * 2;
-      double rr = 0.0, wr = 0.0;
-      for (int tl = lane; tl < tps; tl += 32) {
-        rr += __ldcg(base + 2 * tl);
-        wr += __ldcg(base + 2 * tl + 1);
+      double rr0 = 0.0, wr0 = 0.0, rr1 = 0.0, wr1 = 0.0;
+      int tl = lane;
+      for (; tl + 32 < tps; tl += 64) {
+        const double2 u = __ldcg(reinterpret_cast<const double2*>(base) + tl);
+        const double2 v = __ldcg(reinterpret_cast<const double2*>(base) + tl + 32);
+        rr0 += u.x; wr0 += u.y;
+        rr1 += v.x; wr1 += v.y;
       }
-      rr = warp_sum(rr);
-      wr = warp_sum(wr);
+      if (tl < tps) {
+        const double2 u = __ldcg(reinterpret_cast<const double2*>(base) + tl);
+        rr0 += u.x; wr0 += u.y;
+      }
+      double rr = warp_sum(rr0 + rr1);
+      double wr = warp_sum(wr0 + wr1);
       if (lane == 0) {
         SysState z = st[s];
         if (it < 0) {
@@ -358,13 +596,13 @@ __global__ void __launch_bounds__(KCG_NT, 1) cg_persistent_kernel(const CgArgs a
     __syncthreads();
     if (blockIdx.x == 0 && tid == 0 && it >= 0 && it < a.history_cap) {
       double m = 0.0;
-      for (int i = 0; i < nact; ++i) m = fmax(m, st[act[i]].rel);
+      for (int ii = 0; ii < nact; ++ii) m = fmax(m, st[act[ii]].rel);
       a.history[it] = m;
     }
     ++it;
   }
   if (blockIdx.x == 0)
-    for (int s = tid; s < a.n_sys; s += KCG_NT) a.state_out[s] = st[s];
+    for (int s = tid; s < a.n_sys; s += NT) a.state_out[s] = st[s];
 }
 
 // --------------------------------------------------------------------------- apply / residual
@@ -542,13 +780,14 @@ cudaError_t launch_rhs(int K, cudaStream_t s, const double* Y, const double* E, 
   return cudaGetLastError();
 }
 
-template <int K>
+template <int K, bool HITS>
 static cudaError_t cg_config_t(int n_sys, int* max_grid, size_t* smem) {
-  const size_t sm = 2 * (size_t)cg_stage_bytes(K) + (size_t)n_sys * (sizeof(SysState) + sizeof(int));
-  cudaError_t e = cudaFuncSetAttribute(cg_persistent_kernel<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  const size_t sm = cg_stages(K) * (size_t)cg_stage_bytes(K) + cg_xstage_bytes(K) +
+                    (size_t)n_sys * (sizeof(SysState) + sizeof(int));
+  cudaError_t e = cudaFuncSetAttribute(cg_persistent_kernel<K, HITS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
   if (e != cudaSuccess) return e;
   int nb = 0, dev = 0, nsm = 0;
-  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, cg_persistent_kernel<K>, KCG_NT, sm);
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, cg_persistent_kernel<K, HITS>, cg_threads(K), sm);
   if (e != cudaSuccess) return e;
   e = cudaGetDevice(&dev);
   if (e != cudaSuccess) return e;
@@ -559,15 +798,21 @@ static cudaError_t cg_config_t(int n_sys, int* max_grid, size_t* smem) {
   return nb > 0 ? cudaSuccess : cudaErrorInvalidConfiguration;
 }
 
-cudaError_t cg_kernel_config(int K, int n_sys, int* max_grid, size_t* smem) {
-  KCG_DISPATCH(K, return cg_config_t<KK>(n_sys, max_grid, smem));
+cudaError_t cg_kernel_config(int K, bool hits, int n_sys, int* max_grid, size_t* smem) {
+  if (hits) { KCG_DISPATCH(K, return (cg_config_t<KK, true>(n_sys, max_grid, smem))); }
+  else { KCG_DISPATCH(K, return (cg_config_t<KK, false>(n_sys, max_grid, smem))); }
   return cudaErrorInvalidValue;
 }
 
 cudaError_t launch_cg(int K, cudaStream_t s, const CgArgs& a, const CgMaps& m, int grid, size_t smem) {
   void* args[2] = {(void*)&a, (void*)&m};
-  KCG_DISPATCH(K, return cudaLaunchCooperativeKernel((const void*)cg_persistent_kernel<KK>, dim3(grid),
-                                                      dim3(KCG_NT), args, smem, s));
+  if (a.hits) {
+    KCG_DISPATCH(K, return cudaLaunchCooperativeKernel((const void*)cg_persistent_kernel<KK, true>, dim3(grid),
+                                                        dim3(cg_threads(KK)), args, smem, s));
+  } else {
+    KCG_DISPATCH(K, return cudaLaunchCooperativeKernel((const void*)cg_persistent_kernel<KK, false>, dim3(grid),
+                                                        dim3(cg_threads(KK)), args, smem, s));
+  }
   return cudaErrorInvalidValue;
 }
 

@@ -19,7 +19,7 @@ from typing import Optional
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "lib", "libkroncg.so")
+LIB_PATH = os.environ.get("KCG_LIB_PATH") or os.path.join(_HERE, "lib", "libkroncg.so")
 
 if not os.path.exists(LIB_PATH):
     raise ImportError(f"libkroncg.so not built ({LIB_PATH}); run __graft_entry__.build()")
