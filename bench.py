@@ -127,6 +127,15 @@ def _patches_for(config: str, world: int, rank: int):
     return probs, list(range(len(probs))), costs
 
 
+def _oracle_iterations(config):
+    p = os.path.join(ROOT, "tests", "golden", "oracle_iterations.json")
+    if not os.path.exists(p):
+        return None
+    with open(p) as f:
+        d = json.load(f)
+    return d.get(config, {}).get("kron_cg_iterations")
+
+
 def _cpu_baseline(problems, gpu_iters_per_patch, budget_s=20.0):
     """Oracle (as it stands) on a bounded sample: assemble face 0 literally, run textbook CG for a
     bounded number of iterations, extrapolate to one full-sky solve with the measured per-face
@@ -150,7 +159,7 @@ def _cpu_baseline(problems, gpu_iters_per_patch, budget_s=20.0):
         t_it = (time.perf_counter() - t2) / max(res.iterations, 1)
         del probe
     n_faces = len(gpu_iters_per_patch)
-    total_its = sum(gpu_iters_per_patch)
+    total_its = sum(gpu_iters_per_patch)   # GPU counts (equal to the oracle's, see parity tests)
     t_sky = n_faces * t_asm + total_its * t_it
     return {"value": 1.0 / t_sky, "unit": "full-sky solves/s", "cores": 1, "kind": "oracle",
             "sample": (f"oracle (scipy CSR, literal Kronecker assembly, textbook HS-CG) on face 0 of "
@@ -187,11 +196,10 @@ def run_reference(args):
                 times.append((t_asm, t_it))
     t_asm = statistics.mean(t for t, _ in times)
     t_it = statistics.mean(t for _, t in times)
-    # full-sky extrapolation with the oracle's own iteration count model: the sample face's
-    # iteration count (probe run once, cheap relative to assembly at these sizes is not true,
-    # so use the survey-independent count from a full oracle solve only if requested)
-    its_face = args.ref_face_iters
-    t_sky = n_faces * (t_asm + its_face * t_it)
+    # extrapolation to one full solve with the ORACLE's own per-face iteration counts
+    # (tests/golden/oracle_iterations.json, written by scripts/oracle_iterations.py from oracle/)
+    its_faces = _oracle_iterations(args.config) or [args.ref_face_iters] * n_faces
+    t_sky = n_faces * t_asm + sum(its_faces) * t_it
     val = 1.0 / t_sky
     line = {
         "impl": "reference", "metric": METRIC, "value": val, "unit": "full-sky solves/s",
@@ -203,7 +211,7 @@ def run_reference(args):
         "cpu_baseline": {"value": val, "unit": "full-sky solves/s", "cores": 1, "kind": "oracle",
                          "sample": (f"per step: literal assembly of face 0 + {iters_sample} textbook "
                                     f"CG iterations (1 thread); extrapolated as {n_faces} faces x "
-                                    f"(assembly + {its_face} iterations)")},
+                                    f"assembly + {sum(its_faces)} oracle face-iterations")},
         "e2e": {"value": val, "unit": "full-sky solves/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
         "cg_iters_per_s": 1.0 / t_it,
@@ -365,7 +373,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--ref-iters", type=int, default=8, help="oracle CG iterations per reference step")
     ap.add_argument("--ref-face-iters", type=int, default=180,
-                    help="iterations per face used to extrapolate the reference arm (fullsky mean)")
+                    help="fallback iterations per face if tests/golden/oracle_iterations.json lacks the config")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "b200":
         print("warning: warmup < 3 violates the timing rules", file=sys.stderr)
