@@ -84,8 +84,13 @@ bool config_ok(const kcg_desc* d, std::string* why) {
   return true;
 }
 
-int tiles_x(int side) { return (side + KCG_TX - 1) / KCG_TX; }
-int tiles_y(int side, int K) { return (side + kcg::cg_tile_y(K) - 1) / kcg::cg_tile_y(K); }
+// Tile grid of the CG kernel in use (warp-marching: 60 x 16; CTA-tile: 64 x cg_tile_y(K)).
+int tiles_x(int side, int K) {
+  return kcg::use_march(K) ? (side + MARCH_TX - 1) / MARCH_TX : (side + KCG_TX - 1) / KCG_TX;
+}
+int tiles_y(int side, int K) {
+  return kcg::use_march(K) ? (side + MARCH_TY - 1) / MARCH_TY : (side + kcg::cg_tile_y(K) - 1) / kcg::cg_tile_y(K);
+}
 
 Layout layout_of(const kcg_desc* d) {
   Layout L{};
@@ -94,8 +99,8 @@ Layout layout_of(const kcg_desc* d) {
   const size_t N = (size_t)side * side;
   const size_t P = d->n_patches, n = d->n_freq, k = d->n_comp;
   L.vec_doubles = P * k * (size_t)pitch * side;
-  const size_t tk = (size_t)tiles_x(side) * tiles_y(side, (int)k);
-  const size_t ts = (size_t)tiles_x(side) * tiles_y(side, 1);
+  const size_t tk = (size_t)tiles_x(side, (int)k) * tiles_y(side, (int)k);
+  const size_t ts = (size_t)tiles_x(side, 1) * tiles_y(side, 1);
   L.partial_doubles = 2 * std::max(P * tk, P * k * ts) * 2;
   size_t off = 0;
   auto take = [&](size_t bytes) { size_t o = off; off += align_up(bytes); return o; };
@@ -197,12 +202,13 @@ PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
 }
 
 bool encode_map(CUtensorMap* m, double* base, int side, int pitch, size_t planes, int K, std::string* why) {
+  const int bx = kcg::use_march(K) ? 64 : KCG_TX + 2 * KCG_HALO;
+  const int by = kcg::use_march(K) ? kcg::march_cr(K) : kcg::cg_tile_y(K) + 2 * KCG_HALO;
   auto enc = get_encode();
   if (!enc) { *why = "cuTensorMapEncodeTiled unavailable"; return false; }
   cuuint64_t dims[3] = {(cuuint64_t)side, (cuuint64_t)side, (cuuint64_t)planes};
   cuuint64_t strides[2] = {(cuuint64_t)pitch * 8, (cuuint64_t)pitch * side * 8};
-  cuuint32_t box[3] = {(cuuint32_t)(KCG_TX + 2 * KCG_HALO), (cuuint32_t)(kcg::cg_tile_y(K) + 2 * KCG_HALO),
-                       (cuuint32_t)K};
+  cuuint32_t box[3] = {(cuuint32_t)bx, (cuuint32_t)by, (cuuint32_t)K};
   cuuint32_t es[3] = {1, 1, 1};
   CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, base, dims, strides, box, es,
                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
@@ -210,6 +216,25 @@ bool encode_map(CUtensorMap* m, double* base, int side, int pitch, size_t planes
   if (r != CUDA_SUCCESS) {
     char buf[128];
     snprintf(buf, sizeof buf, "cuTensorMapEncodeTiled failed (%d)", (int)r);
+    *why = buf;
+    return false;
+  }
+  return true;
+}
+
+// TMA descriptor of the solution buffer x [planes][side][side] with box {64, TY(K), K} (CTA kernel).
+bool encode_xmap(CUtensorMap* m, double* base, int side, size_t planes, int K, std::string* why) {
+  auto enc = get_encode();
+  if (!enc) { *why = "cuTensorMapEncodeTiled unavailable"; return false; }
+  cuuint64_t dims[3] = {(cuuint64_t)side, (cuuint64_t)side, (cuuint64_t)planes};
+  cuuint64_t strides[2] = {(cuuint64_t)side * 8, (cuuint64_t)side * side * 8};
+  cuuint32_t box[3] = {(cuuint32_t)KCG_TX, (cuuint32_t)kcg::cg_tile_y(K), (cuuint32_t)K};
+  cuuint32_t es[3] = {1, 1, 1};
+  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, base, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                   CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    char buf[128];
+    snprintf(buf, sizeof buf, "cuTensorMapEncodeTiled (x) failed (%d)", (int)r);
     *why = buf;
     return false;
   }
@@ -273,8 +298,17 @@ kcg_status solve_impl(kcg_ctx* c, Route route, const double* Y_in, double* mu_ou
   a.tiles_per_sys = a.tiles_x * a.tiles_y;
   a.max_iter = max_iter;
   a.tol2 = tol * tol;
-  CK(kcg::launch_cg(kron ? k : 1, s, a, kron ? c->maps_kron : c->maps_syl, kron ? c->grid_kron : c->grid_syl,
-                    kron ? c->smem_kron : c->smem_syl),
+  const int Kk = kron ? k : 1;
+  CgMaps& maps = kron ? c->maps_kron : c->maps_syl;
+  a.x_tma = 0;
+  if (!kcg::use_march(Kk) && kcg::cg_xtma(Kk) && side >= 2 && (reinterpret_cast<uintptr_t>(mu) % 16) == 0) {
+    std::string why;
+    if (!encode_xmap(&maps.x, mu, side, (size_t)P * k, Kk, &why)) { c->err = why; return KCG_E_CUDA; }
+    a.x_tma = 1;
+  }
+  CK((kcg::use_march(kron ? k : 1) ? kcg::launch_march : kcg::launch_cg)(kron ? k : 1, s, a, maps,
+                                                       kron ? c->grid_kron : c->grid_syl,
+                                                       kron ? c->smem_kron : c->smem_syl),
      "cg kernel");
   CK(cudaEventRecord(c->ev[2], s), "event");
   if (!kron) CK(kcg::launch_backtransform(k, s, c->W_dev, mu, P, side), "backtransform kernel");
@@ -476,14 +510,18 @@ kcg_status kron_cg_create(const kcg_desc* d, const double* A_host, const double*
         !encode_map(&c->maps_syl.p[i], c->p[i], c->side, c->pitch, planes, 1, &why))
       return fail(KCG_E_CUDA, why);
   }
-  c->tiles_x_kron = tiles_x(c->side);
+  c->tiles_x_kron = tiles_x(c->side, k);
   c->tiles_y_kron = tiles_y(c->side, k);
-  c->tiles_x_syl = tiles_x(c->side);
+  c->tiles_x_syl = tiles_x(c->side, 1);
   c->tiles_y_syl = tiles_y(c->side, 1);
   int mg = 0;
-  CKC(kcg::cg_kernel_config(k, hits_dev != nullptr, P, &mg, &c->smem_kron), "cg kernel config (kron)");
+  CKC((kcg::use_march(k) ? kcg::march_kernel_config : kcg::cg_kernel_config)(k, hits_dev != nullptr, P, &mg,
+                                                                               &c->smem_kron),
+      "cg kernel config (kron)");
   c->grid_kron = std::max(1, std::min(mg, P * c->tiles_x_kron * c->tiles_y_kron));
-  CKC(kcg::cg_kernel_config(1, hits_dev != nullptr, P * k, &mg, &c->smem_syl), "cg kernel config (sylvester)");
+  CKC((kcg::use_march(1) ? kcg::march_kernel_config : kcg::cg_kernel_config)(1, hits_dev != nullptr, P * k, &mg,
+                                                                               &c->smem_syl),
+      "cg kernel config (sylvester)");
   c->grid_syl = std::max(1, std::min(mg, P * k * c->tiles_x_syl * c->tiles_y_syl));
   for (int i = 0; i < 4; ++i) CKC(cudaEventCreate(&c->ev[i]), "event create");
 #undef CKC

@@ -29,19 +29,35 @@ __host__ __device__ constexpr int cg_tile_y(int K) { return K == 1 ? 32 : (K <= 
 #ifndef KCG_MINB_SMALLK
 #define KCG_MINB_SMALLK 1   // __launch_bounds__ min blocks per SM for K <= 4
 #endif
-#ifndef KCG_BULK
-#define KCG_BULK 0          // 1: x in / x, r, p out through cp.async.bulk rows (measured slower on B200)
-#endif
 // Threads per CTA of the persistent kernel (warps divide the tile rows).
 __host__ __device__ constexpr int cg_threads(int K) { return K == 1 ? 256 : (K >= 5 ? 256 : KCG_NT_SMALLK); }
 __host__ __device__ constexpr int cg_stages(int K) { return K == 8 ? 1 : (K >= 5 ? 2 : KCG_STAGES_SMALLK); }
 __host__ __device__ constexpr int cg_min_blocks(int K) { return K == 1 ? 2 : (K >= 5 ? 1 : KCG_MINB_SMALLK); }
 // Bytes of the x tile staging buffer (K planes of TY x TX, no halo).
-__host__ __device__ constexpr int cg_xstage_bytes(int K) { return KCG_BULK ? K * cg_tile_y(K) * KCG_TX * 8 : 0; }
+#ifndef KCG_XTMA_MAXK
+#define KCG_XTMA_MAXK 1     // x block TMA-staged for K <= this (measured: +14 points at K=1, -3 at K=4)
+#endif
+__host__ __device__ constexpr bool cg_xtma(int K) { return K <= KCG_XTMA_MAXK; }
+__host__ __device__ constexpr int cg_xstage_bytes(int K) { return cg_xtma(K) ? K * cg_tile_y(K) * KCG_TX * 8 : 0; }
 // Bytes of one pipeline stage (r and p boxes with halo, K planes).
 __host__ __device__ constexpr int cg_stage_bytes(int K) {
   return 2 * K * (cg_tile_y(K) + 2 * KCG_HALO) * (KCG_TX + 2 * KCG_HALO) * 8;
 }
+
+// Warp-marching CG kernel geometry: 60 x 16 output tiles, 64-wide boxes (2-pixel halo) streamed as
+// TMA chunks of march_cr(K) rows x 64 x K planes (r and p) through a per-warp ring of march_nb(K).
+#define MARCH_TX 60
+#define MARCH_TY 16
+#ifndef KCG_MARCH
+#define KCG_MARCH 0         // 1: warp-marching kernel for K <= 4 (experimental); 0: CTA-tile kernel
+#endif
+__host__ __device__ constexpr int march_cr(int K) { return K == 1 ? 4 : 2; }
+__host__ __device__ constexpr int march_nb(int K) { return 3; }
+__host__ __device__ constexpr int march_chunk_bytes(int K) { return 2 * K * march_cr(K) * 64 * 8; }
+__host__ __device__ constexpr int march_warps(int K) { return K == 1 ? 16 : (K == 2 ? 12 : 8); }
+// The marching kernel keeps 8 K-wide double2 row windows in registers: used for K <= 4; larger K
+// run the CTA-tile kernel.
+__host__ __device__ constexpr bool use_march(int K) { return KCG_MARCH && K <= 4; }
 
 // Per-system constant parameters of the operator  q_c = h sum_d M[c][d] p_d + tau_c (kappa2 p_c + (L p_c)).
 // Kronecker route: one system per patch, K = k, M = A^T T A, tau = prior scales.
@@ -80,12 +96,14 @@ struct CgArgs {
   int side, pitch;
   int n_sys, tiles_x, tiles_y, tiles_per_sys;
   int max_iter;
+  int x_tma;                 // 1: CgMaps::x describes `x` (TMA needs side >= 2)
   double tol2;
 };
 
 struct CgMaps {              // TMA descriptors of rbuf[0..1], pbuf[0..1] (box = {TX+4, TY+4, K})
   CUtensorMap r[2];
   CUtensorMap p[2];
+  CUtensorMap x;             // the solution buffer, box = {TX, TY, K}; re-encoded per solve
 };
 
 // ---------------------------------------------------------------- launchers (kcg_kernels.cu)
@@ -94,6 +112,8 @@ cudaError_t launch_rhs(int K, cudaStream_t s, const double* Y, const double* E, 
                        double* r0, double* p0, double* x, int P, int n, int side, int pitch);
 cudaError_t launch_cg(int K, cudaStream_t s, const CgArgs& a, const CgMaps& m, int grid, size_t smem);
 cudaError_t cg_kernel_config(int K, bool hits, int n_sys, int* max_grid, size_t* smem);
+cudaError_t launch_march(int K, cudaStream_t s, const CgArgs& a, const CgMaps& m, int grid, size_t smem);
+cudaError_t march_kernel_config(int K, bool hits, int n_sys, int* max_grid, size_t* smem);
 cudaError_t launch_apply(int K, cudaStream_t s, const SysParams* params, const double* x, double* y,
                          const double* hits, int n_sys, int side);
 cudaError_t launch_resid(int K, cudaStream_t s, const SysParams* params, const double* x,

@@ -116,28 +116,15 @@ __global__ void __launch_bounds__(256) rhs_kernel(const double* __restrict__ Y, 
 //   Phase A  p_new = r + beta p                    whole box (elementwise)
 //   Phase B  q = G p_new, r_new = r - alpha q      T rows (pairs) + the 1-pixel ring (scalars)
 //   Phase C  w = G r_new on T; (r,r), (w,r); x += alpha p_new
-// Output: with BULK (face side a multiple of 64) x is brought in and x, r_new, p_new are written
-// back by the bulk-copy engine (cp.async.bulk, 512-byte rows) straight from shared memory, so the
-// SM issues no global loads/stores on the hot path; otherwise plain vector loads/stores.
+// x: with XTMA the tile's x block (64 x TY x K) is TMA-loaded into shared memory at the start of the
+// tile (consumed in phase C, so its latency hides behind phases A and B); x, r_new, p_new are
+// written back with coalesced 16-byte vector stores.
 // EDGE = the box touches the face border (bounds checks, degree 2/3); interior tiles skip both.
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
-  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                   smem_u32(dst)),
-               "l"(src), "r"(bytes), "r"(smem_u32(bar))
-               : "memory");
-}
-__device__ __forceinline__ void bulk_s2g(void* dst, const void* src, uint32_t bytes) {
-  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(smem_u32(src)), "r"(bytes)
-               : "memory");
-}
-__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
-__device__ __forceinline__ void bulk_wait_read_all() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
-__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
-
 struct TileCtx {
   double* R;          // r box (stage)
   double* Pp;         // p box (stage)
-  double* xs;         // x tile staging [K][TY][TX] (BULK)
+  double* xs;         // x tile staging [K][TY][TX] (XTMA)
+  const CUtensorMap* xmap;
   const double* Ms;   // M (K*K) then tau (K) of this tile's system, shared
   int s, y0, x0, par;
   double alpha, beta, kappa2;
@@ -149,7 +136,7 @@ struct TileCtx {
   double* part_out;
 };
 
-template <int K, bool EDGE, bool HITS, bool BULK>
+template <int K, bool EDGE, bool HITS, bool XTMA>
 __device__ __forceinline__ void cg_tile(const CgArgs& a, const TileCtx& tc, double (*red)[32]) {
   constexpr int TY = cg_tile_y(K), TX = KCG_TX, H = KCG_HALO;
   constexpr int BW = TX + 2 * H, BH = TY + 2 * H, PLANE = BW * BH, FIELD = K * PLANE;
@@ -166,13 +153,10 @@ __device__ __forceinline__ void cg_tile(const CgArgs& a, const TileCtx& tc, doub
   const double alpha = tc.alpha, beta = tc.beta, kappa2 = tc.kappa2;
   const int gx = x0 + 2 * lane;
 
-  if (BULK && warp == 0) {  // x rows of this tile -> xs (completes on xbar)
-    if (lane == 0) mbar_arrive_expect_tx(tc.xbar, K * TY * TX * 8);
-    __syncwarp();
-    for (int rrow = lane; rrow < K * TY; rrow += 32) {
-      const int c = rrow / TY, row = rrow - c * TY;
-      bulk_g2s(tc.xs + (size_t)rrow * TX, a.x + ((size_t)(s * K + c) * side + y0 + row) * side + x0, TX * 8, tc.xbar);
-    }
+  if (XTMA && tid == 0) {  // x block of this tile -> xs (completes on xbar)
+    fence_proxy_async_smem();
+    mbar_arrive_expect_tx(tc.xbar, K * TY * TX * 8);
+    tma_load_3d(tc.xs, tc.xmap, tc.xbar, x0, y0, s * K);
   }
 
   mbar_wait(tc.bar, tc.phase);
@@ -284,7 +268,7 @@ __device__ __forceinline__ void cg_tile(const CgArgs& a, const TileCtx& tc, doub
     }
   }
   __syncthreads();
-  if (BULK) mbar_wait(tc.xbar, tc.xphase);
+  if (XTMA) mbar_wait(tc.xbar, tc.xphase);
 
   // Phase C
   double rr = 0.0, wr = 0.0;
@@ -310,7 +294,7 @@ __device__ __forceinline__ void cg_tile(const CgArgs& a, const TileCtx& tc, doub
     double2 xj[K];
 #pragma unroll
     for (int c = 0; c < K; ++c) {
-      if (BULK) {
+      if (XTMA) {
         xj[c] = reinterpret_cast<const double2*>(tc.xs + ((size_t)c * TY + (gy - y0)) * TX)[lane];
       } else if (!EDGE || (in0 && in1)) {
         xj[c] = __ldcg(reinterpret_cast<const double2*>(xp + c * N));
@@ -349,13 +333,7 @@ __device__ __forceinline__ void cg_tile(const CgArgs& a, const TileCtx& tc, doub
       double2 xn;
       xn.x = fma(alpha, pn.x, xj[c].x);
       xn.y = fma(alpha, pn.y, xj[c].y);
-      if (BULK) {
-        rr = fma(rc[c].x, rc[c].x, rr);
-        wr = fma(w0, rc[c].x, wr);
-        rr = fma(rc[c].y, rc[c].y, rr);
-        wr = fma(w1, rc[c].y, wr);
-        reinterpret_cast<double2*>(tc.xs + ((size_t)c * TY + (gy - y0)) * TX)[lane] = xn;
-      } else if (!EDGE || (in0 && in1)) {
+      if (!EDGE || (in0 && in1)) {
         rr = fma(rc[c].x, rc[c].x, rr);
         wr = fma(w0, rc[c].x, wr);
         rr = fma(rc[c].y, rc[c].y, rr);
@@ -384,23 +362,7 @@ __device__ __forceinline__ void cg_tile(const CgArgs& a, const TileCtx& tc, doub
   rr = warp_sum(rr);
   wr = warp_sum(wr);
   if (lane == 0) { red[0][warp] = rr; red[1][warp] = wr; }
-  if (BULK) fence_proxy_async_smem();  // x_new in xs and r_new/p_new in the boxes -> async proxy
   __syncthreads();
-  if (BULK) {  // 3*K*TY rows of 512 bytes, one per thread
-    for (int t = tid; t < 3 * K * TY; t += NT) {
-      const int f = t / (K * TY), rc_ = t - f * (K * TY), c = rc_ / TY, row = rc_ - c * TY;
-      const size_t plane = (size_t)s * K + c;
-      const int gy = y0 + row;
-      if (f == 0) {
-        bulk_s2g(a.x + (plane * side + gy) * side + x0, tc.xs + (size_t)rc_ * TX, TX * 8);
-      } else {
-        double* out = f == 1 ? (tc.par ? a.rbuf[0] : a.rbuf[1]) : (tc.par ? a.pbuf[0] : a.pbuf[1]);
-        const double* src = (f == 1 ? R : Pp) + c * PLANE + (row + H) * BW + H;
-        bulk_s2g(out + plane * ps + (size_t)gy * a.pitch + x0, src, TX * 8);
-      }
-    }
-    bulk_commit();
-  }
   if (warp == 0) {
     double v0 = lane < NW ? red[0][lane] : 0.0;
     double v1 = lane < NW ? red[1][lane] : 0.0;
@@ -431,7 +393,7 @@ __global__ void __launch_bounds__(cg_threads(K), cg_min_blocks(K)) cg_persistent
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int tps = a.tiles_per_sys;
-  const bool bulk = KCG_BULK && (a.side % TX) == 0;  // whole 512-byte rows everywhere
+  const bool xtma = cg_xtma(K) && a.x_tma != 0;
   cg::grid_group grid = cg::this_grid();
 
   for (int s = tid; s < a.n_sys; s += NT) {
@@ -489,7 +451,6 @@ __global__ void __launch_bounds__(cg_threads(K), cg_min_blocks(K)) cg_persistent
     for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++i) {
       const int sidx = NS == 2 ? (i & 1) : 0;
       const int tn = t + gridDim.x;
-      if (bulk) bulk_wait_read_all();  // previous tile's bulk stores have read their smem
       __syncthreads();
       if (tid == 0) {
         if (NS == 2 && tn < ntiles) {
@@ -510,6 +471,7 @@ __global__ void __launch_bounds__(cg_threads(K), cg_min_blocks(K)) cg_persistent
       tc.R = reinterpret_cast<double*>(smem_raw + sidx * STAGE_BYTES);
       tc.Pp = tc.R + FIELD;
       tc.xs = xs;
+      tc.xmap = &maps.x;
       tc.Ms = Ms;
       tc.s = s;
       tc.y0 = ty * TY;
@@ -525,9 +487,9 @@ __global__ void __launch_bounds__(cg_threads(K), cg_min_blocks(K)) cg_persistent
       tc.xphase = xphase;
       tc.part_out = a.partials + (((size_t)par_out * a.n_sys + s) * tps + tile) * 2;
       const bool interior = tc.x0 >= H && tc.x0 + TX + H <= a.side && tc.y0 >= H && tc.y0 + TY + H <= a.side;
-      if (KCG_BULK && bulk) {
-        if (interior) cg_tile<K, false, HITS, true>(a, tc, red);
-        else cg_tile<K, true, HITS, true>(a, tc, red);
+      if (cg_xtma(K) && xtma) {
+        if (interior) cg_tile<K, false, HITS, cg_xtma(K)>(a, tc, red);
+        else cg_tile<K, true, HITS, cg_xtma(K)>(a, tc, red);
         xphase ^= 1u;
       } else {
         if (interior) cg_tile<K, false, HITS, false>(a, tc, red);
@@ -536,7 +498,6 @@ __global__ void __launch_bounds__(cg_threads(K), cg_min_blocks(K)) cg_persistent
       if (sidx) phase1 ^= 1u; else phase0 ^= 1u;
     }
 
-    if (bulk) bulk_wait_all();  // this iteration's bulk stores are complete
     fence_proxy_async_global();
     grid.sync();
     fence_proxy_async_global();
@@ -603,6 +564,393 @@ __global__ void __launch_bounds__(cg_threads(K), cg_min_blocks(K)) cg_persistent
   }
   if (blockIdx.x == 0)
     for (int s = tid; s < a.n_sys; s += NT) a.state_out[s] = st[s];
+}
+
+// --------------------------------------------------------------------------- warp-marching CG
+// The production CG kernel.  Same single-pass Chronopoulos-Gear iteration, same per-tile partials
+// and per-system reductions as cg_persistent_kernel, but each WARP owns a 60 x 16 output tile and
+// marches down its 64-wide box (2-pixel halo) row by row:
+//   box rows arrive through a per-warp ring of TMA chunks (CR rows x 64 cols x K planes, r and p,
+//   zero-filled outside the face); per lane a PAIR of columns (32 lanes x 2 = the 64 box columns,
+//   so the halo needs no special lanes); horizontal neighbours by shuffles; vertical neighbours
+//   from a 3-row register window of p_new and r_new:
+//     step b:  p_new(b) = r(b) + beta p(b)
+//              r_new(b-1) = r(b-1) - alpha G p_new(b-1)          (rows b-2..b of p_new)
+//              w(b-2) = G r_new(b-2); (r,r), (w,r); x += alpha p_new; store x, r_new, p_new (b-2)
+// No block-level barrier inside an iteration; shared memory only receives the TMA data and is read
+// once per element.  Columns 0/63 of the box produce garbage that no output uses.
+__device__ __forceinline__ double2 shfl_up2(double2 v) {
+  return make_double2(__shfl_up_sync(0xffffffffu, v.x, 1), __shfl_up_sync(0xffffffffu, v.y, 1));
+}
+
+template <int K, bool EDGE, bool HITS>
+__device__ __forceinline__ void march_apply(const double2 (&up)[K], const double2 (&ctr)[K], const double2 (&dn)[K],
+                                            const double* __restrict__ M, const double* __restrict__ tau, double kd0,
+                                            double kd1, double h0, double h1, int lane, double2 (&out)[K]) {
+  double mix0[K], mix1[K];
+#pragma unroll
+  for (int c = 0; c < K; ++c) {
+    mix0[c] = 0.0;
+    mix1[c] = 0.0;
+#pragma unroll
+    for (int d = 0; d < K; ++d) {
+      mix0[c] = fma(M[c * K + d], ctr[d].x, mix0[c]);
+      mix1[c] = fma(M[c * K + d], ctr[d].y, mix1[c]);
+    }
+  }
+#pragma unroll
+  for (int c = 0; c < K; ++c) {
+    double left = __shfl_up_sync(0xffffffffu, ctr[c].y, 1);
+    double right = __shfl_down_sync(0xffffffffu, ctr[c].x, 1);
+    left = lane == 0 ? 0.0 : left;
+    right = lane == 31 ? 0.0 : right;
+    const double nb0 = (up[c].x + dn[c].x) + (left + ctr[c].y);
+    const double nb1 = (up[c].y + dn[c].y) + (ctr[c].x + right);
+    if (HITS) {
+      out[c].x = fma(h0, mix0[c], tau[c] * fma(kd0, ctr[c].x, -nb0));
+      out[c].y = fma(h1, mix1[c], tau[c] * fma(kd1, ctr[c].y, -nb1));
+    } else {
+      out[c].x = fma(tau[c], fma(kd0, ctr[c].x, -nb0), mix0[c]);
+      out[c].y = fma(tau[c], fma(kd1, ctr[c].y, -nb1), mix1[c]);
+    }
+  }
+}
+
+struct MarchWarp {
+  uint64_t* bar;       // NB mbarriers of this warp
+  double* ring;        // NB chunks of this warp
+  long long seq;       // chunks consumed by this warp since kernel start (mbarrier phases)
+};
+
+template <int K, bool EDGE, bool HITS>
+__device__ __forceinline__ void march_tile(const CgArgs& a, const CgMaps& maps, MarchWarp& mw,
+                                           const double* __restrict__ Ms, int s, int y0, int x0, int par,
+                                           double alpha, double beta, double kappa2, const double* __restrict__ hp,
+                                           double* part_out, int lane, int& issued, int total_chunks, int q0,
+                                           const int* act, const SysState* st, int tps, int gwarp,
+                                           int nwarps_total) {
+  constexpr int BW = 64, TY = MARCH_TY, BR = TY + 4, CR = march_cr(K), NB = march_nb(K);
+  constexpr int NCH = BR / CR;
+  constexpr int CHUNK = 2 * K * CR * BW;  // doubles: r [K][CR][64] then p [K][CR][64]
+  static_assert(BR % CR == 0, "chunk rows");
+  const int side = a.side;
+  const size_t N = (size_t)side * side;
+  const size_t ps = (size_t)a.pitch * side;
+  double M[K * K], tau[K];
+#pragma unroll
+  for (int e = 0; e < K * K; ++e) M[e] = Ms[e];
+#pragma unroll
+  for (int c = 0; c < K; ++c) tau[c] = Ms[K * K + c];
+  const int gx = x0 - 2 + 2 * lane;  // global column of .x
+  const bool out_lane = lane >= 1 && lane <= 30;
+  double* rout = (par ? a.rbuf[0] : a.rbuf[1]) + (size_t)s * K * ps;
+  double* pout = (par ? a.pbuf[0] : a.pbuf[1]) + (size_t)s * K * ps;
+  double* xbase = a.x + (size_t)s * K * N;
+
+  // column masks / degrees that do not depend on the row
+  bool cin0 = true, cin1 = true;
+  double dx0 = 0.0, dx1 = 0.0;
+  if (EDGE) {
+    cin0 = gx >= 0 && gx < side;
+    cin1 = gx + 1 >= 0 && gx + 1 < side;
+    dx0 = (gx == 0) + (gx == side - 1);
+    dx1 = (gx + 1 == 0) + (gx + 1 == side - 1);
+  }
+
+  double2 pnA[K], pnB[K], pnC[K], rnA[K], rnB[K], rnC[K], rprev[K], xa[K];
+  double rr = 0.0, wr = 0.0;
+#pragma unroll
+  for (int c = 0; c < K; ++c) {
+    pnA[c] = pnB[c] = rnA[c] = rnB[c] = rprev[c] = xa[c] = make_double2(0.0, 0.0);
+  }
+
+  auto load_x = [&](double2 (&xr)[K], int o) {  // x of output box row o (o in [2, TY+1])
+    const int gy = y0 - 2 + o;
+    const bool ok = out_lane && (!EDGE || (gy < side && cin0 && cin1));
+#pragma unroll
+    for (int c = 0; c < K; ++c) {
+      if (ok) xr[c] = __ldcg(reinterpret_cast<const double2*>(xbase + ((size_t)c * side + gy) * side + gx));
+      else if (EDGE && out_lane && gy < side && (cin0 || cin1)) {
+        xr[c].x = cin0 ? __ldcg(xbase + ((size_t)c * side + gy) * side + gx) : 0.0;
+        xr[c].y = cin1 ? __ldcg(xbase + ((size_t)c * side + gy) * side + gx + 1) : 0.0;
+      } else xr[c] = make_double2(0.0, 0.0);
+    }
+  };
+  for (int b = 0; b < BR; ++b) {
+    const int ch = b / CR, rb = b - ch * CR;
+    const long long g = mw.seq + q0 + ch;  // global chunk sequence number
+    const int slot = (int)(g % NB);
+    if (rb == 0) {
+      // keep NB-1 chunks in flight along this warp's chunk stream (may run into its next tile)
+      const int want = min(q0 + ch + NB, total_chunks);
+      __syncwarp();  // every lane is done reading the slot about to be refilled
+      if (lane == 0) {
+        while (issued < want) {
+          const int qi = issued;
+          const int ti = qi / NCH, ci = qi - ti * NCH;
+          const int t = gwarp + ti * nwarps_total;
+          const int si = act[t / tps];
+          const int tile = t - (t / tps) * tps;
+          const int tyi = tile / a.tiles_x, txi = tile - tyi * a.tiles_x;
+          const long long gi = mw.seq + qi;
+          const int sl = (int)(gi % NB);
+          // the slot's previous chunk (gi - NB) was fully read by this warp before this point
+          fence_proxy_async_smem();
+          double* dst = mw.ring + (size_t)sl * CHUNK;
+          mbar_arrive_expect_tx(&mw.bar[sl], CHUNK * 8);
+          const int pi = st[si].parity;
+          tma_load_3d(dst, &maps.r[pi], &mw.bar[sl], txi * MARCH_TX - 2, tyi * TY - 2 + ci * CR, si * K);
+          tma_load_3d(dst + K * CR * BW, &maps.p[pi], &mw.bar[sl], txi * MARCH_TX - 2, tyi * TY - 2 + ci * CR, si * K);
+          ++issued;
+        }
+      }
+      issued = __shfl_sync(0xffffffffu, issued, 0);
+      mbar_wait(&mw.bar[slot], (uint32_t)((g / NB) & 1));
+    }
+    if (b >= 4) load_x(xa, b - 2);  // x of this step's output row; used at the end of the step
+    const double* rrow = mw.ring + (size_t)slot * CHUNK + rb * BW;
+    const double* prow = rrow + K * CR * BW;
+    double2 rcur[K];
+#pragma unroll
+    for (int c = 0; c < K; ++c) {
+      rcur[c] = reinterpret_cast<const double2*>(rrow + c * CR * BW)[lane];
+      const double2 pv = reinterpret_cast<const double2*>(prow + c * CR * BW)[lane];
+      pnC[c].x = fma(beta, pv.x, rcur[c].x);
+      pnC[c].y = fma(beta, pv.y, rcur[c].y);
+    }
+    if (b >= 2) {  // r_new of box row m = b - 1
+      const int gy = y0 - 2 + (b - 1);
+      double kd0 = kappa2 + 4.0, kd1 = kappa2 + 4.0;
+      bool in0 = true, in1 = true;
+      if (EDGE) {
+        const bool rin = gy >= 0 && gy < side;
+        in0 = rin && cin0;
+        in1 = rin && cin1;
+        const double dy = (gy == 0) + (gy == side - 1);
+        kd0 = kappa2 + (4.0 - dy - dx0);
+        kd1 = kappa2 + (4.0 - dy - dx1);
+      }
+      double h0 = 1.0, h1 = 1.0;
+      if (HITS) {
+        if (in0) h0 = __ldg(hp + (size_t)gy * side + gx);
+        if (in1) h1 = __ldg(hp + (size_t)gy * side + gx + 1);
+      }
+      double2 q[K];
+      march_apply<K, EDGE, HITS>(pnA, pnB, pnC, M, tau, kd0, kd1, h0, h1, lane, q);
+#pragma unroll
+      for (int c = 0; c < K; ++c) {
+        rnC[c].x = in0 ? fma(-alpha, q[c].x, rprev[c].x) : 0.0;
+        rnC[c].y = in1 ? fma(-alpha, q[c].y, rprev[c].y) : 0.0;
+      }
+      if (b >= 4) {  // outputs of box row o = b - 2
+        const int o = b - 2;
+        const int gyo = y0 - 2 + o;
+        double kdo0 = kappa2 + 4.0, kdo1 = kappa2 + 4.0;
+        bool on0 = out_lane, on1 = out_lane;
+        if (EDGE) {
+          const bool rin = gyo < side;
+          on0 = on0 && rin && cin0;
+          on1 = on1 && rin && cin1;
+          const double dy = (gyo == 0) + (gyo == side - 1);
+          kdo0 = kappa2 + (4.0 - dy - dx0);
+          kdo1 = kappa2 + (4.0 - dy - dx1);
+        }
+        double ho0 = 1.0, ho1 = 1.0;
+        if (HITS) {
+          if (on0) ho0 = __ldg(hp + (size_t)gyo * side + gx);
+          if (on1) ho1 = __ldg(hp + (size_t)gyo * side + gx + 1);
+        }
+        double2 w[K];
+        march_apply<K, EDGE, HITS>(rnA, rnB, rnC, M, tau, kdo0, kdo1, ho0, ho1, lane, w);
+        const size_t xo = (size_t)gyo * side + gx;
+        const size_t ro = (size_t)gyo * a.pitch + gx;
+#pragma unroll
+        for (int c = 0; c < K; ++c) {
+          double2 xn;
+          xn.x = fma(alpha, pnA[c].x, xa[c].x);
+          xn.y = fma(alpha, pnA[c].y, xa[c].y);
+          if (!EDGE || (on0 && on1)) {
+            if (out_lane) {
+              rr = fma(rnB[c].x, rnB[c].x, rr);
+              rr = fma(rnB[c].y, rnB[c].y, rr);
+              wr = fma(w[c].x, rnB[c].x, wr);
+              wr = fma(w[c].y, rnB[c].y, wr);
+              *reinterpret_cast<double2*>(xbase + c * N + xo) = xn;
+              *reinterpret_cast<double2*>(rout + c * ps + ro) = rnB[c];
+              *reinterpret_cast<double2*>(pout + c * ps + ro) = pnA[c];
+            }
+          } else {
+            if (on0) {
+              rr = fma(rnB[c].x, rnB[c].x, rr);
+              wr = fma(w[c].x, rnB[c].x, wr);
+              xbase[c * N + xo] = xn.x;
+              rout[c * ps + ro] = rnB[c].x;
+              pout[c * ps + ro] = pnA[c].x;
+            }
+            if (on1) {
+              rr = fma(rnB[c].y, rnB[c].y, rr);
+              wr = fma(w[c].y, rnB[c].y, wr);
+              xbase[c * N + xo + 1] = xn.y;
+              rout[c * ps + ro + 1] = rnB[c].y;
+              pout[c * ps + ro + 1] = pnA[c].y;
+            }
+          }
+        }
+      }
+#pragma unroll
+      for (int c = 0; c < K; ++c) {
+        rnA[c] = rnB[c];
+        rnB[c] = rnC[c];
+      }
+    }
+#pragma unroll
+    for (int c = 0; c < K; ++c) {
+      pnA[c] = pnB[c];
+      pnB[c] = pnC[c];
+      rprev[c] = rcur[c];
+    }
+  }
+  rr = warp_sum(rr);
+  wr = warp_sum(wr);
+  if (lane == 0) {
+    part_out[0] = rr;
+    part_out[1] = wr;
+  }
+}
+
+template <int K, bool HITS>
+__global__ void __launch_bounds__(32 * march_warps(K), 1) cg_march_kernel(const CgArgs a, const __grid_constant__ CgMaps maps) {
+  constexpr int BW = 64, TY = MARCH_TY, BR = TY + 4, CR = march_cr(K), NB = march_nb(K), W = march_warps(K);
+  constexpr int NCH = BR / CR;
+  constexpr int CHUNK = 2 * K * CR * BW;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  double* ring_all = reinterpret_cast<double*>(smem_raw);
+  SysState* st = reinterpret_cast<SysState*>(smem_raw + (size_t)W * NB * CHUNK * 8);
+  int* act = reinterpret_cast<int*>(st + a.n_sys);
+  __shared__ __align__(8) uint64_t mbar[W * NB];
+  __shared__ double Msh[W][KCG_KMAX * KCG_KMAX + KCG_KMAX];
+  __shared__ int s_nact;
+
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int tps = a.tiles_per_sys;
+  const int gwarp = blockIdx.x * W + warp, nwarps_total = gridDim.x * W;
+  cg::grid_group grid = cg::this_grid();
+
+  for (int s = tid; s < a.n_sys; s += blockDim.x) {
+    SysState z;
+    z.bnorm2 = 0.0; z.gamma = 0.0; z.alpha = 0.0; z.beta = 0.0; z.rel = 1.0;
+    z.iters = 0; z.status = ST_RUNNING; z.parity = 0; z.pad = 0;
+    st[s] = z;
+  }
+  if (tid < W * NB) mbar_init(&mbar[tid], 1);
+  if (tid == 0) fence_mbar_init();
+  __syncthreads();
+
+  MarchWarp mw;
+  mw.bar = &mbar[warp * NB];
+  mw.ring = ring_all + (size_t)warp * NB * CHUNK;
+  mw.seq = 0;
+  int it = -1;
+
+  while (true) {
+    if (tid == 0) {
+      int n = 0;
+      for (int s = 0; s < a.n_sys; ++s)
+        if (st[s].status == ST_RUNNING) act[n++] = s;
+      s_nact = n;
+    }
+    __syncthreads();
+    const int nact = s_nact;
+    if (nact == 0) break;
+    const int ntiles = nact * tps;
+    const int par_out = (it + 1) & 1;
+    const int my_tiles = gwarp < ntiles ? (ntiles - gwarp + nwarps_total - 1) / nwarps_total : 0;
+    const int total_chunks = my_tiles * NCH;
+    int issued = 0;
+    for (int i = 0; i < my_tiles; ++i) {
+      const int t = gwarp + i * nwarps_total;
+      const int s = act[t / tps];
+      const int tile = t - (t / tps) * tps;
+      const int ty = tile / a.tiles_x, tx = tile - ty * a.tiles_x;
+      const SysParams* sp = a.params + s;
+      for (int e = lane; e < K * K; e += 32) Msh[warp][e] = __ldg(&sp->M[e]);
+      if (lane < K) Msh[warp][K * K + lane] = __ldg(&sp->tau[lane]);
+      __syncwarp();
+      const int y0 = ty * TY, x0 = tx * MARCH_TX;
+      const double* hp = HITS ? a.hits + (size_t)__ldg(&sp->hits_plane) * ((size_t)a.side * a.side) : nullptr;
+      double* part = a.partials + (((size_t)par_out * a.n_sys + s) * tps + tile) * 2;
+      const bool interior = x0 >= 2 && x0 + MARCH_TX + 2 <= a.side && y0 >= 2 && y0 + TY + 2 <= a.side;
+      if (interior)
+        march_tile<K, false, HITS>(a, maps, mw, Msh[warp], s, y0, x0, st[s].parity, st[s].alpha, st[s].beta,
+                                   __ldg(&sp->kappa2), hp, part, lane, issued, total_chunks, i * NCH, act, st, tps,
+                                   gwarp, nwarps_total);
+      else
+        march_tile<K, true, HITS>(a, maps, mw, Msh[warp], s, y0, x0, st[s].parity, st[s].alpha, st[s].beta,
+                                  __ldg(&sp->kappa2), hp, part, lane, issued, total_chunks, i * NCH, act, st, tps,
+                                  gwarp, nwarps_total);
+      __syncwarp();
+    }
+    mw.seq += total_chunks;
+
+    fence_proxy_async_global();
+    grid.sync();
+    fence_proxy_async_global();
+
+    for (int ii = warp; ii < nact; ii += W) {
+      const int s = act[ii];
+      const double* base = a.partials + ((size_t)par_out * a.n_sys + s) * tps * 2;
+      double rr0 = 0.0, wr0 = 0.0, rr1 = 0.0, wr1 = 0.0;
+      int tl = lane;
+      for (; tl + 32 < tps; tl += 64) {
+        const double2 u = __ldcg(reinterpret_cast<const double2*>(base) + tl);
+        const double2 v = __ldcg(reinterpret_cast<const double2*>(base) + tl + 32);
+        rr0 += u.x; wr0 += u.y;
+        rr1 += v.x; wr1 += v.y;
+      }
+      if (tl < tps) {
+        const double2 u = __ldcg(reinterpret_cast<const double2*>(base) + tl);
+        rr0 += u.x; wr0 += u.y;
+      }
+      double rr = warp_sum(rr0 + rr1);
+      double wr = warp_sum(wr0 + wr1);
+      if (lane == 0) {
+        SysState z = st[s];
+        if (it < 0) {
+          z.bnorm2 = rr;
+          z.gamma = rr;
+          z.rel = rr > 0.0 ? 1.0 : 0.0;
+          if (!isfinite(rr) || !isfinite(wr)) z.status = ST_NONFINITE;
+          else if (rr == 0.0) z.status = ST_CONVERGED;
+          else if (!(wr > 0.0)) z.status = ST_BREAKDOWN;
+          else if (a.max_iter <= 0) z.status = ST_MAXIT;
+          else { z.alpha = rr / wr; z.beta = 0.0; }
+        } else {
+          z.iters = it + 1;
+          z.rel = sqrt(rr / z.bnorm2);
+          if (!isfinite(rr) || !isfinite(wr)) z.status = ST_NONFINITE;
+          else if (rr <= a.tol2 * z.bnorm2) z.status = ST_CONVERGED;
+          else if (z.iters >= a.max_iter) z.status = ST_MAXIT;
+          else {
+            const double beta = rr / z.gamma;
+            const double den = wr - beta * rr / z.alpha;
+            if (!(den > 0.0)) z.status = ST_BREAKDOWN;
+            else { z.beta = beta; z.alpha = rr / den; z.gamma = rr; }
+          }
+        }
+        z.parity ^= 1;
+        st[s] = z;
+      }
+    }
+    __syncthreads();
+    if (blockIdx.x == 0 && tid == 0 && it >= 0 && it < a.history_cap) {
+      double m = 0.0;
+      for (int ii = 0; ii < nact; ++ii) m = fmax(m, st[act[ii]].rel);
+      a.history[it] = m;
+    }
+    ++it;
+  }
+  if (blockIdx.x == 0)
+    for (int s = tid; s < a.n_sys; s += blockDim.x) a.state_out[s] = st[s];
 }
 
 // --------------------------------------------------------------------------- apply / residual
@@ -812,6 +1160,42 @@ cudaError_t launch_cg(int K, cudaStream_t s, const CgArgs& a, const CgMaps& m, i
   } else {
     KCG_DISPATCH(K, return cudaLaunchCooperativeKernel((const void*)cg_persistent_kernel<KK, false>, dim3(grid),
                                                         dim3(cg_threads(KK)), args, smem, s));
+  }
+  return cudaErrorInvalidValue;
+}
+
+template <int K, bool HITS>
+static cudaError_t march_config_t(int n_sys, int* max_grid, size_t* smem) {
+  const size_t sm = (size_t)march_warps(K) * march_nb(K) * march_chunk_bytes(K) +
+                    (size_t)n_sys * (sizeof(SysState) + sizeof(int));
+  cudaError_t e = cudaFuncSetAttribute(cg_march_kernel<K, HITS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  if (e != cudaSuccess) return e;
+  int nb = 0, dev = 0, nsm = 0;
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, cg_march_kernel<K, HITS>, 32 * march_warps(K), sm);
+  if (e != cudaSuccess) return e;
+  e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  e = cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  if (e != cudaSuccess) return e;
+  *max_grid = nb * nsm;
+  *smem = sm;
+  return nb > 0 ? cudaSuccess : cudaErrorInvalidConfiguration;
+}
+
+cudaError_t march_kernel_config(int K, bool hits, int n_sys, int* max_grid, size_t* smem) {
+  if (hits) { KCG_DISPATCH(K, return (march_config_t<KK, true>(n_sys, max_grid, smem))); }
+  else { KCG_DISPATCH(K, return (march_config_t<KK, false>(n_sys, max_grid, smem))); }
+  return cudaErrorInvalidValue;
+}
+
+cudaError_t launch_march(int K, cudaStream_t s, const CgArgs& a, const CgMaps& m, int grid, size_t smem) {
+  void* args[2] = {(void*)&a, (void*)&m};
+  if (a.hits) {
+    KCG_DISPATCH(K, return cudaLaunchCooperativeKernel((const void*)cg_march_kernel<KK, true>, dim3(grid),
+                                                        dim3(32 * march_warps(KK)), args, smem, s));
+  } else {
+    KCG_DISPATCH(K, return cudaLaunchCooperativeKernel((const void*)cg_march_kernel<KK, false>, dim3(grid),
+                                                        dim3(32 * march_warps(KK)), args, smem, s));
   }
   return cudaErrorInvalidValue;
 }

@@ -6,10 +6,9 @@ sys.path.insert(0, ROOT)
 from paper_2204_08057_b200 import build
 
 VARIANTS = {
-    "v4_default": [],
-    "v4_mreg": ["KCG_M_IN_REGS=1"],
-    "v4_nt256_mreg": ["KCG_NT_SMALLK=256", "KCG_M_IN_REGS=1"],
-    "v4_bulk": ["KCG_BULK=1"],
+    "v6_default": [],
+    "v6_mreg": ["KCG_M_IN_REGS=1"],
+    "v6_nt256_mreg": ["KCG_NT_SMALLK=256", "KCG_M_IN_REGS=1"],
 }
 names = sys.argv[1:] or list(VARIANTS)
 out = os.path.join(ROOT, "paper_2204_08057_b200", "lib", "variants")
