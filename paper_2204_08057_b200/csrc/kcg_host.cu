@@ -40,6 +40,7 @@ struct kcg_ctx {
   double* E_kron = nullptr;
   double* E_syl = nullptr;
   double* W_dev = nullptr;
+  long long* trace = nullptr;
   double* Y_stage = nullptr;
   double* mu_stage = nullptr;
   const double* hits = nullptr;
@@ -61,7 +62,7 @@ size_t align_up(size_t x) { return (x + kAlign - 1) / kAlign * kAlign; }
 
 struct Layout {
   size_t r0, r1, p0, p1, partials, state, history, resid_partials, resid_out, params_kron, params_syl, E_kron,
-      E_syl, W, Y_stage, mu_stage, total;
+      E_syl, W, Y_stage, mu_stage, trace, total;
   size_t vec_doubles, partial_doubles;
 };
 
@@ -118,6 +119,7 @@ Layout layout_of(const kcg_desc* d) {
   L.E_kron = take(P * n * k * 8);
   L.E_syl = take(P * n * k * 8);
   L.W = take(P * k * k * 8);
+  L.trace = KCG_TRACE ? take((size_t)KCG_TRACE_ITERS * KCG_TRACE_COLS * 8) : 0;
   if (d->host_staging) {
     L.Y_stage = take(P * n * N * 8);
     L.mu_stage = take(P * k * N * 8);
@@ -298,6 +300,7 @@ kcg_status solve_impl(kcg_ctx* c, Route route, const double* Y_in, double* mu_ou
   a.tiles_per_sys = a.tiles_x * a.tiles_y;
   a.max_iter = max_iter;
   a.tol2 = tol * tol;
+  a.trace = c->trace;
   const int Kk = kron ? k : 1;
   CgMaps& maps = kron ? c->maps_kron : c->maps_syl;
   a.x_tma = 0;
@@ -435,6 +438,7 @@ kcg_status kron_cg_create(const kcg_desc* d, const double* A_host, const double*
   c->E_kron = reinterpret_cast<double*>(c->ws + L.E_kron);
   c->E_syl = reinterpret_cast<double*>(c->ws + L.E_syl);
   c->W_dev = reinterpret_cast<double*>(c->ws + L.W);
+  if (KCG_TRACE) c->trace = reinterpret_cast<long long*>(c->ws + L.trace);
   if (d->host_staging) {
     c->Y_stage = reinterpret_cast<double*>(c->ws + L.Y_stage);
     c->mu_stage = reinterpret_cast<double*>(c->ws + L.mu_stage);
@@ -585,6 +589,14 @@ const char* kcg_status_string(int s) {
     case KCG_E_STATE: return "KCG_E_STATE";
     default: return "KCG_UNKNOWN";
   }
+}
+
+// Diagnostic (not part of the ABI header): copy the phase trace of the last solve (KCG_TRACE builds).
+KCG_API int kcg_debug_trace(kcg_ctx* c, long long* out, int max_iters) {
+  if (!c || !c->trace || !out) return 0;
+  const int n = std::min(max_iters, KCG_TRACE_ITERS);
+  cudaMemcpy(out, c->trace, (size_t)n * KCG_TRACE_COLS * 8, cudaMemcpyDeviceToHost);
+  return KCG_TRACE_COLS;
 }
 
 void kron_cg_destroy(kcg_ctx* c) {

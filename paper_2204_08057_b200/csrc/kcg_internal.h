@@ -13,35 +13,38 @@
 namespace kcg {
 
 // Compile-time tile height of the persistent kernel for K component planes per system.
-#ifndef KCG_TY_SMALLK
-#define KCG_TY_SMALLK 16    // tile height for 2 <= K <= 4
+// Tile geometry / threads per CTA of the CTA-tile CG kernel, per K (component planes per system).
+// Each stage holds the r and p boxes (tile + 2-pixel halo) and, with x-TMA, the tile's x block.
+#ifndef KCG_TY1
+#define KCG_TY1 32          // tile rows, K = 1 (Sylvester columns)
 #endif
-#ifndef KCG_NT_SMALLK
-#define KCG_NT_SMALLK 512   // threads per CTA for K <= 4
+#ifndef KCG_TY4
+#define KCG_TY4 16          // tile rows, K = 4
 #endif
+#ifndef KCG_NT4
+#define KCG_NT4 512         // threads, K = 4 (warps must divide the tile rows)
+#endif
+#ifndef KCG_XTMA_MAXK
+#define KCG_XTMA_MAXK 3     // x block TMA-staged with the boxes for K <= this (K=4: measured slower)
+#endif
+#ifndef KCG_TRACE
+#define KCG_TRACE 0         // 1: record per-iteration phase timestamps (diagnostic builds only)
+#endif
+#define KCG_TRACE_ITERS 1024
+#define KCG_TRACE_COLS 160  // [it][0..2] = CTA 0 start / after grid.sync / after reduction, [it][3+b] = CTA b tiles done
 #ifndef KCG_M_IN_REGS
 #define KCG_M_IN_REGS 0     // keep the K x K mixing block in registers (else read from shared)
 #endif
-__host__ __device__ constexpr int cg_tile_y(int K) { return K == 1 ? 32 : (K <= 4 ? KCG_TY_SMALLK : 8); }
-#ifndef KCG_STAGES_SMALLK
-#define KCG_STAGES_SMALLK 2 // TMA pipeline stages per CTA for K <= 4
-#endif
-#ifndef KCG_MINB_SMALLK
-#define KCG_MINB_SMALLK 1   // __launch_bounds__ min blocks per SM for K <= 4
-#endif
-// Threads per CTA of the persistent kernel (warps divide the tile rows).
-__host__ __device__ constexpr int cg_threads(int K) { return K == 1 ? 256 : (K >= 5 ? 256 : KCG_NT_SMALLK); }
-__host__ __device__ constexpr int cg_stages(int K) { return K == 8 ? 1 : (K >= 5 ? 2 : KCG_STAGES_SMALLK); }
-__host__ __device__ constexpr int cg_min_blocks(int K) { return K == 1 ? 2 : (K >= 5 ? 1 : KCG_MINB_SMALLK); }
-// Bytes of the x tile staging buffer (K planes of TY x TX, no halo).
-#ifndef KCG_XTMA_MAXK
-#define KCG_XTMA_MAXK 1     // x block TMA-staged for K <= this (measured: +14 points at K=1, -3 at K=4)
-#endif
-__host__ __device__ constexpr bool cg_xtma(int K) { return K <= KCG_XTMA_MAXK; }
+__host__ __device__ constexpr int cg_tile_y(int K) { return K == 1 ? KCG_TY1 : (K <= 3 ? 16 : (K == 4 ? KCG_TY4 : 8)); }
+__host__ __device__ constexpr int cg_threads(int K) { return K == 1 ? 256 : (K <= 3 ? 512 : (K == 4 ? KCG_NT4 : 256)); }
+__host__ __device__ constexpr int cg_stages(int K) { return 2; }
+__host__ __device__ constexpr int cg_min_blocks(int K) { return K == 1 ? 2 : 1; }
+__host__ __device__ constexpr bool cg_xtma(int K) { return K <= KCG_XTMA_MAXK && K <= 6; }  // K>=7: smem
+// Bytes of the x block staged with a tile.
 __host__ __device__ constexpr int cg_xstage_bytes(int K) { return cg_xtma(K) ? K * cg_tile_y(K) * KCG_TX * 8 : 0; }
-// Bytes of one pipeline stage (r and p boxes with halo, K planes).
+// Bytes of one pipeline stage (r and p boxes with halo, K planes, + x block).
 __host__ __device__ constexpr int cg_stage_bytes(int K) {
-  return 2 * K * (cg_tile_y(K) + 2 * KCG_HALO) * (KCG_TX + 2 * KCG_HALO) * 8;
+  return 2 * K * (cg_tile_y(K) + 2 * KCG_HALO) * (KCG_TX + 2 * KCG_HALO) * 8 + cg_xstage_bytes(K);
 }
 
 // Warp-marching CG kernel geometry: 60 x 16 output tiles, 64-wide boxes (2-pixel halo) streamed as
@@ -97,6 +100,7 @@ struct CgArgs {
   int n_sys, tiles_x, tiles_y, tiles_per_sys;
   int max_iter;
   int x_tma;                 // 1: CgMaps::x describes `x` (TMA needs side >= 2)
+  long long* trace;          // KCG_TRACE builds only: per-iteration %globaltimer stamps
   double tol2;
 };
 

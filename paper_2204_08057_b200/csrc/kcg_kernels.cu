@@ -68,6 +68,11 @@ __device__ __forceinline__ void fence_proxy_async_smem() {
 __device__ __forceinline__ void fence_proxy_async_global() {
   asm volatile("fence.proxy.async.global;" ::: "memory");
 }
+__device__ __forceinline__ long long globaltimer() {
+  long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
@@ -109,6 +114,95 @@ __global__ void __launch_bounds__(256) rhs_kernel(const double* __restrict__ Y, 
   }
 }
 
+// --------------------------------------------------------------------------- CG scalar update
+// One CG scalar step for a system from its reduced partials (r,r) and (w,r) (Chronopoulos-Gear):
+// the start pass (it < 0) gives ||b||^2 and alpha_0 = (b,b)/(Gb,b); afterwards
+// beta = gamma'/gamma, alpha = gamma'/(delta - beta gamma'/alpha); stop on ||r|| <= tol ||b||.
+__device__ __forceinline__ SysState cg_update(SysState z, double rr, double wr, int it, const CgArgs& a) {
+  if (it < 0) {
+    z.bnorm2 = rr;
+    z.gamma = rr;
+    z.rel = rr > 0.0 ? 1.0 : 0.0;
+    if (!isfinite(rr) || !isfinite(wr)) z.status = ST_NONFINITE;
+    else if (rr == 0.0) z.status = ST_CONVERGED;
+    else if (!(wr > 0.0)) z.status = ST_BREAKDOWN;
+    else if (a.max_iter <= 0) z.status = ST_MAXIT;
+    else { z.alpha = rr / wr; z.beta = 0.0; }
+  } else {
+    z.iters = it + 1;
+    z.rel = sqrt(rr / z.bnorm2);
+    if (!isfinite(rr) || !isfinite(wr)) z.status = ST_NONFINITE;
+    else if (rr <= a.tol2 * z.bnorm2) z.status = ST_CONVERGED;
+    else if (z.iters >= a.max_iter) z.status = ST_MAXIT;
+    else {
+      const double beta = rr / z.gamma;
+      const double den = wr - beta * rr / z.alpha;
+      if (!(den > 0.0)) z.status = ST_BREAKDOWN;
+      else { z.beta = beta; z.alpha = rr / den; z.gamma = rr; }
+    }
+  }
+  z.parity ^= 1;
+  return z;
+}
+
+// After the iteration's grid barrier: CTA b reduces the tile partials of active systems b, b+grid,...
+// with all its threads (one round of independent loads; thread t sums tiles t, t+NT, ... in order,
+// then a fixed warp/CTA tree -> deterministic, independent of grid size and batch composition),
+// publishes the new state in a.state_out; a second grid barrier; every CTA pulls the states.
+template <int NT>
+__device__ __forceinline__ void reduce_update_systems(const CgArgs& a, SysState* st, const int* act, int nact,
+                                                      int par_out, int it, double (*red)[32]) {
+  constexpr int NW = NT / 32, U = 4;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int tps = a.tiles_per_sys;
+  for (int ii = blockIdx.x; ii < nact; ii += gridDim.x) {
+    const int s = act[ii];
+    const double2* base = reinterpret_cast<const double2*>(a.partials + ((size_t)par_out * a.n_sys + s) * tps * 2);
+    double rr = 0.0, wr = 0.0;
+    for (int t0 = tid; t0 < tps; t0 += U * NT) {
+      double2 v[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int tl = t0 + u * NT;
+        v[u] = tl < tps ? __ldcg(base + tl) : make_double2(0.0, 0.0);
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        rr += v[u].x;
+        wr += v[u].y;
+      }
+    }
+    rr = warp_sum(rr);
+    wr = warp_sum(wr);
+    if (lane == 0) { red[0][warp] = rr; red[1][warp] = wr; }
+    __syncthreads();
+    if (tid == 0) {
+      double r2 = 0.0, w2 = 0.0;
+      for (int w = 0; w < NW; ++w) { r2 += red[0][w]; w2 += red[1][w]; }
+      a.state_out[s] = cg_update(st[s], r2, w2, it, a);
+    }
+    __syncthreads();
+  }
+  __threadfence();
+  cg::this_grid().sync();
+  for (int ii = tid; ii < nact; ii += NT) {
+    const int s = act[ii];
+    const SysState* g = a.state_out + s;
+    SysState z;
+    z.bnorm2 = __ldcg(&g->bnorm2);
+    z.gamma = __ldcg(&g->gamma);
+    z.alpha = __ldcg(&g->alpha);
+    z.beta = __ldcg(&g->beta);
+    z.rel = __ldcg(&g->rel);
+    z.iters = __ldcg(&g->iters);
+    z.status = __ldcg(&g->status);
+    z.parity = __ldcg(&g->parity);
+    z.pad = 0;
+    st[s] = z;
+  }
+  __syncthreads();
+}
+
 // --------------------------------------------------------------------------- persistent CG
 // One tile of one system: box = tile + 2-pixel halo, K planes of r and p staged by TMA (zero fill
 // outside the face).  Warp w owns T rows w, w+NW, ...; lane l owns the pixel PAIR at tile columns
@@ -123,16 +217,13 @@ __global__ void __launch_bounds__(256) rhs_kernel(const double* __restrict__ Y, 
 struct TileCtx {
   double* R;          // r box (stage)
   double* Pp;         // p box (stage)
-  double* xs;         // x tile staging [K][TY][TX] (XTMA)
-  const CUtensorMap* xmap;
+  double* xs;         // x block of the tile in the stage [K][TY][TX] (XTMA)
   const double* Ms;   // M (K*K) then tau (K) of this tile's system, shared
   int s, y0, x0, par;
   double alpha, beta, kappa2;
   const double* hp;   // hits plane or nullptr
   uint64_t* bar;      // stage mbarrier
   uint32_t phase;
-  uint64_t* xbar;     // x staging mbarrier
-  uint32_t xphase;
   double* part_out;
 };
 
@@ -152,12 +243,6 @@ __device__ __forceinline__ void cg_tile(const CgArgs& a, const TileCtx& tc, doub
   const int s = tc.s, y0 = tc.y0, x0 = tc.x0;
   const double alpha = tc.alpha, beta = tc.beta, kappa2 = tc.kappa2;
   const int gx = x0 + 2 * lane;
-
-  if (XTMA && tid == 0) {  // x block of this tile -> xs (completes on xbar)
-    fence_proxy_async_smem();
-    mbar_arrive_expect_tx(tc.xbar, K * TY * TX * 8);
-    tma_load_3d(tc.xs, tc.xmap, tc.xbar, x0, y0, s * K);
-  }
 
   mbar_wait(tc.bar, tc.phase);
 
@@ -268,7 +353,6 @@ __device__ __forceinline__ void cg_tile(const CgArgs& a, const TileCtx& tc, doub
     }
   }
   __syncthreads();
-  if (XTMA) mbar_wait(tc.xbar, tc.xphase);
 
   // Phase C
   double rr = 0.0, wr = 0.0;
@@ -377,16 +461,15 @@ __global__ void __launch_bounds__(cg_threads(K), cg_min_blocks(K)) cg_persistent
   constexpr int TY = cg_tile_y(K), TX = KCG_TX, H = KCG_HALO;
   constexpr int BW = TX + 2 * H, BH = TY + 2 * H;
   constexpr int FIELD = K * BW * BH;  // doubles of one field box
-  constexpr int STAGE_BYTES = 2 * FIELD * 8;
+  constexpr int XBYTES = cg_xstage_bytes(K);  // x block, TMA-staged with the boxes (0 if disabled)
+  constexpr int STAGE_BYTES = 2 * FIELD * 8 + XBYTES;
   constexpr int NT = cg_threads(K), NW = NT / 32, NS = cg_stages(K);
   static_assert(STAGE_BYTES == cg_stage_bytes(K), "stage size");
 
   extern __shared__ __align__(128) unsigned char smem_raw[];
-  double* xs = reinterpret_cast<double*>(smem_raw + NS * STAGE_BYTES);
-  SysState* st = reinterpret_cast<SysState*>(smem_raw + NS * STAGE_BYTES + cg_xstage_bytes(K));
+  SysState* st = reinterpret_cast<SysState*>(smem_raw + NS * STAGE_BYTES);
   int* act = reinterpret_cast<int*>(st + a.n_sys);
   __shared__ __align__(8) uint64_t mbar[2];
-  __shared__ __align__(8) uint64_t xbar;
   __shared__ double red[2][32];
   __shared__ double Ms[KCG_KMAX * KCG_KMAX + KCG_KMAX];
   __shared__ int s_nact;
@@ -405,12 +488,11 @@ __global__ void __launch_bounds__(cg_threads(K), cg_min_blocks(K)) cg_persistent
   if (tid == 0) {
     mbar_init(&mbar[0], 1);
     mbar_init(&mbar[1], 1);
-    mbar_init(&xbar, 1);
     fence_mbar_init();
   }
   __syncthreads();
 
-  uint32_t phase0 = 0, phase1 = 0, xphase = 0;
+  uint32_t phase0 = 0, phase1 = 0;
   int it = -1;  // -1 = start pass (alpha = beta = 0): r, p <- b and (b, b), (G b, b)
 
   // TMA of tile t (index into the active-tile list) into stage sidx; parity flip for speculation
@@ -420,7 +502,8 @@ __global__ void __launch_bounds__(cg_threads(K), cg_min_blocks(K)) cg_persistent
     const int ty = tile / a.tiles_x, tx = tile - ty * a.tiles_x;
     const int par = st[s].parity ^ flip;
     double* dst = reinterpret_cast<double*>(smem_raw + sidx * STAGE_BYTES);
-    mbar_arrive_expect_tx(&mbar[sidx], STAGE_BYTES);
+    mbar_arrive_expect_tx(&mbar[sidx], xtma ? STAGE_BYTES : 2 * FIELD * 8);
+    if (xtma) tma_load_3d(dst + 2 * FIELD, &maps.x, &mbar[sidx], tx * TX, ty * TY, s * K);
     tma_load_3d(dst, &maps.r[par], &mbar[sidx], tx * TX - H, ty * TY - H, s * K);
     tma_load_3d(dst + FIELD, &maps.p[par], &mbar[sidx], tx * TX - H, ty * TY - H, s * K);
   };
@@ -444,6 +527,8 @@ __global__ void __launch_bounds__(cg_threads(K), cg_min_blocks(K)) cg_persistent
     if (nact == 0) break;
     const int ntiles = nact * tps;
     const int par_out = (it + 1) & 1;
+    const bool tr = KCG_TRACE && a.trace && it + 1 < KCG_TRACE_ITERS;
+    if (tr && blockIdx.x == 0 && tid == 0) a.trace[(size_t)(it + 1) * KCG_TRACE_COLS + 0] = globaltimer();
 
     if (!spec && (int)blockIdx.x < ntiles && tid == 0) issue(blockIdx.x, 0, 0);
     spec = false;
@@ -470,8 +555,7 @@ __global__ void __launch_bounds__(cg_threads(K), cg_min_blocks(K)) cg_persistent
       TileCtx tc;
       tc.R = reinterpret_cast<double*>(smem_raw + sidx * STAGE_BYTES);
       tc.Pp = tc.R + FIELD;
-      tc.xs = xs;
-      tc.xmap = &maps.x;
+      tc.xs = tc.R + 2 * FIELD;
       tc.Ms = Ms;
       tc.s = s;
       tc.y0 = ty * TY;
@@ -483,14 +567,11 @@ __global__ void __launch_bounds__(cg_threads(K), cg_min_blocks(K)) cg_persistent
       tc.hp = HITS ? a.hits + (size_t)__ldg(&sp->hits_plane) * ((size_t)a.side * a.side) : nullptr;
       tc.bar = &mbar[sidx];
       tc.phase = sidx ? phase1 : phase0;
-      tc.xbar = &xbar;
-      tc.xphase = xphase;
       tc.part_out = a.partials + (((size_t)par_out * a.n_sys + s) * tps + tile) * 2;
       const bool interior = tc.x0 >= H && tc.x0 + TX + H <= a.side && tc.y0 >= H && tc.y0 + TY + H <= a.side;
       if (cg_xtma(K) && xtma) {
         if (interior) cg_tile<K, false, HITS, cg_xtma(K)>(a, tc, red);
         else cg_tile<K, true, HITS, cg_xtma(K)>(a, tc, red);
-        xphase ^= 1u;
       } else {
         if (interior) cg_tile<K, false, HITS, false>(a, tc, red);
         else cg_tile<K, true, HITS, false>(a, tc, red);
@@ -498,63 +579,20 @@ __global__ void __launch_bounds__(cg_threads(K), cg_min_blocks(K)) cg_persistent
       if (sidx) phase1 ^= 1u; else phase0 ^= 1u;
     }
 
+    if (tr && tid == 0 && blockIdx.x < KCG_TRACE_COLS - 3)
+      a.trace[(size_t)(it + 1) * KCG_TRACE_COLS + 3 + blockIdx.x] = globaltimer();
     fence_proxy_async_global();
     grid.sync();
     fence_proxy_async_global();
+    if (tr && blockIdx.x == 0 && tid == 0) a.trace[(size_t)(it + 1) * KCG_TRACE_COLS + 1] = globaltimer();
     // speculative first load of the next iteration (same active set, flipped parity) overlaps the
     // reduction below; verified against the new active count at the top of the loop
     if (it >= 0 && (int)blockIdx.x < ntiles && tid == 0) issue(blockIdx.x, 0, 1);
     spec = it >= 0 && (int)blockIdx.x < ntiles;
     nact_prev = nact;
 
-    // Per-system reduction of the tile partials (fixed order -> deterministic, independent of the
-    // grid size and of which other systems are in the batch), then the CG scalar recurrences.
-    for (int ii = warp; ii < nact; ii += NW) {
-      const int s = act[ii];
-      const double* base = a.partials + ((size_t)par_out * a.n_sys + s) * tps * 2;
-      double rr0 = 0.0, wr0 = 0.0, rr1 = 0.0, wr1 = 0.0;
-      int tl = lane;
-      for (; tl + 32 < tps; tl += 64) {
-        const double2 u = __ldcg(reinterpret_cast<const double2*>(base) + tl);
-        const double2 v = __ldcg(reinterpret_cast<const double2*>(base) + tl + 32);
-        rr0 += u.x; wr0 += u.y;
-        rr1 += v.x; wr1 += v.y;
-      }
-      if (tl < tps) {
-        const double2 u = __ldcg(reinterpret_cast<const double2*>(base) + tl);
-        rr0 += u.x; wr0 += u.y;
-      }
-      double rr = warp_sum(rr0 + rr1);
-      double wr = warp_sum(wr0 + wr1);
-      if (lane == 0) {
-        SysState z = st[s];
-        if (it < 0) {
-          z.bnorm2 = rr;
-          z.gamma = rr;
-          z.rel = rr > 0.0 ? 1.0 : 0.0;
-          if (!isfinite(rr) || !isfinite(wr)) z.status = ST_NONFINITE;
-          else if (rr == 0.0) z.status = ST_CONVERGED;
-          else if (!(wr > 0.0)) z.status = ST_BREAKDOWN;
-          else if (a.max_iter <= 0) z.status = ST_MAXIT;
-          else { z.alpha = rr / wr; z.beta = 0.0; }
-        } else {
-          z.iters = it + 1;
-          z.rel = sqrt(rr / z.bnorm2);
-          if (!isfinite(rr) || !isfinite(wr)) z.status = ST_NONFINITE;
-          else if (rr <= a.tol2 * z.bnorm2) z.status = ST_CONVERGED;
-          else if (z.iters >= a.max_iter) z.status = ST_MAXIT;
-          else {
-            const double beta = rr / z.gamma;
-            const double den = wr - beta * rr / z.alpha;
-            if (!(den > 0.0)) z.status = ST_BREAKDOWN;
-            else { z.beta = beta; z.alpha = rr / den; z.gamma = rr; }
-          }
-        }
-        z.parity ^= 1;
-        st[s] = z;
-      }
-    }
-    __syncthreads();
+    reduce_update_systems<NT>(a, st, act, nact, par_out, it, red);
+    if (tr && blockIdx.x == 0 && tid == 0) a.trace[(size_t)(it + 1) * KCG_TRACE_COLS + 2] = globaltimer();
     if (blockIdx.x == 0 && tid == 0 && it >= 0 && it < a.history_cap) {
       double m = 0.0;
       for (int ii = 0; ii < nact; ++ii) m = fmax(m, st[act[ii]].rel);
@@ -829,6 +867,7 @@ __global__ void __launch_bounds__(32 * march_warps(K), 1) cg_march_kernel(const 
   int* act = reinterpret_cast<int*>(st + a.n_sys);
   __shared__ __align__(8) uint64_t mbar[W * NB];
   __shared__ double Msh[W][KCG_KMAX * KCG_KMAX + KCG_KMAX];
+  __shared__ double red[2][32];
   __shared__ int s_nact;
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -896,52 +935,7 @@ __global__ void __launch_bounds__(32 * march_warps(K), 1) cg_march_kernel(const 
     grid.sync();
     fence_proxy_async_global();
 
-    for (int ii = warp; ii < nact; ii += W) {
-      const int s = act[ii];
-      const double* base = a.partials + ((size_t)par_out * a.n_sys + s) * tps * 2;
-      double rr0 = 0.0, wr0 = 0.0, rr1 = 0.0, wr1 = 0.0;
-      int tl = lane;
-      for (; tl + 32 < tps; tl += 64) {
-        const double2 u = __ldcg(reinterpret_cast<const double2*>(base) + tl);
-        const double2 v = __ldcg(reinterpret_cast<const double2*>(base) + tl + 32);
-        rr0 += u.x; wr0 += u.y;
-        rr1 += v.x; wr1 += v.y;
-      }
-      if (tl < tps) {
-        const double2 u = __ldcg(reinterpret_cast<const double2*>(base) + tl);
-        rr0 += u.x; wr0 += u.y;
-      }
-      double rr = warp_sum(rr0 + rr1);
-      double wr = warp_sum(wr0 + wr1);
-      if (lane == 0) {
-        SysState z = st[s];
-        if (it < 0) {
-          z.bnorm2 = rr;
-          z.gamma = rr;
-          z.rel = rr > 0.0 ? 1.0 : 0.0;
-          if (!isfinite(rr) || !isfinite(wr)) z.status = ST_NONFINITE;
-          else if (rr == 0.0) z.status = ST_CONVERGED;
-          else if (!(wr > 0.0)) z.status = ST_BREAKDOWN;
-          else if (a.max_iter <= 0) z.status = ST_MAXIT;
-          else { z.alpha = rr / wr; z.beta = 0.0; }
-        } else {
-          z.iters = it + 1;
-          z.rel = sqrt(rr / z.bnorm2);
-          if (!isfinite(rr) || !isfinite(wr)) z.status = ST_NONFINITE;
-          else if (rr <= a.tol2 * z.bnorm2) z.status = ST_CONVERGED;
-          else if (z.iters >= a.max_iter) z.status = ST_MAXIT;
-          else {
-            const double beta = rr / z.gamma;
-            const double den = wr - beta * rr / z.alpha;
-            if (!(den > 0.0)) z.status = ST_BREAKDOWN;
-            else { z.beta = beta; z.alpha = rr / den; z.gamma = rr; }
-          }
-        }
-        z.parity ^= 1;
-        st[s] = z;
-      }
-    }
-    __syncthreads();
+    reduce_update_systems<32 * W>(a, st, act, nact, par_out, it, red);
     if (blockIdx.x == 0 && tid == 0 && it >= 0 && it < a.history_cap) {
       double m = 0.0;
       for (int ii = 0; ii < nact; ++ii) m = fmax(m, st[act[ii]].rel);
@@ -1130,7 +1124,7 @@ cudaError_t launch_rhs(int K, cudaStream_t s, const double* Y, const double* E, 
 
 template <int K, bool HITS>
 static cudaError_t cg_config_t(int n_sys, int* max_grid, size_t* smem) {
-  const size_t sm = cg_stages(K) * (size_t)cg_stage_bytes(K) + cg_xstage_bytes(K) +
+  const size_t sm = cg_stages(K) * (size_t)cg_stage_bytes(K) +
                     (size_t)n_sys * (sizeof(SysState) + sizeof(int));
   cudaError_t e = cudaFuncSetAttribute(cg_persistent_kernel<K, HITS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
   if (e != cudaSuccess) return e;
