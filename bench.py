@@ -293,7 +293,8 @@ def run_b200(args):
     def agg(reps_, t):
         # whole-job numbers: gather per-rank sums
         loc = torch.tensor([sum(r["loop_bytes"] for r in reps_), sum(r["loop_time_s"] for r in reps_),
-                            sum(r["system_iterations"] for r in reps_), len(reps_)],
+                            sum(r["system_iterations"] for r in reps_), len(reps_),
+                            sum(r["system_iterations"] + r["n_systems"] for r in reps_)],
                            dtype=torch.float64, device=dev)
         if world > 1:
             allv = [torch.zeros_like(loc) for _ in range(world)]
@@ -314,14 +315,22 @@ def run_b200(args):
     K = args.steps
 
     def roofline(g, route):
-        # dominant kernel = cg_persistent_kernel; rank 0's launches (CUDA events around it)
+        # dominant kernel = cg_persistent_kernel; rank 0's launches (CUDA events around it).
+        # achieved = the bytes this implementation's pass structure must move (report.loop_bytes:
+        # r, p read + written every pass, x read + written every other pass = 40 K N B per
+        # iteration on average) / kernel time.  model_48kN = SURVEY 8(d)'s B_min = 48 K N B per
+        # pass (x every pass) over the same time: the iteration rate as a fraction of that roofline.
         bytes_, tsec = g[0][0], g[0][1]
         ach = bytes_ / tsec / 1e9 if tsec > 0 else 0.0
+        kk = problems[0].k if route == "kron" else 1
+        b48 = 48.0 * kk * problems[0].side ** 2 * g[0][4]
         return {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,
                 "traffic": _traffic(args.config, route), "kernel": "cg_persistent_kernel",
                 "peak_source": peak_src,
                 "algorithmic_bytes_per_launch": bytes_ / max(g[0][3], 1),
-                "avg_launch_ms": tsec / max(g[0][3], 1) * 1e3}
+                "avg_launch_ms": tsec / max(g[0][3], 1) * 1e3,
+                "model_48kN": {"bytes_per_launch": b48 / max(g[0][3], 1),
+                               "frac": (b48 / tsec / 1e9) / peak if tsec > 0 else 0.0}}
 
     sys_its_main = sum(v[2] for v in g_main) / K
     line = {
@@ -344,7 +353,8 @@ def run_b200(args):
                 "h2d_bytes_per_step": int(st["Y"].nbytes) * (world if world > 1 else 1),
                 "d2h_bytes_per_step": int(mu_host.numel() * 8) * (world if world > 1 else 1),
                 "api": "kron_cg_solve_host (C ABI, pinned host buffers)"},
-        "gpu_launches": K * (5 if args.route == "sylvester" else 4),
+        # per solve: rhs, CG, x fix-up, residual apply + reduce (+ back-transform, Sylvester)
+        "gpu_launches": K * (6 if args.route == "sylvester" else 5),
         "clocks": clocks,
         "sylvester" if args.route == "kron" else "kron": {
             "value": K / t_other, "ms_per_step": t_other / K * 1e3,

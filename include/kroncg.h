@@ -100,7 +100,10 @@ typedef struct {
   double wall_time_s;      /* device time of the whole solve (CUDA events, launching stream)  */
   double loop_time_s;      /* device time of the persistent CG kernel alone                  */
   long long system_iterations; /* sum over systems of iterations (+1 start pass each)        */
-  double loop_bytes;       /* algorithmic HBM bytes of the CG kernel: 48*K*N per system-pass  */
+  double loop_bytes;       /* algorithmic HBM bytes of the CG kernel: per system-pass read +   */
+                           /* write of r and p (32*K*N), plus x read + write (16*K*N) on the   */
+                           /* passes that update x (every other pass: x += a_{q-1} p_{q-1} +   */
+                           /* a_q p_q; a pending half-step is added after the loop)          */
   size_t peak_mem_bytes;   /* workspace bytes                                                */
   double* history;         /* optional caller array [history_cap] (NULL = skip)               */
   int history_len;

@@ -41,6 +41,7 @@ struct kcg_ctx {
   double* E_syl = nullptr;
   double* W_dev = nullptr;
   long long* trace = nullptr;
+  unsigned* sync = nullptr;
   double* Y_stage = nullptr;
   double* mu_stage = nullptr;
   const double* hits = nullptr;
@@ -62,7 +63,7 @@ size_t align_up(size_t x) { return (x + kAlign - 1) / kAlign * kAlign; }
 
 struct Layout {
   size_t r0, r1, p0, p1, partials, state, history, resid_partials, resid_out, params_kron, params_syl, E_kron,
-      E_syl, W, Y_stage, mu_stage, trace, total;
+      E_syl, W, Y_stage, mu_stage, trace, sync, total;
   size_t vec_doubles, partial_doubles;
 };
 
@@ -85,13 +86,9 @@ bool config_ok(const kcg_desc* d, std::string* why) {
   return true;
 }
 
-// Tile grid of the CG kernel in use (warp-marching: 60 x 16; CTA-tile: 64 x cg_tile_y(K)).
-int tiles_x(int side, int K) {
-  return kcg::use_march(K) ? (side + MARCH_TX - 1) / MARCH_TX : (side + KCG_TX - 1) / KCG_TX;
-}
-int tiles_y(int side, int K) {
-  return kcg::use_march(K) ? (side + MARCH_TY - 1) / MARCH_TY : (side + kcg::cg_tile_y(K) - 1) / kcg::cg_tile_y(K);
-}
+// Tile grid of the CG kernel (64 x cg_tile_y(K) tiles).
+int tiles_x(int side, int K) { return (side + KCG_TX - 1) / KCG_TX; }
+int tiles_y(int side, int K) { return (side + kcg::cg_tile_y(K) - 1) / kcg::cg_tile_y(K); }
 
 Layout layout_of(const kcg_desc* d) {
   Layout L{};
@@ -112,6 +109,7 @@ Layout layout_of(const kcg_desc* d) {
   L.partials = take(L.partial_doubles * 8);
   L.state = take(P * k * sizeof(SysState));
   L.history = take((size_t)std::max(d->history_cap, 1) * 8);
+  L.sync = take(4 * sizeof(unsigned));
   L.resid_partials = take(P * (size_t)kcg::apply_tiles_per_sys(side) * 2 * 8);
   L.resid_out = take(P * 2 * 8);
   L.params_kron = take(P * sizeof(SysParams));
@@ -204,8 +202,8 @@ PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
 }
 
 bool encode_map(CUtensorMap* m, double* base, int side, int pitch, size_t planes, int K, std::string* why) {
-  const int bx = kcg::use_march(K) ? 64 : KCG_TX + 2 * KCG_HALO;
-  const int by = kcg::use_march(K) ? kcg::march_cr(K) : kcg::cg_tile_y(K) + 2 * KCG_HALO;
+  const int bx = KCG_TX + 2 * KCG_HALO;
+  const int by = kcg::cg_tile_y(K) + 2 * KCG_HALO;
   auto enc = get_encode();
   if (!enc) { *why = "cuTensorMapEncodeTiled unavailable"; return false; }
   cuuint64_t dims[3] = {(cuuint64_t)side, (cuuint64_t)side, (cuuint64_t)planes};
@@ -301,19 +299,20 @@ kcg_status solve_impl(kcg_ctx* c, Route route, const double* Y_in, double* mu_ou
   a.max_iter = max_iter;
   a.tol2 = tol * tol;
   a.trace = c->trace;
+  a.sync = c->sync;
+  CK(cudaMemsetAsync(c->sync, 0, 4 * sizeof(unsigned), s), "memset sync");
   const int Kk = kron ? k : 1;
   CgMaps& maps = kron ? c->maps_kron : c->maps_syl;
   a.x_tma = 0;
-  if (!kcg::use_march(Kk) && kcg::cg_xtma(Kk) && side >= 2 && (reinterpret_cast<uintptr_t>(mu) % 16) == 0) {
+  if (side >= 2 && (reinterpret_cast<uintptr_t>(mu) % 16) == 0) {
     std::string why;
     if (!encode_xmap(&maps.x, mu, side, (size_t)P * k, Kk, &why)) { c->err = why; return KCG_E_CUDA; }
     a.x_tma = 1;
   }
-  CK((kcg::use_march(kron ? k : 1) ? kcg::launch_march : kcg::launch_cg)(kron ? k : 1, s, a, maps,
-                                                       kron ? c->grid_kron : c->grid_syl,
-                                                       kron ? c->smem_kron : c->smem_syl),
+  CK(kcg::launch_cg(Kk, s, a, maps, kron ? c->grid_kron : c->grid_syl, kron ? c->smem_kron : c->smem_syl),
      "cg kernel");
   CK(cudaEventRecord(c->ev[2], s), "event");
+  if (KCG_X2) CK(kcg::launch_xfix(Kk, s, c->state, c->p[0], c->p[1], mu, a.n_sys, side, c->pitch), "x fix-up kernel");
   if (!kron) CK(kcg::launch_backtransform(k, s, c->W_dev, mu, P, side), "backtransform kernel");
   CK(kcg::launch_resid(k, s, c->params_kron, mu, Y, c->E_kron, c->hits, c->resid_partials, c->resid_out, P, n, side),
      "residual kernel");
@@ -327,13 +326,14 @@ kcg_status solve_impl(kcg_ctx* c, Route route, const double* Y_in, double* mu_ou
 
   // report
   int worst = KCG_OK, maxit = 0, allconv = 1;
-  long long sumit = 0, passes = 0;
+  long long sumit = 0, passes = 0, xpasses = 0;
   double maxrel = 0.0;
   for (int i = 0; i < a.n_sys; ++i) {
     const SysState& z = c->st_host[i];
     maxit = std::max(maxit, z.iters);
     sumit += z.iters;
     passes += z.iters + 1;
+    xpasses += KCG_X2 ? z.iters / 2 : z.iters;
     maxrel = std::max(maxrel, z.rel);
     if (z.status != kcg::ST_CONVERGED) allconv = 0;
     int code = KCG_OK;
@@ -363,7 +363,8 @@ kcg_status solve_impl(kcg_ctx* c, Route route, const double* Y_in, double* mu_ou
     rep->wall_time_s = t03 * 1e-3;
     rep->loop_time_s = t12 * 1e-3;
     rep->system_iterations = sumit;
-    rep->loop_bytes = 48.0 * (kron ? k : 1) * (double)N * (double)passes;
+    // per pass: read + write r and p (32 B per pixel and plane); x passes also read + write x
+    rep->loop_bytes = (32.0 * (double)passes + 16.0 * (double)xpasses) * (kron ? k : 1) * (double)N;
     rep->peak_mem_bytes = c->ws_need;
     rep->history_len = std::min(maxit, c->d.history_cap);
     if (rep->history && rep->history_len > 0) {
@@ -439,6 +440,7 @@ kcg_status kron_cg_create(const kcg_desc* d, const double* A_host, const double*
   c->E_syl = reinterpret_cast<double*>(c->ws + L.E_syl);
   c->W_dev = reinterpret_cast<double*>(c->ws + L.W);
   if (KCG_TRACE) c->trace = reinterpret_cast<long long*>(c->ws + L.trace);
+  c->sync = reinterpret_cast<unsigned*>(c->ws + L.sync);
   if (d->host_staging) {
     c->Y_stage = reinterpret_cast<double*>(c->ws + L.Y_stage);
     c->mu_stage = reinterpret_cast<double*>(c->ws + L.mu_stage);
@@ -519,12 +521,10 @@ kcg_status kron_cg_create(const kcg_desc* d, const double* A_host, const double*
   c->tiles_x_syl = tiles_x(c->side, 1);
   c->tiles_y_syl = tiles_y(c->side, 1);
   int mg = 0;
-  CKC((kcg::use_march(k) ? kcg::march_kernel_config : kcg::cg_kernel_config)(k, hits_dev != nullptr, P, &mg,
-                                                                               &c->smem_kron),
+  CKC(kcg::cg_kernel_config(k, hits_dev != nullptr, P, &mg, &c->smem_kron),
       "cg kernel config (kron)");
   c->grid_kron = std::max(1, std::min(mg, P * c->tiles_x_kron * c->tiles_y_kron));
-  CKC((kcg::use_march(1) ? kcg::march_kernel_config : kcg::cg_kernel_config)(1, hits_dev != nullptr, P * k, &mg,
-                                                                               &c->smem_syl),
+  CKC(kcg::cg_kernel_config(1, hits_dev != nullptr, P * k, &mg, &c->smem_syl),
       "cg kernel config (sylvester)");
   c->grid_syl = std::max(1, std::min(mg, P * k * c->tiles_x_syl * c->tiles_y_syl));
   for (int i = 0; i < 4; ++i) CKC(cudaEventCreate(&c->ev[i]), "event create");
@@ -589,6 +589,18 @@ const char* kcg_status_string(int s) {
     case KCG_E_STATE: return "KCG_E_STATE";
     default: return "KCG_UNKNOWN";
   }
+}
+
+// Diagnostic (not part of the ABI header): launch configuration of the CG kernel per route:
+// out = {grid_kron, grid_syl, smem_kron, smem_syl, sm_count}.
+KCG_API int kcg_debug_config(const kcg_ctx* c, long long* out) {
+  if (!c || !out) return 0;
+  int dev = 0, nsm = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  out[0] = c->grid_kron; out[1] = c->grid_syl; out[2] = (long long)c->smem_kron; out[3] = (long long)c->smem_syl;
+  out[4] = nsm;
+  return 5;
 }
 
 // Diagnostic (not part of the ABI header): copy the phase trace of the last solve (KCG_TRACE builds).

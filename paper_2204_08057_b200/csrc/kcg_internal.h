@@ -32,13 +32,37 @@ namespace kcg {
 #endif
 #define KCG_TRACE_ITERS 1024
 #define KCG_TRACE_COLS 160  // [it][0..2] = CTA 0 start / after grid.sync / after reduction, [it][3+b] = CTA b tiles done
+#ifndef KCG_SERP
+#define KCG_SERP 1          // serpentine tile order across passes (L2 reuse when the state fits)
+#endif
+#ifndef KCG_ONEBAR
+#define KCG_ONEBAR 0        // single-barrier last-arriver reduction (else 2 grid.sync per pass)
+#endif
+#ifndef KCG_RED_MAX
+#define KCG_RED_MAX 4096    // redundant per-CTA reduction when active systems x tiles <= this
+#endif
+#ifndef KCG_DYN
+#define KCG_DYN 1           // dynamic tile claiming after each CTA's first two tiles
+#endif
+#ifndef KCG_XPF
+#define KCG_XPF 1           // prefetch the next tile's x block into L2 (TMA prefetch) when not staged
+#endif
+#ifndef KCG_X2
+#define KCG_X2 1            // update x every other pass (x += a_{q-1} p_{q-1} + a_q p_q): 40kN B/iter
+#endif
+#ifndef KCG_DEFER
+#define KCG_DEFER 1         // defer the CTA sum of a tile's partials to the next barrier
+#endif
 #ifndef KCG_M_IN_REGS
 #define KCG_M_IN_REGS 0     // keep the K x K mixing block in registers (else read from shared)
 #endif
 __host__ __device__ constexpr int cg_tile_y(int K) { return K == 1 ? KCG_TY1 : (K <= 3 ? 16 : (K == 4 ? KCG_TY4 : 8)); }
 __host__ __device__ constexpr int cg_threads(int K) { return K == 1 ? 256 : (K <= 3 ? 512 : (K == 4 ? KCG_NT4 : 256)); }
 __host__ __device__ constexpr int cg_stages(int K) { return 2; }
-__host__ __device__ constexpr int cg_min_blocks(int K) { return K == 1 ? 2 : 1; }
+#ifndef KCG_MINB4
+#define KCG_MINB4 1         // resident CTAs per SM, K = 4
+#endif
+__host__ __device__ constexpr int cg_min_blocks(int K) { return K == 1 ? 2 : (K == 4 ? KCG_MINB4 : 1); }
 __host__ __device__ constexpr bool cg_xtma(int K) { return K <= KCG_XTMA_MAXK && K <= 6; }  // K>=7: smem
 // Bytes of the x block staged with a tile.
 __host__ __device__ constexpr int cg_xstage_bytes(int K) { return cg_xtma(K) ? K * cg_tile_y(K) * KCG_TX * 8 : 0; }
@@ -46,21 +70,6 @@ __host__ __device__ constexpr int cg_xstage_bytes(int K) { return cg_xtma(K) ? K
 __host__ __device__ constexpr int cg_stage_bytes(int K) {
   return 2 * K * (cg_tile_y(K) + 2 * KCG_HALO) * (KCG_TX + 2 * KCG_HALO) * 8 + cg_xstage_bytes(K);
 }
-
-// Warp-marching CG kernel geometry: 60 x 16 output tiles, 64-wide boxes (2-pixel halo) streamed as
-// TMA chunks of march_cr(K) rows x 64 x K planes (r and p) through a per-warp ring of march_nb(K).
-#define MARCH_TX 60
-#define MARCH_TY 16
-#ifndef KCG_MARCH
-#define KCG_MARCH 0         // 1: warp-marching kernel for K <= 4 (experimental); 0: CTA-tile kernel
-#endif
-__host__ __device__ constexpr int march_cr(int K) { return K == 1 ? 4 : 2; }
-__host__ __device__ constexpr int march_nb(int K) { return 3; }
-__host__ __device__ constexpr int march_chunk_bytes(int K) { return 2 * K * march_cr(K) * 64 * 8; }
-__host__ __device__ constexpr int march_warps(int K) { return K == 1 ? 16 : (K == 2 ? 12 : 8); }
-// The marching kernel keeps 8 K-wide double2 row windows in registers: used for K <= 4; larger K
-// run the CTA-tile kernel.
-__host__ __device__ constexpr bool use_march(int K) { return KCG_MARCH && K <= 4; }
 
 // Per-system constant parameters of the operator  q_c = h sum_d M[c][d] p_d + tau_c (kappa2 p_c + (L p_c)).
 // Kronecker route: one system per patch, K = k, M = A^T T A, tau = prior scales.
@@ -84,6 +93,8 @@ struct SysState {
   int status;
   int parity;      // which ping-pong buffer holds the current r, p
   int pad;
+  double alpha_last;  // alpha used by the last completed pass (X2: its alpha p_new is pending in x
+                      // when `iters` is odd -- added by the next x pass or by the fix-up kernel)
 };
 
 struct CgArgs {
@@ -99,8 +110,9 @@ struct CgArgs {
   int side, pitch;
   int n_sys, tiles_x, tiles_y, tiles_per_sys;
   int max_iter;
-  int x_tma;                 // 1: CgMaps::x describes `x` (TMA needs side >= 2)
+  int x_tma;                 // 1: CgMaps::x describes `x` (TMA needs side >= 2): staged (K <= 3) or L2-prefetched
   long long* trace;          // KCG_TRACE builds only: per-iteration %globaltimer stamps
+  unsigned* sync;            // [0] arrival counter, [1] generation flag, [2..3] tile claims (zeroed per launch)
   double tol2;
 };
 
@@ -116,13 +128,13 @@ cudaError_t launch_rhs(int K, cudaStream_t s, const double* Y, const double* E, 
                        double* r0, double* p0, double* x, int P, int n, int side, int pitch);
 cudaError_t launch_cg(int K, cudaStream_t s, const CgArgs& a, const CgMaps& m, int grid, size_t smem);
 cudaError_t cg_kernel_config(int K, bool hits, int n_sys, int* max_grid, size_t* smem);
-cudaError_t launch_march(int K, cudaStream_t s, const CgArgs& a, const CgMaps& m, int grid, size_t smem);
-cudaError_t march_kernel_config(int K, bool hits, int n_sys, int* max_grid, size_t* smem);
 cudaError_t launch_apply(int K, cudaStream_t s, const SysParams* params, const double* x, double* y,
                          const double* hits, int n_sys, int side);
 cudaError_t launch_resid(int K, cudaStream_t s, const SysParams* params, const double* x,
                          const double* Y, const double* E, const double* hits, double* partials,
                          double* out, int n_sys, int n, int side);
+cudaError_t launch_xfix(int K, cudaStream_t s, const SysState* st, const double* p0, const double* p1, double* x,
+                        int n_sys, int side, int pitch);
 cudaError_t launch_backtransform(int K, cudaStream_t s, const double* W, double* x, int P, int side);
 int apply_tiles_per_sys(int side);
 

@@ -62,6 +62,11 @@ __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, u
       "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar))
       : "memory");
 }
+__device__ __forceinline__ void tma_prefetch_l2_3d(const CUtensorMap* map, int c0, int c1, int c2) {
+  asm volatile("cp.async.bulk.prefetch.tensor.3d.L2.global [%0, {%1, %2, %3}];" ::"l"(reinterpret_cast<uint64_t>(map)),
+               "r"(c0), "r"(c1), "r"(c2)
+               : "memory");
+}
 __device__ __forceinline__ void fence_proxy_async_smem() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
@@ -129,6 +134,7 @@ __device__ __forceinline__ SysState cg_update(SysState z, double rr, double wr, 
     else if (a.max_iter <= 0) z.status = ST_MAXIT;
     else { z.alpha = rr / wr; z.beta = 0.0; }
   } else {
+    z.alpha_last = z.alpha;  // the step this pass used
     z.iters = it + 1;
     z.rel = sqrt(rr / z.bnorm2);
     if (!isfinite(rr) || !isfinite(wr)) z.status = ST_NONFINITE;
@@ -145,47 +151,58 @@ __device__ __forceinline__ SysState cg_update(SysState z, double rr, double wr, 
   return z;
 }
 
-// After the iteration's grid barrier: CTA b reduces the tile partials of active systems b, b+grid,...
-// with all its threads (one round of independent loads; thread t sums tiles t, t+NT, ... in order,
-// then a fixed warp/CTA tree -> deterministic, independent of grid size and batch composition),
-// publishes the new state in a.state_out; a second grid barrier; every CTA pulls the states.
+// ---------------------------------------------------------------------- per-iteration reduction
+// Canonical order of a system's reduction, used by every mode below so that the scalars -- and
+// hence the iterates -- are bitwise independent of the mode, the grid size and the batch
+// composition: slot t in [0, NT) sums the tile partials t, t+NT, t+2NT, ... in order; the slots of a
+// warp are combined by the xor-shuffle tree; the NW warp sums are added in warp order.
+#define KCG_RB 8  // systems reduced per CTA pass (shared slots [KCG_RB][2][NW])
+
+// The CTA reduces systems act[ii], ii = ii0, ii0 + step, ... and applies the CG scalar update.
+// Results go to st_smem[s] (redundant mode: every CTA computes the same values) or a.state_out[s].
 template <int NT>
-__device__ __forceinline__ void reduce_update_systems(const CgArgs& a, SysState* st, const int* act, int nact,
-                                                      int par_out, int it, double (*red)[32]) {
-  constexpr int NW = NT / 32, U = 4;
+__device__ __forceinline__ void reduce_systems_cta(const CgArgs& a, SysState* st, const int* act, int nact, int ii0,
+                                                   int step, int par_out, int it, double (*rs)[2][NT / 32],
+                                                   bool to_global) {
+  constexpr int NW = NT / 32;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int tps = a.tiles_per_sys;
-  for (int ii = blockIdx.x; ii < nact; ii += gridDim.x) {
-    const int s = act[ii];
-    const double2* base = reinterpret_cast<const double2*>(a.partials + ((size_t)par_out * a.n_sys + s) * tps * 2);
-    double rr = 0.0, wr = 0.0;
-    for (int t0 = tid; t0 < tps; t0 += U * NT) {
-      double2 v[U];
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const int tl = t0 + u * NT;
-        v[u] = tl < tps ? __ldcg(base + tl) : make_double2(0.0, 0.0);
+  for (int first = ii0; first < nact; first += KCG_RB * step) {
+    int nb = 0;
+#pragma unroll 2
+    for (int b = 0; b < KCG_RB; ++b) {
+      const int ii = first + b * step;
+      if (ii >= nact) break;
+      const int s = act[ii];
+      const double2* base = reinterpret_cast<const double2*>(a.partials + ((size_t)par_out * a.n_sys + s) * tps * 2);
+      double rr = 0.0, wr = 0.0;
+      for (int t = tid; t < tps; t += NT) {
+        const double2 v = __ldcg(base + t);
+        rr += v.x;
+        wr += v.y;
       }
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        rr += v[u].x;
-        wr += v[u].y;
-      }
+      rr = warp_sum(rr);
+      wr = warp_sum(wr);
+      if (lane == 0) { rs[b][0][warp] = rr; rs[b][1][warp] = wr; }
+      ++nb;
     }
-    rr = warp_sum(rr);
-    wr = warp_sum(wr);
-    if (lane == 0) { red[0][warp] = rr; red[1][warp] = wr; }
     __syncthreads();
-    if (tid == 0) {
+    if (tid < nb) {
+      const int s = act[first + tid * step];
       double r2 = 0.0, w2 = 0.0;
-      for (int w = 0; w < NW; ++w) { r2 += red[0][w]; w2 += red[1][w]; }
-      a.state_out[s] = cg_update(st[s], r2, w2, it, a);
+      for (int w = 0; w < NW; ++w) { r2 += rs[tid][0][w]; w2 += rs[tid][1][w]; }
+      const SysState z = cg_update(st[s], r2, w2, it, a);
+      if (to_global) a.state_out[s] = z;
+      else st[s] = z;
     }
     __syncthreads();
   }
-  __threadfence();
-  cg::this_grid().sync();
-  for (int ii = tid; ii < nact; ii += NT) {
+}
+
+// Every CTA pulls the states published in a.state_out by the reducing CTA(s).
+template <int NT>
+__device__ __forceinline__ void pull_states(const CgArgs& a, SysState* st, const int* act, int nact) {
+  for (int ii = threadIdx.x; ii < nact; ii += NT) {
     const int s = act[ii];
     const SysState* g = a.state_out + s;
     SysState z;
@@ -198,9 +215,106 @@ __device__ __forceinline__ void reduce_update_systems(const CgArgs& a, SysState*
     z.status = __ldcg(&g->status);
     z.parity = __ldcg(&g->parity);
     z.pad = 0;
+    z.alpha_last = __ldcg(&g->alpha_last);
     st[s] = z;
   }
   __syncthreads();
+}
+
+__device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_u32(unsigned* p, unsigned v) {
+  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ void spin_until_geq(const unsigned* p, unsigned target) {
+  if (ld_acquire_u32(p) >= target) return;
+  const long long t0 = clock64();
+  while (ld_acquire_u32(p) < target) {
+    if (clock64() - t0 > (1LL << 34)) __trap();  // ~8 s: a lost arrival, never a legal wait
+  }
+}
+
+// The iteration's barrier + reduction.  Modes (chosen per iteration, all in the canonical order):
+//  REDUNDANT  (nact <= KCG_RB and nact*tps <= KCG_RED_MAX): one grid barrier, then every CTA reduces
+//             every active system itself -- no second barrier, no state broadcast.
+//  ONEBAR     (KCG_ONEBAR): CTAs arrive on a monotonic counter a.sync[0]; the LAST to arrive reduces
+//             all systems, publishes the states and releases the generation flag a.sync[1].
+//  otherwise  grid barrier; CTA b reduces systems b, b+grid, ...; second grid barrier; pull.
+// a.sync is zeroed before each launch.  `after_count` runs on thread 0 once every CTA's stores of the pass are visible (the speculative
+// TMA of the next pass).
+template <int NT, typename F>
+__device__ __forceinline__ void iteration_reduce(const CgArgs& a, SysState* st, const int* act, int nact,
+                                                 int par_out, int it, double (*rs)[2][NT / 32], unsigned& epoch,
+                                                 F after_count) {
+  __shared__ int s_last;
+  const int tid = threadIdx.x;
+  const bool small = nact <= KCG_RB && nact * a.tiles_per_sys <= KCG_RED_MAX;
+  if (small || !KCG_ONEBAR) {
+    fence_proxy_async_global();
+    cg::this_grid().sync();
+    fence_proxy_async_global();
+    if (tid == 0) after_count();
+    if (small) {
+      reduce_systems_cta<NT>(a, st, act, nact, 0, 1, par_out, it, rs, false);
+    } else {
+      reduce_systems_cta<NT>(a, st, act, nact, blockIdx.x, gridDim.x, par_out, it, rs, true);
+      __threadfence();
+      cg::this_grid().sync();
+      pull_states<NT>(a, st, act, nact);
+    }
+    return;
+  }
+  ++epoch;  // ONEBAR iterations so far (uniform across CTAs: the mode choice is)
+  const unsigned target = epoch * gridDim.x;
+  __syncthreads();  // every partial / state store of this CTA is issued
+  if (tid == 0) {
+    fence_proxy_async_global();
+    __threadfence();
+    const unsigned prev = atomicAdd(a.sync, 1u);
+    s_last = prev + 1 == target;
+    if (!s_last) spin_until_geq(a.sync, target);
+    __threadfence();
+    fence_proxy_async_global();
+    after_count();
+  }
+  __syncthreads();
+  if (s_last) {
+#if KCG_ONEBAR == 2
+    {  // EXPERIMENT: warp per system, lanes in order (not the canonical order)
+      constexpr int NW = NT / 32, U = 8;
+      const int lane = tid & 31, warp = tid >> 5, tps = a.tiles_per_sys;
+      for (int ii = warp; ii < nact; ii += NW) {
+        const int s = act[ii];
+        const double2* base = reinterpret_cast<const double2*>(a.partials + ((size_t)par_out * a.n_sys + s) * tps * 2);
+        double rr = 0.0, wr = 0.0;
+        for (int t0 = lane; t0 < tps; t0 += U * 32) {
+          double2 v[U];
+#pragma unroll
+          for (int u = 0; u < U; ++u) v[u] = t0 + u * 32 < tps ? __ldcg(base + t0 + u * 32) : make_double2(0.0, 0.0);
+#pragma unroll
+          for (int u = 0; u < U; ++u) { rr += v[u].x; wr += v[u].y; }
+        }
+        rr = warp_sum(rr);
+        wr = warp_sum(wr);
+        if (lane == 0) a.state_out[s] = cg_update(st[s], rr, wr, it, a);
+      }
+      __syncthreads();
+    }
+#else
+    reduce_systems_cta<NT>(a, st, act, nact, 0, 1, par_out, it, rs, true);
+#endif
+    if (tid == 0) {
+      __threadfence();
+      st_release_u32(a.sync + 1, epoch);
+    }
+  } else if (tid == 0) {
+    spin_until_geq(a.sync + 1, epoch);
+  }
+  __syncthreads();
+  pull_states<NT>(a, st, act, nact);
 }
 
 // --------------------------------------------------------------------------- persistent CG
@@ -209,7 +323,7 @@ __device__ __forceinline__ void reduce_update_systems(const CgArgs& a, SysState*
 // 2l, 2l+1 (double2 in shared and global memory); horizontal neighbours come from shuffles.
 //   Phase A  p_new = r + beta p                    whole box (elementwise)
 //   Phase B  q = G p_new, r_new = r - alpha q      T rows (pairs) + the 1-pixel ring (scalars)
-//   Phase C  w = G r_new on T; (r,r), (w,r); x += alpha p_new
+//   Phase C  w = G r_new on T; (r,r), (w,r); x += alpha p_new (+ alpha_prev p_old, X2)
 // x: with XTMA the tile's x block (64 x TY x K) is TMA-loaded into shared memory at the start of the
 // tile (consumed in phase C, so its latency hides behind phases A and B); x, r_new, p_new are
 // written back with coalesced 16-byte vector stores.
@@ -220,7 +334,9 @@ struct TileCtx {
   double* xs;         // x block of the tile in the stage [K][TY][TX] (XTMA)
   const double* Ms;   // M (K*K) then tau (K) of this tile's system, shared
   int s, y0, x0, par;
+  bool xpass;         // this pass updates x (every pass without KCG_X2; even passes >= 2 with it)
   double alpha, beta, kappa2;
+  double alpha_prev;  // X2: alpha of the previous pass (its p_new is this pass's p_old), else 0
   const double* hp;   // hits plane or nullptr
   uint64_t* bar;      // stage mbarrier
   uint32_t phase;
@@ -228,9 +344,9 @@ struct TileCtx {
 };
 
 template <int K, bool EDGE, bool HITS, bool XTMA>
-__device__ __forceinline__ void cg_tile(const CgArgs& a, const TileCtx& tc, double (*red)[32]) {
+__device__ __forceinline__ void cg_tile(const CgArgs& a, const TileCtx& tc, double (*tred)[cg_threads(K) / 32]) {
   constexpr int TY = cg_tile_y(K), TX = KCG_TX, H = KCG_HALO;
-  constexpr int BW = TX + 2 * H, BH = TY + 2 * H, PLANE = BW * BH, FIELD = K * PLANE;
+  constexpr int BW = TX + 2 * H, BH = TY + 2 * H, PLANE = BW * BH;
   constexpr int NT = cg_threads(K), NW = NT / 32, RPW = TY / NW;
   constexpr int RP = 2 * (TX + 2) + 2 * TY;  // ring points
   static_assert(TX == 64 && RPW * NW == TY, "pair mapping needs TX = 64 and NW | TY");
@@ -246,20 +362,47 @@ __device__ __forceinline__ void cg_tile(const CgArgs& a, const TileCtx& tc, doub
 
   mbar_wait(tc.bar, tc.phase);
 
-  // Phase A
+  // Phase A: p_new = r + beta p over the whole box.  The tile interior is done in the pair
+  // mapping of phases B/C, so on x passes the thread keeps its pairs' x increment
+  //   xinc = alpha_prev p_old + alpha p_new   (X2: x is updated every other pass, see cg_update)
+  // in registers; the 2-pixel frame of the box is a flat loop over double2 units.
+  double2 xinc[RPW][K];
   {
     double2* P2 = reinterpret_cast<double2*>(Pp);
     const double2* R2 = reinterpret_cast<const double2*>(R);
-    if (beta == 0.0) {
-      for (int e = tid; e < FIELD / 2; e += NT) P2[e] = R2[e];
-    } else {
-      for (int e = tid; e < FIELD / 2; e += NT) {
-        const double2 r = R2[e];
-        double2 p = P2[e];
-        p.x = fma(beta, p.x, r.x);
-        p.y = fma(beta, p.y, r.y);
-        P2[e] = p;
+    const double ap = tc.alpha_prev;
+#pragma unroll
+    for (int j = 0; j < RPW; ++j) {
+      const int ly = warp + j * NW + H;
+#pragma unroll
+      for (int c = 0; c < K; ++c) {
+        const int e = (c * PLANE + ly * BW + H) / 2 + lane;
+        const double2 r = R2[e], po = P2[e];
+        double2 pn;
+        pn.x = fma(beta, po.x, r.x);
+        pn.y = fma(beta, po.y, r.y);
+        P2[e] = pn;
+        xinc[j][c].x = fma(alpha, pn.x, ap * po.x);
+        xinc[j][c].y = fma(alpha, pn.y, ap * po.y);
       }
+    }
+    constexpr int FR = 4 * (BW / 2) + 2 * TY;  // frame double2 units per plane
+    for (int u = tid; u < K * FR; u += NT) {
+      const int c = u / FR, v = u - c * FR;
+      int e;
+      if (v < 4 * (BW / 2)) {
+        const int rr = v / (BW / 2);
+        e = (rr < 2 ? rr : BH - 4 + rr) * (BW / 2) + (v - rr * (BW / 2));
+      } else {
+        const int w = v - 4 * (BW / 2);
+        e = (H + (w >> 1)) * (BW / 2) + ((w & 1) ? BW / 2 - 1 : 0);
+      }
+      e += c * (PLANE / 2);
+      const double2 r = R2[e], po = P2[e];
+      double2 pn;
+      pn.x = fma(beta, po.x, r.x);
+      pn.y = fma(beta, po.y, r.y);
+      P2[e] = pn;
     }
   }
   __syncthreads();
@@ -376,15 +519,17 @@ __device__ __forceinline__ void cg_tile(const CgArgs& a, const TileCtx& tc, doub
     }
     double* xp = a.x + ((size_t)s * K * side + gy) * side + gx;
     double2 xj[K];
+    if (tc.xpass) {
 #pragma unroll
-    for (int c = 0; c < K; ++c) {
-      if (XTMA) {
-        xj[c] = reinterpret_cast<const double2*>(tc.xs + ((size_t)c * TY + (gy - y0)) * TX)[lane];
-      } else if (!EDGE || (in0 && in1)) {
-        xj[c] = __ldcg(reinterpret_cast<const double2*>(xp + c * N));
-      } else {
-        xj[c].x = in0 ? __ldcg(xp + c * N) : 0.0;
-        xj[c].y = in1 ? __ldcg(xp + c * N + 1) : 0.0;
+      for (int c = 0; c < K; ++c) {
+        if (XTMA) {
+          xj[c] = reinterpret_cast<const double2*>(tc.xs + ((size_t)c * TY + (gy - y0)) * TX)[lane];
+        } else if (!EDGE || (in0 && in1)) {
+          xj[c] = __ldcg(reinterpret_cast<const double2*>(xp + c * N));
+        } else {
+          xj[c].x = in0 ? __ldcg(xp + c * N) : 0.0;
+          xj[c].y = in1 ? __ldcg(xp + c * N + 1) : 0.0;
+        }
       }
     }
     double2 rc[K];
@@ -415,28 +560,28 @@ __device__ __forceinline__ void cg_tile(const CgArgs& a, const TileCtx& tc, doub
       const double w1 = HITS ? fma(h1, mix1, tau[c] * fma(kd1, rc[c].y, -nb1)) : fma(tau[c], fma(kd1, rc[c].y, -nb1), mix1);
       const double2 pn = reinterpret_cast<const double2*>(Pp + c * PLANE + ly * BW)[1 + lane];
       double2 xn;
-      xn.x = fma(alpha, pn.x, xj[c].x);
-      xn.y = fma(alpha, pn.y, xj[c].y);
+      xn.x = xj[c].x + xinc[j][c].x;
+      xn.y = xj[c].y + xinc[j][c].y;
       if (!EDGE || (in0 && in1)) {
         rr = fma(rc[c].x, rc[c].x, rr);
         wr = fma(w0, rc[c].x, wr);
         rr = fma(rc[c].y, rc[c].y, rr);
         wr = fma(w1, rc[c].y, wr);
-        *reinterpret_cast<double2*>(xp + c * N) = xn;
+        if (tc.xpass) *reinterpret_cast<double2*>(xp + c * N) = xn;
         *reinterpret_cast<double2*>(rout + c * ps) = rc[c];
         *reinterpret_cast<double2*>(pout + c * ps) = pn;
       } else {
         if (in0) {
           rr = fma(rc[c].x, rc[c].x, rr);
           wr = fma(w0, rc[c].x, wr);
-          xp[c * N] = xn.x;
+          if (tc.xpass) xp[c * N] = xn.x;
           rout[c * ps] = rc[c].x;
           pout[c * ps] = pn.x;
         }
         if (in1) {
           rr = fma(rc[c].y, rc[c].y, rr);
           wr = fma(w1, rc[c].y, wr);
-          xp[c * N + 1] = xn.y;
+          if (tc.xpass) xp[c * N + 1] = xn.y;
           rout[c * ps + 1] = rc[c].y;
           pout[c * ps + 1] = pn.y;
         }
@@ -445,14 +590,30 @@ __device__ __forceinline__ void cg_tile(const CgArgs& a, const TileCtx& tc, doub
   }
   rr = warp_sum(rr);
   wr = warp_sum(wr);
-  if (lane == 0) { red[0][warp] = rr; red[1][warp] = wr; }
-  __syncthreads();
+  // per-warp partials; warp 0 sums them (fixed order) after the next CTA barrier (flush_tile_partial)
+  if (lane == 0) { tred[0][warp] = rr; tred[1][warp] = wr; }
+  if (!KCG_DEFER) {
+    __syncthreads();
+    if (warp == 0) {
+      double v0 = lane < NW ? tred[0][lane] : 0.0;
+      double v1 = lane < NW ? tred[1][lane] : 0.0;
+      v0 = warp_sum(v0);
+      v1 = warp_sum(v1);
+      if (lane == 0) { tc.part_out[0] = v0; tc.part_out[1] = v1; }
+    }
+  }
+}
+
+// Tile partial (r,r), (w,r) of a finished tile: the fixed-order sum of its per-warp values, written
+// by warp 0 after a barrier that follows the tile (deferred, so a tile needs no barrier of its own).
+template <int NW>
+__device__ __forceinline__ void flush_tile_partial(const double (*tred)[NW], double* part_out, int warp, int lane) {
   if (warp == 0) {
-    double v0 = lane < NW ? red[0][lane] : 0.0;
-    double v1 = lane < NW ? red[1][lane] : 0.0;
+    double v0 = lane < NW ? tred[0][lane] : 0.0;
+    double v1 = lane < NW ? tred[1][lane] : 0.0;
     v0 = warp_sum(v0);
     v1 = warp_sum(v1);
-    if (lane == 0) { tc.part_out[0] = v0; tc.part_out[1] = v1; }
+    if (lane == 0) { part_out[0] = v0; part_out[1] = v1; }
   }
 }
 
@@ -470,19 +631,25 @@ __global__ void __launch_bounds__(cg_threads(K), cg_min_blocks(K)) cg_persistent
   SysState* st = reinterpret_cast<SysState*>(smem_raw + NS * STAGE_BYTES);
   int* act = reinterpret_cast<int*>(st + a.n_sys);
   __shared__ __align__(8) uint64_t mbar[2];
-  __shared__ double red[2][32];
+  __shared__ double tred[2][2][NW];  // per-warp tile partials, double-buffered by tile parity
+  // per-warp system sums of the iteration reduction: aliased onto pipeline stage 1, which is idle
+  // from the end of a pass's last tile until the first prefetch of the next pass
+  double (*rs)[2][NW] = reinterpret_cast<double (*)[2][NW]>(smem_raw + STAGE_BYTES);
+  static_assert(NS == 2 && (size_t)KCG_RB * 2 * NW * 8 <= (size_t)STAGE_BYTES, "rs alias");  // per-warp tile partials, double-buffered by tile parity
   __shared__ double Ms[KCG_KMAX * KCG_KMAX + KCG_KMAX];
   __shared__ int s_nact;
+  __shared__ int s_sched[2][2];  // [buffer][current tile, next tile]
+  __shared__ int s_info[2][4];   // [stage][system, tile, tile row, tile col] of the tile in that stage
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int tps = a.tiles_per_sys;
   const bool xtma = cg_xtma(K) && a.x_tma != 0;
-  cg::grid_group grid = cg::this_grid();
+  unsigned epoch = 0;  // ONEBAR barrier generations
 
   for (int s = tid; s < a.n_sys; s += NT) {
     SysState z;
     z.bnorm2 = 0.0; z.gamma = 0.0; z.alpha = 0.0; z.beta = 0.0; z.rel = 1.0;
-    z.iters = 0; z.status = ST_RUNNING; z.parity = 0; z.pad = 0;
+    z.iters = 0; z.status = ST_RUNNING; z.parity = 0; z.pad = 0; z.alpha_last = 0.0;
     st[s] = z;
   }
   if (tid == 0) {
@@ -496,14 +663,23 @@ __global__ void __launch_bounds__(cg_threads(K), cg_min_blocks(K)) cg_persistent
   int it = -1;  // -1 = start pass (alpha = beta = 0): r, p <- b and (b, b), (G b, b)
 
   // TMA of tile t (index into the active-tile list) into stage sidx; parity flip for speculation
+  // pass q = it + 1 updates x iff xpass_of(q) (KCG_X2: even passes >= 2; else every pass >= 1)
+  auto xpass_of = [](int q) { return KCG_X2 ? (q >= 2 && (q & 1) == 0) : (q >= 1); };
+  // Thread 0: TMA of (physical) tile t into stage sidx (parity flipped for the speculative load of
+  // the next pass) and its coordinates into s_info[sidx] for all threads.  On x passes the x block
+  // comes with the boxes (XTMA) or is prefetched into L2 (read by phase C).
   auto issue = [&](int t, int sidx, int flip) {
     const int s = act[t / tps];
     const int tile = t - (t / tps) * tps;
     const int ty = tile / a.tiles_x, tx = tile - ty * a.tiles_x;
+    s_info[sidx][0] = s; s_info[sidx][1] = tile; s_info[sidx][2] = ty; s_info[sidx][3] = tx;
     const int par = st[s].parity ^ flip;
     double* dst = reinterpret_cast<double*>(smem_raw + sidx * STAGE_BYTES);
-    mbar_arrive_expect_tx(&mbar[sidx], xtma ? STAGE_BYTES : 2 * FIELD * 8);
-    if (xtma) tma_load_3d(dst + 2 * FIELD, &maps.x, &mbar[sidx], tx * TX, ty * TY, s * K);
+    const bool xp = xpass_of(it + 1 + flip);
+    const bool xl = xtma && xp;
+    mbar_arrive_expect_tx(&mbar[sidx], xl ? STAGE_BYTES : 2 * FIELD * 8);
+    if (xl) tma_load_3d(dst + 2 * FIELD, &maps.x, &mbar[sidx], tx * TX, ty * TY, s * K);
+    else if (xp && a.x_tma && KCG_XPF) tma_prefetch_l2_3d(&maps.x, tx * TX, ty * TY, s * K);
     tma_load_3d(dst, &maps.r[par], &mbar[sidx], tx * TX - H, ty * TY - H, s * K);
     tma_load_3d(dst + FIELD, &maps.p[par], &mbar[sidx], tx * TX - H, ty * TY - H, s * K);
   };
@@ -530,25 +706,36 @@ __global__ void __launch_bounds__(cg_threads(K), cg_min_blocks(K)) cg_persistent
     const bool tr = KCG_TRACE && a.trace && it + 1 < KCG_TRACE_ITERS;
     if (tr && blockIdx.x == 0 && tid == 0) a.trace[(size_t)(it + 1) * KCG_TRACE_COLS + 0] = globaltimer();
 
-    if (!spec && (int)blockIdx.x < ntiles && tid == 0) issue(blockIdx.x, 0, 0);
+    // serpentine order: odd passes walk the active-tile list backwards, so the first tiles of a
+    // pass are the ones the previous pass wrote last (still L2-resident when the state fits)
+    const bool rev = KCG_SERP && (par_out != 0);
+    if (!spec && (int)blockIdx.x < ntiles && tid == 0) issue(rev ? ntiles - 1 - (int)blockIdx.x : (int)blockIdx.x, 0, 0);
     spec = false;
+    // Tile schedule (logical indices into the active-tile list): CTA b starts with tiles b and
+    // b + grid; with KCG_DYN the rest are claimed from the pass's counter a.sync[2 + par_out]
+    // (starting at 2 grid), one claim ahead so the atomic's latency hides behind a whole tile;
+    // without it, b + 2 grid, b + 3 grid, ...  Both buffers of s_sched are written by thread 0 one
+    // tile ahead of their readers (separated by the top-of-tile barrier).
+    unsigned* ctr = a.sync + 2 + par_out;
+    const int G = gridDim.x;
+    if (tid == 0) { s_sched[0][0] = blockIdx.x; s_sched[0][1] = blockIdx.x + G; }
     int i = 0;
-    for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++i) {
-      const int sidx = NS == 2 ? (i & 1) : 0;
-      const int tn = t + gridDim.x;
+    double* prev_part = nullptr;  // partial slot of the previous tile, flushed after the next barrier
+    for (;; ++i) {
+      const int sidx = i & 1;
       __syncthreads();
+      const int t = s_sched[i & 1][0], tn = s_sched[i & 1][1];
+      if (prev_part) flush_tile_partial<NW>(tred[(i - 1) & 1], prev_part, warp, lane);
+      if (t >= ntiles) break;
+      unsigned claim = 0;
       if (tid == 0) {
-        if (NS == 2 && tn < ntiles) {
+        if (tn < ntiles) {
           fence_proxy_async_smem();
-          issue(tn, sidx ^ 1, 0);
-        } else if (NS == 1 && i > 0) {
-          fence_proxy_async_smem();
-          issue(t, 0, 0);
+          issue(rev ? ntiles - 1 - tn : tn, sidx ^ 1, 0);
         }
+        if (KCG_DYN && tn < ntiles) claim = atomicAdd(ctr, 1u);
       }
-      const int s = act[t / tps];
-      const int tile = t - (t / tps) * tps;
-      const int ty = tile / a.tiles_x, tx = tile - ty * a.tiles_x;
+      const int s = s_info[sidx][0], tile = s_info[sidx][1], ty = s_info[sidx][2], tx = s_info[sidx][3];
       const SysParams* sp = a.params + s;
       if (tid < K * K) Ms[tid] = __ldg(&sp->M[tid]);
       else if (tid < K * K + K) Ms[tid] = __ldg(&sp->tau[tid - K * K]);
@@ -563,6 +750,8 @@ __global__ void __launch_bounds__(cg_threads(K), cg_min_blocks(K)) cg_persistent
       tc.par = st[s].parity;
       tc.alpha = st[s].alpha;
       tc.beta = st[s].beta;
+      tc.xpass = xpass_of(it + 1);
+      tc.alpha_prev = KCG_X2 ? st[s].alpha_last : 0.0;
       tc.kappa2 = __ldg(&sp->kappa2);
       tc.hp = HITS ? a.hits + (size_t)__ldg(&sp->hits_plane) * ((size_t)a.side * a.side) : nullptr;
       tc.bar = &mbar[sidx];
@@ -570,28 +759,34 @@ __global__ void __launch_bounds__(cg_threads(K), cg_min_blocks(K)) cg_persistent
       tc.part_out = a.partials + (((size_t)par_out * a.n_sys + s) * tps + tile) * 2;
       const bool interior = tc.x0 >= H && tc.x0 + TX + H <= a.side && tc.y0 >= H && tc.y0 + TY + H <= a.side;
       if (cg_xtma(K) && xtma) {
-        if (interior) cg_tile<K, false, HITS, cg_xtma(K)>(a, tc, red);
-        else cg_tile<K, true, HITS, cg_xtma(K)>(a, tc, red);
+        if (interior) cg_tile<K, false, HITS, cg_xtma(K)>(a, tc, tred[i & 1]);
+        else cg_tile<K, true, HITS, cg_xtma(K)>(a, tc, tred[i & 1]);
       } else {
-        if (interior) cg_tile<K, false, HITS, false>(a, tc, red);
-        else cg_tile<K, true, HITS, false>(a, tc, red);
+        if (interior) cg_tile<K, false, HITS, false>(a, tc, tred[i & 1]);
+        else cg_tile<K, true, HITS, false>(a, tc, tred[i & 1]);
       }
       if (sidx) phase1 ^= 1u; else phase0 ^= 1u;
-    }
+      if (KCG_DEFER) prev_part = tc.part_out;
+      if (tid == 0) {  // the tile after tn (the claim's value is consumed only now)
+        s_sched[(i + 1) & 1][0] = tn;
+        s_sched[(i + 1) & 1][1] = tn >= ntiles ? ntiles : (KCG_DYN ? 2 * G + (int)claim : tn + G);
+      }
+    }  // (the loop exits at a top-of-tile barrier, after flushing the last tile's partial)
 
     if (tr && tid == 0 && blockIdx.x < KCG_TRACE_COLS - 3)
       a.trace[(size_t)(it + 1) * KCG_TRACE_COLS + 3 + blockIdx.x] = globaltimer();
-    fence_proxy_async_global();
-    grid.sync();
-    fence_proxy_async_global();
-    if (tr && blockIdx.x == 0 && tid == 0) a.trace[(size_t)(it + 1) * KCG_TRACE_COLS + 1] = globaltimer();
-    // speculative first load of the next iteration (same active set, flipped parity) overlaps the
-    // reduction below; verified against the new active count at the top of the loop
-    if (it >= 0 && (int)blockIdx.x < ntiles && tid == 0) issue(blockIdx.x, 0, 1);
-    spec = it >= 0 && (int)blockIdx.x < ntiles;
+    // speculative first load of the next iteration (same active set, flipped parity and order)
+    // overlaps the reduction; verified against the new active count at the top of the loop
+    const int spec_t = (KCG_SERP && !rev) ? ntiles - 1 - (int)blockIdx.x : (int)blockIdx.x;
+    const bool do_spec = it >= 0 && (int)blockIdx.x < ntiles;
+    iteration_reduce<NT>(a, st, act, nact, par_out, it, rs, epoch, [&]() {
+      if (tr && blockIdx.x == 0) a.trace[(size_t)(it + 1) * KCG_TRACE_COLS + 1] = globaltimer();
+      if (KCG_DYN && blockIdx.x == 0) *ctr = 0u;  // quiescent now; next used two passes later
+      if (do_spec) issue(spec_t, 0, 1);
+    });
+    spec = do_spec;
     nact_prev = nact;
 
-    reduce_update_systems<NT>(a, st, act, nact, par_out, it, red);
     if (tr && blockIdx.x == 0 && tid == 0) a.trace[(size_t)(it + 1) * KCG_TRACE_COLS + 2] = globaltimer();
     if (blockIdx.x == 0 && tid == 0 && it >= 0 && it < a.history_cap) {
       double m = 0.0;
@@ -602,349 +797,6 @@ __global__ void __launch_bounds__(cg_threads(K), cg_min_blocks(K)) cg_persistent
   }
   if (blockIdx.x == 0)
     for (int s = tid; s < a.n_sys; s += NT) a.state_out[s] = st[s];
-}
-
-// --------------------------------------------------------------------------- warp-marching CG
-// The production CG kernel.  Same single-pass Chronopoulos-Gear iteration, same per-tile partials
-// and per-system reductions as cg_persistent_kernel, but each WARP owns a 60 x 16 output tile and
-// marches down its 64-wide box (2-pixel halo) row by row:
-//   box rows arrive through a per-warp ring of TMA chunks (CR rows x 64 cols x K planes, r and p,
-//   zero-filled outside the face); per lane a PAIR of columns (32 lanes x 2 = the 64 box columns,
-//   so the halo needs no special lanes); horizontal neighbours by shuffles; vertical neighbours
-//   from a 3-row register window of p_new and r_new:
-//     step b:  p_new(b) = r(b) + beta p(b)
-//              r_new(b-1) = r(b-1) - alpha G p_new(b-1)          (rows b-2..b of p_new)
-//              w(b-2) = G r_new(b-2); (r,r), (w,r); x += alpha p_new; store x, r_new, p_new (b-2)
-// No block-level barrier inside an iteration; shared memory only receives the TMA data and is read
-// once per element.  Columns 0/63 of the box produce garbage that no output uses.
-__device__ __forceinline__ double2 shfl_up2(double2 v) {
-  return make_double2(__shfl_up_sync(0xffffffffu, v.x, 1), __shfl_up_sync(0xffffffffu, v.y, 1));
-}
-
-template <int K, bool EDGE, bool HITS>
-__device__ __forceinline__ void march_apply(const double2 (&up)[K], const double2 (&ctr)[K], const double2 (&dn)[K],
-                                            const double* __restrict__ M, const double* __restrict__ tau, double kd0,
-                                            double kd1, double h0, double h1, int lane, double2 (&out)[K]) {
-  double mix0[K], mix1[K];
-#pragma unroll
-  for (int c = 0; c < K; ++c) {
-    mix0[c] = 0.0;
-    mix1[c] = 0.0;
-#pragma unroll
-    for (int d = 0; d < K; ++d) {
-      mix0[c] = fma(M[c * K + d], ctr[d].x, mix0[c]);
-      mix1[c] = fma(M[c * K + d], ctr[d].y, mix1[c]);
-    }
-  }
-#pragma unroll
-  for (int c = 0; c < K; ++c) {
-    double left = __shfl_up_sync(0xffffffffu, ctr[c].y, 1);
-    double right = __shfl_down_sync(0xffffffffu, ctr[c].x, 1);
-    left = lane == 0 ? 0.0 : left;
-    right = lane == 31 ? 0.0 : right;
-    const double nb0 = (up[c].x + dn[c].x) + (left + ctr[c].y);
-    const double nb1 = (up[c].y + dn[c].y) + (ctr[c].x + right);
-    if (HITS) {
-      out[c].x = fma(h0, mix0[c], tau[c] * fma(kd0, ctr[c].x, -nb0));
-      out[c].y = fma(h1, mix1[c], tau[c] * fma(kd1, ctr[c].y, -nb1));
-    } else {
-      out[c].x = fma(tau[c], fma(kd0, ctr[c].x, -nb0), mix0[c]);
-      out[c].y = fma(tau[c], fma(kd1, ctr[c].y, -nb1), mix1[c]);
-    }
-  }
-}
-
-struct MarchWarp {
-  uint64_t* bar;       // NB mbarriers of this warp
-  double* ring;        // NB chunks of this warp
-  long long seq;       // chunks consumed by this warp since kernel start (mbarrier phases)
-};
-
-template <int K, bool EDGE, bool HITS>
-__device__ __forceinline__ void march_tile(const CgArgs& a, const CgMaps& maps, MarchWarp& mw,
-                                           const double* __restrict__ Ms, int s, int y0, int x0, int par,
-                                           double alpha, double beta, double kappa2, const double* __restrict__ hp,
-                                           double* part_out, int lane, int& issued, int total_chunks, int q0,
-                                           const int* act, const SysState* st, int tps, int gwarp,
-                                           int nwarps_total) {
-  constexpr int BW = 64, TY = MARCH_TY, BR = TY + 4, CR = march_cr(K), NB = march_nb(K);
-  constexpr int NCH = BR / CR;
-  constexpr int CHUNK = 2 * K * CR * BW;  // doubles: r [K][CR][64] then p [K][CR][64]
-  static_assert(BR % CR == 0, "chunk rows");
-  const int side = a.side;
-  const size_t N = (size_t)side * side;
-  const size_t ps = (size_t)a.pitch * side;
-  double M[K * K], tau[K];
-#pragma unroll
-  for (int e = 0; e < K * K; ++e) M[e] = Ms[e];
-#pragma unroll
-  for (int c = 0; c < K; ++c) tau[c] = Ms[K * K + c];
-  const int gx = x0 - 2 + 2 * lane;  // global column of .x
-  const bool out_lane = lane >= 1 && lane <= 30;
-  double* rout = (par ? a.rbuf[0] : a.rbuf[1]) + (size_t)s * K * ps;
-  double* pout = (par ? a.pbuf[0] : a.pbuf[1]) + (size_t)s * K * ps;
-  double* xbase = a.x + (size_t)s * K * N;
-
-  // column masks / degrees that do not depend on the row
-  bool cin0 = true, cin1 = true;
-  double dx0 = 0.0, dx1 = 0.0;
-  if (EDGE) {
-    cin0 = gx >= 0 && gx < side;
-    cin1 = gx + 1 >= 0 && gx + 1 < side;
-    dx0 = (gx == 0) + (gx == side - 1);
-    dx1 = (gx + 1 == 0) + (gx + 1 == side - 1);
-  }
-
-  double2 pnA[K], pnB[K], pnC[K], rnA[K], rnB[K], rnC[K], rprev[K], xa[K];
-  double rr = 0.0, wr = 0.0;
-#pragma unroll
-  for (int c = 0; c < K; ++c) {
-    pnA[c] = pnB[c] = rnA[c] = rnB[c] = rprev[c] = xa[c] = make_double2(0.0, 0.0);
-  }
-
-  auto load_x = [&](double2 (&xr)[K], int o) {  // x of output box row o (o in [2, TY+1])
-    const int gy = y0 - 2 + o;
-    const bool ok = out_lane && (!EDGE || (gy < side && cin0 && cin1));
-#pragma unroll
-    for (int c = 0; c < K; ++c) {
-      if (ok) xr[c] = __ldcg(reinterpret_cast<const double2*>(xbase + ((size_t)c * side + gy) * side + gx));
-      else if (EDGE && out_lane && gy < side && (cin0 || cin1)) {
-        xr[c].x = cin0 ? __ldcg(xbase + ((size_t)c * side + gy) * side + gx) : 0.0;
-        xr[c].y = cin1 ? __ldcg(xbase + ((size_t)c * side + gy) * side + gx + 1) : 0.0;
-      } else xr[c] = make_double2(0.0, 0.0);
-    }
-  };
-  for (int b = 0; b < BR; ++b) {
-    const int ch = b / CR, rb = b - ch * CR;
-    const long long g = mw.seq + q0 + ch;  // global chunk sequence number
-    const int slot = (int)(g % NB);
-    if (rb == 0) {
-      // keep NB-1 chunks in flight along this warp's chunk stream (may run into its next tile)
-      const int want = min(q0 + ch + NB, total_chunks);
-      __syncwarp();  // every lane is done reading the slot about to be refilled
-      if (lane == 0) {
-        while (issued < want) {
-          const int qi = issued;
-          const int ti = qi / NCH, ci = qi - ti * NCH;
-          const int t = gwarp + ti * nwarps_total;
-          const int si = act[t / tps];
-          const int tile = t - (t / tps) * tps;
-          const int tyi = tile / a.tiles_x, txi = tile - tyi * a.tiles_x;
-          const long long gi = mw.seq + qi;
-          const int sl = (int)(gi % NB);
-          // the slot's previous chunk (gi - NB) was fully read by this warp before this point
-          fence_proxy_async_smem();
-          double* dst = mw.ring + (size_t)sl * CHUNK;
-          mbar_arrive_expect_tx(&mw.bar[sl], CHUNK * 8);
-          const int pi = st[si].parity;
-          tma_load_3d(dst, &maps.r[pi], &mw.bar[sl], txi * MARCH_TX - 2, tyi * TY - 2 + ci * CR, si * K);
-          tma_load_3d(dst + K * CR * BW, &maps.p[pi], &mw.bar[sl], txi * MARCH_TX - 2, tyi * TY - 2 + ci * CR, si * K);
-          ++issued;
-        }
-      }
-      issued = __shfl_sync(0xffffffffu, issued, 0);
-      mbar_wait(&mw.bar[slot], (uint32_t)((g / NB) & 1));
-    }
-    if (b >= 4) load_x(xa, b - 2);  // x of this step's output row; used at the end of the step
-    const double* rrow = mw.ring + (size_t)slot * CHUNK + rb * BW;
-    const double* prow = rrow + K * CR * BW;
-    double2 rcur[K];
-#pragma unroll
-    for (int c = 0; c < K; ++c) {
-      rcur[c] = reinterpret_cast<const double2*>(rrow + c * CR * BW)[lane];
-      const double2 pv = reinterpret_cast<const double2*>(prow + c * CR * BW)[lane];
-      pnC[c].x = fma(beta, pv.x, rcur[c].x);
-      pnC[c].y = fma(beta, pv.y, rcur[c].y);
-    }
-    if (b >= 2) {  // r_new of box row m = b - 1
-      const int gy = y0 - 2 + (b - 1);
-      double kd0 = kappa2 + 4.0, kd1 = kappa2 + 4.0;
-      bool in0 = true, in1 = true;
-      if (EDGE) {
-        const bool rin = gy >= 0 && gy < side;
-        in0 = rin && cin0;
-        in1 = rin && cin1;
-        const double dy = (gy == 0) + (gy == side - 1);
-        kd0 = kappa2 + (4.0 - dy - dx0);
-        kd1 = kappa2 + (4.0 - dy - dx1);
-      }
-      double h0 = 1.0, h1 = 1.0;
-      if (HITS) {
-        if (in0) h0 = __ldg(hp + (size_t)gy * side + gx);
-        if (in1) h1 = __ldg(hp + (size_t)gy * side + gx + 1);
-      }
-      double2 q[K];
-      march_apply<K, EDGE, HITS>(pnA, pnB, pnC, M, tau, kd0, kd1, h0, h1, lane, q);
-#pragma unroll
-      for (int c = 0; c < K; ++c) {
-        rnC[c].x = in0 ? fma(-alpha, q[c].x, rprev[c].x) : 0.0;
-        rnC[c].y = in1 ? fma(-alpha, q[c].y, rprev[c].y) : 0.0;
-      }
-      if (b >= 4) {  // outputs of box row o = b - 2
-        const int o = b - 2;
-        const int gyo = y0 - 2 + o;
-        double kdo0 = kappa2 + 4.0, kdo1 = kappa2 + 4.0;
-        bool on0 = out_lane, on1 = out_lane;
-        if (EDGE) {
-          const bool rin = gyo < side;
-          on0 = on0 && rin && cin0;
-          on1 = on1 && rin && cin1;
-          const double dy = (gyo == 0) + (gyo == side - 1);
-          kdo0 = kappa2 + (4.0 - dy - dx0);
-          kdo1 = kappa2 + (4.0 - dy - dx1);
-        }
-        double ho0 = 1.0, ho1 = 1.0;
-        if (HITS) {
-          if (on0) ho0 = __ldg(hp + (size_t)gyo * side + gx);
-          if (on1) ho1 = __ldg(hp + (size_t)gyo * side + gx + 1);
-        }
-        double2 w[K];
-        march_apply<K, EDGE, HITS>(rnA, rnB, rnC, M, tau, kdo0, kdo1, ho0, ho1, lane, w);
-        const size_t xo = (size_t)gyo * side + gx;
-        const size_t ro = (size_t)gyo * a.pitch + gx;
-#pragma unroll
-        for (int c = 0; c < K; ++c) {
-          double2 xn;
-          xn.x = fma(alpha, pnA[c].x, xa[c].x);
-          xn.y = fma(alpha, pnA[c].y, xa[c].y);
-          if (!EDGE || (on0 && on1)) {
-            if (out_lane) {
-              rr = fma(rnB[c].x, rnB[c].x, rr);
-              rr = fma(rnB[c].y, rnB[c].y, rr);
-              wr = fma(w[c].x, rnB[c].x, wr);
-              wr = fma(w[c].y, rnB[c].y, wr);
-              *reinterpret_cast<double2*>(xbase + c * N + xo) = xn;
-              *reinterpret_cast<double2*>(rout + c * ps + ro) = rnB[c];
-              *reinterpret_cast<double2*>(pout + c * ps + ro) = pnA[c];
-            }
-          } else {
-            if (on0) {
-              rr = fma(rnB[c].x, rnB[c].x, rr);
-              wr = fma(w[c].x, rnB[c].x, wr);
-              xbase[c * N + xo] = xn.x;
-              rout[c * ps + ro] = rnB[c].x;
-              pout[c * ps + ro] = pnA[c].x;
-            }
-            if (on1) {
-              rr = fma(rnB[c].y, rnB[c].y, rr);
-              wr = fma(w[c].y, rnB[c].y, wr);
-              xbase[c * N + xo + 1] = xn.y;
-              rout[c * ps + ro + 1] = rnB[c].y;
-              pout[c * ps + ro + 1] = pnA[c].y;
-            }
-          }
-        }
-      }
-#pragma unroll
-      for (int c = 0; c < K; ++c) {
-        rnA[c] = rnB[c];
-        rnB[c] = rnC[c];
-      }
-    }
-#pragma unroll
-    for (int c = 0; c < K; ++c) {
-      pnA[c] = pnB[c];
-      pnB[c] = pnC[c];
-      rprev[c] = rcur[c];
-    }
-  }
-  rr = warp_sum(rr);
-  wr = warp_sum(wr);
-  if (lane == 0) {
-    part_out[0] = rr;
-    part_out[1] = wr;
-  }
-}
-
-template <int K, bool HITS>
-__global__ void __launch_bounds__(32 * march_warps(K), 1) cg_march_kernel(const CgArgs a, const __grid_constant__ CgMaps maps) {
-  constexpr int BW = 64, TY = MARCH_TY, BR = TY + 4, CR = march_cr(K), NB = march_nb(K), W = march_warps(K);
-  constexpr int NCH = BR / CR;
-  constexpr int CHUNK = 2 * K * CR * BW;
-  extern __shared__ __align__(128) unsigned char smem_raw[];
-  double* ring_all = reinterpret_cast<double*>(smem_raw);
-  SysState* st = reinterpret_cast<SysState*>(smem_raw + (size_t)W * NB * CHUNK * 8);
-  int* act = reinterpret_cast<int*>(st + a.n_sys);
-  __shared__ __align__(8) uint64_t mbar[W * NB];
-  __shared__ double Msh[W][KCG_KMAX * KCG_KMAX + KCG_KMAX];
-  __shared__ double red[2][32];
-  __shared__ int s_nact;
-
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int tps = a.tiles_per_sys;
-  const int gwarp = blockIdx.x * W + warp, nwarps_total = gridDim.x * W;
-  cg::grid_group grid = cg::this_grid();
-
-  for (int s = tid; s < a.n_sys; s += blockDim.x) {
-    SysState z;
-    z.bnorm2 = 0.0; z.gamma = 0.0; z.alpha = 0.0; z.beta = 0.0; z.rel = 1.0;
-    z.iters = 0; z.status = ST_RUNNING; z.parity = 0; z.pad = 0;
-    st[s] = z;
-  }
-  if (tid < W * NB) mbar_init(&mbar[tid], 1);
-  if (tid == 0) fence_mbar_init();
-  __syncthreads();
-
-  MarchWarp mw;
-  mw.bar = &mbar[warp * NB];
-  mw.ring = ring_all + (size_t)warp * NB * CHUNK;
-  mw.seq = 0;
-  int it = -1;
-
-  while (true) {
-    if (tid == 0) {
-      int n = 0;
-      for (int s = 0; s < a.n_sys; ++s)
-        if (st[s].status == ST_RUNNING) act[n++] = s;
-      s_nact = n;
-    }
-    __syncthreads();
-    const int nact = s_nact;
-    if (nact == 0) break;
-    const int ntiles = nact * tps;
-    const int par_out = (it + 1) & 1;
-    const int my_tiles = gwarp < ntiles ? (ntiles - gwarp + nwarps_total - 1) / nwarps_total : 0;
-    const int total_chunks = my_tiles * NCH;
-    int issued = 0;
-    for (int i = 0; i < my_tiles; ++i) {
-      const int t = gwarp + i * nwarps_total;
-      const int s = act[t / tps];
-      const int tile = t - (t / tps) * tps;
-      const int ty = tile / a.tiles_x, tx = tile - ty * a.tiles_x;
-      const SysParams* sp = a.params + s;
-      for (int e = lane; e < K * K; e += 32) Msh[warp][e] = __ldg(&sp->M[e]);
-      if (lane < K) Msh[warp][K * K + lane] = __ldg(&sp->tau[lane]);
-      __syncwarp();
-      const int y0 = ty * TY, x0 = tx * MARCH_TX;
-      const double* hp = HITS ? a.hits + (size_t)__ldg(&sp->hits_plane) * ((size_t)a.side * a.side) : nullptr;
-      double* part = a.partials + (((size_t)par_out * a.n_sys + s) * tps + tile) * 2;
-      const bool interior = x0 >= 2 && x0 + MARCH_TX + 2 <= a.side && y0 >= 2 && y0 + TY + 2 <= a.side;
-      if (interior)
-        march_tile<K, false, HITS>(a, maps, mw, Msh[warp], s, y0, x0, st[s].parity, st[s].alpha, st[s].beta,
-                                   __ldg(&sp->kappa2), hp, part, lane, issued, total_chunks, i * NCH, act, st, tps,
-                                   gwarp, nwarps_total);
-      else
-        march_tile<K, true, HITS>(a, maps, mw, Msh[warp], s, y0, x0, st[s].parity, st[s].alpha, st[s].beta,
-                                  __ldg(&sp->kappa2), hp, part, lane, issued, total_chunks, i * NCH, act, st, tps,
-                                  gwarp, nwarps_total);
-      __syncwarp();
-    }
-    mw.seq += total_chunks;
-
-    fence_proxy_async_global();
-    grid.sync();
-    fence_proxy_async_global();
-
-    reduce_update_systems<32 * W>(a, st, act, nact, par_out, it, red);
-    if (blockIdx.x == 0 && tid == 0 && it >= 0 && it < a.history_cap) {
-      double m = 0.0;
-      for (int ii = 0; ii < nact; ++ii) m = fmax(m, st[act[ii]].rel);
-      a.history[it] = m;
-    }
-    ++it;
-  }
-  if (blockIdx.x == 0)
-    for (int s = tid; s < a.n_sys; s += blockDim.x) a.state_out[s] = st[s];
 }
 
 // --------------------------------------------------------------------------- apply / residual
@@ -1068,6 +920,27 @@ __global__ void __launch_bounds__(256) reduce_pairs_kernel(const double* __restr
   }
 }
 
+// --------------------------------------------------------------------------- X2 fix-up
+// x += alpha_last p for every system whose last pass left its x increment pending (odd `iters`,
+// KCG_X2); p = the system's current p planes (buffer `parity`, row pitch `pitch`).
+template <int K>
+__global__ void __launch_bounds__(256) xfix_kernel(const SysState* __restrict__ st, const double* __restrict__ p0,
+                                                   const double* __restrict__ p1, double* __restrict__ x, int side,
+                                                   int pitch) {
+  const int s = blockIdx.y;
+  const SysState z = st[s];
+  if (!KCG_X2 || (z.iters & 1) == 0) return;
+  const double al = z.alpha_last;
+  const double* p = (z.parity ? p1 : p0) + (size_t)s * K * pitch * side;
+  double* xs = x + (size_t)s * K * side * side;
+  const size_t N = (size_t)side * side;
+  for (size_t j = (size_t)blockIdx.x * blockDim.x + threadIdx.x; j < N; j += (size_t)gridDim.x * blockDim.x) {
+    const size_t gy = j / side, gx = j - gy * side;
+#pragma unroll
+    for (int c = 0; c < K; ++c) xs[c * N + j] = fma(al, p[(size_t)c * pitch * side + gy * pitch + gx], xs[c * N + j]);
+  }
+}
+
 // --------------------------------------------------------------------------- back-transform
 // x[p][c][j] = sum_i W[p][c][i] xt[p][i][j]   (X = Xt W^T), in place.
 template <int K>
@@ -1158,42 +1031,6 @@ cudaError_t launch_cg(int K, cudaStream_t s, const CgArgs& a, const CgMaps& m, i
   return cudaErrorInvalidValue;
 }
 
-template <int K, bool HITS>
-static cudaError_t march_config_t(int n_sys, int* max_grid, size_t* smem) {
-  const size_t sm = (size_t)march_warps(K) * march_nb(K) * march_chunk_bytes(K) +
-                    (size_t)n_sys * (sizeof(SysState) + sizeof(int));
-  cudaError_t e = cudaFuncSetAttribute(cg_march_kernel<K, HITS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-  if (e != cudaSuccess) return e;
-  int nb = 0, dev = 0, nsm = 0;
-  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, cg_march_kernel<K, HITS>, 32 * march_warps(K), sm);
-  if (e != cudaSuccess) return e;
-  e = cudaGetDevice(&dev);
-  if (e != cudaSuccess) return e;
-  e = cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-  if (e != cudaSuccess) return e;
-  *max_grid = nb * nsm;
-  *smem = sm;
-  return nb > 0 ? cudaSuccess : cudaErrorInvalidConfiguration;
-}
-
-cudaError_t march_kernel_config(int K, bool hits, int n_sys, int* max_grid, size_t* smem) {
-  if (hits) { KCG_DISPATCH(K, return (march_config_t<KK, true>(n_sys, max_grid, smem))); }
-  else { KCG_DISPATCH(K, return (march_config_t<KK, false>(n_sys, max_grid, smem))); }
-  return cudaErrorInvalidValue;
-}
-
-cudaError_t launch_march(int K, cudaStream_t s, const CgArgs& a, const CgMaps& m, int grid, size_t smem) {
-  void* args[2] = {(void*)&a, (void*)&m};
-  if (a.hits) {
-    KCG_DISPATCH(K, return cudaLaunchCooperativeKernel((const void*)cg_march_kernel<KK, true>, dim3(grid),
-                                                        dim3(32 * march_warps(KK)), args, smem, s));
-  } else {
-    KCG_DISPATCH(K, return cudaLaunchCooperativeKernel((const void*)cg_march_kernel<KK, false>, dim3(grid),
-                                                        dim3(32 * march_warps(KK)), args, smem, s));
-  }
-  return cudaErrorInvalidValue;
-}
-
 template <int K, bool R>
 static cudaError_t apply_t(cudaStream_t s, const SysParams* params, const double* x, double* y, const double* Y,
                            const double* E, const double* hits, double* partials, int n_sys, int n, int side) {
@@ -1218,6 +1055,14 @@ cudaError_t launch_resid(int K, cudaStream_t s, const SysParams* params, const d
   KCG_DISPATCH(K, e = (apply_t<KK, true>(s, params, x, nullptr, Y, E, hits, partials, n_sys, n, side)));
   if (e != cudaSuccess) return e;
   reduce_pairs_kernel<<<n_sys, 256, 0, s>>>(partials, out, apply_tiles_per_sys(side));
+  return cudaGetLastError();
+}
+
+cudaError_t launch_xfix(int K, cudaStream_t s, const SysState* st, const double* p0, const double* p1, double* x,
+                        int n_sys, int side, int pitch) {
+  const size_t N = (size_t)side * side;
+  dim3 g(grid_for(N), n_sys);
+  KCG_DISPATCH(K, (xfix_kernel<KK><<<g, 256, 0, s>>>(st, p0, p1, x, side, pitch)));
   return cudaGetLastError();
 }
 

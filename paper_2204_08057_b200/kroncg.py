@@ -245,6 +245,15 @@ class KronCG:
             raise self._err(st)
         return rho, W
 
+    def launch_config(self) -> dict:
+        """Diagnostic: CG-kernel grid / dynamic smem per route and the device SM count
+        (kcg_debug_config, not part of the ABI header)."""
+        f = _lib.kcg_debug_config
+        f.restype, f.argtypes = C.c_int, [_ctxp, C.c_void_p]
+        out = (C.c_longlong * 5)()
+        f(self._ctx, out)
+        return dict(grid_kron=out[0], grid_syl=out[1], smem_kron=out[2], smem_syl=out[3], sm_count=out[4])
+
     def close(self):
         if getattr(self, "_ctx", None) is not None and self._ctx.value:
             kron_cg_destroy(self._ctx)

@@ -6,11 +6,8 @@ sys.path.insert(0, ROOT)
 from paper_2204_08057_b200 import build
 
 VARIANTS = {
-    "v10_default": [],
-    "v10_v7cfg": ["KCG_TY4=16", "KCG_NT4=512", "KCG_XTMA_MAXK=3"],
-    "v10_v7cfg_ty1_32": ["KCG_TY4=16", "KCG_NT4=512", "KCG_XTMA_MAXK=3", "KCG_TY1=32"],
-    "v10_trace": ["KCG_TRACE=1"],
-    "v10_trace_v7cfg": ["KCG_TRACE=1", "KCG_TY4=16", "KCG_NT4=512", "KCG_XTMA_MAXK=3"],
+    "xpf": [],
+    "noxpf": ["KCG_XPF=0"],
 }
 names = sys.argv[1:] or list(VARIANTS)
 out = os.path.join(ROOT, "paper_2204_08057_b200", "lib", "variants")

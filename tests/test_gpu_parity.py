@@ -224,3 +224,17 @@ def test_routes_agree():
     a, _ = ctx.solve(Y, tol=TOL)
     b, _ = ctx.sylvester(Y, tol=TOL)
     assert rel(_np(a), _np(b)) <= 1e-8
+
+
+def test_launch_occupancy():
+    """The persistent kernel runs one CTA per SM for K=4 and two per SM for the K=1 Sylvester
+    systems, also at the full-sky batch of 12 faces x 4 columns (shared-memory budget)."""
+    from paper_2204_08057_b200 import build
+    build.build()
+    from paper_2204_08057_b200.kroncg import KronCG
+    rng = np.random.default_rng(0)
+    P, n, k = 12, 9, 4
+    ctx = KronCG(10, rng.uniform(0.5, 1.5, (P, n, k)), np.ones((P, n)), np.ones((P, k)), np.full(P, 0.1))
+    cfg = ctx.launch_config()
+    assert cfg["grid_kron"] == cfg["sm_count"], cfg
+    assert cfg["grid_syl"] == 2 * cfg["sm_count"], cfg
