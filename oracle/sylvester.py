@@ -53,7 +53,9 @@ def small_factor(A, noise_prec, tau):
 
 
 def solve(level, A, noise_prec, tau, kappa2, Y, hits=None, prior="laplacian",
-          tol=1e-10, max_iter=100000) -> SylvesterResult:
+          tol=1e-10, max_iter=100000, precond=None) -> SylvesterResult:
+    """precond=None (the paper's CG) or "jacobi": z = r / diag(Q0 + rho_i N_h) -- the k = 1 case of
+    the pixel-block Jacobi option (reading R10)."""
     A = np.asarray(A, dtype=np.float64)
     n, k = A.shape
     N = grid.side_of(level) ** 2
@@ -67,7 +69,11 @@ def solve(level, A, noise_prec, tau, kappa2, Y, hits=None, prior="laplacian",
     its, rels, ok = [], [], True
     for i in range(k):
         H = (Q0 + rho[i] * sp.diags(h)).tocsr()      # (Q0 + rho_i N_h)
-        res = cg_mod.cg_hs(H, Ft[:, i], tol=tol, max_iter=max_iter)
+        pc = None
+        if precond == "jacobi":
+            dH = H.diagonal().copy()
+            pc = lambda r, dH=dH: r / dH
+        res = cg_mod.cg_hs(H, Ft[:, i], tol=tol, max_iter=max_iter, precond=pc)
         Xt[:, i] = res.x
         its.append(res.iterations)
         rels.append(res.rel_residual)
@@ -76,6 +82,6 @@ def solve(level, A, noise_prec, tau, kappa2, Y, hits=None, prior="laplacian",
     return SylvesterResult(X.T.reshape(-1).copy(), its, ok, rho, W, rels)
 
 
-def problem_solve(p, tol=1e-10, max_iter=100000) -> SylvesterResult:
+def problem_solve(p, tol=1e-10, max_iter=100000, precond=None) -> SylvesterResult:
     return solve(p.level, p.A, p.noise_prec, p.tau, p.kappa2, p.Y, p.hits, p.prior,
-                 tol=tol, max_iter=max_iter)
+                 tol=tol, max_iter=max_iter, precond=precond)

@@ -82,7 +82,11 @@ bool desc_ok(const kcg_desc* d, std::string* why) {
 bool config_ok(const kcg_desc* d, std::string* why) {
   if (d->prior != KCG_PRIOR_LAPLACIAN) { *why = "only KCG_PRIOR_LAPLACIAN is built"; return false; }
   if (d->layout != KCG_LAYOUT_ROW_MAJOR) { *why = "only KCG_LAYOUT_ROW_MAJOR is built"; return false; }
-  if (d->precond != KCG_PRECOND_NONE) { *why = "only KCG_PRECOND_NONE is built"; return false; }
+  if (d->precond != KCG_PRECOND_NONE && d->precond != KCG_PRECOND_BLOCK_JACOBI) { *why = "unknown precond"; return false; }
+  if (d->precond == KCG_PRECOND_BLOCK_JACOBI && d->n_comp > 7) {
+    *why = "KCG_PRECOND_BLOCK_JACOBI is built for n_comp <= 7 (shared-memory budget)";
+    return false;
+  }
   return true;
 }
 
@@ -99,7 +103,7 @@ Layout layout_of(const kcg_desc* d) {
   L.vec_doubles = P * k * (size_t)pitch * side;
   const size_t tk = (size_t)tiles_x(side, (int)k) * tiles_y(side, (int)k);
   const size_t ts = (size_t)tiles_x(side, 1) * tiles_y(side, 1);
-  L.partial_doubles = 2 * std::max(P * tk, P * k * ts) * 2;
+  L.partial_doubles = 2 * std::max(P * tk, P * k * ts) * 3;  // [2 parities][systems][tiles][<= 3]
   size_t off = 0;
   auto take = [&](size_t bytes) { size_t o = off; off += align_up(bytes); return o; };
   L.r0 = take(L.vec_doubles * 8);
@@ -163,6 +167,44 @@ void jacobi_eig(int k, std::vector<double> C, std::vector<double>* lam, std::vec
   }
   lam->resize(k);
   for (int i = 0; i < k; ++i) (*lam)[i] = C[i * k + i];
+}
+
+// Inverse of a small SPD matrix (Gauss-Jordan with partial pivoting; k <= 8).
+void small_inverse(int k, const double* A, double* Ainv) {
+  std::vector<double> T((size_t)k * 2 * k, 0.0);
+  for (int i = 0; i < k; ++i) {
+    for (int j = 0; j < k; ++j) T[i * 2 * k + j] = A[i * k + j];
+    T[i * 2 * k + k + i] = 1.0;
+  }
+  for (int c = 0; c < k; ++c) {
+    int piv = c;
+    for (int i = c + 1; i < k; ++i)
+      if (std::fabs(T[i * 2 * k + c]) > std::fabs(T[piv * 2 * k + c])) piv = i;
+    if (piv != c)
+      for (int j = 0; j < 2 * k; ++j) std::swap(T[c * 2 * k + j], T[piv * 2 * k + j]);
+    const double inv = 1.0 / T[c * 2 * k + c];
+    for (int j = 0; j < 2 * k; ++j) T[c * 2 * k + j] *= inv;
+    for (int i = 0; i < k; ++i)
+      if (i != c) {
+        const double f = T[i * 2 * k + c];
+        for (int j = 0; j < 2 * k; ++j) T[i * 2 * k + j] -= f * T[c * 2 * k + j];
+      }
+  }
+  for (int i = 0; i < k; ++i)
+    for (int j = 0; j < k; ++j) Ainv[i * k + j] = T[i * 2 * k + k + j];
+}
+
+// Pixel-block Jacobi blocks for hits = 1 (reading R10): Kinv_d = (M + (kappa2 + d) diag(tau))^{-1},
+// d = 2, 3, 4, stored compactly (K x K each) in sp.Kinv.
+void set_block_jacobi(int K, const double* M, const double* tau, double kappa2, SysParams* sp) {
+  std::vector<double> A((size_t)K * K), Ai((size_t)K * K);
+  double* out = &sp->Kinv[0][0];
+  for (int d = 2; d <= 4; ++d) {
+    for (int i = 0; i < K; ++i)
+      for (int j = 0; j < K; ++j) A[i * K + j] = M[i * K + j] + (i == j ? (kappa2 + d) * tau[i] : 0.0);
+    small_inverse(K, A.data(), Ai.data());
+    for (int e = 0; e < K * K; ++e) out[(d - 2) * K * K + e] = Ai[e];
+  }
 }
 
 // Lemma 2: M W = P W diag(rho), W^T P W = I, rho ascending, largest-|.| entry of each
@@ -292,6 +334,9 @@ kcg_status solve_impl(kcg_ctx* c, Route route, const double* Y_in, double* mu_ou
   a.hits = c->hits;
   a.side = side;
   a.pitch = c->pitch;
+  a.rows = side;
+  a.row0 = 0;
+  a.ghost = 0;
   a.n_sys = kron ? P : P * k;
   a.tiles_x = kron ? c->tiles_x_kron : c->tiles_x_syl;
   a.tiles_y = kron ? c->tiles_y_kron : c->tiles_y_syl;
@@ -309,7 +354,8 @@ kcg_status solve_impl(kcg_ctx* c, Route route, const double* Y_in, double* mu_ou
     if (!encode_xmap(&maps.x, mu, side, (size_t)P * k, Kk, &why)) { c->err = why; return KCG_E_CUDA; }
     a.x_tma = 1;
   }
-  CK(kcg::launch_cg(Kk, s, a, maps, kron ? c->grid_kron : c->grid_syl, kron ? c->smem_kron : c->smem_syl),
+  CK(kcg::launch_cg(Kk, c->d.precond == KCG_PRECOND_BLOCK_JACOBI, s, a, maps, kron ? c->grid_kron : c->grid_syl,
+                    kron ? c->smem_kron : c->smem_syl),
      "cg kernel");
   CK(cudaEventRecord(c->ev[2], s), "event");
   if (KCG_X2) CK(kcg::launch_xfix(Kk, s, c->state, c->p[0], c->p[1], mu, a.n_sys, side, c->pitch), "x fix-up kernel");
@@ -480,6 +526,7 @@ kcg_status kron_cg_create(const kcg_desc* d, const double* A_host, const double*
     for (int a = 0; a < k; ++a) sk.tau[a] = phi[a];
     sk.kappa2 = kappa2_host[p];
     sk.hits_plane = p;
+    set_block_jacobi(k, M.data(), phi, kappa2_host[p], &sk);
     for (int i = 0; i < k; ++i) {
       SysParams& sy = ps[(size_t)p * k + i];
       std::memset(&sy, 0, sizeof sy);
@@ -487,6 +534,7 @@ kcg_status kron_cg_create(const kcg_desc* d, const double* A_host, const double*
       sy.tau[0] = 1.0;
       sy.kappa2 = kappa2_host[p];
       sy.hits_plane = p;
+      set_block_jacobi(1, sy.M, sy.tau, sy.kappa2, &sy);
     }
   }
   kcg_status st;
@@ -521,10 +569,11 @@ kcg_status kron_cg_create(const kcg_desc* d, const double* A_host, const double*
   c->tiles_x_syl = tiles_x(c->side, 1);
   c->tiles_y_syl = tiles_y(c->side, 1);
   int mg = 0;
-  CKC(kcg::cg_kernel_config(k, hits_dev != nullptr, P, &mg, &c->smem_kron),
+  const bool prec = d->precond == KCG_PRECOND_BLOCK_JACOBI;
+  CKC(kcg::cg_kernel_config(k, hits_dev != nullptr, prec, P, &mg, &c->smem_kron),
       "cg kernel config (kron)");
   c->grid_kron = std::max(1, std::min(mg, P * c->tiles_x_kron * c->tiles_y_kron));
-  CKC(kcg::cg_kernel_config(1, hits_dev != nullptr, P * k, &mg, &c->smem_syl),
+  CKC(kcg::cg_kernel_config(1, hits_dev != nullptr, prec, P * k, &mg, &c->smem_syl),
       "cg kernel config (sylvester)");
   c->grid_syl = std::max(1, std::min(mg, P * k * c->tiles_x_syl * c->tiles_y_syl));
   for (int i = 0; i < 4; ++i) CKC(cudaEventCreate(&c->ev[i]), "event create");
@@ -589,6 +638,30 @@ const char* kcg_status_string(int s) {
     case KCG_E_STATE: return "KCG_E_STATE";
     default: return "KCG_UNKNOWN";
   }
+}
+
+// Diagnostic (not part of the ABI header): the per-system CG state after the last solve, as
+// doubles {bnorm2, gamma, alpha, beta, rel, iters, status, parity, alpha_last} per system.
+KCG_API int kcg_debug_state(const kcg_ctx* c, double* out, int max_sys) {
+  if (!c || !out) return 0;
+  const int n = std::min(max_sys, (int)c->st_host.size());
+  for (int i = 0; i < n; ++i) {
+    const SysState& z = c->st_host[i];
+    double* o = out + 9 * i;
+    o[0] = z.bnorm2; o[1] = z.gamma; o[2] = z.alpha; o[3] = z.beta; o[4] = z.rel;
+    o[5] = z.iters; o[6] = z.status; o[7] = z.parity; o[8] = z.alpha_last;
+  }
+  return n;
+}
+
+// Diagnostic (not part of the ABI header): copy the device SysParams array of a route (0 kron,
+// 1 sylvester) into out (at most max_bytes); returns sizeof(SysParams).
+KCG_API int kcg_debug_params(const kcg_ctx* c, int route, void* out, size_t max_bytes) {
+  if (!c || !out) return 0;
+  const size_t n = route == 0 ? (size_t)c->P : (size_t)c->P * c->k;
+  cudaMemcpy(out, route == 0 ? c->params_kron : c->params_syl, std::min(max_bytes, n * sizeof(SysParams)),
+             cudaMemcpyDeviceToHost);
+  return (int)sizeof(SysParams);
 }
 
 // Diagnostic (not part of the ABI header): launch configuration of the CG kernel per route:

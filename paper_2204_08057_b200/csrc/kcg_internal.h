@@ -35,9 +35,6 @@ namespace kcg {
 #ifndef KCG_SERP
 #define KCG_SERP 1          // serpentine tile order across passes (L2 reuse when the state fits)
 #endif
-#ifndef KCG_ONEBAR
-#define KCG_ONEBAR 0        // single-barrier last-arriver reduction (else 2 grid.sync per pass)
-#endif
 #ifndef KCG_RED_MAX
 #define KCG_RED_MAX 4096    // redundant per-CTA reduction when active systems x tiles <= this
 #endif
@@ -50,12 +47,6 @@ namespace kcg {
 #ifndef KCG_X2
 #define KCG_X2 1            // update x every other pass (x += a_{q-1} p_{q-1} + a_q p_q): 40kN B/iter
 #endif
-#ifndef KCG_DEFER
-#define KCG_DEFER 1         // defer the CTA sum of a tile's partials to the next barrier
-#endif
-#ifndef KCG_M_IN_REGS
-#define KCG_M_IN_REGS 0     // keep the K x K mixing block in registers (else read from shared)
-#endif
 __host__ __device__ constexpr int cg_tile_y(int K) { return K == 1 ? KCG_TY1 : (K <= 3 ? 16 : (K == 4 ? KCG_TY4 : 8)); }
 __host__ __device__ constexpr int cg_threads(int K) { return K == 1 ? 256 : (K <= 3 ? 512 : (K == 4 ? KCG_NT4 : 256)); }
 __host__ __device__ constexpr int cg_stages(int K) { return 2; }
@@ -66,6 +57,8 @@ __host__ __device__ constexpr int cg_min_blocks(int K) { return K == 1 ? 2 : (K 
 __host__ __device__ constexpr bool cg_xtma(int K) { return K <= KCG_XTMA_MAXK && K <= 6; }  // K>=7: smem
 // Bytes of the x block staged with a tile.
 __host__ __device__ constexpr int cg_xstage_bytes(int K) { return cg_xtma(K) ? K * cg_tile_y(K) * KCG_TX * 8 : 0; }
+// Bytes of the preconditioner's u box (tile + 1-pixel ring, K planes, row pitch TX + 4).
+__host__ __device__ constexpr int cg_ubox_bytes(int K) { return K * (cg_tile_y(K) + 2) * (KCG_TX + 2 * KCG_HALO) * 8; }
 // Bytes of one pipeline stage (r and p boxes with halo, K planes, + x block).
 __host__ __device__ constexpr int cg_stage_bytes(int K) {
   return 2 * K * (cg_tile_y(K) + 2 * KCG_HALO) * (KCG_TX + 2 * KCG_HALO) * 8 + cg_xstage_bytes(K);
@@ -79,6 +72,9 @@ struct SysParams {
   double tau[KCG_KMAX];
   double kappa2;
   double hits_plane;              // index of the hits plane (patch) as a double (exact)
+  // pixel-block Jacobi (hits = 1): inverses of M + (kappa2 + d) diag(tau) for degree d = 2, 3, 4,
+  // each row-major K x K, stored compactly one after the other (Kinv[0][0 .. 3 K K))
+  double Kinv[3][KCG_KMAX * KCG_KMAX];
 };
 
 // Per-system iteration state (kept redundantly in every CTA's shared memory).
@@ -108,11 +104,13 @@ struct CgArgs {
   const double* hits;        // [P][side][side] or nullptr
   int history_cap;
   int side, pitch;
+  int rows, row0, ghost;     // local slab rows, global face row of local row 0, ghost rows of r/p
+                             // buffers above and below (row-slab mode; else side, 0, 0)
   int n_sys, tiles_x, tiles_y, tiles_per_sys;
   int max_iter;
   int x_tma;                 // 1: CgMaps::x describes `x` (TMA needs side >= 2): staged (K <= 3) or L2-prefetched
   long long* trace;          // KCG_TRACE builds only: per-iteration %globaltimer stamps
-  unsigned* sync;            // [0] arrival counter, [1] generation flag, [2..3] tile claims (zeroed per launch)
+  unsigned* sync;            // [2..3] tile-claim counters of the two pass parities (zeroed per launch)
   double tol2;
 };
 
@@ -126,8 +124,8 @@ struct CgMaps {              // TMA descriptors of rbuf[0..1], pbuf[0..1] (box =
 // All return cudaError_t of the launch.
 cudaError_t launch_rhs(int K, cudaStream_t s, const double* Y, const double* E, const double* hits,
                        double* r0, double* p0, double* x, int P, int n, int side, int pitch);
-cudaError_t launch_cg(int K, cudaStream_t s, const CgArgs& a, const CgMaps& m, int grid, size_t smem);
-cudaError_t cg_kernel_config(int K, bool hits, int n_sys, int* max_grid, size_t* smem);
+cudaError_t launch_cg(int K, bool prec, cudaStream_t s, const CgArgs& a, const CgMaps& m, int grid, size_t smem);
+cudaError_t cg_kernel_config(int K, bool hits, bool prec, int n_sys, int* max_grid, size_t* smem);
 cudaError_t launch_apply(int K, cudaStream_t s, const SysParams* params, const double* x, double* y,
                          const double* hits, int n_sys, int side);
 cudaError_t launch_resid(int K, cudaStream_t s, const SysParams* params, const double* x,

@@ -120,31 +120,33 @@ __global__ void __launch_bounds__(256) rhs_kernel(const double* __restrict__ Y, 
 }
 
 // --------------------------------------------------------------------------- CG scalar update
-// One CG scalar step for a system from its reduced partials (r,r) and (w,r) (Chronopoulos-Gear):
-// the start pass (it < 0) gives ||b||^2 and alpha_0 = (b,b)/(Gb,b); afterwards
-// beta = gamma'/gamma, alpha = gamma'/(delta - beta gamma'/alpha); stop on ||r|| <= tol ||b||.
-__device__ __forceinline__ SysState cg_update(SysState z, double rr, double wr, int it, const CgArgs& a) {
+// One CG scalar step for a system from its reduced partials (Chronopoulos-Gear, preconditioned
+// form of oracle/cg.py cg_single_pass): rr = (r,r), ru = (r,u), wu = (w,u) with u = K^{-1} r,
+// w = G u (u = r, ru = rr without a preconditioner).  The start pass (it < 0) gives ||b||^2,
+// gamma_0 = (b,u_0) and alpha_0 = gamma_0/delta_0; afterwards beta = gamma'/gamma,
+// alpha = gamma'/(delta - beta gamma'/alpha); stop on ||r|| <= tol ||b|| (reading R8).
+__device__ __forceinline__ SysState cg_update(SysState z, double rr, double ru, double wu, int it, const CgArgs& a) {
   if (it < 0) {
     z.bnorm2 = rr;
-    z.gamma = rr;
+    z.gamma = ru;
     z.rel = rr > 0.0 ? 1.0 : 0.0;
-    if (!isfinite(rr) || !isfinite(wr)) z.status = ST_NONFINITE;
+    if (!isfinite(rr) || !isfinite(ru) || !isfinite(wu)) z.status = ST_NONFINITE;
     else if (rr == 0.0) z.status = ST_CONVERGED;
-    else if (!(wr > 0.0)) z.status = ST_BREAKDOWN;
+    else if (!(wu > 0.0) || !(ru > 0.0)) z.status = ST_BREAKDOWN;
     else if (a.max_iter <= 0) z.status = ST_MAXIT;
-    else { z.alpha = rr / wr; z.beta = 0.0; }
+    else { z.alpha = ru / wu; z.beta = 0.0; }
   } else {
     z.alpha_last = z.alpha;  // the step this pass used
     z.iters = it + 1;
     z.rel = sqrt(rr / z.bnorm2);
-    if (!isfinite(rr) || !isfinite(wr)) z.status = ST_NONFINITE;
+    if (!isfinite(rr) || !isfinite(ru) || !isfinite(wu)) z.status = ST_NONFINITE;
     else if (rr <= a.tol2 * z.bnorm2) z.status = ST_CONVERGED;
     else if (z.iters >= a.max_iter) z.status = ST_MAXIT;
     else {
-      const double beta = rr / z.gamma;
-      const double den = wr - beta * rr / z.alpha;
-      if (!(den > 0.0)) z.status = ST_BREAKDOWN;
-      else { z.beta = beta; z.alpha = rr / den; z.gamma = rr; }
+      const double beta = ru / z.gamma;
+      const double den = wu - beta * ru / z.alpha;
+      if (!(den > 0.0) || !(ru > 0.0)) z.status = ST_BREAKDOWN;
+      else { z.beta = beta; z.alpha = ru / den; z.gamma = ru; }
     }
   }
   z.parity ^= 1;
@@ -152,17 +154,34 @@ __device__ __forceinline__ SysState cg_update(SysState z, double rr, double wr, 
 }
 
 // ---------------------------------------------------------------------- per-iteration reduction
+// Tile partials: NP doubles per tile, (rr, wr) without a preconditioner, (rr, ru, wu) with one.
 // Canonical order of a system's reduction, used by every mode below so that the scalars -- and
 // hence the iterates -- are bitwise independent of the mode, the grid size and the batch
 // composition: slot t in [0, NT) sums the tile partials t, t+NT, t+2NT, ... in order; the slots of a
 // warp are combined by the xor-shuffle tree; the NW warp sums are added in warp order.
-#define KCG_RB 8  // systems reduced per CTA pass (shared slots [KCG_RB][2][NW])
+#define KCG_RB 8  // systems reduced per CTA pass (shared slots [KCG_RB][3][NW])
+
+template <int NP>
+__device__ __forceinline__ void load_partial(const double* base, int t, double (&v)[3]) {
+  if (NP == 2) {
+    const double2 d = __ldcg(reinterpret_cast<const double2*>(base) + t);
+    v[0] = d.x; v[1] = d.y; v[2] = 0.0;
+  } else {
+    v[0] = __ldcg(base + 3 * t); v[1] = __ldcg(base + 3 * t + 1); v[2] = __ldcg(base + 3 * t + 2);
+  }
+}
+
+// Scalar update from the NP reduced sums (without a preconditioner ru = rr, wu = wr).
+template <int NP>
+__device__ __forceinline__ SysState update_from(SysState z, const double (&v)[3], int it, const CgArgs& a) {
+  return NP == 2 ? cg_update(z, v[0], v[0], v[1], it, a) : cg_update(z, v[0], v[1], v[2], it, a);
+}
 
 // The CTA reduces systems act[ii], ii = ii0, ii0 + step, ... and applies the CG scalar update.
-// Results go to st_smem[s] (redundant mode: every CTA computes the same values) or a.state_out[s].
-template <int NT>
+// Results go to st[s] (redundant mode: every CTA computes the same values) or a.state_out[s].
+template <int NT, int NP>
 __device__ __forceinline__ void reduce_systems_cta(const CgArgs& a, SysState* st, const int* act, int nact, int ii0,
-                                                   int step, int par_out, int it, double (*rs)[2][NT / 32],
+                                                   int step, int par_out, int it, double (*rs)[3][NT / 32],
                                                    bool to_global) {
   constexpr int NW = NT / 32;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -174,24 +193,29 @@ __device__ __forceinline__ void reduce_systems_cta(const CgArgs& a, SysState* st
       const int ii = first + b * step;
       if (ii >= nact) break;
       const int s = act[ii];
-      const double2* base = reinterpret_cast<const double2*>(a.partials + ((size_t)par_out * a.n_sys + s) * tps * 2);
-      double rr = 0.0, wr = 0.0;
+      const double* base = a.partials + ((size_t)par_out * a.n_sys + s) * tps * NP;
+      double acc[3] = {0.0, 0.0, 0.0};
       for (int t = tid; t < tps; t += NT) {
-        const double2 v = __ldcg(base + t);
-        rr += v.x;
-        wr += v.y;
+        double v[3];
+        load_partial<NP>(base, t, v);
+#pragma unroll
+        for (int q = 0; q < NP; ++q) acc[q] += v[q];
       }
-      rr = warp_sum(rr);
-      wr = warp_sum(wr);
-      if (lane == 0) { rs[b][0][warp] = rr; rs[b][1][warp] = wr; }
+#pragma unroll
+      for (int q = 0; q < NP; ++q) {
+        acc[q] = warp_sum(acc[q]);
+        if (lane == 0) rs[b][q][warp] = acc[q];
+      }
       ++nb;
     }
     __syncthreads();
     if (tid < nb) {
       const int s = act[first + tid * step];
-      double r2 = 0.0, w2 = 0.0;
-      for (int w = 0; w < NW; ++w) { r2 += rs[tid][0][w]; w2 += rs[tid][1][w]; }
-      const SysState z = cg_update(st[s], r2, w2, it, a);
+      double v[3] = {0.0, 0.0, 0.0};
+      for (int w = 0; w < NW; ++w)
+#pragma unroll
+        for (int q = 0; q < NP; ++q) v[q] += rs[tid][q][w];
+      const SysState z = update_from<NP>(st[s], v, it, a);
       if (to_global) a.state_out[s] = z;
       else st[s] = z;
     }
@@ -221,151 +245,170 @@ __device__ __forceinline__ void pull_states(const CgArgs& a, SysState* st, const
   __syncthreads();
 }
 
-__device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
-  unsigned v;
-  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-  return v;
-}
-__device__ __forceinline__ void st_release_u32(unsigned* p, unsigned v) {
-  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
-}
-__device__ __forceinline__ void spin_until_geq(const unsigned* p, unsigned target) {
-  if (ld_acquire_u32(p) >= target) return;
-  const long long t0 = clock64();
-  while (ld_acquire_u32(p) < target) {
-    if (clock64() - t0 > (1LL << 34)) __trap();  // ~8 s: a lost arrival, never a legal wait
+// The iteration's barrier + reduction (both modes in the canonical order):
+//  REDUNDANT  (nact <= KCG_RB and nact*tps <= KCG_RED_MAX): one grid barrier, then every CTA reduces
+//             every active system itself -- no second barrier, no state broadcast.
+//  otherwise  grid barrier; CTA b reduces systems b, b+grid, ...; second grid barrier; pull.
+// `after_count` runs on thread 0 once every CTA's stores of the pass are visible (the speculative
+// TMA of the next pass).
+template <int NT, int NP, typename F>
+__device__ __forceinline__ void iteration_reduce(const CgArgs& a, SysState* st, const int* act, int nact,
+                                                 int par_out, int it, double (*rs)[3][NT / 32], F after_count) {
+  const bool small = nact <= KCG_RB && nact * a.tiles_per_sys <= KCG_RED_MAX;
+  fence_proxy_async_global();
+  cg::this_grid().sync();
+  fence_proxy_async_global();
+  if (threadIdx.x == 0) after_count();
+  if (small) {
+    reduce_systems_cta<NT, NP>(a, st, act, nact, 0, 1, par_out, it, rs, false);
+  } else {
+    reduce_systems_cta<NT, NP>(a, st, act, nact, blockIdx.x, gridDim.x, par_out, it, rs, true);
+    __threadfence();
+    cg::this_grid().sync();
+    pull_states<NT>(a, st, act, nact);
   }
 }
 
-// The iteration's barrier + reduction.  Modes (chosen per iteration, all in the canonical order):
-//  REDUNDANT  (nact <= KCG_RB and nact*tps <= KCG_RED_MAX): one grid barrier, then every CTA reduces
-//             every active system itself -- no second barrier, no state broadcast.
-//  ONEBAR     (KCG_ONEBAR): CTAs arrive on a monotonic counter a.sync[0]; the LAST to arrive reduces
-//             all systems, publishes the states and releases the generation flag a.sync[1].
-//  otherwise  grid barrier; CTA b reduces systems b, b+grid, ...; second grid barrier; pull.
-// a.sync is zeroed before each launch.  `after_count` runs on thread 0 once every CTA's stores of the pass are visible (the speculative
-// TMA of the next pass).
-template <int NT, typename F>
-__device__ __forceinline__ void iteration_reduce(const CgArgs& a, SysState* st, const int* act, int nact,
-                                                 int par_out, int it, double (*rs)[2][NT / 32], unsigned& epoch,
-                                                 F after_count) {
-  __shared__ int s_last;
-  const int tid = threadIdx.x;
-  const bool small = nact <= KCG_RB && nact * a.tiles_per_sys <= KCG_RED_MAX;
-  if (small || !KCG_ONEBAR) {
-    fence_proxy_async_global();
-    cg::this_grid().sync();
-    fence_proxy_async_global();
-    if (tid == 0) after_count();
-    if (small) {
-      reduce_systems_cta<NT>(a, st, act, nact, 0, 1, par_out, it, rs, false);
-    } else {
-      reduce_systems_cta<NT>(a, st, act, nact, blockIdx.x, gridDim.x, par_out, it, rs, true);
-      __threadfence();
-      cg::this_grid().sync();
-      pull_states<NT>(a, st, act, nact);
+// --------------------------------------------------------------------------- the operator
+// Per pixel j and plane c (G = M (x) N_h + P (x) (kappa2 I + L), Alg.MatvecD/MatvecQ/MatvecBCBT):
+//   (G v)_c(j) = h_j sum_d M[c][d] v_d(j) + tau_c ((kappa2 + deg_j) v_c(j) - sum_{nbr} v_c(nbr))
+// `nb` = the neighbour sum, `kd` = kappa2 + deg_j, `mix` = sum_d M[c][d] v_d(j).
+template <bool HITS>
+__device__ __forceinline__ double op_point(double h, double mix, double tau, double kd, double v, double nb) {
+  return HITS ? fma(h, mix, tau * fma(kd, v, -nb)) : fma(tau, fma(kd, v, -nb), mix);
+}
+
+// Pixel-block Jacobi (reading R10): u = K_j^{-1} r with K_j = h_j M + (kappa2 + deg_j) diag(tau),
+// the k x k diagonal block of G at pixel j.  hits = 1: the three inverses (deg 2, 3, 4) are
+// precomputed on the host (Kinv, shared); with hits K_j is factorised per pixel (Cholesky).
+template <int K, bool HITS>
+__device__ __forceinline__ void precond_pixel(const double* Kinv, const double* M,
+                                              const double* tau, double kappa2, double h, int deg,
+                                              const double (&r)[K], double (&u)[K]) {
+  if (!HITS) {
+    const double* Ki = Kinv + (deg - 2) * K * K;
+#pragma unroll
+    for (int c = 0; c < K; ++c) {
+      double v = 0.0;
+#pragma unroll
+      for (int d = 0; d < K; ++d) v = fma(Ki[c * K + d], r[d], v);
+      u[c] = v;
     }
-    return;
-  }
-  ++epoch;  // ONEBAR iterations so far (uniform across CTAs: the mode choice is)
-  const unsigned target = epoch * gridDim.x;
-  __syncthreads();  // every partial / state store of this CTA is issued
-  if (tid == 0) {
-    fence_proxy_async_global();
-    __threadfence();
-    const unsigned prev = atomicAdd(a.sync, 1u);
-    s_last = prev + 1 == target;
-    if (!s_last) spin_until_geq(a.sync, target);
-    __threadfence();
-    fence_proxy_async_global();
-    after_count();
-  }
-  __syncthreads();
-  if (s_last) {
-#if KCG_ONEBAR == 2
-    {  // EXPERIMENT: warp per system, lanes in order (not the canonical order)
-      constexpr int NW = NT / 32, U = 8;
-      const int lane = tid & 31, warp = tid >> 5, tps = a.tiles_per_sys;
-      for (int ii = warp; ii < nact; ii += NW) {
-        const int s = act[ii];
-        const double2* base = reinterpret_cast<const double2*>(a.partials + ((size_t)par_out * a.n_sys + s) * tps * 2);
-        double rr = 0.0, wr = 0.0;
-        for (int t0 = lane; t0 < tps; t0 += U * 32) {
-          double2 v[U];
+  } else {
+    double L[K][K];
+    const double kd = kappa2 + deg;
 #pragma unroll
-          for (int u = 0; u < U; ++u) v[u] = t0 + u * 32 < tps ? __ldcg(base + t0 + u * 32) : make_double2(0.0, 0.0);
+    for (int c = 0; c < K; ++c)
 #pragma unroll
-          for (int u = 0; u < U; ++u) { rr += v[u].x; wr += v[u].y; }
-        }
-        rr = warp_sum(rr);
-        wr = warp_sum(wr);
-        if (lane == 0) a.state_out[s] = cg_update(st[s], rr, wr, it, a);
+      for (int d = 0; d <= c; ++d) L[c][d] = fma(h, M[c * K + d], c == d ? kd * tau[c] : 0.0);
+#pragma unroll
+    for (int j = 0; j < K; ++j) {  // in-register Cholesky, K = L L^T
+      double dsum = L[j][j];
+#pragma unroll
+      for (int m = 0; m < j; ++m) dsum = fma(-L[j][m], L[j][m], dsum);
+      const double ljj = sqrt(dsum), inv = 1.0 / ljj;
+      L[j][j] = ljj;
+#pragma unroll
+      for (int i = j + 1; i < K; ++i) {
+        double v = L[i][j];
+#pragma unroll
+        for (int m = 0; m < j; ++m) v = fma(-L[i][m], L[j][m], v);
+        L[i][j] = v * inv;
       }
-      __syncthreads();
     }
-#else
-    reduce_systems_cta<NT>(a, st, act, nact, 0, 1, par_out, it, rs, true);
-#endif
-    if (tid == 0) {
-      __threadfence();
-      st_release_u32(a.sync + 1, epoch);
+    double y[K];
+#pragma unroll
+    for (int i = 0; i < K; ++i) {
+      double v = r[i];
+#pragma unroll
+      for (int m = 0; m < i; ++m) v = fma(-L[i][m], y[m], v);
+      y[i] = v / L[i][i];
     }
-  } else if (tid == 0) {
-    spin_until_geq(a.sync + 1, epoch);
+#pragma unroll
+    for (int i = K - 1; i >= 0; --i) {
+      double v = y[i];
+#pragma unroll
+      for (int m = i + 1; m < K; ++m) v = fma(-L[m][i], u[m], v);
+      u[i] = v / L[i][i];
+    }
   }
-  __syncthreads();
-  pull_states<NT>(a, st, act, nact);
 }
 
 // --------------------------------------------------------------------------- persistent CG
 // One tile of one system: box = tile + 2-pixel halo, K planes of r and p staged by TMA (zero fill
-// outside the face).  Warp w owns T rows w, w+NW, ...; lane l owns the pixel PAIR at tile columns
-// 2l, 2l+1 (double2 in shared and global memory); horizontal neighbours come from shuffles.
-//   Phase A  p_new = r + beta p                    whole box (elementwise)
-//   Phase B  q = G p_new, r_new = r - alpha q      T rows (pairs) + the 1-pixel ring (scalars)
-//   Phase C  w = G r_new on T; (r,r), (w,r); x += alpha p_new (+ alpha_prev p_old, X2)
-// x: with XTMA the tile's x block (64 x TY x K) is TMA-loaded into shared memory at the start of the
-// tile (consumed in phase C, so its latency hides behind phases A and B); x, r_new, p_new are
-// written back with coalesced 16-byte vector stores.
-// EDGE = the box touches the face border (bounds checks, degree 2/3); interior tiles skip both.
+// outside the face; in row-slab mode the rows beyond the slab are the ghost rows its neighbours
+// wrote).  Warp w owns tile rows w, w+NW, ...; lane l owns the pixel PAIR at tile columns 2l, 2l+1
+// (double2 in shared and global memory); horizontal neighbours come from shuffles.
+//   Phase A  p_new = u + beta p, u = K^{-1} r        whole box; interior pairs keep the x increment
+//   Phase B  q = G p_new, r_new = r - alpha q         tile rows (pairs) + the 1-pixel ring (scalars)
+//   Phase B' u_new = K^{-1} r_new on tile + ring      (PREC only, into the U box)
+//   Phase C  w = G u_new on the tile; (r,r), (r,u), (w,u); x += xinc on x passes; store r, p, x
+// Geometry: the tile origin (y0 local row of the slab, x0 column); global face row = a.row0 + local
+// row; the face is side x side; the slab holds a.rows local rows (= side without slabs).
+// EDGE = the box touches the face border or the slab end (bounds checks, degree 2/3).
 struct TileCtx {
   double* R;          // r box (stage)
   double* Pp;         // p box (stage)
+  double* U;          // PREC: u box [K][TY+2][BW] (tile + ring; shared by both stages)
   double* xs;         // x block of the tile in the stage [K][TY][TX] (XTMA)
-  const double* Ms;   // M (K*K) then tau (K) of this tile's system, shared
+  const double* Ms;   // M (K*K), tau (K), Kinv (3 K*K) of this tile's system, shared (valid after
+                      // the phase-A barrier: written at the top of the tile by other threads)
+  const SysParams* sp;  // the same parameters in global memory (read before that barrier)
   int s, y0, x0, par;
   bool xpass;         // this pass updates x (every pass without KCG_X2; even passes >= 2 with it)
   double alpha, beta, kappa2;
   double alpha_prev;  // X2: alpha of the previous pass (its p_new is this pass's p_old), else 0
-  const double* hp;   // hits plane or nullptr
+  const double* hp;   // hits plane (slab rows) or nullptr
   uint64_t* bar;      // stage mbarrier
   uint32_t phase;
   double* part_out;
+  double* dump;       // KCG_TRACE == 2 diagnostic builds: smem snapshots of one tile (else nullptr)
 };
 
-template <int K, bool EDGE, bool HITS, bool XTMA>
+// KCG_TRACE == 2: copy n doubles of shared memory to dst (all threads; barrier after)
+__device__ __forceinline__ void dump_smem(double* dst, const double* src, int n) {
+  if (dst)
+    for (int e0 = 0; e0 < n; e0 += blockDim.x)
+      if (e0 + (int)threadIdx.x < n) dst[e0 + threadIdx.x] = src[e0 + threadIdx.x];
+  __syncwarp();
+  __syncthreads();
+}
+
+template <int K, bool EDGE, bool HITS, bool XTMA, bool PREC>
 __device__ __forceinline__ void cg_tile(const CgArgs& a, const TileCtx& tc, double (*tred)[cg_threads(K) / 32]) {
   constexpr int TY = cg_tile_y(K), TX = KCG_TX, H = KCG_HALO;
   constexpr int BW = TX + 2 * H, BH = TY + 2 * H, PLANE = BW * BH;
+  constexpr int UPLANE = BW * (TY + 2);
   constexpr int NT = cg_threads(K), NW = NT / 32, RPW = TY / NW;
   constexpr int RP = 2 * (TX + 2) + 2 * TY;  // ring points
   static_assert(TX == 64 && RPW * NW == TY, "pair mapping needs TX = 64 and NW | TY");
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int side = a.side;
-  const size_t N = (size_t)side * side;
-  const size_t ps = (size_t)a.pitch * side;
+  const int side = a.side, rows = a.rows, row0 = a.row0;
+  const size_t N = (size_t)rows * side;                   // pixels of one local plane
+  const size_t ps = (size_t)a.pitch * (rows + 2 * a.ghost);  // one r/p buffer plane
   double* __restrict__ R = tc.R;
   double* __restrict__ Pp = tc.Pp;
   const int s = tc.s, y0 = tc.y0, x0 = tc.x0;
   const double alpha = tc.alpha, beta = tc.beta, kappa2 = tc.kappa2;
   const int gx = x0 + 2 * lane;
+  const double* __restrict__ M = tc.Ms;
+  const double* Mg = tc.sp->M;           // phase A (before the barrier): global copies
+  const double* Kinvg = &tc.sp->Kinv[0][0];
+  // degree of a pixel from its global face coordinates (free boundary, reading R2)
+  auto degree = [&](int gyg, int gxx) { return 4 - (gyg == 0) - (gyg == side - 1) - (gxx == 0) - (gxx == side - 1); };
+  auto in_face = [&](int gyg, int gxx) { return gyg >= 0 && gyg < side && gxx >= 0 && gxx < side; };
+  auto hit = [&](int ly, int gxx) { return HITS ? __ldg(tc.hp + (size_t)ly * side + gxx) : 1.0; };
 
   mbar_wait(tc.bar, tc.phase);
+  if (KCG_TRACE == 2) dump_smem(tc.dump, R, K * PLANE);
 
-  // Phase A: p_new = r + beta p over the whole box.  The tile interior is done in the pair
-  // mapping of phases B/C, so on x passes the thread keeps its pairs' x increment
-  //   xinc = alpha_prev p_old + alpha p_new   (X2: x is updated every other pass, see cg_update)
-  // in registers; the 2-pixel frame of the box is a flat loop over double2 units.
+  double tau[K];
+#pragma unroll
+  for (int c = 0; c < K; ++c) tau[c] = __ldg(&tc.sp->tau[c]);
+
+  // Phase A.  Interior pairs in the pair mapping (the thread keeps its pairs' x increment
+  //   xinc = alpha_prev p_old + alpha p_new   (X2: x is updated every other pass)
+  // in registers); the 2-pixel frame of the box as a flat loop over double2 units (pixel pairs).
   double2 xinc[RPW][K];
   {
     double2* P2 = reinterpret_cast<double2*>(Pp);
@@ -373,76 +416,103 @@ __device__ __forceinline__ void cg_tile(const CgArgs& a, const TileCtx& tc, doub
     const double ap = tc.alpha_prev;
 #pragma unroll
     for (int j = 0; j < RPW; ++j) {
-      const int ly = warp + j * NW + H;
+      const int ly = warp + j * NW;
+      const int e0 = ((ly + H) * BW + H) / 2 + lane;
+      double2 uu[K];
+#pragma unroll
+      for (int c = 0; c < K; ++c) uu[c] = R2[e0 + c * (PLANE / 2)];
+      if (PREC) {
+        const int gyg = row0 + y0 + ly;
+        const bool f0 = !EDGE || in_face(gyg, gx), f1 = !EDGE || in_face(gyg, gx + 1);
+        const int d0 = EDGE ? (f0 ? degree(gyg, gx) : 4) : 4, d1 = EDGE ? (f1 ? degree(gyg, gx + 1) : 4) : 4;
+        const double h0 = HITS && f0 ? hit(y0 + ly, gx) : 1.0, h1 = HITS && f1 ? hit(y0 + ly, gx + 1) : 1.0;
+        double r0[K], r1[K], u0[K], u1[K];
+#pragma unroll
+        for (int c = 0; c < K; ++c) { r0[c] = uu[c].x; r1[c] = uu[c].y; }
+        precond_pixel<K, HITS>(Kinvg, Mg, tau, kappa2, h0, d0, r0, u0);
+        precond_pixel<K, HITS>(Kinvg, Mg, tau, kappa2, h1, d1, r1, u1);
+#pragma unroll
+        for (int c = 0; c < K; ++c) uu[c] = make_double2(u0[c], u1[c]);
+      }
 #pragma unroll
       for (int c = 0; c < K; ++c) {
-        const int e = (c * PLANE + ly * BW + H) / 2 + lane;
-        const double2 r = R2[e], po = P2[e];
+        const int e = e0 + c * (PLANE / 2);
+        const double2 po = P2[e];
         double2 pn;
-        pn.x = fma(beta, po.x, r.x);
-        pn.y = fma(beta, po.y, r.y);
+        pn.x = fma(beta, po.x, uu[c].x);
+        pn.y = fma(beta, po.y, uu[c].y);
         P2[e] = pn;
         xinc[j][c].x = fma(alpha, pn.x, ap * po.x);
         xinc[j][c].y = fma(alpha, pn.y, ap * po.y);
       }
     }
     constexpr int FR = 4 * (BW / 2) + 2 * TY;  // frame double2 units per plane
-    for (int u = tid; u < K * FR; u += NT) {
-      const int c = u / FR, v = u - c * FR;
-      int e;
-      if (v < 4 * (BW / 2)) {
-        const int rr = v / (BW / 2);
-        e = (rr < 2 ? rr : BH - 4 + rr) * (BW / 2) + (v - rr * (BW / 2));
+    constexpr int NFR = PREC ? FR : K * FR;
+    // uniform trip count (every warp arrives converged at the barrier below)
+    for (int v0 = 0; v0 < NFR; v0 += NT) {
+      const int v = v0 + tid;
+      if (v >= NFR) continue;
+      const int c0 = PREC ? 0 : v / FR, w0 = PREC ? v : v - c0 * FR;
+      int by, bu;  // box row, double2 column unit
+      if (w0 < 4 * (BW / 2)) {
+        const int rr = w0 / (BW / 2);
+        by = rr < 2 ? rr : BH - 4 + rr;
+        bu = w0 - rr * (BW / 2);
       } else {
-        const int w = v - 4 * (BW / 2);
-        e = (H + (w >> 1)) * (BW / 2) + ((w & 1) ? BW / 2 - 1 : 0);
+        const int w = w0 - 4 * (BW / 2);
+        by = H + (w >> 1);
+        bu = (w & 1) ? BW / 2 - 1 : 0;
       }
-      e += c * (PLANE / 2);
-      const double2 r = R2[e], po = P2[e];
-      double2 pn;
-      pn.x = fma(beta, po.x, r.x);
-      pn.y = fma(beta, po.y, r.y);
-      P2[e] = pn;
+      const int e = by * (BW / 2) + bu;
+      if (!PREC) {
+        const double2 r = R2[e + c0 * (PLANE / 2)], po = P2[e + c0 * (PLANE / 2)];
+        P2[e + c0 * (PLANE / 2)] = make_double2(fma(beta, po.x, r.x), fma(beta, po.y, r.y));
+      } else {
+        const int gyg = row0 + y0 - H + by, gxx = x0 - H + 2 * bu;
+        const bool f0 = in_face(gyg, gxx), f1 = in_face(gyg, gxx + 1);
+        const int d0 = f0 ? degree(gyg, gxx) : 4, d1 = f1 ? degree(gyg, gxx + 1) : 4;
+        const double h0 = HITS && f0 ? hit(y0 - H + by, gxx) : 1.0, h1 = HITS && f1 ? hit(y0 - H + by, gxx + 1) : 1.0;
+        double r0[K], r1[K], u0[K], u1[K];
+#pragma unroll
+        for (int c = 0; c < K; ++c) {
+          const double2 r = R2[e + c * (PLANE / 2)];
+          r0[c] = r.x; r1[c] = r.y;
+        }
+        precond_pixel<K, HITS>(Kinvg, Mg, tau, kappa2, h0, d0, r0, u0);
+        precond_pixel<K, HITS>(Kinvg, Mg, tau, kappa2, h1, d1, r1, u1);
+#pragma unroll
+        for (int c = 0; c < K; ++c) {
+          const double2 po = P2[e + c * (PLANE / 2)];
+          P2[e + c * (PLANE / 2)] = make_double2(fma(beta, po.x, u0[c]), fma(beta, po.y, u1[c]));
+        }
+      }
     }
   }
+  __syncwarp();
   __syncthreads();
 
-#if KCG_M_IN_REGS
-  double M[K * K];
-#pragma unroll
-  for (int e = 0; e < K * K; ++e) M[e] = tc.Ms[e];
-#else
-  const double* M = tc.Ms;
-#endif
-  double tau[K];
-#pragma unroll
-  for (int c = 0; c < K; ++c) tau[c] = tc.Ms[K * K + c];
-
-  // Phase B1: T rows, pairs
+  // Phase B1: tile rows, pairs
 #pragma unroll
   for (int j = 0; j < RPW; ++j) {
-    const int gy = y0 + warp + j * NW;
-    const int ly = gy - y0 + H;
+    const int ly = warp + j * NW;            // local tile row
+    const int by = ly + H;                   // box row
+    const int gyg = row0 + y0 + ly;
     bool in0 = true, in1 = true;
     double kd0 = kappa2 + 4.0, kd1 = kappa2 + 4.0;
     if (EDGE) {
-      in0 = gy < side && gx < side;
-      in1 = gy < side && gx + 1 < side;
-      const double dy = (gy == 0) + (gy == side - 1);
-      kd0 = kappa2 + (4.0 - dy - (gx == 0) - (gx == side - 1));
-      kd1 = kappa2 + (4.0 - dy - (gx + 1 == 0) - (gx + 1 == side - 1));
+      const bool rin = y0 + ly < rows;
+      in0 = rin && gx < side;
+      in1 = rin && gx + 1 < side;
+      kd0 = kappa2 + degree(gyg, gx);
+      kd1 = kappa2 + degree(gyg, gx + 1);
     }
-    double h0 = 1.0, h1 = 1.0;
-    if (HITS) {
-      if (in0) h0 = __ldg(tc.hp + (size_t)gy * side + gx);
-      if (in1) h1 = __ldg(tc.hp + (size_t)gy * side + gx + 1);
-    }
+    const double h0 = HITS && in0 ? hit(y0 + ly, gx) : 1.0, h1 = HITS && in1 ? hit(y0 + ly, gx + 1) : 1.0;
     double2 pc[K];
 #pragma unroll
-    for (int c = 0; c < K; ++c) pc[c] = reinterpret_cast<const double2*>(Pp + c * PLANE + ly * BW)[1 + lane];
+    for (int c = 0; c < K; ++c) pc[c] = reinterpret_cast<const double2*>(Pp + c * PLANE + by * BW)[1 + lane];
 #pragma unroll
     for (int c = 0; c < K; ++c) {
-      const double* row = Pp + c * PLANE + ly * BW;
+      const double* row = Pp + c * PLANE + by * BW;
       const double2 up = reinterpret_cast<const double2*>(row - BW)[1 + lane];
       const double2 dn = reinterpret_cast<const double2*>(row + BW)[1 + lane];
       const double el = row[H - 1], er = row[H + TX];  // broadcast loads, no branch
@@ -458,29 +528,32 @@ __device__ __forceinline__ void cg_tile(const CgArgs& a, const TileCtx& tc, doub
         mix0 = fma(M[c * K + d], pc[d].x, mix0);
         mix1 = fma(M[c * K + d], pc[d].y, mix1);
       }
-      const double q0 = HITS ? fma(h0, mix0, tau[c] * fma(kd0, pc[c].x, -nb0)) : fma(tau[c], fma(kd0, pc[c].x, -nb0), mix0);
-      const double q1 = HITS ? fma(h1, mix1, tau[c] * fma(kd1, pc[c].y, -nb1)) : fma(tau[c], fma(kd1, pc[c].y, -nb1), mix1);
-      double2* rp = reinterpret_cast<double2*>(R + c * PLANE + ly * BW) + 1 + lane;
+      const double q0 = op_point<HITS>(h0, mix0, tau[c], kd0, pc[c].x, nb0);
+      const double q1 = op_point<HITS>(h1, mix1, tau[c], kd1, pc[c].y, nb1);
+      double2* rp = reinterpret_cast<double2*>(R + c * PLANE + by * BW) + 1 + lane;
       double2 rv = *rp;
       if (in0) rv.x = fma(-alpha, q0, rv.x);
       if (in1) rv.y = fma(-alpha, q1, rv.y);
       *rp = rv;
     }
   }
-  // Phase B2: the 1-pixel ring around T (scalars)
-  for (int t = tid; t < RP; t += NT) {
-    int ly, lx;
-    if (t < TX + 2) { ly = H - 1; lx = H - 1 + t; }
-    else if (t < 2 * (TX + 2)) { ly = H + TY; lx = H - 1 + (t - (TX + 2)); }
-    else { const int u = t - 2 * (TX + 2); ly = H + (u >> 1); lx = (u & 1) ? H + TX : H - 1; }
-    const int gyr = y0 - H + ly, gxr = x0 - H + lx;
+  // Phase B2: the 1-pixel ring around the tile (scalars).  Ring pixels outside the face are
+  // skipped (their r stays 0); in slab mode ring rows beyond the slab are real (ghost) pixels.
+  for (int t0 = 0; t0 < RP; t0 += NT) {
+    const int t = t0 + tid;
+    if (t >= RP) continue;
+    int by, bx;
+    if (t < TX + 2) { by = H - 1; bx = H - 1 + t; }
+    else if (t < 2 * (TX + 2)) { by = H + TY; bx = H - 1 + (t - (TX + 2)); }
+    else { const int u = t - 2 * (TX + 2); by = H + (u >> 1); bx = (u & 1) ? H + TX : H - 1; }
+    const int ly = y0 - H + by, gxr = x0 - H + bx, gyg = row0 + ly;
     double kd = kappa2 + 4.0;
     if (EDGE) {
-      if (gyr < 0 || gyr >= side || gxr < 0 || gxr >= side) continue;
-      kd = kappa2 + (4.0 - (gyr == 0) - (gyr == side - 1) - (gxr == 0) - (gxr == side - 1));
+      if (!in_face(gyg, gxr)) continue;
+      kd = kappa2 + degree(gyg, gxr);
     }
-    const double h = HITS ? __ldg(tc.hp + (size_t)gyr * side + gxr) : 1.0;
-    const int o = ly * BW + lx;
+    const double h = HITS ? hit(ly, gxr) : 1.0;
+    const int o = by * BW + bx;
     double pcs[K];
 #pragma unroll
     for (int c = 0; c < K; ++c) pcs[c] = Pp[c * PLANE + o];
@@ -491,39 +564,70 @@ __device__ __forceinline__ void cg_tile(const CgArgs& a, const TileCtx& tc, doub
       double mix = 0.0;
 #pragma unroll
       for (int d = 0; d < K; ++d) mix = fma(M[c * K + d], pcs[d], mix);
-      const double q = HITS ? fma(h, mix, tau[c] * fma(kd, pcs[c], -nb)) : fma(tau[c], fma(kd, pcs[c], -nb), mix);
-      R[c * PLANE + o] = fma(-alpha, q, R[c * PLANE + o]);
+      R[c * PLANE + o] = fma(-alpha, op_point<HITS>(h, mix, tau[c], kd, pcs[c], nb), R[c * PLANE + o]);
     }
   }
+  __syncwarp();
   __syncthreads();
 
-  // Phase C
-  double rr = 0.0, wr = 0.0;
+  if (KCG_TRACE == 2) dump_smem(tc.dump ? tc.dump + 8192 : nullptr, R, K * PLANE);
+  // Phase B' (PREC): u_new = K^{-1} r_new on tile + ring into U (row by of the R box = U row by-1).
+  if (PREC) {
+    constexpr int UPTS = (TY + 2) * (TX + 2);
+    for (int t0 = 0; t0 < UPTS; t0 += NT) {
+      const int t = t0 + tid;
+      if (t >= UPTS) continue;
+      const int uy = t / (TX + 2), ux = t - uy * (TX + 2);  // U row (tile row uy-1), column ux-1
+      const int ly = y0 - 1 + uy, gxr = x0 - 1 + ux, gyg = row0 + ly;
+      const int o = (uy + 1) * BW + (ux + 1);
+      const bool f = in_face(gyg, gxr) && ly <= rows;  // beyond: r = 0 and unused
+      double r[K], u[K];
+#pragma unroll
+      for (int c = 0; c < K; ++c) r[c] = R[c * PLANE + o];
+      if (f) {
+        precond_pixel<K, HITS>(tc.Ms + K * K + K, M, tau, kappa2, HITS ? hit(ly, gxr) : 1.0, degree(gyg, gxr), r, u);
+      } else {
+#pragma unroll
+        for (int c = 0; c < K; ++c) u[c] = 0.0;
+      }
+#pragma unroll
+      for (int c = 0; c < K; ++c) tc.U[c * UPLANE + uy * BW + ux + 1] = u[c];
+    }
+    __syncwarp();
+    __syncthreads();
+  }
+
+  if (KCG_TRACE == 2) {
+    dump_smem(tc.dump ? tc.dump + 2 * 8192 : nullptr, R, K * PLANE);
+    if (PREC) dump_smem(tc.dump ? tc.dump + 3 * 8192 : nullptr, tc.U, K * UPLANE);
+  }
+  // Phase C.  Stencil source S = r_new (R box) or u_new (U box, same indexing: U = S + BW).
+  constexpr bool USEU = PREC;
+  const double* __restrict__ S = USEU ? tc.U - BW : R;
+  constexpr int SPLANE = USEU ? UPLANE : PLANE;
+  double rr = 0.0, ru = 0.0, wu = 0.0;
 #pragma unroll
   for (int j = 0; j < RPW; ++j) {
-    const int gy = y0 + warp + j * NW;
-    const int ly = gy - y0 + H;
+    const int ly = warp + j * NW;
+    const int by = ly + H;
+    const int gyg = row0 + y0 + ly;
     bool in0 = true, in1 = true;
     double kd0 = kappa2 + 4.0, kd1 = kappa2 + 4.0;
     if (EDGE) {
-      in0 = gy < side && gx < side;
-      in1 = gy < side && gx + 1 < side;
-      const double dy = (gy == 0) + (gy == side - 1);
-      kd0 = kappa2 + (4.0 - dy - (gx == 0) - (gx == side - 1));
-      kd1 = kappa2 + (4.0 - dy - (gx + 1 == 0) - (gx + 1 == side - 1));
+      const bool rin = y0 + ly < rows;
+      in0 = rin && gx < side;
+      in1 = rin && gx + 1 < side;
+      kd0 = kappa2 + degree(gyg, gx);
+      kd1 = kappa2 + degree(gyg, gx + 1);
     }
-    double h0 = 1.0, h1 = 1.0;
-    if (HITS) {
-      if (in0) h0 = __ldg(tc.hp + (size_t)gy * side + gx);
-      if (in1) h1 = __ldg(tc.hp + (size_t)gy * side + gx + 1);
-    }
-    double* xp = a.x + ((size_t)s * K * side + gy) * side + gx;
+    const double h0 = HITS && in0 ? hit(y0 + ly, gx) : 1.0, h1 = HITS && in1 ? hit(y0 + ly, gx + 1) : 1.0;
+    double* xp = a.x + ((size_t)s * K * rows + y0 + ly) * side + gx;
     double2 xj[K];
     if (tc.xpass) {
 #pragma unroll
       for (int c = 0; c < K; ++c) {
         if (XTMA) {
-          xj[c] = reinterpret_cast<const double2*>(tc.xs + ((size_t)c * TY + (gy - y0)) * TX)[lane];
+          xj[c] = reinterpret_cast<const double2*>(tc.xs + ((size_t)c * TY + ly) * TX)[lane];
         } else if (!EDGE || (in0 && in1)) {
           xj[c] = __ldcg(reinterpret_cast<const double2*>(xp + c * N));
         } else {
@@ -532,55 +636,60 @@ __device__ __forceinline__ void cg_tile(const CgArgs& a, const TileCtx& tc, doub
         }
       }
     }
-    double2 rc[K];
+    double2 rc[K], sc[K];
 #pragma unroll
-    for (int c = 0; c < K; ++c) rc[c] = reinterpret_cast<const double2*>(R + c * PLANE + ly * BW)[1 + lane];
-    const size_t ro = ((size_t)s * K) * ps + (size_t)gy * a.pitch + gx;
+    for (int c = 0; c < K; ++c) {
+      rc[c] = reinterpret_cast<const double2*>(R + c * PLANE + by * BW)[1 + lane];
+      sc[c] = USEU ? reinterpret_cast<const double2*>(S + c * SPLANE + by * BW)[1 + lane] : rc[c];
+    }
+    const size_t ro = ((size_t)s * K) * ps + (size_t)(y0 + ly + a.ghost) * a.pitch + gx;
     double* rout = (tc.par ? a.rbuf[0] : a.rbuf[1]) + ro;  // select, not a dynamic param index
     double* pout = (tc.par ? a.pbuf[0] : a.pbuf[1]) + ro;
 #pragma unroll
     for (int c = 0; c < K; ++c) {
-      const double* row = R + c * PLANE + ly * BW;
+      const double* row = S + c * SPLANE + by * BW;
       const double2 up = reinterpret_cast<const double2*>(row - BW)[1 + lane];
       const double2 dn = reinterpret_cast<const double2*>(row + BW)[1 + lane];
       const double el = row[H - 1], er = row[H + TX];
-      double left = __shfl_up_sync(0xffffffffu, rc[c].y, 1);
-      double right = __shfl_down_sync(0xffffffffu, rc[c].x, 1);
+      double left = __shfl_up_sync(0xffffffffu, sc[c].y, 1);
+      double right = __shfl_down_sync(0xffffffffu, sc[c].x, 1);
       left = lane == 0 ? el : left;
       right = lane == 31 ? er : right;
-      const double nb0 = (up.x + dn.x) + (left + rc[c].y);
-      const double nb1 = (up.y + dn.y) + (rc[c].x + right);
+      const double nb0 = (up.x + dn.x) + (left + sc[c].y);
+      const double nb1 = (up.y + dn.y) + (sc[c].x + right);
       double mix0 = 0.0, mix1 = 0.0;
 #pragma unroll
       for (int d = 0; d < K; ++d) {
-        mix0 = fma(M[c * K + d], rc[d].x, mix0);
-        mix1 = fma(M[c * K + d], rc[d].y, mix1);
+        mix0 = fma(M[c * K + d], sc[d].x, mix0);
+        mix1 = fma(M[c * K + d], sc[d].y, mix1);
       }
-      const double w0 = HITS ? fma(h0, mix0, tau[c] * fma(kd0, rc[c].x, -nb0)) : fma(tau[c], fma(kd0, rc[c].x, -nb0), mix0);
-      const double w1 = HITS ? fma(h1, mix1, tau[c] * fma(kd1, rc[c].y, -nb1)) : fma(tau[c], fma(kd1, rc[c].y, -nb1), mix1);
-      const double2 pn = reinterpret_cast<const double2*>(Pp + c * PLANE + ly * BW)[1 + lane];
+      const double w0 = op_point<HITS>(h0, mix0, tau[c], kd0, sc[c].x, nb0);
+      const double w1 = op_point<HITS>(h1, mix1, tau[c], kd1, sc[c].y, nb1);
+      const double2 pn = reinterpret_cast<const double2*>(Pp + c * PLANE + by * BW)[1 + lane];
       double2 xn;
       xn.x = xj[c].x + xinc[j][c].x;
       xn.y = xj[c].y + xinc[j][c].y;
-      if (!EDGE || (in0 && in1)) {
+      if (in0) {
         rr = fma(rc[c].x, rc[c].x, rr);
-        wr = fma(w0, rc[c].x, wr);
+        if (PREC) ru = fma(rc[c].x, sc[c].x, ru);
+        wu = fma(w0, sc[c].x, wu);
+      }
+      if (in1) {
         rr = fma(rc[c].y, rc[c].y, rr);
-        wr = fma(w1, rc[c].y, wr);
+        if (PREC) ru = fma(rc[c].y, sc[c].y, ru);
+        wu = fma(w1, sc[c].y, wu);
+      }
+      if (!EDGE || (in0 && in1)) {
         if (tc.xpass) *reinterpret_cast<double2*>(xp + c * N) = xn;
         *reinterpret_cast<double2*>(rout + c * ps) = rc[c];
         *reinterpret_cast<double2*>(pout + c * ps) = pn;
       } else {
         if (in0) {
-          rr = fma(rc[c].x, rc[c].x, rr);
-          wr = fma(w0, rc[c].x, wr);
           if (tc.xpass) xp[c * N] = xn.x;
           rout[c * ps] = rc[c].x;
           pout[c * ps] = pn.x;
         }
         if (in1) {
-          rr = fma(rc[c].y, rc[c].y, rr);
-          wr = fma(w1, rc[c].y, wr);
           if (tc.xpass) xp[c * N + 1] = xn.y;
           rout[c * ps + 1] = rc[c].y;
           pout[c * ps + 1] = pn.y;
@@ -589,54 +698,58 @@ __device__ __forceinline__ void cg_tile(const CgArgs& a, const TileCtx& tc, doub
     }
   }
   rr = warp_sum(rr);
-  wr = warp_sum(wr);
+  wu = warp_sum(wu);
+  if (PREC) ru = warp_sum(ru);
   // per-warp partials; warp 0 sums them (fixed order) after the next CTA barrier (flush_tile_partial)
-  if (lane == 0) { tred[0][warp] = rr; tred[1][warp] = wr; }
-  if (!KCG_DEFER) {
+  if (lane == 0) {
+    tred[0][warp] = rr;
+    if (PREC) { tred[1][warp] = ru; tred[2][warp] = wu; }
+    else tred[1][warp] = wu;
+  }
+  if (KCG_TRACE == 2) {
     __syncthreads();
-    if (warp == 0) {
-      double v0 = lane < NW ? tred[0][lane] : 0.0;
-      double v1 = lane < NW ? tred[1][lane] : 0.0;
-      v0 = warp_sum(v0);
-      v1 = warp_sum(v1);
-      if (lane == 0) { tc.part_out[0] = v0; tc.part_out[1] = v1; }
+    dump_smem(tc.dump ? tc.dump + 4 * 8192 : nullptr, &tred[0][0], 3 * NW);
+  }
+}
+
+// Tile partials of a finished tile: the fixed-order sums of its per-warp values, written by warp 0
+// after a barrier that follows the tile (deferred, so a tile needs no barrier of its own).
+template <int NW, int NP>
+__device__ __forceinline__ void flush_tile_partial(const double (*tred)[NW], double* part_out, int warp, int lane) {
+  if (warp == 0) {
+#pragma unroll
+    for (int q = 0; q < NP; ++q) {
+      double v = lane < NW ? tred[q][lane] : 0.0;
+      v = warp_sum(v);
+      if (lane == 0) part_out[q] = v;
     }
   }
 }
 
-// Tile partial (r,r), (w,r) of a finished tile: the fixed-order sum of its per-warp values, written
-// by warp 0 after a barrier that follows the tile (deferred, so a tile needs no barrier of its own).
-template <int NW>
-__device__ __forceinline__ void flush_tile_partial(const double (*tred)[NW], double* part_out, int warp, int lane) {
-  if (warp == 0) {
-    double v0 = lane < NW ? tred[0][lane] : 0.0;
-    double v1 = lane < NW ? tred[1][lane] : 0.0;
-    v0 = warp_sum(v0);
-    v1 = warp_sum(v1);
-    if (lane == 0) { part_out[0] = v0; part_out[1] = v1; }
-  }
-}
-
-template <int K, bool HITS>
+template <int K, bool HITS, bool PREC>
 __global__ void __launch_bounds__(cg_threads(K), cg_min_blocks(K)) cg_persistent_kernel(const CgArgs a, const __grid_constant__ CgMaps maps) {
   constexpr int TY = cg_tile_y(K), TX = KCG_TX, H = KCG_HALO;
   constexpr int BW = TX + 2 * H, BH = TY + 2 * H;
   constexpr int FIELD = K * BW * BH;  // doubles of one field box
   constexpr int XBYTES = cg_xstage_bytes(K);  // x block, TMA-staged with the boxes (0 if disabled)
   constexpr int STAGE_BYTES = 2 * FIELD * 8 + XBYTES;
+  constexpr int UBYTES = PREC ? cg_ubox_bytes(K) : 0;
   constexpr int NT = cg_threads(K), NW = NT / 32, NS = cg_stages(K);
+  constexpr int NP = PREC ? 3 : 2;  // partials per tile
+  constexpr int MSZ = K * K + K + (PREC ? 3 * K * K : 0);
   static_assert(STAGE_BYTES == cg_stage_bytes(K), "stage size");
 
   extern __shared__ __align__(128) unsigned char smem_raw[];
-  SysState* st = reinterpret_cast<SysState*>(smem_raw + NS * STAGE_BYTES);
+  double* ubox = reinterpret_cast<double*>(smem_raw + NS * STAGE_BYTES);
+  SysState* st = reinterpret_cast<SysState*>(smem_raw + NS * STAGE_BYTES + UBYTES);
   int* act = reinterpret_cast<int*>(st + a.n_sys);
   __shared__ __align__(8) uint64_t mbar[2];
-  __shared__ double tred[2][2][NW];  // per-warp tile partials, double-buffered by tile parity
+  __shared__ double tred[2][3][NW];  // per-warp tile partials, double-buffered by tile parity
   // per-warp system sums of the iteration reduction: aliased onto pipeline stage 1, which is idle
   // from the end of a pass's last tile until the first prefetch of the next pass
-  double (*rs)[2][NW] = reinterpret_cast<double (*)[2][NW]>(smem_raw + STAGE_BYTES);
-  static_assert(NS == 2 && (size_t)KCG_RB * 2 * NW * 8 <= (size_t)STAGE_BYTES, "rs alias");  // per-warp tile partials, double-buffered by tile parity
-  __shared__ double Ms[KCG_KMAX * KCG_KMAX + KCG_KMAX];
+  double (*rs)[3][NW] = reinterpret_cast<double (*)[3][NW]>(smem_raw + STAGE_BYTES);
+  static_assert(NS == 2 && (size_t)KCG_RB * 3 * NW * 8 <= (size_t)STAGE_BYTES, "rs alias");
+  __shared__ double Ms[MSZ];
   __shared__ int s_nact;
   __shared__ int s_sched[2][2];  // [buffer][current tile, next tile]
   __shared__ int s_info[2][4];   // [stage][system, tile, tile row, tile col] of the tile in that stage
@@ -644,8 +757,12 @@ __global__ void __launch_bounds__(cg_threads(K), cg_min_blocks(K)) cg_persistent
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int tps = a.tiles_per_sys;
   const bool xtma = cg_xtma(K) && a.x_tma != 0;
-  unsigned epoch = 0;  // ONEBAR barrier generations
 
+  if (tid == 0) {  // the launch must provide the dynamic shared memory this layout assumes
+    unsigned dyn;
+    asm volatile("mov.u32 %0, %%dynamic_smem_size;" : "=r"(dyn));
+    if ((size_t)dyn < (size_t)NS * STAGE_BYTES + UBYTES + (size_t)a.n_sys * (sizeof(SysState) + sizeof(int))) __trap();
+  }
   for (int s = tid; s < a.n_sys; s += NT) {
     SysState z;
     z.bnorm2 = 0.0; z.gamma = 0.0; z.alpha = 0.0; z.beta = 0.0; z.rel = 1.0;
@@ -660,14 +777,14 @@ __global__ void __launch_bounds__(cg_threads(K), cg_min_blocks(K)) cg_persistent
   __syncthreads();
 
   uint32_t phase0 = 0, phase1 = 0;
-  int it = -1;  // -1 = start pass (alpha = beta = 0): r, p <- b and (b, b), (G b, b)
+  int it = -1;  // -1 = start pass (alpha = beta = 0): p <- u_0 = K^{-1} b, (b,b), (b,u_0), (G u_0, u_0)
 
-  // TMA of tile t (index into the active-tile list) into stage sidx; parity flip for speculation
   // pass q = it + 1 updates x iff xpass_of(q) (KCG_X2: even passes >= 2; else every pass >= 1)
   auto xpass_of = [](int q) { return KCG_X2 ? (q >= 2 && (q & 1) == 0) : (q >= 1); };
   // Thread 0: TMA of (physical) tile t into stage sidx (parity flipped for the speculative load of
   // the next pass) and its coordinates into s_info[sidx] for all threads.  On x passes the x block
-  // comes with the boxes (XTMA) or is prefetched into L2 (read by phase C).
+  // comes with the boxes (XTMA) or is prefetched into L2 (read by phase C).  r/p buffers carry
+  // a.ghost ghost rows above and below the slab (row-slab mode), hence the + ghost.
   auto issue = [&](int t, int sidx, int flip) {
     const int s = act[t / tps];
     const int tile = t - (t / tps) * tps;
@@ -680,8 +797,8 @@ __global__ void __launch_bounds__(cg_threads(K), cg_min_blocks(K)) cg_persistent
     mbar_arrive_expect_tx(&mbar[sidx], xl ? STAGE_BYTES : 2 * FIELD * 8);
     if (xl) tma_load_3d(dst + 2 * FIELD, &maps.x, &mbar[sidx], tx * TX, ty * TY, s * K);
     else if (xp && a.x_tma && KCG_XPF) tma_prefetch_l2_3d(&maps.x, tx * TX, ty * TY, s * K);
-    tma_load_3d(dst, &maps.r[par], &mbar[sidx], tx * TX - H, ty * TY - H, s * K);
-    tma_load_3d(dst + FIELD, &maps.p[par], &mbar[sidx], tx * TX - H, ty * TY - H, s * K);
+    tma_load_3d(dst, &maps.r[par], &mbar[sidx], tx * TX - H, ty * TY - H + a.ghost, s * K);
+    tma_load_3d(dst + FIELD, &maps.p[par], &mbar[sidx], tx * TX - H, ty * TY - H + a.ghost, s * K);
   };
 
   int nact_prev = -1;
@@ -703,7 +820,7 @@ __global__ void __launch_bounds__(cg_threads(K), cg_min_blocks(K)) cg_persistent
     if (nact == 0) break;
     const int ntiles = nact * tps;
     const int par_out = (it + 1) & 1;
-    const bool tr = KCG_TRACE && a.trace && it + 1 < KCG_TRACE_ITERS;
+    const bool tr = KCG_TRACE == 1 && a.trace && it + 1 < KCG_TRACE_ITERS;
     if (tr && blockIdx.x == 0 && tid == 0) a.trace[(size_t)(it + 1) * KCG_TRACE_COLS + 0] = globaltimer();
 
     // serpentine order: odd passes walk the active-tile list backwards, so the first tiles of a
@@ -725,7 +842,7 @@ __global__ void __launch_bounds__(cg_threads(K), cg_min_blocks(K)) cg_persistent
       const int sidx = i & 1;
       __syncthreads();
       const int t = s_sched[i & 1][0], tn = s_sched[i & 1][1];
-      if (prev_part) flush_tile_partial<NW>(tred[(i - 1) & 1], prev_part, warp, lane);
+      if (prev_part) flush_tile_partial<NW, NP>(tred[(i - 1) & 1], prev_part, warp, lane);
       if (t >= ntiles) break;
       unsigned claim = 0;
       if (tid == 0) {
@@ -739,11 +856,14 @@ __global__ void __launch_bounds__(cg_threads(K), cg_min_blocks(K)) cg_persistent
       const SysParams* sp = a.params + s;
       if (tid < K * K) Ms[tid] = __ldg(&sp->M[tid]);
       else if (tid < K * K + K) Ms[tid] = __ldg(&sp->tau[tid - K * K]);
+      else if (PREC && tid < MSZ) Ms[tid] = __ldg(&sp->Kinv[0][0] + (tid - K * K - K));
       TileCtx tc;
       tc.R = reinterpret_cast<double*>(smem_raw + sidx * STAGE_BYTES);
       tc.Pp = tc.R + FIELD;
       tc.xs = tc.R + 2 * FIELD;
+      tc.U = ubox;
       tc.Ms = Ms;
+      tc.sp = sp;
       tc.s = s;
       tc.y0 = ty * TY;
       tc.x0 = tx * TX;
@@ -753,20 +873,24 @@ __global__ void __launch_bounds__(cg_threads(K), cg_min_blocks(K)) cg_persistent
       tc.xpass = xpass_of(it + 1);
       tc.alpha_prev = KCG_X2 ? st[s].alpha_last : 0.0;
       tc.kappa2 = __ldg(&sp->kappa2);
-      tc.hp = HITS ? a.hits + (size_t)__ldg(&sp->hits_plane) * ((size_t)a.side * a.side) : nullptr;
+      tc.hp = HITS ? a.hits + (size_t)__ldg(&sp->hits_plane) * ((size_t)a.rows * a.side) : nullptr;
       tc.bar = &mbar[sidx];
       tc.phase = sidx ? phase1 : phase0;
-      tc.part_out = a.partials + (((size_t)par_out * a.n_sys + s) * tps + tile) * 2;
-      const bool interior = tc.x0 >= H && tc.x0 + TX + H <= a.side && tc.y0 >= H && tc.y0 + TY + H <= a.side;
+      tc.part_out = a.partials + (((size_t)par_out * a.n_sys + s) * tps + tile) * NP;
+      tc.dump = (KCG_TRACE == 2 && a.trace && it < 0 && blockIdx.x == 0 && i == 0)
+                    ? reinterpret_cast<double*>(a.trace) : nullptr;
+      const int gy0 = a.row0 + tc.y0;
+      const bool interior = tc.x0 >= H && tc.x0 + TX + H <= a.side && gy0 >= H && gy0 + TY + H <= a.side &&
+                            tc.y0 + TY <= a.rows;
       if (cg_xtma(K) && xtma) {
-        if (interior) cg_tile<K, false, HITS, cg_xtma(K)>(a, tc, tred[i & 1]);
-        else cg_tile<K, true, HITS, cg_xtma(K)>(a, tc, tred[i & 1]);
+        if (interior) cg_tile<K, false, HITS, cg_xtma(K), PREC>(a, tc, tred[i & 1]);
+        else cg_tile<K, true, HITS, cg_xtma(K), PREC>(a, tc, tred[i & 1]);
       } else {
-        if (interior) cg_tile<K, false, HITS, false>(a, tc, tred[i & 1]);
-        else cg_tile<K, true, HITS, false>(a, tc, tred[i & 1]);
+        if (interior) cg_tile<K, false, HITS, false, PREC>(a, tc, tred[i & 1]);
+        else cg_tile<K, true, HITS, false, PREC>(a, tc, tred[i & 1]);
       }
       if (sidx) phase1 ^= 1u; else phase0 ^= 1u;
-      if (KCG_DEFER) prev_part = tc.part_out;
+      prev_part = tc.part_out;
       if (tid == 0) {  // the tile after tn (the claim's value is consumed only now)
         s_sched[(i + 1) & 1][0] = tn;
         s_sched[(i + 1) & 1][1] = tn >= ntiles ? ntiles : (KCG_DYN ? 2 * G + (int)claim : tn + G);
@@ -779,7 +903,7 @@ __global__ void __launch_bounds__(cg_threads(K), cg_min_blocks(K)) cg_persistent
     // overlaps the reduction; verified against the new active count at the top of the loop
     const int spec_t = (KCG_SERP && !rev) ? ntiles - 1 - (int)blockIdx.x : (int)blockIdx.x;
     const bool do_spec = it >= 0 && (int)blockIdx.x < ntiles;
-    iteration_reduce<NT>(a, st, act, nact, par_out, it, rs, epoch, [&]() {
+    iteration_reduce<NT, NP>(a, st, act, nact, par_out, it, rs, [&]() {
       if (tr && blockIdx.x == 0) a.trace[(size_t)(it + 1) * KCG_TRACE_COLS + 1] = globaltimer();
       if (KCG_DYN && blockIdx.x == 0) *ctr = 0u;  // quiescent now; next used two passes later
       if (do_spec) issue(spec_t, 0, 1);
@@ -995,14 +1119,15 @@ cudaError_t launch_rhs(int K, cudaStream_t s, const double* Y, const double* E, 
   return cudaGetLastError();
 }
 
-template <int K, bool HITS>
+template <int K, bool HITS, bool PREC>
 static cudaError_t cg_config_t(int n_sys, int* max_grid, size_t* smem) {
-  const size_t sm = cg_stages(K) * (size_t)cg_stage_bytes(K) +
+  const size_t sm = cg_stages(K) * (size_t)cg_stage_bytes(K) + (PREC ? (size_t)cg_ubox_bytes(K) : 0) +
                     (size_t)n_sys * (sizeof(SysState) + sizeof(int));
-  cudaError_t e = cudaFuncSetAttribute(cg_persistent_kernel<K, HITS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  auto kern = cg_persistent_kernel<K, HITS, PREC>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
   if (e != cudaSuccess) return e;
   int nb = 0, dev = 0, nsm = 0;
-  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, cg_persistent_kernel<K, HITS>, cg_threads(K), sm);
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, cg_threads(K), sm);
   if (e != cudaSuccess) return e;
   e = cudaGetDevice(&dev);
   if (e != cudaSuccess) return e;
@@ -1013,20 +1138,45 @@ static cudaError_t cg_config_t(int n_sys, int* max_grid, size_t* smem) {
   return nb > 0 ? cudaSuccess : cudaErrorInvalidConfiguration;
 }
 
-cudaError_t cg_kernel_config(int K, bool hits, int n_sys, int* max_grid, size_t* smem) {
-  if (hits) { KCG_DISPATCH(K, return (cg_config_t<KK, true>(n_sys, max_grid, smem))); }
-  else { KCG_DISPATCH(K, return (cg_config_t<KK, false>(n_sys, max_grid, smem))); }
+// The preconditioned kernel needs the u box on top of the two stages: built for K <= 7.
+#define KCG_DISPATCH_PREC(K, CALL)            \
+  switch (K) {                                \
+    case 1: { constexpr int KK = 1; CALL; } break; \
+    case 2: { constexpr int KK = 2; CALL; } break; \
+    case 3: { constexpr int KK = 3; CALL; } break; \
+    case 4: { constexpr int KK = 4; CALL; } break; \
+    case 5: { constexpr int KK = 5; CALL; } break; \
+    case 6: { constexpr int KK = 6; CALL; } break; \
+    case 7: { constexpr int KK = 7; CALL; } break; \
+    default: return cudaErrorInvalidValue;    \
+  }
+
+cudaError_t cg_kernel_config(int K, bool hits, bool prec, int n_sys, int* max_grid, size_t* smem) {
+  if (prec) {
+    if (hits) { KCG_DISPATCH_PREC(K, return (cg_config_t<KK, true, true>(n_sys, max_grid, smem))); }
+    else { KCG_DISPATCH_PREC(K, return (cg_config_t<KK, false, true>(n_sys, max_grid, smem))); }
+  } else {
+    if (hits) { KCG_DISPATCH(K, return (cg_config_t<KK, true, false>(n_sys, max_grid, smem))); }
+    else { KCG_DISPATCH(K, return (cg_config_t<KK, false, false>(n_sys, max_grid, smem))); }
+  }
   return cudaErrorInvalidValue;
 }
 
-cudaError_t launch_cg(int K, cudaStream_t s, const CgArgs& a, const CgMaps& m, int grid, size_t smem) {
+template <int K, bool HITS, bool PREC>
+static cudaError_t launch_cg_t(cudaStream_t s, const CgArgs& a, const CgMaps& m, int grid, size_t smem) {
   void* args[2] = {(void*)&a, (void*)&m};
-  if (a.hits) {
-    KCG_DISPATCH(K, return cudaLaunchCooperativeKernel((const void*)cg_persistent_kernel<KK, true>, dim3(grid),
-                                                        dim3(cg_threads(KK)), args, smem, s));
+  return cudaLaunchCooperativeKernel((const void*)cg_persistent_kernel<K, HITS, PREC>, dim3(grid),
+                                     dim3(cg_threads(K)), args, smem, s);
+}
+
+cudaError_t launch_cg(int K, bool prec, cudaStream_t s, const CgArgs& a, const CgMaps& m, int grid, size_t smem) {
+  const bool hits = a.hits != nullptr;
+  if (prec) {
+    if (hits) { KCG_DISPATCH_PREC(K, return (launch_cg_t<KK, true, true>(s, a, m, grid, smem))); }
+    else { KCG_DISPATCH_PREC(K, return (launch_cg_t<KK, false, true>(s, a, m, grid, smem))); }
   } else {
-    KCG_DISPATCH(K, return cudaLaunchCooperativeKernel((const void*)cg_persistent_kernel<KK, false>, dim3(grid),
-                                                        dim3(cg_threads(KK)), args, smem, s));
+    if (hits) { KCG_DISPATCH(K, return (launch_cg_t<KK, true, false>(s, a, m, grid, smem))); }
+    else { KCG_DISPATCH(K, return (launch_cg_t<KK, false, false>(s, a, m, grid, smem))); }
   }
   return cudaErrorInvalidValue;
 }

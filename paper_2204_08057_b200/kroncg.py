@@ -103,10 +103,11 @@ class KronCG:
 
     Parameters are host numpy arrays in the C-ABI layouts (A [P][n][k], noise_prec [P][n],
     prior_scale [P][k], kappa2 [P]); hits an optional torch CUDA tensor [P][side][side].
+    precond: "none" (the paper's CG) or "block_jacobi" (pixel-block Jacobi, reading R10).
     """
 
     def __init__(self, level, A, noise_prec, prior_scale, kappa2, hits=None, device=None,
-                 host_staging=False, history_cap=0, stream=None):
+                 host_staging=False, history_cap=0, stream=None, precond="none"):
         import torch
         A = np.ascontiguousarray(np.asarray(A, dtype=np.float64))
         if A.ndim == 2:
@@ -120,8 +121,9 @@ class KronCG:
         self.side = 1 << level
         self.N = self.side * self.side
         self.device = torch.device(device if device is not None else "cuda")
+        pc = {"none": KCG_PRECOND_NONE, "block_jacobi": KCG_PRECOND_BLOCK_JACOBI}[precond]
         self.desc = kcg_desc(level, n, k, P, KCG_PRIOR_LAPLACIAN, KCG_LAYOUT_ROW_MAJOR,
-                             KCG_PRECOND_NONE, int(bool(host_staging)), int(history_cap))
+                             pc, int(bool(host_staging)), int(history_cap))
         ws = kron_cg_workspace_size(C.byref(self.desc))
         if ws == 0:
             raise KcgError(KCG_E_SHAPE, "invalid descriptor")

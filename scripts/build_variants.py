@@ -6,8 +6,7 @@ sys.path.insert(0, ROOT)
 from paper_2204_08057_b200 import build
 
 VARIANTS = {
-    "xpf": [],
-    "noxpf": ["KCG_XPF=0"],
+    "dump": ["KCG_TRACE=2"],
 }
 names = sys.argv[1:] or list(VARIANTS)
 out = os.path.join(ROOT, "paper_2204_08057_b200", "lib", "variants")

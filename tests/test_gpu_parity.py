@@ -238,3 +238,61 @@ def test_launch_occupancy():
     cfg = ctx.launch_config()
     assert cfg["grid_kron"] == cfg["sm_count"], cfg
     assert cfg["grid_syl"] == 2 * cfg["sm_count"], cfg
+
+
+# ----------------------------------------------------------------------------- block-Jacobi PCG
+def _check_kron_pc(ps, its_tol=2, err_tol=1e-8):
+    ctx, Y = make_ctx(ps, precond="block_jacobi")
+    mu, rep = ctx.solve(Y, tol=TOL)
+    mu = _np(mu)
+    assert rep["converged"], rep
+    for i, p in enumerate(ps):
+        G, b = model.problem_system(p)
+        K = cg.block_jacobi_precond(p.level, p.A, p.noise_prec, p.tau, p.kappa2, p.hits)
+        ref = cg.cg_hs(G, b, tol=TOL, precond=K)
+        assert ref.converged
+        assert rel(mu[i], ref.x) <= err_tol, (i, rel(mu[i], ref.x))
+        assert abs(rep["iterations_per"][i] - ref.iterations) <= its_tol, \
+            (i, rep["iterations_per"][i], ref.iterations)
+    return ctx, Y, mu, rep
+
+
+def test_pcg_tiny_medium():
+    _, _, _, rep = _check_kron_pc(make_config("tiny"))
+    ref_plain = cg.cg_hs(*model.problem_system(make_config("tiny")[0]), tol=TOL)
+    assert rep["iterations"] < ref_plain.iterations      # the preconditioner does something
+    _check_kron_pc(make_config("medium"))
+
+
+@pytest.mark.parametrize("level,k,hits", [(0, 1, None), (1, 2, "random"), (3, 3, None), (4, 4, "random"),
+                                          (5, 5, None), (6, 6, "random"), (5, 7, None), (7, 4, None)])
+def test_pcg_edge(level, k, hits):
+    _check_kron_pc([make_patch(level, 9, k, seed=110 + s, tau="loguniform", hits=hits) for s in range(2)])
+
+
+def test_pcg_planck_vs_exact():
+    p = make_config("planck")[0]
+    ctx, Y = make_ctx([p], precond="block_jacobi")
+    mu, rep = ctx.solve(Y, tol=TOL)
+    assert rep["converged"] and rel(_np(mu)[0], exact.problem_dct_exact(p)) <= 1e-8
+    assert rep["rel_residual_true"] <= 2 * TOL
+
+
+def test_pcg_sylvester_jacobi():
+    ps = [make_patch(5, 9, 3, seed=120, tau="loguniform", hits="random"),
+          make_patch(5, 9, 3, seed=121, tau="loguniform")]
+    ctx, Y = make_ctx(ps, precond="block_jacobi")
+    mu, rep = ctx.sylvester(Y, tol=TOL)
+    mu = _np(mu)
+    for i, p in enumerate(ps):
+        ref = sylvester.problem_solve(p, tol=TOL, precond="jacobi")
+        assert rel(mu[i], ref.x) <= 1e-8
+        gits = rep["iterations_per"][i * 3:(i + 1) * 3]
+        assert all(abs(a - b) <= 2 for a, b in zip(gits, ref.iterations)), (gits, ref.iterations)
+
+
+def test_pcg_k8_rejected():
+    from paper_2204_08057_b200.kroncg import KcgError
+    with pytest.raises(KcgError) as e:
+        make_ctx([make_patch(3, 9, 8, seed=1)], precond="block_jacobi")
+    assert e.value.status == 4

@@ -71,6 +71,17 @@ def test_sylvester_k1_is_single_shifted_system():
     assert rel(res.x, exact.dense_solve(G, b)) <= 1e-8
 
 
+def test_sylvester_jacobi_preconditioned():
+    """The Jacobi option (diag of the shifted operator) changes the iterates, not the solution."""
+    p = make_patch(4, 9, 3, seed=12, hits="random")
+    plain = sylvester.problem_solve(p, tol=1e-11)
+    pc = sylvester.problem_solve(p, tol=1e-11, precond="jacobi")
+    G, b = model.problem_system(p)
+    x_star = exact.dense_solve(G, b)
+    assert pc.converged and rel(pc.x, x_star) <= 1e-8
+    assert pc.iterations != plain.iterations
+
+
 @pytest.mark.slow
 def test_sylvester_medium_matches_dct():
     p = make_config("medium")[0]
