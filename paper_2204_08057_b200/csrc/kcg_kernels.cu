@@ -120,8 +120,8 @@ __global__ void __launch_bounds__(256) rhs_kernel(const double* __restrict__ Y, 
 }
 
 // --------------------------------------------------------------------------- CG scalar update
-// One CG scalar step for a system from its reduced partials (Chronopoulos-Gear, preconditioned
-// form of oracle/cg.py cg_single_pass): rr = (r,r), ru = (r,u), wu = (w,u) with u = K^{-1} r,
+// One CG scalar step for a system from its reduced partials (Chronopoulos-Gear single-reduction
+// CG, preconditioned form; reading R9/R10): rr = (r,r), ru = (r,u), wu = (w,u) with u = K^{-1} r,
 // w = G u (u = r, ru = rr without a preconditioner).  The start pass (it < 0) gives ||b||^2,
 // gamma_0 = (b,u_0) and alpha_0 = gamma_0/delta_0; afterwards beta = gamma'/gamma,
 // alpha = gamma'/(delta - beta gamma'/alpha); stop on ||r|| <= tol ||b|| (reading R8).
