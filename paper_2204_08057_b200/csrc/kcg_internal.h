@@ -22,7 +22,7 @@ namespace kcg {
 #define KCG_TY4 16          // tile rows, K = 4
 #endif
 #ifndef KCG_NT4
-#define KCG_NT4 512         // threads, K = 4 (warps must divide the tile rows)
+#define KCG_NT4 256         // threads, K = 4 (warps must divide the tile rows; 256: no spills)
 #endif
 #ifndef KCG_XTMA_MAXK
 #define KCG_XTMA_MAXK 3     // x block TMA-staged with the boxes for K <= this (K=4: measured slower)

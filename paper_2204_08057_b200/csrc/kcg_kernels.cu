@@ -374,7 +374,7 @@ __device__ __forceinline__ void dump_smem(double* dst, const double* src, int n)
   __syncthreads();
 }
 
-template <int K, bool EDGE, bool HITS, bool XTMA, bool PREC>
+template <int K, bool EDGE, bool HITS, bool XTMA, bool PREC, bool SLAB>
 __device__ __forceinline__ void cg_tile(const CgArgs& a, const TileCtx& tc, double (*tred)[cg_threads(K) / 32]) {
   constexpr int TY = cg_tile_y(K), TX = KCG_TX, H = KCG_HALO;
   constexpr int BW = TX + 2 * H, BH = TY + 2 * H, PLANE = BW * BH;
@@ -383,9 +383,9 @@ __device__ __forceinline__ void cg_tile(const CgArgs& a, const TileCtx& tc, doub
   constexpr int RP = 2 * (TX + 2) + 2 * TY;  // ring points
   static_assert(TX == 64 && RPW * NW == TY, "pair mapping needs TX = 64 and NW | TY");
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int side = a.side, rows = a.rows, row0 = a.row0;
+  const int side = a.side, rows = SLAB ? a.rows : side, row0 = SLAB ? a.row0 : 0, ghost = SLAB ? a.ghost : 0;
   const size_t N = (size_t)rows * side;                   // pixels of one local plane
-  const size_t ps = (size_t)a.pitch * (rows + 2 * a.ghost);  // one r/p buffer plane
+  const size_t ps = (size_t)a.pitch * (rows + 2 * ghost);  // one r/p buffer plane
   double* __restrict__ R = tc.R;
   double* __restrict__ Pp = tc.Pp;
   const int s = tc.s, y0 = tc.y0, x0 = tc.x0;
@@ -402,9 +402,10 @@ __device__ __forceinline__ void cg_tile(const CgArgs& a, const TileCtx& tc, doub
   mbar_wait(tc.bar, tc.phase);
   if (KCG_TRACE == 2) dump_smem(tc.dump, R, K * PLANE);
 
-  double tau[K];
+  double tau[K];  // PREC: needed in phase A (global copy); else read from shared after the barrier
+  if (PREC)
 #pragma unroll
-  for (int c = 0; c < K; ++c) tau[c] = __ldg(&tc.sp->tau[c]);
+    for (int c = 0; c < K; ++c) tau[c] = __ldg(&tc.sp->tau[c]);
 
   // Phase A.  Interior pairs in the pair mapping (the thread keeps its pairs' x increment
   //   xinc = alpha_prev p_old + alpha p_new   (X2: x is updated every other pass)
@@ -418,6 +419,19 @@ __device__ __forceinline__ void cg_tile(const CgArgs& a, const TileCtx& tc, doub
     for (int j = 0; j < RPW; ++j) {
       const int ly = warp + j * NW;
       const int e0 = ((ly + H) * BW + H) / 2 + lane;
+      if constexpr (!PREC) {
+#pragma unroll
+        for (int c = 0; c < K; ++c) {
+          const int e = e0 + c * (PLANE / 2);
+          const double2 r = R2[e], po = P2[e];
+          double2 pn;
+          pn.x = fma(beta, po.x, r.x);
+          pn.y = fma(beta, po.y, r.y);
+          P2[e] = pn;
+          xinc[j][c].x = fma(alpha, pn.x, ap * po.x);
+          xinc[j][c].y = fma(alpha, pn.y, ap * po.y);
+        }
+      } else {
       double2 uu[K];
 #pragma unroll
       for (int c = 0; c < K; ++c) uu[c] = R2[e0 + c * (PLANE / 2)];
@@ -445,6 +459,7 @@ __device__ __forceinline__ void cg_tile(const CgArgs& a, const TileCtx& tc, doub
         xinc[j][c].x = fma(alpha, pn.x, ap * po.x);
         xinc[j][c].y = fma(alpha, pn.y, ap * po.y);
       }
+      }  // PREC
     }
     constexpr int FR = 4 * (BW / 2) + 2 * TY;  // frame double2 units per plane
     constexpr int NFR = PREC ? FR : K * FR;
@@ -490,6 +505,10 @@ __device__ __forceinline__ void cg_tile(const CgArgs& a, const TileCtx& tc, doub
   }
   __syncwarp();
   __syncthreads();
+
+  if (!PREC)
+#pragma unroll
+    for (int c = 0; c < K; ++c) tau[c] = M[K * K + c];
 
   // Phase B1: tile rows, pairs
 #pragma unroll
@@ -642,7 +661,7 @@ __device__ __forceinline__ void cg_tile(const CgArgs& a, const TileCtx& tc, doub
       rc[c] = reinterpret_cast<const double2*>(R + c * PLANE + by * BW)[1 + lane];
       sc[c] = USEU ? reinterpret_cast<const double2*>(S + c * SPLANE + by * BW)[1 + lane] : rc[c];
     }
-    const size_t ro = ((size_t)s * K) * ps + (size_t)(y0 + ly + a.ghost) * a.pitch + gx;
+    const size_t ro = ((size_t)s * K) * ps + (size_t)(y0 + ly + ghost) * a.pitch + gx;
     double* rout = (tc.par ? a.rbuf[0] : a.rbuf[1]) + ro;  // select, not a dynamic param index
     double* pout = (tc.par ? a.pbuf[0] : a.pbuf[1]) + ro;
 #pragma unroll
@@ -726,7 +745,7 @@ __device__ __forceinline__ void flush_tile_partial(const double (*tred)[NW], dou
   }
 }
 
-template <int K, bool HITS, bool PREC>
+template <int K, bool HITS, bool PREC, bool SLAB>
 __global__ void __launch_bounds__(cg_threads(K), cg_min_blocks(K)) cg_persistent_kernel(const CgArgs a, const __grid_constant__ CgMaps maps) {
   constexpr int TY = cg_tile_y(K), TX = KCG_TX, H = KCG_HALO;
   constexpr int BW = TX + 2 * H, BH = TY + 2 * H;
@@ -797,8 +816,8 @@ __global__ void __launch_bounds__(cg_threads(K), cg_min_blocks(K)) cg_persistent
     mbar_arrive_expect_tx(&mbar[sidx], xl ? STAGE_BYTES : 2 * FIELD * 8);
     if (xl) tma_load_3d(dst + 2 * FIELD, &maps.x, &mbar[sidx], tx * TX, ty * TY, s * K);
     else if (xp && a.x_tma && KCG_XPF) tma_prefetch_l2_3d(&maps.x, tx * TX, ty * TY, s * K);
-    tma_load_3d(dst, &maps.r[par], &mbar[sidx], tx * TX - H, ty * TY - H + a.ghost, s * K);
-    tma_load_3d(dst + FIELD, &maps.p[par], &mbar[sidx], tx * TX - H, ty * TY - H + a.ghost, s * K);
+    tma_load_3d(dst, &maps.r[par], &mbar[sidx], tx * TX - H, ty * TY - H + (SLAB ? a.ghost : 0), s * K);
+    tma_load_3d(dst + FIELD, &maps.p[par], &mbar[sidx], tx * TX - H, ty * TY - H + (SLAB ? a.ghost : 0), s * K);
   };
 
   int nact_prev = -1;
@@ -873,21 +892,21 @@ __global__ void __launch_bounds__(cg_threads(K), cg_min_blocks(K)) cg_persistent
       tc.xpass = xpass_of(it + 1);
       tc.alpha_prev = KCG_X2 ? st[s].alpha_last : 0.0;
       tc.kappa2 = __ldg(&sp->kappa2);
-      tc.hp = HITS ? a.hits + (size_t)__ldg(&sp->hits_plane) * ((size_t)a.rows * a.side) : nullptr;
+      tc.hp = HITS ? a.hits + (size_t)__ldg(&sp->hits_plane) * ((size_t)(SLAB ? a.rows : a.side) * a.side) : nullptr;
       tc.bar = &mbar[sidx];
       tc.phase = sidx ? phase1 : phase0;
       tc.part_out = a.partials + (((size_t)par_out * a.n_sys + s) * tps + tile) * NP;
       tc.dump = (KCG_TRACE == 2 && a.trace && it < 0 && blockIdx.x == 0 && i == 0)
                     ? reinterpret_cast<double*>(a.trace) : nullptr;
-      const int gy0 = a.row0 + tc.y0;
+      const int gy0 = (SLAB ? a.row0 : 0) + tc.y0;
       const bool interior = tc.x0 >= H && tc.x0 + TX + H <= a.side && gy0 >= H && gy0 + TY + H <= a.side &&
-                            tc.y0 + TY <= a.rows;
+                            tc.y0 + TY <= (SLAB ? a.rows : a.side);
       if (cg_xtma(K) && xtma) {
-        if (interior) cg_tile<K, false, HITS, cg_xtma(K), PREC>(a, tc, tred[i & 1]);
-        else cg_tile<K, true, HITS, cg_xtma(K), PREC>(a, tc, tred[i & 1]);
+        if (interior) cg_tile<K, false, HITS, cg_xtma(K), PREC, SLAB>(a, tc, tred[i & 1]);
+        else cg_tile<K, true, HITS, cg_xtma(K), PREC, SLAB>(a, tc, tred[i & 1]);
       } else {
-        if (interior) cg_tile<K, false, HITS, false, PREC>(a, tc, tred[i & 1]);
-        else cg_tile<K, true, HITS, false, PREC>(a, tc, tred[i & 1]);
+        if (interior) cg_tile<K, false, HITS, false, PREC, SLAB>(a, tc, tred[i & 1]);
+        else cg_tile<K, true, HITS, false, PREC, SLAB>(a, tc, tred[i & 1]);
       }
       if (sidx) phase1 ^= 1u; else phase0 ^= 1u;
       prev_part = tc.part_out;
@@ -1123,7 +1142,7 @@ template <int K, bool HITS, bool PREC>
 static cudaError_t cg_config_t(int n_sys, int* max_grid, size_t* smem) {
   const size_t sm = cg_stages(K) * (size_t)cg_stage_bytes(K) + (PREC ? (size_t)cg_ubox_bytes(K) : 0) +
                     (size_t)n_sys * (sizeof(SysState) + sizeof(int));
-  auto kern = cg_persistent_kernel<K, HITS, PREC>;
+  auto kern = cg_persistent_kernel<K, HITS, PREC, false>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
   if (e != cudaSuccess) return e;
   int nb = 0, dev = 0, nsm = 0;
@@ -1165,7 +1184,7 @@ cudaError_t cg_kernel_config(int K, bool hits, bool prec, int n_sys, int* max_gr
 template <int K, bool HITS, bool PREC>
 static cudaError_t launch_cg_t(cudaStream_t s, const CgArgs& a, const CgMaps& m, int grid, size_t smem) {
   void* args[2] = {(void*)&a, (void*)&m};
-  return cudaLaunchCooperativeKernel((const void*)cg_persistent_kernel<K, HITS, PREC>, dim3(grid),
+  return cudaLaunchCooperativeKernel((const void*)cg_persistent_kernel<K, HITS, PREC, false>, dim3(grid),
                                      dim3(cg_threads(K)), args, smem, s);
 }
 
