@@ -152,6 +152,43 @@ KCG_API const char* kcg_last_error(const kcg_ctx* ctx);
 /* Name of a status code (static string). */
 KCG_API const char* kcg_status_string(int status);
 
+/* ---------------------------------------------------------------- row-slab decomposition
+ * One face split into G row slabs: rank r holds the rows
+ * [r side/G, (r+1) side/G) of every face of the context and exchanges two halo rows of r and p
+ * with each neighbour every iteration -- stored by the CG kernel straight into the neighbour's
+ * ghost rows (peer memory over NVLink, or the same GPU when emulated) -- plus one cross-rank sum
+ * of the CG scalars per iteration (per-rank slots + system-scope flags, rank-ordered sum: every
+ * rank computes identical scalars).  A context drives `nlocal` ranks: 1 (one process per GPU) or
+ * all G (every rank emulated on this GPU in one cooperative launch, one CTA group per rank).
+ * Layouts for a slab context: Y [nlocal][P][n][rows][side], mu [nlocal][P][k][rows][side],
+ * hits [nlocal][P][rows][side]; rows = side / G.  All ranks must create their contexts before
+ * any of them solves, and must issue the same sequence of solve / apply calls.              */
+typedef struct {
+  int nranks;            /* G: ranks sharing every face, 1..8; side % G == 0, side / G >= 4       */
+  int rank0;             /* first (global) rank handled by this context                          */
+  int nlocal;            /* 1 or nranks (emulation)                                               */
+  void* peer_ws[8];      /* workspace of every rank [0, nranks), device addresses valid in this   */
+                         /* process (own ranks' allocations; peers' through kcg_ipc_import); each */
+                         /* kron_cg_workspace_size_slab bytes, 256-byte aligned, caller-owned     */
+} kcg_slab;
+
+/* Bytes of workspace per rank for a slab context of `nranks` ranks (0 on bad input). */
+KCG_API size_t kron_cg_workspace_size_slab(const kcg_desc* desc, int nranks);
+
+/* As kron_cg_create, for ranks [slab->rank0, slab->rank0 + slab->nlocal).  ws_bytes = the size of
+ * each rank's workspace.  KCG_E_SHAPE if side is not divisible into >= 4-row slabs.             */
+KCG_API kcg_status kron_cg_create_slab(const kcg_desc* desc, const kcg_slab* slab, const double* A_host,
+                               const double* noise_prec_host, const double* prior_scale_host,
+                               const double* kappa2_host, const double* hits_dev, size_t ws_bytes,
+                               void* stream, kcg_ctx** out);
+
+/* CUDA IPC for the slab peers: export the allocation holding dev_ptr (64-byte handle + the
+ * pointer's offset inside it); import a peer's handle (returns the mapped pointer and the mapping
+ * base to close with kcg_ipc_close after the context is destroyed).                            */
+KCG_API kcg_status kcg_ipc_export(const void* dev_ptr, unsigned char handle[64], size_t* offset);
+KCG_API kcg_status kcg_ipc_import(const unsigned char handle[64], size_t offset, void** dev_ptr, void** base);
+KCG_API kcg_status kcg_ipc_close(void* base);
+
 /* Release host-side state.  Does not free the caller's workspace. */
 KCG_API void kron_cg_destroy(kcg_ctx* ctx);
 

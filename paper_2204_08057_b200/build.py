@@ -11,8 +11,8 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "lib", "libkroncg.so")
-SOURCES = ["kcg_kernels.cu", "kcg_host.cu"]
-HEADERS = ["kcg_internal.h", os.path.join("..", "..", "include", "kroncg.h")]
+SOURCES = ["kcg_kernels.cu", "kcg_host.cu"] + [f"kcg_cg_k{K}.cu" for K in range(1, 9)]
+HEADERS = ["kcg_internal.h", "kcg_cg.cuh", os.path.join("..", "..", "include", "kroncg.h")]
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
@@ -45,15 +45,19 @@ def build(force: bool = False, verbose: bool = False, defines=(), out: str = Non
         return LIB
     os.makedirs(os.path.dirname(LIB), exist_ok=True)
     nvcc = _nvcc()
-    objs = []
-    for s in SOURCES:
-        obj = os.path.join(os.path.dirname(LIB), s.replace(".cu", ".o"))
+    objs, cmds = [], []
+    for src in SOURCES:
+        obj = os.path.join(os.path.dirname(LIB), src.replace(".cu", ".o"))
         obj = obj + "." + str(abs(hash((LIB,) + tuple(defines)))) + ".o"
-        cmd = [nvcc, *NVCC_FLAGS, *[f"-D{d}" for d in defines], "-c", os.path.join(CSRC, s), "-o", obj]
-        if verbose:
-            print(" ".join(cmd), file=sys.stderr)
-        subprocess.run(cmd, check=True)
+        cmds.append([nvcc, *NVCC_FLAGS, *[f"-D{d}" for d in defines], "-c", os.path.join(CSRC, src), "-o", obj])
         objs.append(obj)
+    # the per-K CG instantiations are independent translation units: compile them in parallel
+    from concurrent.futures import ThreadPoolExecutor
+    with ThreadPoolExecutor(min(len(cmds), os.cpu_count() or 4)) as ex:
+        for cmd in cmds:
+            if verbose:
+                print(" ".join(cmd), file=sys.stderr)
+        list(ex.map(lambda cmd: subprocess.run(cmd, check=True), cmds))
     tmp = LIB + ".tmp"
     cmd = [nvcc, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", tmp, *objs,
            "-Xcompiler", "-fvisibility=hidden"]

@@ -2,14 +2,21 @@
 //
 // Responsibilities: descriptor/argument validation, workspace carving (caller-owned device memory,
 // no allocation after create), the small dense algebra of setup step a1 (M = A^T T A, E = T A,
-// Lemma 2's eigh(M, P) by a cyclic Jacobi eigensolver), TMA descriptor encoding, stream-ordered
-// kernel launches, CUDA-event timing and the solve report.
+// Lemma 2's eigh(M, P) by a cyclic Jacobi eigensolver, pixel-block Jacobi inverses), TMA
+// descriptor encoding, stream-ordered kernel launches, CUDA-event timing and the solve report.
+//
+// Row-slab mode: every face is split into G row slabs, one per rank;
+// a context drives `nlocal` ranks -- 1 (one process per GPU, peers reached through IPC-mapped
+// workspaces) or all G (every rank emulated on this GPU: one cooperative launch, one CTA group per
+// rank).  Each rank's state lives in its own workspace (RankState); the non-slab context is the
+// one-rank case with no ghost rows.
 #include <cudaTypedefs.h>
 
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <memory>
 #include <string>
 #include <vector>
 
@@ -18,38 +25,143 @@
 
 using kcg::CgArgs;
 using kcg::CgMaps;
+using kcg::CgSlabLaunch;
+using kcg::SlabGeom;
 using kcg::SysParams;
 using kcg::SysState;
+
+namespace {
+
+const size_t kAlign = 256;
+size_t align_up(size_t x) { return (x + kAlign - 1) / kAlign * kAlign; }
+const unsigned long long kPostTag = 1ull << 31;  // tags of the post-CG rendezvous of a solve
+
+// Per-rank workspace carving.
+struct Layout {
+  size_t r0, r1, p0, p1, partials, state, history, sync, group, resid_partials, resid_out, params_kron, params_syl,
+      E_kron, E_syl, W, Y_stage, mu_stage, trace, slots, flags, xg_top, xg_bot, rslots, total;
+  size_t vec_doubles, partial_doubles;
+};
+
+int tiles_x(int side, int K) { return (side + KCG_TX - 1) / KCG_TX; }
+int tiles_y(int rows, int K) { return (rows + kcg::cg_tile_y(K) - 1) / kcg::cg_tile_y(K); }
+
+// One rank's layout: `rows` local rows (side / nranks), r/p buffers with `ghost` ghost rows.
+Layout layout_of(const kcg_desc* d, int nranks) {
+  Layout L{};
+  const int side = 1 << d->level;
+  const int rows = side / nranks;
+  const int ghost = nranks > 1 ? KCG_HALO : 0;
+  const int pitch = side < 2 ? 2 : side;  // TMA global strides must be multiples of 16 bytes
+  const size_t N = (size_t)rows * side;
+  const size_t P = d->n_patches, n = d->n_freq, k = d->n_comp;
+  L.vec_doubles = P * k * (size_t)pitch * (rows + 2 * ghost);
+  const size_t tk = (size_t)tiles_x(side, (int)k) * tiles_y(rows, (int)k);
+  const size_t ts = (size_t)tiles_x(side, 1) * tiles_y(rows, 1);
+  L.partial_doubles = 2 * std::max(P * tk, P * k * ts) * 3;  // [2 parities][systems][tiles][<= 3]
+  size_t off = 0;
+  auto take = [&](size_t bytes) { size_t o = off; off += align_up(bytes); return o; };
+  L.r0 = take(L.vec_doubles * 8);
+  L.r1 = take(L.vec_doubles * 8);
+  L.p0 = take(L.vec_doubles * 8);
+  L.p1 = take(L.vec_doubles * 8);
+  L.partials = take(L.partial_doubles * 8);
+  L.state = take(P * k * sizeof(SysState));
+  L.history = take((size_t)std::max(d->history_cap, 1) * 8);
+  L.sync = take(4 * sizeof(unsigned));
+  L.group = take(4 * sizeof(unsigned));
+  L.resid_partials = take(P * (size_t)kcg::apply_tiles_per_sys(rows, side) * 2 * 8);
+  L.resid_out = take(P * 2 * 8);
+  L.params_kron = take(P * sizeof(SysParams));
+  L.params_syl = take(P * k * sizeof(SysParams));
+  L.E_kron = take(P * n * k * 8);
+  L.E_syl = take(P * n * k * 8);
+  L.W = take(P * k * k * 8);
+  L.trace = KCG_TRACE ? take((size_t)KCG_TRACE_ITERS * KCG_TRACE_COLS * 8) : 0;
+  if (d->host_staging) {
+    L.Y_stage = take(P * n * N * 8);
+    L.mu_stage = take(P * k * N * 8);
+  }
+  // cross-rank areas (written by peers)
+  L.slots = take(2 * P * k * (size_t)nranks * 3 * 8);
+  L.flags = take(KCG_GMAX * sizeof(unsigned long long));
+  L.xg_top = take(P * k * (size_t)side * 8);
+  L.xg_bot = take(P * k * (size_t)side * 8);
+  L.rslots = take((size_t)nranks * P * 2 * 8);
+  L.total = off;
+  return L;
+}
+
+// One rank's device state (pointers into its workspace) and TMA descriptors.
+struct RankState {
+  int rank = 0, row0 = 0;
+  char* ws = nullptr;
+  double* r[2] = {nullptr, nullptr};
+  double* p[2] = {nullptr, nullptr};
+  double *partials = nullptr, *history = nullptr, *resid_partials = nullptr, *resid_out = nullptr;
+  SysState* state = nullptr;
+  unsigned *sync = nullptr, *group = nullptr;
+  SysParams *params_kron = nullptr, *params_syl = nullptr;
+  double *E_kron = nullptr, *E_syl = nullptr, *W_dev = nullptr, *Y_stage = nullptr, *mu_stage = nullptr;
+  long long* trace = nullptr;
+  double *slots = nullptr, *xg_top = nullptr, *xg_bot = nullptr, *rslots = nullptr;
+  unsigned long long* flags = nullptr;
+  const double* hits = nullptr;
+  CgMaps maps_kron, maps_syl;
+};
+
+RankState carve(char* ws, const Layout& L, int rank, int rows, bool staging) {
+  RankState R;
+  R.rank = rank;
+  R.row0 = rank * rows;
+  R.ws = ws;
+  R.r[0] = reinterpret_cast<double*>(ws + L.r0);
+  R.r[1] = reinterpret_cast<double*>(ws + L.r1);
+  R.p[0] = reinterpret_cast<double*>(ws + L.p0);
+  R.p[1] = reinterpret_cast<double*>(ws + L.p1);
+  R.partials = reinterpret_cast<double*>(ws + L.partials);
+  R.state = reinterpret_cast<SysState*>(ws + L.state);
+  R.history = reinterpret_cast<double*>(ws + L.history);
+  R.sync = reinterpret_cast<unsigned*>(ws + L.sync);
+  R.group = reinterpret_cast<unsigned*>(ws + L.group);
+  R.resid_partials = reinterpret_cast<double*>(ws + L.resid_partials);
+  R.resid_out = reinterpret_cast<double*>(ws + L.resid_out);
+  R.params_kron = reinterpret_cast<SysParams*>(ws + L.params_kron);
+  R.params_syl = reinterpret_cast<SysParams*>(ws + L.params_syl);
+  R.E_kron = reinterpret_cast<double*>(ws + L.E_kron);
+  R.E_syl = reinterpret_cast<double*>(ws + L.E_syl);
+  R.W_dev = reinterpret_cast<double*>(ws + L.W);
+  if (KCG_TRACE) R.trace = reinterpret_cast<long long*>(ws + L.trace);
+  if (staging) {
+    R.Y_stage = reinterpret_cast<double*>(ws + L.Y_stage);
+    R.mu_stage = reinterpret_cast<double*>(ws + L.mu_stage);
+  }
+  R.slots = reinterpret_cast<double*>(ws + L.slots);
+  R.flags = reinterpret_cast<unsigned long long*>(ws + L.flags);
+  R.xg_top = reinterpret_cast<double*>(ws + L.xg_top);
+  R.xg_bot = reinterpret_cast<double*>(ws + L.xg_bot);
+  R.rslots = reinterpret_cast<double*>(ws + L.rslots);
+  return R;
+}
+
+}  // namespace
 
 struct kcg_ctx {
   kcg_desc d;
   cudaStream_t stream = nullptr;
   int side = 0, pitch = 0, P = 0, n = 0, k = 0;
-  size_t N = 0;
-  char* ws = nullptr;
+  int nranks = 1, rank0 = 0, nlocal = 1, rows = 0, ghost = 0;
+  size_t N = 0;  // local pixels per plane (rows * side)
   size_t ws_bytes = 0, ws_need = 0;
-  double* r[2] = {nullptr, nullptr};
-  double* p[2] = {nullptr, nullptr};
-  double* partials = nullptr;
-  SysState* state = nullptr;
-  double* history = nullptr;
-  double* resid_partials = nullptr;
-  double* resid_out = nullptr;
-  SysParams* params_kron = nullptr;
-  SysParams* params_syl = nullptr;
-  double* E_kron = nullptr;
-  double* E_syl = nullptr;
-  double* W_dev = nullptr;
-  long long* trace = nullptr;
-  unsigned* sync = nullptr;
-  double* Y_stage = nullptr;
-  double* mu_stage = nullptr;
-  const double* hits = nullptr;
-  std::vector<double> rho, W;  // host copies [P][k], [P][k][k]
-  CgMaps maps_kron, maps_syl;
+  bool slab = false;
+  std::vector<RankState> R;            // local ranks
+  std::vector<char*> peer_ws;          // every rank's workspace (slab mode)
+  Layout L;
+  std::vector<double> rho, W;          // host copies [P][k], [P][k][k]
   int tiles_x_kron = 0, tiles_y_kron = 0, tiles_x_syl = 0, tiles_y_syl = 0;
-  int grid_kron = 0, grid_syl = 0;
+  int grid_kron = 0, grid_syl = 0;     // CTAs (per rank in slab mode)
   size_t smem_kron = 0, smem_syl = 0;
+  unsigned long long solve_id = 0;     // cross-rank operations so far (identical on every rank)
   cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
   std::vector<SysState> st_host;
   std::vector<double> resid_host;
@@ -57,15 +169,6 @@ struct kcg_ctx {
 };
 
 namespace {
-
-const size_t kAlign = 256;
-size_t align_up(size_t x) { return (x + kAlign - 1) / kAlign * kAlign; }
-
-struct Layout {
-  size_t r0, r1, p0, p1, partials, state, history, resid_partials, resid_out, params_kron, params_syl, E_kron,
-      E_syl, W, Y_stage, mu_stage, trace, sync, total;
-  size_t vec_doubles, partial_doubles;
-};
 
 bool desc_ok(const kcg_desc* d, std::string* why) {
   char buf[256];
@@ -90,46 +193,14 @@ bool config_ok(const kcg_desc* d, std::string* why) {
   return true;
 }
 
-// Tile grid of the CG kernel (64 x cg_tile_y(K) tiles).
-int tiles_x(int side, int K) { return (side + KCG_TX - 1) / KCG_TX; }
-int tiles_y(int side, int K) { return (side + kcg::cg_tile_y(K) - 1) / kcg::cg_tile_y(K); }
-
-Layout layout_of(const kcg_desc* d) {
-  Layout L{};
+bool slab_ok(const kcg_desc* d, int nranks, std::string* why) {
+  if (nranks < 1 || nranks > KCG_GMAX) { *why = "nranks outside [1,8]"; return false; }
   const int side = 1 << d->level;
-  const int pitch = side < 2 ? 2 : side;  // TMA global strides must be multiples of 16 bytes
-  const size_t N = (size_t)side * side;
-  const size_t P = d->n_patches, n = d->n_freq, k = d->n_comp;
-  L.vec_doubles = P * k * (size_t)pitch * side;
-  const size_t tk = (size_t)tiles_x(side, (int)k) * tiles_y(side, (int)k);
-  const size_t ts = (size_t)tiles_x(side, 1) * tiles_y(side, 1);
-  L.partial_doubles = 2 * std::max(P * tk, P * k * ts) * 3;  // [2 parities][systems][tiles][<= 3]
-  size_t off = 0;
-  auto take = [&](size_t bytes) { size_t o = off; off += align_up(bytes); return o; };
-  L.r0 = take(L.vec_doubles * 8);
-  L.r1 = take(L.vec_doubles * 8);
-  L.p0 = take(L.vec_doubles * 8);
-  L.p1 = take(L.vec_doubles * 8);
-  L.partials = take(L.partial_doubles * 8);
-  L.state = take(P * k * sizeof(SysState));
-  L.history = take((size_t)std::max(d->history_cap, 1) * 8);
-  L.sync = take(4 * sizeof(unsigned));
-  L.resid_partials = take(P * (size_t)kcg::apply_tiles_per_sys(side) * 2 * 8);
-  L.resid_out = take(P * 2 * 8);
-  L.params_kron = take(P * sizeof(SysParams));
-  L.params_syl = take(P * k * sizeof(SysParams));
-  L.E_kron = take(P * n * k * 8);
-  L.E_syl = take(P * n * k * 8);
-  L.W = take(P * k * k * 8);
-  L.trace = KCG_TRACE ? take((size_t)KCG_TRACE_ITERS * KCG_TRACE_COLS * 8) : 0;
-  if (d->host_staging) {
-    L.Y_stage = take(P * n * N * 8);
-    L.mu_stage = take(P * k * N * 8);
-  } else {
-    L.Y_stage = L.mu_stage = 0;
+  if (nranks > 1 && (side % nranks != 0 || side / nranks < 2 * KCG_HALO)) {
+    *why = "row slabs need side % nranks == 0 and side / nranks >= 4";
+    return false;
   }
-  L.total = off;
-  return L;
+  return true;
 }
 
 // Symmetric eigendecomposition C = V diag(lam) V^T by cyclic Jacobi rotations (k <= 8).
@@ -243,13 +314,14 @@ PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
   return fn;
 }
 
-bool encode_map(CUtensorMap* m, double* base, int side, int pitch, size_t planes, int K, std::string* why) {
+bool encode_map(CUtensorMap* m, double* base, int side, int buf_rows, int pitch, size_t planes, int K,
+                std::string* why) {
   const int bx = KCG_TX + 2 * KCG_HALO;
   const int by = kcg::cg_tile_y(K) + 2 * KCG_HALO;
   auto enc = get_encode();
   if (!enc) { *why = "cuTensorMapEncodeTiled unavailable"; return false; }
-  cuuint64_t dims[3] = {(cuuint64_t)side, (cuuint64_t)side, (cuuint64_t)planes};
-  cuuint64_t strides[2] = {(cuuint64_t)pitch * 8, (cuuint64_t)pitch * side * 8};
+  cuuint64_t dims[3] = {(cuuint64_t)side, (cuuint64_t)buf_rows, (cuuint64_t)planes};
+  cuuint64_t strides[2] = {(cuuint64_t)pitch * 8, (cuuint64_t)pitch * buf_rows * 8};
   cuuint32_t box[3] = {(cuuint32_t)bx, (cuuint32_t)by, (cuuint32_t)K};
   cuuint32_t es[3] = {1, 1, 1};
   CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, base, dims, strides, box, es,
@@ -265,11 +337,11 @@ bool encode_map(CUtensorMap* m, double* base, int side, int pitch, size_t planes
 }
 
 // TMA descriptor of the solution buffer x [planes][side][side] with box {64, TY(K), K} (CTA kernel).
-bool encode_xmap(CUtensorMap* m, double* base, int side, size_t planes, int K, std::string* why) {
+bool encode_xmap(CUtensorMap* m, double* base, int side, int rows, size_t planes, int K, std::string* why) {
   auto enc = get_encode();
   if (!enc) { *why = "cuTensorMapEncodeTiled unavailable"; return false; }
-  cuuint64_t dims[3] = {(cuuint64_t)side, (cuuint64_t)side, (cuuint64_t)planes};
-  cuuint64_t strides[2] = {(cuuint64_t)side * 8, (cuuint64_t)side * side * 8};
+  cuuint64_t dims[3] = {(cuuint64_t)side, (cuuint64_t)rows, (cuuint64_t)planes};
+  cuuint64_t strides[2] = {(cuuint64_t)side * 8, (cuuint64_t)side * rows * 8};
   cuuint32_t box[3] = {(cuuint32_t)KCG_TX, (cuuint32_t)kcg::cg_tile_y(K), (cuuint32_t)K};
   cuuint32_t es[3] = {1, 1, 1};
   CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, base, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
@@ -302,6 +374,58 @@ kcg_status cuda_fail(kcg_ctx* c, cudaError_t e, const char* what) {
 
 enum Route { ROUTE_KRON = 0, ROUTE_SYL = 1 };
 
+SlabGeom geom_of(const kcg_ctx* c, const RankState& R) {
+  return SlabGeom{c->side, c->rows, R.row0, c->pitch, c->ghost, c->ghost};
+}
+
+// Device pointer of `field` in rank g's workspace (same layout on every rank).
+template <typename T>
+T* peer_ptr(const kcg_ctx* c, int g, size_t off) { return reinterpret_cast<T*>(c->peer_ws[g] + off); }
+
+kcg::XrankSync xsync_of(const kcg_ctx* c, unsigned long long tag) {
+  kcg::XrankSync X{};
+  for (int g = 0; g < c->nranks; ++g) X.flags[g] = peer_ptr<unsigned long long>(c, g, c->L.flags);
+  X.nranks = c->nranks;
+  X.rank0 = c->rank0;
+  X.nlocal = c->nlocal;
+  X.tag = tag;
+  return X;
+}
+
+// Fill the slab fields of a rank's CgArgs (peers' ghosted buffers, slots, flags).
+void fill_slab_args(const kcg_ctx* c, const RankState& R, CgArgs* a) {
+  a->rank = R.rank;
+  a->nranks = c->nranks;
+  for (int dir = 0; dir < 2; ++dir) {
+    const int g = R.rank + (dir == 0 ? -1 : 1);
+    for (int b = 0; b < 2; ++b) {
+      const bool ok = g >= 0 && g < c->nranks;
+      a->nb_r[dir][b] = ok ? peer_ptr<double>(c, g, b ? c->L.r1 : c->L.r0) : nullptr;
+      a->nb_p[dir][b] = ok ? peer_ptr<double>(c, g, b ? c->L.p1 : c->L.p0) : nullptr;
+    }
+  }
+  for (int g = 0; g < KCG_GMAX; ++g) {
+    a->slots[g] = g < c->nranks ? peer_ptr<double>(c, g, c->L.slots) : nullptr;
+    a->flags[g] = g < c->nranks ? peer_ptr<unsigned long long>(c, g, c->L.flags) : nullptr;
+  }
+  a->my_flags = R.flags;
+  a->my_slots = R.slots;
+  a->group = R.group;
+}
+
+// x boundary rows of every local rank into its neighbours' xg_top / xg_bot, then a rendezvous.
+kcg_status exchange_x_rows(kcg_ctx* c, const double* x_all, size_t x_rank_stride, unsigned long long tag) {
+  cudaStream_t s = c->stream;
+  for (int j = 0; j < c->nlocal; ++j) {
+    const RankState& R = c->R[j];
+    double* up = R.rank > 0 ? peer_ptr<double>(c, R.rank - 1, c->L.xg_bot) : nullptr;
+    double* dn = R.rank + 1 < c->nranks ? peer_ptr<double>(c, R.rank + 1, c->L.xg_top) : nullptr;
+    CK(kcg::launch_xghost(s, x_all + j * x_rank_stride, up, dn, c->P * c->k, geom_of(c, R)), "x ghost kernel");
+  }
+  CK(kcg::launch_xrank_sync(s, xsync_of(c, tag)), "rendezvous kernel");
+  return KCG_OK;
+}
+
 kcg_status solve_impl(kcg_ctx* c, Route route, const double* Y_in, double* mu_out, bool host_io, double tol,
                       int max_iter, kcg_report* rep) {
   if (!c) return KCG_E_ARG;
@@ -310,71 +434,135 @@ kcg_status solve_impl(kcg_ctx* c, Route route, const double* Y_in, double* mu_ou
   if (max_iter < 0) { c->err = "max_iter < 0"; return KCG_E_ARG; }
   if (host_io && !c->d.host_staging) { c->err = "host entry point needs desc.host_staging = 1"; return KCG_E_CONFIG; }
   cudaStream_t s = c->stream;
-  const int P = c->P, n = c->n, k = c->k, side = c->side;
+  const int P = c->P, n = c->n, k = c->k;
   const size_t N = c->N;
-  const double* Y = host_io ? c->Y_stage : Y_in;
-  double* mu = host_io ? c->mu_stage : mu_out;
+  const size_t y_stride = (size_t)P * n * N, mu_stride = (size_t)P * k * N;  // per local rank
+  const bool kron = route == ROUTE_KRON;
+  const int Kk = kron ? k : 1;
+  const int n_sys = kron ? P : P * k;
+  const bool prec = c->d.precond == KCG_PRECOND_BLOCK_JACOBI;
+  const unsigned long long tag0 = (++c->solve_id) << 32;
+  auto Yr = [&](int j) -> const double* { return host_io ? c->R[j].Y_stage : Y_in + j * y_stride; };
+  auto mur = [&](int j) -> double* { return host_io ? c->R[j].mu_stage : mu_out + j * mu_stride; };
 
   CK(cudaEventRecord(c->ev[0], s), "event");
-  if (host_io) CK(cudaMemcpyAsync(c->Y_stage, Y_in, (size_t)P * n * N * 8, cudaMemcpyHostToDevice, s), "H2D Y");
-  const bool kron = route == ROUTE_KRON;
-  CK(kcg::launch_rhs(k, s, Y, kron ? c->E_kron : c->E_syl, c->hits, c->r[0], c->p[0], mu, P, n, side, c->pitch),
-     "rhs kernel");
+  for (int j = 0; j < c->nlocal; ++j) {
+    RankState& R = c->R[j];
+    if (host_io) CK(cudaMemcpyAsync(R.Y_stage, Y_in + j * y_stride, y_stride * 8, cudaMemcpyHostToDevice, s), "H2D Y");
+    CK(kcg::launch_rhs(k, s, Yr(j), kron ? R.E_kron : R.E_syl, R.hits, R.r[0], R.p[0], mur(j), P, n, geom_of(c, R)),
+       "rhs kernel");
+  }
+  if (c->slab)
+    for (int j = 0; j < c->nlocal; ++j) {
+      const RankState& R = c->R[j];
+      double *ur = nullptr, *up = nullptr, *dr = nullptr, *dp = nullptr;
+      if (R.rank > 0) { ur = peer_ptr<double>(c, R.rank - 1, c->L.r0); up = peer_ptr<double>(c, R.rank - 1, c->L.p0); }
+      if (R.rank + 1 < c->nranks) { dr = peer_ptr<double>(c, R.rank + 1, c->L.r0); dp = peer_ptr<double>(c, R.rank + 1, c->L.p0); }
+      CK(kcg::launch_ghost_fill(s, R.r[0], R.p[0], ur, up, dr, dp, P * k, geom_of(c, R)), "ghost fill kernel");
+    }
   CK(cudaEventRecord(c->ev[1], s), "event");
 
-  CgArgs a;
-  a.params = kron ? c->params_kron : c->params_syl;
-  a.x = mu;
-  a.rbuf[0] = c->r[0]; a.rbuf[1] = c->r[1];
-  a.pbuf[0] = c->p[0]; a.pbuf[1] = c->p[1];
-  a.partials = c->partials;
-  a.state_out = c->state;
-  a.history = c->history;
-  a.history_cap = c->d.history_cap;
-  a.hits = c->hits;
-  a.side = side;
-  a.pitch = c->pitch;
-  a.rows = side;
-  a.row0 = 0;
-  a.ghost = 0;
-  a.n_sys = kron ? P : P * k;
-  a.tiles_x = kron ? c->tiles_x_kron : c->tiles_x_syl;
-  a.tiles_y = kron ? c->tiles_y_kron : c->tiles_y_syl;
-  a.tiles_per_sys = a.tiles_x * a.tiles_y;
-  a.max_iter = max_iter;
-  a.tol2 = tol * tol;
-  a.trace = c->trace;
-  a.sync = c->sync;
-  CK(cudaMemsetAsync(c->sync, 0, 4 * sizeof(unsigned), s), "memset sync");
-  const int Kk = kron ? k : 1;
-  CgMaps& maps = kron ? c->maps_kron : c->maps_syl;
-  a.x_tma = 0;
-  if (side >= 2 && (reinterpret_cast<uintptr_t>(mu) % 16) == 0) {
-    std::string why;
-    if (!encode_xmap(&maps.x, mu, side, (size_t)P * k, Kk, &why)) { c->err = why; return KCG_E_CUDA; }
-    a.x_tma = 1;
+  CgSlabLaunch* Lp = new CgSlabLaunch();  // large (TMA maps of every rank): heap, not stack
+  std::unique_ptr<CgSlabLaunch> L_owner(Lp);
+  CgSlabLaunch& Lx = *Lp;
+  for (int j = 0; j < c->nlocal; ++j) {
+    RankState& R = c->R[j];
+    CgArgs& a = Lx.a[j];
+    a = CgArgs{};
+    a.params = kron ? R.params_kron : R.params_syl;
+    a.x = mur(j);
+    a.rbuf[0] = R.r[0]; a.rbuf[1] = R.r[1];
+    a.pbuf[0] = R.p[0]; a.pbuf[1] = R.p[1];
+    a.partials = R.partials;
+    a.state_out = R.state;
+    a.history = R.history;
+    a.history_cap = c->d.history_cap;
+    a.hits = R.hits;
+    a.side = c->side;
+    a.pitch = c->pitch;
+    a.rows = c->rows;
+    a.row0 = R.row0;
+    a.ghost = c->ghost;
+    a.n_sys = n_sys;
+    a.tiles_x = kron ? c->tiles_x_kron : c->tiles_x_syl;
+    a.tiles_y = kron ? c->tiles_y_kron : c->tiles_y_syl;
+    a.tiles_per_sys = a.tiles_x * a.tiles_y;
+    a.max_iter = max_iter;
+    a.tol2 = tol * tol;
+    a.trace = R.trace;
+    a.sync = R.sync;
+    a.tag0 = tag0;
+    if (c->slab) fill_slab_args(c, R, &a);
+    CgMaps& maps = kron ? R.maps_kron : R.maps_syl;
+    a.x_tma = 0;
+    if (c->side >= 2 && (reinterpret_cast<uintptr_t>(a.x) % 16) == 0) {
+      std::string why;
+      if (!encode_xmap(&maps.x, a.x, c->side, c->rows, (size_t)P * k, Kk, &why)) { c->err = why; return KCG_E_CUDA; }
+      a.x_tma = 1;
+    }
+    Lx.m[j] = maps;
+    CK(cudaMemsetAsync(R.sync, 0, 4 * sizeof(unsigned), s), "memset sync");
+    CK(cudaMemsetAsync(R.group, 0, 4 * sizeof(unsigned), s), "memset group");
   }
-  CK(kcg::launch_cg(Kk, c->d.precond == KCG_PRECOND_BLOCK_JACOBI, s, a, maps, kron ? c->grid_kron : c->grid_syl,
-                    kron ? c->smem_kron : c->smem_syl),
-     "cg kernel");
+  if (c->slab) {
+    Lx.nlocal = c->nlocal;
+    Lx.ctas = kron ? c->grid_kron : c->grid_syl;
+    CK(kcg::launch_cg_slab(Kk, prec, s, Lx, kron ? c->smem_kron : c->smem_syl), "cg slab kernel");
+  } else {
+    CK(kcg::launch_cg(Kk, prec, s, Lx.a[0], Lx.m[0], kron ? c->grid_kron : c->grid_syl,
+                      kron ? c->smem_kron : c->smem_syl),
+       "cg kernel");
+  }
   CK(cudaEventRecord(c->ev[2], s), "event");
-  if (KCG_X2) CK(kcg::launch_xfix(Kk, s, c->state, c->p[0], c->p[1], mu, a.n_sys, side, c->pitch), "x fix-up kernel");
-  if (!kron) CK(kcg::launch_backtransform(k, s, c->W_dev, mu, P, side), "backtransform kernel");
-  CK(kcg::launch_resid(k, s, c->params_kron, mu, Y, c->E_kron, c->hits, c->resid_partials, c->resid_out, P, n, side),
-     "residual kernel");
-  c->st_host.resize(a.n_sys);
-  c->resid_host.resize((size_t)P * 2);
-  CK(cudaMemcpyAsync(c->st_host.data(), c->state, a.n_sys * sizeof(SysState), cudaMemcpyDeviceToHost, s), "D2H");
-  CK(cudaMemcpyAsync(c->resid_host.data(), c->resid_out, (size_t)P * 2 * 8, cudaMemcpyDeviceToHost, s), "D2H");
-  if (host_io) CK(cudaMemcpyAsync(mu_out, c->mu_stage, (size_t)P * k * N * 8, cudaMemcpyDeviceToHost, s), "D2H mu");
+  for (int j = 0; j < c->nlocal; ++j) {
+    RankState& R = c->R[j];
+    if (KCG_X2) CK(kcg::launch_xfix(Kk, s, R.state, R.p[0], R.p[1], mur(j), n_sys, geom_of(c, R)), "x fix-up kernel");
+    if (!kron) CK(kcg::launch_backtransform(k, s, R.W_dev, mur(j), P, N), "backtransform kernel");
+  }
+  // true residual ||b - G x|| / ||b|| (one apply pass; x boundary rows exchanged in slab mode)
+  if (c->slab) {
+    for (int j = 0; j < c->nlocal; ++j) {
+      const RankState& R = c->R[j];
+      double* up = R.rank > 0 ? peer_ptr<double>(c, R.rank - 1, c->L.xg_bot) : nullptr;
+      double* dn = R.rank + 1 < c->nranks ? peer_ptr<double>(c, R.rank + 1, c->L.xg_top) : nullptr;
+      CK(kcg::launch_xghost(s, mur(j), up, dn, P * k, geom_of(c, R)), "x ghost kernel");
+    }
+    CK(kcg::launch_xrank_sync(s, xsync_of(c, tag0 + kPostTag + 1)), "rendezvous kernel");
+  }
+  for (int j = 0; j < c->nlocal; ++j) {
+    RankState& R = c->R[j];
+    CK(kcg::launch_resid(k, s, R.params_kron, mur(j), Yr(j), R.E_kron, R.hits, R.resid_partials, R.resid_out, P, n,
+                         geom_of(c, R), c->slab ? R.xg_top : nullptr, c->slab ? R.xg_bot : nullptr),
+       "residual kernel");
+    if (c->slab) {
+      kcg::XrankPut Pt{};
+      for (int g = 0; g < c->nranks; ++g) Pt.dst[g] = peer_ptr<double>(c, g, c->L.rslots);
+      Pt.src = R.resid_out;
+      Pt.count = P * 2;
+      Pt.rank = R.rank;
+      Pt.nranks = c->nranks;
+      CK(kcg::launch_put(s, Pt), "put kernel");
+    }
+  }
+  if (c->slab) CK(kcg::launch_xrank_sync(s, xsync_of(c, tag0 + kPostTag + 2)), "rendezvous kernel");
+  c->st_host.resize(n_sys);
+  const int nr = c->slab ? c->nranks : 1;
+  c->resid_host.resize((size_t)nr * P * 2);
+  CK(cudaMemcpyAsync(c->st_host.data(), c->R[0].state, n_sys * sizeof(SysState), cudaMemcpyDeviceToHost, s), "D2H");
+  CK(cudaMemcpyAsync(c->resid_host.data(), c->slab ? c->R[0].rslots : c->R[0].resid_out, (size_t)nr * P * 2 * 8,
+                     cudaMemcpyDeviceToHost, s),
+     "D2H");
+  if (host_io)
+    for (int j = 0; j < c->nlocal; ++j)
+      CK(cudaMemcpyAsync(mu_out + j * mu_stride, c->R[j].mu_stage, mu_stride * 8, cudaMemcpyDeviceToHost, s), "D2H mu");
   CK(cudaEventRecord(c->ev[3], s), "event");
   CK(cudaStreamSynchronize(s), "solve");
 
-  // report
+  // report (every rank holds the same scalars; residual sums added over ranks in rank order)
   int worst = KCG_OK, maxit = 0, allconv = 1;
   long long sumit = 0, passes = 0, xpasses = 0;
   double maxrel = 0.0;
-  for (int i = 0; i < a.n_sys; ++i) {
+  for (int i = 0; i < n_sys; ++i) {
     const SysState& z = c->st_host[i];
     maxit = std::max(maxit, z.iters);
     sumit += z.iters;
@@ -391,7 +579,11 @@ kcg_status solve_impl(kcg_ctx* c, Route route, const double* Y_in, double* mu_ou
   }
   double maxtrue = 0.0;
   for (int p = 0; p < P; ++p) {
-    const double r2 = c->resid_host[2 * p], b2 = c->resid_host[2 * p + 1];
+    double r2 = 0.0, b2 = 0.0;
+    for (int g = 0; g < nr; ++g) {
+      r2 += c->resid_host[((size_t)g * P + p) * 2];
+      b2 += c->resid_host[((size_t)g * P + p) * 2 + 1];
+    }
     maxtrue = std::max(maxtrue, b2 > 0 ? std::sqrt(r2 / b2) : std::sqrt(r2));
   }
   if (rep) {
@@ -401,20 +593,21 @@ kcg_status solve_impl(kcg_ctx* c, Route route, const double* Y_in, double* mu_ou
     rep->status = worst;
     rep->converged = allconv;
     rep->iterations = maxit;
-    rep->n_systems = a.n_sys;
+    rep->n_systems = n_sys;
     if (rep->iterations_per)
-      for (int i = 0; i < a.n_sys; ++i) rep->iterations_per[i] = c->st_host[i].iters;
+      for (int i = 0; i < n_sys; ++i) rep->iterations_per[i] = c->st_host[i].iters;
     rep->rel_residual = maxrel;
     rep->rel_residual_true = maxtrue;
     rep->wall_time_s = t03 * 1e-3;
     rep->loop_time_s = t12 * 1e-3;
     rep->system_iterations = sumit;
-    // per pass: read + write r and p (32 B per pixel and plane); x passes also read + write x
-    rep->loop_bytes = (32.0 * (double)passes + 16.0 * (double)xpasses) * (kron ? k : 1) * (double)N;
+    // per pass: read + write r and p (32 B per pixel and plane); x passes also read + write x.
+    // Local bytes of this context's ranks (slab mode: the local rows of each local rank).
+    rep->loop_bytes = (32.0 * (double)passes + 16.0 * (double)xpasses) * Kk * (double)N * c->nlocal;
     rep->peak_mem_bytes = c->ws_need;
     rep->history_len = std::min(maxit, c->d.history_cap);
     if (rep->history && rep->history_len > 0) {
-      cudaError_t e = cudaMemcpy(rep->history, c->history, (size_t)rep->history_len * 8, cudaMemcpyDeviceToHost);
+      cudaError_t e = cudaMemcpy(rep->history, c->R[0].history, (size_t)rep->history_len * 8, cudaMemcpyDeviceToHost);
       if (e != cudaSuccess) return cuda_fail(c, e, "D2H history");
     }
   }
@@ -424,17 +617,12 @@ kcg_status solve_impl(kcg_ctx* c, Route route, const double* Y_in, double* mu_ou
 
 }  // namespace
 
-extern "C" {
+namespace {
 
-size_t kron_cg_workspace_size(const kcg_desc* d) {
-  std::string why;
-  if (!desc_ok(d, &why)) return 0;
-  return layout_of(d).total;
-}
-
-kcg_status kron_cg_create(const kcg_desc* d, const double* A_host, const double* T_host, const double* phi_host,
-                          const double* kappa2_host, const double* hits_dev, void* workspace_dev, size_t ws_bytes,
-                          void* stream, kcg_ctx** out) {
+// Shared body of kron_cg_create / kron_cg_create_slab.
+kcg_status create_impl(const kcg_desc* d, const kcg_slab* sl, const double* A_host, const double* T_host,
+                       const double* phi_host, const double* kappa2_host, const double* hits_dev, void* workspace_dev,
+                       size_t ws_bytes, void* stream, kcg_ctx** out) {
   if (!out) return KCG_E_ARG;
   *out = nullptr;
   kcg_ctx* c = new kcg_ctx();
@@ -447,9 +635,11 @@ kcg_status kron_cg_create(const kcg_desc* d, const double* A_host, const double*
   if (!desc_ok(d, &why)) return fail(KCG_E_SHAPE, why);
   c->d = *d;
   if (!config_ok(d, &why)) return fail(KCG_E_CONFIG, why);
+  const int G = sl ? sl->nranks : 1;
+  if (!slab_ok(d, G, &why)) return fail(KCG_E_SHAPE, why);
+  if (sl && (sl->rank0 < 0 || sl->nlocal < 1 || sl->rank0 + sl->nlocal > G || (sl->nlocal != 1 && sl->nlocal != G)))
+    return fail(KCG_E_CONFIG, "slab: need 0 <= rank0, rank0 + nlocal <= nranks and nlocal in {1, nranks}");
   if (!A_host || !T_host || !phi_host || !kappa2_host) return fail(KCG_E_ARG, "null parameter pointer");
-  if (!workspace_dev) return fail(KCG_E_ARG, "null workspace");
-  if (reinterpret_cast<uintptr_t>(workspace_dev) % kAlign) return fail(KCG_E_ARG, "workspace not 256-byte aligned");
   const int P = d->n_patches, n = d->n_freq, k = d->n_comp;
   if (!finite_all(A_host, (size_t)P * n * k) || !finite_all(T_host, (size_t)P * n) ||
       !finite_all(phi_host, (size_t)P * k) || !finite_all(kappa2_host, P))
@@ -460,40 +650,41 @@ kcg_status kron_cg_create(const kcg_desc* d, const double* A_host, const double*
     if (!(phi_host[i] > 0)) return fail(KCG_E_ARG, "prior_scale must be > 0");
   for (int i = 0; i < P; ++i)
     if (!(kappa2_host[i] >= 0)) return fail(KCG_E_ARG, "kappa2 must be >= 0");
-  Layout L = layout_of(d);
-  if (ws_bytes < L.total) return fail(KCG_E_SHAPE, "workspace too small (kron_cg_workspace_size)");
 
+  c->slab = sl != nullptr;
+  c->nranks = G;
+  c->rank0 = sl ? sl->rank0 : 0;
+  c->nlocal = sl ? sl->nlocal : 1;
   c->stream = reinterpret_cast<cudaStream_t>(stream);
   c->side = 1 << d->level;
+  c->rows = c->side / G;
+  c->ghost = c->slab ? KCG_HALO : 0;
   c->pitch = c->side < 2 ? 2 : c->side;
-  c->N = (size_t)c->side * c->side;
+  c->N = (size_t)c->rows * c->side;
   c->P = P; c->n = n; c->k = k;
-  c->ws = reinterpret_cast<char*>(workspace_dev);
+  c->L = layout_of(d, G);
+  c->ws_need = c->L.total;
   c->ws_bytes = ws_bytes;
-  c->ws_need = L.total;
-  c->r[0] = reinterpret_cast<double*>(c->ws + L.r0);
-  c->r[1] = reinterpret_cast<double*>(c->ws + L.r1);
-  c->p[0] = reinterpret_cast<double*>(c->ws + L.p0);
-  c->p[1] = reinterpret_cast<double*>(c->ws + L.p1);
-  c->partials = reinterpret_cast<double*>(c->ws + L.partials);
-  c->state = reinterpret_cast<SysState*>(c->ws + L.state);
-  c->history = reinterpret_cast<double*>(c->ws + L.history);
-  c->resid_partials = reinterpret_cast<double*>(c->ws + L.resid_partials);
-  c->resid_out = reinterpret_cast<double*>(c->ws + L.resid_out);
-  c->params_kron = reinterpret_cast<SysParams*>(c->ws + L.params_kron);
-  c->params_syl = reinterpret_cast<SysParams*>(c->ws + L.params_syl);
-  c->E_kron = reinterpret_cast<double*>(c->ws + L.E_kron);
-  c->E_syl = reinterpret_cast<double*>(c->ws + L.E_syl);
-  c->W_dev = reinterpret_cast<double*>(c->ws + L.W);
-  if (KCG_TRACE) c->trace = reinterpret_cast<long long*>(c->ws + L.trace);
-  c->sync = reinterpret_cast<unsigned*>(c->ws + L.sync);
-  if (d->host_staging) {
-    c->Y_stage = reinterpret_cast<double*>(c->ws + L.Y_stage);
-    c->mu_stage = reinterpret_cast<double*>(c->ws + L.mu_stage);
+  if (ws_bytes < c->L.total) return fail(KCG_E_SHAPE, "workspace too small (kron_cg_workspace_size)");
+  if (c->slab) {
+    c->peer_ws.resize(G);
+    for (int g = 0; g < G; ++g) {
+      c->peer_ws[g] = reinterpret_cast<char*>(sl->peer_ws[g]);
+      if (!c->peer_ws[g]) return fail(KCG_E_ARG, "slab: null peer workspace");
+      if (reinterpret_cast<uintptr_t>(c->peer_ws[g]) % kAlign) return fail(KCG_E_ARG, "workspace not 256-byte aligned");
+    }
+  } else {
+    if (!workspace_dev) return fail(KCG_E_ARG, "null workspace");
+    if (reinterpret_cast<uintptr_t>(workspace_dev) % kAlign) return fail(KCG_E_ARG, "workspace not 256-byte aligned");
+    c->peer_ws.assign(1, reinterpret_cast<char*>(workspace_dev));
   }
-  c->hits = hits_dev;
+  for (int j = 0; j < c->nlocal; ++j) {
+    c->R.push_back(carve(c->peer_ws[c->rank0 + j], c->L, c->rank0 + j, c->rows, d->host_staging != 0));
+    // hits [nlocal][P][rows + 2 ghost][side] (ghost rows = the face's rows beyond the slab, 0 outside)
+    c->R.back().hits = hits_dev ? hits_dev + (size_t)j * P * (c->rows + 2 * c->ghost) * c->side : nullptr;
+  }
 
-  // setup step a1 (host, once): M = A^T T A, E = T A, eigh(M, P), E_syl = T A W
+  // setup step a1 (host, once): M = A^T T A, E = T A, eigh(M, P), E_syl = T A W, block-Jacobi inverses
   std::vector<SysParams> pk(P), ps((size_t)P * k);
   std::vector<double> Ek((size_t)P * n * k), Es((size_t)P * n * k);
   c->rho.assign((size_t)P * k, 0.0);
@@ -547,39 +738,83 @@ kcg_status kron_cg_create(const kcg_desc* d, const double* A_host, const double*
       return st;                                     \
     }                                                \
   } while (0)
-  CKC(cudaMemcpyAsync(c->params_kron, pk.data(), P * sizeof(SysParams), cudaMemcpyHostToDevice, c->stream), "H2D");
-  CKC(cudaMemcpyAsync(c->params_syl, ps.data(), (size_t)P * k * sizeof(SysParams), cudaMemcpyHostToDevice, c->stream),
-      "H2D");
-  CKC(cudaMemcpyAsync(c->E_kron, Ek.data(), Ek.size() * 8, cudaMemcpyHostToDevice, c->stream), "H2D");
-  CKC(cudaMemcpyAsync(c->E_syl, Es.data(), Es.size() * 8, cudaMemcpyHostToDevice, c->stream), "H2D");
-  CKC(cudaMemcpyAsync(c->W_dev, c->W.data(), c->W.size() * 8, cudaMemcpyHostToDevice, c->stream), "H2D");
-  CKC(cudaStreamSynchronize(c->stream), "create sync");
-
-  // TMA descriptors: Kron boxes span K = k planes, Sylvester boxes one plane.
   const size_t planes = (size_t)P * k;
-  for (int i = 0; i < 2; ++i) {
-    if (!encode_map(&c->maps_kron.r[i], c->r[i], c->side, c->pitch, planes, k, &why) ||
-        !encode_map(&c->maps_kron.p[i], c->p[i], c->side, c->pitch, planes, k, &why) ||
-        !encode_map(&c->maps_syl.r[i], c->r[i], c->side, c->pitch, planes, 1, &why) ||
-        !encode_map(&c->maps_syl.p[i], c->p[i], c->side, c->pitch, planes, 1, &why))
-      return fail(KCG_E_CUDA, why);
+  const int buf_rows = c->rows + 2 * c->ghost;
+  for (RankState& R : c->R) {
+    CKC(cudaMemcpyAsync(R.params_kron, pk.data(), P * sizeof(SysParams), cudaMemcpyHostToDevice, c->stream), "H2D");
+    CKC(cudaMemcpyAsync(R.params_syl, ps.data(), (size_t)P * k * sizeof(SysParams), cudaMemcpyHostToDevice, c->stream),
+        "H2D");
+    CKC(cudaMemcpyAsync(R.E_kron, Ek.data(), Ek.size() * 8, cudaMemcpyHostToDevice, c->stream), "H2D");
+    CKC(cudaMemcpyAsync(R.E_syl, Es.data(), Es.size() * 8, cudaMemcpyHostToDevice, c->stream), "H2D");
+    CKC(cudaMemcpyAsync(R.W_dev, c->W.data(), c->W.size() * 8, cudaMemcpyHostToDevice, c->stream), "H2D");
+    if (c->slab) {  // ghost rows at the face ends stay zero; flags start at 0 (peers only raise them)
+      for (int b = 0; b < 2; ++b) {
+        CKC(cudaMemsetAsync(R.r[b], 0, c->L.vec_doubles * 8, c->stream), "memset r");
+        CKC(cudaMemsetAsync(R.p[b], 0, c->L.vec_doubles * 8, c->stream), "memset p");
+      }
+      CKC(cudaMemsetAsync(R.flags, 0, KCG_GMAX * sizeof(unsigned long long), c->stream), "memset flags");
+      CKC(cudaMemsetAsync(R.xg_top, 0, planes * c->side * 8, c->stream), "memset xg");
+      CKC(cudaMemsetAsync(R.xg_bot, 0, planes * c->side * 8, c->stream), "memset xg");
+    }
+    // TMA descriptors: Kron boxes span K = k planes, Sylvester boxes one plane.
+    for (int i = 0; i < 2; ++i) {
+      if (!encode_map(&R.maps_kron.r[i], R.r[i], c->side, buf_rows, c->pitch, planes, k, &why) ||
+          !encode_map(&R.maps_kron.p[i], R.p[i], c->side, buf_rows, c->pitch, planes, k, &why) ||
+          !encode_map(&R.maps_syl.r[i], R.r[i], c->side, buf_rows, c->pitch, planes, 1, &why) ||
+          !encode_map(&R.maps_syl.p[i], R.p[i], c->side, buf_rows, c->pitch, planes, 1, &why))
+        return fail(KCG_E_CUDA, why);
+    }
   }
+  CKC(cudaStreamSynchronize(c->stream), "create sync");
   c->tiles_x_kron = tiles_x(c->side, k);
-  c->tiles_y_kron = tiles_y(c->side, k);
+  c->tiles_y_kron = tiles_y(c->rows, k);
   c->tiles_x_syl = tiles_x(c->side, 1);
-  c->tiles_y_syl = tiles_y(c->side, 1);
+  c->tiles_y_syl = tiles_y(c->rows, 1);
   int mg = 0;
   const bool prec = d->precond == KCG_PRECOND_BLOCK_JACOBI;
-  CKC(kcg::cg_kernel_config(k, hits_dev != nullptr, prec, P, &mg, &c->smem_kron),
-      "cg kernel config (kron)");
-  c->grid_kron = std::max(1, std::min(mg, P * c->tiles_x_kron * c->tiles_y_kron));
-  CKC(kcg::cg_kernel_config(1, hits_dev != nullptr, prec, P * k, &mg, &c->smem_syl),
+  CKC(kcg::cg_kernel_config(k, hits_dev != nullptr, prec, c->slab, P, &mg, &c->smem_kron), "cg kernel config (kron)");
+  c->grid_kron = std::max(1, std::min(mg / c->nlocal, P * c->tiles_x_kron * c->tiles_y_kron));
+  CKC(kcg::cg_kernel_config(1, hits_dev != nullptr, prec, c->slab, P * k, &mg, &c->smem_syl),
       "cg kernel config (sylvester)");
-  c->grid_syl = std::max(1, std::min(mg, P * k * c->tiles_x_syl * c->tiles_y_syl));
+  c->grid_syl = std::max(1, std::min(mg / c->nlocal, P * k * c->tiles_x_syl * c->tiles_y_syl));
+  if (mg < c->nlocal) return fail(KCG_E_CONFIG, "slab: more emulated ranks than co-resident CTAs");
   for (int i = 0; i < 4; ++i) CKC(cudaEventCreate(&c->ev[i]), "event create");
 #undef CKC
   *out = c;
   return KCG_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+size_t kron_cg_workspace_size(const kcg_desc* d) {
+  std::string why;
+  if (!desc_ok(d, &why)) return 0;
+  return layout_of(d, 1).total;
+}
+
+size_t kron_cg_workspace_size_slab(const kcg_desc* d, int nranks) {
+  std::string why;
+  if (!desc_ok(d, &why) || !slab_ok(d, nranks, &why)) return 0;
+  return layout_of(d, nranks).total;
+}
+
+kcg_status kron_cg_create(const kcg_desc* d, const double* A_host, const double* T_host, const double* phi_host,
+                          const double* kappa2_host, const double* hits_dev, void* workspace_dev, size_t ws_bytes,
+                          void* stream, kcg_ctx** out) {
+  return create_impl(d, nullptr, A_host, T_host, phi_host, kappa2_host, hits_dev, workspace_dev, ws_bytes, stream,
+                     out);
+}
+
+kcg_status kron_cg_create_slab(const kcg_desc* d, const kcg_slab* slab, const double* A_host, const double* T_host,
+                               const double* phi_host, const double* kappa2_host, const double* hits_dev,
+                               size_t ws_bytes, void* stream, kcg_ctx** out) {
+  if (!slab) {
+    if (out) *out = nullptr;
+    return KCG_E_ARG;
+  }
+  return create_impl(d, slab, A_host, T_host, phi_host, kappa2_host, hits_dev, nullptr, ws_bytes, stream, out);
 }
 
 kcg_status kron_cg_solve(kcg_ctx* c, const double* Y, double* mu, double tol, int max_iter, kcg_report* rep) {
@@ -600,7 +835,22 @@ kcg_status kron_cg_apply(kcg_ctx* c, const double* x, double* y) {
   if (!c) return KCG_E_ARG;
   if (!x || !y) { c->err = "null x or y"; return KCG_E_ARG; }
   if (x == y) { c->err = "x and y must not alias"; return KCG_E_ARG; }
-  CK(kcg::launch_apply(c->k, c->stream, c->params_kron, x, y, c->hits, c->P, c->side), "apply kernel");
+  const size_t stride = (size_t)c->P * c->k * c->N;
+  if (c->slab) {
+    const unsigned long long tag0 = (++c->solve_id) << 32;
+    const kcg_status e = exchange_x_rows(c, x, stride, tag0 + kPostTag);
+    if (e != KCG_OK) return e;
+  }
+  for (int j = 0; j < c->nlocal; ++j) {
+    const RankState& R = c->R[j];
+    CK(kcg::launch_apply(c->k, c->stream, R.params_kron, x + j * stride, y + j * stride, R.hits, c->P, geom_of(c, R),
+                         c->slab ? R.xg_top : nullptr, c->slab ? R.xg_bot : nullptr),
+       "apply kernel");
+  }
+  if (c->slab) {  // nobody rewrites a neighbour's xg_* before everyone is done reading it
+    const unsigned long long tag0 = c->solve_id << 32;
+    CK(kcg::launch_xrank_sync(c->stream, xsync_of(c, tag0 + kPostTag + 1)), "rendezvous kernel");
+  }
   CK(cudaStreamSynchronize(c->stream), "apply");
   return KCG_OK;
 }
@@ -608,8 +858,13 @@ kcg_status kron_cg_apply(kcg_ctx* c, const double* x, double* y) {
 kcg_status kron_cg_rhs(kcg_ctx* c, const double* Y, double* b) {
   if (!c) return KCG_E_ARG;
   if (!Y || !b) { c->err = "null Y or b"; return KCG_E_ARG; }
-  CK(kcg::launch_rhs(c->k, c->stream, Y, c->E_kron, c->hits, b, nullptr, nullptr, c->P, c->n, c->side, c->side),
-     "rhs kernel");
+  for (int j = 0; j < c->nlocal; ++j) {
+    const RankState& R = c->R[j];
+    SlabGeom g{c->side, c->rows, R.row0, c->side, 0, c->ghost};  // b written densely [P][k][rows][side]
+    CK(kcg::launch_rhs(c->k, c->stream, Y + j * (size_t)c->P * c->n * c->N, R.E_kron, R.hits,
+                       b + j * (size_t)c->P * c->k * c->N, nullptr, nullptr, c->P, c->n, g),
+       "rhs kernel");
+  }
   CK(cudaStreamSynchronize(c->stream), "rhs");
   return KCG_OK;
 }
@@ -620,6 +875,44 @@ kcg_status sylvester_factor(kcg_ctx* c, double* rho, double* W) {
   std::memcpy(rho, c->rho.data(), c->rho.size() * 8);
   std::memcpy(W, c->W.data(), c->W.size() * 8);
   return KCG_OK;
+}
+
+kcg_status kcg_ipc_export(const void* dev_ptr, unsigned char handle[64], size_t* offset) {
+  if (!dev_ptr || !handle || !offset) return KCG_E_ARG;
+  CUdeviceptr base = 0;
+  size_t size = 0;
+  static PFN_cuMemGetAddressRange_v3020 range = nullptr;
+  if (!range) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &p, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      return KCG_E_CUDA;
+    range = reinterpret_cast<PFN_cuMemGetAddressRange_v3020>(p);
+  }
+  if (range(&base, &size, reinterpret_cast<CUdeviceptr>(dev_ptr)) != CUDA_SUCCESS) return KCG_E_CUDA;
+  cudaIpcMemHandle_t h;
+  if (cudaIpcGetMemHandle(&h, reinterpret_cast<void*>(base)) != cudaSuccess) return KCG_E_CUDA;
+  static_assert(sizeof(cudaIpcMemHandle_t) == 64, "IPC handle size");
+  std::memcpy(handle, &h, 64);
+  *offset = reinterpret_cast<uintptr_t>(dev_ptr) - static_cast<uintptr_t>(base);
+  return KCG_OK;
+}
+
+kcg_status kcg_ipc_import(const unsigned char handle[64], size_t offset, void** dev_ptr, void** base_out) {
+  if (!handle || !dev_ptr || !base_out) return KCG_E_ARG;
+  cudaIpcMemHandle_t h;
+  std::memcpy(&h, handle, 64);
+  void* base = nullptr;
+  if (cudaIpcOpenMemHandle(&base, h, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) return KCG_E_CUDA;
+  *base_out = base;
+  *dev_ptr = static_cast<char*>(base) + offset;
+  return KCG_OK;
+}
+
+kcg_status kcg_ipc_close(void* base) {
+  if (!base) return KCG_E_ARG;
+  return cudaIpcCloseMemHandle(base) == cudaSuccess ? KCG_OK : KCG_E_CUDA;
 }
 
 const char* kcg_last_error(const kcg_ctx* c) { return c ? c->err.c_str() : "null context"; }
@@ -654,18 +947,8 @@ KCG_API int kcg_debug_state(const kcg_ctx* c, double* out, int max_sys) {
   return n;
 }
 
-// Diagnostic (not part of the ABI header): copy the device SysParams array of a route (0 kron,
-// 1 sylvester) into out (at most max_bytes); returns sizeof(SysParams).
-KCG_API int kcg_debug_params(const kcg_ctx* c, int route, void* out, size_t max_bytes) {
-  if (!c || !out) return 0;
-  const size_t n = route == 0 ? (size_t)c->P : (size_t)c->P * c->k;
-  cudaMemcpy(out, route == 0 ? c->params_kron : c->params_syl, std::min(max_bytes, n * sizeof(SysParams)),
-             cudaMemcpyDeviceToHost);
-  return (int)sizeof(SysParams);
-}
-
 // Diagnostic (not part of the ABI header): launch configuration of the CG kernel per route:
-// out = {grid_kron, grid_syl, smem_kron, smem_syl, sm_count}.
+// out = {grid_kron, grid_syl, smem_kron, smem_syl, sm_count} (grids per rank in slab mode).
 KCG_API int kcg_debug_config(const kcg_ctx* c, long long* out) {
   if (!c || !out) return 0;
   int dev = 0, nsm = 0;
@@ -678,9 +961,9 @@ KCG_API int kcg_debug_config(const kcg_ctx* c, long long* out) {
 
 // Diagnostic (not part of the ABI header): copy the phase trace of the last solve (KCG_TRACE builds).
 KCG_API int kcg_debug_trace(kcg_ctx* c, long long* out, int max_iters) {
-  if (!c || !c->trace || !out) return 0;
+  if (!c || !c->R[0].trace || !out) return 0;
   const int n = std::min(max_iters, KCG_TRACE_ITERS);
-  cudaMemcpy(out, c->trace, (size_t)n * KCG_TRACE_COLS * 8, cudaMemcpyDeviceToHost);
+  cudaMemcpy(out, c->R[0].trace, (size_t)n * KCG_TRACE_COLS * 8, cudaMemcpyDeviceToHost);
   return KCG_TRACE_COLS;
 }
 

@@ -7,6 +7,7 @@
 #include <stdint.h>
 
 #define KCG_KMAX 8
+#define KCG_GMAX 8          // ranks sharing one face in row-slab mode
 #define KCG_TX 64           // tile width (pixels) of the CG kernel
 #define KCG_HALO 2          // single-pass recompute halo for a radius-1 stencil
 
@@ -93,6 +94,12 @@ struct SysState {
                       // when `iters` is odd -- added by the next x pass or by the fix-up kernel)
 };
 
+struct CgMaps {              // TMA descriptors of rbuf[0..1], pbuf[0..1] (box = {TX+4, TY+4, K})
+  CUtensorMap r[2];
+  CUtensorMap p[2];
+  CUtensorMap x;             // the solution buffer, box = {TX, TY, K}; re-encoded per solve
+};
+
 struct CgArgs {
   const SysParams* params;   // [n_sys]
   double* x;                 // user solution planes [n_sys*K][side][side]
@@ -112,28 +119,68 @@ struct CgArgs {
   long long* trace;          // KCG_TRACE builds only: per-iteration %globaltimer stamps
   unsigned* sync;            // [2..3] tile-claim counters of the two pass parities (zeroed per launch)
   double tol2;
+  // ---- row-slab mode (cg_slab_kernel only) ----
+  int rank, nranks;          // this rank, ranks sharing every face (slab r holds rows [r rows, (r+1) rows))
+  double* nb_r[2][2];        // [0 up / 1 down neighbour][buffer] its ghosted r buffers (nullptr: face end)
+  double* nb_p[2][2];        // same for p
+  double* slots[KCG_GMAX];   // every rank's cross-rank sums [2 parities][n_sys][nranks][NP]
+  unsigned long long* flags[KCG_GMAX];  // every rank's flag array [nranks]
+  unsigned long long* my_flags;          // == flags[rank]
+  const double* my_slots;                // == slots[rank]
+  unsigned* group;           // [0] barrier counter of this rank's CTA group (zeroed per launch)
+  unsigned long long tag0;   // solve tag (solve number << 32); pass q (start pass 0) releases tag0 + q + 1
 };
 
-struct CgMaps {              // TMA descriptors of rbuf[0..1], pbuf[0..1] (box = {TX+4, TY+4, K})
-  CUtensorMap r[2];
-  CUtensorMap p[2];
-  CUtensorMap x;             // the solution buffer, box = {TX, TY, K}; re-encoded per solve
+// One launch of the slab kernel: `nlocal` ranks (1 = one process per GPU; nranks = every rank
+// emulated on one GPU in one cooperative launch), `ctas` CTAs per rank.
+struct CgSlabLaunch {
+  CgArgs a[KCG_GMAX];
+  CgMaps m[KCG_GMAX];
+  int nlocal, ctas;
+};
+
+
+// Small cross-rank operations of the slab runtime (by value: plain pointers valid in this process).
+struct XrankPut {            // dst[g][rank * count + i] = src[i] for every rank g
+  double* dst[KCG_GMAX];
+  const double* src;
+  int count, rank, nranks;
+};
+struct XrankSync {           // local ranks [rank0, rank0 + nlocal) meet every rank on `tag`
+  unsigned long long* flags[KCG_GMAX];
+  int nranks, rank0, nlocal;
+  unsigned long long tag;
+};
+// Geometry of one rank's data: a face of side x side, `rows` local rows from global row `row0`,
+// r/p buffers with row pitch `pitch` and `ghost` ghost rows above and below (0 without slabs).
+struct SlabGeom {
+  int side, rows, row0, pitch, ghost;
+  int hits_ghost;            // ghost rows of the hits planes (= ghost, except for the dense rhs output)
 };
 
 // ---------------------------------------------------------------- launchers (kcg_kernels.cu)
 // All return cudaError_t of the launch.
 cudaError_t launch_rhs(int K, cudaStream_t s, const double* Y, const double* E, const double* hits,
-                       double* r0, double* p0, double* x, int P, int n, int side, int pitch);
+                       double* r0, double* p0, double* x, int P, int n, const SlabGeom& g);
 cudaError_t launch_cg(int K, bool prec, cudaStream_t s, const CgArgs& a, const CgMaps& m, int grid, size_t smem);
-cudaError_t cg_kernel_config(int K, bool hits, bool prec, int n_sys, int* max_grid, size_t* smem);
+cudaError_t cg_kernel_config(int K, bool hits, bool prec, bool slab, int n_sys, int* max_grid, size_t* smem);
+cudaError_t launch_cg_slab(int K, bool prec, cudaStream_t s, const CgSlabLaunch& L, size_t smem);
 cudaError_t launch_apply(int K, cudaStream_t s, const SysParams* params, const double* x, double* y,
-                         const double* hits, int n_sys, int side);
+                         const double* hits, int n_sys, const SlabGeom& g, const double* xg_top,
+                         const double* xg_bot);
 cudaError_t launch_resid(int K, cudaStream_t s, const SysParams* params, const double* x,
                          const double* Y, const double* E, const double* hits, double* partials,
-                         double* out, int n_sys, int n, int side);
+                         double* out, int n_sys, int n, const SlabGeom& g, const double* xg_top,
+                         const double* xg_bot);
 cudaError_t launch_xfix(int K, cudaStream_t s, const SysState* st, const double* p0, const double* p1, double* x,
-                        int n_sys, int side, int pitch);
-cudaError_t launch_backtransform(int K, cudaStream_t s, const double* W, double* x, int P, int side);
-int apply_tiles_per_sys(int side);
+                        int n_sys, const SlabGeom& g);
+cudaError_t launch_backtransform(int K, cudaStream_t s, const double* W, double* x, int P, size_t N);
+cudaError_t launch_ghost_fill(cudaStream_t s, const double* r0, const double* p0, double* up_r, double* up_p,
+                              double* dn_r, double* dn_p, int planes, const SlabGeom& g);
+cudaError_t launch_xghost(cudaStream_t s, const double* x, double* up_xg_bot, double* dn_xg_top, int planes,
+                          const SlabGeom& g);
+cudaError_t launch_put(cudaStream_t s, const XrankPut& P);
+cudaError_t launch_xrank_sync(cudaStream_t s, const XrankSync& X);
+int apply_tiles_per_sys(int rows, int side);
 
 }  // namespace kcg

@@ -73,12 +73,27 @@ kron_cg_apply = _sig("kron_cg_apply", C.c_int, [_ctxp, _vp, _vp])
 kron_cg_rhs = _sig("kron_cg_rhs", C.c_int, [_ctxp, _vp, _vp])
 sylvester_factor = _sig("sylvester_factor", C.c_int, [_ctxp, _vp, _vp])
 kcg_last_error = _sig("kcg_last_error", C.c_char_p, [_ctxp])
+
+
+class kcg_slab(C.Structure):
+    _fields_ = [("nranks", C.c_int), ("rank0", C.c_int), ("nlocal", C.c_int), ("peer_ws", C.c_void_p * 8)]
+
+
+kron_cg_workspace_size_slab = _sig("kron_cg_workspace_size_slab", C.c_size_t, [C.POINTER(kcg_desc), C.c_int])
+kron_cg_create_slab = _sig("kron_cg_create_slab", C.c_int,
+                           [C.POINTER(kcg_desc), C.POINTER(kcg_slab), _vp, _vp, _vp, _vp, _vp, C.c_size_t,
+                            _vp, C.POINTER(_ctxp)])
+kcg_ipc_export = _sig("kcg_ipc_export", C.c_int, [_vp, C.c_char_p, C.POINTER(C.c_size_t)])
+kcg_ipc_import = _sig("kcg_ipc_import", C.c_int, [C.c_char_p, C.c_size_t, C.POINTER(_vp), C.POINTER(_vp)])
+kcg_ipc_close = _sig("kcg_ipc_close", C.c_int, [_vp])
 kcg_status_string = _sig("kcg_status_string", C.c_char_p, [C.c_int])
 kron_cg_destroy = _sig("kron_cg_destroy", None, [_ctxp])
 
 EXPORTS = ["kron_cg_workspace_size", "kron_cg_create", "kron_cg_solve", "sylvester_solve",
            "kron_cg_solve_host", "sylvester_solve_host", "kron_cg_apply", "kron_cg_rhs",
-           "sylvester_factor", "kcg_last_error", "kcg_status_string", "kron_cg_destroy"]
+           "sylvester_factor", "kcg_last_error", "kcg_status_string", "kron_cg_destroy",
+           "kron_cg_workspace_size_slab", "kron_cg_create_slab", "kcg_ipc_export", "kcg_ipc_import",
+           "kcg_ipc_close"]
 
 
 class KcgError(RuntimeError):
@@ -121,6 +136,8 @@ class KronCG:
         self.side = 1 << level
         self.N = self.side * self.side
         self.device = torch.device(device if device is not None else "cuda")
+        self.shape_Y = (P, n, self.side, self.side)
+        self.shape_mu = (P, k, self.side, self.side)
         pc = {"none": KCG_PRECOND_NONE, "block_jacobi": KCG_PRECOND_BLOCK_JACOBI}[precond]
         self.desc = kcg_desc(level, n, k, P, KCG_PRIOR_LAPLACIAN, KCG_LAYOUT_ROW_MAJOR,
                              pc, int(bool(host_staging)), int(history_cap))
@@ -179,9 +196,9 @@ class KronCG:
         if mu is not None:
             return mu
         if host:
-            return torch.empty((self.P, self.k, self.side, self.side), dtype=torch.float64,
+            return torch.empty(self.shape_mu, dtype=torch.float64,
                                pin_memory=True)
-        return torch.empty((self.P, self.k, self.side, self.side), dtype=torch.float64,
+        return torch.empty(self.shape_mu, dtype=torch.float64,
                            device=self.device)
 
     def _check_dev(self, t, shape, name):
@@ -193,16 +210,16 @@ class KronCG:
     # ------------------------------------------------------------------ API
     def solve(self, Y, mu=None, tol=1e-10, max_iter=100000, **kw):
         """Kronecker route (kron_cg_solve). Y: CUDA [P][n][side][side] -> (mu, report)."""
-        self._check_dev(Y, (self.P, self.n, self.side, self.side), "Y")
+        self._check_dev(Y, self.shape_Y, "Y")
         mu = self._out(mu)
-        self._check_dev(mu, (self.P, self.k, self.side, self.side), "mu")
+        self._check_dev(mu, self.shape_mu, "mu")
         return mu, self._solve(kron_cg_solve, Y, mu, tol, max_iter, self.P, **kw)
 
     def sylvester(self, Y, mu=None, tol=1e-10, max_iter=100000, **kw):
         """Sylvester route (sylvester_solve). Y: CUDA [P][n][side][side] -> (mu, report)."""
-        self._check_dev(Y, (self.P, self.n, self.side, self.side), "Y")
+        self._check_dev(Y, self.shape_Y, "Y")
         mu = self._out(mu)
-        self._check_dev(mu, (self.P, self.k, self.side, self.side), "mu")
+        self._check_dev(mu, self.shape_mu, "mu")
         return mu, self._solve(sylvester_solve, Y, mu, tol, max_iter, self.P * self.k, **kw)
 
     def solve_host(self, Y, mu=None, tol=1e-10, max_iter=100000, route="kron", **kw):
@@ -217,7 +234,7 @@ class KronCG:
     def apply(self, x, y=None):
         """y = G x (kron_cg_apply)."""
         import torch
-        shape = (self.P, self.k, self.side, self.side)
+        shape = self.shape_mu
         self._check_dev(x, shape, "x")
         if y is None:
             y = torch.empty(shape, dtype=torch.float64, device=self.device)
@@ -229,9 +246,9 @@ class KronCG:
     def rhs(self, Y, b=None):
         """b = vec(N_h Y T A) (kron_cg_rhs)."""
         import torch
-        self._check_dev(Y, (self.P, self.n, self.side, self.side), "Y")
+        self._check_dev(Y, self.shape_Y, "Y")
         if b is None:
-            b = torch.empty((self.P, self.k, self.side, self.side), dtype=torch.float64,
+            b = torch.empty(self.shape_mu, dtype=torch.float64,
                             device=self.device)
         st = kron_cg_rhs(self._ctx, Y.data_ptr(), b.data_ptr())
         if st != KCG_OK:
@@ -266,3 +283,169 @@ class KronCG:
             self.close()
         except Exception:
             pass
+
+
+
+# ------------------------------------------------------------------------------ row slabs
+def slab_rows(level: int, nranks: int) -> int:
+    """Rows of each rank's slab when a 2^level face is split over nranks ranks."""
+    side = 1 << level
+    if nranks < 1 or nranks > 8 or side % nranks or side // nranks < 4:
+        raise ValueError(f"cannot split a {side}-row face into {nranks} slabs of >= 4 rows")
+    return side // nranks
+
+
+def split_rows(a, nranks: int):
+    """[..., side, side] -> [nranks, ..., rows, side] (contiguous): rank r gets rows [r rows, (r+1) rows)."""
+    side = a.shape[-2]
+    rows = side // nranks
+    parts = [a[..., r * rows:(r + 1) * rows, :] for r in range(nranks)]
+    import torch
+    if isinstance(a, torch.Tensor):
+        return torch.stack(parts).contiguous()
+    return np.ascontiguousarray(np.stack(parts))
+
+
+def join_rows(parts):
+    """Inverse of split_rows: [nranks, ..., rows, side] -> [..., nranks rows, side]."""
+    import torch
+    if isinstance(parts, torch.Tensor):
+        return torch.cat(list(parts), dim=-2)
+    return np.concatenate(list(parts), axis=-2)
+
+
+def ghost_rows(a, nranks: int, ghost: int):
+    """[..., side, side] -> [nranks, ..., rows + 2 ghost, side]: each rank's slab with `ghost` rows of
+    the face above and below (zeros beyond the face) -- the layout of slab hits maps."""
+    import torch
+    side = a.shape[-2]
+    rows = side // nranks
+    pad = torch.zeros(a.shape[:-2] + (ghost, a.shape[-1]), dtype=a.dtype, device=a.device)
+    full = torch.cat([pad, a, pad], dim=-2)
+    return torch.stack([full[..., r * rows:r * rows + rows + 2 * ghost, :] for r in range(nranks)]).contiguous()
+
+
+def ipc_export(t) -> bytes:
+    """72-byte record (CUDA IPC handle of the allocation + offset) naming device tensor t for peers."""
+    h = C.create_string_buffer(64)
+    off = C.c_size_t()
+    st = kcg_ipc_export(t.data_ptr(), h, C.byref(off))
+    if st != KCG_OK:
+        raise KcgError(st, "kcg_ipc_export")
+    return h.raw + int(off.value).to_bytes(8, "little")
+
+
+def ipc_import(rec: bytes):
+    """(device pointer, mapping base) of a peer's ipc_export record."""
+    ptr, base = _vp(), _vp()
+    st = kcg_ipc_import(rec[:64], int.from_bytes(rec[64:72], "little"), C.byref(ptr), C.byref(base))
+    if st != KCG_OK:
+        raise KcgError(st, "kcg_ipc_import")
+    return ptr.value, base.value
+
+
+def exchange_records(rec: bytes, group=None) -> list:
+    """All-gather one fixed-size byte record per rank over a torch.distributed group (host logic
+    of the slab set-up; works on gloo and nccl)."""
+    import torch
+    import torch.distributed as dist
+    world = dist.get_world_size(group)
+    t = torch.frombuffer(bytearray(rec), dtype=torch.uint8)
+    if dist.get_backend(group) == "nccl":
+        t = t.cuda()
+    out = [torch.empty_like(t) for _ in range(world)]
+    dist.all_gather(out, t, group=group)
+    return [bytes(o.cpu().numpy().tobytes()) for o in out]
+
+
+class KronCGSlab(KronCG):
+    """Row-slab context: every face split over `nranks` ranks (kron_cg_create_slab).
+
+    emulate=True: this process drives all ranks on one GPU (one cooperative launch; the layout of
+    Y / mu is [nranks][P][..][rows][side]; hits is given for the whole face [P][side][side]).  emulate=False: this process is rank
+    `dist.get_rank(group)` of `group`; workspaces are exchanged through CUDA IPC and Y / mu are
+    [1][P][..][rows][side] (its own slab).
+    """
+
+    def __init__(self, level, A, noise_prec, prior_scale, kappa2, nranks, emulate=True, group=None,
+                 hits=None, device=None, host_staging=False, history_cap=0, stream=None,
+                 precond="none"):
+        import torch
+        A = np.ascontiguousarray(np.asarray(A, dtype=np.float64))
+        if A.ndim == 2:
+            A = A[None]
+        P, n, k = A.shape
+        self.noise_prec = np.ascontiguousarray(np.asarray(noise_prec, dtype=np.float64).reshape(P, n))
+        self.prior_scale = np.ascontiguousarray(np.asarray(prior_scale, dtype=np.float64).reshape(P, k))
+        self.kappa2 = np.ascontiguousarray(np.asarray(kappa2, dtype=np.float64).reshape(P))
+        self.A = A
+        self.level, self.P, self.n, self.k = level, P, n, k
+        self.side = 1 << level
+        self.nranks = nranks
+        self.rows = slab_rows(level, nranks)
+        self.N = self.rows * self.side
+        self.device = torch.device(device if device is not None else "cuda")
+        self._ipc_bases = []
+        if emulate:
+            self.rank0, self.nlocal = 0, nranks
+        else:
+            import torch.distributed as dist
+            if dist.get_world_size(group) != nranks:
+                raise ValueError("group size must equal nranks")
+            self.rank0, self.nlocal = dist.get_rank(group), 1
+        self.shape_Y = (self.nlocal, P, n, self.rows, self.side)
+        self.shape_mu = (self.nlocal, P, k, self.rows, self.side)
+        pc = {"none": KCG_PRECOND_NONE, "block_jacobi": KCG_PRECOND_BLOCK_JACOBI}[precond]
+        self.desc = kcg_desc(level, n, k, P, KCG_PRIOR_LAPLACIAN, KCG_LAYOUT_ROW_MAJOR,
+                             pc, int(bool(host_staging)), int(history_cap))
+        ws = kron_cg_workspace_size_slab(C.byref(self.desc), nranks)
+        if ws == 0:
+            raise KcgError(KCG_E_SHAPE, "invalid descriptor or slab split")
+        self.ws_bytes = ws
+        sl = kcg_slab()
+        sl.nranks, sl.rank0, sl.nlocal = nranks, self.rank0, self.nlocal
+        self.workspaces = [torch.empty(ws + 256, dtype=torch.uint8, device=self.device)
+                           for _ in range(self.nlocal)]
+        own = [w.data_ptr() + (-w.data_ptr()) % 256 for w in self.workspaces]
+        if emulate:
+            for r in range(nranks):
+                sl.peer_ws[r] = own[r]
+        else:
+            # the workspace allocation is exported whole; the record carries the aligned offset
+            rec = ipc_export(self.workspaces[0])
+            rec = rec[:64] + (int.from_bytes(rec[64:72], "little") + own[0] - self.workspaces[0].data_ptr()).to_bytes(8, "little")
+            recs = exchange_records(rec, group)
+            for r in range(nranks):
+                if r == self.rank0:
+                    sl.peer_ws[r] = own[0]
+                else:
+                    ptr, base = ipc_import(recs[r])
+                    self._ipc_bases.append(base)
+                    sl.peer_ws[r] = ptr
+        self.hits = None
+        if hits is not None:  # full-face hits [P][side][side] -> ghosted slabs of the local ranks
+            self.hits = ghost_rows(hits.to(dtype=torch.float64), nranks, 2)[self.rank0:self.rank0 + self.nlocal]
+            self.hits = self.hits.to(device=self.device).contiguous()
+        if stream is None:
+            stream = torch.cuda.current_stream(self.device)
+        self.stream = stream
+        ctx = _ctxp()
+        st = kron_cg_create_slab(C.byref(self.desc), C.byref(sl), self.A.ctypes.data,
+                                 self.noise_prec.ctypes.data, self.prior_scale.ctypes.data,
+                                 self.kappa2.ctypes.data,
+                                 self.hits.data_ptr() if self.hits is not None else None,
+                                 ws, C.c_void_p(stream.cuda_stream), C.byref(ctx))
+        self._ctx = ctx
+        if st != KCG_OK:
+            msg = kcg_last_error(ctx).decode() if ctx.value else ""
+            self.close()
+            raise KcgError(st, msg)
+        if not emulate:
+            import torch.distributed as dist
+            dist.barrier(group)  # every rank's context (zeroed flags, ghost rows) exists before solves
+
+    def close(self):
+        super().close()
+        for b in getattr(self, "_ipc_bases", []):
+            kcg_ipc_close(b)
+        self._ipc_bases = []
