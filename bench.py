@@ -107,24 +107,54 @@ def _dist():
 
 
 def _patches_for(config: str, world: int, rank: int):
+    """This rank's faces and role.  Faces are grouped (sharding.plan_groups): a group of g ranks
+    batches its faces in one context and, for g > 1, splits every face into g row slabs (one per
+    rank of the group).  Returns (problems of the group, their indices, costs, g, slab index)."""
     from synth import CONFIGS
     from synth.problems import make_patch
-    from paper_2204_08057_b200.sharding import assign_lpt, patch_cost
+    from paper_2204_08057_b200.sharding import patch_cost, rank_role
     c = CONFIGS[config]
-    probs = [make_patch(c["level"], c["n"], c["k"], sd, tau=c["tau"], kappa2=c["kappa2"])
-             for sd in c["seeds"]] if world == 1 else None
-    if probs is None:
-        # cost model needs only the small parameters: draw all faces (cheap at these sizes is
-        # not true for Y, so draw full problems only for this rank's faces afterwards)
-        probs_all = [make_patch(min(c["level"], 2), c["n"], c["k"], sd, tau=c["tau"],
-                                kappa2=c["kappa2"]) for sd in c["seeds"]]
-        costs = [patch_cost(c["level"], p.A, p.noise_prec, p.tau, p.kappa2) for p in probs_all]
-        mine = assign_lpt(costs, world)[rank]
-        probs = [make_patch(c["level"], c["n"], c["k"], c["seeds"][i], tau=c["tau"],
-                            kappa2=c["kappa2"]) for i in mine]
-        return probs, mine, costs
-    costs = [patch_cost(c["level"], p.A, p.noise_prec, p.tau, p.kappa2) for p in probs]
-    return probs, list(range(len(probs))), costs
+    if world == 1:
+        probs = [make_patch(c["level"], c["n"], c["k"], sd, tau=c["tau"], kappa2=c["kappa2"]) for sd in c["seeds"]]
+        costs = [patch_cost(c["level"], p.A, p.noise_prec, p.tau, p.kappa2) for p in probs]
+        return probs, list(range(len(probs))), costs, 1, 0
+    # the cost model needs only the small parameters (identical draws at a tiny level); full
+    # problems are drawn for this rank's group only
+    probs_all = [make_patch(min(c["level"], 2), c["n"], c["k"], sd, tau=c["tau"], kappa2=c["kappa2"])
+                 for sd in c["seeds"]]
+    costs = [patch_cost(c["level"], p.A, p.noise_prec, p.tau, p.kappa2) for p in probs_all]
+    g, grp, slab, mine = rank_role(costs, world, rank)
+    probs = [make_patch(c["level"], c["n"], c["k"], c["seeds"][i], tau=c["tau"], kappa2=c["kappa2"]) for i in mine]
+    return probs, mine, costs, g, slab
+
+
+def _slab_probe(dev, G=8, steps=5):
+    """Cost of the row-slab machinery on one GPU: the planck face (L=10, k=4) solved unsplit and
+    split into G row slabs with all G ranks emulated in one cooperative launch (halo rows through
+    the neighbours' ghost rows, per-iteration cross-rank scalar sums through slots + flags).  On a
+    real G-GPU run each rank does 1/G of the bytes; here one GPU does all of them, so the per-pass
+    difference is the protocol's overhead."""
+    import torch
+    from synth import make_config
+    from synth.problems import stack
+    from paper_2204_08057_b200.kroncg import KronCG, KronCGSlab, split_rows
+    p = make_config("planck")[0]
+    st = stack([p])
+    Y = torch.from_numpy(st["Y"]).to(dev)
+    c1 = KronCG(p.level, st["A"], st["noise_prec"], st["tau"], st["kappa2"], device=dev)
+    cs = KronCGSlab(p.level, st["A"], st["noise_prec"], st["tau"], st["kappa2"], G, emulate=True, device=dev)
+    Ys = split_rows(Y, G)
+    out = {"config": "planck", "slabs": G}
+    for name, fn in (("unsplit", lambda: c1.solve(Y, tol=TOL)[1]), ("slab", lambda: cs.solve(Ys, tol=TOL)[1])):
+        for _ in range(2):
+            fn()
+        reps = [fn() for _ in range(steps)]
+        lt = sum(r["loop_time_s"] for r in reps) / steps
+        it = reps[-1]["iterations"]
+        out[name] = {"solves_per_s": steps / sum(r["wall_time_s"] for r in reps), "iterations": it,
+                     "cg_kernel_us_per_pass": lt / (it + 1) * 1e6}
+    out["overhead_us_per_pass"] = out["slab"]["cg_kernel_us_per_pass"] - out["unsplit"]["cg_kernel_us_per_pass"]
+    return out
 
 
 def _oracle_iterations(config):
@@ -240,14 +270,22 @@ def run_b200(args):
     from paper_2204_08057_b200.kroncg import KronCG
     from synth.problems import stack
 
-    problems, mine, costs = _patches_for(args.config, world, rank)
+    problems, mine, costs, g, slab = _patches_for(args.config, world, rank)
     st = stack(problems)
-    ctx = KronCG(problems[0].level, st["A"], st["noise_prec"], st["tau"], st["kappa2"],
-                 device=dev, host_staging=True)
-    Y = torch.from_numpy(st["Y"]).to(dev)
-    mu = torch.empty((len(problems), problems[0].k, problems[0].side, problems[0].side),
-                     dtype=torch.float64, device=dev)
-    Y_host = torch.from_numpy(st["Y"]).pin_memory()
+    if g == 1:
+        ctx = KronCG(problems[0].level, st["A"], st["noise_prec"], st["tau"], st["kappa2"],
+                     device=dev, host_staging=True)
+        Yn = st["Y"]
+    else:
+        # every rank creates every group (same order), then joins its own: slabs of its group's faces
+        from paper_2204_08057_b200.kroncg import KronCGSlab, split_rows
+        groups = [dist.new_group(list(range(j * g, (j + 1) * g))) for j in range(world // g)]
+        ctx = KronCGSlab(problems[0].level, st["A"], st["noise_prec"], st["tau"], st["kappa2"], g,
+                         emulate=False, group=groups[rank // g], device=dev, host_staging=True)
+        Yn = split_rows(st["Y"], g)[slab:slab + 1]
+    Y = torch.from_numpy(Yn).to(dev)
+    mu = torch.empty(ctx.shape_mu, dtype=torch.float64, device=dev)
+    Y_host = torch.from_numpy(Yn).pin_memory()
     mu_host = torch.empty(mu.shape, dtype=torch.float64).pin_memory()
     stream = torch.cuda.current_stream(dev)
 
@@ -294,7 +332,8 @@ def run_b200(args):
         # whole-job numbers: gather per-rank sums
         loc = torch.tensor([sum(r["loop_bytes"] for r in reps_), sum(r["loop_time_s"] for r in reps_),
                             sum(r["system_iterations"] for r in reps_), len(reps_),
-                            sum(r["system_iterations"] + r["n_systems"] for r in reps_)],
+                            sum(r["system_iterations"] + r["n_systems"] for r in reps_),
+                            1.0 if slab == 0 else 0.0],
                            dtype=torch.float64, device=dev)
         if world > 1:
             allv = [torch.zeros_like(loc) for _ in range(world)]
@@ -305,6 +344,10 @@ def run_b200(args):
 
     g_main = agg(reps, t_main)
     g_other = agg(reps_other, t_other)
+    io = torch.tensor([float(Y_host.numel() * 8), float(mu_host.numel() * 8)], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(io)  # whole-job bytes moved by the e2e step (every rank's own slab / faces)
+    h2d_bytes, d2h_bytes = int(io[0].item()), int(io[1].item())
     if rank != 0:
         if world > 1:
             dist.barrier()
@@ -313,6 +356,8 @@ def run_b200(args):
 
     peak, peak_src = _peaks()
     K = args.steps
+
+    gsz = g
 
     def roofline(g, route):
         # dominant kernel = cg_persistent_kernel; rank 0's launches (CUDA events around it).
@@ -323,7 +368,7 @@ def run_b200(args):
         bytes_, tsec = g[0][0], g[0][1]
         ach = bytes_ / tsec / 1e9 if tsec > 0 else 0.0
         kk = problems[0].k if route == "kron" else 1
-        b48 = 48.0 * kk * problems[0].side ** 2 * g[0][4]
+        b48 = 48.0 * kk * problems[0].side ** 2 / gsz * g[0][4]
         return {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,
                 "traffic": _traffic(args.config, route), "kernel": "cg_persistent_kernel",
                 "peak_source": peak_src,
@@ -332,7 +377,7 @@ def run_b200(args):
                 "model_48kN": {"bytes_per_launch": b48 / max(g[0][3], 1),
                                "frac": (b48 / tsec / 1e9) / peak if tsec > 0 else 0.0}}
 
-    sys_its_main = sum(v[2] for v in g_main) / K
+    sys_its_main = sum(v[2] for v in g_main if v[5] > 0) / K  # each group's faces counted once
     line = {
         "metric": METRIC,
         "value": K / t_main,
@@ -343,25 +388,27 @@ def run_b200(args):
         "data": "synthetic (synth/ recipe of SURVEY 8(d), seeds per BASELINE config)",
         "config": {"workload": args.config, "level": problems[0].level, "n": problems[0].n,
                    "k": problems[0].k, "patches": len(costs), "tol": TOL, "route": args.route,
-                   "parallelism": f"face-shard{world}",
+                   "parallelism": f"face-shard{world}" if g == 1 else f"face-groups{world // g}x-rowslab{g}",
                    "l2": "no flush: inputs (Y) and solver state exceed the 126 MB L2"},
         "cg_iters_per_s": sys_its_main * K / t_main,
         "face_iterations_per_solve": sys_its_main,
         "iterations_per_face_rank0": reps[-1]["iterations_per"],
         "roofline": roofline(g_main, args.route),
         "e2e": {"value": len(reps_e2e) / t_e2e, "unit": "full-sky solves/s",
-                "h2d_bytes_per_step": int(st["Y"].nbytes) * (world if world > 1 else 1),
-                "d2h_bytes_per_step": int(mu_host.numel() * 8) * (world if world > 1 else 1),
+                "h2d_bytes_per_step": h2d_bytes,
+                "d2h_bytes_per_step": d2h_bytes,
                 "api": "kron_cg_solve_host (C ABI, pinned host buffers)"},
         # per solve: rhs, CG, x fix-up, residual apply + reduce (+ back-transform, Sylvester)
         "gpu_launches": K * (6 if args.route == "sylvester" else 5),
         "clocks": clocks,
         "sylvester" if args.route == "kron" else "kron": {
             "value": K / t_other, "ms_per_step": t_other / K * 1e3,
-            "system_iterations_per_solve": sum(v[2] for v in g_other) / K,
+            "system_iterations_per_solve": sum(v[2] for v in g_other if v[5] > 0) / K,
             "roofline": roofline(g_other, "sylvester" if args.route == "kron" else "kron")},
         "true_rel_residual": reps[-1]["rel_residual_true"],
     }
+    if world == 1 and not args.no_slab_probe:
+        line["slab_emulation"] = _slab_probe(dev)
     if world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = _cpu_baseline(problems, reps[-1]["iterations_per"])
     print(json.dumps(line), flush=True)
@@ -381,6 +428,7 @@ def main():
     ap.add_argument("--route", default="kron", choices=["kron", "sylvester"])
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-slab-probe", action="store_true")
     ap.add_argument("--ref-iters", type=int, default=8, help="oracle CG iterations per reference step")
     ap.add_argument("--ref-face-iters", type=int, default=180,
                     help="fallback iterations per face if tests/golden/oracle_iterations.json lacks the config")

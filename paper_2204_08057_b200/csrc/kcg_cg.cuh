@@ -252,14 +252,6 @@ __device__ __forceinline__ void pull_states(const CgArgs& a, SysState* st, const
 // ------------------------------------------------------------------ row-slab cross-rank protocol
 // System-scope release/acquire on 64-bit flags in (peer) global memory, and a barrier over the CTAs
 // of one rank's group (a monotonic counter zeroed before each launch).
-__device__ __forceinline__ unsigned long long ld_acquire_sys_u64(const unsigned long long* p) {
-  unsigned long long v;
-  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
-  return v;
-}
-__device__ __forceinline__ void st_release_sys_u64(unsigned long long* p, unsigned long long v) {
-  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
-}
 __device__ __forceinline__ unsigned ld_acquire_gpu_u32(const unsigned* p) {
   unsigned v;
   asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
@@ -271,31 +263,42 @@ __device__ __forceinline__ void spin_geq_u32(const unsigned* p, unsigned target)
   while (ld_acquire_gpu_u32(p) < target)
     if (clock64() - t0 > (1LL << 34)) __trap();
 }
-__device__ __forceinline__ void spin_geq_sys_u64(const unsigned long long* p, unsigned long long target) {
-  const long long t0 = clock64();
-  while (ld_acquire_sys_u64(p) < target)
-    if (clock64() - t0 > (1LL << 34)) __trap();
-}
 // Barrier over the ncta CTAs of one group: generation `epoch` (1, 2, ...) completes when the counter
 // reaches epoch * ncta.
+// The fence is system scope: it also publishes (cumulatively, after the CTA barrier) the CTA's
+// peer stores of ghost rows before the rank's CTA 0 raises its cross-rank flag.
 __device__ __forceinline__ void group_sync(unsigned* ctr, int ncta, unsigned epoch) {
   __syncwarp();
   __syncthreads();
   if (threadIdx.x == 0) {
-    __threadfence();
+    __threadfence_system();
     atomicAdd(ctr, 1u);
     spin_geq_u32(ctr, epoch * (unsigned)ncta);
     __threadfence();
   }
   __syncthreads();
 }
-// Cross-rank rendezvous on `tag` by thread 0 of a rank's CTA 0: publish to every rank, wait for all.
+__device__ __forceinline__ unsigned long long ld_relaxed_sys_u64(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.relaxed.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_relaxed_sys_u64(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.relaxed.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+// Cross-rank rendezvous on `tag` by one thread: ONE system-scope fence, then relaxed stores of the
+// tag into every rank's flag array (release by fence + store); waiting polls the flags with relaxed
+// system-scope loads and fences once after all of them (acquire).  A release / acquire per flag
+// would serialise G fences.
 __device__ __forceinline__ void xrank_signal(const CgArgs& a, unsigned long long tag) {
   __threadfence_system();
-  for (int q = 0; q < a.nranks; ++q) st_release_sys_u64(a.flags[q] + a.rank, tag);
+  for (int q = 0; q < a.nranks; ++q) st_relaxed_sys_u64(a.flags[q] + a.rank, tag);
 }
 __device__ __forceinline__ void xrank_wait(const CgArgs& a, unsigned long long tag) {
-  for (int q = 0; q < a.nranks; ++q) spin_geq_sys_u64(a.my_flags + q, tag);
+  const long long t0 = clock64();
+  for (int q = 0; q < a.nranks; ++q)
+    while (ld_relaxed_sys_u64(a.my_flags + q) < tag)
+      if (clock64() - t0 > (1LL << 34)) __trap();
   __threadfence_system();
 }
 
@@ -1084,7 +1087,6 @@ __device__ __forceinline__ void cg_body(const CgArgs& a, const CgMaps& maps, con
     // overlaps the reduction; verified against the new active count at the top of the loop
     const int spec_t = (KCG_SERP && !rev) ? ntiles - 1 - cta : cta;
     const bool do_spec = it >= 0 && cta < ntiles;
-    if (SLAB) __threadfence_system();  // this thread's ghost-row stores into the neighbours
     iteration_reduce<NT, NP, SLAB>(a, st, act, nact, par_out, it, rs, cta, ncta, gepoch, [&]() {
       if (tr && cta == 0) a.trace[(size_t)(it + 1) * KCG_TRACE_COLS + 1] = globaltimer();
       if (KCG_DYN && cta == 0) *ctr = 0u;  // quiescent now; next used two passes later

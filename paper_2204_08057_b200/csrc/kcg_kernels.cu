@@ -242,9 +242,12 @@ __global__ void xrank_sync_kernel(XrankSync X) {
   if (threadIdx.x != 0) return;
   __threadfence_system();
   for (int j = 0; j < X.nlocal; ++j)
-    for (int q = 0; q < X.nranks; ++q) st_release_sys_u64(X.flags[q] + X.rank0 + j, X.tag);
+    for (int q = 0; q < X.nranks; ++q) st_relaxed_sys_u64(X.flags[q] + X.rank0 + j, X.tag);
+  const long long t0 = clock64();
   for (int j = 0; j < X.nlocal; ++j)
-    for (int q = 0; q < X.nranks; ++q) spin_geq_sys_u64(X.flags[X.rank0 + j] + q, X.tag);
+    for (int q = 0; q < X.nranks; ++q)
+      while (ld_relaxed_sys_u64(X.flags[X.rank0 + j] + q) < X.tag)
+        if (clock64() - t0 > (1LL << 34)) __trap();
   __threadfence_system();
 }
 

@@ -54,3 +54,39 @@ def makespan(costs: Sequence[float], plan: List[List[int]]) -> float:
 
 def shard_for_rank(costs: Sequence[float], world: int, rank: int) -> List[int]:
     return assign_lpt(costs, world)[rank]
+
+
+# ----------------------------------------------------------------------------- slab groups
+# With more GPUs than faces can balance (12 faces over 8 GPUs: 1.5 faces each, per-face iteration
+# counts 89-319), ranks are grouped: a group of g ranks splits each of its faces into g row slabs
+# (kron_cg_create_slab) and faces are assigned to groups by LPT.  A single face
+# (planck, stress) is split over all ranks.
+# Modelled per-pass cost of the cross-rank exchange (halo rows + scalar sum), in units of one full
+# face's CG pass (~40 us on a B200 for N = 4^10, k = 4; the exchange is a few us over NVLink).
+SLAB_PASS_OVERHEAD = 0.15
+
+
+def plan_groups(costs: Sequence[float], world: int):
+    """Choose the group size g (a power of two dividing world, <= 8) minimising the modelled
+    makespan  max_group(sum cost) / g + SLAB_PASS_OVERHEAD * max_group(max cost) [g > 1]
+    (faces of a group iterate together in one batch; converged faces drop out, so the group's
+    passes = its slowest face's).  Ties -> smaller g.  Returns (g, faces_per_group) with
+    faces_per_group[j] the faces of group j (ranks j*g .. j*g+g-1)."""
+    best = None
+    g = 1
+    while g <= min(world, 8):
+        if world % g == 0:
+            plan = assign_lpt(costs, world // g)
+            t = makespan(costs, plan) / g
+            if g > 1:
+                t += SLAB_PASS_OVERHEAD * max(max(costs[i] for i in part) for part in plan if part)
+            if best is None or t < best[0] - 1e-12:
+                best = (t, g, plan)
+        g *= 2
+    return best[1], best[2]
+
+
+def rank_role(costs: Sequence[float], world: int, rank: int):
+    """(g, group index, slab index within the group, faces of the group) of one rank."""
+    g, plan = plan_groups(costs, world)
+    return g, rank // g, rank % g, plan[rank // g]

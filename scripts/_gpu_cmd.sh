@@ -1,5 +1,3 @@
 mkdir -p gpurun_out
-timeout 1500 python -m pytest tests -q -m gpu > gpurun_out/pytest_gpu.log 2>&1; echo pytest rc $? >> gpurun_out/pytest_gpu.log
-for c in "planck 200 kron" "fullsky 40 kron" "fullsky 40 sylvester" "stress 60 kron"; do
-    timeout 200 python scripts/kernel_probe.py $c 2>&1 | tail -1
-done > gpurun_out/probe.txt 2>&1
+for G in 2 8; do KCG_LIB_PATH=paper_2204_08057_b200/lib/variants/trace.so timeout 300 python scripts/trace_slab.py $G; done > gpurun_out/trace_slab.txt 2>&1
+KCG_LIB_PATH=paper_2204_08057_b200/lib/variants/trace.so timeout 300 python scripts/trace_probe.py planck 100 kron >> gpurun_out/trace_slab.txt 2>&1

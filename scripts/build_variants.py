@@ -6,8 +6,7 @@ sys.path.insert(0, ROOT)
 from paper_2204_08057_b200 import build
 
 VARIANTS = {
-    "n512": [],
-    "n256": ["KCG_NT4=256"],
+    "trace": ["KCG_TRACE=1"],
 }
 names = sys.argv[1:] or list(VARIANTS)
 out = os.path.join(ROOT, "paper_2204_08057_b200", "lib", "variants")
