@@ -7,8 +7,10 @@ PAPER.md:
   * Sec. 3 P:L100-106 -- D_{j1 j2} = 1 for neighbours, 0 otherwise, and the diagonal is
     minus the row sum of the off-diagonals; i.e. D = Adj - Deg = -(graph Laplacian).
   * Alg.MatvecD P:L128-138 -- v(j) <- sum of neighbours - rowsum * v(j).
-Readings (R1, R2, R11): row-major pixel order idx = y*side + x; free face
-boundary (corner 2, edge 3, interior 4 neighbours); Alg.MatvecD evaluated out-of-place.
+Readings (R1, R2, R11): row-major pixel order idx = y*side + x (default) or the
+HEALPix NESTED order inside a face (the bits of x on the even, of y on the odd positions of idx,
+i.e. the Z-order curve; "Find neighbours" works on HEALPix indices); free face boundary
+(corner 2, edge 3, interior 4 neighbours); Alg.MatvecD evaluated out-of-place.
 """
 
 from __future__ import annotations
@@ -21,6 +23,25 @@ def side_of(level: int) -> int:
     if level < 0 or level > 12:
         raise ValueError("level out of range [0, 12]")
     return 1 << level
+
+
+def nest_index(level: int, x: int, y: int) -> int:
+    """HEALPix NESTED index of pixel (x, y) inside a face: bit b of x -> bit 2b, of y -> 2b+1."""
+    out = 0
+    for b in range(level):
+        out |= ((x >> b) & 1) << (2 * b)
+        out |= ((y >> b) & 1) << (2 * b + 1)
+    return out
+
+
+def pixel_index(level: int, layout: str = "row"):
+    """[side][side] array of the pixel index of (y, x) in the given layout ("row" or "nested")."""
+    s = side_of(level)
+    if layout == "row":
+        return np.arange(s * s).reshape(s, s)
+    if layout == "nested":
+        return np.array([[nest_index(level, x, y) for x in range(s)] for y in range(s)], dtype=np.int64)
+    raise ValueError(f"unknown layout {layout!r}")
 
 
 def neighbors(level: int, j: int) -> list:
@@ -41,11 +62,11 @@ def neighbors(level: int, j: int) -> list:
     return sorted(out)
 
 
-def adjacency(level: int) -> sp.csr_matrix:
-    """Adjacency matrix of the face grid (symmetric 0/1), scipy CSR."""
+def adjacency(level: int, layout: str = "row") -> sp.csr_matrix:
+    """Adjacency matrix of the face grid (symmetric 0/1) with pixels numbered in `layout`."""
     s = side_of(level)
     N = s * s
-    idx = np.arange(N).reshape(s, s)
+    idx = pixel_index(level, layout)
     rows, cols = [], []
     # horizontal edges (y, x) -- (y, x+1)
     a = idx[:, :-1].ravel()
@@ -62,20 +83,20 @@ def adjacency(level: int) -> sp.csr_matrix:
     return sp.csr_matrix((np.ones(r.size), (r, c)), shape=(N, N))
 
 
-def rowsums(level: int) -> np.ndarray:
+def rowsums(level: int, layout: str = "row") -> np.ndarray:
     """Precomputed off-diagonal row sums of D = neighbour counts."""
-    return np.asarray(adjacency(level).sum(axis=1)).ravel()
+    return np.asarray(adjacency(level, layout).sum(axis=1)).ravel()
 
 
-def D_matrix(level: int) -> sp.csr_matrix:
+def D_matrix(level: int, layout: str = "row") -> sp.csr_matrix:
     """D with D_ij = 1 for neighbours and D_jj = -sum_{l != j} D_jl (P:L102-106)."""
-    Adj = adjacency(level)
-    return (Adj - sp.diags(rowsums(level))).tocsr()
+    Adj = adjacency(level, layout)
+    return (Adj - sp.diags(rowsums(level, layout))).tocsr()
 
 
-def laplacian(level: int) -> sp.csr_matrix:
+def laplacian(level: int, layout: str = "row") -> sp.csr_matrix:
     """Graph Laplacian L = Deg - Adj = -D."""
-    return (-D_matrix(level)).tocsr()
+    return (-D_matrix(level, layout)).tocsr()
 
 
 def apply_D_loop(level: int, v: np.ndarray) -> np.ndarray:

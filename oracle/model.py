@@ -22,14 +22,14 @@ import scipy.sparse as sp
 from . import grid
 
 
-def prior_Q0(level: int, kappa2: float, prior: str = "laplacian") -> sp.csr_matrix:
-    """Single-source prior precision Q0 (before the per-source scale phi_l)."""
+def prior_Q0(level: int, kappa2: float, prior: str = "laplacian", layout: str = "row") -> sp.csr_matrix:
+    """Single-source prior precision Q0 (before the per-source scale phi_l), pixels in `layout`."""
     N = grid.side_of(level) ** 2
     I = sp.identity(N, format="csr")
     if prior == "laplacian":
-        return (kappa2 * I + grid.laplacian(level)).tocsr()
+        return (kappa2 * I + grid.laplacian(level, layout)).tocsr()
     if prior == "d2":
-        D = grid.D_matrix(level)
+        D = grid.D_matrix(level, layout)
         return (D @ D + kappa2 * I).tocsr()
     raise ValueError(f"unknown prior {prior!r}")
 
@@ -55,17 +55,19 @@ def C_matrix(level: int, noise_prec: np.ndarray, hits=None) -> sp.csr_matrix:
     return sp.diags(np.kron(np.asarray(noise_prec, dtype=np.float64), h)).tocsr()
 
 
-def Q_matrix(level: int, tau: np.ndarray, kappa2: float, prior: str = "laplacian") -> sp.csr_matrix:
+def Q_matrix(level: int, tau: np.ndarray, kappa2: float, prior: str = "laplacian",
+             layout: str = "row") -> sp.csr_matrix:
     """Q = P (x) Q0, P = diag(phi) (P:L140-148)."""
     return sp.kron(sp.diags(np.asarray(tau, dtype=np.float64)),
-                   prior_Q0(level, kappa2, prior), format="csr")
+                   prior_Q0(level, kappa2, prior, layout), format="csr")
 
 
-def assemble_G(level, A, noise_prec, tau, kappa2, hits=None, prior="laplacian") -> sp.csr_matrix:
-    """G = Q + B^T C B  (Eq.(Q*) P:L75, Eq.(Axb)), literal sparse assembly."""
+def assemble_G(level, A, noise_prec, tau, kappa2, hits=None, prior="laplacian", layout="row") -> sp.csr_matrix:
+    """G = Q + B^T C B  (Eq.(Q*) P:L75, Eq.(Axb)), literal sparse assembly.  `hits` is a
+    vector in the same pixel layout as the grid."""
     B = B_matrix(level, A)
     C = C_matrix(level, noise_prec, hits)
-    Q = Q_matrix(level, tau, kappa2, prior)
+    Q = Q_matrix(level, tau, kappa2, prior, layout)
     return (B.T @ C @ B + Q).tocsr()
 
 
@@ -82,10 +84,23 @@ def assemble_rhs(level, A, noise_prec, Y, hits=None) -> np.ndarray:
     return B.T @ (C @ vec_maps(Y))
 
 
-def problem_system(p):
-    """(G, b) for a synth.PatchProblem-like object."""
-    G = assemble_G(p.level, p.A, p.noise_prec, p.tau, p.kappa2, p.hits, p.prior)
-    b = assemble_rhs(p.level, p.A, p.noise_prec, p.Y, p.hits)
+def to_layout(level: int, maps: np.ndarray, layout: str) -> np.ndarray:
+    """Maps stored as [..][side][side] (row, column) -> [..][N] vectors in `layout` order."""
+    maps = np.asarray(maps, dtype=np.float64)
+    s = grid.side_of(level)
+    flat = maps.reshape(maps.shape[:-2] + (s * s,))
+    if layout == "row":
+        return flat.copy()
+    out = np.empty_like(flat)
+    out[..., grid.pixel_index(level, layout).reshape(-1)] = flat
+    return out
+
+
+def problem_system(p, layout: str = "row"):
+    """(G, b) for a synth.PatchProblem-like object, pixels numbered in `layout`."""
+    hits = None if p.hits is None else to_layout(p.level, p.hits, layout)
+    G = assemble_G(p.level, p.A, p.noise_prec, p.tau, p.kappa2, hits, p.prior, layout)
+    b = assemble_rhs(p.level, p.A, p.noise_prec, to_layout(p.level, p.Y, layout), hits)
     return G, b
 
 

@@ -88,13 +88,26 @@ __device__ __forceinline__ double warp_sum(double v) {
   return v;
 }
 
+// --------------------------------------------------------------------------- NESTED order
+// HEALPix NESTED pixel index inside a face (reading R1): bit b of x -> bit 2b, bit b of y -> 2b+1.
+__device__ __forceinline__ uint32_t part1by1(uint32_t v) {
+  v &= 0xffffu;
+  v = (v | (v << 8)) & 0x00ff00ffu;
+  v = (v | (v << 4)) & 0x0f0f0f0fu;
+  v = (v | (v << 2)) & 0x33333333u;
+  v = (v | (v << 1)) & 0x55555555u;
+  return v;
+}
+__device__ __forceinline__ uint32_t nest_of(uint32_t x, uint32_t y) { return part1by1(x) | (part1by1(y) << 1); }
+
 // --------------------------------------------------------------------------- rhs
 // b[p][c][j] = h_j sum_f Y[p][f][j] E[p][f][c];  r0 = b (internal pitch), p0 = 0, x = 0.
 template <int K>
 __global__ void __launch_bounds__(256) rhs_kernel(const double* __restrict__ Y, const double* __restrict__ E,
                                                   const double* __restrict__ hits, double* __restrict__ r0,
                                                   double* __restrict__ p0, double* __restrict__ x, int n,
-                                                  int side, int rows, int pitch, int ghost, int hghost) {
+                                                  int side, int rows, int pitch, int ghost, int hghost,
+                                                  int nested) {
   extern __shared__ double Es[];  // [n][K]
   const int p = blockIdx.y;
   for (int e = threadIdx.x; e < n * K; e += blockDim.x) Es[e] = E[(size_t)p * n * K + e];
@@ -105,7 +118,8 @@ __global__ void __launch_bounds__(256) rhs_kernel(const double* __restrict__ Y, 
     double acc[K];
 #pragma unroll
     for (int c = 0; c < K; ++c) acc[c] = 0.0;
-    const double* yp = Y + (size_t)p * n * N + j;
+    const size_t jy = nested ? nest_of((uint32_t)(j % side), (uint32_t)(j / side)) : j;  // Y's pixel index
+    const double* yp = Y + (size_t)p * n * N + jy;
     for (int f = 0; f < n; ++f) {
       const double y = __ldg(yp + (size_t)f * N);
 #pragma unroll

@@ -39,7 +39,7 @@ const unsigned long long kPostTag = 1ull << 31;  // tags of the post-CG rendezvo
 // Per-rank workspace carving.
 struct Layout {
   size_t r0, r1, p0, p1, partials, state, history, sync, group, resid_partials, resid_out, params_kron, params_syl,
-      E_kron, E_syl, W, Y_stage, mu_stage, trace, slots, flags, xg_top, xg_bot, rslots, total;
+      E_kron, E_syl, W, Y_stage, mu_stage, trace, slots, flags, xg_top, xg_bot, rslots, x_rm, y_rm, hits_rm, total;
   size_t vec_doubles, partial_doubles;
 };
 
@@ -88,6 +88,11 @@ Layout layout_of(const kcg_desc* d, int nranks) {
   L.xg_top = take(P * k * (size_t)side * 8);
   L.xg_bot = take(P * k * (size_t)side * 8);
   L.rslots = take((size_t)nranks * P * 2 * 8);
+  if (d->layout == KCG_LAYOUT_NESTED) {  // row-major working copies (the kernels' layout)
+    L.x_rm = take(P * k * N * 8);
+    L.y_rm = take(P * k * N * 8);
+    L.hits_rm = take(P * N * 8);
+  }
   L.total = off;
   return L;
 }
@@ -105,12 +110,13 @@ struct RankState {
   double *E_kron = nullptr, *E_syl = nullptr, *W_dev = nullptr, *Y_stage = nullptr, *mu_stage = nullptr;
   long long* trace = nullptr;
   double *slots = nullptr, *xg_top = nullptr, *xg_bot = nullptr, *rslots = nullptr;
+  double *x_rm = nullptr, *y_rm = nullptr, *hits_rm = nullptr;  // NESTED layout only
   unsigned long long* flags = nullptr;
   const double* hits = nullptr;
   CgMaps maps_kron, maps_syl;
 };
 
-RankState carve(char* ws, const Layout& L, int rank, int rows, bool staging) {
+RankState carve(char* ws, const Layout& L, int rank, int rows, bool staging, bool nested) {
   RankState R;
   R.rank = rank;
   R.row0 = rank * rows;
@@ -141,6 +147,11 @@ RankState carve(char* ws, const Layout& L, int rank, int rows, bool staging) {
   R.xg_top = reinterpret_cast<double*>(ws + L.xg_top);
   R.xg_bot = reinterpret_cast<double*>(ws + L.xg_bot);
   R.rslots = reinterpret_cast<double*>(ws + L.rslots);
+  if (nested) {
+    R.x_rm = reinterpret_cast<double*>(ws + L.x_rm);
+    R.y_rm = reinterpret_cast<double*>(ws + L.y_rm);
+    R.hits_rm = reinterpret_cast<double*>(ws + L.hits_rm);
+  }
   return R;
 }
 
@@ -184,7 +195,7 @@ bool desc_ok(const kcg_desc* d, std::string* why) {
 
 bool config_ok(const kcg_desc* d, std::string* why) {
   if (d->prior != KCG_PRIOR_LAPLACIAN) { *why = "only KCG_PRIOR_LAPLACIAN is built"; return false; }
-  if (d->layout != KCG_LAYOUT_ROW_MAJOR) { *why = "only KCG_LAYOUT_ROW_MAJOR is built"; return false; }
+  if (d->layout != KCG_LAYOUT_ROW_MAJOR && d->layout != KCG_LAYOUT_NESTED) { *why = "unknown layout"; return false; }
   if (d->precond != KCG_PRECOND_NONE && d->precond != KCG_PRECOND_BLOCK_JACOBI) { *why = "unknown precond"; return false; }
   if (d->precond == KCG_PRECOND_BLOCK_JACOBI && d->n_comp > 7) {
     *why = "KCG_PRECOND_BLOCK_JACOBI is built for n_comp <= 7 (shared-memory budget)";
@@ -375,7 +386,7 @@ kcg_status cuda_fail(kcg_ctx* c, cudaError_t e, const char* what) {
 enum Route { ROUTE_KRON = 0, ROUTE_SYL = 1 };
 
 SlabGeom geom_of(const kcg_ctx* c, const RankState& R) {
-  return SlabGeom{c->side, c->rows, R.row0, c->pitch, c->ghost, c->ghost};
+  return SlabGeom{c->side, c->rows, R.row0, c->pitch, c->ghost, c->ghost, c->d.layout == KCG_LAYOUT_NESTED};
 }
 
 // Device pointer of `field` in rank g's workspace (same layout on every rank).
@@ -443,7 +454,9 @@ kcg_status solve_impl(kcg_ctx* c, Route route, const double* Y_in, double* mu_ou
   const bool prec = c->d.precond == KCG_PRECOND_BLOCK_JACOBI;
   const unsigned long long tag0 = (++c->solve_id) << 32;
   auto Yr = [&](int j) -> const double* { return host_io ? c->R[j].Y_stage : Y_in + j * y_stride; };
-  auto mur = [&](int j) -> double* { return host_io ? c->R[j].mu_stage : mu_out + j * mu_stride; };
+  auto muu = [&](int j) -> double* { return host_io ? c->R[j].mu_stage : mu_out + j * mu_stride; };
+  // the kernels' solution buffer: the user's mu, or the row-major copy for a NESTED layout
+  auto mur = [&](int j) -> double* { return c->R[j].x_rm ? c->R[j].x_rm : muu(j); };
 
   CK(cudaEventRecord(c->ev[0], s), "event");
   for (int j = 0; j < c->nlocal; ++j) {
@@ -545,6 +558,8 @@ kcg_status solve_impl(kcg_ctx* c, Route route, const double* Y_in, double* mu_ou
     }
   }
   if (c->slab) CK(kcg::launch_xrank_sync(s, xsync_of(c, tag0 + kPostTag + 2)), "rendezvous kernel");
+  for (int j = 0; j < c->nlocal; ++j)
+    if (c->R[j].x_rm) CK(kcg::launch_permute(s, c->R[j].x_rm, muu(j), (size_t)P * k, c->side, true), "permute mu");
   c->st_host.resize(n_sys);
   const int nr = c->slab ? c->nranks : 1;
   c->resid_host.resize((size_t)nr * P * 2);
@@ -637,6 +652,8 @@ kcg_status create_impl(const kcg_desc* d, const kcg_slab* sl, const double* A_ho
   if (!config_ok(d, &why)) return fail(KCG_E_CONFIG, why);
   const int G = sl ? sl->nranks : 1;
   if (!slab_ok(d, G, &why)) return fail(KCG_E_SHAPE, why);
+  if (sl && d->layout == KCG_LAYOUT_NESTED)
+    return fail(KCG_E_CONFIG, "row slabs need KCG_LAYOUT_ROW_MAJOR (a NESTED face is not split into row slabs)");
   if (sl && (sl->rank0 < 0 || sl->nlocal < 1 || sl->rank0 + sl->nlocal > G || (sl->nlocal != 1 && sl->nlocal != G)))
     return fail(KCG_E_CONFIG, "slab: need 0 <= rank0, rank0 + nlocal <= nranks and nlocal in {1, nranks}");
   if (!A_host || !T_host || !phi_host || !kappa2_host) return fail(KCG_E_ARG, "null parameter pointer");
@@ -679,7 +696,8 @@ kcg_status create_impl(const kcg_desc* d, const kcg_slab* sl, const double* A_ho
     c->peer_ws.assign(1, reinterpret_cast<char*>(workspace_dev));
   }
   for (int j = 0; j < c->nlocal; ++j) {
-    c->R.push_back(carve(c->peer_ws[c->rank0 + j], c->L, c->rank0 + j, c->rows, d->host_staging != 0));
+    c->R.push_back(carve(c->peer_ws[c->rank0 + j], c->L, c->rank0 + j, c->rows, d->host_staging != 0,
+                         d->layout == KCG_LAYOUT_NESTED));
     // hits [nlocal][P][rows + 2 ghost][side] (ghost rows = the face's rows beyond the slab, 0 outside)
     c->R.back().hits = hits_dev ? hits_dev + (size_t)j * P * (c->rows + 2 * c->ghost) * c->side : nullptr;
   }
@@ -741,6 +759,10 @@ kcg_status create_impl(const kcg_desc* d, const kcg_slab* sl, const double* A_ho
   const size_t planes = (size_t)P * k;
   const int buf_rows = c->rows + 2 * c->ghost;
   for (RankState& R : c->R) {
+    if (R.hits_rm && R.hits) {  // NESTED hits -> the kernels' row-major copy
+      CKC(kcg::launch_permute(c->stream, R.hits, R.hits_rm, (size_t)P, c->side, false), "permute hits");
+      R.hits = R.hits_rm;
+    }
     CKC(cudaMemcpyAsync(R.params_kron, pk.data(), P * sizeof(SysParams), cudaMemcpyHostToDevice, c->stream), "H2D");
     CKC(cudaMemcpyAsync(R.params_syl, ps.data(), (size_t)P * k * sizeof(SysParams), cudaMemcpyHostToDevice, c->stream),
         "H2D");
@@ -843,9 +865,17 @@ kcg_status kron_cg_apply(kcg_ctx* c, const double* x, double* y) {
   }
   for (int j = 0; j < c->nlocal; ++j) {
     const RankState& R = c->R[j];
-    CK(kcg::launch_apply(c->k, c->stream, R.params_kron, x + j * stride, y + j * stride, R.hits, c->P, geom_of(c, R),
+    const double* xi = x + j * stride;
+    double* yo = y + j * stride;
+    if (R.x_rm) {  // NESTED: gather, apply in row-major, scatter
+      CK(kcg::launch_permute(c->stream, xi, R.x_rm, (size_t)c->P * c->k, c->side, false), "permute x");
+      xi = R.x_rm;
+      yo = R.y_rm;
+    }
+    CK(kcg::launch_apply(c->k, c->stream, R.params_kron, xi, yo, R.hits, c->P, geom_of(c, R),
                          c->slab ? R.xg_top : nullptr, c->slab ? R.xg_bot : nullptr),
        "apply kernel");
+    if (R.x_rm) CK(kcg::launch_permute(c->stream, R.y_rm, y + j * stride, (size_t)c->P * c->k, c->side, true), "permute y");
   }
   if (c->slab) {  // nobody rewrites a neighbour's xg_* before everyone is done reading it
     const unsigned long long tag0 = c->solve_id << 32;
@@ -860,10 +890,13 @@ kcg_status kron_cg_rhs(kcg_ctx* c, const double* Y, double* b) {
   if (!Y || !b) { c->err = "null Y or b"; return KCG_E_ARG; }
   for (int j = 0; j < c->nlocal; ++j) {
     const RankState& R = c->R[j];
-    SlabGeom g{c->side, c->rows, R.row0, c->side, 0, c->ghost};  // b written densely [P][k][rows][side]
-    CK(kcg::launch_rhs(c->k, c->stream, Y + j * (size_t)c->P * c->n * c->N, R.E_kron, R.hits,
-                       b + j * (size_t)c->P * c->k * c->N, nullptr, nullptr, c->P, c->n, g),
+    SlabGeom g{c->side, c->rows, R.row0, c->side, 0, c->ghost, c->d.layout == KCG_LAYOUT_NESTED};  // dense b
+    double* bo = R.y_rm ? R.y_rm : b + j * (size_t)c->P * c->k * c->N;
+    CK(kcg::launch_rhs(c->k, c->stream, Y + j * (size_t)c->P * c->n * c->N, R.E_kron, R.hits, bo, nullptr, nullptr,
+                       c->P, c->n, g),
        "rhs kernel");
+    if (R.y_rm) CK(kcg::launch_permute(c->stream, R.y_rm, b + j * (size_t)c->P * c->k * c->N, (size_t)c->P * c->k,
+                                       c->side, true), "permute b");
   }
   CK(cudaStreamSynchronize(c->stream), "rhs");
   return KCG_OK;

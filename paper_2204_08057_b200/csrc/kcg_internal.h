@@ -156,6 +156,7 @@ struct XrankSync {           // local ranks [rank0, rank0 + nlocal) meet every r
 struct SlabGeom {
   int side, rows, row0, pitch, ghost;
   int hits_ghost;            // ghost rows of the hits planes (= ghost, except for the dense rhs output)
+  int nested;                // 1: the data maps Y are in HEALPix NESTED order inside the face (reading R1)
 };
 
 // ---------------------------------------------------------------- launchers (kcg_kernels.cu)
@@ -181,6 +182,8 @@ cudaError_t launch_xghost(cudaStream_t s, const double* x, double* up_xg_bot, do
                           const SlabGeom& g);
 cudaError_t launch_put(cudaStream_t s, const XrankPut& P);
 cudaError_t launch_xrank_sync(cudaStream_t s, const XrankSync& X);
+// dst[plane][nest(x,y)] = src[plane][y side + x] (to_nested) or the inverse gather.
+cudaError_t launch_permute(cudaStream_t s, const double* src, double* dst, size_t planes, int side, bool to_nested);
 int apply_tiles_per_sys(int rows, int side);
 
 }  // namespace kcg

@@ -31,7 +31,8 @@ __global__ void __launch_bounds__(AP_NT) apply_kernel(const SysParams* __restric
                                                       const double* __restrict__ Y, const double* __restrict__ E,
                                                       const double* __restrict__ hits,
                                                       double* __restrict__ partials, int n, int side, int rows,
-                                                      int row0, int ghost, const double* __restrict__ xg_top,
+                                                      int row0, int ghost, int nested,
+                                                      const double* __restrict__ xg_top,
                                                       const double* __restrict__ xg_bot) {
   constexpr int BW = AP_TX + 2, BH = AP_TY + 2, PLANE = BW * BH;
   extern __shared__ double xs[];  // [K][BH][BW], then E [n][K] if RESID
@@ -80,7 +81,7 @@ __global__ void __launch_bounds__(AP_NT) apply_kernel(const SysParams* __restric
     if (RESID) {
 #pragma unroll
       for (int c = 0; c < K; ++c) bq[c] = 0.0;
-      const double* yp = Y + (size_t)s * n * N + (size_t)ly * side + gx;
+      const double* yp = Y + (size_t)s * n * N + (nested ? (size_t)nest_of(gx, ly) : (size_t)ly * side + gx);
       for (int f = 0; f < n; ++f) {
         const double yv = yp[(size_t)f * N];
 #pragma unroll
@@ -251,6 +252,18 @@ __global__ void xrank_sync_kernel(XrankSync X) {
   __threadfence_system();
 }
 
+// --------------------------------------------------------------------------- NESTED permutation
+__global__ void __launch_bounds__(256) permute_kernel(const double* __restrict__ src, double* __restrict__ dst,
+                                                      size_t planes, int side, int to_nested) {
+  const size_t N = (size_t)side * side;
+  for (size_t e = (size_t)blockIdx.x * blockDim.x + threadIdx.x; e < planes * N; e += (size_t)gridDim.x * blockDim.x) {
+    const size_t pl = e / N, j = e - pl * N;
+    const size_t jn = nest_of((uint32_t)(j % side), (uint32_t)(j / side));
+    if (to_nested) dst[pl * N + jn] = src[e];
+    else dst[e] = src[pl * N + jn];
+  }
+}
+
 // --------------------------------------------------------------------------- launchers
 #define KCG_DISPATCH(K, CALL)                 \
   switch (K) {                                \
@@ -277,7 +290,7 @@ cudaError_t launch_rhs(int K, cudaStream_t s, const double* Y, const double* E, 
   dim3 gr(grid_for(N), P);
   const size_t sm = (size_t)n * K * sizeof(double);
   KCG_DISPATCH(K, (rhs_kernel<KK><<<gr, 256, sm, s>>>(Y, E, hits, r0, p0, x, n, g.side, g.rows, g.pitch, g.ghost,
-                                                     g.hits_ghost)));
+                                                     g.hits_ghost, g.nested)));
   return cudaGetLastError();
 }
 
@@ -305,7 +318,7 @@ static cudaError_t apply_t(cudaStream_t s, const SysParams* params, const double
   if (e != cudaSuccess) return e;
   dim3 gr(apply_tiles_per_sys(g.rows, g.side), n_sys);
   apply_kernel<K, R><<<gr, AP_NT, sm, s>>>(params, x, y, Y, E, hits, partials, n, g.side, g.rows, g.row0,
-                                           g.hits_ghost, xg_top, xg_bot);
+                                           g.hits_ghost, g.nested, xg_top, xg_bot);
   return cudaGetLastError();
 }
 
@@ -368,4 +381,13 @@ cudaError_t launch_xrank_sync(cudaStream_t s, const XrankSync& X) {
   return cudaGetLastError();
 }
 
+}  // namespace kcg
+
+namespace kcg {
+cudaError_t launch_permute(cudaStream_t s, const double* src, double* dst, size_t planes, int side, bool to_nested) {
+  const size_t n = planes * (size_t)side * side;
+  permute_kernel<<<(unsigned)std::max<size_t>(1, std::min<size_t>((n + 255) / 256, 148 * 8)), 256, 0, s>>>(
+      src, dst, planes, side, to_nested ? 1 : 0);
+  return cudaGetLastError();
+}
 }  // namespace kcg

@@ -107,3 +107,28 @@ def test_level_range_errors():
         grid.side_of(13)
     with pytest.raises(IndexError):
         grid.neighbors(1, 4)
+
+
+def test_nested_index_is_the_z_order_curve():
+    """HEALPix NESTED inside a face = Morton / Z-order: level 2 visits the 2x2 blocks in Z order and
+    each block in Z order (pixel (x, y) listed by increasing nested index)."""
+    order = sorted(((grid.nest_index(2, x, y), (x, y)) for y in range(4) for x in range(4)))
+    assert [xy for _, xy in order] == [(0, 0), (1, 0), (0, 1), (1, 1), (2, 0), (3, 0), (2, 1), (3, 1),
+                                       (0, 2), (1, 2), (0, 3), (1, 3), (2, 2), (3, 2), (2, 3), (3, 3)]
+    for level in (0, 1, 3, 5):
+        idx = grid.pixel_index(level, "nested").reshape(-1)
+        assert sorted(idx) == list(range(4 ** level))          # a permutation
+    assert grid.nest_index(10, 1023, 1023) == 4 ** 10 - 1
+
+
+@pytest.mark.parametrize("level", [1, 2, 4])
+def test_nested_laplacian_is_the_permuted_row_major_one(level):
+    """L_nested = Pi L_row Pi^T with Pi the row-major -> nested permutation (the grid graph does not
+    depend on how its vertices are numbered)."""
+    perm = grid.pixel_index(level, "nested").reshape(-1)      # perm[row-major j] = nested index
+    N = 4 ** level
+    Pi = np.zeros((N, N))
+    Pi[perm, np.arange(N)] = 1.0
+    Ln = grid.laplacian(level, "nested").toarray()
+    Lr = grid.laplacian(level).toarray()
+    assert np.array_equal(Ln, Pi @ Lr @ Pi.T)
