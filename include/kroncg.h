@@ -9,7 +9,8 @@
  * grid with free boundary (reading R2).  In matrix form, with X = reshape(mu, N, k):
  *   G vec(X) = vec( N_h X M + Q0 X P ),   M = A^T T A,   P = diag(prior_scale),
  *   b        = vec( N_h Y T A ),
- *   Q0 = kappa2 I + L  (KCG_PRIOR_LAPLACIAN; BASELINE configs, reading R3/R24),
+ *   Q0 = kappa2 I + L  (KCG_PRIOR_LAPLACIAN; BASELINE configs, reading R3/R24) or
+ *   Q0 = D^2 + kappa2 I (KCG_PRIOR_D2; the paper's phi D^2),
  *   L  = graph Laplacian of the 4-neighbour face grid = -D of P:L100-106.
  *
  * Routes:
@@ -81,9 +82,12 @@ typedef struct {
   int n_freq;       /* n, number of frequency maps; 1 <= n <= 64                                  */
   int n_comp;       /* k (paper m), number of sources; 1 <= k <= 8 and k <= n                      */
   int n_patches;    /* independent faces in this context (1..64)                                  */
-  int prior;        /* KCG_PRIOR_LAPLACIAN (only value supported in this build)                    */
-  int layout;       /* KCG_LAYOUT_ROW_MAJOR (only value supported in this build)                   */
-  int precond;      /* KCG_PRECOND_NONE (the paper's CG) -- only value in this build        */
+  int prior;        /* KCG_PRIOR_LAPLACIAN: Q0 = kappa2 I + L (configs); KCG_PRIOR_D2: Q0 = D^2 +   */
+                    /* kappa2 I (the paper's phi D^2; n_comp <= 4, no row slabs)        */
+  int layout;       /* KCG_LAYOUT_ROW_MAJOR (y*side + x) or KCG_LAYOUT_NESTED (HEALPix NESTED      */
+                    /* within the face; Y, mu, hits, apply/rhs arguments; no row slabs)            */
+  int precond;      /* KCG_PRECOND_NONE (the paper's CG) or KCG_PRECOND_BLOCK_JACOBI (pixel */
+                    /* k x k blocks of G, reading R10; n_comp <= 7)                                 */
   int host_staging; /* 1: workspace also holds Y / mu staging for the *_host entry points          */
   int history_cap;  /* per-iteration max relative residual recorded on device (0 = off)            */
 } kcg_desc;

@@ -44,7 +44,9 @@ struct Layout {
 };
 
 int tiles_x(int side, int K) { return (side + KCG_TX - 1) / KCG_TX; }
-int tiles_y(int rows, int K) { return (rows + kcg::cg_tile_y(K) - 1) / kcg::cg_tile_y(K); }
+int tiles_y(int rows, int K, bool d2 = false) {
+  return (rows + kcg::tile_y_of(K, d2) - 1) / kcg::tile_y_of(K, d2);
+}
 
 // One rank's layout: `rows` local rows (side / nranks), r/p buffers with `ghost` ghost rows.
 Layout layout_of(const kcg_desc* d, int nranks) {
@@ -56,8 +58,9 @@ Layout layout_of(const kcg_desc* d, int nranks) {
   const size_t N = (size_t)rows * side;
   const size_t P = d->n_patches, n = d->n_freq, k = d->n_comp;
   L.vec_doubles = P * k * (size_t)pitch * (rows + 2 * ghost);
-  const size_t tk = (size_t)tiles_x(side, (int)k) * tiles_y(rows, (int)k);
-  const size_t ts = (size_t)tiles_x(side, 1) * tiles_y(rows, 1);
+  const bool d2 = d->prior == KCG_PRIOR_D2;
+  const size_t tk = (size_t)tiles_x(side, (int)k) * tiles_y(rows, (int)k, d2);
+  const size_t ts = (size_t)tiles_x(side, 1) * tiles_y(rows, 1, d2);
   L.partial_doubles = 2 * std::max(P * tk, P * k * ts) * 3;  // [2 parities][systems][tiles][<= 3]
   size_t off = 0;
   auto take = [&](size_t bytes) { size_t o = off; off += align_up(bytes); return o; };
@@ -194,7 +197,11 @@ bool desc_ok(const kcg_desc* d, std::string* why) {
 }
 
 bool config_ok(const kcg_desc* d, std::string* why) {
-  if (d->prior != KCG_PRIOR_LAPLACIAN) { *why = "only KCG_PRIOR_LAPLACIAN is built"; return false; }
+  if (d->prior != KCG_PRIOR_LAPLACIAN && d->prior != KCG_PRIOR_D2) { *why = "unknown prior"; return false; }
+  if (d->prior == KCG_PRIOR_D2 && d->n_comp > 4) {
+    *why = "KCG_PRIOR_D2 is built for n_comp <= 4 (halo-4 boxes in shared memory)";
+    return false;
+  }
   if (d->layout != KCG_LAYOUT_ROW_MAJOR && d->layout != KCG_LAYOUT_NESTED) { *why = "unknown layout"; return false; }
   if (d->precond != KCG_PRECOND_NONE && d->precond != KCG_PRECOND_BLOCK_JACOBI) { *why = "unknown precond"; return false; }
   if (d->precond == KCG_PRECOND_BLOCK_JACOBI && d->n_comp > 7) {
@@ -276,14 +283,15 @@ void small_inverse(int k, const double* A, double* Ainv) {
     for (int j = 0; j < k; ++j) Ainv[i * k + j] = T[i * 2 * k + k + j];
 }
 
-// Pixel-block Jacobi blocks for hits = 1 (reading R10): Kinv_d = (M + (kappa2 + d) diag(tau))^{-1},
-// d = 2, 3, 4, stored compactly (K x K each) in sp.Kinv.
-void set_block_jacobi(int K, const double* M, const double* tau, double kappa2, SysParams* sp) {
+// Pixel-block Jacobi blocks for hits = 1 (reading R10): Kinv_d = (M + diag(Q0)_d diag(tau))^{-1} for
+// degree d = 2, 3, 4, with diag(Q0)_d = kappa2 + d (Laplacian) or kappa2 + d^2 + d (D^2), stored
+// compactly (K x K each) in sp.Kinv.
+void set_block_jacobi(int K, const double* M, const double* tau, double kappa2, SysParams* sp, bool d2) {
   std::vector<double> A((size_t)K * K), Ai((size_t)K * K);
   double* out = &sp->Kinv[0][0];
   for (int d = 2; d <= 4; ++d) {
     for (int i = 0; i < K; ++i)
-      for (int j = 0; j < K; ++j) A[i * K + j] = M[i * K + j] + (i == j ? (kappa2 + d) * tau[i] : 0.0);
+      for (int j = 0; j < K; ++j) A[i * K + j] = M[i * K + j] + (i == j ? (kappa2 + (d2 ? d * d + d : d)) * tau[i] : 0.0);
     small_inverse(K, A.data(), Ai.data());
     for (int e = 0; e < K * K; ++e) out[(d - 2) * K * K + e] = Ai[e];
   }
@@ -325,10 +333,10 @@ PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
   return fn;
 }
 
-bool encode_map(CUtensorMap* m, double* base, int side, int buf_rows, int pitch, size_t planes, int K,
+bool encode_map(CUtensorMap* m, double* base, int side, int buf_rows, int pitch, size_t planes, int K, bool d2,
                 std::string* why) {
-  const int bx = KCG_TX + 2 * KCG_HALO;
-  const int by = kcg::cg_tile_y(K) + 2 * KCG_HALO;
+  const int bx = KCG_TX + 2 * kcg::halo_of(d2);
+  const int by = kcg::tile_y_of(K, d2) + 2 * kcg::halo_of(d2);
   auto enc = get_encode();
   if (!enc) { *why = "cuTensorMapEncodeTiled unavailable"; return false; }
   cuuint64_t dims[3] = {(cuuint64_t)side, (cuuint64_t)buf_rows, (cuuint64_t)planes};
@@ -348,12 +356,12 @@ bool encode_map(CUtensorMap* m, double* base, int side, int buf_rows, int pitch,
 }
 
 // TMA descriptor of the solution buffer x [planes][side][side] with box {64, TY(K), K} (CTA kernel).
-bool encode_xmap(CUtensorMap* m, double* base, int side, int rows, size_t planes, int K, std::string* why) {
+bool encode_xmap(CUtensorMap* m, double* base, int side, int rows, size_t planes, int K, bool d2, std::string* why) {
   auto enc = get_encode();
   if (!enc) { *why = "cuTensorMapEncodeTiled unavailable"; return false; }
   cuuint64_t dims[3] = {(cuuint64_t)side, (cuuint64_t)rows, (cuuint64_t)planes};
   cuuint64_t strides[2] = {(cuuint64_t)side * 8, (cuuint64_t)side * rows * 8};
-  cuuint32_t box[3] = {(cuuint32_t)KCG_TX, (cuuint32_t)kcg::cg_tile_y(K), (cuuint32_t)K};
+  cuuint32_t box[3] = {(cuuint32_t)KCG_TX, (cuuint32_t)kcg::tile_y_of(K, d2), (cuuint32_t)K};
   cuuint32_t es[3] = {1, 1, 1};
   CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, base, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
                    CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
@@ -386,7 +394,8 @@ kcg_status cuda_fail(kcg_ctx* c, cudaError_t e, const char* what) {
 enum Route { ROUTE_KRON = 0, ROUTE_SYL = 1 };
 
 SlabGeom geom_of(const kcg_ctx* c, const RankState& R) {
-  return SlabGeom{c->side, c->rows, R.row0, c->pitch, c->ghost, c->ghost, c->d.layout == KCG_LAYOUT_NESTED};
+  return SlabGeom{c->side, c->rows, R.row0, c->pitch, c->ghost, c->ghost, c->d.layout == KCG_LAYOUT_NESTED,
+                  c->d.prior == KCG_PRIOR_D2};
 }
 
 // Device pointer of `field` in rank g's workspace (same layout on every rank).
@@ -510,7 +519,10 @@ kcg_status solve_impl(kcg_ctx* c, Route route, const double* Y_in, double* mu_ou
     a.x_tma = 0;
     if (c->side >= 2 && (reinterpret_cast<uintptr_t>(a.x) % 16) == 0) {
       std::string why;
-      if (!encode_xmap(&maps.x, a.x, c->side, c->rows, (size_t)P * k, Kk, &why)) { c->err = why; return KCG_E_CUDA; }
+      if (!encode_xmap(&maps.x, a.x, c->side, c->rows, (size_t)P * k, Kk, c->d.prior == KCG_PRIOR_D2, &why)) {
+        c->err = why;
+        return KCG_E_CUDA;
+      }
       a.x_tma = 1;
     }
     Lx.m[j] = maps;
@@ -522,7 +534,7 @@ kcg_status solve_impl(kcg_ctx* c, Route route, const double* Y_in, double* mu_ou
     Lx.ctas = kron ? c->grid_kron : c->grid_syl;
     CK(kcg::launch_cg_slab(Kk, prec, s, Lx, kron ? c->smem_kron : c->smem_syl), "cg slab kernel");
   } else {
-    CK(kcg::launch_cg(Kk, prec, s, Lx.a[0], Lx.m[0], kron ? c->grid_kron : c->grid_syl,
+    CK(kcg::launch_cg(Kk, prec, c->d.prior == KCG_PRIOR_D2, s, Lx.a[0], Lx.m[0], kron ? c->grid_kron : c->grid_syl,
                       kron ? c->smem_kron : c->smem_syl),
        "cg kernel");
   }
@@ -652,6 +664,7 @@ kcg_status create_impl(const kcg_desc* d, const kcg_slab* sl, const double* A_ho
   if (!config_ok(d, &why)) return fail(KCG_E_CONFIG, why);
   const int G = sl ? sl->nranks : 1;
   if (!slab_ok(d, G, &why)) return fail(KCG_E_SHAPE, why);
+  if (sl && d->prior == KCG_PRIOR_D2) return fail(KCG_E_CONFIG, "row slabs are built for KCG_PRIOR_LAPLACIAN");
   if (sl && d->layout == KCG_LAYOUT_NESTED)
     return fail(KCG_E_CONFIG, "row slabs need KCG_LAYOUT_ROW_MAJOR (a NESTED face is not split into row slabs)");
   if (sl && (sl->rank0 < 0 || sl->nlocal < 1 || sl->rank0 + sl->nlocal > G || (sl->nlocal != 1 && sl->nlocal != G)))
@@ -668,6 +681,7 @@ kcg_status create_impl(const kcg_desc* d, const kcg_slab* sl, const double* A_ho
   for (int i = 0; i < P; ++i)
     if (!(kappa2_host[i] >= 0)) return fail(KCG_E_ARG, "kappa2 must be >= 0");
 
+  const bool d2 = d->prior == KCG_PRIOR_D2;
   c->slab = sl != nullptr;
   c->nranks = G;
   c->rank0 = sl ? sl->rank0 : 0;
@@ -735,7 +749,7 @@ kcg_status create_impl(const kcg_desc* d, const kcg_slab* sl, const double* A_ho
     for (int a = 0; a < k; ++a) sk.tau[a] = phi[a];
     sk.kappa2 = kappa2_host[p];
     sk.hits_plane = p;
-    set_block_jacobi(k, M.data(), phi, kappa2_host[p], &sk);
+    set_block_jacobi(k, M.data(), phi, kappa2_host[p], &sk, d2);
     for (int i = 0; i < k; ++i) {
       SysParams& sy = ps[(size_t)p * k + i];
       std::memset(&sy, 0, sizeof sy);
@@ -743,7 +757,7 @@ kcg_status create_impl(const kcg_desc* d, const kcg_slab* sl, const double* A_ho
       sy.tau[0] = 1.0;
       sy.kappa2 = kappa2_host[p];
       sy.hits_plane = p;
-      set_block_jacobi(1, sy.M, sy.tau, sy.kappa2, &sy);
+      set_block_jacobi(1, sy.M, sy.tau, sy.kappa2, &sy, d2);
     }
   }
   kcg_status st;
@@ -780,23 +794,23 @@ kcg_status create_impl(const kcg_desc* d, const kcg_slab* sl, const double* A_ho
     }
     // TMA descriptors: Kron boxes span K = k planes, Sylvester boxes one plane.
     for (int i = 0; i < 2; ++i) {
-      if (!encode_map(&R.maps_kron.r[i], R.r[i], c->side, buf_rows, c->pitch, planes, k, &why) ||
-          !encode_map(&R.maps_kron.p[i], R.p[i], c->side, buf_rows, c->pitch, planes, k, &why) ||
-          !encode_map(&R.maps_syl.r[i], R.r[i], c->side, buf_rows, c->pitch, planes, 1, &why) ||
-          !encode_map(&R.maps_syl.p[i], R.p[i], c->side, buf_rows, c->pitch, planes, 1, &why))
+      if (!encode_map(&R.maps_kron.r[i], R.r[i], c->side, buf_rows, c->pitch, planes, k, d2, &why) ||
+          !encode_map(&R.maps_kron.p[i], R.p[i], c->side, buf_rows, c->pitch, planes, k, d2, &why) ||
+          !encode_map(&R.maps_syl.r[i], R.r[i], c->side, buf_rows, c->pitch, planes, 1, d2, &why) ||
+          !encode_map(&R.maps_syl.p[i], R.p[i], c->side, buf_rows, c->pitch, planes, 1, d2, &why))
         return fail(KCG_E_CUDA, why);
     }
   }
   CKC(cudaStreamSynchronize(c->stream), "create sync");
   c->tiles_x_kron = tiles_x(c->side, k);
-  c->tiles_y_kron = tiles_y(c->rows, k);
+  c->tiles_y_kron = tiles_y(c->rows, k, d2);
   c->tiles_x_syl = tiles_x(c->side, 1);
-  c->tiles_y_syl = tiles_y(c->rows, 1);
+  c->tiles_y_syl = tiles_y(c->rows, 1, d2);
   int mg = 0;
   const bool prec = d->precond == KCG_PRECOND_BLOCK_JACOBI;
-  CKC(kcg::cg_kernel_config(k, hits_dev != nullptr, prec, c->slab, P, &mg, &c->smem_kron), "cg kernel config (kron)");
+  CKC(kcg::cg_kernel_config(k, hits_dev != nullptr, prec, c->slab, d2, P, &mg, &c->smem_kron), "cg kernel config (kron)");
   c->grid_kron = std::max(1, std::min(mg / c->nlocal, P * c->tiles_x_kron * c->tiles_y_kron));
-  CKC(kcg::cg_kernel_config(1, hits_dev != nullptr, prec, c->slab, P * k, &mg, &c->smem_syl),
+  CKC(kcg::cg_kernel_config(1, hits_dev != nullptr, prec, c->slab, d2, P * k, &mg, &c->smem_syl),
       "cg kernel config (sylvester)");
   c->grid_syl = std::max(1, std::min(mg / c->nlocal, P * k * c->tiles_x_syl * c->tiles_y_syl));
   if (mg < c->nlocal) return fail(KCG_E_CONFIG, "slab: more emulated ranks than co-resident CTAs");
@@ -890,7 +904,8 @@ kcg_status kron_cg_rhs(kcg_ctx* c, const double* Y, double* b) {
   if (!Y || !b) { c->err = "null Y or b"; return KCG_E_ARG; }
   for (int j = 0; j < c->nlocal; ++j) {
     const RankState& R = c->R[j];
-    SlabGeom g{c->side, c->rows, R.row0, c->side, 0, c->ghost, c->d.layout == KCG_LAYOUT_NESTED};  // dense b
+    SlabGeom g{c->side, c->rows, R.row0, c->side, 0, c->ghost, c->d.layout == KCG_LAYOUT_NESTED,
+               c->d.prior == KCG_PRIOR_D2};  // dense b
     double* bo = R.y_rm ? R.y_rm : b + j * (size_t)c->P * c->k * c->N;
     CK(kcg::launch_rhs(c->k, c->stream, Y + j * (size_t)c->P * c->n * c->N, R.E_kron, R.hits, bo, nullptr, nullptr,
                        c->P, c->n, g),

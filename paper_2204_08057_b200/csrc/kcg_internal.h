@@ -65,6 +65,22 @@ __host__ __device__ constexpr int cg_stage_bytes(int K) {
   return 2 * K * (cg_tile_y(K) + 2 * KCG_HALO) * (KCG_TX + 2 * KCG_HALO) * 8 + cg_xstage_bytes(K);
 }
 
+// ---- D2 prior (the paper's phi D^2 + kappa2 I, radius-2 stencil): single-pass recomputation
+// needs a 4-pixel halo.  Generic point loops (tile 64 x TY2, 256 threads), no x staging; scratch
+// boxes for D p (tile + 3-ring), D r / D u (tile + 1-ring) and p_old of the tile (X2).
+#define KCG_HALO2 4
+__host__ __device__ constexpr int d2_tile_y(int K) { return K == 1 ? 16 : 8; }
+__host__ __device__ constexpr int d2_box_w() { return KCG_TX + 2 * KCG_HALO2; }
+__host__ __device__ constexpr int d2_stage_bytes(int K) { return 2 * K * (d2_tile_y(K) + 2 * KCG_HALO2) * d2_box_w() * 8; }
+__host__ __device__ constexpr int d2_sbox_bytes(int K) { return K * (d2_tile_y(K) + 6) * d2_box_w() * 8; }
+__host__ __device__ constexpr int d2_pold_bytes(int K) { return K * d2_tile_y(K) * KCG_TX * 8; }
+__host__ __device__ constexpr int d2_ubox_bytes(int K) { return K * (d2_tile_y(K) + 4) * d2_box_w() * 8; }
+// geometry by prior
+__host__ __device__ constexpr int tile_y_of(int K, bool d2) { return d2 ? d2_tile_y(K) : cg_tile_y(K); }
+__host__ __device__ constexpr int halo_of(bool d2) { return d2 ? KCG_HALO2 : KCG_HALO; }
+__host__ __device__ constexpr int threads_of(int K, bool d2) { return d2 ? 256 : cg_threads(K); }
+__host__ __device__ constexpr int min_blocks_of(int K, bool d2) { return d2 ? 1 : cg_min_blocks(K); }
+
 // Per-system constant parameters of the operator  q_c = h sum_d M[c][d] p_d + tau_c (kappa2 p_c + (L p_c)).
 // Kronecker route: one system per patch, K = k, M = A^T T A, tau = prior scales.
 // Sylvester route: one system per (patch, column i), K = 1, M = [rho_i], tau = [1].
@@ -157,14 +173,17 @@ struct SlabGeom {
   int side, rows, row0, pitch, ghost;
   int hits_ghost;            // ghost rows of the hits planes (= ghost, except for the dense rhs output)
   int nested;                // 1: the data maps Y are in HEALPix NESTED order inside the face (reading R1)
+  int d2;                    // 1: prior Q0 = D^2 + kappa2 I (radius-2 operator)
 };
 
 // ---------------------------------------------------------------- launchers (kcg_kernels.cu)
 // All return cudaError_t of the launch.
 cudaError_t launch_rhs(int K, cudaStream_t s, const double* Y, const double* E, const double* hits,
                        double* r0, double* p0, double* x, int P, int n, const SlabGeom& g);
-cudaError_t launch_cg(int K, bool prec, cudaStream_t s, const CgArgs& a, const CgMaps& m, int grid, size_t smem);
-cudaError_t cg_kernel_config(int K, bool hits, bool prec, bool slab, int n_sys, int* max_grid, size_t* smem);
+cudaError_t launch_cg(int K, bool prec, bool d2, cudaStream_t s, const CgArgs& a, const CgMaps& m, int grid,
+                      size_t smem);
+cudaError_t cg_kernel_config(int K, bool hits, bool prec, bool slab, bool d2, int n_sys, int* max_grid,
+                             size_t* smem);
 cudaError_t launch_cg_slab(int K, bool prec, cudaStream_t s, const CgSlabLaunch& L, size_t smem);
 cudaError_t launch_apply(int K, cudaStream_t s, const SysParams* params, const double* x, double* y,
                          const double* hits, int n_sys, const SlabGeom& g, const double* xg_top,

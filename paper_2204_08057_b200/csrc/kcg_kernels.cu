@@ -24,8 +24,9 @@ int apply_tiles_per_sys(int rows, int side) {
 // RESID = false: y = G x.   RESID = true: partials[s][tile] = (||b - G x||^2, ||b||^2) over the
 // tile, with b = h Y E recomputed from the data (E = T A).  Slab geometry: `rows` local rows from
 // global face row `row0`; the halo rows beyond the slab come from xg_top / xg_bot ([planes][side],
-// the neighbours' boundary rows; nullptr or outside the face -> 0).
-template <int K, bool RESID>
+// the neighbours' boundary rows; nullptr or outside the face -> 0).  D2: Q0 = D^2 + kappa2 I, the
+// tile's x is staged with a 2-pixel halo and D x is formed on tile + 1-ring first (no slabs).
+template <int K, bool RESID, bool D2>
 __global__ void __launch_bounds__(AP_NT) apply_kernel(const SysParams* __restrict__ params,
                                                       const double* __restrict__ x, double* __restrict__ y,
                                                       const double* __restrict__ Y, const double* __restrict__ E,
@@ -34,8 +35,9 @@ __global__ void __launch_bounds__(AP_NT) apply_kernel(const SysParams* __restric
                                                       int row0, int ghost, int nested,
                                                       const double* __restrict__ xg_top,
                                                       const double* __restrict__ xg_bot) {
-  constexpr int BW = AP_TX + 2, BH = AP_TY + 2, PLANE = BW * BH;
-  extern __shared__ double xs[];  // [K][BH][BW], then E [n][K] if RESID
+  constexpr int HA = D2 ? 2 : 1;
+  constexpr int BW = AP_TX + 2 * HA, BH = AP_TY + 2 * HA, PLANE = BW * BH;
+  extern __shared__ double xs[];  // [K][BH][BW], then (D2) D x [K][BH][BW], then E [n][K] if RESID
   __shared__ double red[2][AP_NT / 32];
   const int s = blockIdx.y;
   const int tiles_x = (side + AP_TX - 1) / AP_TX;
@@ -45,7 +47,7 @@ __global__ void __launch_bounds__(AP_NT) apply_kernel(const SysParams* __restric
   const SysParams* sp = params + s;
   for (int e = threadIdx.x; e < K * PLANE; e += AP_NT) {
     const int c = e / PLANE, r = e - c * PLANE;
-    const int ly = ty0 - 1 + r / BW, gx = tx0 - 1 + r % BW, gyg = row0 + ly;
+    const int ly = ty0 - HA + r / BW, gx = tx0 - HA + r % BW, gyg = row0 + ly;
     double v = 0.0;
     if (gx >= 0 && gx < side && gyg >= 0 && gyg < side) {
       const size_t plane = (size_t)(s * K + c);
@@ -55,10 +57,25 @@ __global__ void __launch_bounds__(AP_NT) apply_kernel(const SysParams* __restric
     }
     xs[e] = v;
   }
-  double* Es = xs + K * PLANE;
+  double* Ds = xs + K * PLANE;                  // D2: D x on tile + 1-ring (zero outside the face)
+  double* Es = xs + (D2 ? 2 : 1) * K * PLANE;
   if (RESID)
     for (int e = threadIdx.x; e < n * K; e += AP_NT) Es[e] = E[(size_t)s * n * K + e];
   __syncthreads();
+  auto degf = [&](int gy, int gx) { return 4 - (gy == 0) - (gy == side - 1) - (gx == 0) - (gx == side - 1); };
+  if (D2) {
+    for (int e = threadIdx.x; e < K * PLANE; e += AP_NT) {
+      const int c = e / PLANE, r = e - c * PLANE, by = r / BW, bx = r % BW;
+      const int gy = row0 + ty0 - HA + by, gx = tx0 - HA + bx;
+      double v = 0.0;
+      if (by >= 1 && by < BH - 1 && bx >= 1 && bx < BW - 1 && gy >= 0 && gy < side && gx >= 0 && gx < side) {
+        const double* xl = xs + e;
+        v = ((xl[-BW] + xl[BW]) + (xl[-1] + xl[1])) - degf(gy, gx) * xl[0];
+      }
+      Ds[e] = v;
+    }
+    __syncthreads();
+  }
   double M[K * K], tau[K];
 #pragma unroll
   for (int e = 0; e < K * K; ++e) M[e] = sp->M[e];
@@ -71,8 +88,8 @@ __global__ void __launch_bounds__(AP_NT) apply_kernel(const SysParams* __restric
   for (int pt = threadIdx.x; pt < AP_TY * AP_TX; pt += AP_NT) {
     const int ly = ty0 + pt / AP_TX, gx = tx0 + pt % AP_TX, gyg = row0 + ly;
     if (ly >= rows || gx >= side) continue;
-    const int o = (pt / AP_TX + 1) * BW + pt % AP_TX + 1;
-    const double deg = 4.0 - (gyg == 0) - (gyg == side - 1) - (gx == 0) - (gx == side - 1);
+    const int o = (pt / AP_TX + HA) * BW + pt % AP_TX + HA;
+    const int deg = degf(gyg, gx);
     const double h = hp ? hp[(size_t)ly * side + gx] : 1.0;
     double xc[K];
 #pragma unroll
@@ -90,12 +107,18 @@ __global__ void __launch_bounds__(AP_NT) apply_kernel(const SysParams* __restric
     }
 #pragma unroll
     for (int c = 0; c < K; ++c) {
-      const double* xl = xs + c * PLANE + o;
-      const double nb = (xl[-BW] + xl[BW]) + (xl[-1] + xl[1]);
+      double q0;  // (Q0 x)_c without the kappa2 term: (L x) or (D^2 x)
+      if (D2) {
+        const double* dl = Ds + c * PLANE + o;
+        q0 = ((dl[-BW] + dl[BW]) + (dl[-1] + dl[1])) - deg * dl[0];
+      } else {
+        const double* xl = xs + c * PLANE + o;
+        q0 = deg * xl[0] - ((xl[-BW] + xl[BW]) + (xl[-1] + xl[1]));
+      }
       double mix = 0.0;
 #pragma unroll
       for (int d = 0; d < K; ++d) mix = fma(M[c * K + d], xc[d], mix);
-      const double q = fma(h, mix, tau[c] * fma(kappa2 + deg, xc[c], -nb));
+      const double q = fma(h, mix, tau[c] * fma(kappa2, xc[c], q0));
       if (RESID) {
         const double b = h * bq[c];
         const double rres = b - q;
@@ -294,13 +317,15 @@ cudaError_t launch_rhs(int K, cudaStream_t s, const double* Y, const double* E, 
   return cudaGetLastError();
 }
 
-cudaError_t cg_kernel_config(int K, bool hits, bool prec, bool slab, int n_sys, int* max_grid, size_t* smem) {
-  KCG_DISPATCH(K, return CgEntry<KK>::config(hits, prec, slab, n_sys, max_grid, smem));
+cudaError_t cg_kernel_config(int K, bool hits, bool prec, bool slab, bool d2, int n_sys, int* max_grid,
+                             size_t* smem) {
+  KCG_DISPATCH(K, return CgEntry<KK>::config(hits, prec, slab, d2, n_sys, max_grid, smem));
   return cudaErrorInvalidValue;
 }
 
-cudaError_t launch_cg(int K, bool prec, cudaStream_t s, const CgArgs& a, const CgMaps& m, int grid, size_t smem) {
-  KCG_DISPATCH(K, return CgEntry<KK>::launch(prec, s, a, m, grid, smem));
+cudaError_t launch_cg(int K, bool prec, bool d2, cudaStream_t s, const CgArgs& a, const CgMaps& m, int grid,
+                      size_t smem) {
+  KCG_DISPATCH(K, return CgEntry<KK>::launch(prec, d2, s, a, m, grid, smem));
   return cudaErrorInvalidValue;
 }
 
@@ -309,24 +334,27 @@ cudaError_t launch_cg_slab(int K, bool prec, cudaStream_t s, const CgSlabLaunch&
   return cudaErrorInvalidValue;
 }
 
-template <int K, bool R>
+template <int K, bool R, bool D2>
 static cudaError_t apply_t(cudaStream_t s, const SysParams* params, const double* x, double* y, const double* Y,
                            const double* E, const double* hits, double* partials, int n_sys, int n, const SlabGeom& g,
                            const double* xg_top, const double* xg_bot) {
-  const size_t sm = ((size_t)K * (AP_TX + 2) * (AP_TY + 2) + (R ? (size_t)n * K : 0)) * sizeof(double);
-  cudaError_t e = cudaFuncSetAttribute(apply_kernel<K, R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  constexpr int HA = D2 ? 2 : 1;
+  const size_t plane = (size_t)(AP_TX + 2 * HA) * (AP_TY + 2 * HA);
+  const size_t sm = ((D2 ? 2 : 1) * (size_t)K * plane + (R ? (size_t)n * K : 0)) * sizeof(double);
+  cudaError_t e = cudaFuncSetAttribute(apply_kernel<K, R, D2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
   if (e != cudaSuccess) return e;
   dim3 gr(apply_tiles_per_sys(g.rows, g.side), n_sys);
-  apply_kernel<K, R><<<gr, AP_NT, sm, s>>>(params, x, y, Y, E, hits, partials, n, g.side, g.rows, g.row0,
-                                           g.hits_ghost, g.nested, xg_top, xg_bot);
+  apply_kernel<K, R, D2><<<gr, AP_NT, sm, s>>>(params, x, y, Y, E, hits, partials, n, g.side, g.rows, g.row0,
+                                               g.hits_ghost, g.nested, xg_top, xg_bot);
   return cudaGetLastError();
 }
 
 cudaError_t launch_apply(int K, cudaStream_t s, const SysParams* params, const double* x, double* y,
                          const double* hits, int n_sys, const SlabGeom& g, const double* xg_top,
                          const double* xg_bot) {
-  KCG_DISPATCH(K, return (apply_t<KK, false>(s, params, x, y, nullptr, nullptr, hits, nullptr, n_sys, 0, g, xg_top,
-                                             xg_bot)));
+  if (g.d2) { KCG_DISPATCH(K, return (apply_t<KK, false, true>(s, params, x, y, nullptr, nullptr, hits, nullptr, n_sys, 0, g, xg_top, xg_bot))); }
+  KCG_DISPATCH(K, return (apply_t<KK, false, false>(s, params, x, y, nullptr, nullptr, hits, nullptr, n_sys, 0, g,
+                                                    xg_top, xg_bot)));
   return cudaErrorInvalidValue;
 }
 
@@ -334,7 +362,8 @@ cudaError_t launch_resid(int K, cudaStream_t s, const SysParams* params, const d
                          const double* E, const double* hits, double* partials, double* out, int n_sys, int n,
                          const SlabGeom& g, const double* xg_top, const double* xg_bot) {
   cudaError_t e = cudaSuccess;
-  KCG_DISPATCH(K, e = (apply_t<KK, true>(s, params, x, nullptr, Y, E, hits, partials, n_sys, n, g, xg_top, xg_bot)));
+  if (g.d2) { KCG_DISPATCH(K, e = (apply_t<KK, true, true>(s, params, x, nullptr, Y, E, hits, partials, n_sys, n, g, xg_top, xg_bot))); }
+  else { KCG_DISPATCH(K, e = (apply_t<KK, true, false>(s, params, x, nullptr, Y, E, hits, partials, n_sys, n, g, xg_top, xg_bot))); }
   if (e != cudaSuccess) return e;
   reduce_pairs_kernel<<<n_sys, 256, 0, s>>>(partials, out, apply_tiles_per_sys(g.rows, g.side));
   return cudaGetLastError();

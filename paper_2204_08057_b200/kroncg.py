@@ -119,12 +119,14 @@ class KronCG:
     Parameters are host numpy arrays in the C-ABI layouts (A [P][n][k], noise_prec [P][n],
     prior_scale [P][k], kappa2 [P]); hits an optional torch CUDA tensor [P][side][side].
     precond: "none" (the paper's CG) or "block_jacobi" (pixel-block Jacobi, reading R10).
+    prior: "laplacian" (Q0 = kappa2 I + L, the configs) or "d2" (Q0 = D^2 + kappa2 I, the paper's).
     layout: "row" (pixel y*side + x) or "nested" (HEALPix NESTED inside the face, reading R1): Y, mu,
     hits and the apply / rhs arguments keep their [..][side][side] shapes, read as flat [N] vectors.
     """
 
     def __init__(self, level, A, noise_prec, prior_scale, kappa2, hits=None, device=None,
-                 host_staging=False, history_cap=0, stream=None, precond="none", layout="row"):
+                 host_staging=False, history_cap=0, stream=None, precond="none", layout="row",
+                 prior="laplacian"):
         import torch
         A = np.ascontiguousarray(np.asarray(A, dtype=np.float64))
         if A.ndim == 2:
@@ -142,7 +144,8 @@ class KronCG:
         self.shape_mu = (P, k, self.side, self.side)
         pc = {"none": KCG_PRECOND_NONE, "block_jacobi": KCG_PRECOND_BLOCK_JACOBI}[precond]
         lay = {"row": KCG_LAYOUT_ROW_MAJOR, "nested": KCG_LAYOUT_NESTED}[layout]
-        self.desc = kcg_desc(level, n, k, P, KCG_PRIOR_LAPLACIAN, lay,
+        pr = {"laplacian": KCG_PRIOR_LAPLACIAN, "d2": KCG_PRIOR_D2}[prior]
+        self.desc = kcg_desc(level, n, k, P, pr, lay,
                              pc, int(bool(host_staging)), int(history_cap))
         ws = kron_cg_workspace_size(C.byref(self.desc))
         if ws == 0:

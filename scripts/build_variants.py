@@ -6,7 +6,10 @@ sys.path.insert(0, ROOT)
 from paper_2204_08057_b200 import build
 
 VARIANTS = {
-    "trace": ["KCG_TRACE=1"],
+    "a16x256": [],
+    "b8x256x2": ["KCG_TY4=8", "KCG_MINB4=2"],
+    "c8x128x2": ["KCG_TY4=8", "KCG_NT4=128", "KCG_MINB4=2"],
+    "d16x128": ["KCG_NT4=128"],
 }
 names = sys.argv[1:] or list(VARIANTS)
 out = os.path.join(ROOT, "paper_2204_08057_b200", "lib", "variants")

@@ -20,6 +20,7 @@ def make_ctx(problems, **kw):
     from paper_2204_08057_b200.kroncg import KronCG
     st = stack(problems)
     hits = torch.from_numpy(st["hits"]).cuda() if st["hits"] is not None else None
+    kw.setdefault("prior", problems[0].prior)
     ctx = KronCG(problems[0].level, st["A"], st["noise_prec"], st["tau"], st["kappa2"],
                  hits=hits, **kw)
     Y = torch.from_numpy(st["Y"]).cuda()
