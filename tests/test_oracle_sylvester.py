@@ -87,3 +87,61 @@ def test_sylvester_medium_matches_dct():
     p = make_config("medium")[0]
     res = sylvester.problem_solve(p, tol=1e-10)
     assert rel(res.x, exact.problem_dct_exact(p)) <= 1e-8
+
+
+# ----------------------------------------------------------------------- block-Lanczos (NEXT-1)
+def test_lanczos_tiny_medium_match_exact():
+    from oracle import lanczos
+    for name in ("tiny", "medium"):
+        p = make_config(name)[0]
+        r = lanczos.problem_solve(p, tol=1e-10)
+        assert r.converged
+        assert rel(r.x, exact.problem_dct_exact(p)) <= 1e-8
+
+
+def test_lanczos_relation_orthonormality_and_galerkin():
+    """Early steps (orthogonality intact): AA V_j = V_{j+1} T_j (Lanczos relation), V^T N V = I,
+    and the Galerkin solution satisfies T Z + Z S^ = E_1 B_0 (Eq.(Sylv-small))."""
+    from oracle import grid, lanczos, model as mdl
+    p = make_patch(4, 9, 3, seed=21, tau="loguniform", hits="random")
+    r = lanczos.problem_solve(p, tol=1e-30, max_iter=4, keep_basis=True)
+    m, h = p.k, p.hits.reshape(-1)
+    Vs = np.hstack(r.V)                                   # N x 4m
+    assert np.abs(Vs.T @ (h[:, None] * Vs) - np.eye(4 * m)).max() <= 1e-10
+    Q0 = mdl.prior_Q0(p.level, p.kappa2)
+    AV = (Q0 @ Vs[:, :3 * m]) / h[:, None]
+    T = np.zeros((4 * m, 3 * m))
+    for a in range(3):
+        T[a * m:(a + 1) * m, a * m:(a + 1) * m] = r.H[a]
+        T[(a + 1) * m:(a + 2) * m, a * m:(a + 1) * m] = r.B[a + 1]
+        if a + 1 < 3:
+            T[a * m:(a + 1) * m, (a + 1) * m:(a + 2) * m] = r.B[a + 1].T
+    assert np.abs(AV - Vs @ T).max() <= 1e-9 * np.abs(AV).max()
+
+
+def test_lanczos_residual_estimate_is_the_u_basis_residual():
+    """Paper's gamma (reading R26) = ||(AA M + M S^ - Y^) U||_N,F^2 for the Galerkin
+    iterate M_j = V Z (checked while the basis is still orthonormal)."""
+    from oracle import lanczos, model as mdl
+    from oracle.sylvester import small_factor
+    p = make_patch(4, 9, 3, seed=22, tau="loguniform")
+    for steps in (2, 4):
+        r = lanczos.problem_solve(p, tol=1e-30, max_iter=steps, keep_basis=True)
+        m, N = p.k, p.N
+        Mk, P, rho, W = small_factor(p.A, p.noise_prec, p.tau)
+        U = P @ W
+        Yhat = (p.Y.reshape(p.n, N).T @ np.diag(p.noise_prec) @ p.A) @ np.linalg.inv(P)
+        M = r.x.reshape(m, N).T
+        Q0 = mdl.prior_Q0(p.level, p.kappa2)
+        R = Q0 @ M + M @ (Mk @ np.linalg.inv(P)) - Yhat
+        est = r.gamma_history[-1] * np.linalg.norm(r.B[0])
+        assert np.isclose(np.linalg.norm(R @ U), est, rtol=1e-6), (np.linalg.norm(R @ U), est)
+
+
+def test_lanczos_k1_is_plain_lanczos_on_the_shifted_system():
+    """m = 1: S^ = rho (scalar); the solution of (N^{-1} Q0 + rho) x = y^ (dense solve)."""
+    from oracle import lanczos
+    p = make_patch(3, 4, 1, seed=1, tau="given", tau_values=[2.0])
+    r = lanczos.problem_solve(p, tol=1e-12)
+    G, b = model.problem_system(p)
+    assert rel(r.x, exact.dense_solve(G, b)) <= 1e-9
