@@ -112,7 +112,7 @@ def solve(level, A, noise_prec, tau, kappa2, Y, hits=None, prior="laplacian", to
     Z = Qm @ F @ Uinv
     # rerun Lanczos with the stored coefficients to assemble M = sum_j V_j G_j
     Mx = np.zeros((N, m))
-    V = Yhat @ np.linalg.inv(B0)
+    V = np.linalg.solve(B0.T, Yhat.T).T                         # Y^ B_0^{-1}, as n_qr formed V_1 (R30)
     V_old = np.zeros_like(V)
     for j in range(1, i + 1):
         Mx += V @ Z[(j - 1) * m:j * m, :]

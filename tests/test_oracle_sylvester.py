@@ -145,3 +145,19 @@ def test_lanczos_k1_is_plain_lanczos_on_the_shifted_system():
     r = lanczos.problem_solve(p, tol=1e-12)
     G, b = model.problem_system(p)
     assert rel(r.x, exact.dense_solve(G, b)) <= 1e-9
+
+
+@pytest.mark.parametrize("level,seed", [(5, 70), (6, 70)])
+def test_lanczos_with_hits_matches_the_direct_solve(level, seed):
+    """Non-uniform hits: N_h^{-1} Q0 is only N-symmetric (Lemma 1) and the basis loses
+    orthogonality early (max |V^T N V - I| ~ 0.2 at L = 6).  The second Lanczos pass must then
+    rebuild the first pass's blocks exactly (Alg. SylvSolver, reading R30): a replay
+    whose V_1 = Y^ B_0^{-1} is rounded differently from the first pass's drifts to ~1e-6."""
+    import scipy.sparse.linalg as ssl
+    from oracle import lanczos
+    p = make_patch(level, 9, 3, seed=seed, tau="loguniform", hits="random")
+    r = lanczos.problem_solve(p, tol=1e-10)
+    G, b = model.problem_system(p)
+    ref = ssl.spsolve(G.tocsc(), b)
+    assert r.converged
+    assert rel(r.x, ref) <= 5e-9
