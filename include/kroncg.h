@@ -90,6 +90,13 @@ typedef struct {
                     /* k x k blocks of G, reading R10; n_comp <= 7)                                 */
   int host_staging; /* 1: workspace also holds Y / mu staging for the *_host entry points          */
   int history_cap;  /* per-iteration max relative residual recorded on device (0 = off)            */
+  int lanczos_cap;  /* block-Lanczos route (sylvester_lanczos_solve): 0 = not provisioned; else the   */
+                    /* most Lanczos steps a solve may take (coefficients H_i, B_i, eliminations kept  */
+                    /* on device: ~(5k^2 + k^3) * 8 bytes per step and patch); KCG_PRIOR_LAPLACIAN,    */
+                    /* no row slabs                                                                    */
+  int lanczos_store;/* 1: keep the whole Lanczos basis V_1..V_cap in HBM (P*k*N*8*(lanczos_cap + 1)     */
+                    /* bytes) and assemble M in one streaming pass; 0: the paper's memory-lean second  */
+                    /* Lanczos pass, four block slots                                      */
 } kcg_desc;
 
 /* Solve report, filled on return (host memory). */
@@ -132,6 +139,23 @@ KCG_API kcg_status kron_cg_solve(kcg_ctx* ctx, const double* Y_dev, double* mu_d
  * ||rt_i|| <= tol ||ft_i|| (reading R15).  report->iterations_per is [P*k].                   */
 KCG_API kcg_status sylvester_solve(kcg_ctx* ctx, const double* Y_dev, double* mu_dev, double tol,
                            int max_iter, kcg_report* report);
+
+/* Block-Lanczos Sylvester solver -- the paper's Alg. SylvSolver: block Lanczos on
+ * N_h^{-1} Q0 in the N_h inner product (Alg. Lanczos, Lemma 1) started from
+ * Y^ = Y T A P^{-1} = V_1 B_0, Galerkin projection T_i Z + Z S^ = E_1 B_0 (Eq.(Sylv-small)) with
+ * S^ = M P^{-1} = U R U^{-1} (Lemma 2), stop after the first step i with sqrt(gamma_i) <= tol ||B_0||_F
+ * (gamma = the paper's residual estimate), Z from Eq.(soln-constr) P:L484-486 and
+ * M = sum_j V_j G_j (Eq.(soln-darstellung)) written to mu_dev [P][k][N].  One context may run it
+ * only if desc.lanczos_cap > 0 (KCG_E_CONFIG otherwise); max_iter is capped at lanczos_cap.
+ * report->iterations_per is [P] (Lanczos steps per patch), report->rel_residual the max over
+ * patches of sqrt(gamma)/||B_0||_F, report->rel_residual_true ||b - G mu||/||b|| as for CG.
+ * A rank-deficient block (the Krylov space stops growing before convergence, e.g. 4^level < 2k)
+ * gives KCG_E_BREAKDOWN; an exhausted space (W = V H to rounding) is an exact projection and
+ * converges.                                                                                    */
+KCG_API kcg_status sylvester_lanczos_solve(kcg_ctx* ctx, const double* Y_dev, double* mu_dev, double tol,
+                                   int max_iter, kcg_report* report);
+KCG_API kcg_status sylvester_lanczos_solve_host(kcg_ctx* ctx, const double* Y_host, double* mu_host, double tol,
+                                        int max_iter, kcg_report* report);
 
 /* Same as above with HOST buffers: copies Y in and mu out through the context's staging buffers
  * (desc.host_staging = 1), copies included in report->wall_time_s.                            */

@@ -39,7 +39,9 @@ const unsigned long long kPostTag = 1ull << 31;  // tags of the post-CG rendezvo
 // Per-rank workspace carving.
 struct Layout {
   size_t r0, r1, p0, p1, partials, state, history, sync, group, resid_partials, resid_out, params_kron, params_syl,
-      E_kron, E_syl, W, Y_stage, mu_stage, trace, slots, flags, xg_top, xg_bot, rslots, x_rm, y_rm, hits_rm, total;
+      E_kron, E_syl, W, Y_stage, mu_stage, trace, slots, flags, xg_top, xg_bot, rslots, x_rm, y_rm, hits_rm,
+      lz_V, lz_part, lz_st, lz_H, lz_R, lz_Ri, lz_Sinv, lz_g, lz_Z, lz_prm, E_lz, total;
+  int lz_slots;
   size_t vec_doubles, partial_doubles;
 };
 
@@ -96,6 +98,21 @@ Layout layout_of(const kcg_desc* d, int nranks) {
     L.y_rm = take(P * k * N * 8);
     L.hits_rm = take(P * N * 8);
   }
+  if (d->lanczos_cap > 0 && nranks == 1) {  // block-Lanczos route (Alg. SylvSolver)
+    const size_t cap = (size_t)d->lanczos_cap, kk = k * k;
+    L.lz_slots = d->lanczos_store ? d->lanczos_cap + 1 : 4;
+    L.lz_V = take((size_t)L.lz_slots * P * k * pitch * rows * 8);
+    L.lz_part = take(P * (size_t)KCG_LZ_GRID_MAX * kcg::lz_npart((int)k) * 8);
+    L.lz_st = take(P * sizeof(kcg::LzState));
+    L.lz_H = take(P * cap * kk * 8);
+    L.lz_R = take(P * (cap + 1) * kk * 8);
+    L.lz_Ri = take(P * (cap + 1) * kk * 8);
+    L.lz_Sinv = take(P * cap * k * kk * 8);
+    L.lz_g = take(P * cap * k * k * 8);
+    L.lz_Z = take(P * cap * kk * 8);
+    L.lz_prm = take(P * sizeof(kcg::LzFace));
+    L.E_lz = take(P * n * k * 8);
+  }
   L.total = off;
   return L;
 }
@@ -117,6 +134,12 @@ struct RankState {
   unsigned long long* flags = nullptr;
   const double* hits = nullptr;
   CgMaps maps_kron, maps_syl;
+  // block-Lanczos route
+  double *lz_V = nullptr, *lz_part = nullptr, *lz_H = nullptr, *lz_R = nullptr, *lz_Ri = nullptr,
+         *lz_Sinv = nullptr, *lz_g = nullptr, *lz_Z = nullptr, *E_lz = nullptr;
+  kcg::LzState* lz_st = nullptr;
+  kcg::LzFace* lz_prm = nullptr;
+  CUtensorMap lz_map;
 };
 
 RankState carve(char* ws, const Layout& L, int rank, int rows, bool staging, bool nested) {
@@ -150,6 +173,19 @@ RankState carve(char* ws, const Layout& L, int rank, int rows, bool staging, boo
   R.xg_top = reinterpret_cast<double*>(ws + L.xg_top);
   R.xg_bot = reinterpret_cast<double*>(ws + L.xg_bot);
   R.rslots = reinterpret_cast<double*>(ws + L.rslots);
+  if (L.lz_slots > 0) {
+    R.lz_V = reinterpret_cast<double*>(ws + L.lz_V);
+    R.lz_part = reinterpret_cast<double*>(ws + L.lz_part);
+    R.lz_st = reinterpret_cast<kcg::LzState*>(ws + L.lz_st);
+    R.lz_H = reinterpret_cast<double*>(ws + L.lz_H);
+    R.lz_R = reinterpret_cast<double*>(ws + L.lz_R);
+    R.lz_Ri = reinterpret_cast<double*>(ws + L.lz_Ri);
+    R.lz_Sinv = reinterpret_cast<double*>(ws + L.lz_Sinv);
+    R.lz_g = reinterpret_cast<double*>(ws + L.lz_g);
+    R.lz_Z = reinterpret_cast<double*>(ws + L.lz_Z);
+    R.lz_prm = reinterpret_cast<kcg::LzFace*>(ws + L.lz_prm);
+    R.E_lz = reinterpret_cast<double*>(ws + L.E_lz);
+  }
   if (nested) {
     R.x_rm = reinterpret_cast<double*>(ws + L.x_rm);
     R.y_rm = reinterpret_cast<double*>(ws + L.y_rm);
@@ -175,6 +211,9 @@ struct kcg_ctx {
   int tiles_x_kron = 0, tiles_y_kron = 0, tiles_x_syl = 0, tiles_y_syl = 0;
   int grid_kron = 0, grid_syl = 0;     // CTAs (per rank in slab mode)
   size_t smem_kron = 0, smem_syl = 0;
+  int grid_lz = 0, tiles_x_lz = 0, tiles_y_lz = 0;  // block-Lanczos kernel
+  size_t smem_lz = 0;
+  std::vector<kcg::LzState> lz_host;
   unsigned long long solve_id = 0;     // cross-rank operations so far (identical on every rank)
   cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
   std::vector<SysState> st_host;
@@ -193,6 +232,8 @@ bool desc_ok(const kcg_desc* d, std::string* why) {
   if (d->n_comp > d->n_freq) { *why = "n_comp > n_freq (A cannot have full column rank)"; return false; }
   if (d->n_patches < 1 || d->n_patches > 64) { *why = "n_patches outside [1,64]"; return false; }
   if (d->history_cap < 0) { *why = "history_cap < 0"; return false; }
+  if (d->lanczos_cap < 0 || d->lanczos_cap > 1000000) { *why = "lanczos_cap outside [0, 1e6]"; return false; }
+  if (d->lanczos_store != 0 && d->lanczos_store != 1) { *why = "lanczos_store must be 0 or 1"; return false; }
   return true;
 }
 
@@ -203,6 +244,10 @@ bool config_ok(const kcg_desc* d, std::string* why) {
     return false;
   }
   if (d->layout != KCG_LAYOUT_ROW_MAJOR && d->layout != KCG_LAYOUT_NESTED) { *why = "unknown layout"; return false; }
+  if (d->lanczos_cap > 0 && d->prior != KCG_PRIOR_LAPLACIAN) {
+    *why = "the block-Lanczos route (lanczos_cap > 0) is built for KCG_PRIOR_LAPLACIAN";
+    return false;
+  }
   if (d->precond != KCG_PRECOND_NONE && d->precond != KCG_PRECOND_BLOCK_JACOBI) { *why = "unknown precond"; return false; }
   if (d->precond == KCG_PRECOND_BLOCK_JACOBI && d->n_comp > 7) {
     *why = "KCG_PRECOND_BLOCK_JACOBI is built for n_comp <= 7 (shared-memory budget)";
@@ -368,6 +413,25 @@ bool encode_xmap(CUtensorMap* m, double* base, int side, int rows, size_t planes
   if (r != CUDA_SUCCESS) {
     char buf[128];
     snprintf(buf, sizeof buf, "cuTensorMapEncodeTiled (x) failed (%d)", (int)r);
+    *why = buf;
+    return false;
+  }
+  return true;
+}
+
+// TMA descriptor of the block-Lanczos slots [planes][side][pitch], box {64 + 4, TY + 4, K}.
+bool encode_lzmap(CUtensorMap* m, double* base, int side, int pitch, size_t planes, int K, std::string* why) {
+  auto enc = get_encode();
+  if (!enc) { *why = "cuTensorMapEncodeTiled unavailable"; return false; }
+  cuuint64_t dims[3] = {(cuuint64_t)side, (cuuint64_t)side, (cuuint64_t)planes};
+  cuuint64_t strides[2] = {(cuuint64_t)pitch * 8, (cuuint64_t)pitch * side * 8};
+  cuuint32_t box[3] = {(cuuint32_t)(KCG_TX + 4), (cuuint32_t)(kcg::lz_tile_y(K) + 4), (cuuint32_t)K};
+  cuuint32_t es[3] = {1, 1, 1};
+  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, base, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                   CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    char buf[128];
+    snprintf(buf, sizeof buf, "cuTensorMapEncodeTiled (lanczos) failed (%d)", (int)r);
     *why = buf;
     return false;
   }
@@ -642,6 +706,130 @@ kcg_status solve_impl(kcg_ctx* c, Route route, const double* Y_in, double* mu_ou
   return (kcg_status)worst;
 }
 
+
+// Block-Lanczos Sylvester solve (Alg. SylvSolver): rhs kernel (Y^ = Y T A P^{-1} into
+// slot 0), one cooperative launch (Lanczos passes + gamma + coefficients + replay), store mode:
+// the assembly kernel; then the true residual of G mu = b as for CG.
+kcg_status lanczos_impl(kcg_ctx* c, const double* Y_in, double* mu_out, bool host_io, double tol, int max_iter,
+                        kcg_report* rep) {
+  if (!c) return KCG_E_ARG;
+  if (c->L.lz_slots <= 0 || c->slab) {
+    c->err = c->slab ? "block-Lanczos route: no row slabs" : "block-Lanczos route needs desc.lanczos_cap > 0";
+    return KCG_E_CONFIG;
+  }
+  if (!Y_in || !mu_out) { c->err = "null Y or mu"; return KCG_E_ARG; }
+  if (!(tol > 0.0) || !std::isfinite(tol)) { c->err = "tol must be finite and > 0"; return KCG_E_ARG; }
+  if (max_iter < 0) { c->err = "max_iter < 0"; return KCG_E_ARG; }
+  if (host_io && !c->d.host_staging) { c->err = "host entry point needs desc.host_staging = 1"; return KCG_E_CONFIG; }
+  cudaStream_t s = c->stream;
+  const int P = c->P, n = c->n, k = c->k;
+  const size_t N = c->N;
+  RankState& R = c->R[0];
+  const double* Yr = host_io ? R.Y_stage : Y_in;
+  double* muu = host_io ? R.mu_stage : mu_out;
+  double* mur = R.x_rm ? R.x_rm : muu;
+  const int cap = c->d.lanczos_cap;
+  const int mit = std::min(max_iter, cap);
+
+  CK(cudaEventRecord(c->ev[0], s), "event");
+  if (host_io) CK(cudaMemcpyAsync(R.Y_stage, Y_in, (size_t)P * n * N * 8, cudaMemcpyHostToDevice, s), "H2D Y");
+  SlabGeom g{c->side, c->side, 0, c->pitch, 0, 0, c->d.layout == KCG_LAYOUT_NESTED, false};
+  CK(kcg::launch_rhs(k, s, Yr, R.E_lz, nullptr, R.lz_V, nullptr, nullptr, P, n, g), "lanczos rhs kernel");
+  CK(cudaMemsetAsync(R.lz_st, 0, P * sizeof(kcg::LzState), s), "memset lanczos state");
+  CK(cudaEventRecord(c->ev[1], s), "event");
+  kcg::LzArgs a{};
+  a.prm = R.lz_prm;
+  a.hits = R.hits;
+  a.V = R.lz_V;
+  a.Mx = mur;
+  a.part = R.lz_part;
+  a.st = R.lz_st;
+  a.Hs = R.lz_H;
+  a.Rs = R.lz_R;
+  a.Ri = R.lz_Ri;
+  a.Sinv = R.lz_Sinv;
+  a.gv = R.lz_g;
+  a.Zs = R.lz_Z;
+  a.P = P;
+  a.side = c->side;
+  a.pitch = c->pitch;
+  a.tiles_x = c->tiles_x_lz;
+  a.tiles_y = c->tiles_y_lz;
+  a.tps = a.tiles_x * a.tiles_y;
+  a.cap = cap;
+  a.max_iter = mit;
+  a.store = c->d.lanczos_store;
+  a.tol = tol;
+  a.trace = R.trace;
+  CK(kcg::launch_lanczos(k, R.hits != nullptr, s, a, R.lz_map, c->grid_lz, c->smem_lz), "lanczos kernel");
+  if (a.store) CK(kcg::launch_lz_assemble(k, s, a), "lanczos assembly kernel");
+  CK(cudaEventRecord(c->ev[2], s), "event");
+  CK(kcg::launch_resid(k, s, R.params_kron, mur, Yr, R.E_kron, R.hits, R.resid_partials, R.resid_out, P, n,
+                       geom_of(c, R), nullptr, nullptr),
+     "residual kernel");
+  if (R.x_rm) CK(kcg::launch_permute(s, R.x_rm, muu, (size_t)P * k, c->side, true), "permute mu");
+  c->lz_host.resize(P);
+  c->resid_host.resize((size_t)P * 2);
+  CK(cudaMemcpyAsync(c->lz_host.data(), R.lz_st, P * sizeof(kcg::LzState), cudaMemcpyDeviceToHost, s), "D2H");
+  CK(cudaMemcpyAsync(c->resid_host.data(), R.resid_out, (size_t)P * 2 * 8, cudaMemcpyDeviceToHost, s), "D2H");
+  if (host_io) CK(cudaMemcpyAsync(mu_out, R.mu_stage, (size_t)P * k * N * 8, cudaMemcpyDeviceToHost, s), "D2H mu");
+  CK(cudaEventRecord(c->ev[3], s), "event");
+  CK(cudaStreamSynchronize(s), "lanczos solve");
+
+  int worst = KCG_OK, maxit = 0, allconv = 1;
+  long long sumit = 0;
+  double maxrel = 0.0, bytes = 0.0;
+  const double vec = 8.0 * k * (double)N;  // one block vector of a patch
+  for (int p = 0; p < P; ++p) {
+    const kcg::LzState& z = c->lz_host[p];
+    maxit = std::max(maxit, z.iters);
+    sumit += z.iters;
+    maxrel = std::max(maxrel, z.rel);
+    if (z.status != kcg::ST_CONVERGED) allconv = 0;
+    int code = KCG_OK;
+    if (z.status == kcg::ST_NONFINITE) code = KCG_E_NONFINITE;
+    else if (z.status == kcg::ST_BREAKDOWN) code = KCG_E_BREAKDOWN;
+    else if (z.status == kcg::ST_MAXIT || z.status == kcg::ST_RUNNING) code = KCG_NOT_CONVERGED;
+    auto rank = [](int cd) { return cd == KCG_E_NONFINITE ? 3 : cd == KCG_E_BREAKDOWN ? 2 : cd == KCG_NOT_CONVERGED ? 1 : 0; };
+    if (rank(code) > rank(worst)) worst = code;
+    // algorithmic bytes: Gram pass reads Y^; step 1 reads Y^ and writes V_1; step i >= 2 reads V_{i-1}
+    // (and V_{i-2} from i = 3) and writes V_i; assembly reads V_1..V_i and writes M (store) or replays
+    // the steps with M read + written (M only written on the first replay step)
+    const int i = z.iters;
+    double b = vec;  // Gram of Y^
+    if (i >= 1) b += 2 * vec;
+    if (i >= 2) b += (2.0 + 3.0 * (i - 2)) * vec;
+    if (c->d.lanczos_store) b += (i > 0 ? (double)i + 1.0 : 1.0) * vec;
+    else b += (i >= 2 ? 5.0 * i - 4.0 : i == 1 ? 2.0 : 1.0) * vec;  // V reads/writes 3i-3, M 2i-1
+    bytes += b;
+  }
+  double maxtrue = 0.0;
+  for (int p = 0; p < P; ++p) {
+    const double r2 = c->resid_host[(size_t)p * 2], b2 = c->resid_host[(size_t)p * 2 + 1];
+    maxtrue = std::max(maxtrue, b2 > 0 ? std::sqrt(r2 / b2) : std::sqrt(r2));
+  }
+  if (rep) {
+    float t03 = 0.f, t12 = 0.f;
+    cudaEventElapsedTime(&t03, c->ev[0], c->ev[3]);
+    cudaEventElapsedTime(&t12, c->ev[1], c->ev[2]);
+    rep->status = worst;
+    rep->converged = allconv;
+    rep->iterations = maxit;
+    rep->n_systems = P;
+    if (rep->iterations_per)
+      for (int p = 0; p < P; ++p) rep->iterations_per[p] = c->lz_host[p].iters;
+    rep->rel_residual = maxrel;
+    rep->rel_residual_true = maxtrue;
+    rep->wall_time_s = t03 * 1e-3;
+    rep->loop_time_s = t12 * 1e-3;
+    rep->system_iterations = sumit;
+    rep->loop_bytes = bytes;
+    rep->peak_mem_bytes = c->ws_need;
+    rep->history_len = 0;
+  }
+  c->err.clear();
+  return (kcg_status)worst;
+}
 }  // namespace
 
 namespace {
@@ -801,6 +989,33 @@ kcg_status create_impl(const kcg_desc* d, const kcg_slab* sl, const double* A_ho
         return fail(KCG_E_CUDA, why);
     }
   }
+  if (c->L.lz_slots > 0) {  // block-Lanczos constants: Lemma 2 factor, E = T A P^{-1} (Y^ = Y E)
+    std::vector<kcg::LzFace> lf(P);
+    std::vector<double> El((size_t)P * n * k);
+    for (int p = 0; p < P; ++p) {
+      kcg::LzFace& F = lf[p];
+      std::memset(&F, 0, sizeof F);
+      for (int i = 0; i < k; ++i) {
+        F.rho[i] = c->rho[(size_t)p * k + i];
+        F.phi[i] = phi_host[(size_t)p * k + i];
+        for (int cc = 0; cc < k; ++cc) F.W[cc * k + i] = c->W[((size_t)p * k + cc) * k + i];
+      }
+      F.kappa2 = kappa2_host[p];
+      for (int f = 0; f < n; ++f)
+        for (int a = 0; a < k; ++a)
+          El[((size_t)p * n + f) * k + a] = T_host[(size_t)p * n + f] * A_host[((size_t)p * n + f) * k + a] / phi_host[(size_t)p * k + a];
+    }
+    RankState& R = c->R[0];
+    CKC(cudaMemcpyAsync(R.lz_prm, lf.data(), P * sizeof(kcg::LzFace), cudaMemcpyHostToDevice, c->stream), "H2D");
+    CKC(cudaMemcpyAsync(R.E_lz, El.data(), El.size() * 8, cudaMemcpyHostToDevice, c->stream), "H2D");
+    if (!encode_lzmap(&R.lz_map, R.lz_V, c->side, c->pitch, (size_t)c->L.lz_slots * P * k, k, &why))
+      return fail(KCG_E_CUDA, why);
+    int mgl = 0;
+    CKC(kcg::lz_kernel_config(k, hits_dev != nullptr, &mgl, &c->smem_lz), "lanczos kernel config");
+    c->grid_lz = std::max(1, mgl);
+    c->tiles_x_lz = (c->side + KCG_TX - 1) / KCG_TX;
+    c->tiles_y_lz = (c->side + kcg::lz_tile_y(k) - 1) / kcg::lz_tile_y(k);
+  }
   CKC(cudaStreamSynchronize(c->stream), "create sync");
   c->tiles_x_kron = tiles_x(c->side, k);
   c->tiles_y_kron = tiles_y(c->rows, k, d2);
@@ -858,6 +1073,14 @@ kcg_status kron_cg_solve(kcg_ctx* c, const double* Y, double* mu, double tol, in
 }
 kcg_status sylvester_solve(kcg_ctx* c, const double* Y, double* mu, double tol, int max_iter, kcg_report* rep) {
   return solve_impl(c, ROUTE_SYL, Y, mu, false, tol, max_iter, rep);
+}
+kcg_status sylvester_lanczos_solve(kcg_ctx* c, const double* Y, double* mu, double tol, int max_iter,
+                                   kcg_report* rep) {
+  return lanczos_impl(c, Y, mu, false, tol, max_iter, rep);
+}
+kcg_status sylvester_lanczos_solve_host(kcg_ctx* c, const double* Y, double* mu, double tol, int max_iter,
+                                        kcg_report* rep) {
+  return lanczos_impl(c, Y, mu, true, tol, max_iter, rep);
 }
 kcg_status kron_cg_solve_host(kcg_ctx* c, const double* Y, double* mu, double tol, int max_iter, kcg_report* rep) {
   return solve_impl(c, ROUTE_KRON, Y, mu, true, tol, max_iter, rep);

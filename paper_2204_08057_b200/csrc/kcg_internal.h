@@ -176,6 +176,45 @@ struct SlabGeom {
   int d2;                    // 1: prior Q0 = D^2 + kappa2 I (radius-2 operator)
 };
 
+// ---- block-Lanczos Sylvester solver (Alg. SylvSolver)
+#define KCG_LZ_GRID_MAX 512  // partial-sum rows per face in the workspace (>= the cooperative grid)
+struct LzFace {              // per-face constants, host-computed at create (Lemma 2)
+  double rho[KCG_KMAX];      // ascending eigenvalues of S^ = M P^{-1}
+  double W[KCG_KMAX * KCG_KMAX];  // W[c*K + j]: eigenvector j (W^T P W = I); U = P W, U^{-1} = W^T
+  double phi[KCG_KMAX];      // P = diag(phi)
+  double kappa2;
+};
+struct LzState {             // per-face state, written by the face's reducer CTA
+  int iters;                 // completed Lanczos steps i
+  int status;                // ST_*
+  double bnorm;              // ||B_0||_F
+  double rel;                // sqrt(gamma_i) / ||B_0||_F (the paper's residual estimate)
+};
+struct LzArgs {
+  const LzFace* prm;         // [P]
+  const double* hits;        // [P][side][side] or nullptr (N_h = I)
+  double* V;                 // block slots [nslots][P][K][side][pitch]: slot 0 = Y^ = Y T A P^{-1}
+  double* Mx;                // solution M [P][K][side][side] (row-major pixels)
+  double* part;              // per-CTA Gram partials [P][KCG_LZ_GRID_MAX][NPART]
+  LzState* st;               // [P]
+  double* Hs;                // H_i          [P][cap][K*K]
+  double* Rs;                // B_0, B_2, .. [P][cap+1][K*K]  (Rs[a] normalises V_{a+1}: V_{a+1} Rs[a] = W_a)
+  double* Ri;                // Rs^{-1}      [P][cap+1][K*K]
+  double* Sinv;              // per shift j: Schur complement inverses of T_i + rho_j I  [P][cap][K][K*K]
+  double* gv;                // per shift j: eliminated right-hand sides                 [P][cap][K][K]
+  double* Zs;                // coefficients G_i of M = sum V_i G_i (Eq.(soln-darstellung)) [P][cap][K*K]
+  int P, side, pitch, tiles_x, tiles_y, tps, cap, max_iter, store;
+  double tol;
+  long long* trace;          // KCG_TRACE builds: [pass][5 + CTA] %globaltimer stamps (else nullptr)
+};
+// V slot of block q: the HBM-resident basis (store) keeps every block; the paper's memory-lean
+// two-pass mode rotates three slots after Y^.
+__host__ __device__ inline int lz_slot(int store, int q) { return store ? q : (q == 0 ? 0 : 1 + (q - 1) % 3); }
+__host__ __device__ constexpr int lz_tile_y(int K) { return K <= 2 ? 16 : 8; }
+__host__ __device__ constexpr int lz_npart(int K) {
+  return ((2 * K + 3) / 4) * ((2 * K + 3) / 4 + 1) / 2 * 16;
+}
+
 // ---------------------------------------------------------------- launchers (kcg_kernels.cu)
 // All return cudaError_t of the launch.
 cudaError_t launch_rhs(int K, cudaStream_t s, const double* Y, const double* E, const double* hits,
@@ -204,5 +243,18 @@ cudaError_t launch_xrank_sync(cudaStream_t s, const XrankSync& X);
 // dst[plane][nest(x,y)] = src[plane][y side + x] (to_nested) or the inverse gather.
 cudaError_t launch_permute(cudaStream_t s, const double* src, double* dst, size_t planes, int side, bool to_nested);
 int apply_tiles_per_sys(int rows, int side);
+// block-Lanczos (kcg_lanczos_*.cu): one cooperative launch runs the Lanczos passes, the residual
+// estimate, the coefficients and (two-pass mode) the replay that assembles M; store mode follows it
+// with lz_assemble.
+cudaError_t lz_kernel_config(int K, bool hits, int* max_grid, size_t* smem);
+cudaError_t launch_lanczos(int K, bool hits, cudaStream_t s, const LzArgs& a, const CUtensorMap& vmap, int grid,
+                           size_t smem);
+cudaError_t launch_lz_assemble(int K, cudaStream_t s, const LzArgs& a);
+template <int K>
+struct LzEntry {  // defined in kcg_lanczos.cuh, instantiated per K in kcg_lanczos_{a,b}.cu
+  static cudaError_t config(bool hits, int* max_grid, size_t* smem);
+  static cudaError_t launch(bool hits, cudaStream_t s, const LzArgs& a, const CUtensorMap& vmap, int grid, size_t smem);
+  static cudaError_t assemble(cudaStream_t s, const LzArgs& a);
+};
 
 }  // namespace kcg

@@ -1,0 +1,810 @@
+#pragma once
+// sm_100a fp64 block-Lanczos Sylvester solver -- the paper's Alg. SylvSolver for
+//   N_h^{-1} Q0 M + M S^ = Y^,   S^ = A^T T A P^{-1},  Y^ = Y T A P^{-1}     (Eq.(Axb-Sylv))
+// with the block Lanczos process in the N_h inner product (Alg. Lanczos, Lemma 1
+// P:L317-327), the Galerkin projection T_i Z + Z S^ = E_1 B_0 (Eq.(Sylv-small)), S^ = U R U^{-1}
+// (Lemma 2), the residual estimate gamma and M = sum_i V_i G_i
+// (Eq.(soln-darstellung)) assembled by rerunning Lanczos or, with the basis
+// kept in HBM, by one streaming pass.
+//
+// B200 formulation (readings R25-R30):
+//  * One pass per Lanczos step reads V_{i-1} (tile + 2-pixel halo) and V_{i-2} and writes V_i:
+//    W_{i-1} = N^{-1} Q0 V_{i-1} - V_{i-2} B_{i-1}^T and V_i = (W_{i-1} - V_{i-1} H_{i-1}) B_i^{-1} are
+//    RECOMPUTED on the tile + 1 ring (never stored), then W_i = N^{-1} Q0 V_i - V_{i-1} B_i^T on the
+//    tile: 3 block-vectors of HBM traffic per step (24 K N bytes) instead of the textbook 7+.
+//  * ONE reduction per step: the N-weighted Gram of [V_i, W_i] gives H_i = V_i^T N W_i,
+//    Gv = V_i^T N V_i and C0 = W_i^T N W_i, and the Cholesky-QR Gram of W_i - V_i H_i follows as
+//    C = C0 - 2 H^T H + H^T Gv H (exact algebra; Gv keeps it accurate as orthogonality decays).
+//  * gamma by block forward elimination of (T_i + rho_j I) f = E_1 B_0 u_j, one shift per warp,
+//    O(m^3) per step per shift (the "only the needed entries" idea the paper cites) --
+//    the same quantity as the paper's eigendecomposition formula; the coefficients Z come from the
+//    stored eliminations by back substitution.
+//  * Deterministic: static contiguous tile chunks per CTA, fixed-order sums.
+#include "kcg_cg.cuh"
+
+namespace kcg {
+
+template <int K>
+struct LzCfg {
+  static constexpr int TX = KCG_TX;
+  static constexpr int TY = lz_tile_y(K);
+  static constexpr int HB = 2;                         // box halo: V_{i-1} is needed on the tile + 2 ring
+  static constexpr int BW = TX + 2 * HB, BH = TY + 2 * HB;
+  static constexpr int RW = TX + 2, RH = TY + 2, RN = RW * RH;  // tile + 1 ring (V_i region)
+  static constexpr int BOX = K * BH * BW;
+  static constexpr int STAGES = K <= 4 ? 2 : 1;
+  static constexpr int KP = (2 * K + 3) / 4 * 4;      // Gram rows [V, W] padded to 4
+  static constexpr int NB4 = KP / 4;
+  static constexpr int NJOB = NB4 * (NB4 + 1) / 2;    // upper-triangle 4x4 blocks of the Gram
+  static constexpr int NPART = NJOB * 16;
+  static constexpr int NT = 256;
+  static constexpr int SL = NT / NJOB;                // pixel slices per Gram block
+  static constexpr int NPIX = TX * TY;
+  static constexpr int OFF_U = STAGES * 2 * BOX;      // U = [V_i (K planes); W_i (K); 0 pad] on the ring grid
+  static constexpr int OFF_HS = OFF_U + KP * RN;      // hits of the tile
+  static constexpr int OFF_MAT = OFF_HS + NPIX;       // Hp, Bp, Ri, Bc, Z (K x K each)
+  static constexpr int OFF_RED = OFF_MAT + 5 * K * K; // flush scratch [NT][4]
+  static constexpr int DOUBLES = OFF_RED + NT * 4;
+  static constexpr size_t SMEM = (size_t)DOUBLES * 8 + 64;  // + mbarriers
+  // reducer scratch (in the box area, idle between passes)
+  static constexpr int SC_GAM = 0;                          // raw Gram [NPART]
+  static constexpr int SC_GRP = SC_GAM + NPART;              // group sums [NT]
+  static constexpr int SC_M = SC_GRP + NT;                   // Gv, H, C0, T1, C, R, X(Rinv), B0 [8][K*K]
+  static constexpr int SC_W = SC_M + 8 * K * K;              // per-shift warp scratch [K][8 K*K]
+  static constexpr int SC_RES = SC_W + K * 9 * K * K;        // residual per shift [K] + flags
+  static constexpr int SC_END = SC_RES + 2 * K + 8;
+  static_assert(SC_END <= OFF_U, "reducer scratch exceeds the box area");
+  static_assert(SMEM <= 227 * 1024, "shared memory budget");
+};
+
+enum { LZ_GRAM0 = 0, LZ_STEP = 1, LZ_REPLAY = 2 };
+
+// ------------------------------------------------------------------------- small dense algebra
+// Warp-cooperative on K x K row-major matrices in shared memory (K <= 8); lanes own entries.
+template <int K>
+__device__ __forceinline__ void w_matmul(const double* A, const double* B, double* Cm, bool transB = false) {
+  const int lane = threadIdx.x & 31;
+  for (int e = lane; e < K * K; e += 32) {
+    const int r = e / K, c = e - r * K;
+    double s = 0.0;
+#pragma unroll
+    for (int k = 0; k < K; ++k) s = fma(A[r * K + k], transB ? B[c * K + k] : B[k * K + c], s);
+    Cm[e] = s;
+  }
+  __syncwarp();
+}
+// Upper Cholesky C = R^T R (reads the upper triangle of C).  Returns false on a non-positive pivot.
+template <int K>
+__device__ __forceinline__ bool w_chol(const double* Cm, double* R) {
+  const int lane = threadIdx.x & 31;
+  bool ok = true;
+  for (int e = lane; e < K * K; e += 32) R[e] = 0.0;
+  __syncwarp();
+  for (int j = 0; j < K; ++j) {
+    double d = Cm[j * K + j];
+    for (int k = 0; k < j; ++k) d = fma(-R[k * K + j], R[k * K + j], d);
+    ok = ok && (d > 0.0) && isfinite(d);
+    const double rjj = sqrt(d > 0.0 ? d : 0.0);
+    if (lane > j && lane < K) {
+      double v = Cm[j * K + lane];
+      for (int k = 0; k < j; ++k) v = fma(-R[k * K + j], R[k * K + lane], v);
+      R[j * K + lane] = v / rjj;
+    }
+    if (lane == 0) R[j * K + j] = rjj;
+    __syncwarp();
+  }
+  return ok;
+}
+// X = R^{-1} for upper-triangular R (lane l owns column l).
+template <int K>
+__device__ __forceinline__ void w_triinv(const double* R, double* X) {
+  const int lane = threadIdx.x & 31;
+  if (lane < K) {
+    const int l = lane;
+    for (int j = K - 1; j > l; --j) X[j * K + l] = 0.0;
+    X[l * K + l] = 1.0 / R[l * K + l];
+    for (int j = l - 1; j >= 0; --j) {
+      double s = 0.0;
+      for (int k = j + 1; k <= l; ++k) s = fma(R[j * K + k], X[k * K + l], s);
+      X[j * K + l] = -s / R[j * K + j];
+    }
+  }
+  __syncwarp();
+}
+// Sinv = S^{-1} for SPD S via S = R^T R: S^{-1} = X X^T with X = R^{-1}.
+template <int K>
+__device__ __forceinline__ bool w_spdinv(const double* S, double* R, double* X, double* Sinv) {
+  const bool ok = w_chol<K>(S, R);
+  w_triinv<K>(R, X);
+  w_matmul<K>(X, X, Sinv, true);
+  return ok;
+}
+
+__device__ __forceinline__ int lz_deg(int gy, int gx, int side) {
+  return 4 - (gy == 0) - (gy == side - 1) - (gx == 0) - (gx == side - 1);
+}
+
+// ------------------------------------------------------------------------- partial flush
+// Per-thread Gram accumulators -> the CTA's partial of face f (fixed slice order).
+template <int K>
+__device__ __forceinline__ void lz_flush(const LzArgs& a, int f, double (&acc)[16], double* sm) {
+  using C = LzCfg<K>;
+  const int tid = threadIdx.x;
+  double* red = sm + C::OFF_RED;
+  double* dst = a.part + ((size_t)f * KCG_LZ_GRID_MAX + blockIdx.x) * C::NPART;
+#pragma unroll
+  for (int rd = 0; rd < 4; ++rd) {
+#pragma unroll
+    for (int j = 0; j < 4; ++j) red[tid * 4 + j] = acc[rd * 4 + j];
+    __syncthreads();
+    if (tid < C::NJOB * 4) {
+      const int job = tid >> 2, j = tid & 3;
+      double s = 0.0;
+      for (int sl = 0; sl < C::SL; ++sl) s += red[(sl * C::NJOB + job) * 4 + j];
+      dst[job * 16 + rd * 4 + j] = s;
+    }
+    __syncthreads();
+  }
+}
+
+// ------------------------------------------------------------------------- one pass over the tiles
+// mode LZ_GRAM0 (q = 0): Gram of Y^.  LZ_STEP (q = i >= 1): Lanczos step i.  LZ_REPLAY (q >= 1):
+// rebuild V_q and accumulate M += V_q G_q.  The active faces act[0..nact) are split into contiguous
+// tile chunks, one per CTA.
+template <int K, bool HITS>
+__device__ __forceinline__ void lz_pass(const LzArgs& a, const CUtensorMap* vmap, int q, int mode, const int* act,
+                                        const int* its, int nact, double* sm, uint64_t* bar, uint32_t& ph0,
+                                        uint32_t& ph1) {
+  using C = LzCfg<K>;
+  const int tid = threadIdx.x, cta = blockIdx.x, ncta = gridDim.x;
+  const long long T = (long long)nact * a.tps;
+  const long long t0 = T * cta / ncta, t1 = T * (cta + 1) / ncta;
+  if (t0 >= t1) return;
+  const int side = a.side;
+  const size_t pstride = (size_t)a.pitch * side;
+  const int slot1 = q == 0 ? 0 : lz_slot(a.store, q - 1);
+  const int slot2 = q >= 3 ? lz_slot(a.store, q - 2) : 0;
+  const int slotq = lz_slot(a.store, q);
+  const int nbox = q >= 3 ? 2 : 1;
+  double* U = sm + C::OFF_U;
+  double* hs = sm + C::OFF_HS;
+  double* mats = sm + C::OFF_MAT;
+  const double* Hp = mats;
+  const double* Bp = mats + K * K;
+  const double* Ri = mats + 2 * K * K;
+  const double* Bc = mats + 3 * K * K;
+  const double* Zm = mats + 4 * K * K;
+
+  auto issue = [&](long long t, int s) {
+    const int f = act[t / a.tps];
+    const int lt = (int)(t % a.tps);
+    const int ty = lt / a.tiles_x, tx = lt - ty * a.tiles_x;
+    double* b1 = sm + s * 2 * C::BOX;
+    fence_proxy_async_smem();
+    mbar_arrive_expect_tx(&bar[s], nbox * C::BOX * 8);
+    tma_load_3d(b1, vmap, &bar[s], tx * C::TX - C::HB, ty * C::TY - C::HB, (slot1 * a.P + f) * K);
+    if (nbox == 2) tma_load_3d(b1 + C::BOX, vmap, &bar[s], tx * C::TX - C::HB, ty * C::TY - C::HB, (slot2 * a.P + f) * K);
+  };
+  if (tid == 0)
+    for (int s = 0; s < C::STAGES && t0 + s < t1; ++s) issue(t0 + s, s);
+
+  double acc[16];
+#pragma unroll
+  for (int j = 0; j < 16; ++j) acc[j] = 0.0;
+  int cur = -1, its_f = 0;
+  double kap = 0.0;
+  const double* hp = nullptr;
+  for (long long t = t0; t < t1; ++t) {
+    const int s = C::STAGES == 1 ? 0 : (int)((t - t0) & 1);
+    const int ai = (int)(t / a.tps);
+    const int f = act[ai];
+    const int lt = (int)(t % a.tps);
+    const int y0 = (lt / a.tiles_x) * C::TY, x0 = (lt % a.tiles_x) * C::TX;
+    if (f != cur) {
+      if (cur >= 0 && mode != LZ_REPLAY) lz_flush<K>(a, cur, acc, sm);
+#pragma unroll
+      for (int j = 0; j < 16; ++j) acc[j] = 0.0;
+      cur = f;
+      its_f = its[ai];
+      kap = a.prm[f].kappa2;
+      hp = HITS ? a.hits + (size_t)f * side * side : nullptr;
+      if (mode != LZ_GRAM0) {
+        const size_t fc = (size_t)f * a.cap, fr = (size_t)f * (a.cap + 1);
+        for (int e = tid; e < K * K; e += C::NT) {
+          mats[e] = q >= 2 ? __ldcg(a.Hs + (fc + q - 2) * K * K + e) : 0.0;
+          mats[K * K + e] = q >= 2 ? __ldcg(a.Rs + (fr + q - 2) * K * K + e) : 0.0;
+          mats[2 * K * K + e] = __ldcg(a.Ri + (fr + q - 1) * K * K + e);
+          mats[3 * K * K + e] = __ldcg(a.Rs + (fr + q - 1) * K * K + e);
+          mats[4 * K * K + e] = mode == LZ_REPLAY ? __ldcg(a.Zs + (fc + q - 1) * K * K + e) : 0.0;
+        }
+      }
+      __syncthreads();
+    }
+    if (s == 0) { mbar_wait(&bar[0], ph0 & 1u); ++ph0; }
+    else { mbar_wait(&bar[1], ph1 & 1u); ++ph1; }
+    const double* B1 = sm + s * 2 * C::BOX;
+    const double* B2 = B1 + C::BOX;
+
+    // ---- step A: V_q on the tile + 1 ring (zero outside the face: free boundary, reading R2)
+    for (int e = tid; e < C::RN; e += C::NT) {
+      const int ry = e / C::RW, rx = e - ry * C::RW;
+      const int gy = y0 - 1 + ry, gx = x0 - 1 + rx;
+      const int bi = (ry + 1) * C::BW + rx + 1;
+      double v[K];
+      if (gy < 0 || gy >= side || gx < 0 || gx >= side) {
+#pragma unroll
+        for (int c = 0; c < K; ++c) v[c] = 0.0;
+      } else if (mode == LZ_GRAM0) {
+#pragma unroll
+        for (int c = 0; c < K; ++c) v[c] = B1[c * C::BH * C::BW + bi];
+      } else {
+        double t[K];
+        if (q == 1) {
+#pragma unroll
+          for (int c = 0; c < K; ++c) t[c] = B1[c * C::BH * C::BW + bi];
+        } else {
+          const double kd = kap + (double)lz_deg(gy, gx, side);
+          const double h = HITS ? __ldg(hp + (size_t)gy * side + gx) : 1.0;
+#pragma unroll
+          for (int c = 0; c < K; ++c) {
+            const double* p = B1 + c * C::BH * C::BW + bi;
+            const double w = fma(kd, p[0], -(p[-C::BW] + p[C::BW] + p[-1] + p[1]));
+            t[c] = HITS ? w / h : w;
+          }
+          if (q >= 3) {
+#pragma unroll
+            for (int c = 0; c < K; ++c)
+#pragma unroll
+              for (int d = 0; d < K; ++d) t[c] = fma(-B2[d * C::BH * C::BW + bi], Bp[c * K + d], t[c]);
+          }
+#pragma unroll
+          for (int c = 0; c < K; ++c)
+#pragma unroll
+            for (int d = 0; d < K; ++d) t[c] = fma(-B1[d * C::BH * C::BW + bi], Hp[d * K + c], t[c]);
+        }
+#pragma unroll
+        for (int c = 0; c < K; ++c) {
+          double s2 = 0.0;
+#pragma unroll
+          for (int d = 0; d < K; ++d) s2 = fma(t[d], Ri[d * K + c], s2);
+          v[c] = s2;
+        }
+      }
+#pragma unroll
+      for (int c = 0; c < K; ++c) U[c * C::RN + e] = v[c];
+    }
+    __syncthreads();
+
+    // ---- step B: W_q on the tile (or the replay's M update); store V_q
+    for (int e = tid; e < C::NPIX; e += C::NT) {
+      const int ly = e / C::TX, lx = e - ly * C::TX;
+      const int gy = y0 + ly, gx = x0 + lx;
+      const int ri = (ly + 1) * C::RW + lx + 1;
+      const int bi = (ly + 2) * C::BW + lx + 2;
+      const bool in = gy < side && gx < side;
+      if (mode == LZ_REPLAY) {
+        if (in) {
+          const size_t px = (size_t)gy * side + gx;
+          const size_t N = (size_t)side * side;
+#pragma unroll
+          for (int c = 0; c < K; ++c) {
+            double m = q > 1 ? a.Mx[((size_t)f * K + c) * N + px] : 0.0;
+#pragma unroll
+            for (int d = 0; d < K; ++d) m = fma(U[d * C::RN + ri], Zm[d * K + c], m);
+            a.Mx[((size_t)f * K + c) * N + px] = m;
+          }
+          if (q < its_f) {
+#pragma unroll
+            for (int c = 0; c < K; ++c)
+              a.V[((size_t)(slotq * a.P + f) * K + c) * pstride + (size_t)gy * a.pitch + gx] = U[c * C::RN + ri];
+          }
+        }
+      } else {
+        double w[K];
+        double h = 1.0;
+        if (!in) {
+          h = 0.0;
+#pragma unroll
+          for (int c = 0; c < K; ++c) w[c] = 0.0;
+        } else if (mode == LZ_GRAM0) {
+          if (HITS) h = __ldg(hp + (size_t)gy * side + gx);
+#pragma unroll
+          for (int c = 0; c < K; ++c) w[c] = 0.0;
+        } else {
+          const double kd = kap + (double)lz_deg(gy, gx, side);
+          if (HITS) h = __ldg(hp + (size_t)gy * side + gx);
+#pragma unroll
+          for (int c = 0; c < K; ++c) {
+            const double* p = U + c * C::RN + ri;
+            const double s2 = fma(kd, p[0], -(p[-C::RW] + p[C::RW] + p[-1] + p[1]));
+            w[c] = HITS ? s2 / h : s2;
+          }
+          if (q >= 2) {
+#pragma unroll
+            for (int c = 0; c < K; ++c)
+#pragma unroll
+              for (int d = 0; d < K; ++d) w[c] = fma(-B1[d * C::BH * C::BW + bi], Bc[c * K + d], w[c]);
+          }
+#pragma unroll
+          for (int c = 0; c < K; ++c)
+            a.V[((size_t)(slotq * a.P + f) * K + c) * pstride + (size_t)gy * a.pitch + gx] = U[c * C::RN + ri];
+        }
+#pragma unroll
+        for (int c = 0; c < K; ++c) U[(K + c) * C::RN + ri] = w[c];
+        if (HITS) hs[e] = h;
+      }
+    }
+    __syncthreads();
+
+    // ---- N-weighted Gram of [V_q, W_q] (upper-triangle 4x4 blocks, one per thread group)
+    if (mode != LZ_REPLAY) {
+      const int job = tid % C::NJOB, sl = tid / C::NJOB;
+      if (sl < C::SL) {
+        int bi = 0, r = job;
+        while (r >= C::NB4 - bi) { r -= C::NB4 - bi; ++bi; }
+        const int bj = bi + r;
+        const double* ua = U + bi * 4 * C::RN;
+        const double* ub = U + bj * 4 * C::RN;
+        for (int px = sl; px < C::NPIX; px += C::SL) {
+          const int ly = px / C::TX, lx = px - ly * C::TX;
+          const int ri = (ly + 1) * C::RW + lx + 1;
+          double xa[4], yb[4];
+#pragma unroll
+          for (int j = 0; j < 4; ++j) { xa[j] = ua[j * C::RN + ri]; yb[j] = ub[j * C::RN + ri]; }
+          if (HITS) {
+            const double h = hs[px];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) xa[j] *= h;
+          }
+#pragma unroll
+          for (int i = 0; i < 4; ++i)
+#pragma unroll
+            for (int j = 0; j < 4; ++j) acc[i * 4 + j] = fma(xa[i], yb[j], acc[i * 4 + j]);
+        }
+      }
+    }
+    __syncthreads();  // U and the stage's boxes are free
+    if (tid == 0 && t + C::STAGES < t1) issue(t + C::STAGES, s);
+  }
+  if (mode != LZ_REPLAY && cur >= 0) lz_flush<K>(a, cur, acc, sm);
+}
+
+// ------------------------------------------------------------------------- per-face reduction
+// Reducer CTA of face act[ai] after pass q: sums the CTA partials (fixed order), then
+//   q = 0: B_0 = chol(Y^T N Y^);  q = i >= 1: H_i, C = W^T N W (Cholesky-QR Gram), B_{i+1} = chol(C),
+//   per shift j: T_i + rho_j I eliminated by one more block row, gamma_j = ||B_{i+1} f_last||^2;
+//   stop when sqrt(gamma) <= tol ||B_0||_F (Alg. SylvSolver).
+template <int K>
+__device__ void lz_reduce(const LzArgs& a, int q, const int* act, int nact, int ai, double* sm) {
+  using C = LzCfg<K>;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, ncta = gridDim.x;
+  const int f = act[ai];
+  const long long T = (long long)nact * a.tps;
+  const long long f0 = (long long)ai * a.tps, f1 = f0 + a.tps;
+  const size_t fc = (size_t)f * a.cap, fr = (size_t)f * (a.cap + 1);
+  // the previous step's elimination of every shift does not depend on this pass: fetch it first
+  // (overlaps the L2 latency with the partial sums below)
+  if (q >= 2 && warp < K) {
+    double* Sp = sm + C::SC_W + warp * 9 * K * K + K * K;
+    double* Bs = Sp + K * K;
+    double* gp = Bs + 6 * K * K;  // past Si: the 9th K x K slot of the warp
+    const double* spg = a.Sinv + ((fc + q - 2) * K + warp) * K * K;
+    for (int e = lane; e < K * K; e += 32) {
+      Sp[e] = __ldcg(spg + e);
+      Bs[e] = __ldcg(a.Rs + (fr + q - 1) * K * K + e);  // sub-diagonal block between blocks q-2, q-1
+    }
+    if (lane < K) gp[lane] = __ldcg(a.gv + ((fc + q - 2) * K + warp) * K + lane);
+  }
+  // CTAs whose chunk intersects the face's tiles: b_lo .. b_hi
+  int b_lo = (int)((f0 * ncta) / T);
+  while (b_lo > 0 && T * b_lo / ncta > f0) --b_lo;
+  while (T * (b_lo + 1) / ncta <= f0) ++b_lo;
+  int b_hi = b_lo;
+  while (b_hi + 1 < ncta && T * (b_hi + 1) / ncta < f1) ++b_hi;
+  double* gam = sm + C::SC_GAM;
+  double* grp = sm + C::SC_GRP;
+  constexpr int NG = C::NT / C::NPART;
+  {
+    const int g = tid / C::NPART, e = tid - g * C::NPART;
+    if (g < NG) {
+      // loads issued 8 at a time (memory-level parallelism), added in CTA order
+      double s = 0.0;
+      const double* src = a.part + (size_t)f * KCG_LZ_GRID_MAX * C::NPART + e;
+      for (int b0 = b_lo + g; b0 <= b_hi; b0 += 8 * NG) {
+        double v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const int b = b0 + u * NG;
+          const bool ok = b <= b_hi && T * (b + 1) / ncta > T * b / ncta;
+          v[u] = ok ? __ldcg(src + (size_t)b * C::NPART) : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) s += v[u];
+      }
+      grp[g * C::NPART + e] = s;
+    }
+  }
+  __syncthreads();
+  if (tid < C::NPART) {
+    double s = 0.0;
+    for (int g = 0; g < NG; ++g) s += grp[g * C::NPART + tid];
+    gam[tid] = s;
+  }
+  __syncthreads();
+  double* Gv = sm + C::SC_M;
+  double* H = Gv + K * K;
+  double* C0 = H + K * K;
+  double* T1 = C0 + K * K;
+  double* Cm = T1 + K * K;
+  double* R = Cm + K * K;
+  double* X = R + K * K;
+  double* B0 = X + K * K;
+  double* res = sm + C::SC_RES;
+  int* flag = reinterpret_cast<int*>(res + K);
+  auto G = [&](int i, int j) {  // symmetric Gram entry from the upper-triangle blocks
+    if (i > j) { const int t = i; i = j; j = t; }
+    const int bi = i >> 2, bj = j >> 2;
+    const int job = bi * C::NB4 - bi * (bi - 1) / 2 + (bj - bi);
+    return gam[job * 16 + (i & 3) * 4 + (j & 3)];
+  };
+  for (int e = tid; e < K * K; e += C::NT) {
+    const int r = e / K, c = e - r * K;
+    Gv[e] = G(r, c);
+    H[e] = G(r, K + c);
+    C0[e] = G(K + r, K + c);
+  }
+  __syncthreads();
+  const LzFace& pf = a.prm[f];
+  if (q == 0) {
+    if (warp == 0) {
+      const bool ok = w_chol<K>(Gv, R);
+      w_triinv<K>(R, X);
+      if (lane == 0) {
+        double tr = 0.0, fro = 0.0;
+        for (int e = 0; e < K * K; ++e) fro += R[e] * R[e];
+        for (int c = 0; c < K; ++c) tr += Gv[c * K + c];
+        LzState z{};
+        z.iters = 0;
+        z.bnorm = sqrt(fro);
+        z.rel = 1.0;
+        if (!isfinite(tr)) z.status = ST_NONFINITE;
+        else if (tr == 0.0) { z.status = ST_CONVERGED; z.bnorm = 0.0; z.rel = 0.0; }
+        else if (!ok) z.status = ST_BREAKDOWN;
+        else if (a.max_iter <= 0) z.status = ST_MAXIT;
+        else z.status = ST_RUNNING;
+        a.st[f] = z;
+      }
+      for (int e = lane; e < K * K; e += 32) {
+        a.Rs[fr * K * K + e] = R[e];
+        a.Ri[fr * K * K + e] = X[e];
+      }
+    }
+    return;
+  }
+  // C = C0 - 2 H^T H + H^T Gv H   (Gram of W - V H given V^T N W = H)
+  if (warp == 0) {
+    w_matmul<K>(Gv, H, T1);
+    for (int e = lane; e < K * K; e += 32) {
+      const int r = e / K, c = e - r * K;
+      double s = C0[e];
+      for (int k = 0; k < K; ++k) s = fma(H[k * K + r], fma(-2.0, H[k * K + c], T1[k * K + c]), s);
+      Cm[e] = s;
+    }
+    __syncwarp();
+    const bool ok = w_chol<K>(Cm, R);
+    if (ok) w_triinv<K>(R, X);
+    if (lane == 0) {
+      // Krylov space exhausted (W - V H = 0 up to rounding): B_{i+1} = 0, the projection is exact
+      double cmax = 0.0, c0max = 0.0;
+      for (int e = 0; e < K * K; ++e) { cmax = fmax(cmax, fabs(Cm[e])); c0max = fmax(c0max, fabs(C0[e])); }
+      flag[0] = ok ? 1 : (cmax <= 1e-14 * c0max ? 2 : 0);
+    }
+    __syncwarp();
+    if (flag[0] == 2)
+      for (int e = lane; e < K * K; e += 32) { R[e] = 0.0; X[e] = 0.0; }
+    for (int e = lane; e < K * K; e += 32) B0[e] = __ldcg(a.Rs + fr * K * K + e);
+  }
+  __syncthreads();
+  // per shift j (one warp each): block forward elimination of (T_i + rho_j I) f = E_1 B_0 u_j
+  const int blk = q - 1;  // block index of H_i in T_i
+  if (warp < K) {
+    const int j = warp;
+    double* D = sm + C::SC_W + j * 9 * K * K;
+    double* Sp = D + K * K;
+    double* Bs = Sp + K * K;
+    double* Xm = Bs + K * K;
+    double* S = Xm + K * K;
+    double* Rw = S + K * K;
+    double* Xw = Rw + K * K;
+    double* Si = Xw + K * K;
+    __shared__ double gvec[KCG_KMAX][KCG_KMAX], fvec[KCG_KMAX][KCG_KMAX];
+    const double rho = pf.rho[j];
+    for (int e = lane; e < K * K; e += 32) {
+      const int r = e / K, c = e - r * K;
+      D[e] = (r >= c ? H[e] : H[c * K + r]) + (r == c ? rho : 0.0);  // lower triangle of H (reading R29)
+    }
+    __syncwarp();
+    if (blk == 0) {
+      for (int e = lane; e < K * K; e += 32) S[e] = D[e];
+      if (lane < K) {  // g = B_0 u_j, u_j = P w_j
+        double s = 0.0;
+        for (int c = 0; c < K; ++c) s = fma(B0[lane * K + c], pf.phi[c] * pf.W[c * K + j], s);
+        gvec[j][lane] = s;
+      }
+      __syncwarp();
+    } else {
+      const double gp = lane < K ? Bs[6 * K * K + lane] : 0.0;  // prefetched at entry
+      w_matmul<K>(Bs, Sp, Xm);                 // X = B S_{blk-1}^{-1}
+      for (int e = lane; e < K * K; e += 32) {  // S = D - X B^T
+        const int r = e / K, c = e - r * K;
+        double s = D[e];
+        for (int k = 0; k < K; ++k) s = fma(-Xm[r * K + k], Bs[c * K + k], s);
+        S[e] = s;
+      }
+      if (lane < K) fvec[j][lane] = gp;
+      __syncwarp();
+      if (lane < K) {  // g = -X g_prev
+        double s = 0.0;
+        for (int c = 0; c < K; ++c) s = fma(-Xm[lane * K + c], fvec[j][c], s);
+        gvec[j][lane] = s;
+      }
+      __syncwarp();
+    }
+    w_spdinv<K>(S, Rw, Xw, Si);
+    if (lane < K) {  // f = S^{-1} g
+      double s = 0.0;
+      for (int c = 0; c < K; ++c) s = fma(Si[lane * K + c], gvec[j][c], s);
+      fvec[j][lane] = s;
+    }
+    __syncwarp();
+    if (lane == 0) {  // ||B_{i+1} f||^2
+      double g2 = 0.0;
+      for (int r = 0; r < K; ++r) {
+        double s = 0.0;
+        for (int c = 0; c < K; ++c) s = fma(R[r * K + c], fvec[j][c], s);
+        g2 = fma(s, s, g2);
+      }
+      res[j] = g2;
+    }
+    double* so = a.Sinv + ((fc + blk) * K + j) * K * K;
+    for (int e = lane; e < K * K; e += 32) so[e] = Si[e];
+    if (lane < K) a.gv[((fc + blk) * K + j) * K + lane] = gvec[j][lane];
+  }
+  __syncthreads();
+  if (tid == 0) {
+    LzState z = a.st[f];
+    double gam2 = 0.0;
+    for (int j = 0; j < K; ++j) gam2 += res[j];
+    z.iters = q;
+    z.rel = z.bnorm > 0.0 ? sqrt(gam2) / z.bnorm : 0.0;
+    bool fin = isfinite(gam2);
+    for (int e = 0; e < K * K; ++e) fin = fin && isfinite(Cm[e]) && isfinite(H[e]);
+    if (!fin) z.status = ST_NONFINITE;
+    else if (flag[0] == 0) z.status = ST_BREAKDOWN;
+    else if (flag[0] == 2 || sqrt(gam2) <= a.tol * z.bnorm) z.status = ST_CONVERGED;
+    else if (q >= a.max_iter || q >= a.cap) z.status = ST_MAXIT;
+    else z.status = ST_RUNNING;
+    a.st[f] = z;
+  }
+  for (int e = tid; e < K * K; e += C::NT) {
+    a.Hs[(fc + blk) * K * K + e] = H[e];
+    if (q + 1 <= a.cap) {
+      a.Rs[(fr + q) * K * K + e] = R[e];
+      a.Ri[(fr + q) * K * K + e] = X[e];
+    }
+  }
+}
+
+// ------------------------------------------------------------------------- coefficients Z
+// Back substitution of the stored eliminations per shift j gives column j of Q F (Eq.(soln-constr)),
+// then Z = (Q F) U^{-1} = (Q F) W^T (reading R27), block by block: G_a = Z[a].
+template <int K>
+__device__ void lz_coeffs(const LzArgs& a, int f, double* sm) {
+  using C = LzCfg<K>;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int i = __ldcg(&a.st[f].iters);
+  if (i <= 0) return;
+  const size_t fc = (size_t)f * a.cap, fr = (size_t)f * (a.cap + 1);
+  if (warp < K) {
+    const int j = warp;
+    double fv = 0.0;  // lane r holds f_a[r]
+    for (int blk = i - 1; blk >= 0; --blk) {
+      const double* Si = a.Sinv + ((fc + blk) * K + j) * K * K;
+      double rhs = lane < K ? __ldcg(a.gv + ((fc + blk) * K + j) * K + lane) : 0.0;
+      if (blk < i - 1) {  // rhs -= B_{blk+1}^T f_{blk+1}
+        const double* Bn = a.Rs + (fr + blk + 1) * K * K;
+        double s = 0.0;
+#pragma unroll
+        for (int c = 0; c < K; ++c) s = fma(lane < K ? __ldcg(Bn + c * K + lane) : 0.0, __shfl_sync(0xffffffffu, fv, c), s);
+        rhs -= s;
+      }
+      double s = 0.0;
+#pragma unroll
+      for (int c = 0; c < K; ++c) s = fma(lane < K ? __ldcg(Si + lane * K + c) : 0.0, __shfl_sync(0xffffffffu, rhs, c), s);
+      fv = s;
+      if (lane < K) a.Zs[(fc + blk) * K * K + lane * K + j] = fv;  // F[blk][r][j]
+    }
+  }
+  __syncthreads();
+  const LzFace& pf = a.prm[f];
+  for (int rr = tid; rr < i * K; rr += C::NT) {  // Z[a][r][:] = F[a][r][:] W^T
+    double* z = a.Zs + fc * K * K + (size_t)rr * K;
+    double Fr[K];
+#pragma unroll
+    for (int j = 0; j < K; ++j) Fr[j] = z[j];
+#pragma unroll
+    for (int c = 0; c < K; ++c) {
+      double s = 0.0;
+#pragma unroll
+      for (int j = 0; j < K; ++j) s = fma(Fr[j], pf.W[c * K + j], s);
+      z[c] = s;
+    }
+  }
+}
+
+// ------------------------------------------------------------------------- the persistent kernel
+template <int K, bool HITS>
+__global__ void __launch_bounds__(256, 1)
+    lanczos_kernel(const __grid_constant__ LzArgs a, const __grid_constant__ CUtensorMap vmap) {
+  using C = LzCfg<K>;
+  extern __shared__ __align__(128) double sm[];
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sm + C::DOUBLES);
+  __shared__ int act[64], its[64];
+  __shared__ int nact_s, qmax_s;
+  const int tid = threadIdx.x, cta = blockIdx.x, ncta = gridDim.x;
+  cg::grid_group grid = cg::this_grid();
+  if (tid == 0) {
+    for (int s = 0; s < C::STAGES; ++s) mbar_init(&bar[s], 1);
+    fence_mbar_init();
+  }
+  for (int e = tid; e < (C::KP - 2 * K) * C::RN; e += C::NT) sm[C::OFF_U + 2 * K * C::RN + e] = 0.0;
+  __syncthreads();
+  uint32_t ph0 = 0, ph1 = 0;
+
+  // Lanczos passes (q = 0: B_0), one grid barrier before and one after the per-face reductions
+  for (int q = 0;; ++q) {
+    if (tid == 0) {
+      int n = 0;
+      for (int f = 0; f < a.P; ++f)
+        if (q == 0 || __ldcg(&a.st[f].status) == ST_RUNNING) { its[n] = 0; act[n++] = f; }
+      nact_s = n;
+    }
+    __syncthreads();
+    const int nact = nact_s;
+    if (nact == 0) break;
+    long long* tr = (KCG_TRACE && a.trace && q < KCG_TRACE_ITERS) ? a.trace + (size_t)q * KCG_TRACE_COLS : nullptr;
+    if (tr && cta == 0 && tid == 0) tr[0] = globaltimer();
+    lz_pass<K, HITS>(a, &vmap, q, q == 0 ? LZ_GRAM0 : LZ_STEP, act, its, nact, sm, bar, ph0, ph1);
+    if (tr && tid == 0 && 5 + cta < KCG_TRACE_COLS) tr[5 + cta] = globaltimer();
+    fence_proxy_async_global();
+    __threadfence();
+    grid.sync();
+    if (tr && cta == 0 && tid == 0) tr[2] = globaltimer();
+    for (int ai = cta; ai < nact; ai += ncta) {
+      lz_reduce<K>(a, q, act, nact, ai, sm);
+      __syncthreads();
+    }
+    if (tr && cta == 0 && tid == 0) tr[3] = globaltimer();
+    __threadfence();
+    grid.sync();
+    if (tr && cta == 0 && tid == 0) tr[4] = globaltimer();
+  }
+  // coefficients
+  for (int f = cta; f < a.P; f += ncta) {
+    lz_coeffs<K>(a, f, sm);
+    __syncthreads();
+  }
+  __threadfence();
+  grid.sync();
+  if (a.store) return;  // lz_assemble_kernel streams the stored basis
+  // replay (the paper's second Lanczos pass): rebuild V_q and add V_q G_q
+  const size_t N = (size_t)a.side * a.side;
+  for (int f = 0; f < a.P; ++f)
+    if (__ldcg(&a.st[f].iters) == 0)
+      for (size_t e = (size_t)cta * C::NT + tid; e < (size_t)K * N; e += (size_t)ncta * C::NT) a.Mx[(size_t)f * K * N + e] = 0.0;
+  if (tid == 0) {
+    int m = 0;
+    for (int f = 0; f < a.P; ++f) m = max(m, __ldcg(&a.st[f].iters));
+    qmax_s = m;
+  }
+  __syncthreads();
+  const int qmax = qmax_s;
+  for (int q = 1; q <= qmax; ++q) {
+    if (tid == 0) {
+      int n = 0;
+      for (int f = 0; f < a.P; ++f) {
+        const int it = __ldcg(&a.st[f].iters);
+        if (it >= q) { its[n] = it; act[n++] = f; }
+      }
+      nact_s = n;
+    }
+    __syncthreads();
+    lz_pass<K, HITS>(a, &vmap, q, LZ_REPLAY, act, its, nact_s, sm, bar, ph0, ph1);
+    fence_proxy_async_global();
+    __threadfence();
+    grid.sync();
+  }
+}
+
+// M = sum_q V_q G_q from the HBM-resident basis (store mode): one streaming pass over the blocks.
+template <int K>
+__global__ void __launch_bounds__(256) lz_assemble_kernel(const LzArgs a) {
+  const int f = blockIdx.y;
+  const int it = a.st[f].iters;
+  const size_t N = (size_t)a.side * a.side, pstride = (size_t)a.pitch * a.side;
+  const double* Z = a.Zs + (size_t)f * a.cap * K * K;
+  for (size_t px = (size_t)blockIdx.x * blockDim.x + threadIdx.x; px < N; px += (size_t)gridDim.x * blockDim.x) {
+    const size_t gy = px / a.side, gx = px - gy * a.side;
+    const size_t off = gy * a.pitch + gx;
+    double m[K];
+#pragma unroll
+    for (int c = 0; c < K; ++c) m[c] = 0.0;
+    int q = 1;
+    for (; q + 1 <= it; q += 2) {
+      double v0[K], v1[K];
+      const double* b0 = a.V + ((size_t)(q * a.P + f) * K) * pstride + off;
+      const double* b1 = a.V + ((size_t)((q + 1) * a.P + f) * K) * pstride + off;
+#pragma unroll
+      for (int d = 0; d < K; ++d) { v0[d] = __ldcs(b0 + d * pstride); v1[d] = __ldcs(b1 + d * pstride); }
+      const double* z0 = Z + (size_t)(q - 1) * K * K;
+      // same order as the replay: all of block q, then block q + 1 (bitwise-identical M)
+#pragma unroll
+      for (int c = 0; c < K; ++c) {
+#pragma unroll
+        for (int d = 0; d < K; ++d) m[c] = fma(v0[d], __ldg(z0 + d * K + c), m[c]);
+#pragma unroll
+        for (int d = 0; d < K; ++d) m[c] = fma(v1[d], __ldg(z0 + K * K + d * K + c), m[c]);
+      }
+    }
+    if (q <= it) {
+      const double* b0 = a.V + ((size_t)(q * a.P + f) * K) * pstride + off;
+      const double* z0 = Z + (size_t)(q - 1) * K * K;
+      double v0[K];
+#pragma unroll
+      for (int d = 0; d < K; ++d) v0[d] = __ldcs(b0 + d * pstride);
+#pragma unroll
+      for (int c = 0; c < K; ++c)
+#pragma unroll
+        for (int d = 0; d < K; ++d) m[c] = fma(v0[d], __ldg(z0 + d * K + c), m[c]);
+    }
+#pragma unroll
+    for (int c = 0; c < K; ++c) a.Mx[((size_t)f * K + c) * N + px] = m[c];
+  }
+}
+
+// ------------------------------------------------------------------------- host entry points
+template <int K>
+cudaError_t LzEntry<K>::config(bool hits, int* max_grid, size_t* smem) {
+  using C = LzCfg<K>;
+  const void* f = hits ? (const void*)lanczos_kernel<K, true> : (const void*)lanczos_kernel<K, false>;
+  cudaError_t e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM);
+  if (e != cudaSuccess) return e;
+  int dev = 0, nsm = 0, per = 0;
+  if ((e = cudaGetDevice(&dev)) != cudaSuccess) return e;
+  if ((e = cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev)) != cudaSuccess) return e;
+  if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, f, C::NT, C::SMEM)) != cudaSuccess) return e;
+  *max_grid = std::min(per * nsm, KCG_LZ_GRID_MAX);
+  *smem = C::SMEM;
+  return cudaSuccess;
+}
+
+template <int K>
+cudaError_t LzEntry<K>::launch(bool hits, cudaStream_t s, const LzArgs& a, const CUtensorMap& vmap, int grid,
+                               size_t smem) {
+  void* args[2] = {(void*)&a, (void*)&vmap};
+  const void* f = hits ? (const void*)lanczos_kernel<K, true> : (const void*)lanczos_kernel<K, false>;
+  return cudaLaunchCooperativeKernel(f, dim3(grid), dim3(LzCfg<K>::NT), args, smem, s);
+}
+
+template <int K>
+cudaError_t LzEntry<K>::assemble(cudaStream_t s, const LzArgs& a) {
+  int dev = 0, nsm = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  const size_t N = (size_t)a.side * a.side;
+  const int bx = (int)std::max<size_t>(1, std::min<size_t>((N + 255) / 256, (size_t)nsm * 8 / std::max(1, a.P) + 1));
+  lz_assemble_kernel<K><<<dim3(bx, a.P), 256, 0, s>>>(a);
+  return cudaGetLastError();
+}
+
+}  // namespace kcg

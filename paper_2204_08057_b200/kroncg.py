@@ -36,7 +36,8 @@ KCG_PRECOND_NONE, KCG_PRECOND_BLOCK_JACOBI = 0, 1
 class kcg_desc(C.Structure):
     _fields_ = [("level", C.c_int), ("n_freq", C.c_int), ("n_comp", C.c_int),
                 ("n_patches", C.c_int), ("prior", C.c_int), ("layout", C.c_int),
-                ("precond", C.c_int), ("host_staging", C.c_int), ("history_cap", C.c_int)]
+                ("precond", C.c_int), ("host_staging", C.c_int), ("history_cap", C.c_int),
+                ("lanczos_cap", C.c_int), ("lanczos_store", C.c_int)]
 
 
 class kcg_report(C.Structure):
@@ -69,6 +70,8 @@ kron_cg_solve = _sig("kron_cg_solve", C.c_int, _solve_args)
 sylvester_solve = _sig("sylvester_solve", C.c_int, _solve_args)
 kron_cg_solve_host = _sig("kron_cg_solve_host", C.c_int, _solve_args)
 sylvester_solve_host = _sig("sylvester_solve_host", C.c_int, _solve_args)
+sylvester_lanczos_solve = _sig("sylvester_lanczos_solve", C.c_int, _solve_args)
+sylvester_lanczos_solve_host = _sig("sylvester_lanczos_solve_host", C.c_int, _solve_args)
 kron_cg_apply = _sig("kron_cg_apply", C.c_int, [_ctxp, _vp, _vp])
 kron_cg_rhs = _sig("kron_cg_rhs", C.c_int, [_ctxp, _vp, _vp])
 sylvester_factor = _sig("sylvester_factor", C.c_int, [_ctxp, _vp, _vp])
@@ -93,7 +96,7 @@ EXPORTS = ["kron_cg_workspace_size", "kron_cg_create", "kron_cg_solve", "sylvest
            "kron_cg_solve_host", "sylvester_solve_host", "kron_cg_apply", "kron_cg_rhs",
            "sylvester_factor", "kcg_last_error", "kcg_status_string", "kron_cg_destroy",
            "kron_cg_workspace_size_slab", "kron_cg_create_slab", "kcg_ipc_export", "kcg_ipc_import",
-           "kcg_ipc_close"]
+           "kcg_ipc_close", "sylvester_lanczos_solve", "sylvester_lanczos_solve_host"]
 
 
 class KcgError(RuntimeError):
@@ -122,11 +125,14 @@ class KronCG:
     prior: "laplacian" (Q0 = kappa2 I + L, the configs) or "d2" (Q0 = D^2 + kappa2 I, the paper's).
     layout: "row" (pixel y*side + x) or "nested" (HEALPix NESTED inside the face, reading R1): Y, mu,
     hits and the apply / rhs arguments keep their [..][side][side] shapes, read as flat [N] vectors.
+    lanczos_cap: > 0 provisions the block-Lanczos route (``lanczos``, Alg. SylvSolver) for up to that
+    many Lanczos steps; lanczos_store keeps the whole basis in HBM (one assembly pass) instead of
+    the paper's second Lanczos pass.
     """
 
     def __init__(self, level, A, noise_prec, prior_scale, kappa2, hits=None, device=None,
                  host_staging=False, history_cap=0, stream=None, precond="none", layout="row",
-                 prior="laplacian"):
+                 prior="laplacian", lanczos_cap=0, lanczos_store=False):
         import torch
         A = np.ascontiguousarray(np.asarray(A, dtype=np.float64))
         if A.ndim == 2:
@@ -146,7 +152,8 @@ class KronCG:
         lay = {"row": KCG_LAYOUT_ROW_MAJOR, "nested": KCG_LAYOUT_NESTED}[layout]
         pr = {"laplacian": KCG_PRIOR_LAPLACIAN, "d2": KCG_PRIOR_D2}[prior]
         self.desc = kcg_desc(level, n, k, P, pr, lay,
-                             pc, int(bool(host_staging)), int(history_cap))
+                             pc, int(bool(host_staging)), int(history_cap), int(lanczos_cap),
+                             int(bool(lanczos_store)))
         ws = kron_cg_workspace_size(C.byref(self.desc))
         if ws == 0:
             raise KcgError(KCG_E_SHAPE, "invalid descriptor")
@@ -228,13 +235,23 @@ class KronCG:
         self._check_dev(mu, self.shape_mu, "mu")
         return mu, self._solve(sylvester_solve, Y, mu, tol, max_iter, self.P * self.k, **kw)
 
+    def lanczos(self, Y, mu=None, tol=1e-10, max_iter=100000, **kw):
+        """Block-Lanczos Sylvester solver (sylvester_lanczos_solve, Alg. SylvSolver).
+        Y: CUDA [P][n][side][side] -> (mu, report); report["iterations_per"] = Lanczos steps per patch."""
+        self._check_dev(Y, self.shape_Y, "Y")
+        mu = self._out(mu)
+        self._check_dev(mu, self.shape_mu, "mu")
+        return mu, self._solve(sylvester_lanczos_solve, Y, mu, tol, max_iter, self.P, **kw)
+
     def solve_host(self, Y, mu=None, tol=1e-10, max_iter=100000, route="kron", **kw):
-        """Host-buffer entry points (kron_cg_solve_host / sylvester_solve_host).
+        """Host-buffer entry points (kron_cg_solve_host / sylvester_solve_host /
+        sylvester_lanczos_solve_host).
 
         Y and mu are CPU tensors (pinned for full-speed copies) or numpy arrays."""
         mu = self._out(mu, host=True)
-        fn = kron_cg_solve_host if route == "kron" else sylvester_solve_host
-        n_sys = self.P if route == "kron" else self.P * self.k
+        fn = {"kron": kron_cg_solve_host, "sylvester": sylvester_solve_host,
+              "lanczos": sylvester_lanczos_solve_host}[route]
+        n_sys = self.P * self.k if route == "sylvester" else self.P
         return mu, self._solve(fn, Y, mu, tol, max_iter, n_sys, **kw)
 
     def apply(self, x, y=None):
