@@ -7,7 +7,8 @@
 One "step" = one full pass of the hot path over one batch of synthetic input: the right-hand side
 (a2), the whole CG iteration (a3-a5) to tolerance 1e-10 for every face, the termination report with
 the true residual (a7), all faces batched in one launch per rank (a8).  The Sylvester route (a6) is
-timed in the same run and reported under "sylvester".  Faces are sharded across ranks (LPT on the
+timed in the same run and reported under "sylvester"; the paper's block-Lanczos Sylvester solver
+(Alg. SylvSolver) under "lanczos" (its own context: HBM-resident basis).  Faces are sharded across ranks (LPT on the
 sqrt(cond) cost model); there is no data-path collective, only the timing barrier/max.
 
 `value` is whole-job full-sky solves/s (device time, CUDA events on the launching stream, max over
@@ -250,6 +251,37 @@ def run_reference(args):
     return 0
 
 
+def _lanczos_leg(problems, st, dev, timed, args):
+    """The paper's block-Lanczos Sylvester solver (Alg. SylvSolver, sylvester_lanczos_solve) on this
+    rank's faces: HBM-resident basis (lanczos_store) sized for the oracle's step counts, inputs
+    resident; its own context (the basis is not part of the CG workspace)."""
+    import torch
+    from paper_2204_08057_b200.kroncg import KronCG
+    ctx = KronCG(problems[0].level, st["A"], st["noise_prec"], st["tau"], st["kappa2"], device=dev,
+                 lanczos_cap=args.lanczos_cap, lanczos_store=True)
+    Y = torch.from_numpy(st["Y"]).to(dev)
+    mu = torch.empty(ctx.shape_mu, dtype=torch.float64, device=dev)
+    fn = lambda: ctx.lanczos(Y, mu, tol=TOL)[1]
+    for _ in range(max(1, args.warmup)):
+        r = fn()
+        assert r["converged"], r
+    t, reps = timed(fn, args.steps)
+    peak, peak_src = _peaks()
+    b = sum(r["loop_bytes"] for r in reps)
+    tl = sum(r["loop_time_s"] for r in reps)
+    out = {"value": len(reps) / t, "ms_per_step": t / len(reps) * 1e3,
+           "unit": "full-sky solves/s" if args.config == "fullsky" else "solves/s",
+           "lanczos_steps_per_face": reps[-1]["iterations_per"], "mode": "hbm-resident basis (lanczos_store)",
+           "true_rel_residual": reps[-1]["rel_residual_true"],
+           "roofline": {"bound": "hbm", "achieved": b / tl / 1e9, "peak": peak, "unit": "GB/s",
+                        "frac": b / tl / 1e9 / peak, "traffic": None,
+                        "kernel": "lanczos_kernel + lz_assemble_kernel", "peak_source": peak_src,
+                        "algorithmic_bytes_per_launch": b / len(reps), "avg_launch_ms": tl / len(reps) * 1e3}}
+    del ctx, Y, mu
+    torch.cuda.empty_cache()
+    return out
+
+
 def run_b200(args):
     import torch
     import torch.distributed as dist
@@ -327,6 +359,9 @@ def run_b200(args):
     t_other, reps_other = timed(other_fn, args.steps)
     host()
     t_e2e, reps_e2e = timed(host, max(1, args.e2e_steps))
+    lz = None
+    if g == 1 and not args.no_lanczos:
+        lz = _lanczos_leg(problems, st, dev, timed, args)
 
     def agg(reps_, t):
         # whole-job numbers: gather per-rank sums
@@ -407,6 +442,8 @@ def run_b200(args):
             "roofline": roofline(g_other, "sylvester" if args.route == "kron" else "kron")},
         "true_rel_residual": reps[-1]["rel_residual_true"],
     }
+    if lz is not None:
+        line["lanczos"] = lz
     if world == 1 and not args.no_slab_probe:
         line["slab_emulation"] = _slab_probe(dev)
     if world == 1 and not args.no_cpu_baseline:
@@ -429,6 +466,9 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-slab-probe", action="store_true")
+    ap.add_argument("--no-lanczos", action="store_true", help="skip the block-Lanczos (Alg. SylvSolver) leg")
+    ap.add_argument("--lanczos-cap", type=int, default=128,
+                    help="Lanczos steps provisioned (HBM-resident basis: P k N 8 (cap + 1) bytes)")
     ap.add_argument("--ref-iters", type=int, default=8, help="oracle CG iterations per reference step")
     ap.add_argument("--ref-face-iters", type=int, default=180,
                     help="fallback iterations per face if tests/golden/oracle_iterations.json lacks the config")

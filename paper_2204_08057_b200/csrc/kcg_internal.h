@@ -211,8 +211,8 @@ struct LzArgs {
 // two-pass mode rotates three slots after Y^.
 __host__ __device__ inline int lz_slot(int store, int q) { return store ? q : (q == 0 ? 0 : 1 + (q - 1) % 3); }
 __host__ __device__ constexpr int lz_tile_y(int K) { return K <= 2 ? 16 : 8; }
-__host__ __device__ constexpr int lz_npart(int K) {
-  return ((2 * K + 3) / 4) * ((2 * K + 3) / 4 + 1) / 2 * 16;
+__host__ __device__ constexpr int lz_npart(int K) {  // Gram partial per CTA and face
+  return K <= 4 ? K * (2 * K + 1) : ((2 * K + 3) / 4) * ((2 * K + 3) / 4 + 1) / 2 * 16;
 }
 
 // ---------------------------------------------------------------- launchers (kcg_kernels.cu)

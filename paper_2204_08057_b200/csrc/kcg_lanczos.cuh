@@ -32,11 +32,13 @@ struct LzCfg {
   static constexpr int BW = TX + 2 * HB, BH = TY + 2 * HB;
   static constexpr int RW = TX + 2, RH = TY + 2, RN = RW * RH;  // tile + 1 ring (V_i region)
   static constexpr int BOX = K * BH * BW;
-  static constexpr int STAGES = K <= 4 ? 2 : 1;
+  static constexpr int STAGES = K <= 4 ? 3 : (K == 5 ? 2 : 1);  // TMA tiles in flight
   static constexpr int KP = (2 * K + 3) / 4 * 4;      // Gram rows [V, W] padded to 4
   static constexpr int NB4 = KP / 4;
   static constexpr int NJOB = NB4 * (NB4 + 1) / 2;    // upper-triangle 4x4 blocks of the Gram
-  static constexpr int NPART = NJOB * 16;
+  static constexpr bool REGG = K <= 4;                 // Gram accumulated in registers in step B
+  static constexpr int NPART = REGG ? K * (2 * K + 1) : NJOB * 16;
+  static constexpr int NACC = REGG ? K * (2 * K + 1) : 16;
   static constexpr int NT = 256;
   static constexpr int SL = NT / NJOB;                // pixel slices per Gram block
   static constexpr int NPIX = TX * TY;
@@ -127,23 +129,40 @@ __device__ __forceinline__ int lz_deg(int gy, int gx, int side) {
 // ------------------------------------------------------------------------- partial flush
 // Per-thread Gram accumulators -> the CTA's partial of face f (fixed slice order).
 template <int K>
-__device__ __forceinline__ void lz_flush(const LzArgs& a, int f, double (&acc)[16], double* sm) {
+__device__ __forceinline__ void lz_flush(const LzArgs& a, int f, double (&acc)[LzCfg<K>::NACC], double* sm) {
   using C = LzCfg<K>;
   const int tid = threadIdx.x;
   double* red = sm + C::OFF_RED;
   double* dst = a.part + ((size_t)f * KCG_LZ_GRID_MAX + blockIdx.x) * C::NPART;
+  if constexpr (C::REGG) {
+    // xor-shuffle tree per warp, then the warps in order (fixed order: deterministic)
+    const int lane = tid & 31, warp = tid >> 5;
 #pragma unroll
-  for (int rd = 0; rd < 4; ++rd) {
-#pragma unroll
-    for (int j = 0; j < 4; ++j) red[tid * 4 + j] = acc[rd * 4 + j];
-    __syncthreads();
-    if (tid < C::NJOB * 4) {
-      const int job = tid >> 2, j = tid & 3;
-      double s = 0.0;
-      for (int sl = 0; sl < C::SL; ++sl) s += red[(sl * C::NJOB + job) * 4 + j];
-      dst[job * 16 + rd * 4 + j] = s;
+    for (int e = 0; e < C::NACC; ++e) {
+      const double v = warp_sum(acc[e]);
+      if (lane == 0) red[warp * C::NACC + e] = v;
     }
     __syncthreads();
+    if (tid < C::NACC) {
+      double s = 0.0;
+      for (int w = 0; w < C::NT / 32; ++w) s += red[w * C::NACC + tid];
+      dst[tid] = s;
+    }
+    __syncthreads();
+  } else {
+#pragma unroll
+    for (int rd = 0; rd < 4; ++rd) {
+#pragma unroll
+      for (int j = 0; j < 4; ++j) red[tid * 4 + j] = acc[rd * 4 + j];
+      __syncthreads();
+      if (tid < C::NJOB * 4) {
+        const int job = tid >> 2, j = tid & 3;
+        double s = 0.0;
+        for (int sl = 0; sl < C::SL; ++sl) s += red[(sl * C::NJOB + job) * 4 + j];
+        dst[job * 16 + rd * 4 + j] = s;
+      }
+      __syncthreads();
+    }
   }
 }
 
@@ -153,8 +172,7 @@ __device__ __forceinline__ void lz_flush(const LzArgs& a, int f, double (&acc)[1
 // tile chunks, one per CTA.
 template <int K, bool HITS>
 __device__ __forceinline__ void lz_pass(const LzArgs& a, const CUtensorMap* vmap, int q, int mode, const int* act,
-                                        const int* its, int nact, double* sm, uint64_t* bar, uint32_t& ph0,
-                                        uint32_t& ph1) {
+                                        const int* its, int nact, double* sm, uint64_t* bar, uint32_t& phbits) {
   using C = LzCfg<K>;
   const int tid = threadIdx.x, cta = blockIdx.x, ncta = gridDim.x;
   const long long T = (long long)nact * a.tps;
@@ -169,15 +187,16 @@ __device__ __forceinline__ void lz_pass(const LzArgs& a, const CUtensorMap* vmap
   double* U = sm + C::OFF_U;
   double* hs = sm + C::OFF_HS;
   double* mats = sm + C::OFF_MAT;
-  const double* Hp = mats;
-  const double* Bp = mats + K * K;
+  const double* P1m = mats;           // Hp Ri   (after the face prologue)
+  const double* P2m = mats + K * K;   // Bp^T Ri
   const double* Ri = mats + 2 * K * K;
   const double* Bc = mats + 3 * K * K;
   const double* Zm = mats + 4 * K * K;
 
   auto issue = [&](long long t, int s) {
-    const int f = act[t / a.tps];
-    const int lt = (int)(t % a.tps);
+    const int ti = (int)t;
+    const int f = act[ti / a.tps];
+    const int lt = ti - (ti / a.tps) * a.tps;
     const int ty = lt / a.tiles_x, tx = lt - ty * a.tiles_x;
     double* b1 = sm + s * 2 * C::BOX;
     fence_proxy_async_smem();
@@ -188,22 +207,22 @@ __device__ __forceinline__ void lz_pass(const LzArgs& a, const CUtensorMap* vmap
   if (tid == 0)
     for (int s = 0; s < C::STAGES && t0 + s < t1; ++s) issue(t0 + s, s);
 
-  double acc[16];
+  double acc[C::NACC];  // Gram accumulators: packed upper triangle of [V, W] (K <= 4) or a 4x4 block
 #pragma unroll
-  for (int j = 0; j < 16; ++j) acc[j] = 0.0;
+  for (int j = 0; j < C::NACC; ++j) acc[j] = 0.0;
   int cur = -1, its_f = 0;
   double kap = 0.0;
   const double* hp = nullptr;
   for (long long t = t0; t < t1; ++t) {
-    const int s = C::STAGES == 1 ? 0 : (int)((t - t0) & 1);
-    const int ai = (int)(t / a.tps);
+    const int s = C::STAGES == 1 ? 0 : (int)((t - t0) % C::STAGES);
+    const int ai = (int)t / a.tps;
     const int f = act[ai];
-    const int lt = (int)(t % a.tps);
+    const int lt = (int)t - ai * a.tps;
     const int y0 = (lt / a.tiles_x) * C::TY, x0 = (lt % a.tiles_x) * C::TX;
     if (f != cur) {
       if (cur >= 0 && mode != LZ_REPLAY) lz_flush<K>(a, cur, acc, sm);
 #pragma unroll
-      for (int j = 0; j < 16; ++j) acc[j] = 0.0;
+      for (int j = 0; j < C::NACC; ++j) acc[j] = 0.0;
       cur = f;
       its_f = its[ai];
       kap = a.prm[f].kappa2;
@@ -217,91 +236,127 @@ __device__ __forceinline__ void lz_pass(const LzArgs& a, const CUtensorMap* vmap
           mats[3 * K * K + e] = __ldcg(a.Rs + (fr + q - 1) * K * K + e);
           mats[4 * K * K + e] = mode == LZ_REPLAY ? __ldcg(a.Zs + (fc + q - 1) * K * K + e) : 0.0;
         }
+        __syncthreads();
+        // fold the step-A products: V_q = w Ri - V_{q-2} (Bp^T Ri) - V_{q-1} (Hp Ri)
+        double p1 = 0.0, p2 = 0.0;
+        if (tid < K * K) {
+          const int d = tid / K, c = tid - d * K;
+          for (int e2 = 0; e2 < K; ++e2) {
+            p1 = fma(mats[d * K + e2], mats[2 * K * K + e2 * K + c], p1);
+            p2 = fma(mats[K * K + e2 * K + d], mats[2 * K * K + e2 * K + c], p2);
+          }
+        }
+        __syncthreads();
+        if (tid < K * K) { mats[tid] = p1; mats[K * K + tid] = p2; }
       }
       __syncthreads();
     }
-    if (s == 0) { mbar_wait(&bar[0], ph0 & 1u); ++ph0; }
-    else { mbar_wait(&bar[1], ph1 & 1u); ++ph1; }
+    mbar_wait(&bar[s], (phbits >> s) & 1u);
+    phbits ^= 1u << s;
     const double* B1 = sm + s * 2 * C::BOX;
     const double* B2 = B1 + C::BOX;
 
     // ---- step A: V_q on the tile + 1 ring (zero outside the face: free boundary, reading R2)
-    for (int e = tid; e < C::RN; e += C::NT) {
-      const int ry = e / C::RW, rx = e - ry * C::RW;
-      const int gy = y0 - 1 + ry, gx = x0 - 1 + rx;
-      const int bi = (ry + 1) * C::BW + rx + 1;
-      double v[K];
-      if (gy < 0 || gy >= side || gx < 0 || gx >= side) {
+    {
+      // this tile's step-A matrices: registers for K <= 4, shared memory (broadcast) above
+      constexpr int NR = C::REGG ? K * K : 1;
+      double r1v[NR], r2v[NR], rrv[NR];
+      if constexpr (C::REGG) {
 #pragma unroll
-        for (int c = 0; c < K; ++c) v[c] = 0.0;
-      } else if (mode == LZ_GRAM0) {
+        for (int e2 = 0; e2 < K * K; ++e2) { rrv[e2] = Ri[e2]; r1v[e2] = P1m[e2]; r2v[e2] = P2m[e2]; }
+      }
+      auto rr = [&](int i) { if constexpr (C::REGG) return rrv[i]; else return Ri[i]; };
+      auto r1 = [&](int i) { if constexpr (C::REGG) return r1v[i]; else return P1m[i]; };
+      auto r2 = [&](int i) { if constexpr (C::REGG) return r2v[i]; else return P2m[i]; };
+      for (int e = tid; e < C::RN; e += C::NT) {
+        const int ry = e / C::RW, rx = e - ry * C::RW;
+        const int gy = y0 - 1 + ry, gx = x0 - 1 + rx;
+        const int bi = (ry + 1) * C::BW + rx + 1;
+        double v[K];
+        if (gy < 0 || gy >= side || gx < 0 || gx >= side) {
 #pragma unroll
-        for (int c = 0; c < K; ++c) v[c] = B1[c * C::BH * C::BW + bi];
-      } else {
-        double t[K];
-        if (q == 1) {
+          for (int c = 0; c < K; ++c) v[c] = 0.0;
+        } else if (mode == LZ_GRAM0) {
 #pragma unroll
-          for (int c = 0; c < K; ++c) t[c] = B1[c * C::BH * C::BW + bi];
+          for (int c = 0; c < K; ++c) v[c] = B1[c * C::BH * C::BW + bi];
         } else {
-          const double kd = kap + (double)lz_deg(gy, gx, side);
-          const double h = HITS ? __ldg(hp + (size_t)gy * side + gx) : 1.0;
+          double w[K], v1[K];
+#pragma unroll
+          for (int c = 0; c < K; ++c) v1[c] = B1[c * C::BH * C::BW + bi];
+          if (q == 1) {
+#pragma unroll
+            for (int c = 0; c < K; ++c) w[c] = v1[c];
+          } else {
+            const double kd = kap + (double)lz_deg(gy, gx, side);
+            const double h = HITS ? __ldg(hp + (size_t)gy * side + gx) : 1.0;
+#pragma unroll
+            for (int c = 0; c < K; ++c) {
+              const double* p = B1 + c * C::BH * C::BW + bi;
+              const double s2 = fma(kd, v1[c], -(p[-C::BW] + p[C::BW] + p[-1] + p[1]));
+              w[c] = HITS ? s2 / h : s2;
+            }
+          }
 #pragma unroll
           for (int c = 0; c < K; ++c) {
-            const double* p = B1 + c * C::BH * C::BW + bi;
-            const double w = fma(kd, p[0], -(p[-C::BW] + p[C::BW] + p[-1] + p[1]));
-            t[c] = HITS ? w / h : w;
+            double s2 = 0.0;
+#pragma unroll
+            for (int d = 0; d < K; ++d) s2 = fma(w[d], rr(d * K + c), s2);
+            if (q >= 2) {
+#pragma unroll
+              for (int d = 0; d < K; ++d) s2 = fma(-v1[d], r1(d * K + c), s2);
+            }
+            if (q >= 3) {
+#pragma unroll
+              for (int d = 0; d < K; ++d) s2 = fma(-B2[d * C::BH * C::BW + bi], r2(d * K + c), s2);
+            }
+            v[c] = s2;
           }
-          if (q >= 3) {
-#pragma unroll
-            for (int c = 0; c < K; ++c)
-#pragma unroll
-              for (int d = 0; d < K; ++d) t[c] = fma(-B2[d * C::BH * C::BW + bi], Bp[c * K + d], t[c]);
-          }
-#pragma unroll
-          for (int c = 0; c < K; ++c)
-#pragma unroll
-            for (int d = 0; d < K; ++d) t[c] = fma(-B1[d * C::BH * C::BW + bi], Hp[d * K + c], t[c]);
         }
 #pragma unroll
-        for (int c = 0; c < K; ++c) {
-          double s2 = 0.0;
-#pragma unroll
-          for (int d = 0; d < K; ++d) s2 = fma(t[d], Ri[d * K + c], s2);
-          v[c] = s2;
-        }
+        for (int c = 0; c < K; ++c) U[c * C::RN + e] = v[c];
       }
-#pragma unroll
-      for (int c = 0; c < K; ++c) U[c * C::RN + e] = v[c];
     }
     __syncthreads();
 
-    // ---- step B: W_q on the tile (or the replay's M update); store V_q
-    for (int e = tid; e < C::NPIX; e += C::NT) {
-      const int ly = e / C::TX, lx = e - ly * C::TX;
-      const int gy = y0 + ly, gx = x0 + lx;
-      const int ri = (ly + 1) * C::RW + lx + 1;
-      const int bi = (ly + 2) * C::BW + lx + 2;
-      const bool in = gy < side && gx < side;
-      if (mode == LZ_REPLAY) {
-        if (in) {
-          const size_t px = (size_t)gy * side + gx;
-          const size_t N = (size_t)side * side;
+    // ---- step B: W_q on the tile (or the replay's M update); store V_q; Gram (K <= 4: in registers)
+    {
+      constexpr int NRB = C::REGG ? K * K : 1;
+      double rbv[NRB];
+      const double* rbs = mode == LZ_REPLAY ? Zm : Bc;
+      if constexpr (C::REGG) {
 #pragma unroll
-          for (int c = 0; c < K; ++c) {
-            double m = q > 1 ? a.Mx[((size_t)f * K + c) * N + px] : 0.0;
+        for (int e2 = 0; e2 < K * K; ++e2) rbv[e2] = rbs[e2];
+      }
+      auto rb = [&](int i) { if constexpr (C::REGG) return rbv[i]; else return rbs[i]; };
+      for (int e = tid; e < C::NPIX; e += C::NT) {
+        const int ly = e / C::TX, lx = e - ly * C::TX;
+        const int gy = y0 + ly, gx = x0 + lx;
+        const int ri = (ly + 1) * C::RW + lx + 1;
+        const int bi = (ly + 2) * C::BW + lx + 2;
+        const bool in = gy < side && gx < side;
+        if (mode == LZ_REPLAY) {
+          if (in) {
+            const size_t px = (size_t)gy * side + gx;
+            const size_t N = (size_t)side * side;
 #pragma unroll
-            for (int d = 0; d < K; ++d) m = fma(U[d * C::RN + ri], Zm[d * K + c], m);
-            a.Mx[((size_t)f * K + c) * N + px] = m;
+            for (int c = 0; c < K; ++c) {
+              double m = q > 1 ? a.Mx[((size_t)f * K + c) * N + px] : 0.0;
+#pragma unroll
+              for (int d = 0; d < K; ++d) m = fma(U[d * C::RN + ri], rb(d * K + c), m);
+              a.Mx[((size_t)f * K + c) * N + px] = m;
+            }
+            if (q < its_f) {
+#pragma unroll
+              for (int c = 0; c < K; ++c)
+                a.V[((size_t)(slotq * a.P + f) * K + c) * pstride + (size_t)gy * a.pitch + gx] = U[c * C::RN + ri];
+            }
           }
-          if (q < its_f) {
-#pragma unroll
-            for (int c = 0; c < K; ++c)
-              a.V[((size_t)(slotq * a.P + f) * K + c) * pstride + (size_t)gy * a.pitch + gx] = U[c * C::RN + ri];
-          }
+          continue;
         }
-      } else {
-        double w[K];
+        double w[K], vq[K];
         double h = 1.0;
+#pragma unroll
+        for (int c = 0; c < K; ++c) vq[c] = U[c * C::RN + ri];
         if (!in) {
           h = 0.0;
 #pragma unroll
@@ -316,55 +371,71 @@ __device__ __forceinline__ void lz_pass(const LzArgs& a, const CUtensorMap* vmap
 #pragma unroll
           for (int c = 0; c < K; ++c) {
             const double* p = U + c * C::RN + ri;
-            const double s2 = fma(kd, p[0], -(p[-C::RW] + p[C::RW] + p[-1] + p[1]));
+            const double s2 = fma(kd, vq[c], -(p[-C::RW] + p[C::RW] + p[-1] + p[1]));
             w[c] = HITS ? s2 / h : s2;
           }
           if (q >= 2) {
 #pragma unroll
             for (int c = 0; c < K; ++c)
 #pragma unroll
-              for (int d = 0; d < K; ++d) w[c] = fma(-B1[d * C::BH * C::BW + bi], Bc[c * K + d], w[c]);
+              for (int d = 0; d < K; ++d) w[c] = fma(-B1[d * C::BH * C::BW + bi], rb(c * K + d), w[c]);
           }
 #pragma unroll
           for (int c = 0; c < K; ++c)
-            a.V[((size_t)(slotq * a.P + f) * K + c) * pstride + (size_t)gy * a.pitch + gx] = U[c * C::RN + ri];
+            a.V[((size_t)(slotq * a.P + f) * K + c) * pstride + (size_t)gy * a.pitch + gx] = vq[c];
         }
+        if constexpr (C::REGG) {
+          // N-weighted Gram of u = [V_q, W_q] at this pixel, packed upper triangle
+          double u[2 * K];
 #pragma unroll
-        for (int c = 0; c < K; ++c) U[(K + c) * C::RN + ri] = w[c];
-        if (HITS) hs[e] = h;
+          for (int c = 0; c < K; ++c) { u[c] = vq[c]; u[K + c] = w[c]; }
+          int idx = 0;
+#pragma unroll
+          for (int i = 0; i < 2 * K; ++i) {
+            const double hu = HITS ? h * u[i] : u[i];
+#pragma unroll
+            for (int j = i; j < 2 * K; ++j) { acc[idx] = fma(hu, u[j], acc[idx]); ++idx; }
+          }
+        } else {
+#pragma unroll
+          for (int c = 0; c < K; ++c) U[(K + c) * C::RN + ri] = w[c];
+          if (HITS) hs[e] = h;
+        }
       }
     }
     __syncthreads();
+    if (tid == 0 && t + C::STAGES < t1) issue(t + C::STAGES, s);  // the stage's boxes are free
 
-    // ---- N-weighted Gram of [V_q, W_q] (upper-triangle 4x4 blocks, one per thread group)
-    if (mode != LZ_REPLAY) {
-      const int job = tid % C::NJOB, sl = tid / C::NJOB;
-      if (sl < C::SL) {
-        int bi = 0, r = job;
-        while (r >= C::NB4 - bi) { r -= C::NB4 - bi; ++bi; }
-        const int bj = bi + r;
-        const double* ua = U + bi * 4 * C::RN;
-        const double* ub = U + bj * 4 * C::RN;
-        for (int px = sl; px < C::NPIX; px += C::SL) {
-          const int ly = px / C::TX, lx = px - ly * C::TX;
-          const int ri = (ly + 1) * C::RW + lx + 1;
-          double xa[4], yb[4];
+    // ---- K > 4: N-weighted Gram of [V_q, W_q] (upper-triangle 4x4 blocks, one per thread group)
+    if constexpr (!C::REGG) {
+      if (mode != LZ_REPLAY) {
+        const int job = tid % C::NJOB, sl = tid / C::NJOB;
+        if (sl < C::SL) {
+          int bi = 0, r = job;
+          while (r >= C::NB4 - bi) { r -= C::NB4 - bi; ++bi; }
+          const int bj = bi + r;
+          const double* ua = U + bi * 4 * C::RN;
+          const double* ub = U + bj * 4 * C::RN;
+          for (int px = sl; px < C::NPIX; px += C::SL) {
+            const int ly = px / C::TX, lx = px - ly * C::TX;
+            const int ri = (ly + 1) * C::RW + lx + 1;
+            double xa[4], yb[4];
 #pragma unroll
-          for (int j = 0; j < 4; ++j) { xa[j] = ua[j * C::RN + ri]; yb[j] = ub[j * C::RN + ri]; }
-          if (HITS) {
-            const double h = hs[px];
+            for (int j = 0; j < 4; ++j) { xa[j] = ua[j * C::RN + ri]; yb[j] = ub[j * C::RN + ri]; }
+            if (HITS) {
+              const double h = hs[px];
 #pragma unroll
-            for (int j = 0; j < 4; ++j) xa[j] *= h;
+              for (int j = 0; j < 4; ++j) xa[j] *= h;
+            }
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+#pragma unroll
+              for (int j = 0; j < 4; ++j) acc[i * 4 + j] = fma(xa[i], yb[j], acc[i * 4 + j]);
           }
-#pragma unroll
-          for (int i = 0; i < 4; ++i)
-#pragma unroll
-            for (int j = 0; j < 4; ++j) acc[i * 4 + j] = fma(xa[i], yb[j], acc[i * 4 + j]);
         }
       }
+      __syncthreads();  // U is free
     }
-    __syncthreads();  // U and the stage's boxes are free
-    if (tid == 0 && t + C::STAGES < t1) issue(t + C::STAGES, s);
   }
   if (mode != LZ_REPLAY && cur >= 0) lz_flush<K>(a, cur, acc, sm);
 }
@@ -395,12 +466,13 @@ __device__ void lz_reduce(const LzArgs& a, int q, const int* act, int nact, int 
     }
     if (lane < K) gp[lane] = __ldcg(a.gv + ((fc + q - 2) * K + warp) * K + lane);
   }
-  // CTAs whose chunk intersects the face's tiles: b_lo .. b_hi
-  int b_lo = (int)((f0 * ncta) / T);
-  while (b_lo > 0 && T * b_lo / ncta > f0) --b_lo;
-  while (T * (b_lo + 1) / ncta <= f0) ++b_lo;
-  int b_hi = b_lo;
-  while (b_hi + 1 < ncta && T * (b_hi + 1) / ncta < f1) ++b_hi;
+  // CTAs whose chunk [T b / ncta, T (b+1) / ncta) holds the face's first / last tile, and the chunk
+  // starts in between (empty chunks hold no partial)
+  const int b_lo = (int)(((f0 + 1) * ncta + T - 1) / T) - 1;
+  const int b_hi = (int)((f1 * ncta + T - 1) / T) - 1;
+  __shared__ long long cst[KCG_LZ_GRID_MAX + 1];
+  for (int b = b_lo + tid; b <= b_hi + 1; b += C::NT) cst[b - b_lo] = T * b / ncta;
+  __syncthreads();
   double* gam = sm + C::SC_GAM;
   double* grp = sm + C::SC_GRP;
   constexpr int NG = C::NT / C::NPART;
@@ -415,7 +487,7 @@ __device__ void lz_reduce(const LzArgs& a, int q, const int* act, int nact, int 
 #pragma unroll
         for (int u = 0; u < 8; ++u) {
           const int b = b0 + u * NG;
-          const bool ok = b <= b_hi && T * (b + 1) / ncta > T * b / ncta;
+          const bool ok = b <= b_hi && cst[b + 1 - b_lo] > cst[b - b_lo];
           v[u] = ok ? __ldcg(src + (size_t)b * C::NPART) : 0.0;
         }
 #pragma unroll
@@ -441,8 +513,9 @@ __device__ void lz_reduce(const LzArgs& a, int q, const int* act, int nact, int 
   double* B0 = X + K * K;
   double* res = sm + C::SC_RES;
   int* flag = reinterpret_cast<int*>(res + K);
-  auto G = [&](int i, int j) {  // symmetric Gram entry from the upper-triangle blocks
+  auto G = [&](int i, int j) {  // symmetric Gram entry (packed upper triangle, or 4x4 blocks)
     if (i > j) { const int t = i; i = j; j = t; }
+    if constexpr (C::REGG) return gam[i * (2 * K) - i * (i - 1) / 2 + (j - i)];
     const int bi = i >> 2, bj = j >> 2;
     const int job = bi * C::NB4 - bi * (bi - 1) / 2 + (bj - bi);
     return gam[job * 16 + (i & 3) * 4 + (j & 3)];
@@ -648,7 +721,7 @@ __global__ void __launch_bounds__(256, 1)
     lanczos_kernel(const __grid_constant__ LzArgs a, const __grid_constant__ CUtensorMap vmap) {
   using C = LzCfg<K>;
   extern __shared__ __align__(128) double sm[];
-  uint64_t* bar = reinterpret_cast<uint64_t*>(sm + C::DOUBLES);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sm + C::DOUBLES);  // [STAGES]
   __shared__ int act[64], its[64];
   __shared__ int nact_s, qmax_s;
   const int tid = threadIdx.x, cta = blockIdx.x, ncta = gridDim.x;
@@ -659,7 +732,7 @@ __global__ void __launch_bounds__(256, 1)
   }
   for (int e = tid; e < (C::KP - 2 * K) * C::RN; e += C::NT) sm[C::OFF_U + 2 * K * C::RN + e] = 0.0;
   __syncthreads();
-  uint32_t ph0 = 0, ph1 = 0;
+  uint32_t phbits = 0;  // mbarrier phase parity per stage
 
   // Lanczos passes (q = 0: B_0), one grid barrier before and one after the per-face reductions
   for (int q = 0;; ++q) {
@@ -674,7 +747,7 @@ __global__ void __launch_bounds__(256, 1)
     if (nact == 0) break;
     long long* tr = (KCG_TRACE && a.trace && q < KCG_TRACE_ITERS) ? a.trace + (size_t)q * KCG_TRACE_COLS : nullptr;
     if (tr && cta == 0 && tid == 0) tr[0] = globaltimer();
-    lz_pass<K, HITS>(a, &vmap, q, q == 0 ? LZ_GRAM0 : LZ_STEP, act, its, nact, sm, bar, ph0, ph1);
+    lz_pass<K, HITS>(a, &vmap, q, q == 0 ? LZ_GRAM0 : LZ_STEP, act, its, nact, sm, bar, phbits);
     if (tr && tid == 0 && 5 + cta < KCG_TRACE_COLS) tr[5 + cta] = globaltimer();
     fence_proxy_async_global();
     __threadfence();
@@ -719,7 +792,7 @@ __global__ void __launch_bounds__(256, 1)
       nact_s = n;
     }
     __syncthreads();
-    lz_pass<K, HITS>(a, &vmap, q, LZ_REPLAY, act, its, nact_s, sm, bar, ph0, ph1);
+    lz_pass<K, HITS>(a, &vmap, q, LZ_REPLAY, act, its, nact_s, sm, bar, phbits);
     fence_proxy_async_global();
     __threadfence();
     grid.sync();
