@@ -92,7 +92,7 @@ typedef struct {
   int history_cap;  /* per-iteration max relative residual recorded on device (0 = off)            */
   int lanczos_cap;  /* block-Lanczos route (sylvester_lanczos_solve): 0 = not provisioned; else the   */
                     /* most Lanczos steps a solve may take (coefficients H_i, B_i, eliminations kept  */
-                    /* on device: ~(5k^2 + k^3) * 8 bytes per step and patch); KCG_PRIOR_LAPLACIAN,    */
+                    /* on device: ~(5k^2 + k^3) * 8 bytes per step and patch); either prior (D2: k <= 4), */
                     /* no row slabs                                                                    */
   int lanczos_store;/* 1: keep the whole Lanczos basis V_1..V_cap in HBM (P*k*N*8*(lanczos_cap + 1)     */
                     /* bytes) and assemble M in one streaming pass; 0: the paper's memory-lean second  */

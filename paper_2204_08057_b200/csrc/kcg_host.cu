@@ -244,8 +244,8 @@ bool config_ok(const kcg_desc* d, std::string* why) {
     return false;
   }
   if (d->layout != KCG_LAYOUT_ROW_MAJOR && d->layout != KCG_LAYOUT_NESTED) { *why = "unknown layout"; return false; }
-  if (d->lanczos_cap > 0 && d->prior != KCG_PRIOR_LAPLACIAN) {
-    *why = "the block-Lanczos route (lanczos_cap > 0) is built for KCG_PRIOR_LAPLACIAN";
+  if (d->lanczos_cap > 0 && d->prior == KCG_PRIOR_D2 && d->n_comp > 4) {
+    *why = "the block-Lanczos route with KCG_PRIOR_D2 is built for n_comp <= 4 (halo-4 boxes)";
     return false;
   }
   if (d->precond != KCG_PRECOND_NONE && d->precond != KCG_PRECOND_BLOCK_JACOBI) { *why = "unknown precond"; return false; }
@@ -420,12 +420,13 @@ bool encode_xmap(CUtensorMap* m, double* base, int side, int rows, size_t planes
 }
 
 // TMA descriptor of the block-Lanczos slots [planes][side][pitch], box {64 + 4, TY + 4, K}.
-bool encode_lzmap(CUtensorMap* m, double* base, int side, int pitch, size_t planes, int K, std::string* why) {
+bool encode_lzmap(CUtensorMap* m, double* base, int side, int pitch, size_t planes, int K, bool d2, std::string* why) {
   auto enc = get_encode();
   if (!enc) { *why = "cuTensorMapEncodeTiled unavailable"; return false; }
   cuuint64_t dims[3] = {(cuuint64_t)side, (cuuint64_t)side, (cuuint64_t)planes};
   cuuint64_t strides[2] = {(cuuint64_t)pitch * 8, (cuuint64_t)pitch * side * 8};
-  cuuint32_t box[3] = {(cuuint32_t)(KCG_TX + 4), (cuuint32_t)(kcg::lz_tile_y(K) + 4), (cuuint32_t)K};
+  const int hb = kcg::lz_halo(d2);
+  cuuint32_t box[3] = {(cuuint32_t)(KCG_TX + 2 * hb), (cuuint32_t)(kcg::lz_tile_y(K) + 2 * hb), (cuuint32_t)K};
   cuuint32_t es[3] = {1, 1, 1};
   CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, base, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
                    CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
@@ -733,7 +734,7 @@ kcg_status lanczos_impl(kcg_ctx* c, const double* Y_in, double* mu_out, bool hos
 
   CK(cudaEventRecord(c->ev[0], s), "event");
   if (host_io) CK(cudaMemcpyAsync(R.Y_stage, Y_in, (size_t)P * n * N * 8, cudaMemcpyHostToDevice, s), "H2D Y");
-  SlabGeom g{c->side, c->side, 0, c->pitch, 0, 0, c->d.layout == KCG_LAYOUT_NESTED, false};
+  SlabGeom g{c->side, c->side, 0, c->pitch, 0, 0, c->d.layout == KCG_LAYOUT_NESTED, c->d.prior == KCG_PRIOR_D2};
   CK(kcg::launch_rhs(k, s, Yr, R.E_lz, nullptr, R.lz_V, nullptr, nullptr, P, n, g), "lanczos rhs kernel");
   CK(cudaMemsetAsync(R.lz_st, 0, P * sizeof(kcg::LzState), s), "memset lanczos state");
   CK(cudaEventRecord(c->ev[1], s), "event");
@@ -761,7 +762,8 @@ kcg_status lanczos_impl(kcg_ctx* c, const double* Y_in, double* mu_out, bool hos
   a.store = c->d.lanczos_store;
   a.tol = tol;
   a.trace = R.trace;
-  CK(kcg::launch_lanczos(k, R.hits != nullptr, s, a, R.lz_map, c->grid_lz, c->smem_lz), "lanczos kernel");
+  CK(kcg::launch_lanczos(k, R.hits != nullptr, c->d.prior == KCG_PRIOR_D2, s, a, R.lz_map, c->grid_lz, c->smem_lz),
+     "lanczos kernel");
   if (a.store) CK(kcg::launch_lz_assemble(k, s, a), "lanczos assembly kernel");
   CK(cudaEventRecord(c->ev[2], s), "event");
   CK(kcg::launch_resid(k, s, R.params_kron, mur, Yr, R.E_kron, R.hits, R.resid_partials, R.resid_out, P, n,
@@ -1008,10 +1010,10 @@ kcg_status create_impl(const kcg_desc* d, const kcg_slab* sl, const double* A_ho
     RankState& R = c->R[0];
     CKC(cudaMemcpyAsync(R.lz_prm, lf.data(), P * sizeof(kcg::LzFace), cudaMemcpyHostToDevice, c->stream), "H2D");
     CKC(cudaMemcpyAsync(R.E_lz, El.data(), El.size() * 8, cudaMemcpyHostToDevice, c->stream), "H2D");
-    if (!encode_lzmap(&R.lz_map, R.lz_V, c->side, c->pitch, (size_t)c->L.lz_slots * P * k, k, &why))
+    if (!encode_lzmap(&R.lz_map, R.lz_V, c->side, c->pitch, (size_t)c->L.lz_slots * P * k, k, d2, &why))
       return fail(KCG_E_CUDA, why);
     int mgl = 0;
-    CKC(kcg::lz_kernel_config(k, hits_dev != nullptr, &mgl, &c->smem_lz), "lanczos kernel config");
+    CKC(kcg::lz_kernel_config(k, hits_dev != nullptr, d2, &mgl, &c->smem_lz), "lanczos kernel config");
     c->grid_lz = std::max(1, mgl);
     c->tiles_x_lz = (c->side + KCG_TX - 1) / KCG_TX;
     c->tiles_y_lz = (c->side + kcg::lz_tile_y(k) - 1) / kcg::lz_tile_y(k);

@@ -246,14 +246,16 @@ int apply_tiles_per_sys(int rows, int side);
 // block-Lanczos (kcg_lanczos_*.cu): one cooperative launch runs the Lanczos passes, the residual
 // estimate, the coefficients and (two-pass mode) the replay that assembles M; store mode follows it
 // with lz_assemble.
-cudaError_t lz_kernel_config(int K, bool hits, int* max_grid, size_t* smem);
-cudaError_t launch_lanczos(int K, bool hits, cudaStream_t s, const LzArgs& a, const CUtensorMap& vmap, int grid,
-                           size_t smem);
+cudaError_t lz_kernel_config(int K, bool hits, bool d2, int* max_grid, size_t* smem);
+cudaError_t launch_lanczos(int K, bool hits, bool d2, cudaStream_t s, const LzArgs& a, const CUtensorMap& vmap,
+                           int grid, size_t smem);
+__host__ __device__ constexpr int lz_halo(bool d2) { return d2 ? 4 : 2; }
 cudaError_t launch_lz_assemble(int K, cudaStream_t s, const LzArgs& a);
 template <int K>
 struct LzEntry {  // defined in kcg_lanczos.cuh, instantiated per K in kcg_lanczos_{a,b}.cu
-  static cudaError_t config(bool hits, int* max_grid, size_t* smem);
-  static cudaError_t launch(bool hits, cudaStream_t s, const LzArgs& a, const CUtensorMap& vmap, int grid, size_t smem);
+  static cudaError_t config(bool hits, bool d2, int* max_grid, size_t* smem);
+  static cudaError_t launch(bool hits, bool d2, cudaStream_t s, const LzArgs& a, const CUtensorMap& vmap, int grid,
+                            size_t smem);
   static cudaError_t assemble(cudaStream_t s, const LzArgs& a);
 };
 

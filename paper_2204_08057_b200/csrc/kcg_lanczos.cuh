@@ -24,15 +24,16 @@
 
 namespace kcg {
 
-template <int K>
+template <int K, bool D2 = false>
 struct LzCfg {
   static constexpr int TX = KCG_TX;
   static constexpr int TY = lz_tile_y(K);
-  static constexpr int HB = 2;                         // box halo: V_{i-1} is needed on the tile + 2 ring
+  static constexpr int HB = D2 ? 4 : 2;                // box halo: V_{i-1} is needed on the tile + 2 RR ring
+  static constexpr int RR = D2 ? 2 : 1;                // ring of V_i (the operator's radius)
   static constexpr int BW = TX + 2 * HB, BH = TY + 2 * HB;
-  static constexpr int RW = TX + 2, RH = TY + 2, RN = RW * RH;  // tile + 1 ring (V_i region)
+  static constexpr int RW = TX + 2 * RR, RH = TY + 2 * RR, RN = RW * RH;  // V_i region
   static constexpr int BOX = K * BH * BW;
-  static constexpr int STAGES = K <= 4 ? 3 : (K == 5 ? 2 : 1);  // TMA tiles in flight
+  static constexpr int STAGES = D2 ? 2 : (K <= 4 ? 3 : (K == 5 ? 2 : 1));  // TMA tiles in flight
   static constexpr int KP = (2 * K + 3) / 4 * 4;      // Gram rows [V, W] padded to 4
   static constexpr int NB4 = KP / 4;
   static constexpr int NJOB = NB4 * (NB4 + 1) / 2;    // upper-triangle 4x4 blocks of the Gram
@@ -42,9 +43,13 @@ struct LzCfg {
   static constexpr int NT = 256;
   static constexpr int SL = NT / NJOB;                // pixel slices per Gram block
   static constexpr int NPIX = TX * TY;
-  static constexpr int OFF_U = STAGES * 2 * BOX;      // U = [V_i (K planes); W_i (K); 0 pad] on the ring grid
-  static constexpr int OFF_HS = OFF_U + KP * RN;      // hits of the tile
-  static constexpr int OFF_MAT = OFF_HS + NPIX;       // Hp, Bp, Ri, Bc, Z (K x K each)
+  static constexpr int UPL = REGG ? K : KP;           // U = [V_i; (K > 4: W_i; 0 pad)] on the V_i region
+  static constexpr int DW = TX + 6, DH = TY + 6;      // D2: D V on the tile + 3 ring (step A), + 1 (step B)
+  static constexpr int DVN = D2 ? K * DW * DH : 0;
+  static constexpr int OFF_U = STAGES * 2 * BOX;
+  static constexpr int OFF_HS = OFF_U + UPL * RN;     // hits of the tile (K > 4)
+  static constexpr int OFF_DV = OFF_HS + NPIX;
+  static constexpr int OFF_MAT = OFF_DV + DVN;        // P1, P2, Ri, Bc, Z (K x K each)
   static constexpr int OFF_RED = OFF_MAT + 5 * K * K; // flush scratch [NT][4]
   static constexpr int DOUBLES = OFF_RED + NT * 4;
   static constexpr size_t SMEM = (size_t)DOUBLES * 8 + 64;  // + mbarriers
@@ -52,11 +57,11 @@ struct LzCfg {
   static constexpr int SC_GAM = 0;                          // raw Gram [NPART]
   static constexpr int SC_GRP = SC_GAM + NPART;              // group sums [NT]
   static constexpr int SC_M = SC_GRP + NT;                   // Gv, H, C0, T1, C, R, X(Rinv), B0 [8][K*K]
-  static constexpr int SC_W = SC_M + 8 * K * K;              // per-shift warp scratch [K][8 K*K]
+  static constexpr int SC_W = SC_M + 8 * K * K;              // per-shift warp scratch [K][9 K*K]
   static constexpr int SC_RES = SC_W + K * 9 * K * K;        // residual per shift [K] + flags
   static constexpr int SC_END = SC_RES + 2 * K + 8;
   static_assert(SC_END <= OFF_U, "reducer scratch exceeds the box area");
-  static_assert(SMEM <= 227 * 1024, "shared memory budget");
+  static_assert(SMEM + 6 * 1024 <= 227 * 1024, "shared memory budget (dynamic + static)");
 };
 
 enum { LZ_GRAM0 = 0, LZ_STEP = 1, LZ_REPLAY = 2 };
@@ -170,10 +175,11 @@ __device__ __forceinline__ void lz_flush(const LzArgs& a, int f, double (&acc)[L
 // mode LZ_GRAM0 (q = 0): Gram of Y^.  LZ_STEP (q = i >= 1): Lanczos step i.  LZ_REPLAY (q >= 1):
 // rebuild V_q and accumulate M += V_q G_q.  The active faces act[0..nact) are split into contiguous
 // tile chunks, one per CTA.
-template <int K, bool HITS>
+template <int K, bool HITS, bool D2>
 __device__ __forceinline__ void lz_pass(const LzArgs& a, const CUtensorMap* vmap, int q, int mode, const int* act,
                                         const int* its, int nact, double* sm, uint64_t* bar, uint32_t& phbits) {
-  using C = LzCfg<K>;
+  using C = LzCfg<K, D2>;
+  double* Dv = sm + C::OFF_DV;  // D2 scratch
   const int tid = threadIdx.x, cta = blockIdx.x, ncta = gridDim.x;
   const long long T = (long long)nact * a.tps;
   const long long t0 = T * cta / ncta, t1 = T * (cta + 1) / ncta;
@@ -256,7 +262,24 @@ __device__ __forceinline__ void lz_pass(const LzArgs& a, const CUtensorMap* vmap
     const double* B1 = sm + s * 2 * C::BOX;
     const double* B2 = B1 + C::BOX;
 
-    // ---- step A: V_q on the tile + 1 ring (zero outside the face: free boundary, reading R2)
+    // ---- D2: D V_{q-1} on the tile + 3 ring (D v := 0 outside the face; D = -L)
+    if constexpr (D2) {
+      if (mode != LZ_GRAM0 && q >= 2) {
+        for (int e = tid; e < K * C::DW * C::DH; e += C::NT) {
+          const int c = e / (C::DW * C::DH), r = e - c * (C::DW * C::DH);
+          const int dy = r / C::DW, dx = r - dy * C::DW;
+          const int gy = y0 - 3 + dy, gx = x0 - 3 + dx;
+          double d = 0.0;
+          if (gy >= 0 && gy < side && gx >= 0 && gx < side) {
+            const double* p = B1 + c * C::BH * C::BW + (dy + C::HB - 3) * C::BW + dx + C::HB - 3;
+            d = (p[-C::BW] + p[C::BW] + p[-1] + p[1]) - (double)lz_deg(gy, gx, side) * p[0];
+          }
+          Dv[e] = d;
+        }
+        __syncthreads();
+      }
+    }
+    // ---- step A: V_q on the tile + RR ring (zero outside the face: free boundary, reading R2)
     {
       // this tile's step-A matrices: registers for K <= 4, shared memory (broadcast) above
       constexpr int NR = C::REGG ? K * K : 1;
@@ -270,8 +293,8 @@ __device__ __forceinline__ void lz_pass(const LzArgs& a, const CUtensorMap* vmap
       auto r2 = [&](int i) { if constexpr (C::REGG) return r2v[i]; else return P2m[i]; };
       for (int e = tid; e < C::RN; e += C::NT) {
         const int ry = e / C::RW, rx = e - ry * C::RW;
-        const int gy = y0 - 1 + ry, gx = x0 - 1 + rx;
-        const int bi = (ry + 1) * C::BW + rx + 1;
+        const int gy = y0 - C::RR + ry, gx = x0 - C::RR + rx;
+        const int bi = (ry + C::HB - C::RR) * C::BW + rx + C::HB - C::RR;
         double v[K];
         if (gy < 0 || gy >= side || gx < 0 || gx >= side) {
 #pragma unroll
@@ -291,8 +314,14 @@ __device__ __forceinline__ void lz_pass(const LzArgs& a, const CUtensorMap* vmap
             const double h = HITS ? __ldg(hp + (size_t)gy * side + gx) : 1.0;
 #pragma unroll
             for (int c = 0; c < K; ++c) {
-              const double* p = B1 + c * C::BH * C::BW + bi;
-              const double s2 = fma(kd, v1[c], -(p[-C::BW] + p[C::BW] + p[-1] + p[1]));
+              double s2;
+              if constexpr (D2) {  // Q0 v = D (D v) + kappa2 v
+                const double* d = Dv + c * C::DW * C::DH + (ry + 3 - C::RR) * C::DW + rx + 3 - C::RR;
+                s2 = fma(kap, v1[c], (d[-C::DW] + d[C::DW] + d[-1] + d[1]) - (kd - kap) * d[0]);
+              } else {             // Q0 v = (kappa2 + deg) v - sum_nbr v
+                const double* p = B1 + c * C::BH * C::BW + bi;
+                s2 = fma(kd, v1[c], -(p[-C::BW] + p[C::BW] + p[-1] + p[1]));
+              }
               w[c] = HITS ? s2 / h : s2;
             }
           }
@@ -318,6 +347,24 @@ __device__ __forceinline__ void lz_pass(const LzArgs& a, const CUtensorMap* vmap
     }
     __syncthreads();
 
+    // ---- D2: D V_q on the tile + 1 ring
+    if constexpr (D2) {
+      if (mode == LZ_STEP) {
+        constexpr int W1 = C::TX + 2, H1 = C::TY + 2;
+        for (int e = tid; e < K * W1 * H1; e += C::NT) {
+          const int c = e / (W1 * H1), r = e - c * (W1 * H1);
+          const int dy = r / W1, dx = r - dy * W1;
+          const int gy = y0 - 1 + dy, gx = x0 - 1 + dx;
+          double d = 0.0;
+          if (gy >= 0 && gy < side && gx >= 0 && gx < side) {
+            const double* p = U + c * C::RN + (dy + C::RR - 1) * C::RW + dx + C::RR - 1;
+            d = (p[-C::RW] + p[C::RW] + p[-1] + p[1]) - (double)lz_deg(gy, gx, side) * p[0];
+          }
+          Dv[e] = d;
+        }
+        __syncthreads();
+      }
+    }
     // ---- step B: W_q on the tile (or the replay's M update); store V_q; Gram (K <= 4: in registers)
     {
       constexpr int NRB = C::REGG ? K * K : 1;
@@ -331,8 +378,8 @@ __device__ __forceinline__ void lz_pass(const LzArgs& a, const CUtensorMap* vmap
       for (int e = tid; e < C::NPIX; e += C::NT) {
         const int ly = e / C::TX, lx = e - ly * C::TX;
         const int gy = y0 + ly, gx = x0 + lx;
-        const int ri = (ly + 1) * C::RW + lx + 1;
-        const int bi = (ly + 2) * C::BW + lx + 2;
+        const int ri = (ly + C::RR) * C::RW + lx + C::RR;
+        const int bi = (ly + C::HB) * C::BW + lx + C::HB;
         const bool in = gy < side && gx < side;
         if (mode == LZ_REPLAY) {
           if (in) {
@@ -370,8 +417,15 @@ __device__ __forceinline__ void lz_pass(const LzArgs& a, const CUtensorMap* vmap
           if (HITS) h = __ldg(hp + (size_t)gy * side + gx);
 #pragma unroll
           for (int c = 0; c < K; ++c) {
-            const double* p = U + c * C::RN + ri;
-            const double s2 = fma(kd, vq[c], -(p[-C::RW] + p[C::RW] + p[-1] + p[1]));
+            double s2;
+            if constexpr (D2) {
+              constexpr int W1 = C::TX + 2, H1 = C::TY + 2;
+              const double* d = Dv + c * W1 * H1 + (ly + 1) * W1 + lx + 1;
+              s2 = fma(kap, vq[c], (d[-W1] + d[W1] + d[-1] + d[1]) - (kd - kap) * d[0]);
+            } else {
+              const double* p = U + c * C::RN + ri;
+              s2 = fma(kd, vq[c], -(p[-C::RW] + p[C::RW] + p[-1] + p[1]));
+            }
             w[c] = HITS ? s2 / h : s2;
           }
           if (q >= 2) {
@@ -418,7 +472,7 @@ __device__ __forceinline__ void lz_pass(const LzArgs& a, const CUtensorMap* vmap
           const double* ub = U + bj * 4 * C::RN;
           for (int px = sl; px < C::NPIX; px += C::SL) {
             const int ly = px / C::TX, lx = px - ly * C::TX;
-            const int ri = (ly + 1) * C::RW + lx + 1;
+            const int ri = (ly + C::RR) * C::RW + lx + C::RR;
             double xa[4], yb[4];
 #pragma unroll
             for (int j = 0; j < 4; ++j) { xa[j] = ua[j * C::RN + ri]; yb[j] = ub[j * C::RN + ri]; }
@@ -716,10 +770,10 @@ __device__ void lz_coeffs(const LzArgs& a, int f, double* sm) {
 }
 
 // ------------------------------------------------------------------------- the persistent kernel
-template <int K, bool HITS>
+template <int K, bool HITS, bool D2>
 __global__ void __launch_bounds__(256, 1)
     lanczos_kernel(const __grid_constant__ LzArgs a, const __grid_constant__ CUtensorMap vmap) {
-  using C = LzCfg<K>;
+  using C = LzCfg<K, D2>;
   extern __shared__ __align__(128) double sm[];
   uint64_t* bar = reinterpret_cast<uint64_t*>(sm + C::DOUBLES);  // [STAGES]
   __shared__ int act[64], its[64];
@@ -730,7 +784,8 @@ __global__ void __launch_bounds__(256, 1)
     for (int s = 0; s < C::STAGES; ++s) mbar_init(&bar[s], 1);
     fence_mbar_init();
   }
-  for (int e = tid; e < (C::KP - 2 * K) * C::RN; e += C::NT) sm[C::OFF_U + 2 * K * C::RN + e] = 0.0;
+  if constexpr (!C::REGG)
+    for (int e = tid; e < (C::KP - 2 * K) * C::RN; e += C::NT) sm[C::OFF_U + 2 * K * C::RN + e] = 0.0;
   __syncthreads();
   uint32_t phbits = 0;  // mbarrier phase parity per stage
 
@@ -747,7 +802,7 @@ __global__ void __launch_bounds__(256, 1)
     if (nact == 0) break;
     long long* tr = (KCG_TRACE && a.trace && q < KCG_TRACE_ITERS) ? a.trace + (size_t)q * KCG_TRACE_COLS : nullptr;
     if (tr && cta == 0 && tid == 0) tr[0] = globaltimer();
-    lz_pass<K, HITS>(a, &vmap, q, q == 0 ? LZ_GRAM0 : LZ_STEP, act, its, nact, sm, bar, phbits);
+    lz_pass<K, HITS, D2>(a, &vmap, q, q == 0 ? LZ_GRAM0 : LZ_STEP, act, its, nact, sm, bar, phbits);
     if (tr && tid == 0 && 5 + cta < KCG_TRACE_COLS) tr[5 + cta] = globaltimer();
     fence_proxy_async_global();
     __threadfence();
@@ -792,7 +847,7 @@ __global__ void __launch_bounds__(256, 1)
       nact_s = n;
     }
     __syncthreads();
-    lz_pass<K, HITS>(a, &vmap, q, LZ_REPLAY, act, its, nact_s, sm, bar, phbits);
+    lz_pass<K, HITS, D2>(a, &vmap, q, LZ_REPLAY, act, its, nact_s, sm, bar, phbits);
     fence_proxy_async_global();
     __threadfence();
     grid.sync();
@@ -846,27 +901,41 @@ __global__ void __launch_bounds__(256) lz_assemble_kernel(const LzArgs a) {
 }
 
 // ------------------------------------------------------------------------- host entry points
+template <int K, bool D2>
+const void* lz_kernel_ptr(bool hits) {
+  return hits ? (const void*)lanczos_kernel<K, true, D2> : (const void*)lanczos_kernel<K, false, D2>;
+}
 template <int K>
-cudaError_t LzEntry<K>::config(bool hits, int* max_grid, size_t* smem) {
-  using C = LzCfg<K>;
-  const void* f = hits ? (const void*)lanczos_kernel<K, true> : (const void*)lanczos_kernel<K, false>;
-  cudaError_t e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM);
+const void* lz_kernel_sel(bool hits, bool d2) {
+  if constexpr (K <= 4) {
+    if (d2) return lz_kernel_ptr<K, true>(hits);
+  }
+  return d2 ? nullptr : lz_kernel_ptr<K, false>(hits);
+}
+
+template <int K>
+cudaError_t LzEntry<K>::config(bool hits, bool d2, int* max_grid, size_t* smem) {
+  const void* f = lz_kernel_sel<K>(hits, d2);
+  if (!f) return cudaErrorInvalidValue;  // D2 is built for K <= 4
+  const size_t sm = d2 ? LzCfg<K, (K <= 4)>::SMEM : LzCfg<K, false>::SMEM;
+  cudaError_t e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
   if (e != cudaSuccess) return e;
   int dev = 0, nsm = 0, per = 0;
   if ((e = cudaGetDevice(&dev)) != cudaSuccess) return e;
   if ((e = cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev)) != cudaSuccess) return e;
-  if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, f, C::NT, C::SMEM)) != cudaSuccess) return e;
+  if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, f, 256, sm)) != cudaSuccess) return e;
   *max_grid = std::min(per * nsm, KCG_LZ_GRID_MAX);
-  *smem = C::SMEM;
+  *smem = sm;
   return cudaSuccess;
 }
 
 template <int K>
-cudaError_t LzEntry<K>::launch(bool hits, cudaStream_t s, const LzArgs& a, const CUtensorMap& vmap, int grid,
+cudaError_t LzEntry<K>::launch(bool hits, bool d2, cudaStream_t s, const LzArgs& a, const CUtensorMap& vmap, int grid,
                                size_t smem) {
   void* args[2] = {(void*)&a, (void*)&vmap};
-  const void* f = hits ? (const void*)lanczos_kernel<K, true> : (const void*)lanczos_kernel<K, false>;
-  return cudaLaunchCooperativeKernel(f, dim3(grid), dim3(LzCfg<K>::NT), args, smem, s);
+  const void* f = lz_kernel_sel<K>(hits, d2);
+  if (!f) return cudaErrorInvalidValue;
+  return cudaLaunchCooperativeKernel(f, dim3(grid), dim3(256), args, smem, s);
 }
 
 template <int K>

@@ -24,12 +24,12 @@ extern template struct LzEntry<8>;
     default: return cudaErrorInvalidValue; \
   }
 
-cudaError_t lz_kernel_config(int K, bool hits, int* max_grid, size_t* smem) {
-  KCG_LZ_DISPATCH(config(hits, max_grid, smem))
+cudaError_t lz_kernel_config(int K, bool hits, bool d2, int* max_grid, size_t* smem) {
+  KCG_LZ_DISPATCH(config(hits, d2, max_grid, smem))
 }
-cudaError_t launch_lanczos(int K, bool hits, cudaStream_t s, const LzArgs& a, const CUtensorMap& vmap, int grid,
-                           size_t smem) {
-  KCG_LZ_DISPATCH(launch(hits, s, a, vmap, grid, smem))
+cudaError_t launch_lanczos(int K, bool hits, bool d2, cudaStream_t s, const LzArgs& a, const CUtensorMap& vmap,
+                           int grid, size_t smem) {
+  KCG_LZ_DISPATCH(launch(hits, d2, s, a, vmap, grid, smem))
 }
 cudaError_t launch_lz_assemble(int K, cudaStream_t s, const LzArgs& a) { KCG_LZ_DISPATCH(assemble(s, a)) }
 }  // namespace kcg

@@ -171,3 +171,18 @@ def test_lanczos_fullsky_sample_faces_vs_exact():
         assert rel(mu[i], exact.problem_dct_exact(p)) <= 1e-8
         if gold:
             assert abs(rep["iterations_per"][i] - gold[fi]) <= 2
+
+
+@pytest.mark.parametrize("k,hits", [(1, None), (2, "random"), (3, None), (4, "random")])
+def test_lanczos_d2_prior_vs_oracle(k, hits):
+    """The paper's operator N_h^{-1} D^2 (+ kappa2), radius 2: halo-4 boxes, D V formed in shared
+    memory on the tile + 3 ring (step A) and + 1 ring (step B)."""
+    ps = [make_patch(6, 9, k, seed=300 + 11 * k + s, tau="loguniform", prior="d2", hits=hits) for s in range(2)]
+    _check(ps, prior="d2")
+
+
+def test_lanczos_d2_planck_vs_exact():
+    ps = make_config("planck", prior="d2")
+    ctx, Y, mu, rep = _run(ps, cap=300, store=True, prior="d2")
+    assert rep["converged"]
+    assert rel(mu[0], exact.problem_dct_exact(ps[0])) <= 1e-8

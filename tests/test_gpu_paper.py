@@ -1,0 +1,70 @@
+"""GPU parity on the paper's own workload: App. B physical mixing matrix and
+printed noise precisions, phi = 1, Q0 = D^2 with kappa2 = 0, non-uniform hits,
+HEALPix NESTED pixel order -- all three routes through the C ABI against the oracle (assembled in
+NESTED numbering) and the direct sparse solve.
+
+cond(G) ~ 1e4-1e5 here (T ~ 1e6-3e7 against D^2), so CG iterates at tol 1e-10 sit up to cond * tol
+from the exact solution; CG parity is checked on the residual, the exact error bound and the
+oracle's iteration count, the Sylvester routes (well-conditioned shifted systems) to 1e-8."""
+
+import numpy as np
+import pytest
+import scipy.sparse.linalg as ssl
+
+from gpu_util import have_gpu, rel
+from oracle import cg, model
+from synth.physics import make_paper_patch
+from synth.problems import stack
+
+pytestmark = [pytest.mark.gpu, pytest.mark.skipif(not have_gpu(), reason="needs a CUDA GPU")]
+TOL = 1e-10
+
+
+def _ctx(ps, **kw):
+    import torch
+    from paper_2204_08057_b200 import build
+    build.build()
+    from paper_2204_08057_b200.kroncg import KronCG
+    st = stack(ps)
+    L = ps[0].level
+    nest = lambda a: model.to_layout(L, a, "nested").reshape(np.shape(a))
+    ctx = KronCG(L, st["A"], st["noise_prec"], st["tau"], st["kappa2"],
+                 hits=torch.from_numpy(nest(st["hits"])).cuda(), layout="nested", prior="d2", **kw)
+    return ctx, torch.from_numpy(nest(st["Y"])).cuda()
+
+
+@pytest.mark.parametrize("level", [5, 7])
+def test_paper_workload_kron_and_sylvester(level):
+    ps = [make_paper_patch(level, seed=200 + s) for s in range(3)]
+    ctx, Y = _ctx(ps)
+    mu, rep = ctx.solve(Y, tol=TOL)
+    mu = mu.cpu().numpy()
+    smu, srep = ctx.sylvester(Y, tol=TOL)
+    smu = smu.cpu().numpy()
+    assert rep["converged"] and srep["converged"]
+    for i, p in enumerate(ps):
+        G, b = model.problem_system(p, layout="nested")
+        ref = ssl.spsolve(G.tocsc(), b)
+        o = cg.cg_hs(G, b, tol=TOL)
+        x = mu[i].reshape(-1)
+        assert np.linalg.norm(G @ x - b) <= 5e-10 * np.linalg.norm(b)
+        assert rel(x, ref) <= 1e-5
+        assert abs(rep["iterations_per"][i] - o.iterations) <= max(2, o.iterations // 20)
+        assert rel(smu[i].reshape(-1), ref) <= 1e-8
+
+
+@pytest.mark.parametrize("store", [False, True])
+def test_paper_workload_block_lanczos(store):
+    """The paper's headline solver (Alg. SylvSolver) on the paper's operator and data model."""
+    from oracle import lanczos
+    ps = [make_paper_patch(6, seed=210 + s) for s in range(3)]
+    ctx, Y = _ctx(ps, lanczos_cap=64, lanczos_store=store)
+    mu, rep = ctx.lanczos(Y, tol=TOL)
+    mu = mu.cpu().numpy()
+    assert rep["converged"]
+    for i, p in enumerate(ps):
+        G, b = model.problem_system(p, layout="nested")
+        ref = ssl.spsolve(G.tocsc(), b)
+        assert rel(mu[i].reshape(-1), ref) <= 1e-8
+        o = lanczos.problem_solve(p, tol=TOL)
+        assert abs(rep["iterations_per"][i] - o.iterations) <= 1
