@@ -282,6 +282,36 @@ def _lanczos_leg(problems, st, dev, timed, args):
     return out
 
 
+def _paper_leg(dev, timed, args, level=10, faces=12):
+    """The paper's own workload on the full sky: App. B physical A and printed T,
+    phi = 1, Q0 = D^2 with kappa2 = 0, random hits 1..4, HEALPix NESTED order, 12 faces at level 10
+    (seeds 400..411), through all three routes (inputs resident)."""
+    import torch
+    from paper_2204_08057_b200.kroncg import KronCG
+    from synth.physics import make_paper_patch, nested_order
+    from synth.problems import stack
+    ps = [make_paper_patch(level, seed=400 + f) for f in range(faces)]
+    st = stack(ps)
+    hits = torch.from_numpy(nested_order(st["hits"])).to(dev)
+    Y = torch.from_numpy(nested_order(st["Y"])).to(dev)
+    ctx = KronCG(level, st["A"], st["noise_prec"], st["tau"], st["kappa2"], hits=hits, device=dev,
+                 layout="nested", prior="d2", lanczos_cap=64, lanczos_store=True)
+    mu = torch.empty(ctx.shape_mu, dtype=torch.float64, device=dev)
+    out = {"workload": f"paper: App. B A and T, phi = 1, D^2 prior kappa2 = 0, hits 1..4, NESTED; "
+                       f"{faces} faces, level {level}", "unit": "full-sky solves/s"}
+    for name, fn in (("kron", ctx.solve), ("sylvester", ctx.sylvester), ("lanczos", ctx.lanczos)):
+        call = lambda: fn(Y, mu, tol=TOL)[1]
+        r = call()
+        assert r["converged"], (name, r["status_name"])
+        t, reps = timed(call, args.steps)
+        out[name] = {"value": len(reps) / t, "ms_per_step": t / len(reps) * 1e3,
+                     "iterations_per_system": reps[-1]["iterations_per"],
+                     "true_rel_residual": reps[-1]["rel_residual_true"]}
+    del ctx, Y, mu, hits
+    torch.cuda.empty_cache()
+    return out
+
+
 def run_b200(args):
     import torch
     import torch.distributed as dist
@@ -362,6 +392,9 @@ def run_b200(args):
     lz = None
     if g == 1 and not args.no_lanczos:
         lz = _lanczos_leg(problems, st, dev, timed, args)
+    paper = None
+    if world == 1 and not args.no_paper:
+        paper = _paper_leg(dev, timed, args)
 
     def agg(reps_, t):
         # whole-job numbers: gather per-rank sums
@@ -444,6 +477,8 @@ def run_b200(args):
     }
     if lz is not None:
         line["lanczos"] = lz
+    if paper is not None:
+        line["paper_workload"] = paper
     if world == 1 and not args.no_slab_probe:
         line["slab_emulation"] = _slab_probe(dev)
     if world == 1 and not args.no_cpu_baseline:
@@ -467,6 +502,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-slab-probe", action="store_true")
     ap.add_argument("--no-lanczos", action="store_true", help="skip the block-Lanczos (Alg. SylvSolver) leg")
+    ap.add_argument("--no-paper", action="store_true", help="skip the paper-workload leg (App. B physics, D^2)")
     ap.add_argument("--lanczos-cap", type=int, default=128,
                     help="Lanczos steps provisioned (HBM-resident basis: P k N 8 (cap + 1) bytes)")
     ap.add_argument("--ref-iters", type=int, default=8, help="oracle CG iterations per reference step")

@@ -157,6 +157,23 @@ KCG_API kcg_status sylvester_lanczos_solve(kcg_ctx* ctx, const double* Y_dev, do
 KCG_API kcg_status sylvester_lanczos_solve_host(kcg_ctx* ctx, const double* Y_host, double* mu_host, double tol,
                                         int max_iter, kcg_report* report);
 
+/* Many right-hand sides / parameter sweeps: G x = b for a GIVEN b_dev
+ * [P][k][N] (user layout; each patch of the context is one system -- P copies of one parameter set
+ * make P right-hand sides of one operator, P parameter sets one sweep), CG route, x0 = 0, stop on
+ * ||r|| <= tol ||b||.  x_dev [P][k][N].  No row slabs (KCG_E_CONFIG).                          */
+KCG_API kcg_status kron_cg_solve_b(kcg_ctx* ctx, const double* b_dev, double* x_dev, double tol, int max_iter,
+                           kcg_report* report);
+
+/* Posterior variances diag(Q^{-1}) = diag(G^{-1}) ("of most importance ... the main
+ * diagonal") by Hutchinson's estimator with n_probes Rademacher probes:
+ *   var = (1/s) sum_i z_i (.) G^{-1} z_i,   z_i[p][c][j] = +1 or -1 = sign bit of
+ *   splitmix64(splitmix64(seed) + ((i P + p) k + c) N + j)   (j = the pixel's user-layout index)
+ * -- an unbiased estimate; Var(var_j) = (1/s) sum_{l != j} (G^{-1})_{jl}^2.  Each probe is one batched
+ * CG solve (kron_cg_solve_b) of all patches to tol.  var_dev [P][k][N]; scratch_dev 2 P k N doubles
+ * (caller-owned).  report aggregates the probes (iterations = max, times and bytes summed).      */
+KCG_API kcg_status posterior_variance(kcg_ctx* ctx, int n_probes, unsigned long long seed, double* var_dev,
+                              double* scratch_dev, double tol, int max_iter, kcg_report* report);
+
 /* Same as above with HOST buffers: copies Y in and mu out through the context's staging buffers
  * (desc.host_staging = 1), copies included in report->wall_time_s.                            */
 KCG_API kcg_status kron_cg_solve_host(kcg_ctx* ctx, const double* Y_host, double* mu_host, double tol,

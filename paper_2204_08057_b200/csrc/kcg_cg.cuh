@@ -102,6 +102,7 @@ __device__ __forceinline__ uint32_t nest_of(uint32_t x, uint32_t y) { return par
 
 // --------------------------------------------------------------------------- rhs
 // b[p][c][j] = h_j sum_f Y[p][f][j] E[p][f][c];  r0 = b (internal pitch), p0 = 0, x = 0.
+// E == nullptr (b given, kron_cg_solve_b): Y holds b itself, [p][K][j] (n == K), copied as is.
 template <int K>
 __global__ void __launch_bounds__(256) rhs_kernel(const double* __restrict__ Y, const double* __restrict__ E,
                                                   const double* __restrict__ hits, double* __restrict__ r0,
@@ -110,7 +111,8 @@ __global__ void __launch_bounds__(256) rhs_kernel(const double* __restrict__ Y, 
                                                   int nested) {
   extern __shared__ double Es[];  // [n][K]
   const int p = blockIdx.y;
-  for (int e = threadIdx.x; e < n * K; e += blockDim.x) Es[e] = E[(size_t)p * n * K + e];
+  if (E)
+    for (int e = threadIdx.x; e < n * K; e += blockDim.x) Es[e] = E[(size_t)p * n * K + e];
   __syncthreads();
   const size_t N = (size_t)rows * side;                 // local pixels (a row slab in slab mode)
   const size_t ps = (size_t)pitch * (rows + 2 * ghost);  // r/p plane incl. ghost rows
@@ -120,13 +122,18 @@ __global__ void __launch_bounds__(256) rhs_kernel(const double* __restrict__ Y, 
     for (int c = 0; c < K; ++c) acc[c] = 0.0;
     const size_t jy = nested ? nest_of((uint32_t)(j % side), (uint32_t)(j / side)) : j;  // Y's pixel index
     const double* yp = Y + (size_t)p * n * N + jy;
-    for (int f = 0; f < n; ++f) {
-      const double y = __ldg(yp + (size_t)f * N);
+    if (E) {
+      for (int f = 0; f < n; ++f) {
+        const double y = __ldg(yp + (size_t)f * N);
 #pragma unroll
-      for (int c = 0; c < K; ++c) acc[c] = fma(y, Es[f * K + c], acc[c]);
+        for (int c = 0; c < K; ++c) acc[c] = fma(y, Es[f * K + c], acc[c]);
+      }
+    } else {
+#pragma unroll
+      for (int c = 0; c < K; ++c) acc[c] = __ldg(yp + (size_t)c * N);
     }
     const size_t gy = j / side, gx = j - gy * side;
-    const double h = hits ? __ldg(hits + (size_t)p * (rows + 2 * hghost) * side + (gy + hghost) * side + gx) : 1.0;
+    const double h = (hits && E) ? __ldg(hits + (size_t)p * (rows + 2 * hghost) * side + (gy + hghost) * side + gx) : 1.0;
 #pragma unroll
     for (int c = 0; c < K; ++c) {
       const size_t plane = (size_t)p * K + c;

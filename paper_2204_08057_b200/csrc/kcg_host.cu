@@ -511,9 +511,18 @@ kcg_status exchange_x_rows(kcg_ctx* c, const double* x_all, size_t x_rank_stride
   return KCG_OK;
 }
 
+// Right-hand side given as the data Y (IN_Y), as b = G mu itself in the user's layout (IN_B_USER,
+// kron_cg_solve_b), or as b in the kernels' row-major working layout with mu returned in that
+// layout too (IN_B_WORK: the posterior-variance probes).
+enum InputMode { IN_Y = 0, IN_B_USER = 1, IN_B_WORK = 2 };
+
 kcg_status solve_impl(kcg_ctx* c, Route route, const double* Y_in, double* mu_out, bool host_io, double tol,
-                      int max_iter, kcg_report* rep) {
+                      int max_iter, kcg_report* rep, InputMode inmode = IN_Y) {
   if (!c) return KCG_E_ARG;
+  if (inmode != IN_Y && (route != ROUTE_KRON || host_io || c->slab)) {
+    c->err = "a given right-hand side b needs the Kronecker route, device buffers and no row slabs";
+    return KCG_E_CONFIG;
+  }
   if (!Y_in || !mu_out) { c->err = "null Y or mu"; return KCG_E_ARG; }
   if (!(tol > 0.0) || !std::isfinite(tol)) { c->err = "tol must be finite and > 0"; return KCG_E_ARG; }
   if (max_iter < 0) { c->err = "max_iter < 0"; return KCG_E_ARG; }
@@ -527,16 +536,26 @@ kcg_status solve_impl(kcg_ctx* c, Route route, const double* Y_in, double* mu_ou
   const int n_sys = kron ? P : P * k;
   const bool prec = c->d.precond == KCG_PRECOND_BLOCK_JACOBI;
   const unsigned long long tag0 = (++c->solve_id) << 32;
-  auto Yr = [&](int j) -> const double* { return host_io ? c->R[j].Y_stage : Y_in + j * y_stride; };
+  const bool bgiven = inmode != IN_Y;
+  auto Yr = [&](int j) -> const double* {
+    if (bgiven) return (inmode == IN_B_USER && c->R[j].y_rm) ? c->R[j].y_rm : Y_in;  // b, working layout
+    return host_io ? c->R[j].Y_stage : Y_in + j * y_stride;
+  };
   auto muu = [&](int j) -> double* { return host_io ? c->R[j].mu_stage : mu_out + j * mu_stride; };
   // the kernels' solution buffer: the user's mu, or the row-major copy for a NESTED layout
-  auto mur = [&](int j) -> double* { return c->R[j].x_rm ? c->R[j].x_rm : muu(j); };
+  auto mur = [&](int j) -> double* { return (c->R[j].x_rm && inmode != IN_B_WORK) ? c->R[j].x_rm : muu(j); };
+  // geometry of the data / b reads: b is in the working layout (no NESTED gather)
+  auto gin = [&](const RankState& R) { SlabGeom g = geom_of(c, R); if (bgiven) g.nested = 0; return g; };
+  const int nin = bgiven ? k : n;  // planes per patch of the rhs input
 
   CK(cudaEventRecord(c->ev[0], s), "event");
   for (int j = 0; j < c->nlocal; ++j) {
     RankState& R = c->R[j];
     if (host_io) CK(cudaMemcpyAsync(R.Y_stage, Y_in + j * y_stride, y_stride * 8, cudaMemcpyHostToDevice, s), "H2D Y");
-    CK(kcg::launch_rhs(k, s, Yr(j), kron ? R.E_kron : R.E_syl, R.hits, R.r[0], R.p[0], mur(j), P, n, geom_of(c, R)),
+    if (inmode == IN_B_USER && R.y_rm)
+      CK(kcg::launch_permute(s, Y_in, R.y_rm, (size_t)P * k, c->side, false), "permute b");
+    CK(kcg::launch_rhs(k, s, Yr(j), bgiven ? nullptr : (kron ? R.E_kron : R.E_syl), R.hits, R.r[0], R.p[0], mur(j), P,
+                       nin, gin(R)),
        "rhs kernel");
   }
   if (c->slab)
@@ -621,8 +640,8 @@ kcg_status solve_impl(kcg_ctx* c, Route route, const double* Y_in, double* mu_ou
   }
   for (int j = 0; j < c->nlocal; ++j) {
     RankState& R = c->R[j];
-    CK(kcg::launch_resid(k, s, R.params_kron, mur(j), Yr(j), R.E_kron, R.hits, R.resid_partials, R.resid_out, P, n,
-                         geom_of(c, R), c->slab ? R.xg_top : nullptr, c->slab ? R.xg_bot : nullptr),
+    CK(kcg::launch_resid(k, s, R.params_kron, mur(j), Yr(j), bgiven ? nullptr : R.E_kron, R.hits, R.resid_partials,
+                         R.resid_out, P, nin, gin(R), c->slab ? R.xg_top : nullptr, c->slab ? R.xg_bot : nullptr),
        "residual kernel");
     if (c->slab) {
       kcg::XrankPut Pt{};
@@ -636,7 +655,8 @@ kcg_status solve_impl(kcg_ctx* c, Route route, const double* Y_in, double* mu_ou
   }
   if (c->slab) CK(kcg::launch_xrank_sync(s, xsync_of(c, tag0 + kPostTag + 2)), "rendezvous kernel");
   for (int j = 0; j < c->nlocal; ++j)
-    if (c->R[j].x_rm) CK(kcg::launch_permute(s, c->R[j].x_rm, muu(j), (size_t)P * k, c->side, true), "permute mu");
+    if (c->R[j].x_rm && inmode != IN_B_WORK)
+      CK(kcg::launch_permute(s, c->R[j].x_rm, muu(j), (size_t)P * k, c->side, true), "permute mu");
   c->st_host.resize(n_sys);
   const int nr = c->slab ? c->nranks : 1;
   c->resid_host.resize((size_t)nr * P * 2);
@@ -1076,6 +1096,51 @@ kcg_status kron_cg_solve(kcg_ctx* c, const double* Y, double* mu, double tol, in
 kcg_status sylvester_solve(kcg_ctx* c, const double* Y, double* mu, double tol, int max_iter, kcg_report* rep) {
   return solve_impl(c, ROUTE_SYL, Y, mu, false, tol, max_iter, rep);
 }
+kcg_status kron_cg_solve_b(kcg_ctx* c, const double* b, double* x, double tol, int max_iter, kcg_report* rep) {
+  return solve_impl(c, ROUTE_KRON, b, x, false, tol, max_iter, rep, IN_B_USER);
+}
+
+kcg_status posterior_variance(kcg_ctx* c, int n_probes, unsigned long long seed, double* var, double* scratch,
+                              double tol, int max_iter, kcg_report* rep) {
+  if (!c) return KCG_E_ARG;
+  if (!var || !scratch) { c->err = "null var or scratch"; return KCG_E_ARG; }
+  if (n_probes < 1) { c->err = "n_probes < 1"; return KCG_E_ARG; }
+  if (c->slab) { c->err = "posterior_variance: no row slabs"; return KCG_E_CONFIG; }
+  cudaStream_t s = c->stream;
+  const RankState& R = c->R[0];
+  const size_t planes = (size_t)c->P * c->k, tot = planes * c->N;
+  double* z = scratch;
+  double* x = scratch + tot;
+  double* acc = R.y_rm ? R.y_rm : var;  // row-major accumulator (NESTED: scattered at the end)
+  kcg_report sub{}, all{};
+  int worst = KCG_OK, maxit = 0;
+  double wall = 0.0, loop = 0.0, bytes = 0.0, maxrel = 0.0, maxtrue = 0.0;
+  long long sumit = 0;
+  for (int i = 0; i < n_probes; ++i) {
+    CK(kcg::launch_probe(s, z, c->P, c->k, c->side, c->d.layout == KCG_LAYOUT_NESTED, seed, i), "probe kernel");
+    sub = kcg_report{};
+    const kcg_status st = solve_impl(c, ROUTE_KRON, z, x, false, tol, max_iter, &sub, IN_B_WORK);
+    if (st != KCG_OK && st != KCG_NOT_CONVERGED) return st;
+    if (st == KCG_NOT_CONVERGED) worst = KCG_NOT_CONVERGED;
+    CK(kcg::launch_var_accum(s, z, x, acc, tot, i == 0, i == n_probes - 1 ? 1.0 / n_probes : 1.0), "accumulate kernel");
+    wall += sub.wall_time_s; loop += sub.loop_time_s; bytes += sub.loop_bytes;
+    maxit = std::max(maxit, sub.iterations); sumit += sub.system_iterations;
+    maxrel = std::max(maxrel, sub.rel_residual); maxtrue = std::max(maxtrue, sub.rel_residual_true);
+  }
+  if (R.y_rm) CK(kcg::launch_permute(s, R.y_rm, var, planes, c->side, true), "permute var");
+  CK(cudaStreamSynchronize(s), "posterior variance");
+  if (rep) {
+    all = sub;
+    all.status = worst; all.iterations = maxit; all.system_iterations = sumit;
+    all.rel_residual = maxrel; all.rel_residual_true = maxtrue;
+    all.wall_time_s = wall; all.loop_time_s = loop; all.loop_bytes = bytes;
+    all.iterations_per = rep->iterations_per; all.history = rep->history; all.history_len = 0;
+    *rep = all;
+  }
+  c->err.clear();
+  return (kcg_status)worst;
+}
+
 kcg_status sylvester_lanczos_solve(kcg_ctx* c, const double* Y, double* mu, double tol, int max_iter,
                                    kcg_report* rep) {
   return lanczos_impl(c, Y, mu, false, tol, max_iter, rep);

@@ -243,6 +243,12 @@ cudaError_t launch_xrank_sync(cudaStream_t s, const XrankSync& X);
 // dst[plane][nest(x,y)] = src[plane][y side + x] (to_nested) or the inverse gather.
 cudaError_t launch_permute(cudaStream_t s, const double* src, double* dst, size_t planes, int side, bool to_nested);
 int apply_tiles_per_sys(int rows, int side);
+// Posterior variances (Hutchinson): z[p][c][pixel] = Rademacher(seed, probe, p, c, j) in the working
+// row-major layout, j = the pixel's index in the user layout; var (=|+=) z * x, times scale.
+cudaError_t launch_probe(cudaStream_t s, double* z, int P, int K, int side, bool nested, unsigned long long seed,
+                         int probe);
+cudaError_t launch_var_accum(cudaStream_t s, const double* z, const double* x, double* var, size_t n, bool first,
+                             double scale);
 // block-Lanczos (kcg_lanczos_*.cu): one cooperative launch runs the Lanczos passes, the residual
 // estimate, the coefficients and (two-pass mode) the replay that assembles M; store mode follows it
 // with lz_assemble.

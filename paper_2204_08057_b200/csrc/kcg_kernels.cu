@@ -22,7 +22,7 @@ int apply_tiles_per_sys(int rows, int side) {
 }
 
 // RESID = false: y = G x.   RESID = true: partials[s][tile] = (||b - G x||^2, ||b||^2) over the
-// tile, with b = h Y E recomputed from the data (E = T A).  Slab geometry: `rows` local rows from
+// tile, with b = h Y E recomputed from the data (E = T A), or b = Y itself when E == nullptr.  Slab geometry: `rows` local rows from
 // global face row `row0`; the halo rows beyond the slab come from xg_top / xg_bot ([planes][side],
 // the neighbours' boundary rows; nullptr or outside the face -> 0).  D2: Q0 = D^2 + kappa2 I, the
 // tile's x is staged with a 2-pixel halo and D x is formed on tile + 1-ring first (no slabs).
@@ -59,7 +59,7 @@ __global__ void __launch_bounds__(AP_NT) apply_kernel(const SysParams* __restric
   }
   double* Ds = xs + K * PLANE;                  // D2: D x on tile + 1-ring (zero outside the face)
   double* Es = xs + (D2 ? 2 : 1) * K * PLANE;
-  if (RESID)
+  if (RESID && E)
     for (int e = threadIdx.x; e < n * K; e += AP_NT) Es[e] = E[(size_t)s * n * K + e];
   __syncthreads();
   auto degf = [&](int gy, int gx) { return 4 - (gy == 0) - (gy == side - 1) - (gx == 0) - (gx == side - 1); };
@@ -99,10 +99,15 @@ __global__ void __launch_bounds__(AP_NT) apply_kernel(const SysParams* __restric
 #pragma unroll
       for (int c = 0; c < K; ++c) bq[c] = 0.0;
       const double* yp = Y + (size_t)s * n * N + (nested ? (size_t)nest_of(gx, ly) : (size_t)ly * side + gx);
-      for (int f = 0; f < n; ++f) {
-        const double yv = yp[(size_t)f * N];
+      if (E) {
+        for (int f = 0; f < n; ++f) {
+          const double yv = yp[(size_t)f * N];
 #pragma unroll
-        for (int c = 0; c < K; ++c) bq[c] = fma(yv, Es[f * K + c], bq[c]);
+          for (int c = 0; c < K; ++c) bq[c] = fma(yv, Es[f * K + c], bq[c]);
+        }
+      } else {  // b given (n == K): Y holds b, no N_h factor
+#pragma unroll
+        for (int c = 0; c < K; ++c) bq[c] = yp[(size_t)c * N];
       }
     }
 #pragma unroll
@@ -120,7 +125,7 @@ __global__ void __launch_bounds__(AP_NT) apply_kernel(const SysParams* __restric
       for (int d = 0; d < K; ++d) mix = fma(M[c * K + d], xc[d], mix);
       const double q = fma(h, mix, tau[c] * fma(kappa2, xc[c], q0));
       if (RESID) {
-        const double b = h * bq[c];
+        const double b = E ? h * bq[c] : bq[c];
         const double rres = b - q;
         acc0 = fma(rres, rres, acc0);
         acc1 = fma(b, b, acc1);
@@ -419,4 +424,47 @@ cudaError_t launch_permute(cudaStream_t s, const double* src, double* dst, size_
       src, dst, planes, side, to_nested ? 1 : 0);
   return cudaGetLastError();
 }
+// ------------------------------------------------------------------ posterior variances (NEXT-3)
+// SplitMix64 (Steele, Lea & Flood 2014; Vigna's reference constants): the counter-based generator
+// of the Hutchinson probes (the header documents the key; the CPU reference implements it too).
+__device__ __forceinline__ unsigned long long splitmix64(unsigned long long x) {
+  unsigned long long z = x + 0x9E3779B97F4A7C15ull;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+
+__global__ void __launch_bounds__(256) probe_kernel(double* __restrict__ z, int P, int K, int side, int nested,
+                                                    unsigned long long seed, int probe) {
+  const size_t N = (size_t)side * side, tot = (size_t)P * K * N;
+  const unsigned long long s0 = splitmix64(seed);
+  for (size_t e = (size_t)blockIdx.x * blockDim.x + threadIdx.x; e < tot; e += (size_t)gridDim.x * blockDim.x) {
+    const size_t pc = e / N, px = e - pc * N;  // pc = p K + c
+    const size_t gy = px / side, gx = px - gy * side;
+    const size_t j = nested ? (size_t)nest_of((uint32_t)gx, (uint32_t)gy) : px;
+    const unsigned long long key = ((unsigned long long)probe * P * K + pc) * N + j;
+    z[e] = (splitmix64(s0 + key) >> 63) ? -1.0 : 1.0;
+  }
+}
+
+__global__ void __launch_bounds__(256) var_accum_kernel(const double* __restrict__ z, const double* __restrict__ x,
+                                                        double* __restrict__ var, size_t n, int first, double scale) {
+  for (size_t e = (size_t)blockIdx.x * blockDim.x + threadIdx.x; e < n; e += (size_t)gridDim.x * blockDim.x) {
+    const double v = first ? z[e] * x[e] : fma(z[e], x[e], var[e]);
+    var[e] = v * scale;
+  }
+}
+
+cudaError_t launch_probe(cudaStream_t s, double* z, int P, int K, int side, bool nested, unsigned long long seed,
+                         int probe) {
+  probe_kernel<<<grid_for((size_t)P * K * side * side), 256, 0, s>>>(z, P, K, side, nested ? 1 : 0, seed, probe);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_var_accum(cudaStream_t s, const double* z, const double* x, double* var, size_t n, bool first,
+                             double scale) {
+  var_accum_kernel<<<grid_for(n), 256, 0, s>>>(z, x, var, n, first ? 1 : 0, scale);
+  return cudaGetLastError();
+}
+
 }  // namespace kcg

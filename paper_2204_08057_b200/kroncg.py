@@ -72,6 +72,9 @@ kron_cg_solve_host = _sig("kron_cg_solve_host", C.c_int, _solve_args)
 sylvester_solve_host = _sig("sylvester_solve_host", C.c_int, _solve_args)
 sylvester_lanczos_solve = _sig("sylvester_lanczos_solve", C.c_int, _solve_args)
 sylvester_lanczos_solve_host = _sig("sylvester_lanczos_solve_host", C.c_int, _solve_args)
+kron_cg_solve_b = _sig("kron_cg_solve_b", C.c_int, _solve_args)
+posterior_variance = _sig("posterior_variance", C.c_int,
+                          [_ctxp, C.c_int, C.c_ulonglong, _vp, _vp, C.c_double, C.c_int, C.POINTER(kcg_report)])
 kron_cg_apply = _sig("kron_cg_apply", C.c_int, [_ctxp, _vp, _vp])
 kron_cg_rhs = _sig("kron_cg_rhs", C.c_int, [_ctxp, _vp, _vp])
 sylvester_factor = _sig("sylvester_factor", C.c_int, [_ctxp, _vp, _vp])
@@ -96,7 +99,8 @@ EXPORTS = ["kron_cg_workspace_size", "kron_cg_create", "kron_cg_solve", "sylvest
            "kron_cg_solve_host", "sylvester_solve_host", "kron_cg_apply", "kron_cg_rhs",
            "sylvester_factor", "kcg_last_error", "kcg_status_string", "kron_cg_destroy",
            "kron_cg_workspace_size_slab", "kron_cg_create_slab", "kcg_ipc_export", "kcg_ipc_import",
-           "kcg_ipc_close", "sylvester_lanczos_solve", "sylvester_lanczos_solve_host"]
+           "kcg_ipc_close", "sylvester_lanczos_solve", "sylvester_lanczos_solve_host",
+           "kron_cg_solve_b", "posterior_variance"]
 
 
 class KcgError(RuntimeError):
@@ -242,6 +246,29 @@ class KronCG:
         mu = self._out(mu)
         self._check_dev(mu, self.shape_mu, "mu")
         return mu, self._solve(sylvester_lanczos_solve, Y, mu, tol, max_iter, self.P, **kw)
+
+    def solve_b(self, b, x=None, tol=1e-10, max_iter=100000, **kw):
+        """G x = b for given right-hand sides b: CUDA [P][k][side][side] (kron_cg_solve_b)."""
+        self._check_dev(b, self.shape_mu, "b")
+        x = self._out(x)
+        self._check_dev(x, self.shape_mu, "x")
+        return x, self._solve(kron_cg_solve_b, b, x, tol, max_iter, self.P, **kw)
+
+    def posterior_variance(self, n_probes, seed=0, var=None, tol=1e-10, max_iter=100000):
+        """Hutchinson estimate of diag(G^{-1}) with n_probes Rademacher probes (posterior_variance).
+        Returns (var [P][k][side][side], report)."""
+        import torch
+        var = self._out(var)
+        self._check_dev(var, self.shape_mu, "var")
+        scratch = torch.empty((2,) + self.shape_mu, dtype=torch.float64, device=self.device)
+        rep = kcg_report()
+        its = (C.c_int * max(self.P, 1))()
+        rep.iterations_per = C.cast(its, C.POINTER(C.c_int))
+        st = posterior_variance(self._ctx, int(n_probes), C.c_ulonglong(int(seed) & (2**64 - 1)), var.data_ptr(),
+                                scratch.data_ptr(), float(tol), int(max_iter), C.byref(rep))
+        if st not in (KCG_OK, KCG_NOT_CONVERGED):
+            raise self._err(st)
+        return var, self._report(rep, its, None, st)
 
     def solve_host(self, Y, mu=None, tol=1e-10, max_iter=100000, route="kron", **kw):
         """Host-buffer entry points (kron_cg_solve_host / sylvester_solve_host /

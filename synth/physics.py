@@ -54,6 +54,23 @@ def planck_mixing(freqs_ghz=PLANCK_FREQS_GHZ, nu0_ghz=NU0_GHZ) -> np.ndarray:
     return A
 
 
+def nested_order(maps: np.ndarray) -> np.ndarray:
+    """[..][side][side] row-major maps -> the same maps with pixels in HEALPix NESTED order inside the
+    face (reading R1: bit b of x -> bit 2b, bit b of y -> bit 2b+1 of the index), reshaped back to
+    [..][side][side] -- how the paper's HEALPix data arrive (App. A)."""
+    maps = np.asarray(maps)
+    side = maps.shape[-1]
+    y, x = np.meshgrid(np.arange(side), np.arange(side), indexing="ij")
+    idx = np.zeros((side, side), dtype=np.int64)
+    for b in range(max(1, int(side).bit_length())):
+        idx |= ((x >> b) & 1) << (2 * b)
+        idx |= ((y >> b) & 1) << (2 * b + 1)
+    flat = maps.reshape(maps.shape[:-2] + (side * side,))
+    out = np.empty_like(flat)
+    out[..., idx.reshape(-1)] = flat
+    return out.reshape(maps.shape)
+
+
 def make_paper_patch(level: int, seed: int, hits="random", kappa2: float = 0.0) -> PatchProblem:
     """One face of the paper's simulation (sec. 4) in HEALPix NESTED order is produced by
     the caller permuting Y / hits; this returns the row-major maps.  Draw order with

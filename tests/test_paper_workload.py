@@ -63,3 +63,10 @@ def test_paper_system_oracle_routes_agree_with_the_direct_solve(layout):
         # the shifts rho_j of S^ = A^T T A (P = I) dwarf D^2: the shifted systems are nearly
         # identities and the Sylvester routes converge in a few steps
         assert max(s.iterations) < 20 and lz.iterations < 10
+
+
+def test_synth_nested_order_is_the_healpix_nested_numbering():
+    """synth's input reordering (bench.py's paper leg) == the oracle's NESTED numbering (reading R1)."""
+    from synth.physics import nested_order
+    a = np.random.default_rng(0).standard_normal((2, 3, 16, 16))
+    assert np.array_equal(nested_order(a), model.to_layout(4, a, "nested").reshape(a.shape))
