@@ -15,6 +15,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <string>
@@ -426,7 +427,7 @@ bool encode_lzmap(CUtensorMap* m, double* base, int side, int pitch, size_t plan
   cuuint64_t dims[3] = {(cuuint64_t)side, (cuuint64_t)side, (cuuint64_t)planes};
   cuuint64_t strides[2] = {(cuuint64_t)pitch * 8, (cuuint64_t)pitch * side * 8};
   const int hb = kcg::lz_halo(d2);
-  cuuint32_t box[3] = {(cuuint32_t)(KCG_TX + 2 * hb), (cuuint32_t)(kcg::lz_tile_y(K) + 2 * hb), (cuuint32_t)K};
+  cuuint32_t box[3] = {(cuuint32_t)(KCG_TX + 2 * hb), (cuuint32_t)(kcg::lz_tile_y(K, d2) + 2 * hb), (cuuint32_t)K};
   cuuint32_t es[3] = {1, 1, 1};
   CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, base, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
                    CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
@@ -1035,8 +1036,9 @@ kcg_status create_impl(const kcg_desc* d, const kcg_slab* sl, const double* A_ho
     int mgl = 0;
     CKC(kcg::lz_kernel_config(k, hits_dev != nullptr, d2, &mgl, &c->smem_lz), "lanczos kernel config");
     c->grid_lz = std::max(1, mgl);
+    if (const char* ev = std::getenv("KCG_LZ_GRID")) c->grid_lz = std::max(1, std::min(c->grid_lz, std::atoi(ev)));  // diagnostics
     c->tiles_x_lz = (c->side + KCG_TX - 1) / KCG_TX;
-    c->tiles_y_lz = (c->side + kcg::lz_tile_y(k) - 1) / kcg::lz_tile_y(k);
+    c->tiles_y_lz = (c->side + kcg::lz_tile_y(k, d2) - 1) / kcg::lz_tile_y(k, d2);
   }
   CKC(cudaStreamSynchronize(c->stream), "create sync");
   c->tiles_x_kron = tiles_x(c->side, k);

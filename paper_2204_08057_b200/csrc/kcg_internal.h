@@ -210,7 +210,7 @@ struct LzArgs {
 // V slot of block q: the HBM-resident basis (store) keeps every block; the paper's memory-lean
 // two-pass mode rotates three slots after Y^.
 __host__ __device__ inline int lz_slot(int store, int q) { return store ? q : (q == 0 ? 0 : 1 + (q - 1) % 3); }
-__host__ __device__ constexpr int lz_tile_y(int K) { return K <= 2 ? 16 : 8; }
+__host__ __device__ constexpr int lz_tile_y(int K, bool d2) { return d2 ? 8 : (K <= 4 ? 16 : 8); }
 __host__ __device__ constexpr int lz_npart(int K) {  // Gram partial per CTA and face
   return K <= 4 ? K * (2 * K + 1) : ((2 * K + 3) / 4) * ((2 * K + 3) / 4 + 1) / 2 * 16;
 }

@@ -27,13 +27,13 @@ namespace kcg {
 template <int K, bool D2 = false>
 struct LzCfg {
   static constexpr int TX = KCG_TX;
-  static constexpr int TY = lz_tile_y(K);
+  static constexpr int TY = lz_tile_y(K, D2);
   static constexpr int HB = D2 ? 4 : 2;                // box halo: V_{i-1} is needed on the tile + 2 RR ring
   static constexpr int RR = D2 ? 2 : 1;                // ring of V_i (the operator's radius)
   static constexpr int BW = TX + 2 * HB, BH = TY + 2 * HB;
   static constexpr int RW = TX + 2 * RR, RH = TY + 2 * RR, RN = RW * RH;  // V_i region
   static constexpr int BOX = K * BH * BW;
-  static constexpr int STAGES = D2 ? 2 : (K <= 4 ? 3 : (K == 5 ? 2 : 1));  // TMA tiles in flight
+  static constexpr int STAGES = D2 ? 2 : (K <= 2 ? 3 : (K <= 5 ? 2 : 1));  // TMA tiles in flight
   static constexpr int KP = (2 * K + 3) / 4 * 4;      // Gram rows [V, W] padded to 4
   static constexpr int NB4 = KP / 4;
   static constexpr int NJOB = NB4 * (NB4 + 1) / 2;    // upper-triangle 4x4 blocks of the Gram
@@ -48,7 +48,7 @@ struct LzCfg {
   static constexpr int DVN = D2 ? K * DW * DH : 0;
   static constexpr int OFF_U = STAGES * 2 * BOX;
   static constexpr int OFF_HS = OFF_U + UPL * RN;     // hits of the tile (K > 4)
-  static constexpr int OFF_DV = OFF_HS + NPIX;
+  static constexpr int OFF_DV = OFF_HS + (REGG ? 0 : NPIX);
   static constexpr int OFF_MAT = OFF_DV + DVN;        // P1, P2, Ri, Bc, Z (K x K each)
   static constexpr int OFF_RED = OFF_MAT + 5 * K * K; // flush scratch [NT][4]
   static constexpr int DOUBLES = OFF_RED + NT * 4;
@@ -133,9 +133,9 @@ __device__ __forceinline__ int lz_deg(int gy, int gx, int side) {
 
 // ------------------------------------------------------------------------- partial flush
 // Per-thread Gram accumulators -> the CTA's partial of face f (fixed slice order).
-template <int K>
-__device__ __forceinline__ void lz_flush(const LzArgs& a, int f, double (&acc)[LzCfg<K>::NACC], double* sm) {
-  using C = LzCfg<K>;
+template <int K, bool D2>
+__device__ __forceinline__ void lz_flush(const LzArgs& a, int f, double (&acc)[LzCfg<K, D2>::NACC], double* sm) {
+  using C = LzCfg<K, D2>;  // the layout of THIS kernel's shared memory (OFF_RED differs per prior)
   const int tid = threadIdx.x;
   double* red = sm + C::OFF_RED;
   double* dst = a.part + ((size_t)f * KCG_LZ_GRID_MAX + blockIdx.x) * C::NPART;
@@ -226,7 +226,7 @@ __device__ __forceinline__ void lz_pass(const LzArgs& a, const CUtensorMap* vmap
     const int lt = (int)t - ai * a.tps;
     const int y0 = (lt / a.tiles_x) * C::TY, x0 = (lt % a.tiles_x) * C::TX;
     if (f != cur) {
-      if (cur >= 0 && mode != LZ_REPLAY) lz_flush<K>(a, cur, acc, sm);
+      if (cur >= 0 && mode != LZ_REPLAY) lz_flush<K, D2>(a, cur, acc, sm);
 #pragma unroll
       for (int j = 0; j < C::NACC; ++j) acc[j] = 0.0;
       cur = f;
@@ -491,7 +491,7 @@ __device__ __forceinline__ void lz_pass(const LzArgs& a, const CUtensorMap* vmap
       __syncthreads();  // U is free
     }
   }
-  if (mode != LZ_REPLAY && cur >= 0) lz_flush<K>(a, cur, acc, sm);
+  if (mode != LZ_REPLAY && cur >= 0) lz_flush<K, D2>(a, cur, acc, sm);
 }
 
 // ------------------------------------------------------------------------- per-face reduction
@@ -499,9 +499,9 @@ __device__ __forceinline__ void lz_pass(const LzArgs& a, const CUtensorMap* vmap
 //   q = 0: B_0 = chol(Y^T N Y^);  q = i >= 1: H_i, C = W^T N W (Cholesky-QR Gram), B_{i+1} = chol(C),
 //   per shift j: T_i + rho_j I eliminated by one more block row, gamma_j = ||B_{i+1} f_last||^2;
 //   stop when sqrt(gamma) <= tol ||B_0||_F (Alg. SylvSolver).
-template <int K>
+template <int K, bool D2>
 __device__ void lz_reduce(const LzArgs& a, int q, const int* act, int nact, int ai, double* sm) {
-  using C = LzCfg<K>;
+  using C = LzCfg<K, D2>;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, ncta = gridDim.x;
   const int f = act[ai];
   const long long T = (long long)nact * a.tps;
@@ -540,9 +540,11 @@ __device__ void lz_reduce(const LzArgs& a, int q, const int* act, int nact, int 
         double v[8];
 #pragma unroll
         for (int u = 0; u < 8; ++u) {
-          const int b = b0 + u * NG;
-          const bool ok = b <= b_hi && cst[b + 1 - b_lo] > cst[b - b_lo];
-          v[u] = ok ? __ldcg(src + (size_t)b * C::NPART) : 0.0;
+          // clamped index: the compiler may issue the loads before the predicate is known
+          const int b = min(b0 + u * NG, b_hi);
+          const bool ok = b0 + u * NG <= b_hi && cst[b + 1 - b_lo] > cst[b - b_lo];
+          const double pv = __ldcg(src + (size_t)b * C::NPART);
+          v[u] = ok ? pv : 0.0;
         }
 #pragma unroll
         for (int u = 0; u < 8; ++u) s += v[u];
@@ -725,9 +727,9 @@ __device__ void lz_reduce(const LzArgs& a, int q, const int* act, int nact, int 
 // ------------------------------------------------------------------------- coefficients Z
 // Back substitution of the stored eliminations per shift j gives column j of Q F (Eq.(soln-constr)),
 // then Z = (Q F) U^{-1} = (Q F) W^T (reading R27), block by block: G_a = Z[a].
-template <int K>
+template <int K, bool D2>
 __device__ void lz_coeffs(const LzArgs& a, int f, double* sm) {
-  using C = LzCfg<K>;
+  using C = LzCfg<K, D2>;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int i = __ldcg(&a.st[f].iters);
   if (i <= 0) return;
@@ -809,7 +811,7 @@ __global__ void __launch_bounds__(256, 1)
     grid.sync();
     if (tr && cta == 0 && tid == 0) tr[2] = globaltimer();
     for (int ai = cta; ai < nact; ai += ncta) {
-      lz_reduce<K>(a, q, act, nact, ai, sm);
+      lz_reduce<K, D2>(a, q, act, nact, ai, sm);
       __syncthreads();
     }
     if (tr && cta == 0 && tid == 0) tr[3] = globaltimer();
@@ -819,7 +821,7 @@ __global__ void __launch_bounds__(256, 1)
   }
   // coefficients
   for (int f = cta; f < a.P; f += ncta) {
-    lz_coeffs<K>(a, f, sm);
+    lz_coeffs<K, D2>(a, f, sm);
     __syncthreads();
   }
   __threadfence();
