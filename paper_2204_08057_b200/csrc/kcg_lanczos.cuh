@@ -59,7 +59,8 @@ struct LzCfg {
   static constexpr int SC_M = SC_GRP + NT;                   // Gv, H, C0, T1, C, R, X(Rinv), B0 [8][K*K]
   static constexpr int SC_W = SC_M + 8 * K * K;              // per-shift warp scratch [K][9 K*K]
   static constexpr int SC_RES = SC_W + K * 9 * K * K;        // residual per shift [K] + flags
-  static constexpr int SC_END = SC_RES + 2 * K + 8;
+  static constexpr int SC_PRE = SC_RES + 2 * K + 8;         // prefetched B_0, rho, u_j = phi (.) w_j
+  static constexpr int SC_END = SC_PRE + 2 * K * K + K;
   static_assert(SC_END <= OFF_U, "reducer scratch exceeds the box area");
   static_assert(SMEM + 6 * 1024 <= 227 * 1024, "shared memory budget (dynamic + static)");
 };
@@ -499,6 +500,12 @@ __device__ __forceinline__ void lz_pass(const LzArgs& a, const CUtensorMap* vmap
 //   q = 0: B_0 = chol(Y^T N Y^);  q = i >= 1: H_i, C = W^T N W (Cholesky-QR Gram), B_{i+1} = chol(C),
 //   per shift j: T_i + rho_j I eliminated by one more block row, gamma_j = ||B_{i+1} f_last||^2;
 //   stop when sqrt(gamma) <= tol ||B_0||_F (Alg. SylvSolver).
+// KCG_TRACE builds: sub-phase stamps of the reduction on CTA 0 (columns 153..157 of the pass row)
+__device__ __forceinline__ void lz_stamp(const LzArgs& a, int q, int col) {
+  if (KCG_TRACE && a.trace && blockIdx.x == 0 && threadIdx.x == 0 && q < KCG_TRACE_ITERS)
+    a.trace[(size_t)q * KCG_TRACE_COLS + col] = globaltimer();
+}
+
 template <int K, bool D2>
 __device__ void lz_reduce(const LzArgs& a, int q, const int* act, int nact, int ai, double* sm) {
   using C = LzCfg<K, D2>;
@@ -507,6 +514,16 @@ __device__ void lz_reduce(const LzArgs& a, int q, const int* act, int nact, int 
   const long long T = (long long)nact * a.tps;
   const long long f0 = (long long)ai * a.tps, f1 = f0 + a.tps;
   const size_t fc = (size_t)f * a.cap, fr = (size_t)f * (a.cap + 1);
+  // constants of the face and B_0 (L2 reads, issued before the partial sums)
+  if (q >= 1) {
+    double* pre = sm + C::SC_PRE;
+    const LzFace& pf0 = a.prm[f];
+    for (int e = tid; e < K * K; e += C::NT) {
+      pre[e] = __ldcg(a.Rs + fr * K * K + e);                        // B_0
+      pre[K * K + K + e] = pf0.phi[e / K] * pf0.W[e];                 // U = P W: u_j = column j
+    }
+    if (tid < K) pre[K * K + tid] = pf0.rho[tid];
+  }
   // the previous step's elimination of every shift does not depend on this pass: fetch it first
   // (overlaps the L2 latency with the partial sums below)
   if (q >= 2 && warp < K) {
@@ -559,6 +576,7 @@ __device__ void lz_reduce(const LzArgs& a, int q, const int* act, int nact, int 
     gam[tid] = s;
   }
   __syncthreads();
+  lz_stamp(a, q, 153);
   double* Gv = sm + C::SC_M;
   double* H = Gv + K * K;
   double* C0 = H + K * K;
@@ -566,7 +584,6 @@ __device__ void lz_reduce(const LzArgs& a, int q, const int* act, int nact, int 
   double* Cm = T1 + K * K;
   double* R = Cm + K * K;
   double* X = R + K * K;
-  double* B0 = X + K * K;
   double* res = sm + C::SC_RES;
   int* flag = reinterpret_cast<int*>(res + K);
   auto G = [&](int i, int j) {  // symmetric Gram entry (packed upper triangle, or 4x4 blocks)
@@ -583,7 +600,6 @@ __device__ void lz_reduce(const LzArgs& a, int q, const int* act, int nact, int 
     C0[e] = G(K + r, K + c);
   }
   __syncthreads();
-  const LzFace& pf = a.prm[f];
   if (q == 0) {
     if (warp == 0) {
       const bool ok = w_chol<K>(Gv, R);
@@ -610,8 +626,10 @@ __device__ void lz_reduce(const LzArgs& a, int q, const int* act, int nact, int 
     }
     return;
   }
-  // C = C0 - 2 H^T H + H^T Gv H   (Gram of W - V H given V^T N W = H)
-  if (warp == 0) {
+  // C = C0 - 2 H^T H + H^T Gv H   (Gram of W - V H given V^T N W = H).  One warp (a spare one when
+  // K < 8) runs the Cholesky QR while the shift warps run their eliminations; only gamma needs both.
+  const int cwarp = K < 8 ? K : 0;
+  if (warp == cwarp) {
     w_matmul<K>(Gv, H, T1);
     for (int e = lane; e < K * K; e += 32) {
       const int r = e / K, c = e - r * K;
@@ -631,11 +649,11 @@ __device__ void lz_reduce(const LzArgs& a, int q, const int* act, int nact, int 
     __syncwarp();
     if (flag[0] == 2)
       for (int e = lane; e < K * K; e += 32) { R[e] = 0.0; X[e] = 0.0; }
-    for (int e = lane; e < K * K; e += 32) B0[e] = __ldcg(a.Rs + fr * K * K + e);
   }
-  __syncthreads();
+  lz_stamp(a, q, 154);
   // per shift j (one warp each): block forward elimination of (T_i + rho_j I) f = E_1 B_0 u_j
   const int blk = q - 1;  // block index of H_i in T_i
+  __shared__ double gvec[KCG_KMAX][KCG_KMAX], fvec[KCG_KMAX][KCG_KMAX];
   if (warp < K) {
     const int j = warp;
     double* D = sm + C::SC_W + j * 9 * K * K;
@@ -646,8 +664,7 @@ __device__ void lz_reduce(const LzArgs& a, int q, const int* act, int nact, int 
     double* Rw = S + K * K;
     double* Xw = Rw + K * K;
     double* Si = Xw + K * K;
-    __shared__ double gvec[KCG_KMAX][KCG_KMAX], fvec[KCG_KMAX][KCG_KMAX];
-    const double rho = pf.rho[j];
+    const double rho = sm[C::SC_PRE + K * K + j];
     for (int e = lane; e < K * K; e += 32) {
       const int r = e / K, c = e - r * K;
       D[e] = (r >= c ? H[e] : H[c * K + r]) + (r == c ? rho : 0.0);  // lower triangle of H (reading R29)
@@ -657,7 +674,7 @@ __device__ void lz_reduce(const LzArgs& a, int q, const int* act, int nact, int 
       for (int e = lane; e < K * K; e += 32) S[e] = D[e];
       if (lane < K) {  // g = B_0 u_j, u_j = P w_j
         double s = 0.0;
-        for (int c = 0; c < K; ++c) s = fma(B0[lane * K + c], pf.phi[c] * pf.W[c * K + j], s);
+        for (int c = 0; c < K; ++c) s = fma(sm[C::SC_PRE + lane * K + c], sm[C::SC_PRE + K * K + K + c * K + j], s);
         gvec[j][lane] = s;
       }
       __syncwarp();
@@ -686,20 +703,22 @@ __device__ void lz_reduce(const LzArgs& a, int q, const int* act, int nact, int 
       fvec[j][lane] = s;
     }
     __syncwarp();
-    if (lane == 0) {  // ||B_{i+1} f||^2
-      double g2 = 0.0;
-      for (int r = 0; r < K; ++r) {
-        double s = 0.0;
-        for (int c = 0; c < K; ++c) s = fma(R[r * K + c], fvec[j][c], s);
-        g2 = fma(s, s, g2);
-      }
-      res[j] = g2;
-    }
     double* so = a.Sinv + ((fc + blk) * K + j) * K * K;
     for (int e = lane; e < K * K; e += 32) so[e] = Si[e];
     if (lane < K) a.gv[((fc + blk) * K + j) * K + lane] = gvec[j][lane];
   }
+  __syncthreads();  // R (Cholesky warp) and every shift's f_last are ready
+  if (tid < K) {    // gamma_j = ||B_{i+1} f_last||^2
+    double g2 = 0.0;
+    for (int r = 0; r < K; ++r) {
+      double s2 = 0.0;
+      for (int c = 0; c < K; ++c) s2 = fma(R[r * K + c], fvec[tid][c], s2);
+      g2 = fma(s2, s2, g2);
+    }
+    res[tid] = g2;
+  }
   __syncthreads();
+  lz_stamp(a, q, 155);
   if (tid == 0) {
     LzState z = a.st[f];
     double gam2 = 0.0;

@@ -36,5 +36,9 @@ out = {"cfg": cfg, "store": store, "steps": rep["iterations_per"], "loop_ms": re
        "reduce_us": float(np.median(T[q, 3] - T[q, 2])),
        "sync2_us": float(np.median(T[q, 4] - T[q, 3])),
        "next_us": float(np.median(T[q + 1, 0] - T[q, 4])),
+       "red_partials_us": float(np.median(T[q, 153] - T[q, 2])),
+       "red_chol_us": float(np.median(T[q, 154] - T[q, 153])),
+       "red_shifts_us": float(np.median(T[q, 155] - T[q, 154])),
+       "red_tail_us": float(np.median(T[q, 3] - T[q, 155])),
        "tail_ms": float((T[n - 1, 4] - T[0, 0]) / 1e3)}
 print(json.dumps(out))
