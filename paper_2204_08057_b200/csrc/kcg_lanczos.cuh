@@ -326,6 +326,9 @@ __device__ __forceinline__ void lz_pass(const LzArgs& a, const CUtensorMap* vmap
               w[c] = HITS ? s2 / h : s2;
             }
           }
+          double v2[K];  // V_{q-2} at the pixel, loaded once (not once per output component)
+#pragma unroll
+          for (int d = 0; d < K; ++d) v2[d] = q >= 3 ? B2[d * C::BH * C::BW + bi] : 0.0;
 #pragma unroll
           for (int c = 0; c < K; ++c) {
             double s2 = 0.0;
@@ -337,7 +340,7 @@ __device__ __forceinline__ void lz_pass(const LzArgs& a, const CUtensorMap* vmap
             }
             if (q >= 3) {
 #pragma unroll
-              for (int d = 0; d < K; ++d) s2 = fma(-B2[d * C::BH * C::BW + bi], r2(d * K + c), s2);
+              for (int d = 0; d < K; ++d) s2 = fma(-v2[d], r2(d * K + c), s2);
             }
             v[c] = s2;
           }
@@ -430,10 +433,13 @@ __device__ __forceinline__ void lz_pass(const LzArgs& a, const CUtensorMap* vmap
             w[c] = HITS ? s2 / h : s2;
           }
           if (q >= 2) {
+            double vo[K];  // V_{q-1} at the pixel
+#pragma unroll
+            for (int d = 0; d < K; ++d) vo[d] = B1[d * C::BH * C::BW + bi];
 #pragma unroll
             for (int c = 0; c < K; ++c)
 #pragma unroll
-              for (int d = 0; d < K; ++d) w[c] = fma(-B1[d * C::BH * C::BW + bi], rb(c * K + d), w[c]);
+              for (int d = 0; d < K; ++d) w[c] = fma(-vo[d], rb(c * K + d), w[c]);
           }
 #pragma unroll
           for (int c = 0; c < K; ++c)
