@@ -329,20 +329,34 @@ __device__ __forceinline__ void lz_pass(const LzArgs& a, const CUtensorMap* vmap
           double v2[K];  // V_{q-2} at the pixel, loaded once (not once per output component)
 #pragma unroll
           for (int d = 0; d < K; ++d) v2[d] = q >= 3 ? B2[d * C::BH * C::BW + bi] : 0.0;
+          if constexpr (C::REGG) {  // K <= 4: one chain per component (register-bound)
 #pragma unroll
-          for (int c = 0; c < K; ++c) {
-            double s2 = 0.0;
+            for (int c = 0; c < K; ++c) {
+              double s2 = 0.0;
 #pragma unroll
-            for (int d = 0; d < K; ++d) s2 = fma(w[d], rr(d * K + c), s2);
-            if (q >= 2) {
+              for (int d = 0; d < K; ++d) s2 = fma(w[d], rr(d * K + c), s2);
+              if (q >= 2) {
 #pragma unroll
-              for (int d = 0; d < K; ++d) s2 = fma(-v1[d], r1(d * K + c), s2);
+                for (int d = 0; d < K; ++d) s2 = fma(-v1[d], r1(d * K + c), s2);
+              }
+              if (q >= 3) {
+#pragma unroll
+                for (int d = 0; d < K; ++d) s2 = fma(-v2[d], r2(d * K + c), s2);
+              }
+              v[c] = s2;
             }
-            if (q >= 3) {
+          } else {  // K > 4: three independent product chains per component (latency-bound)
 #pragma unroll
-              for (int d = 0; d < K; ++d) s2 = fma(-v2[d], r2(d * K + c), s2);
+            for (int c = 0; c < K; ++c) {
+              double sa = 0.0, sb = 0.0, sc = 0.0;
+#pragma unroll
+              for (int d = 0; d < K; ++d) {
+                sa = fma(w[d], rr(d * K + c), sa);
+                sb = fma(v1[d], r1(d * K + c), sb);
+                sc = fma(v2[d], r2(d * K + c), sc);
+              }
+              v[c] = q >= 3 ? sa - (sb + sc) : (q >= 2 ? sa - sb : sa);
             }
-            v[c] = s2;
           }
         }
 #pragma unroll
@@ -437,9 +451,17 @@ __device__ __forceinline__ void lz_pass(const LzArgs& a, const CUtensorMap* vmap
 #pragma unroll
             for (int d = 0; d < K; ++d) vo[d] = B1[d * C::BH * C::BW + bi];
 #pragma unroll
-            for (int c = 0; c < K; ++c)
+            for (int c = 0; c < K; ++c) {
+              if constexpr (C::REGG) {
 #pragma unroll
-              for (int d = 0; d < K; ++d) w[c] = fma(-vo[d], rb(c * K + d), w[c]);
+                for (int d = 0; d < K; ++d) w[c] = fma(-vo[d], rb(c * K + d), w[c]);
+              } else {
+                double t2 = 0.0;
+#pragma unroll
+                for (int d = 0; d < K; ++d) t2 = fma(vo[d], rb(c * K + d), t2);
+                w[c] -= t2;
+              }
+            }
           }
 #pragma unroll
           for (int c = 0; c < K; ++c)
