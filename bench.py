@@ -201,6 +201,26 @@ def _cpu_baseline(problems, gpu_iters_per_patch, budget_s=20.0):
             "cg_iters_per_s": 1.0 / t_it}
 
 
+def _cpu_baseline_lanczos(problems, steps_per_face, budget_steps=None):
+    """Oracle block Lanczos (oracle.lanczos, Alg. SylvSolver step by step, numpy/scipy as it stands)
+    on face 0 to convergence, 1 BLAS thread; extrapolated to the full sky by the faces' step counts
+    (its per-step cost grows with the step: eigh of T_i every step, so this is an estimate)."""
+    from threadpoolctl import threadpool_limits
+    from oracle import lanczos
+    p = problems[0]
+    with threadpool_limits(limits=1):
+        t0 = time.perf_counter()
+        r = lanczos.problem_solve(p, tol=TOL, max_iter=budget_steps or 100000)
+        t = time.perf_counter() - t0
+    per_step = t / max(r.iterations, 1)
+    t_sky = per_step * sum(steps_per_face)
+    return {"value": 1.0 / t_sky, "unit": "full-sky solves/s", "cores": 1, "kind": "oracle",
+            "sample": (f"oracle.lanczos (Alg. SylvSolver, literal sparse N^-1 Q0, eigh of T_i per step) on face 0 "
+                       f"of {len(problems)}: {r.iterations} steps in {t:.2f} s (L={p.level}, k={p.k}); "
+                       f"extrapolated to {sum(steps_per_face)} face-steps"),
+            "s_face0": t}
+
+
 def run_reference(args):
     """--impl reference: the oracle as it stands, timed on the host cores (rank 0 only)."""
     world, rank, _ = _dist()
@@ -251,7 +271,7 @@ def run_reference(args):
     return 0
 
 
-def _lanczos_leg(problems, st, dev, timed, args):
+def _lanczos_leg(problems, st, dev, timed, args, cpu=False):
     """The paper's block-Lanczos Sylvester solver (Alg. SylvSolver, sylvester_lanczos_solve) on this
     rank's faces: HBM-resident basis (lanczos_store) sized for the oracle's step counts, inputs
     resident; its own context (the basis is not part of the CG workspace)."""
@@ -277,6 +297,8 @@ def _lanczos_leg(problems, st, dev, timed, args):
                         "frac": b / tl / 1e9 / peak, "traffic": None,
                         "kernel": "lanczos_kernel + lz_assemble_kernel", "peak_source": peak_src,
                         "algorithmic_bytes_per_launch": b / len(reps), "avg_launch_ms": tl / len(reps) * 1e3}}
+    if cpu and not args.no_cpu_baseline:
+        out["cpu_baseline"] = _cpu_baseline_lanczos(problems, reps[-1]["iterations_per"])
     del ctx, Y, mu
     torch.cuda.empty_cache()
     return out
@@ -391,7 +413,7 @@ def run_b200(args):
     t_e2e, reps_e2e = timed(host, max(1, args.e2e_steps))
     lz = None
     if g == 1 and not args.no_lanczos:
-        lz = _lanczos_leg(problems, st, dev, timed, args)
+        lz = _lanczos_leg(problems, st, dev, timed, args, cpu=(world == 1))
     paper = None
     if world == 1 and not args.no_paper:
         paper = _paper_leg(dev, timed, args)
