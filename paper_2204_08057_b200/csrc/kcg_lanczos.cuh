@@ -904,48 +904,92 @@ __global__ void __launch_bounds__(256, 1)
 }
 
 // M = sum_q V_q G_q from the HBM-resident basis (store mode): one streaming pass over the blocks.
+// Work units = (face, 512-pixel chunk), faces interleaved so every CTA gets a mix of step counts;
+// a thread owns a pixel pair (double2), four blocks q in flight; G_q of the unit's face staged in
+// shared memory.  Per pixel the sum runs q-major, d-minor -- the replay's order (bitwise equal M).
+#define LZ_ASM_ZMAX 2048  // doubles of G_q staged per unit (longer bases stream from L1/L2)
 template <int K>
 __global__ void __launch_bounds__(256) lz_assemble_kernel(const LzArgs a) {
-  const int f = blockIdx.y;
-  const int it = a.st[f].iters;
+  __shared__ double zs[LZ_ASM_ZMAX];
   const size_t N = (size_t)a.side * a.side, pstride = (size_t)a.pitch * a.side;
-  const double* Z = a.Zs + (size_t)f * a.cap * K * K;
-  for (size_t px = (size_t)blockIdx.x * blockDim.x + threadIdx.x; px < N; px += (size_t)gridDim.x * blockDim.x) {
-    const size_t gy = px / a.side, gx = px - gy * a.side;
-    const size_t off = gy * a.pitch + gx;
-    double m[K];
+  const bool pairs = (a.side & 1) == 0;
+  const size_t per = pairs ? 512 : 256;
+  const size_t nch = (N + per - 1) / per;
+  for (size_t u = blockIdx.x; u < (size_t)a.P * nch; u += gridDim.x) {
+    const int f = (int)(u % a.P);
+    const size_t ch = u / a.P;
+    const int it = __ldcg(&a.st[f].iters);
+    const double* Zg = a.Zs + (size_t)f * a.cap * K * K;
+    const int nz = min(it * K * K, LZ_ASM_ZMAX);
+    __syncthreads();
+    for (int e = threadIdx.x; e < nz; e += blockDim.x) zs[e] = __ldcg(Zg + e);
+    __syncthreads();
+    auto Z = [&](int q, int e) { const int o = (q - 1) * K * K + e; return o < LZ_ASM_ZMAX ? zs[o] : __ldg(Zg + o); };
+    if (pairs) {
+      const size_t px = ch * per + 2 * threadIdx.x;
+      if (px >= N) continue;
+      const size_t gy = px / a.side, gx = px - gy * a.side;
+      const size_t off = gy * a.pitch + gx;
+      double2 m[K];
 #pragma unroll
-    for (int c = 0; c < K; ++c) m[c] = 0.0;
-    int q = 1;
-    for (; q + 1 <= it; q += 2) {
-      double v0[K], v1[K];
-      const double* b0 = a.V + ((size_t)(q * a.P + f) * K) * pstride + off;
-      const double* b1 = a.V + ((size_t)((q + 1) * a.P + f) * K) * pstride + off;
+      for (int c = 0; c < K; ++c) m[c] = make_double2(0.0, 0.0);
+      int q = 1;
+      for (; q + 3 <= it; q += 4) {
+        double2 v[4][K];
 #pragma unroll
-      for (int d = 0; d < K; ++d) { v0[d] = __ldcs(b0 + d * pstride); v1[d] = __ldcs(b1 + d * pstride); }
-      const double* z0 = Z + (size_t)(q - 1) * K * K;
-      // same order as the replay: all of block q, then block q + 1 (bitwise-identical M)
+        for (int r = 0; r < 4; ++r) {
+          const double* b = a.V + ((size_t)((q + r) * a.P + f) * K) * pstride + off;
 #pragma unroll
-      for (int c = 0; c < K; ++c) {
+          for (int d = 0; d < K; ++d) v[r][d] = __ldcs(reinterpret_cast<const double2*>(b + d * pstride));
+        }
 #pragma unroll
-        for (int d = 0; d < K; ++d) m[c] = fma(v0[d], __ldg(z0 + d * K + c), m[c]);
+        for (int r = 0; r < 4; ++r)
 #pragma unroll
-        for (int d = 0; d < K; ++d) m[c] = fma(v1[d], __ldg(z0 + K * K + d * K + c), m[c]);
+          for (int c = 0; c < K; ++c)
+#pragma unroll
+            for (int d = 0; d < K; ++d) {
+              const double z = Z(q + r, d * K + c);
+              m[c].x = fma(v[r][d].x, z, m[c].x);
+              m[c].y = fma(v[r][d].y, z, m[c].y);
+            }
       }
+      for (; q <= it; ++q) {
+        const double* b = a.V + ((size_t)(q * a.P + f) * K) * pstride + off;
+        double2 v[K];
+#pragma unroll
+        for (int d = 0; d < K; ++d) v[d] = __ldcs(reinterpret_cast<const double2*>(b + d * pstride));
+#pragma unroll
+        for (int c = 0; c < K; ++c)
+#pragma unroll
+          for (int d = 0; d < K; ++d) {
+            const double z = Z(q, d * K + c);
+            m[c].x = fma(v[d].x, z, m[c].x);
+            m[c].y = fma(v[d].y, z, m[c].y);
+          }
+      }
+#pragma unroll
+      for (int c = 0; c < K; ++c) *reinterpret_cast<double2*>(a.Mx + ((size_t)f * K + c) * N + px) = m[c];
+    } else {  // side == 1
+      const size_t px = ch * per + threadIdx.x;
+      if (px >= N) continue;
+      const size_t gy = px / a.side, gx = px - gy * a.side;
+      const size_t off = gy * a.pitch + gx;
+      double m[K];
+#pragma unroll
+      for (int c = 0; c < K; ++c) m[c] = 0.0;
+      for (int q = 1; q <= it; ++q) {
+        const double* b = a.V + ((size_t)(q * a.P + f) * K) * pstride + off;
+        double v[K];
+#pragma unroll
+        for (int d = 0; d < K; ++d) v[d] = b[d * pstride];
+#pragma unroll
+        for (int c = 0; c < K; ++c)
+#pragma unroll
+          for (int d = 0; d < K; ++d) m[c] = fma(v[d], Z(q, d * K + c), m[c]);
+      }
+#pragma unroll
+      for (int c = 0; c < K; ++c) a.Mx[((size_t)f * K + c) * N + px] = m[c];
     }
-    if (q <= it) {
-      const double* b0 = a.V + ((size_t)(q * a.P + f) * K) * pstride + off;
-      const double* z0 = Z + (size_t)(q - 1) * K * K;
-      double v0[K];
-#pragma unroll
-      for (int d = 0; d < K; ++d) v0[d] = __ldcs(b0 + d * pstride);
-#pragma unroll
-      for (int c = 0; c < K; ++c)
-#pragma unroll
-        for (int d = 0; d < K; ++d) m[c] = fma(v0[d], __ldg(z0 + d * K + c), m[c]);
-    }
-#pragma unroll
-    for (int c = 0; c < K; ++c) a.Mx[((size_t)f * K + c) * N + px] = m[c];
   }
 }
 
@@ -993,8 +1037,9 @@ cudaError_t LzEntry<K>::assemble(cudaStream_t s, const LzArgs& a) {
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
   const size_t N = (size_t)a.side * a.side;
-  const int bx = (int)std::max<size_t>(1, std::min<size_t>((N + 255) / 256, (size_t)nsm * 8 / std::max(1, a.P) + 1));
-  lz_assemble_kernel<K><<<dim3(bx, a.P), 256, 0, s>>>(a);
+  const size_t units = (size_t)a.P * ((N + 511) / 512);
+  const int bx = (int)std::max<size_t>(1, std::min<size_t>(units, (size_t)nsm * 8));
+  lz_assemble_kernel<K><<<bx, 256, 0, s>>>(a);
   return cudaGetLastError();
 }
 
