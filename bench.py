@@ -304,6 +304,24 @@ def _lanczos_leg(problems, st, dev, timed, args, cpu=False):
     return out
 
 
+def _variance_leg(ctx, timed, args, n_probes=4):
+    """Posterior variances (posterior_variance: Hutchinson) on this rank's faces:
+    one step = n_probes probes, each one batched CG solve of every face with b = the probe."""
+    fn = lambda: ctx.posterior_variance(n_probes, seed=11, tol=TOL)[1]
+    r = fn()
+    assert r["status"] == 0, r["status_name"]
+    t, reps = timed(fn, max(1, args.steps // 2))
+    peak, peak_src = _peaks()
+    b = sum(r["loop_bytes"] for r in reps)
+    tl = sum(r["loop_time_s"] for r in reps)
+    return {"value": len(reps) * n_probes / t, "unit": "probe solves/s (all faces of the rank per probe)",
+            "probes_per_step": n_probes, "ms_per_step": t / len(reps) * 1e3,
+            "face_iterations_per_probe": reps[-1]["system_iterations"] / n_probes,
+            "roofline": {"bound": "hbm", "achieved": b / tl / 1e9, "peak": peak, "unit": "GB/s",
+                         "frac": b / tl / 1e9 / peak, "traffic": None, "kernel": "cg_persistent_kernel",
+                         "peak_source": peak_src}}
+
+
 def _paper_leg(dev, timed, args, level=10, faces=12):
     """The paper's own workload on the full sky: App. B physical A and printed T,
     phi = 1, Q0 = D^2 with kappa2 = 0, random hits 1..4, HEALPix NESTED order, 12 faces at level 10
@@ -414,6 +432,9 @@ def run_b200(args):
     lz = None
     if g == 1 and not args.no_lanczos:
         lz = _lanczos_leg(problems, st, dev, timed, args, cpu=(world == 1))
+    var = None
+    if g == 1 and not args.no_variance:
+        var = _variance_leg(ctx, timed, args)
     paper = None
     if world == 1 and not args.no_paper:
         paper = _paper_leg(dev, timed, args)
@@ -501,10 +522,18 @@ def run_b200(args):
         line["lanczos"] = lz
     if paper is not None:
         line["paper_workload"] = paper
+    if var is not None:
+        line["posterior_variance"] = var
     if world == 1 and not args.no_slab_probe:
         line["slab_emulation"] = _slab_probe(dev)
     if world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = _cpu_baseline(problems, reps[-1]["iterations_per"])
+        if var is not None:  # the oracle's Hutchinson probe = one oracle CG solve per face
+            cb = line["cpu_baseline"]
+            t_probe = len(problems) * cb["s_assembly"] + var["face_iterations_per_probe"] * cb["s_per_face_iteration"]
+            var["cpu_baseline"] = {"value": 1.0 / t_probe, "unit": var["unit"], "cores": 1, "kind": "oracle",
+                                   "sample": "oracle.variance.hutchinson = oracle.cg.cg_hs per probe and face; "
+                                             "timed by the Kron-CG sample above (same CG, same operator)"}
     print(json.dumps(line), flush=True)
     if world > 1:
         dist.barrier()
@@ -525,6 +554,7 @@ def main():
     ap.add_argument("--no-slab-probe", action="store_true")
     ap.add_argument("--no-lanczos", action="store_true", help="skip the block-Lanczos (Alg. SylvSolver) leg")
     ap.add_argument("--no-paper", action="store_true", help="skip the paper-workload leg (App. B physics, D^2)")
+    ap.add_argument("--no-variance", action="store_true", help="skip the posterior-variance (Hutchinson) leg")
     ap.add_argument("--lanczos-cap", type=int, default=128,
                     help="Lanczos steps provisioned (HBM-resident basis: P k N 8 (cap + 1) bytes)")
     ap.add_argument("--ref-iters", type=int, default=8, help="oracle CG iterations per reference step")
