@@ -1019,6 +1019,9 @@ __device__ __forceinline__ void cg_tile_d2(const CgArgs& a, const TileCtx& tc, d
   // Phase B1: r_new = r - alpha (h M p + tau (kappa2 p + D S)) on box rows/cols [2, BH-2)
   constexpr int B1W = TX + 4, B1H = TY + 4;
   const double* __restrict__ Msh = tc.Ms;
+  double Mr[K * K];  // the mixing matrix in registers (not K^2 shared loads per point)
+#pragma unroll
+  for (int e2 = 0; e2 < K * K; ++e2) Mr[e2] = Msh[e2];
   for (int e0 = 0; e0 < B1W * B1H; e0 += NT) {
     const int e = e0 + tid;
     if (e < B1W * B1H) {
@@ -1035,7 +1038,7 @@ __device__ __forceinline__ void cg_tile_d2(const CgArgs& a, const TileCtx& tc, d
         for (int c = 0; c < K; ++c) {
           double mix = 0.0;
 #pragma unroll
-          for (int d = 0; d < K; ++d) mix = fma(Msh[c * K + d], pc[d], mix);
+          for (int d = 0; d < K; ++d) mix = fma(Mr[c * K + d], pc[d], mix);
           const double d2p = Dat(S, c * SPL - BW, by, bx, deg);  // S row = box row - 1
           const double q = fma(h, mix, tau[c] * fma(kappa2, pc[c], d2p));
           double* rp = R + c * PLANE + by * BW + bx;
@@ -1106,6 +1109,9 @@ __device__ __forceinline__ void cg_tile_d2(const CgArgs& a, const TileCtx& tc, d
 #pragma unroll
       for (int c = 0; c < K; ++c) vc[c] = V[c * VPL + by * BW + bx];
       double* xp = a.x + ((size_t)s * K * side + gy) * side + gx;
+      double xo[K];  // x loads issued before the point's arithmetic (L2 latency overlapped)
+#pragma unroll
+      for (int c = 0; c < K; ++c) xo[c] = tc.xpass ? __ldcg(xp + c * N) : 0.0;
       const size_t ro = ((size_t)s * K) * ps + (size_t)gy * a.pitch + gx;
       double* rout = (tc.par ? a.rbuf[0] : a.rbuf[1]) + ro;
       double* pout = (tc.par ? a.pbuf[0] : a.pbuf[1]) + ro;
@@ -1113,7 +1119,7 @@ __device__ __forceinline__ void cg_tile_d2(const CgArgs& a, const TileCtx& tc, d
       for (int c = 0; c < K; ++c) {
         double mix = 0.0;
 #pragma unroll
-        for (int d = 0; d < K; ++d) mix = fma(Msh[c * K + d], vc[d], mix);
+        for (int d = 0; d < K; ++d) mix = fma(Mr[c * K + d], vc[d], mix);
         const double d2v = Dat(S, c * SPL - BW, by, bx, deg);
         const double w = fma(h, mix, tau[c] * fma(kappa2, vc[c], d2v));
         const double rn = R[c * PLANE + by * BW + bx];
@@ -1123,7 +1129,7 @@ __device__ __forceinline__ void cg_tile_d2(const CgArgs& a, const TileCtx& tc, d
         wu = fma(w, vc[c], wu);
         if (tc.xpass) {
           const double po = tc.pold[((size_t)c * TY + ty) * TX + tx];
-          xp[c * N] = __ldcg(xp + c * N) + fma(alpha, pn, ap * po);
+          xp[c * N] = xo[c] + fma(alpha, pn, ap * po);
         }
         rout[c * ps] = rn;
         pout[c * ps] = pn;
