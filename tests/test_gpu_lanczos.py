@@ -186,3 +186,28 @@ def test_lanczos_d2_planck_vs_exact():
     ctx, Y, mu, rep = _run(ps, cap=300, store=True, prior="d2")
     assert rep["converged"]
     assert rel(mu[0], exact.problem_dct_exact(ps[0])) <= 1e-8
+
+
+def test_lanczos_host_entry_point_matches_device():
+    """sylvester_lanczos_solve_host: Y from host memory in, mu to host memory out (copies timed)."""
+    import torch
+    ps = [make_patch(6, 9, 3, seed=610 + s, tau="loguniform") for s in range(2)]
+    ctx, Y = make_ctx(ps, lanczos_cap=200, host_staging=True)
+    mu_d, rep_d = ctx.lanczos(Y, tol=TOL)
+    mu_h, rep_h = ctx.solve_host(Y.cpu().pin_memory(), tol=TOL, route="lanczos")
+    assert rep_h["iterations_per"] == rep_d["iterations_per"]
+    assert np.array_equal(mu_h.numpy(), _np(mu_d))
+    assert rep_h["wall_time_s"] >= rep_h["loop_time_s"] > 0
+
+
+def test_lanczos_configuration_errors():
+    from paper_2204_08057_b200.kroncg import KcgError, KCG_E_CONFIG
+    ps = [make_patch(5, 9, 3, seed=620)]
+    ctx, Y = make_ctx(ps)                       # no lanczos_cap: route not provisioned
+    with pytest.raises(KcgError) as e:
+        ctx.lanczos(Y, tol=TOL)
+    assert e.value.status == KCG_E_CONFIG
+    ps5 = [make_patch(5, 9, 5, seed=621, prior="d2")]
+    with pytest.raises(KcgError) as e:          # D^2 block Lanczos is built for k <= 4
+        make_ctx(ps5, lanczos_cap=50)
+    assert e.value.status == KCG_E_CONFIG
