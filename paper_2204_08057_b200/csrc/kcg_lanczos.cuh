@@ -31,7 +31,9 @@ struct LzCfg {
   static constexpr int HB = D2 ? 4 : 2;                // box halo: V_{i-1} is needed on the tile + 2 RR ring
   static constexpr int RR = D2 ? 2 : 1;                // ring of V_i (the operator's radius)
   static constexpr int BW = TX + 2 * HB, BH = TY + 2 * HB;
-  static constexpr int RW = TX + 2 * RR, RH = TY + 2 * RR, RN = RW * RH;  // V_i region
+  // K <= 4 Laplacian: pixel-pair mapping, the V_i region spans the box columns (16-byte aligned pairs)
+  static constexpr bool PAIRS = !D2 && K <= 4;
+  static constexpr int RW = PAIRS ? BW : TX + 2 * RR, RH = TY + 2 * RR, RN = RW * RH;  // V_i region
   static constexpr int BOX = K * BH * BW;
   static constexpr int STAGES = D2 ? 2 : (K <= 2 ? 3 : (K <= 5 ? 2 : 1));  // TMA tiles in flight
   static constexpr int KP = (2 * K + 3) / 4 * 4;      // Gram rows [V, W] padded to 4
@@ -263,226 +265,393 @@ __device__ __forceinline__ void lz_pass(const LzArgs& a, const CUtensorMap* vmap
     const double* B1 = sm + s * 2 * C::BOX;
     const double* B2 = B1 + C::BOX;
 
-    // ---- D2: D V_{q-1} on the tile + 3 ring (D v := 0 outside the face; D = -L, P:L100-106)
-    if constexpr (D2) {
-      if (mode != LZ_GRAM0 && q >= 2) {
-        for (int e = tid; e < K * C::DW * C::DH; e += C::NT) {
-          const int c = e / (C::DW * C::DH), r = e - c * (C::DW * C::DH);
-          const int dy = r / C::DW, dx = r - dy * C::DW;
-          const int gy = y0 - 3 + dy, gx = x0 - 3 + dx;
-          double d = 0.0;
-          if (gy >= 0 && gy < side && gx >= 0 && gx < side) {
-            const double* p = B1 + c * C::BH * C::BW + (dy + C::HB - 3) * C::BW + dx + C::HB - 3;
-            d = (p[-C::BW] + p[C::BW] + p[-1] + p[1]) - (double)lz_deg(gy, gx, side) * p[0];
-          }
-          Dv[e] = d;
-        }
-        __syncthreads();
-      }
-    }
-    // ---- step A: V_q on the tile + RR ring (zero outside the face: free boundary, reading R2)
-    {
-      // this tile's step-A matrices: registers for K <= 4, shared memory (broadcast) above
-      constexpr int NR = C::REGG ? K * K : 1;
-      double r1v[NR], r2v[NR], rrv[NR];
-      if constexpr (C::REGG) {
+    if constexpr (C::PAIRS) {
+      // ---- step A (pairs): V_q on box columns [0, BW) x ring rows; U col = box col, U row = box row - 1
+      {
+        double rrv[K * K], r1v[K * K], r2v[K * K];
 #pragma unroll
         for (int e2 = 0; e2 < K * K; ++e2) { rrv[e2] = Ri[e2]; r1v[e2] = P1m[e2]; r2v[e2] = P2m[e2]; }
-      }
-      auto rr = [&](int i) { if constexpr (C::REGG) return rrv[i]; else return Ri[i]; };
-      auto r1 = [&](int i) { if constexpr (C::REGG) return r1v[i]; else return P1m[i]; };
-      auto r2 = [&](int i) { if constexpr (C::REGG) return r2v[i]; else return P2m[i]; };
-      for (int e = tid; e < C::RN; e += C::NT) {
-        const int ry = e / C::RW, rx = e - ry * C::RW;
-        const int gy = y0 - C::RR + ry, gx = x0 - C::RR + rx;
-        const int bi = (ry + C::HB - C::RR) * C::BW + rx + C::HB - C::RR;
-        double v[K];
-        if (gy < 0 || gy >= side || gx < 0 || gx >= side) {
+        constexpr int NPR = C::BW / 2;  // pairs per row
+        for (int e = tid; e < C::RH * NPR; e += C::NT) {
+          const int ry = e / NPR, bc = 2 * (e - ry * NPR);
+          const int gy = y0 - 1 + ry, gx = x0 - C::HB + bc;
+          const int bi = (ry + 1) * C::BW + bc;
+          const bool rowin = gy >= 0 && gy < side;
+          // the outermost box columns have no outer neighbour; their V_q is not needed
+          const bool f0 = rowin && bc > 0 && gx >= 0 && gx < side;
+          const bool f1 = rowin && bc + 2 < C::BW && gx + 1 >= 0 && gx + 1 < side;
+          double2 v[K];
+          if (!f0 && !f1) {
 #pragma unroll
-          for (int c = 0; c < K; ++c) v[c] = 0.0;
-        } else if (mode == LZ_GRAM0) {
-#pragma unroll
-          for (int c = 0; c < K; ++c) v[c] = B1[c * C::BH * C::BW + bi];
-        } else {
-          double w[K], v1[K];
-#pragma unroll
-          for (int c = 0; c < K; ++c) v1[c] = B1[c * C::BH * C::BW + bi];
-          if (q == 1) {
-#pragma unroll
-            for (int c = 0; c < K; ++c) w[c] = v1[c];
-          } else {
-            const double kd = kap + (double)lz_deg(gy, gx, side);
-            const double h = HITS ? __ldg(hp + (size_t)gy * side + gx) : 1.0;
+            for (int c = 0; c < K; ++c) v[c] = make_double2(0.0, 0.0);
+          } else if (mode == LZ_GRAM0) {
 #pragma unroll
             for (int c = 0; c < K; ++c) {
-              double s2;
-              if constexpr (D2) {  // Q0 v = D (D v) + kappa2 v
-                const double* d = Dv + c * C::DW * C::DH + (ry + 3 - C::RR) * C::DW + rx + 3 - C::RR;
-                s2 = fma(kap, v1[c], (d[-C::DW] + d[C::DW] + d[-1] + d[1]) - (kd - kap) * d[0]);
-              } else {             // Q0 v = (kappa2 + deg) v - sum_nbr v
-                const double* p = B1 + c * C::BH * C::BW + bi;
-                s2 = fma(kd, v1[c], -(p[-C::BW] + p[C::BW] + p[-1] + p[1]));
-              }
-              w[c] = HITS ? s2 / h : s2;
+              const double2 b = *reinterpret_cast<const double2*>(B1 + c * C::BH * C::BW + bi);
+              v[c] = make_double2(f0 ? b.x : 0.0, f1 ? b.y : 0.0);
             }
-          }
-          double v2[K];  // V_{q-2} at the pixel, loaded once (not once per output component)
+          } else {
+            double2 w[K], v1[K];
 #pragma unroll
-          for (int d = 0; d < K; ++d) v2[d] = q >= 3 ? B2[d * C::BH * C::BW + bi] : 0.0;
-          if constexpr (C::REGG) {  // K <= 4: one chain per component (register-bound)
+            for (int c = 0; c < K; ++c) v1[c] = *reinterpret_cast<const double2*>(B1 + c * C::BH * C::BW + bi);
+            if (q == 1) {
+#pragma unroll
+              for (int c = 0; c < K; ++c) w[c] = v1[c];
+            } else {
+              const double kd0 = kap + (double)lz_deg(gy, gx, side), kd1 = kap + (double)lz_deg(gy, gx + 1, side);
+              const double h0 = HITS && f0 ? __ldg(hp + (size_t)gy * side + gx) : 1.0;
+              const double h1 = HITS && f1 ? __ldg(hp + (size_t)gy * side + gx + 1) : 1.0;
+#pragma unroll
+              for (int c = 0; c < K; ++c) {
+                const double* p = B1 + c * C::BH * C::BW + bi;
+                const double2 up = *reinterpret_cast<const double2*>(p - C::BW);
+                const double2 dn = *reinterpret_cast<const double2*>(p + C::BW);
+                const double l = f0 ? p[-1] : 0.0, r = f1 ? p[2] : 0.0;
+                const double s0 = fma(kd0, v1[c].x, -(((up.x + dn.x) + l) + v1[c].y));
+                const double s1 = fma(kd1, v1[c].y, -(((up.y + dn.y) + v1[c].x) + r));
+                w[c] = make_double2(HITS ? s0 / h0 : s0, HITS ? s1 / h1 : s1);
+              }
+            }
+            double2 v2[K];
+#pragma unroll
+            for (int d = 0; d < K; ++d)
+              v2[d] = q >= 3 ? *reinterpret_cast<const double2*>(B2 + d * C::BH * C::BW + bi) : make_double2(0.0, 0.0);
 #pragma unroll
             for (int c = 0; c < K; ++c) {
-              double s2 = 0.0;
+              double sx = 0.0, sy = 0.0;
 #pragma unroll
-              for (int d = 0; d < K; ++d) s2 = fma(w[d], rr(d * K + c), s2);
+              for (int d = 0; d < K; ++d) { sx = fma(w[d].x, rrv[d * K + c], sx); sy = fma(w[d].y, rrv[d * K + c], sy); }
               if (q >= 2) {
 #pragma unroll
-                for (int d = 0; d < K; ++d) s2 = fma(-v1[d], r1(d * K + c), s2);
+                for (int d = 0; d < K; ++d) { sx = fma(-v1[d].x, r1v[d * K + c], sx); sy = fma(-v1[d].y, r1v[d * K + c], sy); }
               }
               if (q >= 3) {
 #pragma unroll
-                for (int d = 0; d < K; ++d) s2 = fma(-v2[d], r2(d * K + c), s2);
+                for (int d = 0; d < K; ++d) { sx = fma(-v2[d].x, r2v[d * K + c], sx); sy = fma(-v2[d].y, r2v[d * K + c], sy); }
               }
-              v[c] = s2;
-            }
-          } else {  // K > 4: three independent product chains per component (latency-bound)
-#pragma unroll
-            for (int c = 0; c < K; ++c) {
-              double sa = 0.0, sb = 0.0, sc = 0.0;
-#pragma unroll
-              for (int d = 0; d < K; ++d) {
-                sa = fma(w[d], rr(d * K + c), sa);
-                sb = fma(v1[d], r1(d * K + c), sb);
-                sc = fma(v2[d], r2(d * K + c), sc);
-              }
-              v[c] = q >= 3 ? sa - (sb + sc) : (q >= 2 ? sa - sb : sa);
+              v[c] = make_double2(f0 ? sx : 0.0, f1 ? sy : 0.0);
             }
           }
-        }
 #pragma unroll
-        for (int c = 0; c < K; ++c) U[c * C::RN + e] = v[c];
-      }
-    }
-    __syncthreads();
-
-    // ---- D2: D V_q on the tile + 1 ring
-    if constexpr (D2) {
-      if (mode == LZ_STEP) {
-        constexpr int W1 = C::TX + 2, H1 = C::TY + 2;
-        for (int e = tid; e < K * W1 * H1; e += C::NT) {
-          const int c = e / (W1 * H1), r = e - c * (W1 * H1);
-          const int dy = r / W1, dx = r - dy * W1;
-          const int gy = y0 - 1 + dy, gx = x0 - 1 + dx;
-          double d = 0.0;
-          if (gy >= 0 && gy < side && gx >= 0 && gx < side) {
-            const double* p = U + c * C::RN + (dy + C::RR - 1) * C::RW + dx + C::RR - 1;
-            d = (p[-C::RW] + p[C::RW] + p[-1] + p[1]) - (double)lz_deg(gy, gx, side) * p[0];
-          }
-          Dv[e] = d;
+          for (int c = 0; c < K; ++c) *reinterpret_cast<double2*>(U + c * C::RN + ry * C::RW + bc) = v[c];
         }
-        __syncthreads();
       }
-    }
-    // ---- step B: W_q on the tile (or the replay's M update); store V_q; Gram (K <= 4: in registers)
-    {
-      constexpr int NRB = C::REGG ? K * K : 1;
-      double rbv[NRB];
-      const double* rbs = mode == LZ_REPLAY ? Zm : Bc;
-      if constexpr (C::REGG) {
+      __syncthreads();
+      // ---- step B (pairs): W_q on the tile, store V_q, Gram in registers (or the replay's M update)
+      {
+        double rbv[K * K];
+        const double* rbs = mode == LZ_REPLAY ? Zm : Bc;
 #pragma unroll
         for (int e2 = 0; e2 < K * K; ++e2) rbv[e2] = rbs[e2];
-      }
-      auto rb = [&](int i) { if constexpr (C::REGG) return rbv[i]; else return rbs[i]; };
-      for (int e = tid; e < C::NPIX; e += C::NT) {
-        const int ly = e / C::TX, lx = e - ly * C::TX;
-        const int gy = y0 + ly, gx = x0 + lx;
-        const int ri = (ly + C::RR) * C::RW + lx + C::RR;
-        const int bi = (ly + C::HB) * C::BW + lx + C::HB;
-        const bool in = gy < side && gx < side;
-        if (mode == LZ_REPLAY) {
-          if (in) {
-            const size_t px = (size_t)gy * side + gx;
-            const size_t N = (size_t)side * side;
+        constexpr int NPT = C::TX / 2;
+        const size_t N = (size_t)side * side;
+        for (int e = tid; e < C::TY * NPT; e += C::NT) {
+          const int ly = e / NPT, lx = 2 * (e - ly * NPT);
+          const int gy = y0 + ly, gx = x0 + lx;
+          const int ri = (ly + 1) * C::RW + lx + C::HB;
+          const int bi = (ly + C::HB) * C::BW + lx + C::HB;
+          const bool in0 = gy < side && gx < side, in1 = gy < side && gx + 1 < side;
+          double2 vq[K];
+#pragma unroll
+          for (int c = 0; c < K; ++c) vq[c] = *reinterpret_cast<const double2*>(U + c * C::RN + ri);
+          if (mode == LZ_REPLAY) {
+            if (in0) {
+              const size_t px = (size_t)gy * side + gx;
+#pragma unroll
+              for (int c = 0; c < K; ++c) {
+                double* mp = a.Mx + ((size_t)f * K + c) * N + px;
+                double mx = q > 1 ? mp[0] : 0.0, my = (q > 1 && in1) ? mp[1] : 0.0;
+#pragma unroll
+                for (int d = 0; d < K; ++d) { mx = fma(vq[d].x, rbv[d * K + c], mx); my = fma(vq[d].y, rbv[d * K + c], my); }
+                mp[0] = mx;
+                if (in1) mp[1] = my;
+                if (q < its_f) {
+                  double* vp = a.V + ((size_t)(slotq * a.P + f) * K + c) * pstride + (size_t)gy * a.pitch + gx;
+                  vp[0] = vq[c].x;
+                  if (in1) vp[1] = vq[c].y;
+                }
+              }
+            }
+            continue;
+          }
+          double2 w[K];
+          double h0 = 1.0, h1 = 1.0;
+          if (mode == LZ_GRAM0) {
+            if (HITS) { h0 = in0 ? __ldg(hp + (size_t)gy * side + gx) : 0.0; h1 = in1 ? __ldg(hp + (size_t)gy * side + gx + 1) : 0.0; }
+#pragma unroll
+            for (int c = 0; c < K; ++c) w[c] = make_double2(0.0, 0.0);
+          } else {
+            const double kd0 = kap + (double)lz_deg(gy, gx, side), kd1 = kap + (double)lz_deg(gy, gx + 1, side);
+            if (HITS) { h0 = in0 ? __ldg(hp + (size_t)gy * side + gx) : 1.0; h1 = in1 ? __ldg(hp + (size_t)gy * side + gx + 1) : 1.0; }
 #pragma unroll
             for (int c = 0; c < K; ++c) {
-              double m = q > 1 ? a.Mx[((size_t)f * K + c) * N + px] : 0.0;
-#pragma unroll
-              for (int d = 0; d < K; ++d) m = fma(U[d * C::RN + ri], rb(d * K + c), m);
-              a.Mx[((size_t)f * K + c) * N + px] = m;
+              const double* p = U + c * C::RN + ri;
+              const double2 up = *reinterpret_cast<const double2*>(p - C::RW);
+              const double2 dn = *reinterpret_cast<const double2*>(p + C::RW);
+              const double s0 = fma(kd0, vq[c].x, -(((up.x + dn.x) + p[-1]) + vq[c].y));
+              const double s1 = fma(kd1, vq[c].y, -(((up.y + dn.y) + vq[c].x) + p[2]));
+              w[c] = make_double2(HITS ? s0 / h0 : s0, HITS ? s1 / h1 : s1);
             }
-            if (q < its_f) {
+            if (q >= 2) {
+              double2 vo[K];
+#pragma unroll
+              for (int d = 0; d < K; ++d) vo[d] = *reinterpret_cast<const double2*>(B1 + d * C::BH * C::BW + bi);
 #pragma unroll
               for (int c = 0; c < K; ++c)
-                a.V[((size_t)(slotq * a.P + f) * K + c) * pstride + (size_t)gy * a.pitch + gx] = U[c * C::RN + ri];
+#pragma unroll
+                for (int d = 0; d < K; ++d) {
+                  w[c].x = fma(-vo[d].x, rbv[c * K + d], w[c].x);
+                  w[c].y = fma(-vo[d].y, rbv[c * K + d], w[c].y);
+                }
             }
-          }
-          continue;
-        }
-        double w[K], vq[K];
-        double h = 1.0;
+            if (in0) {
 #pragma unroll
-        for (int c = 0; c < K; ++c) vq[c] = U[c * C::RN + ri];
-        if (!in) {
-          h = 0.0;
-#pragma unroll
-          for (int c = 0; c < K; ++c) w[c] = 0.0;
-        } else if (mode == LZ_GRAM0) {
-          if (HITS) h = __ldg(hp + (size_t)gy * side + gx);
-#pragma unroll
-          for (int c = 0; c < K; ++c) w[c] = 0.0;
-        } else {
-          const double kd = kap + (double)lz_deg(gy, gx, side);
-          if (HITS) h = __ldg(hp + (size_t)gy * side + gx);
-#pragma unroll
-          for (int c = 0; c < K; ++c) {
-            double s2;
-            if constexpr (D2) {
-              constexpr int W1 = C::TX + 2, H1 = C::TY + 2;
-              const double* d = Dv + c * W1 * H1 + (ly + 1) * W1 + lx + 1;
-              s2 = fma(kap, vq[c], (d[-W1] + d[W1] + d[-1] + d[1]) - (kd - kap) * d[0]);
-            } else {
-              const double* p = U + c * C::RN + ri;
-              s2 = fma(kd, vq[c], -(p[-C::RW] + p[C::RW] + p[-1] + p[1]));
-            }
-            w[c] = HITS ? s2 / h : s2;
-          }
-          if (q >= 2) {
-            double vo[K];  // V_{q-1} at the pixel
-#pragma unroll
-            for (int d = 0; d < K; ++d) vo[d] = B1[d * C::BH * C::BW + bi];
-#pragma unroll
-            for (int c = 0; c < K; ++c) {
-              if constexpr (C::REGG) {
-#pragma unroll
-                for (int d = 0; d < K; ++d) w[c] = fma(-vo[d], rb(c * K + d), w[c]);
-              } else {
-                double t2 = 0.0;
-#pragma unroll
-                for (int d = 0; d < K; ++d) t2 = fma(vo[d], rb(c * K + d), t2);
-                w[c] -= t2;
+              for (int c = 0; c < K; ++c) {
+                double* vp = a.V + ((size_t)(slotq * a.P + f) * K + c) * pstride + (size_t)gy * a.pitch + gx;
+                if (in1) *reinterpret_cast<double2*>(vp) = vq[c];
+                else vp[0] = vq[c].x;
               }
             }
           }
+          if (!in0) { h0 = 0.0; }
+          if (!in1) { h1 = 0.0; }
+          // N-weighted Gram of u = [V_q, W_q] at both pixels (h = 0 outside the face)
+          {
+            double u0[2 * K], u1[2 * K];
 #pragma unroll
-          for (int c = 0; c < K; ++c)
-            a.V[((size_t)(slotq * a.P + f) * K + c) * pstride + (size_t)gy * a.pitch + gx] = vq[c];
-        }
-        if constexpr (C::REGG) {
-          // N-weighted Gram of u = [V_q, W_q] at this pixel, packed upper triangle
-          double u[2 * K];
+            for (int c = 0; c < K; ++c) { u0[c] = vq[c].x; u0[K + c] = w[c].x; u1[c] = vq[c].y; u1[K + c] = w[c].y; }
+            int idx = 0;
 #pragma unroll
-          for (int c = 0; c < K; ++c) { u[c] = vq[c]; u[K + c] = w[c]; }
-          int idx = 0;
+            for (int i = 0; i < 2 * K; ++i) {
+              const double a0 = h0 * u0[i], a1 = h1 * u1[i];
 #pragma unroll
-          for (int i = 0; i < 2 * K; ++i) {
-            const double hu = HITS ? h * u[i] : u[i];
-#pragma unroll
-            for (int j = i; j < 2 * K; ++j) { acc[idx] = fma(hu, u[j], acc[idx]); ++idx; }
+              for (int j = i; j < 2 * K; ++j) { acc[idx] = fma(a1, u1[j], fma(a0, u0[j], acc[idx])); ++idx; }
+            }
           }
-        } else {
-#pragma unroll
-          for (int c = 0; c < K; ++c) U[(K + c) * C::RN + ri] = w[c];
-          if (HITS) hs[e] = h;
+        }
+      }
+    } else {
+    // ---- D2: D V_{q-1} on the tile + 3 ring (D v := 0 outside the face; D = -L, P:L100-106)
+      if constexpr (D2) {
+        if (mode != LZ_GRAM0 && q >= 2) {
+          for (int e = tid; e < K * C::DW * C::DH; e += C::NT) {
+            const int c = e / (C::DW * C::DH), r = e - c * (C::DW * C::DH);
+            const int dy = r / C::DW, dx = r - dy * C::DW;
+            const int gy = y0 - 3 + dy, gx = x0 - 3 + dx;
+            double d = 0.0;
+            if (gy >= 0 && gy < side && gx >= 0 && gx < side) {
+              const double* p = B1 + c * C::BH * C::BW + (dy + C::HB - 3) * C::BW + dx + C::HB - 3;
+              d = (p[-C::BW] + p[C::BW] + p[-1] + p[1]) - (double)lz_deg(gy, gx, side) * p[0];
+            }
+            Dv[e] = d;
+          }
+          __syncthreads();
+        }
+      }
+      // ---- step A: V_q on the tile + RR ring (zero outside the face: free boundary, reading R2)
+      {
+        // this tile's step-A matrices: registers for K <= 4, shared memory (broadcast) above
+        constexpr int NR = C::REGG ? K * K : 1;
+        double r1v[NR], r2v[NR], rrv[NR];
+        if constexpr (C::REGG) {
+  #pragma unroll
+          for (int e2 = 0; e2 < K * K; ++e2) { rrv[e2] = Ri[e2]; r1v[e2] = P1m[e2]; r2v[e2] = P2m[e2]; }
+        }
+        auto rr = [&](int i) { if constexpr (C::REGG) return rrv[i]; else return Ri[i]; };
+        auto r1 = [&](int i) { if constexpr (C::REGG) return r1v[i]; else return P1m[i]; };
+        auto r2 = [&](int i) { if constexpr (C::REGG) return r2v[i]; else return P2m[i]; };
+        for (int e = tid; e < C::RN; e += C::NT) {
+          const int ry = e / C::RW, rx = e - ry * C::RW;
+          const int gy = y0 - C::RR + ry, gx = x0 - C::RR + rx;
+          const int bi = (ry + C::HB - C::RR) * C::BW + rx + C::HB - C::RR;
+          double v[K];
+          if (gy < 0 || gy >= side || gx < 0 || gx >= side) {
+  #pragma unroll
+            for (int c = 0; c < K; ++c) v[c] = 0.0;
+          } else if (mode == LZ_GRAM0) {
+  #pragma unroll
+            for (int c = 0; c < K; ++c) v[c] = B1[c * C::BH * C::BW + bi];
+          } else {
+            double w[K], v1[K];
+  #pragma unroll
+            for (int c = 0; c < K; ++c) v1[c] = B1[c * C::BH * C::BW + bi];
+            if (q == 1) {
+  #pragma unroll
+              for (int c = 0; c < K; ++c) w[c] = v1[c];
+            } else {
+              const double kd = kap + (double)lz_deg(gy, gx, side);
+              const double h = HITS ? __ldg(hp + (size_t)gy * side + gx) : 1.0;
+  #pragma unroll
+              for (int c = 0; c < K; ++c) {
+                double s2;
+                if constexpr (D2) {  // Q0 v = D (D v) + kappa2 v
+                  const double* d = Dv + c * C::DW * C::DH + (ry + 3 - C::RR) * C::DW + rx + 3 - C::RR;
+                  s2 = fma(kap, v1[c], (d[-C::DW] + d[C::DW] + d[-1] + d[1]) - (kd - kap) * d[0]);
+                } else {             // Q0 v = (kappa2 + deg) v - sum_nbr v
+                  const double* p = B1 + c * C::BH * C::BW + bi;
+                  s2 = fma(kd, v1[c], -(p[-C::BW] + p[C::BW] + p[-1] + p[1]));
+                }
+                w[c] = HITS ? s2 / h : s2;
+              }
+            }
+            double v2[K];  // V_{q-2} at the pixel, loaded once (not once per output component)
+  #pragma unroll
+            for (int d = 0; d < K; ++d) v2[d] = q >= 3 ? B2[d * C::BH * C::BW + bi] : 0.0;
+            if constexpr (C::REGG) {  // K <= 4: one chain per component (register-bound)
+  #pragma unroll
+              for (int c = 0; c < K; ++c) {
+                double s2 = 0.0;
+  #pragma unroll
+                for (int d = 0; d < K; ++d) s2 = fma(w[d], rr(d * K + c), s2);
+                if (q >= 2) {
+  #pragma unroll
+                  for (int d = 0; d < K; ++d) s2 = fma(-v1[d], r1(d * K + c), s2);
+                }
+                if (q >= 3) {
+  #pragma unroll
+                  for (int d = 0; d < K; ++d) s2 = fma(-v2[d], r2(d * K + c), s2);
+                }
+                v[c] = s2;
+              }
+            } else {  // K > 4: three independent product chains per component (latency-bound)
+  #pragma unroll
+              for (int c = 0; c < K; ++c) {
+                double sa = 0.0, sb = 0.0, sc = 0.0;
+  #pragma unroll
+                for (int d = 0; d < K; ++d) {
+                  sa = fma(w[d], rr(d * K + c), sa);
+                  sb = fma(v1[d], r1(d * K + c), sb);
+                  sc = fma(v2[d], r2(d * K + c), sc);
+                }
+                v[c] = q >= 3 ? sa - (sb + sc) : (q >= 2 ? sa - sb : sa);
+              }
+            }
+          }
+  #pragma unroll
+          for (int c = 0; c < K; ++c) U[c * C::RN + e] = v[c];
+        }
+      }
+      __syncthreads();
+  
+      // ---- D2: D V_q on the tile + 1 ring
+      if constexpr (D2) {
+        if (mode == LZ_STEP) {
+          constexpr int W1 = C::TX + 2, H1 = C::TY + 2;
+          for (int e = tid; e < K * W1 * H1; e += C::NT) {
+            const int c = e / (W1 * H1), r = e - c * (W1 * H1);
+            const int dy = r / W1, dx = r - dy * W1;
+            const int gy = y0 - 1 + dy, gx = x0 - 1 + dx;
+            double d = 0.0;
+            if (gy >= 0 && gy < side && gx >= 0 && gx < side) {
+              const double* p = U + c * C::RN + (dy + C::RR - 1) * C::RW + dx + C::RR - 1;
+              d = (p[-C::RW] + p[C::RW] + p[-1] + p[1]) - (double)lz_deg(gy, gx, side) * p[0];
+            }
+            Dv[e] = d;
+          }
+          __syncthreads();
+        }
+      }
+      // ---- step B: W_q on the tile (or the replay's M update); store V_q; Gram (K <= 4: in registers)
+      {
+        constexpr int NRB = C::REGG ? K * K : 1;
+        double rbv[NRB];
+        const double* rbs = mode == LZ_REPLAY ? Zm : Bc;
+        if constexpr (C::REGG) {
+  #pragma unroll
+          for (int e2 = 0; e2 < K * K; ++e2) rbv[e2] = rbs[e2];
+        }
+        auto rb = [&](int i) { if constexpr (C::REGG) return rbv[i]; else return rbs[i]; };
+        for (int e = tid; e < C::NPIX; e += C::NT) {
+          const int ly = e / C::TX, lx = e - ly * C::TX;
+          const int gy = y0 + ly, gx = x0 + lx;
+          const int ri = (ly + C::RR) * C::RW + lx + C::RR;
+          const int bi = (ly + C::HB) * C::BW + lx + C::HB;
+          const bool in = gy < side && gx < side;
+          if (mode == LZ_REPLAY) {
+            if (in) {
+              const size_t px = (size_t)gy * side + gx;
+              const size_t N = (size_t)side * side;
+  #pragma unroll
+              for (int c = 0; c < K; ++c) {
+                double m = q > 1 ? a.Mx[((size_t)f * K + c) * N + px] : 0.0;
+  #pragma unroll
+                for (int d = 0; d < K; ++d) m = fma(U[d * C::RN + ri], rb(d * K + c), m);
+                a.Mx[((size_t)f * K + c) * N + px] = m;
+              }
+              if (q < its_f) {
+  #pragma unroll
+                for (int c = 0; c < K; ++c)
+                  a.V[((size_t)(slotq * a.P + f) * K + c) * pstride + (size_t)gy * a.pitch + gx] = U[c * C::RN + ri];
+              }
+            }
+            continue;
+          }
+          double w[K], vq[K];
+          double h = 1.0;
+  #pragma unroll
+          for (int c = 0; c < K; ++c) vq[c] = U[c * C::RN + ri];
+          if (!in) {
+            h = 0.0;
+  #pragma unroll
+            for (int c = 0; c < K; ++c) w[c] = 0.0;
+          } else if (mode == LZ_GRAM0) {
+            if (HITS) h = __ldg(hp + (size_t)gy * side + gx);
+  #pragma unroll
+            for (int c = 0; c < K; ++c) w[c] = 0.0;
+          } else {
+            const double kd = kap + (double)lz_deg(gy, gx, side);
+            if (HITS) h = __ldg(hp + (size_t)gy * side + gx);
+  #pragma unroll
+            for (int c = 0; c < K; ++c) {
+              double s2;
+              if constexpr (D2) {
+                constexpr int W1 = C::TX + 2, H1 = C::TY + 2;
+                const double* d = Dv + c * W1 * H1 + (ly + 1) * W1 + lx + 1;
+                s2 = fma(kap, vq[c], (d[-W1] + d[W1] + d[-1] + d[1]) - (kd - kap) * d[0]);
+              } else {
+                const double* p = U + c * C::RN + ri;
+                s2 = fma(kd, vq[c], -(p[-C::RW] + p[C::RW] + p[-1] + p[1]));
+              }
+              w[c] = HITS ? s2 / h : s2;
+            }
+            if (q >= 2) {
+              double vo[K];  // V_{q-1} at the pixel
+  #pragma unroll
+              for (int d = 0; d < K; ++d) vo[d] = B1[d * C::BH * C::BW + bi];
+  #pragma unroll
+              for (int c = 0; c < K; ++c) {
+                if constexpr (C::REGG) {
+  #pragma unroll
+                  for (int d = 0; d < K; ++d) w[c] = fma(-vo[d], rb(c * K + d), w[c]);
+                } else {
+                  double t2 = 0.0;
+  #pragma unroll
+                  for (int d = 0; d < K; ++d) t2 = fma(vo[d], rb(c * K + d), t2);
+                  w[c] -= t2;
+                }
+              }
+            }
+  #pragma unroll
+            for (int c = 0; c < K; ++c)
+              a.V[((size_t)(slotq * a.P + f) * K + c) * pstride + (size_t)gy * a.pitch + gx] = vq[c];
+          }
+          if constexpr (C::REGG) {
+            // N-weighted Gram of u = [V_q, W_q] at this pixel, packed upper triangle
+            double u[2 * K];
+  #pragma unroll
+            for (int c = 0; c < K; ++c) { u[c] = vq[c]; u[K + c] = w[c]; }
+            int idx = 0;
+  #pragma unroll
+            for (int i = 0; i < 2 * K; ++i) {
+              const double hu = HITS ? h * u[i] : u[i];
+  #pragma unroll
+              for (int j = i; j < 2 * K; ++j) { acc[idx] = fma(hu, u[j], acc[idx]); ++idx; }
+            }
+          } else {
+  #pragma unroll
+            for (int c = 0; c < K; ++c) U[(K + c) * C::RN + ri] = w[c];
+            if (HITS) hs[e] = h;
+          }
         }
       }
     }
