@@ -294,7 +294,8 @@ def _lanczos_leg(problems, st, dev, timed, args, cpu=False):
            "lanczos_steps_per_face": reps[-1]["iterations_per"], "mode": "hbm-resident basis (lanczos_store)",
            "true_rel_residual": reps[-1]["rel_residual_true"],
            "roofline": {"bound": "hbm", "achieved": b / tl / 1e9, "peak": peak, "unit": "GB/s",
-                        "frac": b / tl / 1e9 / peak, "traffic": None,
+                        "frac": b / tl / 1e9 / peak, "traffic": _traffic(args.config, "lanczos"),
+                        "traffic_note": "ncu dram bytes of the lanczos_kernel launch alone (profiles/ncu_traffic.json)",
                         "kernel": "lanczos_kernel + lz_assemble_kernel", "peak_source": peak_src,
                         "algorithmic_bytes_per_launch": b / len(reps), "avg_launch_ms": tl / len(reps) * 1e3}}
     if cpu and not args.no_cpu_baseline:
