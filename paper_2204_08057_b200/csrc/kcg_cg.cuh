@@ -932,7 +932,7 @@ __device__ __forceinline__ void flush_tile_partial(const double (*tred)[NW], dou
 //   C0  S = D v on tile + 1-ring (v = U or r_new)
 //   C1  w = h M v + tau (kappa2 v + D S) on the tile; (r,r), (r,u), (w,u); x += xinc; stores
 // Block-Jacobi diag: diag(D^2)_jj = deg_j^2 + deg_j.
-template <int K, bool HITS, bool PREC>
+template <int K, bool HITS, bool PREC, bool EDGE>
 __device__ __forceinline__ void cg_tile_d2(const CgArgs& a, const TileCtx& tc, double (*tred)[256 / 32]) {
   constexpr int TY = d2_tile_y(K), TX = KCG_TX, H = KCG_HALO2, BW = d2_box_w(), BH = TY + 2 * H;
   constexpr int PLANE = BW * BH, SPL = BW * (TY + 6), UPL = BW * (TY + 4);
@@ -949,8 +949,10 @@ __device__ __forceinline__ void cg_tile_d2(const CgArgs& a, const TileCtx& tc, d
   const double* __restrict__ Mg = tc.sp->M;
   const double* __restrict__ Kinvg = &tc.sp->Kinv[0][0];
   auto gyx = [&](int by, int bx, int& gy, int& gx) { gy = y0 - H + by; gx = x0 - H + bx; };
-  auto in_face = [&](int gy, int gx) { return gy >= 0 && gy < side && gx >= 0 && gx < side; };
-  auto degree = [&](int gy, int gx) { return 4 - (gy == 0) - (gy == side - 1) - (gx == 0) - (gx == side - 1); };
+  // interior tiles (EDGE = false: the box lies inside the face) skip every boundary test
+  auto in_face = [&](int gy, int gx) { return !EDGE || (gy >= 0 && gy < side && gx >= 0 && gx < side); };
+  auto degree_full = [&](int gy, int gx) { return 4 - (gy == 0) - (gy == side - 1) - (gx == 0) - (gx == side - 1); };
+  auto degree = [&](int gy, int gx) { return EDGE ? degree_full(gy, gx) : 4; };  // box rows/cols >= 1 only
   auto hit = [&](int gy, int gx) { return HITS ? __ldg(tc.hp + (size_t)gy * side + gx) : 1.0; };
   // K_j^{-1} r for PREC: Kinv holds (M + (kappa2 + d^2 + d) P)^{-1}, d = 2, 3, 4 (host)
   double tau[K];
@@ -974,7 +976,8 @@ __device__ __forceinline__ void cg_tile_d2(const CgArgs& a, const TileCtx& tc, d
         int gy, gx;
         gyx(by, bx, gy, gx);
         const bool f0 = in_face(gy, gx), f1 = in_face(gy, gx + 1);
-        const int d0 = f0 ? degree(gy, gx) : 4, d1 = f1 ? degree(gy, gx + 1) : 4;
+        // the outermost box ring may lie on the face boundary even for an interior tile
+        const int d0 = f0 ? degree_full(gy, gx) : 4, d1 = f1 ? degree_full(gy, gx + 1) : 4;
         precond_pixel<K, HITS>(Kinvg, Mg, tau, kappa2, HITS && f0 ? hit(gy, gx) : 1.0, d0, r0, u0, true);
         precond_pixel<K, HITS>(Kinvg, Mg, tau, kappa2, HITS && f1 ? hit(gy, gx + 1) : 1.0, d1, r1, u1, true);
       } else {
@@ -1102,7 +1105,7 @@ __device__ __forceinline__ void cg_tile_d2(const CgArgs& a, const TileCtx& tc, d
     const int ty = e / TX, tx = e - ty * TX;
     const int by = H + ty, bx = H + tx;
     const int gy = y0 + ty, gx = x0 + tx;
-    if (e < TY * TX && gy < side && gx < side) {
+    if (e < TY * TX && (!EDGE || (gy < side && gx < side))) {
       const int deg = degree(gy, gx);
       const double h = hit(gy, gx);
       double vc[K];
@@ -1323,7 +1326,8 @@ __device__ __forceinline__ void cg_body(const CgArgs& a, const CgMaps& maps, con
       const bool interior = tc.x0 >= H && tc.x0 + TX + H <= a.side && gy0 >= H && gy0 + TY + H <= a.side &&
                             tc.y0 + TY <= (SLAB ? a.rows : a.side);
       if constexpr (D2) {
-        cg_tile_d2<K, HITS, PREC>(a, tc, tred[i & 1]);
+        if (interior) cg_tile_d2<K, HITS, PREC, false>(a, tc, tred[i & 1]);
+        else cg_tile_d2<K, HITS, PREC, true>(a, tc, tred[i & 1]);
       } else if (cg_xtma(K) && xtma) {
         if (interior) cg_tile<K, false, HITS, cg_xtma(K), PREC, SLAB>(a, tc, tred[i & 1]);
         else cg_tile<K, true, HITS, cg_xtma(K), PREC, SLAB>(a, tc, tred[i & 1]);
