@@ -57,3 +57,29 @@ def exact_diag(G) -> np.ndarray:
     """diag(G^{-1}) by a dense inverse (small systems only)."""
     Gd = G.toarray() if hasattr(G, "toarray") else np.asarray(G)
     return np.diag(np.linalg.inv(Gd)).copy()
+
+
+def dct_diag_moments(level: int, A, noise_prec, tau, kappa2, prior: str = "laplacian"):
+    """hits = 1: (diag(G^-1), diag(G^-2)) [k][N] in closed form.  G = sum_ab (v_ab v_ab^T) (x) K_ab with
+    the orthonormal 2-D DCT-II modes v_ab(y, x) = u_a(y) u_b(x) and K_ab = M + lam^{Q0}_ab P (the
+    diagonalisation of oracle.exact.dct_exact), so
+        diag(G^-p)[c](y, x) = sum_a u_a(y)^2 sum_b u_b(x)^2 [K_ab^-p]_cc,   p = 1, 2,
+    evaluated as two matrix products per component.  diag(G^-2)_j = sum_l (G^-1)_jl^2 gives the
+    Hutchinson standard error at any size."""
+    A = np.asarray(A, dtype=np.float64)
+    k = A.shape[1]
+    s = 1 << level
+    t = 2.0 - 2.0 * np.cos(np.pi * np.arange(s) / s)
+    lam = t[:, None] + t[None, :]
+    lq = kappa2 + (lam if prior == "laplacian" else lam * lam)
+    M = A.T @ np.diag(np.asarray(noise_prec, dtype=np.float64)) @ A
+    P = np.diag(np.asarray(tau, dtype=np.float64))
+    Kab = M[None, None] + lq[:, :, None, None] * P[None, None]                 # (s, s, k, k)
+    Ki = np.linalg.inv(Kab)
+    Ki2 = Ki @ Ki
+    u = np.sqrt(2.0 / s) * np.cos(np.pi * np.outer(np.arange(s) + 0.5, np.arange(s)) / s)
+    u[:, 0] = np.sqrt(1.0 / s)
+    u2 = u ** 2                                                                 # [y, a]
+    d1 = np.stack([u2 @ Ki[:, :, c, c] @ u2.T for c in range(k)]).reshape(k, s * s)
+    d2 = np.stack([u2 @ Ki2[:, :, c, c] @ u2.T for c in range(k)]).reshape(k, s * s)
+    return d1, d2

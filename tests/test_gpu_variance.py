@@ -95,3 +95,20 @@ def test_posterior_variance_converges_to_the_exact_diagonal():
     d = np.diag(Gi)
     sig = np.sqrt((np.sum(Gi ** 2, axis=1) - d ** 2) / s)
     assert (np.abs(var - d) / sig).max() <= 5.0
+
+
+def test_posterior_variance_at_planck_size_within_its_standard_error():
+    """Full size (planck, L = 10, the bench's CG launch configuration): every one of the 4M entries
+    of the 8-probe estimate within 7 standard errors of the exact diagonal (DCT closed form), and the
+    RMS standardised error at the predicted scale."""
+    from synth import make_config
+    p = make_config("planck")[0]
+    ctx, _ = make_ctx([p])
+    s = 8
+    var, rep = ctx.posterior_variance(s, seed=21, tol=1e-10)
+    var = var.cpu().numpy().reshape(p.k, -1)
+    d1, d2 = variance.dct_diag_moments(p.level, p.A, p.noise_prec, p.tau, p.kappa2)
+    sig = np.sqrt((d2 - d1 ** 2) / s)
+    z = np.abs(var - d1) / sig
+    assert z.max() <= 7.0, z.max()
+    assert 0.8 < np.sqrt(np.mean(z ** 2)) < 1.2

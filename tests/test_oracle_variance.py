@@ -63,3 +63,12 @@ def test_hutchinson_with_cg_equals_exact_solves():
     a = variance.hutchinson([G], p.k, p.N, 4, seed=9)
     b = variance.hutchinson([G], p.k, p.N, 4, seed=9, solve=lambda A, z: exact.dense_solve(A, z))
     assert np.abs(a - b).max() <= 1e-8 * np.abs(b).max()
+
+
+def test_dct_diag_moments_match_the_dense_inverse():
+    p = make_patch(3, 9, 3, seed=14, tau="loguniform")
+    G, _ = model.problem_system(p)
+    Gi = np.linalg.inv(G.toarray())
+    d1, d2 = variance.dct_diag_moments(p.level, p.A, p.noise_prec, p.tau, p.kappa2)
+    assert np.allclose(d1.reshape(-1), np.diag(Gi), rtol=1e-11)
+    assert np.allclose(d2.reshape(-1), np.sum(Gi ** 2, axis=1), rtol=1e-11)
