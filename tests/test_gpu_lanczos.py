@@ -211,3 +211,15 @@ def test_lanczos_configuration_errors():
     with pytest.raises(KcgError) as e:          # D^2 block Lanczos is built for k <= 4
         make_ctx(ps5, lanczos_cap=50)
     assert e.value.status == KCG_E_CONFIG
+
+
+def test_max_level_all_routes_vs_exact():
+    """The largest face the ABI accepts (level 12: 4096 x 4096, 16.8M pixels): Kronecker CG, the
+    Sylvester route and block Lanczos (paper's two-pass mode) against the DCT-exact solution."""
+    p = make_patch(12, 4, 2, seed=700, tau="loguniform")
+    ex = exact.problem_dct_exact(p)
+    ctx, Y = make_ctx([p], lanczos_cap=400)
+    for name, fn in (("kron", ctx.solve), ("sylvester", ctx.sylvester), ("lanczos", ctx.lanczos)):
+        mu, rep = fn(Y, tol=TOL)
+        assert rep["converged"], (name, rep["status_name"])
+        assert rel(_np(mu)[0], ex) <= 1e-8, (name, rel(_np(mu)[0], ex))
