@@ -305,6 +305,34 @@ def _lanczos_leg(problems, st, dev, timed, args, cpu=False):
     return out
 
 
+def _pcg_leg(problems, st, dev, timed, args):
+    """Pixel-block-Jacobi preconditioned CG (reading R10; the paper: preconditioners "can be used",
+    P:L245) on this rank's faces: same metric, fewer iterations, same kernel structure."""
+    import torch
+    from paper_2204_08057_b200.kroncg import KronCG
+    ctx = KronCG(problems[0].level, st["A"], st["noise_prec"], st["tau"], st["kappa2"], device=dev,
+                 precond="block_jacobi")
+    Y = torch.from_numpy(st["Y"]).to(dev)
+    mu = torch.empty(ctx.shape_mu, dtype=torch.float64, device=dev)
+    fn = lambda: ctx.solve(Y, mu, tol=TOL)[1]
+    r = fn()
+    assert r["converged"], r["status_name"]
+    t, reps = timed(fn, args.steps)
+    peak, peak_src = _peaks()
+    b = sum(r["loop_bytes"] for r in reps)
+    tl = sum(r["loop_time_s"] for r in reps)
+    out = {"value": len(reps) / t, "ms_per_step": t / len(reps) * 1e3,
+           "unit": "full-sky solves/s" if args.config == "fullsky" else "solves/s",
+           "face_iterations_per_solve": reps[-1]["system_iterations"], "iterations_per_face": reps[-1]["iterations_per"],
+           "true_rel_residual": reps[-1]["rel_residual_true"],
+           "roofline": {"bound": "hbm", "achieved": b / tl / 1e9, "peak": peak, "unit": "GB/s",
+                        "frac": b / tl / 1e9 / peak, "traffic": None, "kernel": "cg_persistent_kernel (PREC)",
+                        "peak_source": peak_src}}
+    del ctx, Y, mu
+    torch.cuda.empty_cache()
+    return out
+
+
 def _variance_leg(ctx, timed, args, n_probes=4):
     """Posterior variances (posterior_variance: Hutchinson) on this rank's faces:
     one step = n_probes probes, each one batched CG solve of every face with b = the probe."""
@@ -433,6 +461,9 @@ def run_b200(args):
     lz = None
     if g == 1 and not args.no_lanczos:
         lz = _lanczos_leg(problems, st, dev, timed, args, cpu=(world == 1))
+    pcg = None
+    if g == 1 and not args.no_pcg:
+        pcg = _pcg_leg(problems, st, dev, timed, args)
     var = None
     if g == 1 and not args.no_variance:
         var = _variance_leg(ctx, timed, args)
@@ -525,6 +556,8 @@ def run_b200(args):
         line["paper_workload"] = paper
     if var is not None:
         line["posterior_variance"] = var
+    if pcg is not None:
+        line["pcg_block_jacobi"] = pcg
     if world == 1 and not args.no_slab_probe:
         line["slab_emulation"] = _slab_probe(dev)
     if world == 1 and not args.no_cpu_baseline:
@@ -556,6 +589,7 @@ def main():
     ap.add_argument("--no-lanczos", action="store_true", help="skip the block-Lanczos (Alg. SylvSolver) leg")
     ap.add_argument("--no-paper", action="store_true", help="skip the paper-workload leg (App. B physics, D^2)")
     ap.add_argument("--no-variance", action="store_true", help="skip the posterior-variance (Hutchinson) leg")
+    ap.add_argument("--no-pcg", action="store_true", help="skip the block-Jacobi preconditioned CG leg")
     ap.add_argument("--lanczos-cap", type=int, default=128,
                     help="Lanczos steps provisioned (HBM-resident basis: P k N 8 (cap + 1) bytes)")
     ap.add_argument("--ref-iters", type=int, default=8, help="oracle CG iterations per reference step")
