@@ -464,6 +464,21 @@ def run_b200(args):
     pcg = None
     if g == 1 and not args.no_pcg:
         pcg = _pcg_leg(problems, st, dev, timed, args)
+    koh = None
+    if g == 1 and not args.no_kohler:  # Alg. Kohler (NEXT-4): k sequential batched column solves
+        call = lambda: ctx.kohler(Y, mu, tol=TOL)[1]
+        rk = call()
+        assert rk["converged"], rk["status_name"]
+        tk, reps_k = timed(call, args.steps)
+        pk, pk_src = _peaks()
+        bk = sum(r["loop_bytes"] for r in reps_k)
+        tlk = sum(r["loop_time_s"] for r in reps_k)
+        koh = {"value": len(reps_k) / tk, "ms_per_step": tk / len(reps_k) * 1e3,
+               "system_iterations_per_solve": reps_k[-1]["system_iterations"],
+               "roofline": {"bound": "hbm", "achieved": bk / tlk / 1e9, "peak": pk, "unit": "GB/s",
+                            "frac": bk / tlk / 1e9 / pk, "traffic": None,
+                            "kernel": "cg_persistent_kernel (K = 1, one launch per column) + column kernels",
+                            "peak_source": pk_src}}
     var = None
     if g == 1 and not args.no_variance:
         var = _variance_leg(ctx, timed, args)
@@ -558,6 +573,8 @@ def run_b200(args):
         line["posterior_variance"] = var
     if pcg is not None:
         line["pcg_block_jacobi"] = pcg
+    if koh is not None:
+        line["kohler"] = koh
     if world == 1 and not args.no_slab_probe:
         line["slab_emulation"] = _slab_probe(dev)
     if world == 1 and not args.no_cpu_baseline:
@@ -590,6 +607,7 @@ def main():
     ap.add_argument("--no-paper", action="store_true", help="skip the paper-workload leg (App. B physics, D^2)")
     ap.add_argument("--no-variance", action="store_true", help="skip the posterior-variance (Hutchinson) leg")
     ap.add_argument("--no-pcg", action="store_true", help="skip the block-Jacobi preconditioned CG leg")
+    ap.add_argument("--no-kohler", action="store_true", help="skip the Alg. Kohler leg")
     ap.add_argument("--lanczos-cap", type=int, default=128,
                     help="Lanczos steps provisioned (HBM-resident basis: P k N 8 (cap + 1) bytes)")
     ap.add_argument("--ref-iters", type=int, default=8, help="oracle CG iterations per reference step")

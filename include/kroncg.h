@@ -157,6 +157,14 @@ KCG_API kcg_status sylvester_lanczos_solve(kcg_ctx* ctx, const double* Y_dev, do
 KCG_API kcg_status sylvester_lanczos_solve_host(kcg_ctx* ctx, const double* Y_host, double* mu_host, double tol,
                                         int max_iter, kcg_report* report);
 
+/* Alg. Kohler (Kohler's sparse-dense Sylvester solver, the paper's comparison method):
+ * real Schur factor S^ = A^T T A P^{-1} = W R W^T (canonical: ascending eigenvalues on R's diagonal,
+ * W = orthonormalised Lemma-2 eigenvectors), F^ = Y^ W, then for i = 1..k one batched CG solve of
+ * (Q0 + R_ii N_h) X^_i = N_h (F^_i - sum_{j<i} R_ji X^_j) over all patches, X = X^ W^T.  Per-column
+ * stop ||r_i|| <= tol ||rhs_i||; report->iterations_per is [P*k] (patch-major).  No row slabs.     */
+KCG_API kcg_status sylvester_kohler_solve(kcg_ctx* ctx, const double* Y_dev, double* mu_dev, double tol,
+                                  int max_iter, kcg_report* report);
+
 /* Many right-hand sides / parameter sweeps: G x = b for a GIVEN b_dev
  * [P][k][N] (user layout; each patch of the context is one system -- P copies of one parameter set
  * make P right-hand sides of one operator, P parameter sets one sweep), CG route, x0 = 0, stop on

@@ -41,7 +41,8 @@ const unsigned long long kPostTag = 1ull << 31;  // tags of the post-CG rendezvo
 struct Layout {
   size_t r0, r1, p0, p1, partials, state, history, sync, group, resid_partials, resid_out, params_kron, params_syl,
       E_kron, E_syl, W, Y_stage, mu_stage, trace, slots, flags, xg_top, xg_bot, rslots, x_rm, y_rm, hits_rm,
-      lz_V, lz_part, lz_st, lz_H, lz_R, lz_Ri, lz_Sinv, lz_g, lz_Z, lz_prm, E_lz, total;
+      lz_V, lz_part, lz_st, lz_H, lz_R, lz_Ri, lz_Sinv, lz_g, lz_Z, lz_prm, E_lz, params_koh, E_koh, R_koh, W_koh,
+      total;
   int lz_slots;
   size_t vec_doubles, partial_doubles;
 };
@@ -83,6 +84,10 @@ Layout layout_of(const kcg_desc* d, int nranks) {
   L.E_kron = take(P * n * k * 8);
   L.E_syl = take(P * n * k * 8);
   L.W = take(P * k * k * 8);
+  L.params_koh = take(P * k * sizeof(SysParams));  // Alg. Kohler: [column][patch]
+  L.E_koh = take(P * n * k * 8);
+  L.R_koh = take(P * k * k * 8);
+  L.W_koh = take(P * k * k * 8);
   L.trace = KCG_TRACE ? take((size_t)KCG_TRACE_ITERS * KCG_TRACE_COLS * 8) : 0;
   if (d->host_staging) {
     L.Y_stage = take(P * n * N * 8);
@@ -127,7 +132,8 @@ struct RankState {
   double *partials = nullptr, *history = nullptr, *resid_partials = nullptr, *resid_out = nullptr;
   SysState* state = nullptr;
   unsigned *sync = nullptr, *group = nullptr;
-  SysParams *params_kron = nullptr, *params_syl = nullptr;
+  SysParams *params_kron = nullptr, *params_syl = nullptr, *params_koh = nullptr;
+  double *E_koh = nullptr, *R_koh = nullptr, *W_koh = nullptr;
   double *E_kron = nullptr, *E_syl = nullptr, *W_dev = nullptr, *Y_stage = nullptr, *mu_stage = nullptr;
   long long* trace = nullptr;
   double *slots = nullptr, *xg_top = nullptr, *xg_bot = nullptr, *rslots = nullptr;
@@ -161,6 +167,10 @@ RankState carve(char* ws, const Layout& L, int rank, int rows, bool staging, boo
   R.resid_out = reinterpret_cast<double*>(ws + L.resid_out);
   R.params_kron = reinterpret_cast<SysParams*>(ws + L.params_kron);
   R.params_syl = reinterpret_cast<SysParams*>(ws + L.params_syl);
+  R.params_koh = reinterpret_cast<SysParams*>(ws + L.params_koh);
+  R.E_koh = reinterpret_cast<double*>(ws + L.E_koh);
+  R.R_koh = reinterpret_cast<double*>(ws + L.R_koh);
+  R.W_koh = reinterpret_cast<double*>(ws + L.W_koh);
   R.E_kron = reinterpret_cast<double*>(ws + L.E_kron);
   R.E_syl = reinterpret_cast<double*>(ws + L.E_syl);
   R.W_dev = reinterpret_cast<double*>(ws + L.W);
@@ -853,6 +863,126 @@ kcg_status lanczos_impl(kcg_ctx* c, const double* Y_in, double* mu_out, bool hos
   c->err.clear();
   return (kcg_status)worst;
 }
+
+// Alg. Kohler (reading R33): the k columns of every patch solved one after the other,
+// column i's right-hand side carrying the Schur coupling to the columns already solved; each column
+// is one batched launch of the CG kernel over the P patches (K = 1 systems, shift R_ii).
+kcg_status kohler_impl(kcg_ctx* c, const double* Y_in, double* mu_out, double tol, int max_iter, kcg_report* rep) {
+  if (!c) return KCG_E_ARG;
+  if (c->slab) { c->err = "Alg. Kohler route: no row slabs"; return KCG_E_CONFIG; }
+  if (!Y_in || !mu_out) { c->err = "null Y or mu"; return KCG_E_ARG; }
+  if (!(tol > 0.0) || !std::isfinite(tol)) { c->err = "tol must be finite and > 0"; return KCG_E_ARG; }
+  if (max_iter < 0) { c->err = "max_iter < 0"; return KCG_E_ARG; }
+  cudaStream_t s = c->stream;
+  const int P = c->P, n = c->n, k = c->k;
+  const size_t N = c->N;
+  RankState& R = c->R[0];
+  double* mur = R.x_rm ? R.x_rm : mu_out;            // X^ (working layout), then X in place
+  double* xcol = k > 1 ? R.r[1] + (size_t)P * c->pitch * c->side : mur;  // spare planes of r[1]
+  const bool nested = c->d.layout == KCG_LAYOUT_NESTED, d2 = c->d.prior == KCG_PRIOR_D2;
+  const bool prec = c->d.precond == KCG_PRECOND_BLOCK_JACOBI;
+  std::vector<SysState> st((size_t)k * P);
+  CK(cudaEventRecord(c->ev[0], s), "event");
+  CK(cudaEventRecord(c->ev[1], s), "event");
+  CgSlabLaunch* Lp = new CgSlabLaunch();
+  std::unique_ptr<CgSlabLaunch> L_owner(Lp);
+  for (int i = 0; i < k; ++i) {
+    CK(kcg::launch_kohler_rhs(k, s, Y_in, R.E_koh, R.R_koh, mur, R.hits, R.r[0], R.p[0], xcol, P, n, i, c->side,
+                              c->pitch, nested),
+       "kohler rhs kernel");
+    CgArgs& a = Lp->a[0];
+    a = CgArgs{};
+    a.params = R.params_koh + (size_t)i * P;
+    a.x = xcol;
+    a.rbuf[0] = R.r[0]; a.rbuf[1] = R.r[1];
+    a.pbuf[0] = R.p[0]; a.pbuf[1] = R.p[1];
+    a.partials = R.partials;
+    a.state_out = R.state;
+    a.history = R.history;
+    a.history_cap = 0;
+    a.hits = R.hits;
+    a.side = c->side;
+    a.pitch = c->pitch;
+    a.rows = c->rows;
+    a.row0 = 0;
+    a.ghost = 0;
+    a.n_sys = P;
+    a.tiles_x = c->tiles_x_syl;
+    a.tiles_y = c->tiles_y_syl;
+    a.tiles_per_sys = a.tiles_x * a.tiles_y;
+    a.max_iter = max_iter;
+    a.tol2 = tol * tol;
+    a.trace = nullptr;
+    a.sync = R.sync;
+    CgMaps maps = R.maps_syl;
+    a.x_tma = 0;
+    if (c->side >= 2 && (reinterpret_cast<uintptr_t>(a.x) % 16) == 0) {
+      std::string why;
+      if (!encode_xmap(&maps.x, a.x, c->side, c->rows, (size_t)P, 1, d2, &why)) { c->err = why; return KCG_E_CUDA; }
+      a.x_tma = 1;
+    }
+    CK(cudaMemsetAsync(R.sync, 0, 4 * sizeof(unsigned), s), "memset sync");
+    const int grid = std::max(1, std::min(c->grid_syl, P * a.tiles_per_sys));
+    CK(kcg::launch_cg(1, prec, d2, s, a, maps, grid, c->smem_syl), "cg kernel (kohler column)");
+    if (KCG_X2) CK(kcg::launch_xfix(1, s, R.state, R.p[0], R.p[1], xcol, P, geom_of(c, R)), "x fix-up kernel");
+    if (k > 1) CK(kcg::launch_column_copy(s, xcol, mur, P, k, i, N), "column copy kernel");
+    CK(cudaMemcpyAsync(st.data() + (size_t)i * P, R.state, P * sizeof(SysState), cudaMemcpyDeviceToHost, s), "D2H");
+  }
+  CK(kcg::launch_backtransform(k, s, R.W_koh, mur, P, N), "backtransform kernel");
+  CK(cudaEventRecord(c->ev[2], s), "event");
+  CK(kcg::launch_resid(k, s, R.params_kron, mur, Y_in, R.E_kron, R.hits, R.resid_partials, R.resid_out, P, n,
+                       geom_of(c, R), nullptr, nullptr),
+     "residual kernel");
+  if (R.x_rm) CK(kcg::launch_permute(s, R.x_rm, mu_out, (size_t)P * k, c->side, true), "permute mu");
+  c->resid_host.resize((size_t)P * 2);
+  CK(cudaMemcpyAsync(c->resid_host.data(), R.resid_out, (size_t)P * 2 * 8, cudaMemcpyDeviceToHost, s), "D2H");
+  CK(cudaEventRecord(c->ev[3], s), "event");
+  CK(cudaStreamSynchronize(s), "kohler solve");
+  int worst = KCG_OK, maxit = 0, allconv = 1;
+  long long sumit = 0, passes = 0, xpasses = 0;
+  double maxrel = 0.0;
+  for (const SysState& z : st) {
+    maxit = std::max(maxit, z.iters);
+    sumit += z.iters;
+    passes += z.iters + 1;
+    xpasses += KCG_X2 ? z.iters / 2 : z.iters;
+    maxrel = std::max(maxrel, z.rel);
+    if (z.status != kcg::ST_CONVERGED) allconv = 0;
+    int code = KCG_OK;
+    if (z.status == kcg::ST_NONFINITE) code = KCG_E_NONFINITE;
+    else if (z.status == kcg::ST_BREAKDOWN) code = KCG_E_BREAKDOWN;
+    else if (z.status == kcg::ST_MAXIT) code = KCG_NOT_CONVERGED;
+    auto rank = [](int cd) { return cd == KCG_E_NONFINITE ? 3 : cd == KCG_E_BREAKDOWN ? 2 : cd == KCG_NOT_CONVERGED ? 1 : 0; };
+    if (rank(code) > rank(worst)) worst = code;
+  }
+  double maxtrue = 0.0;
+  for (int p = 0; p < P; ++p) {
+    const double r2 = c->resid_host[(size_t)p * 2], b2 = c->resid_host[(size_t)p * 2 + 1];
+    maxtrue = std::max(maxtrue, b2 > 0 ? std::sqrt(r2 / b2) : std::sqrt(r2));
+  }
+  if (rep) {
+    float t03 = 0.f, t12 = 0.f;
+    cudaEventElapsedTime(&t03, c->ev[0], c->ev[3]);
+    cudaEventElapsedTime(&t12, c->ev[1], c->ev[2]);
+    rep->status = worst;
+    rep->converged = allconv;
+    rep->iterations = maxit;
+    rep->n_systems = P * k;
+    if (rep->iterations_per)
+      for (int p = 0; p < P; ++p)
+        for (int i = 0; i < k; ++i) rep->iterations_per[p * k + i] = st[(size_t)i * P + p].iters;
+    rep->rel_residual = maxrel;
+    rep->rel_residual_true = maxtrue;
+    rep->wall_time_s = t03 * 1e-3;
+    rep->loop_time_s = t12 * 1e-3;
+    rep->system_iterations = sumit;
+    rep->loop_bytes = (32.0 * (double)passes + 16.0 * (double)xpasses) * (double)N;
+    rep->peak_mem_bytes = c->ws_need;
+    rep->history_len = 0;
+  }
+  c->err.clear();
+  return (kcg_status)worst;
+}
 }  // namespace
 
 namespace {
@@ -971,6 +1101,61 @@ kcg_status create_impl(const kcg_desc* d, const kcg_slab* sl, const double* A_ho
       set_block_jacobi(1, sy.M, sy.tau, sy.kappa2, &sy, d2);
     }
   }
+  // Alg. Kohler (reading R33): canonical real Schur factor S^ = W R W^T of S^ = M P^{-1}:
+  // W = Q factor (modified Gram-Schmidt, positive diagonal) of the Lemma-2 eigenvectors U = P W_eig
+  // (ascending rho), R = W^T S^ W upper triangular; E = T A P^{-1} W so that F^ = Y^ W = Y E.
+  std::vector<SysParams> pko((size_t)P * k);
+  std::vector<double> Eko((size_t)P * n * k), Rko((size_t)P * k * k), Wko((size_t)P * k * k);
+  for (int p = 0; p < P; ++p) {
+    const double* A = A_host + (size_t)p * n * k;
+    const double* T = T_host + (size_t)p * n;
+    const double* phi = phi_host + (size_t)p * k;
+    const double* We = &c->W[(size_t)p * k * k];
+    std::vector<double> M((size_t)k * k, 0.0), Q((size_t)k * k, 0.0);
+    for (int a = 0; a < k; ++a)
+      for (int b = 0; b < k; ++b) {
+        double v = 0.0;
+        for (int f = 0; f < n; ++f) v += A[f * k + a] * T[f] * A[f * k + b];
+        M[a * k + b] = v;
+      }
+    for (int i = 0; i < k; ++i) {  // modified Gram-Schmidt on u_i = P w_i
+      std::vector<double> v(k);
+      for (int a = 0; a < k; ++a) v[a] = phi[a] * We[a * k + i];
+      for (int j = 0; j < i; ++j) {
+        double d = 0.0;
+        for (int a = 0; a < k; ++a) d += Q[a * k + j] * v[a];
+        for (int a = 0; a < k; ++a) v[a] -= d * Q[a * k + j];
+      }
+      double nr = 0.0;
+      for (int a = 0; a < k; ++a) nr += v[a] * v[a];
+      nr = std::sqrt(nr);
+      for (int a = 0; a < k; ++a) Q[a * k + i] = v[a] / nr;
+    }
+    double* Rp = &Rko[(size_t)p * k * k];
+    for (int i = 0; i < k; ++i)
+      for (int j = 0; j < k; ++j) {  // R = Q^T (M P^{-1}) Q
+        double v = 0.0;
+        for (int a = 0; a < k; ++a)
+          for (int b = 0; b < k; ++b) v += Q[a * k + i] * M[a * k + b] / phi[b] * Q[b * k + j];
+        Rp[i * k + j] = v;
+      }
+    for (int e = 0; e < k * k; ++e) Wko[(size_t)p * k * k + e] = Q[e];
+    for (int f = 0; f < n; ++f)
+      for (int i = 0; i < k; ++i) {
+        double v = 0.0;
+        for (int a = 0; a < k; ++a) v += T[f] * A[f * k + a] / phi[a] * Q[a * k + i];
+        Eko[((size_t)p * n + f) * k + i] = v;
+      }
+    for (int i = 0; i < k; ++i) {
+      SysParams& sy = pko[(size_t)i * P + p];
+      std::memset(&sy, 0, sizeof sy);
+      sy.M[0] = Rp[i * k + i];
+      sy.tau[0] = 1.0;
+      sy.kappa2 = kappa2_host[p];
+      sy.hits_plane = p;
+      set_block_jacobi(1, sy.M, sy.tau, sy.kappa2, &sy, d2);
+    }
+  }
   kcg_status st;
 #define CKC(call, what)                              \
   do {                                               \
@@ -994,6 +1179,11 @@ kcg_status create_impl(const kcg_desc* d, const kcg_slab* sl, const double* A_ho
     CKC(cudaMemcpyAsync(R.E_kron, Ek.data(), Ek.size() * 8, cudaMemcpyHostToDevice, c->stream), "H2D");
     CKC(cudaMemcpyAsync(R.E_syl, Es.data(), Es.size() * 8, cudaMemcpyHostToDevice, c->stream), "H2D");
     CKC(cudaMemcpyAsync(R.W_dev, c->W.data(), c->W.size() * 8, cudaMemcpyHostToDevice, c->stream), "H2D");
+    CKC(cudaMemcpyAsync(R.params_koh, pko.data(), pko.size() * sizeof(SysParams), cudaMemcpyHostToDevice, c->stream),
+        "H2D");
+    CKC(cudaMemcpyAsync(R.E_koh, Eko.data(), Eko.size() * 8, cudaMemcpyHostToDevice, c->stream), "H2D");
+    CKC(cudaMemcpyAsync(R.R_koh, Rko.data(), Rko.size() * 8, cudaMemcpyHostToDevice, c->stream), "H2D");
+    CKC(cudaMemcpyAsync(R.W_koh, Wko.data(), Wko.size() * 8, cudaMemcpyHostToDevice, c->stream), "H2D");
     if (c->slab) {  // ghost rows at the face ends stay zero; flags start at 0 (peers only raise them)
       for (int b = 0; b < 2; ++b) {
         CKC(cudaMemsetAsync(R.r[b], 0, c->L.vec_doubles * 8, c->stream), "memset r");
@@ -1098,6 +1288,11 @@ kcg_status kron_cg_solve(kcg_ctx* c, const double* Y, double* mu, double tol, in
 kcg_status sylvester_solve(kcg_ctx* c, const double* Y, double* mu, double tol, int max_iter, kcg_report* rep) {
   return solve_impl(c, ROUTE_SYL, Y, mu, false, tol, max_iter, rep);
 }
+kcg_status sylvester_kohler_solve(kcg_ctx* c, const double* Y, double* mu, double tol, int max_iter,
+                                  kcg_report* rep) {
+  return kohler_impl(c, Y, mu, tol, max_iter, rep);
+}
+
 kcg_status kron_cg_solve_b(kcg_ctx* c, const double* b, double* x, double tol, int max_iter, kcg_report* rep) {
   return solve_impl(c, ROUTE_KRON, b, x, false, tol, max_iter, rep, IN_B_USER);
 }

@@ -247,6 +247,11 @@ int apply_tiles_per_sys(int rows, int side);
 // row-major layout, j = the pixel's index in the user layout; var (=|+=) z * x, times scale.
 cudaError_t launch_probe(cudaStream_t s, double* z, int P, int K, int side, bool nested, unsigned long long seed,
                          int probe);
+// Alg. Kohler: rhs of column i (F^_i minus the Schur coupling, times N_h) and the column copy.
+cudaError_t launch_kohler_rhs(int K, cudaStream_t s, const double* Y, const double* E, const double* Rk,
+                              const double* Xh, const double* hits, double* r0, double* p0, double* x, int P, int n,
+                              int i, int side, int pitch, bool nested);
+cudaError_t launch_column_copy(cudaStream_t s, const double* src, double* dst, int P, int K, int i, size_t N);
 cudaError_t launch_var_accum(cudaStream_t s, const double* z, const double* x, double* var, size_t n, bool first,
                              double scale);
 // block-Lanczos (kcg_lanczos_*.cu): one cooperative launch runs the Lanczos passes, the residual

@@ -467,4 +467,57 @@ cudaError_t launch_var_accum(cudaStream_t s, const double* z, const double* x, d
   return cudaGetLastError();
 }
 
+// ------------------------------------------------------------------ Alg. Kohler (NEXT-4)
+// Column i of every patch: b = h (Y E[:, i] - sum_{k<i} R[k][i] Xh_k) into r0 plane p (internal
+// pitch), p0 = 0, x = 0.  E = T A P^{-1} W (F^ = Y^ W), R the upper-triangular Schur factor, Xh the
+// columns solved so far ([P][K][N], working row-major layout), Y in the user layout (NESTED gather).
+template <int K>
+__global__ void __launch_bounds__(256) kohler_rhs_kernel(const double* __restrict__ Y, const double* __restrict__ E,
+                                                         const double* __restrict__ Rk, const double* __restrict__ Xh,
+                                                         const double* __restrict__ hits, double* __restrict__ r0,
+                                                         double* __restrict__ p0, double* __restrict__ x, int n, int i,
+                                                         int side, int pitch, int nested) {
+  __shared__ double Ec[64], Rc[KCG_KMAX];
+  const int p = blockIdx.y;
+  for (int f = threadIdx.x; f < n; f += blockDim.x) Ec[f] = E[((size_t)p * n + f) * K + i];
+  if (threadIdx.x < K) Rc[threadIdx.x] = Rk[((size_t)p * K + threadIdx.x) * K + i];
+  __syncthreads();
+  const size_t N = (size_t)side * side;
+  for (size_t j = (size_t)blockIdx.x * blockDim.x + threadIdx.x; j < N; j += (size_t)gridDim.x * blockDim.x) {
+    const size_t gy = j / side, gx = j - gy * side;
+    const size_t jy = nested ? nest_of((uint32_t)gx, (uint32_t)gy) : j;
+    const double* yp = Y + (size_t)p * n * N + jy;
+    double f = 0.0;
+    for (int q = 0; q < n; ++q) f = fma(__ldg(yp + (size_t)q * N), Ec[q], f);
+    for (int k = 0; k < i; ++k) f = fma(-Rc[k], Xh[((size_t)p * K + k) * N + j], f);
+    const double h = hits ? __ldg(hits + (size_t)p * N + j) : 1.0;
+    r0[(size_t)p * pitch * side + gy * pitch + gx] = h * f;
+    p0[(size_t)p * pitch * side + gy * pitch + gx] = 0.0;
+    x[(size_t)p * N + j] = 0.0;
+  }
+}
+
+// dst[p][K][N] plane i <- src[p][N]
+__global__ void __launch_bounds__(256) column_copy_kernel(const double* __restrict__ src, double* __restrict__ dst,
+                                                          int K, int i, size_t N) {
+  const int p = blockIdx.y;
+  for (size_t j = (size_t)blockIdx.x * blockDim.x + threadIdx.x; j < N; j += (size_t)gridDim.x * blockDim.x)
+    dst[((size_t)p * K + i) * N + j] = src[(size_t)p * N + j];
+}
+
+cudaError_t launch_kohler_rhs(int K, cudaStream_t s, const double* Y, const double* E, const double* Rk,
+                              const double* Xh, const double* hits, double* r0, double* p0, double* x, int P, int n,
+                              int i, int side, int pitch, bool nested) {
+  const size_t N = (size_t)side * side;
+  dim3 gr(grid_for(N), P);
+  KCG_DISPATCH(K, (kohler_rhs_kernel<KK><<<gr, 256, 0, s>>>(Y, E, Rk, Xh, hits, r0, p0, x, n, i, side, pitch,
+                                                            nested ? 1 : 0)));
+  return cudaGetLastError();
+}
+
+cudaError_t launch_column_copy(cudaStream_t s, const double* src, double* dst, int P, int K, int i, size_t N) {
+  column_copy_kernel<<<dim3(grid_for(N), P), 256, 0, s>>>(src, dst, K, i, N);
+  return cudaGetLastError();
+}
+
 }  // namespace kcg

@@ -73,6 +73,7 @@ sylvester_solve_host = _sig("sylvester_solve_host", C.c_int, _solve_args)
 sylvester_lanczos_solve = _sig("sylvester_lanczos_solve", C.c_int, _solve_args)
 sylvester_lanczos_solve_host = _sig("sylvester_lanczos_solve_host", C.c_int, _solve_args)
 kron_cg_solve_b = _sig("kron_cg_solve_b", C.c_int, _solve_args)
+sylvester_kohler_solve = _sig("sylvester_kohler_solve", C.c_int, _solve_args)
 posterior_variance = _sig("posterior_variance", C.c_int,
                           [_ctxp, C.c_int, C.c_ulonglong, _vp, _vp, C.c_double, C.c_int, C.POINTER(kcg_report)])
 kron_cg_apply = _sig("kron_cg_apply", C.c_int, [_ctxp, _vp, _vp])
@@ -100,7 +101,7 @@ EXPORTS = ["kron_cg_workspace_size", "kron_cg_create", "kron_cg_solve", "sylvest
            "sylvester_factor", "kcg_last_error", "kcg_status_string", "kron_cg_destroy",
            "kron_cg_workspace_size_slab", "kron_cg_create_slab", "kcg_ipc_export", "kcg_ipc_import",
            "kcg_ipc_close", "sylvester_lanczos_solve", "sylvester_lanczos_solve_host",
-           "kron_cg_solve_b", "posterior_variance"]
+           "kron_cg_solve_b", "posterior_variance", "sylvester_kohler_solve"]
 
 
 class KcgError(RuntimeError):
@@ -246,6 +247,13 @@ class KronCG:
         mu = self._out(mu)
         self._check_dev(mu, self.shape_mu, "mu")
         return mu, self._solve(sylvester_lanczos_solve, Y, mu, tol, max_iter, self.P, **kw)
+
+    def kohler(self, Y, mu=None, tol=1e-10, max_iter=100000, **kw):
+        """Alg. Kohler (sylvester_kohler_solve): Schur-triangular column-by-column solves."""
+        self._check_dev(Y, self.shape_Y, "Y")
+        mu = self._out(mu)
+        self._check_dev(mu, self.shape_mu, "mu")
+        return mu, self._solve(sylvester_kohler_solve, Y, mu, tol, max_iter, self.P * self.k, **kw)
 
     def solve_b(self, b, x=None, tol=1e-10, max_iter=100000, **kw):
         """G x = b for given right-hand sides b: CUDA [P][k][side][side] (kron_cg_solve_b)."""
