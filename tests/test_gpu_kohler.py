@@ -68,3 +68,14 @@ def test_kohler_nested_is_a_permutation():
                    hits=torch.from_numpy(nest(st["hits"])).cuda(), layout="nested")
     mu_n, _ = ctx_n.kohler(torch.from_numpy(nest(st["Y"])).cuda(), tol=TOL)
     assert np.array_equal(mu_n.cpu().numpy(), nest(mu_r.cpu().numpy()))
+
+
+def test_kohler_with_block_jacobi_columns():
+    """precond = block_jacobi: each column's shifted system preconditioned by its diagonal (the
+    k = 1 block Jacobi); same solution as the oracle's unpreconditioned Kohler to the tolerance."""
+    ps = [make_patch(6, 9, 4, seed=850 + s, tau="loguniform", hits="random") for s in range(2)]
+    ctx, Y = make_ctx(ps, precond="block_jacobi")
+    mu, rep = ctx.kohler(Y, tol=TOL)
+    assert rep["converged"]
+    for i, p in enumerate(ps):
+        assert rel(mu.cpu().numpy()[i], kohler.problem_solve(p, tol=TOL).x) <= 1e-8

@@ -112,3 +112,13 @@ def test_posterior_variance_at_planck_size_within_its_standard_error():
     z = np.abs(var - d1) / sig
     assert z.max() <= 7.0, z.max()
     assert 0.8 < np.sqrt(np.mean(z ** 2)) < 1.2
+
+
+def test_posterior_variance_d2_prior_with_hits():
+    """The paper's operator (D^2 prior, random hits): GPU estimate == oracle estimate, same probes."""
+    ps = [make_patch(5, 9, 3, seed=570 + s, tau="loguniform", prior="d2", hits="random") for s in range(2)]
+    ctx, _ = make_ctx(ps)
+    var, rep = ctx.posterior_variance(4, seed=9, tol=TOL)
+    var = var.cpu().numpy().reshape(2, -1)
+    ref = variance.hutchinson([model.problem_system(p)[0] for p in ps], 3, ps[0].N, 4, seed=9, tol=TOL)
+    assert np.abs(var - ref).max() <= 1e-8 * np.abs(ref).max()
