@@ -42,7 +42,13 @@ struct LzCfg {
   static constexpr bool REGG = K <= 4;                 // Gram accumulated in registers in step B
   static constexpr int NPART = REGG ? K * (2 * K + 1) : NJOB * 16;
   static constexpr int NACC = REGG ? K * (2 * K + 1) : 16;
-  static constexpr int NT = 256;
+#ifndef KCG_LZ_WIDE
+#define KCG_LZ_WIDE 0
+#endif
+  // KCG_LZ_WIDE: 512 threads (16 warps, <= 128 registers, step matrices in shared memory) for the
+  // pair-mapped K <= 4 Laplacian kernel instead of 256 threads with register-resident matrices
+  static constexpr int NT = (PAIRS && KCG_LZ_WIDE) ? 512 : 256;
+  static constexpr bool REGM = !(PAIRS && KCG_LZ_WIDE);
   static constexpr int SL = NT / NJOB;                // pixel slices per Gram block
   static constexpr int NPIX = TX * TY;
   static constexpr int UPL = REGG ? K : KP;           // U = [V_i; (K > 4: W_i; 0 pad)] on the V_i region
@@ -53,7 +59,7 @@ struct LzCfg {
   static constexpr int OFF_DV = OFF_HS + (REGG ? 0 : NPIX);
   static constexpr int OFF_MAT = OFF_DV + DVN;        // P1, P2, Ri, Bc, Z (K x K each)
   static constexpr int OFF_RED = OFF_MAT + 5 * K * K; // flush scratch [NT][4]
-  static constexpr int DOUBLES = OFF_RED + NT * 4;
+  static constexpr int DOUBLES = OFF_RED + (REGG ? (NT / 32) * NACC : NT * 4);
   static constexpr size_t SMEM = (size_t)DOUBLES * 8 + 64;  // + mbarriers
   // reducer scratch (in the box area, idle between passes)
   static constexpr int SC_GAM = 0;                          // raw Gram [NPART]
@@ -268,9 +274,15 @@ __device__ __forceinline__ void lz_pass(const LzArgs& a, const CUtensorMap* vmap
     if constexpr (C::PAIRS) {
       // ---- step A (pairs): V_q on box columns [0, BW) x ring rows; U col = box col, U row = box row - 1
       {
-        double rrv[K * K], r1v[K * K], r2v[K * K];
+        constexpr int NRM = C::REGM ? K * K : 1;
+        double rrr[NRM], r1r[NRM], r2r[NRM];
+        if constexpr (C::REGM) {
 #pragma unroll
-        for (int e2 = 0; e2 < K * K; ++e2) { rrv[e2] = Ri[e2]; r1v[e2] = P1m[e2]; r2v[e2] = P2m[e2]; }
+          for (int e2 = 0; e2 < K * K; ++e2) { rrr[e2] = Ri[e2]; r1r[e2] = P1m[e2]; r2r[e2] = P2m[e2]; }
+        }
+        auto rrv = [&](int i2) { if constexpr (C::REGM) return rrr[i2]; else return Ri[i2]; };
+        auto r1v = [&](int i2) { if constexpr (C::REGM) return r1r[i2]; else return P1m[i2]; };
+        auto r2v = [&](int i2) { if constexpr (C::REGM) return r2r[i2]; else return P2m[i2]; };
         constexpr int NPR = C::BW / 2;  // pairs per row
         for (int e = tid; e < C::RH * NPR; e += C::NT) {
           const int ry = e / NPR, bc = 2 * (e - ry * NPR);
@@ -320,14 +332,14 @@ __device__ __forceinline__ void lz_pass(const LzArgs& a, const CUtensorMap* vmap
             for (int c = 0; c < K; ++c) {
               double sx = 0.0, sy = 0.0;
 #pragma unroll
-              for (int d = 0; d < K; ++d) { sx = fma(w[d].x, rrv[d * K + c], sx); sy = fma(w[d].y, rrv[d * K + c], sy); }
+              for (int d = 0; d < K; ++d) { const double m2 = rrv(d * K + c); sx = fma(w[d].x, m2, sx); sy = fma(w[d].y, m2, sy); }
               if (q >= 2) {
 #pragma unroll
-                for (int d = 0; d < K; ++d) { sx = fma(-v1[d].x, r1v[d * K + c], sx); sy = fma(-v1[d].y, r1v[d * K + c], sy); }
+                for (int d = 0; d < K; ++d) { const double m2 = r1v(d * K + c); sx = fma(-v1[d].x, m2, sx); sy = fma(-v1[d].y, m2, sy); }
               }
               if (q >= 3) {
 #pragma unroll
-                for (int d = 0; d < K; ++d) { sx = fma(-v2[d].x, r2v[d * K + c], sx); sy = fma(-v2[d].y, r2v[d * K + c], sy); }
+                for (int d = 0; d < K; ++d) { const double m2 = r2v(d * K + c); sx = fma(-v2[d].x, m2, sx); sy = fma(-v2[d].y, m2, sy); }
               }
               v[c] = make_double2(f0 ? sx : 0.0, f1 ? sy : 0.0);
             }
@@ -339,10 +351,14 @@ __device__ __forceinline__ void lz_pass(const LzArgs& a, const CUtensorMap* vmap
       __syncthreads();
       // ---- step B (pairs): W_q on the tile, store V_q, Gram in registers (or the replay's M update)
       {
-        double rbv[K * K];
+        constexpr int NRB = C::REGM ? K * K : 1;
+        double rbr[NRB];
         const double* rbs = mode == LZ_REPLAY ? Zm : Bc;
+        if constexpr (C::REGM) {
 #pragma unroll
-        for (int e2 = 0; e2 < K * K; ++e2) rbv[e2] = rbs[e2];
+          for (int e2 = 0; e2 < K * K; ++e2) rbr[e2] = rbs[e2];
+        }
+        auto rbv = [&](int i2) { if constexpr (C::REGM) return rbr[i2]; else return rbs[i2]; };
         constexpr int NPT = C::TX / 2;
         const size_t N = (size_t)side * side;
         for (int e = tid; e < C::TY * NPT; e += C::NT) {
@@ -362,7 +378,7 @@ __device__ __forceinline__ void lz_pass(const LzArgs& a, const CUtensorMap* vmap
                 double* mp = a.Mx + ((size_t)f * K + c) * N + px;
                 double mx = q > 1 ? mp[0] : 0.0, my = (q > 1 && in1) ? mp[1] : 0.0;
 #pragma unroll
-                for (int d = 0; d < K; ++d) { mx = fma(vq[d].x, rbv[d * K + c], mx); my = fma(vq[d].y, rbv[d * K + c], my); }
+                for (int d = 0; d < K; ++d) { const double m2 = rbv(d * K + c); mx = fma(vq[d].x, m2, mx); my = fma(vq[d].y, m2, my); }
                 mp[0] = mx;
                 if (in1) mp[1] = my;
                 if (q < its_f) {
@@ -400,8 +416,9 @@ __device__ __forceinline__ void lz_pass(const LzArgs& a, const CUtensorMap* vmap
               for (int c = 0; c < K; ++c)
 #pragma unroll
                 for (int d = 0; d < K; ++d) {
-                  w[c].x = fma(-vo[d].x, rbv[c * K + d], w[c].x);
-                  w[c].y = fma(-vo[d].y, rbv[c * K + d], w[c].y);
+                  const double m2 = rbv(c * K + d);
+                  w[c].x = fma(-vo[d].x, m2, w[c].x);
+                  w[c].y = fma(-vo[d].y, m2, w[c].y);
                 }
             }
             if (in0) {
@@ -989,7 +1006,7 @@ __device__ void lz_coeffs(const LzArgs& a, int f, double* sm) {
 
 // ------------------------------------------------------------------------- the persistent kernel
 template <int K, bool HITS, bool D2>
-__global__ void __launch_bounds__(256, 1)
+__global__ void __launch_bounds__(LzCfg<K, D2>::NT, 1)
     lanczos_kernel(const __grid_constant__ LzArgs a, const __grid_constant__ CUtensorMap vmap) {
   using C = LzCfg<K, D2>;
   extern __shared__ __align__(128) double sm[];
@@ -1185,7 +1202,8 @@ cudaError_t LzEntry<K>::config(bool hits, bool d2, int* max_grid, size_t* smem) 
   int dev = 0, nsm = 0, per = 0;
   if ((e = cudaGetDevice(&dev)) != cudaSuccess) return e;
   if ((e = cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev)) != cudaSuccess) return e;
-  if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, f, 256, sm)) != cudaSuccess) return e;
+  const int nt = d2 ? LzCfg<K, (K <= 4)>::NT : LzCfg<K, false>::NT;
+  if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, f, nt, sm)) != cudaSuccess) return e;
   *max_grid = std::min(per * nsm, KCG_LZ_GRID_MAX);
   *smem = sm;
   return cudaSuccess;
@@ -1197,7 +1215,8 @@ cudaError_t LzEntry<K>::launch(bool hits, bool d2, cudaStream_t s, const LzArgs&
   void* args[2] = {(void*)&a, (void*)&vmap};
   const void* f = lz_kernel_sel<K>(hits, d2);
   if (!f) return cudaErrorInvalidValue;
-  return cudaLaunchCooperativeKernel(f, dim3(grid), dim3(256), args, smem, s);
+  const int nt = d2 ? LzCfg<K, (K <= 4)>::NT : LzCfg<K, false>::NT;
+  return cudaLaunchCooperativeKernel(f, dim3(grid), dim3(nt), args, smem, s);
 }
 
 template <int K>
