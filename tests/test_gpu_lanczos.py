@@ -223,3 +223,21 @@ def test_max_level_all_routes_vs_exact():
         mu, rep = fn(Y, tol=TOL)
         assert rep["converged"], (name, rep["status_name"])
         assert rel(_np(mu)[0], ex) <= 1e-8, (name, rel(_np(mu)[0], ex))
+
+
+def test_lanczos_nonfinite_and_rank_deficient_inputs():
+    """NaN in the data -> KCG_E_NONFINITE; a rank-deficient starting block Y^ (identical maps make
+    Y T A P^{-1} rank one for k = 3) -> the Cholesky QR of B_0 breaks down: KCG_E_BREAKDOWN."""
+    from paper_2204_08057_b200.kroncg import KcgError, KCG_E_NONFINITE, KCG_E_BREAKDOWN
+    ps = [make_patch(4, 9, 3, seed=630)]
+    ctx, Y = make_ctx(ps, lanczos_cap=50)
+    Yn = Y.clone()
+    Yn[0, 2, 3, 3] = float("nan")
+    with pytest.raises(KcgError) as e:
+        ctx.lanczos(Yn, tol=TOL)
+    assert e.value.status == KCG_E_NONFINITE
+    Yr = Y.clone()
+    Yr[0] = Y[0, :1].expand_as(Y[0])                  # every map the same: Y has rank one
+    with pytest.raises(KcgError) as e:
+        ctx.lanczos(Yr.contiguous(), tol=TOL)
+    assert e.value.status == KCG_E_BREAKDOWN
