@@ -136,6 +136,48 @@ __device__ __forceinline__ bool w_spdinv(const double* S, double* R, double* X, 
   return ok;
 }
 
+// Single-thread register versions for K <= 4 (the reduction's critical path: no warp barriers).
+template <int K>
+__device__ __forceinline__ bool r_chol(const double (&Cm)[K][K], double (&R)[K][K]) {  // C = R^T R, R upper
+  bool ok = true;
+#pragma unroll
+  for (int j = 0; j < K; ++j) {
+    double d = Cm[j][j];
+#pragma unroll
+    for (int k = 0; k < j; ++k) d = fma(-R[k][j], R[k][j], d);
+    ok = ok && (d > 0.0) && isfinite(d);
+    const double rjj = sqrt(d > 0.0 ? d : 0.0);
+    R[j][j] = rjj;
+#pragma unroll
+    for (int l = 0; l < K; ++l) {
+      if (l < j) R[j][l] = 0.0;
+      if (l > j) {
+        double v = Cm[j][l];
+#pragma unroll
+        for (int k = 0; k < j; ++k) v = fma(-R[k][j], R[k][l], v);
+        R[j][l] = v / rjj;
+      }
+    }
+  }
+  return ok;
+}
+template <int K>
+__device__ __forceinline__ void r_triinv(const double (&R)[K][K], double (&X)[K][K]) {  // X = R^{-1}, upper
+#pragma unroll
+  for (int l = 0; l < K; ++l) {
+#pragma unroll
+    for (int j = 0; j < K; ++j) X[j][l] = 0.0;
+    X[l][l] = 1.0 / R[l][l];
+#pragma unroll
+    for (int j = l - 1; j >= 0; --j) {
+      double v = 0.0;
+#pragma unroll
+      for (int k = j + 1; k <= l; ++k) v = fma(R[j][k], X[k][l], v);
+      X[j][l] = -v / R[j][j];
+    }
+  }
+}
+
 __device__ __forceinline__ int lz_deg(int gy, int gx, int side) {
   return 4 - (gy == 0) - (gy == side - 1) - (gx == 0) - (gx == side - 1);
 }
@@ -843,6 +885,119 @@ __device__ void lz_reduce(const LzArgs& a, int q, const int* act, int nact, int 
   // C = C0 - 2 H^T H + H^T Gv H   (Gram of W - V H given V^T N W = H).  One warp (a spare one when
   // K < 8) runs the Cholesky QR while the shift warps run their eliminations; only gamma needs both.
   const int cwarp = K < 8 ? K : 0;
+  const int blk = q - 1;  // block index of H_i in T_i
+  __shared__ double gvec[KCG_KMAX][KCG_KMAX], fvec[KCG_KMAX][KCG_KMAX];
+  if constexpr (K <= 4) {
+    // one thread for the Cholesky QR (lane 0 of warp K), one per shift j (lane 0 of warp j), all in
+    // registers and concurrent
+    if (lane == 0 && warp == K) {
+      double Hr[K][K], Gr[K][K], Cr[K][K], Rr[K][K], Xr[K][K];
+#pragma unroll
+      for (int r = 0; r < K; ++r)
+#pragma unroll
+        for (int c = 0; c < K; ++c) { Hr[r][c] = H[r * K + c]; Gr[r][c] = Gv[r * K + c]; }
+      double cmax = 0.0, c0max = 0.0;
+#pragma unroll
+      for (int r = 0; r < K; ++r)
+#pragma unroll
+        for (int c = 0; c < K; ++c) {
+          double t1[K];
+#pragma unroll
+          for (int k = 0; k < K; ++k) {  // (Gv H)[k][c]
+            double v = 0.0;
+#pragma unroll
+            for (int l = 0; l < K; ++l) v = fma(Gr[k][l], Hr[l][c], v);
+            t1[k] = v;
+          }
+          double v = C0[r * K + c];
+#pragma unroll
+          for (int k = 0; k < K; ++k) v = fma(Hr[k][r], fma(-2.0, Hr[k][c], t1[k]), v);
+          Cr[r][c] = v;
+          Cm[r * K + c] = v;
+          cmax = fmax(cmax, fabs(v));
+          c0max = fmax(c0max, fabs(C0[r * K + c]));
+        }
+      const bool ok = r_chol<K>(Cr, Rr);
+      const int fl = ok ? 1 : (cmax <= 1e-14 * c0max ? 2 : 0);
+      if (ok) r_triinv<K>(Rr, Xr);
+#pragma unroll
+      for (int r = 0; r < K; ++r)
+#pragma unroll
+        for (int c = 0; c < K; ++c) {
+          R[r * K + c] = fl == 2 ? 0.0 : Rr[r][c];
+          X[r * K + c] = (fl == 2 || !ok) ? 0.0 : Xr[r][c];
+        }
+      flag[0] = fl;
+    }
+    if (lane == 0 && warp < K) {
+      const int j = warp;
+      const double rho = sm[C::SC_PRE + K * K + j];
+      double S[K][K], g[K];
+#pragma unroll
+      for (int r = 0; r < K; ++r)
+#pragma unroll
+        for (int c = 0; c < K; ++c) S[r][c] = (r >= c ? H[r * K + c] : H[c * K + r]) + (r == c ? rho : 0.0);
+      if (blk == 0) {
+#pragma unroll
+        for (int r = 0; r < K; ++r) {  // g = B_0 u_j
+          double v = 0.0;
+#pragma unroll
+          for (int c = 0; c < K; ++c) v = fma(sm[C::SC_PRE + r * K + c], sm[C::SC_PRE + K * K + K + c * K + j], v);
+          g[r] = v;
+        }
+      } else {
+        const double* Sp = sm + C::SC_W + j * 9 * K * K + K * K;
+        const double* Bs = Sp + K * K;
+        double Xm[K][K];
+#pragma unroll
+        for (int r = 0; r < K; ++r)
+#pragma unroll
+          for (int c = 0; c < K; ++c) {  // X = B S_{blk-1}^{-1}
+            double v = 0.0;
+#pragma unroll
+            for (int k = 0; k < K; ++k) v = fma(Bs[r * K + k], Sp[k * K + c], v);
+            Xm[r][c] = v;
+          }
+#pragma unroll
+        for (int r = 0; r < K; ++r) {
+#pragma unroll
+          for (int c = 0; c < K; ++c) {  // S = D - X B^T
+            double v = S[r][c];
+#pragma unroll
+            for (int k = 0; k < K; ++k) v = fma(-Xm[r][k], Bs[c * K + k], v);
+            S[r][c] = v;
+          }
+          double v = 0.0;  // g = -X g_prev
+#pragma unroll
+          for (int c = 0; c < K; ++c) v = fma(-Xm[r][c], Bs[6 * K * K + c], v);
+          g[r] = v;
+        }
+      }
+      double Rs2[K][K], Xs[K][K], Si[K][K];
+      r_chol<K>(S, Rs2);
+      r_triinv<K>(Rs2, Xs);
+      double* so = a.Sinv + ((fc + blk) * K + j) * K * K;
+#pragma unroll
+      for (int r = 0; r < K; ++r)
+#pragma unroll
+        for (int c = 0; c < K; ++c) {  // S^{-1} = X X^T
+          double v = 0.0;
+#pragma unroll
+          for (int k = 0; k < K; ++k) v = fma(Xs[r][k], Xs[c][k], v);
+          Si[r][c] = v;
+          so[r * K + c] = v;
+        }
+#pragma unroll
+      for (int r = 0; r < K; ++r) {
+        double v = 0.0;
+#pragma unroll
+        for (int c = 0; c < K; ++c) v = fma(Si[r][c], g[c], v);
+        fvec[j][r] = v;
+        gvec[j][r] = g[r];
+        a.gv[((fc + blk) * K + j) * K + r] = g[r];
+      }
+    }
+  } else {
   if (warp == cwarp) {
     w_matmul<K>(Gv, H, T1);
     for (int e = lane; e < K * K; e += 32) {
@@ -864,10 +1019,7 @@ __device__ void lz_reduce(const LzArgs& a, int q, const int* act, int nact, int 
     if (flag[0] == 2)
       for (int e = lane; e < K * K; e += 32) { R[e] = 0.0; X[e] = 0.0; }
   }
-  lz_stamp(a, q, 154);
   // per shift j (one warp each): block forward elimination of (T_i + rho_j I) f = E_1 B_0 u_j
-  const int blk = q - 1;  // block index of H_i in T_i
-  __shared__ double gvec[KCG_KMAX][KCG_KMAX], fvec[KCG_KMAX][KCG_KMAX];
   if (warp < K) {
     const int j = warp;
     double* D = sm + C::SC_W + j * 9 * K * K;
@@ -921,6 +1073,8 @@ __device__ void lz_reduce(const LzArgs& a, int q, const int* act, int nact, int 
     for (int e = lane; e < K * K; e += 32) so[e] = Si[e];
     if (lane < K) a.gv[((fc + blk) * K + j) * K + lane] = gvec[j][lane];
   }
+  }  // K > 4
+  lz_stamp(a, q, 154);
   __syncthreads();  // R (Cholesky warp) and every shift's f_last are ready
   if (tid < K) {    // gamma_j = ||B_{i+1} f_last||^2
     double g2 = 0.0;
