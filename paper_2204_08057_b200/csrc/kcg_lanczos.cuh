@@ -771,6 +771,8 @@ __device__ void lz_reduce(const LzArgs& a, int q, const int* act, int nact, int 
   const long long f0 = (long long)ai * a.tps, f1 = f0 + a.tps;
   const size_t fc = (size_t)f * a.cap, fr = (size_t)f * (a.cap + 1);
   // constants of the face and B_0 (L2 reads, issued before the partial sums)
+  __shared__ LzState zpre;
+  if (q >= 1 && tid == 0) zpre = a.st[f];
   if (q >= 1) {
     double* pre = sm + C::SC_PRE;
     const LzFace& pf0 = a.prm[f];
@@ -809,10 +811,11 @@ __device__ void lz_reduce(const LzArgs& a, int q, const int* act, int nact, int 
       // loads issued 8 at a time (memory-level parallelism), added in CTA order
       double s = 0.0;
       const double* src = a.part + (size_t)f * KCG_LZ_GRID_MAX * C::NPART + e;
-      for (int b0 = b_lo + g; b0 <= b_hi; b0 += 8 * NG) {
-        double v[8];
+      constexpr int UNR = 8;   // loads in flight per thread (24: measured slower)
+      for (int b0 = b_lo + g; b0 <= b_hi; b0 += UNR * NG) {
+        double v[UNR];
 #pragma unroll
-        for (int u = 0; u < 8; ++u) {
+        for (int u = 0; u < UNR; ++u) {
           // clamped index: the compiler may issue the loads before the predicate is known
           const int b = min(b0 + u * NG, b_hi);
           const bool ok = b0 + u * NG <= b_hi && cst[b + 1 - b_lo] > cst[b - b_lo];
@@ -820,7 +823,7 @@ __device__ void lz_reduce(const LzArgs& a, int q, const int* act, int nact, int 
           v[u] = ok ? pv : 0.0;
         }
 #pragma unroll
-        for (int u = 0; u < 8; ++u) s += v[u];
+        for (int u = 0; u < UNR; ++u) s += v[u];
       }
       grp[g * C::NPART + e] = s;
     }
@@ -1088,7 +1091,7 @@ __device__ void lz_reduce(const LzArgs& a, int q, const int* act, int nact, int 
   __syncthreads();
   lz_stamp(a, q, 155);
   if (tid == 0) {
-    LzState z = a.st[f];
+    LzState z = zpre;
     double gam2 = 0.0;
     for (int j = 0; j < K; ++j) gam2 += res[j];
     z.iters = q;
