@@ -241,3 +241,14 @@ def test_lanczos_nonfinite_and_rank_deficient_inputs():
     with pytest.raises(KcgError) as e:
         ctx.lanczos(Yr.contiguous(), tol=TOL)
     assert e.value.status == KCG_E_BREAKDOWN
+
+
+def test_lanczos_batch_composition_changes_only_rounding():
+    """Sharding faces across ranks changes the per-CTA Gram partial grouping (chunks follow the batch),
+    so a face solved alone and inside a batch agree to rounding, with the same step count."""
+    ps = [make_patch(7, 9, 4, seed=640 + s, tau="loguniform") for s in range(3)]
+    _, _, mu_b, rep_b = _run(ps, cap=300)
+    for i, p in enumerate(ps):
+        _, _, mu_1, rep_1 = _run([p], cap=300)
+        assert rep_1["iterations_per"][0] == rep_b["iterations_per"][i]
+        assert rel(mu_1[0], mu_b[i]) <= 1e-12
