@@ -16,6 +16,9 @@ extern template struct CgEntry<8>;
 
 // --------------------------------------------------------------------------- apply / residual
 constexpr int AP_TY = 16, AP_TX = 64, AP_NT = 256;
+#ifndef KCG_AP_MINB
+#define KCG_AP_MINB 4  // resident blocks per SM for apply_kernel, K <= 4 (64 registers: 2.8x faster than 1 under ncu); 2 above
+#endif
 
 int apply_tiles_per_sys(int rows, int side) {
   return ((rows + AP_TY - 1) / AP_TY) * ((side + AP_TX - 1) / AP_TX);
@@ -27,7 +30,7 @@ int apply_tiles_per_sys(int rows, int side) {
 // the neighbours' boundary rows; nullptr or outside the face -> 0).  D2: Q0 = D^2 + kappa2 I, the
 // tile's x is staged with a 2-pixel halo and D x is formed on tile + 1-ring first (no slabs).
 template <int K, bool RESID, bool D2>
-__global__ void __launch_bounds__(AP_NT) apply_kernel(const SysParams* __restrict__ params,
+__global__ void __launch_bounds__(AP_NT, (K <= 4 ? KCG_AP_MINB : 2)) apply_kernel(const SysParams* __restrict__ params,
                                                       const double* __restrict__ x, double* __restrict__ y,
                                                       const double* __restrict__ Y, const double* __restrict__ E,
                                                       const double* __restrict__ hits,
