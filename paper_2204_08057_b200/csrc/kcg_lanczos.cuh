@@ -1267,10 +1267,11 @@ __global__ void __launch_bounds__(256) lz_assemble_kernel(const LzArgs a) {
     __syncthreads();
     for (int e = threadIdx.x; e < nz; e += blockDim.x) zs[e] = __ldcg(Zg + e);
     __syncthreads();
-    auto Z = [&](int q, int e) { const int o = (q - 1) * K * K + e; return o < LZ_ASM_ZMAX ? zs[o] : __ldg(Zg + o); };
-    if (pairs) {
+    // G_q from shared memory when the unit's coefficients fit (block-uniform), else from L1/L2
+    auto pair_body = [&](auto zload) {
+      auto Z = [&](int q, int e) { return zload((q - 1) * K * K + e); };
       const size_t px = ch * per + 2 * threadIdx.x;
-      if (px >= N) continue;
+      if (px >= N) return;
       const size_t gy = px / a.side, gx = px - gy * a.side;
       const size_t off = gy * a.pitch + gx;
       double2 m[K];
@@ -1312,7 +1313,13 @@ __global__ void __launch_bounds__(256) lz_assemble_kernel(const LzArgs a) {
       }
 #pragma unroll
       for (int c = 0; c < K; ++c) *reinterpret_cast<double2*>(a.Mx + ((size_t)f * K + c) * N + px) = m[c];
+    };
+    if (pairs) {
+      if (it * K * K <= LZ_ASM_ZMAX) pair_body([&](int o) { return zs[o]; });
+      else pair_body([&](int o) { return __ldg(Zg + o); });
+      continue;
     } else {  // side == 1
+      auto Z = [&](int q, int e) { const int o = (q - 1) * K * K + e; return o < LZ_ASM_ZMAX ? zs[o] : __ldg(Zg + o); };
       const size_t px = ch * per + threadIdx.x;
       if (px >= N) continue;
       const size_t gy = px / a.side, gx = px - gy * a.side;
