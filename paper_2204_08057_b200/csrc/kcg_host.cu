@@ -833,6 +833,8 @@ kcg_status lanczos_impl(kcg_ctx* c, const double* Y_in, double* mu_out, bool hos
     if (i >= 1) b += 2 * vec;
     if (i >= 2) b += (2.0 + 3.0 * (i - 2)) * vec;
     if (c->d.lanczos_store) b += (i > 0 ? (double)i + 1.0 : 1.0) * vec;
+    else if (c->d.prior != KCG_PRIOR_D2 && k <= 4)  // pair-mapped replay: M every other pass
+      b += (i >= 2 ? 3.0 * i - 3.0 + 2.0 * ((i + 1) / 2) - 1.0 : i == 1 ? 2.0 : 1.0) * vec;
     else b += (i >= 2 ? 5.0 * i - 4.0 : i == 1 ? 2.0 : 1.0) * vec;  // V reads/writes 3i-3, M 2i-1
     bytes += b;
   }

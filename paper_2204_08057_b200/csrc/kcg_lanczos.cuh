@@ -290,7 +290,9 @@ __device__ __forceinline__ void lz_pass(const LzArgs& a, const CUtensorMap* vmap
           mats[e] = q >= 2 ? __ldcg(a.Hs + (fc + q - 2) * K * K + e) : 0.0;
           mats[K * K + e] = q >= 2 ? __ldcg(a.Rs + (fr + q - 2) * K * K + e) : 0.0;
           mats[2 * K * K + e] = __ldcg(a.Ri + (fr + q - 1) * K * K + e);
-          mats[3 * K * K + e] = __ldcg(a.Rs + (fr + q - 1) * K * K + e);
+          // Bc (steps) -- or, in the pair-mapped replay, G_{q-1} (M updated every other pass)
+          mats[3 * K * K + e] = (mode == LZ_REPLAY && C::PAIRS) ? (q >= 2 ? __ldcg(a.Zs + (fc + q - 2) * K * K + e) : 0.0)
+                                                                : __ldcg(a.Rs + (fr + q - 1) * K * K + e);
           mats[4 * K * K + e] = mode == LZ_REPLAY ? __ldcg(a.Zs + (fc + q - 1) * K * K + e) : 0.0;
         }
         __syncthreads();
@@ -413,16 +415,34 @@ __device__ __forceinline__ void lz_pass(const LzArgs& a, const CUtensorMap* vmap
 #pragma unroll
           for (int c = 0; c < K; ++c) vq[c] = *reinterpret_cast<const double2*>(U + c * C::RN + ri);
           if (mode == LZ_REPLAY) {
+            // M is read and written every other pass: on even q it gains V_{q-1} G_{q-1} (V_{q-1} is in
+            // the box) and V_q G_q; an odd last pass adds V_q G_q alone -- the assembly's q-major order
+            const bool upd = (q & 1) == 0 || q == its_f;
             if (in0) {
               const size_t px = (size_t)gy * side + gx;
+              double2 vo[K];
+              if (upd && (q & 1) == 0) {
+#pragma unroll
+                for (int d = 0; d < K; ++d) vo[d] = *reinterpret_cast<const double2*>(B1 + d * C::BH * C::BW + bi);
+              }
 #pragma unroll
               for (int c = 0; c < K; ++c) {
-                double* mp = a.Mx + ((size_t)f * K + c) * N + px;
-                double mx = q > 1 ? mp[0] : 0.0, my = (q > 1 && in1) ? mp[1] : 0.0;
+                if (upd) {
+                  double* mp = a.Mx + ((size_t)f * K + c) * N + px;
+                  double mx = q > 2 ? mp[0] : 0.0, my = (q > 2 && in1) ? mp[1] : 0.0;
+                  if ((q & 1) == 0) {
 #pragma unroll
-                for (int d = 0; d < K; ++d) { const double m2 = rbv(d * K + c); mx = fma(vq[d].x, m2, mx); my = fma(vq[d].y, m2, my); }
-                mp[0] = mx;
-                if (in1) mp[1] = my;
+                    for (int d = 0; d < K; ++d) {
+                      const double m1 = Bc[d * K + c];  // G_{q-1}
+                      mx = fma(vo[d].x, m1, mx);
+                      my = fma(vo[d].y, m1, my);
+                    }
+                  }
+#pragma unroll
+                  for (int d = 0; d < K; ++d) { const double m2 = rbv(d * K + c); mx = fma(vq[d].x, m2, mx); my = fma(vq[d].y, m2, my); }
+                  mp[0] = mx;
+                  if (in1) mp[1] = my;
+                }
                 if (q < its_f) {
                   double* vp = a.V + ((size_t)(slotq * a.P + f) * K + c) * pstride + (size_t)gy * a.pitch + gx;
                   vp[0] = vq[c].x;
