@@ -7,7 +7,7 @@ import subprocess
 import sys
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-LINE = os.path.join(ROOT, "profiles", "r01", "bench_fullsky_v19.json")
+LINE = os.path.join(ROOT, "profiles", "r01", "bench_fullsky_v20.json")
 
 
 def test_committed_bench_line_has_every_contract_key():
