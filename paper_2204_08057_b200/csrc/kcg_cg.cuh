@@ -537,8 +537,13 @@ __device__ __forceinline__ void cg_tile(const CgArgs& a, const TileCtx& tc, doub
   const double alpha = tc.alpha, beta = tc.beta, kappa2 = tc.kappa2;
   const int gx = x0 + 2 * lane;
   const double* __restrict__ M = tc.Ms;
+#if KCG_PREC_SMEM_A
+  const double* Mg = tc.Ms;              // phase A: the shared copy (a barrier follows its writes)
+  const double* Kinvg = tc.Ms + K * K + K;
+#else
   const double* Mg = tc.sp->M;           // phase A (before the barrier): global copies
   const double* Kinvg = &tc.sp->Kinv[0][0];
+#endif
   // degree of a pixel from its global face coordinates (free boundary, reading R2)
   auto degree = [&](int gyg, int gxx) { return 4 - (gyg == 0) - (gyg == side - 1) - (gxx == 0) - (gxx == side - 1); };
   auto in_face = [&](int gyg, int gxx) { return gyg >= 0 && gyg < side && gxx >= 0 && gxx < side; };
@@ -551,7 +556,7 @@ __device__ __forceinline__ void cg_tile(const CgArgs& a, const TileCtx& tc, doub
   double tau[K];  // PREC: needed in phase A (global copy); else read from shared after the barrier
   if (PREC)
 #pragma unroll
-    for (int c = 0; c < K; ++c) tau[c] = __ldg(&tc.sp->tau[c]);
+    for (int c = 0; c < K; ++c) tau[c] = KCG_PREC_SMEM_A ? tc.Ms[K * K + c] : __ldg(&tc.sp->tau[c]);
 
   // Phase A.  Interior pairs in the pair mapping (the thread keeps its pairs' x increment
   //   xinc = alpha_prev p_old + alpha p_new   (X2: x is updated every other pass)
@@ -1297,6 +1302,9 @@ __device__ __forceinline__ void cg_body(const CgArgs& a, const CgMaps& maps, con
       if (tid < K * K) Ms[tid] = __ldg(&sp->M[tid]);
       else if (tid < K * K + K) Ms[tid] = __ldg(&sp->tau[tid - K * K]);
       else if (PREC && tid < MSZ) Ms[tid] = __ldg(&sp->Kinv[0][0] + (tid - K * K - K));
+#if KCG_PREC_SMEM_A
+      if constexpr (PREC && !D2) __syncthreads();  // phase A of the PCG tile reads the shared copy
+#endif
       TileCtx tc;
       tc.R = reinterpret_cast<double*>(smem_raw + sidx * STAGE_BYTES);
       tc.Pp = tc.R + FIELD;

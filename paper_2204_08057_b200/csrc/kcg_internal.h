@@ -45,6 +45,9 @@ namespace kcg {
 #ifndef KCG_XPF
 #define KCG_XPF 1           // prefetch the next tile's x block into L2 (TMA prefetch) when not staged
 #endif
+#ifndef KCG_PREC_SMEM_A
+#define KCG_PREC_SMEM_A 0   // 1: PCG phase A reads the block-Jacobi inverses from shared memory (extra barrier)
+#endif
 #ifndef KCG_X2
 #define KCG_X2 1            // update x every other pass (x += a_{q-1} p_{q-1} + a_q p_q): 40kN B/iter
 #endif
