@@ -27,7 +27,8 @@
  *       noise_prec_host   [P][n]      (T = 1/sigma^2, > 0)
  *       prior_scale_host  [P][k]      (paper phi_l = config tau_i, > 0)
  *       kappa2_host       [P]         (>= 0; kappa2 = 0 with hits = 1 still gives SPD G as M SPD)
- *       hits_dev          [P][side][side] (> 0) or NULL for all ones
+ *       hits_dev          [P][side][side] (finite, > 0: checked on the device at create ->
+ *                         KCG_E_ARG) or NULL for all ones; row slabs: see kcg_slab below
  *       Y                 [P][n][side][side]   row-major pixels idx = y*side + x (reading R1)
  *       mu / x / y        [P][k][side][side]
  *   - Calls are stream-ordered on the stream given at create and BLOCKING: they return after the
@@ -87,7 +88,7 @@ typedef struct {
   int layout;       /* KCG_LAYOUT_ROW_MAJOR (y*side + x) or KCG_LAYOUT_NESTED (HEALPix NESTED      */
                     /* within the face; Y, mu, hits, apply/rhs arguments; no row slabs)            */
   int precond;      /* KCG_PRECOND_NONE (the paper's CG) or KCG_PRECOND_BLOCK_JACOBI (pixel */
-                    /* k x k blocks of G, reading R10; n_comp <= 7)                                 */
+                    /* k x k blocks of G, reading R10; n_comp <= 7; any level incl. 0)              */
   int host_staging; /* 1: workspace also holds Y / mu staging for the *_host entry points          */
   int history_cap;  /* per-iteration max relative residual recorded on device (0 = off)            */
   int lanczos_cap;  /* block-Lanczos route (sylvester_lanczos_solve): 0 = not provisioned; else the   */
@@ -178,7 +179,8 @@ KCG_API kcg_status kron_cg_solve_b(kcg_ctx* ctx, const double* b_dev, double* x_
  *   splitmix64(splitmix64(seed) + ((i P + p) k + c) N + j)   (j = the pixel's user-layout index)
  * -- an unbiased estimate; Var(var_j) = (1/s) sum_{l != j} (G^{-1})_{jl}^2.  Each probe is one batched
  * CG solve (kron_cg_solve_b) of all patches to tol.  var_dev [P][k][N]; scratch_dev 2 P k N doubles
- * (caller-owned).  report aggregates the probes (iterations = max, times and bytes summed).      */
+ * (caller-owned).  report aggregates the probes (iterations = max, times and bytes summed;
+ * iterations_per[p] = the most CG iterations patch p needed over the probes, n_systems = P).     */
 KCG_API kcg_status posterior_variance(kcg_ctx* ctx, int n_probes, unsigned long long seed, double* var_dev,
                               double* scratch_dev, double tol, int max_iter, kcg_report* report);
 
@@ -214,7 +216,10 @@ KCG_API const char* kcg_status_string(int status);
  * rank computes identical scalars).  A context drives `nlocal` ranks: 1 (one process per GPU) or
  * all G (every rank emulated on this GPU in one cooperative launch, one CTA group per rank).
  * Layouts for a slab context: Y [nlocal][P][n][rows][side], mu [nlocal][P][k][rows][side],
- * hits [nlocal][P][rows][side]; rows = side / G.  All ranks must create their contexts before
+ * hits [nlocal][P][rows + 4][side] -- GHOSTED: local rank j's plane p holds the face rows
+ * [row0 - 2, row0 + rows + 2) of patch p (row0 = (rank0 + j) rows), i.e. its own rows plus the two
+ * rows of the slab above and below, zeros beyond the face edge (kroncg.py ghost_rows() builds it
+ * from a full face); rows = side / G.  Its own rows must be finite and > 0 (KCG_E_ARG otherwise).  All ranks must create their contexts before
  * any of them solves, and must issue the same sequence of solve / apply calls.              */
 typedef struct {
   int nranks;            /* G: ranks sharing every face, 1..8; side % G == 0, side / G >= 4       */

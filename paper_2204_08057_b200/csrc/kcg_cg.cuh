@@ -429,7 +429,7 @@ __device__ __forceinline__ void precond_pixel(const double* Kinv, const double* 
                                               const double* tau, double kappa2, double h, int deg,
                                               const double (&r)[K], double (&u)[K], bool d2 = false) {
   if (!HITS) {
-    const double* Ki = Kinv + (deg - 2) * K * K;
+    const double* Ki = Kinv + kinv_slot(deg) * K * K;
 #pragma unroll
     for (int c = 0; c < K; ++c) {
       double v = 0.0;
@@ -959,7 +959,7 @@ __device__ __forceinline__ void cg_tile_d2(const CgArgs& a, const TileCtx& tc, d
   auto degree_full = [&](int gy, int gx) { return 4 - (gy == 0) - (gy == side - 1) - (gx == 0) - (gx == side - 1); };
   auto degree = [&](int gy, int gx) { return EDGE ? degree_full(gy, gx) : 4; };  // box rows/cols >= 1 only
   auto hit = [&](int gy, int gx) { return HITS ? __ldg(tc.hp + (size_t)gy * side + gx) : 1.0; };
-  // K_j^{-1} r for PREC: Kinv holds (M + (kappa2 + d^2 + d) P)^{-1}, d = 2, 3, 4 (host)
+  // K_j^{-1} r for PREC: Kinv holds (M + (kappa2 + d^2 + d) P)^{-1}, d = 2, 3, 4, 0 (host)
   double tau[K];
 #pragma unroll
   for (int c = 0; c < K; ++c) tau[c] = __ldg(&tc.sp->tau[c]);
@@ -1168,7 +1168,7 @@ __device__ __forceinline__ void cg_body(const CgArgs& a, const CgMaps& maps, con
   constexpr int EXTRA = D2 ? d2_sbox_bytes(K) + d2_pold_bytes(K) : 0;  // D2 scratch boxes
   constexpr int NT = threads_of(K, D2), NW = NT / 32, NS = cg_stages(K);
   constexpr int NP = PREC ? 3 : 2;  // partials per tile
-  constexpr int MSZ = K * K + K + (PREC ? 3 * K * K : 0);
+  constexpr int MSZ = K * K + K + (PREC ? 4 * K * K : 0);
   static_assert(D2 || STAGE_BYTES == cg_stage_bytes(K), "stage size");
   static_assert(!D2 || STAGE_BYTES == d2_stage_bytes(K), "stage size (D2)");
 

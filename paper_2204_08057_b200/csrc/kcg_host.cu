@@ -340,16 +340,16 @@ void small_inverse(int k, const double* A, double* Ainv) {
 }
 
 // Pixel-block Jacobi blocks for hits = 1 (reading R10): Kinv_d = (M + diag(Q0)_d diag(tau))^{-1} for
-// degree d = 2, 3, 4, with diag(Q0)_d = kappa2 + d (Laplacian) or kappa2 + d^2 + d (D^2), stored
-// compactly (K x K each) in sp.Kinv.
+// degree d = 2, 3, 4 and 0 (level 0: one pixel, no neighbours), with diag(Q0)_d = kappa2 + d
+// (Laplacian) or kappa2 + d^2 + d (D^2), stored compactly (K x K each) in sp.Kinv, slot kinv_slot(d).
 void set_block_jacobi(int K, const double* M, const double* tau, double kappa2, SysParams* sp, bool d2) {
   std::vector<double> A((size_t)K * K), Ai((size_t)K * K);
   double* out = &sp->Kinv[0][0];
-  for (int d = 2; d <= 4; ++d) {
+  for (int d : {2, 3, 4, 0}) {
     for (int i = 0; i < K; ++i)
       for (int j = 0; j < K; ++j) A[i * K + j] = M[i * K + j] + (i == j ? (kappa2 + (d2 ? d * d + d : d)) * tau[i] : 0.0);
     small_inverse(K, A.data(), Ai.data());
-    for (int e = 0; e < K * K; ++e) out[(d - 2) * K * K + e] = Ai[e];
+    for (int e = 0; e < K * K; ++e) out[kcg::kinv_slot(d) * K * K + e] = Ai[e];
   }
 }
 
@@ -1232,6 +1232,20 @@ kcg_status create_impl(const kcg_desc* d, const kcg_slab* sl, const double* A_ho
     c->tiles_x_lz = (c->side + KCG_TX - 1) / KCG_TX;
     c->tiles_y_lz = (c->side + kcg::lz_tile_y(k, d2) - 1) / kcg::lz_tile_y(k, d2);
   }
+  if (hits_dev) {  // hit counts must be finite and > 0 (G is SPD only then)
+    for (RankState& R : c->R) {
+      CKC(cudaMemsetAsync(R.sync, 0, sizeof(unsigned), c->stream), "memset");
+      for (int p = 0; p < P; ++p)  // the slab's own rows (ghost rows at the face ends are zero)
+        CKC(kcg::launch_count_nonpositive(c->stream, hits_dev + (size_t)(&R - &c->R[0]) * P * buf_rows * c->side +
+                                                         ((size_t)p * buf_rows + c->ghost) * c->side,
+                                          (size_t)c->rows * c->side, R.sync),
+            "hits check kernel");
+      unsigned bad = 0;
+      CKC(cudaMemcpyAsync(&bad, R.sync, sizeof(unsigned), cudaMemcpyDeviceToHost, c->stream), "D2H");
+      CKC(cudaStreamSynchronize(c->stream), "hits check");
+      if (bad) return fail(KCG_E_ARG, "hits must be finite and > 0 (" + std::to_string(bad) + " entries are not)");
+    }
+  }
   CKC(cudaStreamSynchronize(c->stream), "create sync");
   c->tiles_x_kron = tiles_x(c->side, k);
   c->tiles_y_kron = tiles_y(c->rows, k, d2);
@@ -1315,9 +1329,11 @@ kcg_status posterior_variance(kcg_ctx* c, int n_probes, unsigned long long seed,
   int worst = KCG_OK, maxit = 0;
   double wall = 0.0, loop = 0.0, bytes = 0.0, maxrel = 0.0, maxtrue = 0.0;
   long long sumit = 0;
+  std::vector<int> its_probe(c->P), its_max(c->P, 0);  // per-patch iterations: max over the probes
   for (int i = 0; i < n_probes; ++i) {
     CK(kcg::launch_probe(s, z, c->P, c->k, c->side, c->d.layout == KCG_LAYOUT_NESTED, seed, i), "probe kernel");
     sub = kcg_report{};
+    sub.iterations_per = its_probe.data();
     const kcg_status st = solve_impl(c, ROUTE_KRON, z, x, false, tol, max_iter, &sub, IN_B_WORK);
     if (st != KCG_OK && st != KCG_NOT_CONVERGED) return st;
     if (st == KCG_NOT_CONVERGED) worst = KCG_NOT_CONVERGED;
@@ -1325,6 +1341,7 @@ kcg_status posterior_variance(kcg_ctx* c, int n_probes, unsigned long long seed,
     wall += sub.wall_time_s; loop += sub.loop_time_s; bytes += sub.loop_bytes;
     maxit = std::max(maxit, sub.iterations); sumit += sub.system_iterations;
     maxrel = std::max(maxrel, sub.rel_residual); maxtrue = std::max(maxtrue, sub.rel_residual_true);
+    for (int p = 0; p < c->P; ++p) its_max[p] = std::max(its_max[p], its_probe[p]);
   }
   if (R.y_rm) CK(kcg::launch_permute(s, R.y_rm, var, planes, c->side, true), "permute var");
   CK(cudaStreamSynchronize(s), "posterior variance");
@@ -1334,6 +1351,9 @@ kcg_status posterior_variance(kcg_ctx* c, int n_probes, unsigned long long seed,
     all.rel_residual = maxrel; all.rel_residual_true = maxtrue;
     all.wall_time_s = wall; all.loop_time_s = loop; all.loop_bytes = bytes;
     all.iterations_per = rep->iterations_per; all.history = rep->history; all.history_len = 0;
+    all.n_systems = c->P;
+    if (all.iterations_per)
+      for (int p = 0; p < c->P; ++p) all.iterations_per[p] = its_max[p];
     *rep = all;
   }
   c->err.clear();

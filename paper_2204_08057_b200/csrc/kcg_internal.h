@@ -92,10 +92,13 @@ struct SysParams {
   double tau[KCG_KMAX];
   double kappa2;
   double hits_plane;              // index of the hits plane (patch) as a double (exact)
-  // pixel-block Jacobi (hits = 1): inverses of M + (kappa2 + d) diag(tau) for degree d = 2, 3, 4,
-  // each row-major K x K, stored compactly one after the other (Kinv[0][0 .. 3 K K))
-  double Kinv[3][KCG_KMAX * KCG_KMAX];
+  // pixel-block Jacobi (hits = 1): inverses of M + diag(Q0)_d diag(tau) for degree d = 2, 3, 4 and
+  // d = 0 (the single pixel of a level-0 face), each row-major K x K, stored compactly one after the
+  // other (Kinv[0][0 .. 4 K K)); slot of degree d: kinv_slot(d)
+  double Kinv[4][KCG_KMAX * KCG_KMAX];
 };
+
+__host__ __device__ inline int kinv_slot(int deg) { return deg >= 2 ? deg - 2 : 3; }
 
 // Per-system iteration state (kept redundantly in every CTA's shared memory).
 enum { ST_RUNNING = 0, ST_CONVERGED = 1, ST_MAXIT = 2, ST_BREAKDOWN = 3, ST_NONFINITE = 4 };
@@ -255,6 +258,8 @@ cudaError_t launch_kohler_rhs(int K, cudaStream_t s, const double* Y, const doub
                               const double* Xh, const double* hits, double* r0, double* p0, double* x, int P, int n,
                               int i, int side, int pitch, bool nested);
 cudaError_t launch_column_copy(cudaStream_t s, const double* src, double* dst, int P, int K, int i, size_t N);
+// bad += number of entries of v[0..n) that are not finite and > 0 (hits validation at create)
+cudaError_t launch_count_nonpositive(cudaStream_t s, const double* v, size_t n, unsigned* bad);
 cudaError_t launch_var_accum(cudaStream_t s, const double* z, const double* x, double* var, size_t n, bool first,
                              double scale);
 // block-Lanczos (kcg_lanczos_*.cu): one cooperative launch runs the Lanczos passes, the residual

@@ -523,4 +523,26 @@ cudaError_t launch_column_copy(cudaStream_t s, const double* src, double* dst, i
   return cudaGetLastError();
 }
 
+
+
+// --------------------------------------------------------------------------- argument checks
+// Count of entries that are not finite and > 0 (hit counts must be positive): one atomic
+// per block, launched once at create.
+__global__ void __launch_bounds__(256) count_nonpositive_kernel(const double* __restrict__ v, size_t n,
+                                                                unsigned* __restrict__ bad) {
+  unsigned c = 0;
+  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
+    const double h = __ldg(v + i);
+    c += (h > 0.0 && isfinite(h)) ? 0u : 1u;
+  }
+  c = __reduce_add_sync(0xffffffffu, c);
+  if ((threadIdx.x & 31) == 0 && c) atomicAdd(bad, c);
+}
+
+cudaError_t launch_count_nonpositive(cudaStream_t s, const double* v, size_t n, unsigned* bad) {
+  const int grid = (int)std::min<size_t>((n + 255) / 256, 1184);
+  count_nonpositive_kernel<<<std::max(grid, 1), 256, 0, s>>>(v, n, bad);
+  return cudaGetLastError();
+}
+
 }  // namespace kcg

@@ -225,6 +225,18 @@ class KronCG:
                 and t.is_contiguous() and tuple(t.shape) == shape):
             raise ValueError(f"{name} must be a contiguous CUDA float64 tensor of shape {shape}")
 
+    def _check_host(self, a, shape, name):
+        import torch
+        if isinstance(a, np.ndarray):
+            ok = a.dtype == np.float64 and a.flags["C_CONTIGUOUS"] and a.shape == shape
+        elif isinstance(a, torch.Tensor):
+            ok = (not a.is_cuda and a.dtype == torch.float64 and a.is_contiguous()
+                  and tuple(a.shape) == shape)
+        else:
+            ok = False
+        if not ok:
+            raise ValueError(f"{name} must be a C-contiguous host float64 array/tensor of shape {shape}")
+
     # ------------------------------------------------------------------ API
     def solve(self, Y, mu=None, tol=1e-10, max_iter=100000, **kw):
         """Kronecker route (kron_cg_solve). Y: CUDA [P][n][side][side] -> (mu, report)."""
@@ -282,8 +294,12 @@ class KronCG:
         """Host-buffer entry points (kron_cg_solve_host / sylvester_solve_host /
         sylvester_lanczos_solve_host).
 
-        Y and mu are CPU tensors (pinned for full-speed copies) or numpy arrays."""
+        Y and mu are CPU tensors (pinned for full-speed copies) or numpy arrays: C-contiguous
+        float64 of shapes shape_Y and shape_mu (checked here -- the C side copies P n N and P k N
+        doubles through the raw pointers)."""
         mu = self._out(mu, host=True)
+        self._check_host(Y, self.shape_Y, "Y")
+        self._check_host(mu, self.shape_mu, "mu")
         fn = {"kron": kron_cg_solve_host, "sylvester": sylvester_solve_host,
               "lanczos": sylvester_lanczos_solve_host}[route]
         n_sys = self.P * self.k if route == "sylvester" else self.P

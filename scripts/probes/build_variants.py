@@ -1,7 +1,7 @@
 """Build experimental variants of libkroncg (compile-time tile/thread/M-placement knobs)."""
 import os, sys
 from concurrent.futures import ThreadPoolExecutor
-ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+ROOT = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 sys.path.insert(0, ROOT)
 from paper_2204_08057_b200 import build
 

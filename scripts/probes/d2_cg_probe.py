@@ -1,7 +1,7 @@
 """Time the Kronecker-CG and Sylvester routes with the D^2 prior (the paper's operator) on a config:
 usage: d2_cg_probe.py CONFIG [paper]"""
 import json, os, sys
-ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+ROOT = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 sys.path.insert(0, ROOT)
 import torch
 from paper_2204_08057_b200.kroncg import KronCG

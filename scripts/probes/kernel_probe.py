@@ -1,7 +1,7 @@
 """Steady-state CG-kernel bandwidth probe: fixed iteration count (tol 1e-300), all systems active.
 usage: KCG_LIB_PATH=... python scripts/kernel_probe.py [config] [iters] [route]"""
 import os, sys, json
-ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+ROOT = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 sys.path.insert(0, ROOT)
 import torch
 from synth import make_config

@@ -1,7 +1,7 @@
 """Per-pass phase breakdown of the block-Lanczos kernel (needs a KCG_TRACE=1 build).
 usage: KCG_LIB_PATH=.../trace.so python scripts/lz_trace_probe.py [config] [store]"""
 import ctypes, json, os, sys
-ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+ROOT = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 sys.path.insert(0, ROOT)
 import numpy as np
 import torch

@@ -1,6 +1,6 @@
 """Paper workload (App. B physics, D^2, hits, NESTED; 12 faces, L = 10): one solve per route (for ncu)."""
 import os, sys
-ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+ROOT = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 sys.path.insert(0, ROOT)
 import torch
 from paper_2204_08057_b200.kroncg import KronCG

@@ -1,7 +1,7 @@
 """Sample SM / memory clocks, power and throttle reasons (nvidia-smi, 20 ms) during back-to-back
 fullsky Kron-CG solves; print per-solve loop time next to the samples."""
 import json, os, subprocess, sys, threading, time
-ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+ROOT = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 sys.path.insert(0, ROOT)
 import torch
 from paper_2204_08057_b200.kroncg import KronCG

@@ -1,6 +1,6 @@
 """fullsky: 2 Kron solves + 2 Sylvester solves (the residual apply kernel runs once per solve), for ncu."""
 import os, sys
-ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+ROOT = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 sys.path.insert(0, ROOT)
 import torch
 from paper_2204_08057_b200.kroncg import KronCG

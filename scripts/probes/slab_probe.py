@@ -1,6 +1,6 @@
 """Slab-emulation probe: planck face unsplit vs split into G row slabs (all ranks on this GPU)."""
 import json, os, sys
-ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+ROOT = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 sys.path.insert(0, ROOT)
 import torch
 import bench

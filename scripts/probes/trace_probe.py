@@ -1,7 +1,7 @@
 """Per-iteration phase breakdown of the persistent CG kernel (needs a KCG_TRACE=1 build).
 usage: KCG_LIB_PATH=.../trace.so python scripts/trace_probe.py [config] [iters] [route]"""
 import ctypes, os, sys, json
-ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+ROOT = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 sys.path.insert(0, ROOT)
 import numpy as np
 import torch

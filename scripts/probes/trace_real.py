@@ -1,7 +1,7 @@
 """Per-iteration time of the persistent CG kernel during a REAL fullsky solve (tol 1e-10) versus the
 number of faces still active (KCG_TRACE=1 build).  usage: KCG_LIB_PATH=... trace_real.py [config]"""
 import ctypes, json, os, sys
-ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+ROOT = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 sys.path.insert(0, ROOT)
 import numpy as np
 import torch

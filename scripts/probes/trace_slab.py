@@ -1,6 +1,6 @@
 """Per-pass phase breakdown of the slab CG kernel (KCG_TRACE=1 build), planck face split G ways."""
 import ctypes, os, sys, json
-ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+ROOT = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 sys.path.insert(0, ROOT)
 import numpy as np
 import torch
