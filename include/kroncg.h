@@ -76,6 +76,11 @@ typedef enum {
 enum { KCG_PRIOR_LAPLACIAN = 0, KCG_PRIOR_D2 = 1 };
 enum { KCG_LAYOUT_ROW_MAJOR = 0, KCG_LAYOUT_NESTED = 1 };
 enum { KCG_PRECOND_NONE = 0, KCG_PRECOND_BLOCK_JACOBI = 1 };
+/* CG variant ("two variants of the conjugate gradient approach", reading R9): the
+ * single-pass Chronopoulos-Gear form with recomputation (default: one grid-wide reduction and
+ * 48 K N bytes per iteration) or the textbook Hestenes-Stiefel form of Alg. CG (P:L225-241:
+ * two reductions, 72 K N bytes per iteration).  Same iterates in exact arithmetic.             */
+enum { KCG_CG_SINGLE_PASS = 0, KCG_CG_HS = 1 };
 
 /* Problem descriptor (fixed for the life of a context). */
 typedef struct {
@@ -98,6 +103,9 @@ typedef struct {
   int lanczos_store;/* 1: keep the whole Lanczos basis V_1..V_cap in HBM (P*k*N*8*(lanczos_cap + 1)     */
                     /* bytes) and assemble M in one streaming pass; 0: the paper's memory-lean second  */
                     /* Lanczos pass, four block slots                                      */
+  int cg_variant;   /* KCG_CG_SINGLE_PASS (0, default) or KCG_CG_HS; applies to the CG-based routes      */
+                    /* (kron_cg_solve*, sylvester_solve*, kohler, solve_b, posterior_variance); KCG_CG_HS */
+                    /* is not combined with row slabs (KCG_E_CONFIG)                                      */
 } kcg_desc;
 
 /* Solve report, filled on return (host memory). */

@@ -42,7 +42,7 @@ struct Layout {
   size_t r0, r1, p0, p1, partials, state, history, sync, group, resid_partials, resid_out, params_kron, params_syl,
       E_kron, E_syl, W, Y_stage, mu_stage, trace, slots, flags, xg_top, xg_bot, rslots, x_rm, y_rm, hits_rm,
       lz_V, lz_part, lz_st, lz_H, lz_R, lz_Ri, lz_Sinv, lz_g, lz_Z, lz_prm, E_lz, params_koh, E_koh, R_koh, W_koh,
-      total;
+      hs_part, total;
   int lz_slots;
   size_t vec_doubles, partial_doubles;
 };
@@ -119,6 +119,8 @@ Layout layout_of(const kcg_desc* d, int nranks) {
     L.lz_prm = take(P * sizeof(kcg::LzFace));
     L.E_lz = take(P * n * k * 8);
   }
+  if (d->cg_variant == KCG_CG_HS)  // CTA partial sums of the HS variant [2][grid][systems][3]
+    L.hs_part = take(2 * (size_t)KCG_HS_GRID_MAX * P * k * 3 * 8);
   L.total = off;
   return L;
 }
@@ -138,6 +140,7 @@ struct RankState {
   long long* trace = nullptr;
   double *slots = nullptr, *xg_top = nullptr, *xg_bot = nullptr, *rslots = nullptr;
   double *x_rm = nullptr, *y_rm = nullptr, *hits_rm = nullptr;  // NESTED layout only
+  double* hs_part = nullptr;                                      // KCG_CG_HS only
   unsigned long long* flags = nullptr;
   const double* hits = nullptr;
   CgMaps maps_kron, maps_syl;
@@ -197,6 +200,7 @@ RankState carve(char* ws, const Layout& L, int rank, int rows, bool staging, boo
     R.lz_prm = reinterpret_cast<kcg::LzFace*>(ws + L.lz_prm);
     R.E_lz = reinterpret_cast<double*>(ws + L.E_lz);
   }
+  if (L.hs_part) R.hs_part = reinterpret_cast<double*>(ws + L.hs_part);
   if (nested) {
     R.x_rm = reinterpret_cast<double*>(ws + L.x_rm);
     R.y_rm = reinterpret_cast<double*>(ws + L.y_rm);
@@ -245,6 +249,7 @@ bool desc_ok(const kcg_desc* d, std::string* why) {
   if (d->history_cap < 0) { *why = "history_cap < 0"; return false; }
   if (d->lanczos_cap < 0 || d->lanczos_cap > 1000000) { *why = "lanczos_cap outside [0, 1e6]"; return false; }
   if (d->lanczos_store != 0 && d->lanczos_store != 1) { *why = "lanczos_store must be 0 or 1"; return false; }
+  if (d->cg_variant != KCG_CG_SINGLE_PASS && d->cg_variant != KCG_CG_HS) { *why = "unknown cg_variant"; return false; }
   return true;
 }
 
@@ -628,6 +633,10 @@ kcg_status solve_impl(kcg_ctx* c, Route route, const double* Y_in, double* mu_ou
     Lx.nlocal = c->nlocal;
     Lx.ctas = kron ? c->grid_kron : c->grid_syl;
     CK(kcg::launch_cg_slab(Kk, prec, s, Lx, kron ? c->smem_kron : c->smem_syl), "cg slab kernel");
+  } else if (c->d.cg_variant == KCG_CG_HS) {
+    CK(kcg::launch_cg_hs(Kk, prec, c->d.prior == KCG_PRIOR_D2, s, Lx.a[0], c->R[0].r[1], c->R[0].hs_part,
+                         kron ? c->grid_kron : c->grid_syl, kron ? c->smem_kron : c->smem_syl),
+       "cg kernel (HS variant)");
   } else {
     CK(kcg::launch_cg(Kk, prec, c->d.prior == KCG_PRIOR_D2, s, Lx.a[0], Lx.m[0], kron ? c->grid_kron : c->grid_syl,
                       kron ? c->smem_kron : c->smem_syl),
@@ -636,7 +645,10 @@ kcg_status solve_impl(kcg_ctx* c, Route route, const double* Y_in, double* mu_ou
   CK(cudaEventRecord(c->ev[2], s), "event");
   for (int j = 0; j < c->nlocal; ++j) {
     RankState& R = c->R[j];
-    if (KCG_X2) CK(kcg::launch_xfix(Kk, s, R.state, R.p[0], R.p[1], mur(j), n_sys, geom_of(c, R)), "x fix-up kernel");
+    if (c->d.cg_variant == KCG_CG_HS)
+      CK(kcg::launch_hs_xfix(Kk, s, R.state, R.p[0], R.p[1], mur(j), n_sys, c->side, c->pitch), "x fix-up kernel");
+    else if (KCG_X2)
+      CK(kcg::launch_xfix(Kk, s, R.state, R.p[0], R.p[1], mur(j), n_sys, geom_of(c, R)), "x fix-up kernel");
     if (!kron) CK(kcg::launch_backtransform(k, s, R.W_dev, mur(j), P, N), "backtransform kernel");
   }
   // true residual ||b - G x|| / ||b|| (one apply pass; x boundary rows exchanged in slab mode)
@@ -727,6 +739,8 @@ kcg_status solve_impl(kcg_ctx* c, Route route, const double* Y_in, double* mu_ou
     // per pass: read + write r and p (32 B per pixel and plane); x passes also read + write x.
     // Local bytes of this context's ranks (slab mode: the local rows of each local rank).
     rep->loop_bytes = (32.0 * (double)passes + 16.0 * (double)xpasses) * Kk * (double)N * c->nlocal;
+    if (c->d.cg_variant == KCG_CG_HS)  // per iteration: pass A 4 vectors (+ x read + write from the 2nd), pass B 3
+      rep->loop_bytes = (56.0 * (double)sumit + 16.0 * (double)std::max(0LL, sumit - n_sys)) * Kk * (double)N;
     rep->peak_mem_bytes = c->ws_need;
     rep->history_len = std::min(maxit, c->d.history_cap);
     if (rep->history && rep->history_len > 0) {
@@ -925,8 +939,13 @@ kcg_status kohler_impl(kcg_ctx* c, const double* Y_in, double* mu_out, double to
     }
     CK(cudaMemsetAsync(R.sync, 0, 4 * sizeof(unsigned), s), "memset sync");
     const int grid = std::max(1, std::min(c->grid_syl, P * a.tiles_per_sys));
-    CK(kcg::launch_cg(1, prec, d2, s, a, maps, grid, c->smem_syl), "cg kernel (kohler column)");
-    if (KCG_X2) CK(kcg::launch_xfix(1, s, R.state, R.p[0], R.p[1], xcol, P, geom_of(c, R)), "x fix-up kernel");
+    if (c->d.cg_variant == KCG_CG_HS) {
+      CK(kcg::launch_cg_hs(1, prec, d2, s, a, R.r[1], R.hs_part, grid, c->smem_syl), "cg kernel (kohler column, HS)");
+      CK(kcg::launch_hs_xfix(1, s, R.state, R.p[0], R.p[1], xcol, P, c->side, c->pitch), "x fix-up kernel");
+    } else {
+      CK(kcg::launch_cg(1, prec, d2, s, a, maps, grid, c->smem_syl), "cg kernel (kohler column)");
+      if (KCG_X2) CK(kcg::launch_xfix(1, s, R.state, R.p[0], R.p[1], xcol, P, geom_of(c, R)), "x fix-up kernel");
+    }
     if (k > 1) CK(kcg::launch_column_copy(s, xcol, mur, P, k, i, N), "column copy kernel");
     CK(cudaMemcpyAsync(st.data() + (size_t)i * P, R.state, P * sizeof(SysState), cudaMemcpyDeviceToHost, s), "D2H");
   }
@@ -1008,6 +1027,7 @@ kcg_status create_impl(const kcg_desc* d, const kcg_slab* sl, const double* A_ho
   const int G = sl ? sl->nranks : 1;
   if (!slab_ok(d, G, &why)) return fail(KCG_E_SHAPE, why);
   if (sl && d->prior == KCG_PRIOR_D2) return fail(KCG_E_CONFIG, "row slabs are built for KCG_PRIOR_LAPLACIAN");
+  if (sl && d->cg_variant == KCG_CG_HS) return fail(KCG_E_CONFIG, "row slabs run the single-pass CG variant only");
   if (sl && d->layout == KCG_LAYOUT_NESTED)
     return fail(KCG_E_CONFIG, "row slabs need KCG_LAYOUT_ROW_MAJOR (a NESTED face is not split into row slabs)");
   if (sl && (sl->rank0 < 0 || sl->nlocal < 1 || sl->rank0 + sl->nlocal > G || (sl->nlocal != 1 && sl->nlocal != G)))
@@ -1253,6 +1273,17 @@ kcg_status create_impl(const kcg_desc* d, const kcg_slab* sl, const double* A_ho
   c->tiles_y_syl = tiles_y(c->rows, 1, d2);
   int mg = 0;
   const bool prec = d->precond == KCG_PRECOND_BLOCK_JACOBI;
+  if (d->cg_variant == KCG_CG_HS) {  // textbook CG variant: its own tile geometry and grid
+    c->tiles_y_kron = (c->rows + kcg::hs_tile_y(k) - 1) / kcg::hs_tile_y(k);
+    c->tiles_y_syl = (c->rows + kcg::hs_tile_y(1) - 1) / kcg::hs_tile_y(1);
+    CKC(kcg::hs_kernel_config(k, hits_dev != nullptr, prec, d2, P, &mg, &c->smem_kron), "hs kernel config (kron)");
+    c->grid_kron = std::max(1, std::min({mg, KCG_HS_GRID_MAX, P * c->tiles_x_kron * c->tiles_y_kron}));
+    CKC(kcg::hs_kernel_config(1, hits_dev != nullptr, prec, d2, P * k, &mg, &c->smem_syl), "hs kernel config (sylvester)");
+    c->grid_syl = std::max(1, std::min({mg, KCG_HS_GRID_MAX, P * k * c->tiles_x_syl * c->tiles_y_syl}));
+    for (int i = 0; i < 4; ++i) CKC(cudaEventCreate(&c->ev[i]), "event create");
+    *out = c;
+    return KCG_OK;
+  }
   CKC(kcg::cg_kernel_config(k, hits_dev != nullptr, prec, c->slab, d2, P, &mg, &c->smem_kron), "cg kernel config (kron)");
   c->grid_kron = std::max(1, std::min(mg / c->nlocal, P * c->tiles_x_kron * c->tiles_y_kron));
   CKC(kcg::cg_kernel_config(1, hits_dev != nullptr, prec, c->slab, d2, P * k, &mg, &c->smem_syl),

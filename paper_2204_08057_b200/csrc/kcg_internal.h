@@ -182,6 +182,16 @@ struct SlabGeom {
   int d2;                    // 1: prior Q0 = D^2 + kappa2 I (radius-2 operator)
 };
 
+// ---- textbook (HS) CG variant (kcg_hs.cuh; desc.cg_variant = KCG_CG_HS, reading R9)
+#define KCG_HS_GRID_MAX 1024  // CTA partial rows per system in the workspace (>= the cooperative grid)
+__host__ __device__ constexpr int hs_tile_y(int K) { return K <= 2 ? 16 : (K <= 4 ? 8 : 4); }
+cudaError_t hs_kernel_config(int K, bool hits, bool prec, bool d2, int n_sys, int* max_grid, size_t* smem);
+// q: a [n_sys K][side][pitch] scratch vector; part: [2][KCG_HS_GRID_MAX][n_sys][3] doubles
+cudaError_t launch_cg_hs(int K, bool prec, bool d2, cudaStream_t s, const CgArgs& a, double* q, double* part,
+                         int grid, size_t smem);
+cudaError_t launch_hs_xfix(int K, cudaStream_t s, const SysState* st, const double* p0, const double* p1, double* x,
+                           int n_sys, int side, int pitch);
+
 // ---- block-Lanczos Sylvester solver (Alg. SylvSolver)
 #define KCG_LZ_GRID_MAX 512  // partial-sum rows per face in the workspace (>= the cooperative grid)
 struct LzFace {              // per-face constants, host-computed at create (Lemma 2)

@@ -31,13 +31,14 @@ KCG_E_NONFINITE, KCG_E_BREAKDOWN, KCG_E_CUDA, KCG_E_NCCL, KCG_E_STATE = 5, 6, 7,
 KCG_PRIOR_LAPLACIAN, KCG_PRIOR_D2 = 0, 1
 KCG_LAYOUT_ROW_MAJOR, KCG_LAYOUT_NESTED = 0, 1
 KCG_PRECOND_NONE, KCG_PRECOND_BLOCK_JACOBI = 0, 1
+KCG_CG_SINGLE_PASS, KCG_CG_HS = 0, 1
 
 
 class kcg_desc(C.Structure):
     _fields_ = [("level", C.c_int), ("n_freq", C.c_int), ("n_comp", C.c_int),
                 ("n_patches", C.c_int), ("prior", C.c_int), ("layout", C.c_int),
                 ("precond", C.c_int), ("host_staging", C.c_int), ("history_cap", C.c_int),
-                ("lanczos_cap", C.c_int), ("lanczos_store", C.c_int)]
+                ("lanczos_cap", C.c_int), ("lanczos_store", C.c_int), ("cg_variant", C.c_int)]
 
 
 class kcg_report(C.Structure):
@@ -133,11 +134,13 @@ class KronCG:
     lanczos_cap: > 0 provisions the block-Lanczos route (``lanczos``, Alg. SylvSolver) for up to that
     many Lanczos steps; lanczos_store keeps the whole basis in HBM (one assembly pass) instead of
     the paper's second Lanczos pass.
+    cg_variant: "single_pass" (Chronopoulos-Gear with recomputation, one reduction per iteration)
+    or "hs" (textbook Hestenes-Stiefel CG, Alg. CG, two reductions) -- reading R9.
     """
 
     def __init__(self, level, A, noise_prec, prior_scale, kappa2, hits=None, device=None,
                  host_staging=False, history_cap=0, stream=None, precond="none", layout="row",
-                 prior="laplacian", lanczos_cap=0, lanczos_store=False):
+                 prior="laplacian", lanczos_cap=0, lanczos_store=False, cg_variant="single_pass"):
         import torch
         A = np.ascontiguousarray(np.asarray(A, dtype=np.float64))
         if A.ndim == 2:
@@ -156,9 +159,10 @@ class KronCG:
         pc = {"none": KCG_PRECOND_NONE, "block_jacobi": KCG_PRECOND_BLOCK_JACOBI}[precond]
         lay = {"row": KCG_LAYOUT_ROW_MAJOR, "nested": KCG_LAYOUT_NESTED}[layout]
         pr = {"laplacian": KCG_PRIOR_LAPLACIAN, "d2": KCG_PRIOR_D2}[prior]
+        cv = {"single_pass": KCG_CG_SINGLE_PASS, "hs": KCG_CG_HS}[cg_variant]
         self.desc = kcg_desc(level, n, k, P, pr, lay,
                              pc, int(bool(host_staging)), int(history_cap), int(lanczos_cap),
-                             int(bool(lanczos_store)))
+                             int(bool(lanczos_store)), cv)
         ws = kron_cg_workspace_size(C.byref(self.desc))
         if ws == 0:
             raise KcgError(KCG_E_SHAPE, "invalid descriptor")

@@ -56,6 +56,11 @@ def test_host_logic_without_gpu(lib):
     for bad in [K.kcg_desc(13, 9, 4, 1, 0, 0, 0, 0, 0), K.kcg_desc(5, 9, 9, 1, 0, 0, 0, 0, 0),
                 K.kcg_desc(5, 2, 3, 1, 0, 0, 0, 0, 0), K.kcg_desc(5, 9, 3, 0, 0, 0, 0, 0, 0)]:
         assert K.kron_cg_workspace_size(ctypes.byref(bad)) == 0
+    # the textbook-CG variant (reading R9) reserves its CTA partial sums; unknown variants are rejected
+    dh = K.kcg_desc(10, 9, 4, 12, 0, 0, 0, 0, 0, 0, 0, K.KCG_CG_HS)
+    wsh = K.kron_cg_workspace_size(ctypes.byref(dh))
+    assert wsh - ws >= 2 * 1024 * 12 * 4 * 3 * 8
+    assert K.kron_cg_workspace_size(ctypes.byref(K.kcg_desc(10, 9, 4, 12, 0, 0, 0, 0, 0, 0, 0, 2))) == 0
     assert K.kcg_status_string(6) == b"KCG_E_BREAKDOWN"
     # create rejects a bad descriptor before touching the GPU
     ctx = ctypes.c_void_p()
