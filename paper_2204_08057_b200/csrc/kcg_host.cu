@@ -42,7 +42,7 @@ struct Layout {
   size_t r0, r1, p0, p1, partials, state, history, sync, group, resid_partials, resid_out, params_kron, params_syl,
       E_kron, E_syl, W, Y_stage, mu_stage, trace, slots, flags, xg_top, xg_bot, rslots, x_rm, y_rm, hits_rm,
       lz_V, lz_part, lz_st, lz_H, lz_R, lz_Ri, lz_Sinv, lz_g, lz_Z, lz_prm, E_lz, params_koh, E_koh, R_koh, W_koh,
-      hs_part, total;
+      hs_part, res_part, total;
   int lz_slots;
   size_t vec_doubles, partial_doubles;
 };
@@ -119,6 +119,7 @@ Layout layout_of(const kcg_desc* d, int nranks) {
     L.lz_prm = take(P * sizeof(kcg::LzFace));
     L.E_lz = take(P * n * k * 8);
   }
+  L.res_part = take(2 * (size_t)KCG_RES_CTA_MAX * 3 * 8);  // resident kernel: CTA partials [2][grid][3]
   if (d->cg_variant == KCG_CG_HS)  // CTA partial sums of the HS variant [2][grid][systems][3]
     L.hs_part = take(2 * (size_t)KCG_HS_GRID_MAX * P * k * 3 * 8);
   L.total = off;
@@ -141,6 +142,7 @@ struct RankState {
   double *slots = nullptr, *xg_top = nullptr, *xg_bot = nullptr, *rslots = nullptr;
   double *x_rm = nullptr, *y_rm = nullptr, *hits_rm = nullptr;  // NESTED layout only
   double* hs_part = nullptr;                                      // KCG_CG_HS only
+  double* res_part = nullptr;                                     // resident kernel partials
   unsigned long long* flags = nullptr;
   const double* hits = nullptr;
   CgMaps maps_kron, maps_syl;
@@ -201,6 +203,7 @@ RankState carve(char* ws, const Layout& L, int rank, int rows, bool staging, boo
     R.E_lz = reinterpret_cast<double*>(ws + L.E_lz);
   }
   if (L.hs_part) R.hs_part = reinterpret_cast<double*>(ws + L.hs_part);
+  R.res_part = reinterpret_cast<double*>(ws + L.res_part);
   if (nested) {
     R.x_rm = reinterpret_cast<double*>(ws + L.x_rm);
     R.y_rm = reinterpret_cast<double*>(ws + L.y_rm);
@@ -211,8 +214,17 @@ RankState carve(char* ws, const Layout& L, int rank, int rows, bool staging, boo
 
 }  // namespace
 
+// Small-problem regime (kcg_res.cuh): the CG state of a route kept in shared memory, strips of
+// side / nstrip rows, grid = systems * nstrip CTAs (off: the streaming persistent kernel).
+struct ResPlan {
+  bool on = false;
+  int nstrip = 0, grid = 0;
+  size_t smem = 0;
+};
+
 struct kcg_ctx {
   kcg_desc d;
+  ResPlan res_kron, res_syl, res_koh;
   cudaStream_t stream = nullptr;
   int side = 0, pitch = 0, P = 0, n = 0, k = 0;
   int nranks = 1, rank0 = 0, nlocal = 1, rows = 0, ghost = 0;
@@ -587,6 +599,7 @@ kcg_status solve_impl(kcg_ctx* c, Route route, const double* Y_in, double* mu_ou
   CgSlabLaunch* Lp = new CgSlabLaunch();  // large (TMA maps of every rank): heap, not stack
   std::unique_ptr<CgSlabLaunch> L_owner(Lp);
   CgSlabLaunch& Lx = *Lp;
+  const ResPlan res = c->slab ? ResPlan{} : (kron ? c->res_kron : c->res_syl);
   for (int j = 0; j < c->nlocal; ++j) {
     RankState& R = c->R[j];
     CgArgs& a = Lx.a[j];
@@ -633,6 +646,11 @@ kcg_status solve_impl(kcg_ctx* c, Route route, const double* Y_in, double* mu_ou
     Lx.nlocal = c->nlocal;
     Lx.ctas = kron ? c->grid_kron : c->grid_syl;
     CK(kcg::launch_cg_slab(Kk, prec, s, Lx, kron ? c->smem_kron : c->smem_syl), "cg slab kernel");
+  } else if (res.on) {
+    CgArgs& a = Lx.a[0];
+    a.tiles_per_sys = res.nstrip;
+    if (c->d.history_cap > 0) CK(cudaMemsetAsync(a.history, 0, (size_t)c->d.history_cap * 8, s), "memset history");
+    CK(kcg::launch_cg_resident(Kk, prec, s, a, c->R[0].res_part, res.grid, res.smem), "cg kernel (resident)");
   } else if (c->d.cg_variant == KCG_CG_HS) {
     CK(kcg::launch_cg_hs(Kk, prec, c->d.prior == KCG_PRIOR_D2, s, Lx.a[0], c->R[0].r[1], c->R[0].hs_part,
                          kron ? c->grid_kron : c->grid_syl, kron ? c->smem_kron : c->smem_syl),
@@ -645,7 +663,8 @@ kcg_status solve_impl(kcg_ctx* c, Route route, const double* Y_in, double* mu_ou
   CK(cudaEventRecord(c->ev[2], s), "event");
   for (int j = 0; j < c->nlocal; ++j) {
     RankState& R = c->R[j];
-    if (c->d.cg_variant == KCG_CG_HS)
+    if (res.on) {  // x written whole by the resident kernel
+    } else if (c->d.cg_variant == KCG_CG_HS)
       CK(kcg::launch_hs_xfix(Kk, s, R.state, R.p[0], R.p[1], mur(j), n_sys, c->side, c->pitch), "x fix-up kernel");
     else if (KCG_X2)
       CK(kcg::launch_xfix(Kk, s, R.state, R.p[0], R.p[1], mur(j), n_sys, geom_of(c, R)), "x fix-up kernel");
@@ -741,6 +760,12 @@ kcg_status solve_impl(kcg_ctx* c, Route route, const double* Y_in, double* mu_ou
     rep->loop_bytes = (32.0 * (double)passes + 16.0 * (double)xpasses) * Kk * (double)N * c->nlocal;
     if (c->d.cg_variant == KCG_CG_HS)  // per iteration: pass A 4 vectors (+ x read + write from the 2nd), pass B 3
       rep->loop_bytes = (56.0 * (double)sumit + 16.0 * (double)std::max(0LL, sumit - n_sys)) * Kk * (double)N;
+    if (res.on) {  // global bytes of the resident kernel: b in, x out, per pass the strips' halo rows
+      const int rs = c->side / res.nstrip;
+      rep->loop_bytes = 16.0 * Kk * (double)N * n_sys;
+      if (res.nstrip > 1)
+        rep->loop_bytes += (double)passes * res.nstrip * (std::min(4, rs) + 4) * c->side * Kk * 16.0;
+    }
     rep->peak_mem_bytes = c->ws_need;
     rep->history_len = std::min(maxit, c->d.history_cap);
     if (rep->history && rep->history_len > 0) {
@@ -939,7 +964,11 @@ kcg_status kohler_impl(kcg_ctx* c, const double* Y_in, double* mu_out, double to
     }
     CK(cudaMemsetAsync(R.sync, 0, 4 * sizeof(unsigned), s), "memset sync");
     const int grid = std::max(1, std::min(c->grid_syl, P * a.tiles_per_sys));
-    if (c->d.cg_variant == KCG_CG_HS) {
+    if (c->res_koh.on) {
+      a.tiles_per_sys = c->res_koh.nstrip;
+      CK(kcg::launch_cg_resident(1, prec, s, a, R.res_part, c->res_koh.grid, c->res_koh.smem),
+         "cg kernel (kohler column, resident)");
+    } else if (c->d.cg_variant == KCG_CG_HS) {
       CK(kcg::launch_cg_hs(1, prec, d2, s, a, R.r[1], R.hs_part, grid, c->smem_syl), "cg kernel (kohler column, HS)");
       CK(kcg::launch_hs_xfix(1, s, R.state, R.p[0], R.p[1], xcol, P, c->side, c->pitch), "x fix-up kernel");
     } else {
@@ -1007,6 +1036,34 @@ kcg_status kohler_impl(kcg_ctx* c, const double* Y_in, double* mu_out, double to
 }  // namespace
 
 namespace {
+
+// Plan the shared-memory-resident CG kernel for systems of K planes on a side x side face: one CTA per
+// system ("single": the face's K N values are few) or strips of RS >= 2 rows, at most one CTA per SM.
+ResPlan plan_resident(int K, int side, int n_sys, bool hits, bool prec, int nsm) {
+  ResPlan P;
+  if (const char* ev = std::getenv("KCG_RESIDENT"))
+    if (std::atoi(ev) == 0) return P;
+  if (prec && K > 7) return P;
+  const size_t lim = 220 * 1024;  // dynamic smem budget (static: ~3 KB)
+  int best_rs = 0;
+  if ((size_t)K * side * side <= 8192 && kcg::res_smem(K, side, side, hits, prec, n_sys) <= lim && n_sys <= nsm)
+    best_rs = side;
+  for (int rs = 2; !best_rs && rs <= side; rs *= 2) {
+    const long long grid = (long long)n_sys * (side / rs);
+    if (grid <= nsm && grid <= KCG_RES_CTA_MAX && kcg::res_smem(K, rs, side, hits, prec, n_sys) <= lim) best_rs = rs;
+  }
+  if (!best_rs) return P;
+  P.nstrip = side / best_rs;
+  P.grid = n_sys * P.nstrip;
+  P.smem = kcg::res_smem(K, best_rs, side, hits, prec, n_sys);
+  int nb = 0;
+  if (kcg::res_kernel_config(K, hits, prec, P.smem, &nb) != cudaSuccess || nb < 1 || (long long)nb * nsm < P.grid) {
+    cudaGetLastError();
+    return ResPlan{};
+  }
+  P.on = true;
+  return P;
+}
 
 // Shared body of kron_cg_create / kron_cg_create_slab.
 kcg_status create_impl(const kcg_desc* d, const kcg_slab* sl, const double* A_host, const double* T_host,
@@ -1273,6 +1330,14 @@ kcg_status create_impl(const kcg_desc* d, const kcg_slab* sl, const double* A_ho
   c->tiles_y_syl = tiles_y(c->rows, 1, d2);
   int mg = 0;
   const bool prec = d->precond == KCG_PRECOND_BLOCK_JACOBI;
+  if (!c->slab && !d2 && d->cg_variant == KCG_CG_SINGLE_PASS) {  // small-problem regime (state in smem)
+    int dev = 0, nsm = 0;
+    CKC(cudaGetDevice(&dev), "device");
+    CKC(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev), "device attribute");
+    c->res_kron = plan_resident(k, c->side, P, hits_dev != nullptr, prec, nsm);
+    c->res_syl = plan_resident(1, c->side, P * k, hits_dev != nullptr, prec, nsm);
+    c->res_koh = plan_resident(1, c->side, P, hits_dev != nullptr, prec, nsm);
+  }
   if (d->cg_variant == KCG_CG_HS) {  // textbook CG variant: its own tile geometry and grid
     c->tiles_y_kron = (c->rows + kcg::hs_tile_y(k) - 1) / kcg::hs_tile_y(k);
     c->tiles_y_syl = (c->rows + kcg::hs_tile_y(1) - 1) / kcg::hs_tile_y(1);
@@ -1536,7 +1601,8 @@ KCG_API int kcg_debug_state(const kcg_ctx* c, double* out, int max_sys) {
 }
 
 // Diagnostic (not part of the ABI header): launch configuration of the CG kernel per route:
-// out = {grid_kron, grid_syl, smem_kron, smem_syl, sm_count} (grids per rank in slab mode).
+// out = {grid_kron, grid_syl, smem_kron, smem_syl, sm_count, resident strips kron / syl / kohler}
+// (grids per rank in slab mode).
 KCG_API int kcg_debug_config(const kcg_ctx* c, long long* out) {
   if (!c || !out) return 0;
   int dev = 0, nsm = 0;
@@ -1544,7 +1610,11 @@ KCG_API int kcg_debug_config(const kcg_ctx* c, long long* out) {
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
   out[0] = c->grid_kron; out[1] = c->grid_syl; out[2] = (long long)c->smem_kron; out[3] = (long long)c->smem_syl;
   out[4] = nsm;
-  return 5;
+  // the shared-memory-resident plans (small-problem regime): strips per system, 0 = streaming kernel
+  out[5] = c->res_kron.on ? c->res_kron.nstrip : 0;
+  out[6] = c->res_syl.on ? c->res_syl.nstrip : 0;
+  out[7] = c->res_koh.on ? c->res_koh.nstrip : 0;
+  return 8;
 }
 
 // Diagnostic (not part of the ABI header): copy the phase trace of the last solve (KCG_TRACE builds).

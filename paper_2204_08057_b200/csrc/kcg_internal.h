@@ -192,6 +192,13 @@ cudaError_t launch_cg_hs(int K, bool prec, bool d2, cudaStream_t s, const CgArgs
 cudaError_t launch_hs_xfix(int K, cudaStream_t s, const SysState* st, const double* p0, const double* p1, double* x,
                            int n_sys, int side, int pitch);
 
+// ---- small-problem regime: CG state resident in shared memory (kcg_res.cuh)
+#define KCG_RES_CTA_MAX 1024  // CTA partial rows in the workspace [2][KCG_RES_CTA_MAX][3]
+size_t res_smem(int K, int RS, int side, bool hits, bool prec, int n_sys);  // dynamic smem for RS-row strips
+cudaError_t res_kernel_config(int K, bool hits, bool prec, size_t smem, int* blocks_per_sm);
+// a.tiles_per_sys = strips per system (side / RS); grid = n_sys * strips; part: [2][grid][3] doubles
+cudaError_t launch_cg_resident(int K, bool prec, cudaStream_t s, const CgArgs& a, double* part, int grid, size_t smem);
+
 // ---- block-Lanczos Sylvester solver (Alg. SylvSolver)
 #define KCG_LZ_GRID_MAX 512  // partial-sum rows per face in the workspace (>= the cooperative grid)
 struct LzFace {              // per-face constants, host-computed at create (Lemma 2)

@@ -347,9 +347,10 @@ class KronCG:
         (kcg_debug_config, not part of the ABI header)."""
         f = _lib.kcg_debug_config
         f.restype, f.argtypes = C.c_int, [_ctxp, C.c_void_p]
-        out = (C.c_longlong * 5)()
+        out = (C.c_longlong * 8)()
         f(self._ctx, out)
-        return dict(grid_kron=out[0], grid_syl=out[1], smem_kron=out[2], smem_syl=out[3], sm_count=out[4])
+        return dict(grid_kron=out[0], grid_syl=out[1], smem_kron=out[2], smem_syl=out[3], sm_count=out[4],
+                    resident_kron=out[5], resident_syl=out[6], resident_kohler=out[7])
 
     def close(self):
         if getattr(self, "_ctx", None) is not None and self._ctx.value:

@@ -1,0 +1,128 @@
+"""GPU parity of the small-problem regime (kcg_res.cuh: CG state resident in shared memory; SURVEY 8(d)
+"size regimes", the paper's levels 1-10 at P:L600) against the oracle's textbook CG (oracle/cg.py) and
+against the streaming persistent kernel (KCG_RESIDENT=0 at create): same single-pass iteration, same
+scalars, so the iterates agree to rounding and the iteration counts within +-2."""
+
+import os
+
+import numpy as np
+import pytest
+
+from gpu_util import have_gpu, make_ctx, rel
+from oracle import cg, exact, kohler, model, sylvester
+from synth import make_config, make_patch
+
+pytestmark = [pytest.mark.gpu, pytest.mark.skipif(not have_gpu(), reason="needs a CUDA GPU")]
+TOL = 1e-10
+
+
+def _streaming_ctx(ps, **kw):
+    os.environ["KCG_RESIDENT"] = "0"
+    try:
+        return make_ctx(ps, **kw)
+    finally:
+        del os.environ["KCG_RESIDENT"]
+
+
+def _check(ps, precond=None, expect_strips=None):
+    ctx, Y = make_ctx(ps, precond=precond or "none")
+    cfg = ctx.launch_config()
+    assert cfg["resident_kron"] > 0, cfg
+    if expect_strips is not None:
+        assert cfg["resident_kron"] == expect_strips, cfg
+    mu, rep = ctx.solve(Y, tol=TOL)
+    mu = mu.cpu().numpy()
+    assert rep["converged"], rep["status_name"]
+    for i, p in enumerate(ps):
+        G, b = model.problem_system(p)
+        K = cg.block_jacobi_precond(p.level, p.A, p.noise_prec, p.tau, p.kappa2, p.hits) if precond else None
+        ref = cg.cg_hs(G, b, tol=TOL, precond=K)
+        assert rel(mu[i], ref.x) <= 1e-8, (i, rel(mu[i], ref.x))
+        assert abs(rep["iterations_per"][i] - ref.iterations) <= 2, (i, rep["iterations_per"][i], ref.iterations)
+    assert rep["rel_residual_true"] <= 5 * TOL
+    # the streaming kernel: same iteration
+    c2, _ = _streaming_ctx(ps, precond=precond or "none")
+    assert c2.launch_config()["resident_kron"] == 0
+    mu2, rep2 = c2.solve(Y, tol=TOL)
+    assert rel(mu, mu2.cpu().numpy()) <= 1e-10
+    assert all(abs(a - b) <= 1 for a, b in zip(rep["iterations_per"], rep2["iterations_per"]))
+    return ctx, Y, mu, rep
+
+
+def test_resident_tiny_single_cta():
+    _, _, mu, _ = _check(make_config("tiny"), expect_strips=1)
+    assert rel(mu[0], exact.problem_dct_exact(make_config("tiny")[0])) <= 1e-8
+
+
+def test_resident_medium_strips():
+    _, _, mu, _ = _check(make_config("medium"), expect_strips=128)
+    assert rel(mu[0], exact.problem_dct_exact(make_config("medium")[0])) <= 1e-8
+
+
+@pytest.mark.parametrize("level,k,hits,P", [(0, 1, None, 2), (1, 2, "random", 3), (2, 3, None, 2),
+                                            (3, 8, "random", 2), (4, 5, None, 12), (5, 6, "random", 2),
+                                            (6, 4, None, 3), (7, 2, "random", 1), (7, 1, None, 2)])
+def test_resident_levels(level, k, hits, P):
+    _check([make_patch(level, 9, k, seed=700 + s, tau="loguniform", hits=hits) for s in range(P)])
+
+
+@pytest.mark.parametrize("level,k,hits", [(0, 2, None), (3, 4, "random"), (5, 7, None), (6, 3, "random")])
+def test_resident_block_jacobi(level, k, hits):
+    _check([make_patch(level, 9, k, seed=720 + s, tau="loguniform", hits=hits) for s in range(2)],
+           precond="block_jacobi")
+
+
+def test_resident_sylvester_and_kohler_medium():
+    ps = make_config("medium")
+    ctx, Y = make_ctx(ps)
+    cfg = ctx.launch_config()
+    assert cfg["resident_syl"] > 0 and cfg["resident_kohler"] > 0, cfg
+    mu, rep = ctx.sylvester(Y, tol=TOL)
+    ref = sylvester.problem_solve(ps[0], tol=TOL)
+    assert rel(mu.cpu().numpy()[0], ref.x) <= 1e-8
+    assert all(abs(a - b) <= 2 for a, b in zip(rep["iterations_per"], ref.iterations))
+    mk, _ = ctx.kohler(Y, tol=TOL)
+    assert rel(mk.cpu().numpy()[0], kohler.problem_solve(ps[0], tol=TOL).x) <= 1e-8
+
+
+def test_resident_nested_and_fullsky_small_level():
+    """12 faces at level 5 (one CTA per face, no grid barrier) in NESTED order."""
+    import torch
+    from paper_2204_08057_b200.kroncg import KronCG
+    from synth.problems import stack
+    ps = [make_patch(5, 9, 4, seed=100 + f, tau="loguniform") for f in range(12)]
+    st = stack(ps)
+    nest = lambda a: model.to_layout(5, a, "nested").reshape(np.shape(a))
+    ctx = KronCG(5, st["A"], st["noise_prec"], st["tau"], st["kappa2"], layout="nested", history_cap=1000)
+    assert ctx.launch_config()["resident_kron"] == 1
+    mu, rep = ctx.solve(torch.from_numpy(nest(st["Y"])).cuda(), tol=TOL)
+    mu = mu.cpu().numpy()
+    for i, p in enumerate(ps):
+        G, b = model.problem_system(p, layout="nested")
+        ref = cg.cg_hs(G, b, tol=TOL)
+        assert rel(mu[i], ref.x) <= 1e-8
+        assert abs(rep["iterations_per"][i] - ref.iterations) <= 2
+    h = rep["history"]
+    assert len(h) == rep["iterations"] and h[-1] <= TOL < h[-2]
+
+
+def test_resident_zero_rhs_max_iter_nonfinite_and_determinism():
+    import torch
+    from paper_2204_08057_b200.kroncg import KcgError
+    for level in (4, 7):  # single-CTA and strip modes
+        ps = [make_patch(level, 9, 3, seed=1)]
+        ctx, Y = make_ctx(ps)
+        assert ctx.launch_config()["resident_kron"] > 0
+        mu, rep = ctx.solve(torch.zeros_like(Y), tol=TOL)
+        assert rep["iterations"] == 0 and rep["converged"] and not mu.any()
+        mu, rep = ctx.solve(Y, tol=TOL, max_iter=7)
+        assert rep["status_name"] == "KCG_NOT_CONVERGED" and rep["iterations"] == 7
+        G, b = model.problem_system(ps[0])
+        assert rel(mu.cpu().numpy()[0], cg.cg_hs(G, b, tol=1e-30, max_iter=7).x) <= 1e-10
+        m1, _ = ctx.solve(Y, tol=TOL)
+        m2, _ = ctx.solve(Y, tol=TOL)
+        assert torch.equal(m1, m2)
+        Y[0, 1, 2, 2] = float("nan")
+        with pytest.raises(KcgError) as e:
+            ctx.solve(Y, tol=TOL)
+        assert e.value.status == 5
