@@ -127,6 +127,8 @@ typedef struct {
   size_t peak_mem_bytes;   /* workspace bytes                                                */
   double* history;         /* optional caller array [history_cap] (NULL = skip)               */
   int history_len;
+  long long kernel_launches; /* launches of the library's own kernels by this call (counted on */
+                             /* the host at each launch; memsets and copies not included)     */
 } kcg_report;
 
 /* Bytes of device workspace needed for desc (256-byte aligned sub-buffers). 0 on bad desc. */

@@ -242,6 +242,7 @@ struct kcg_ctx {
   size_t smem_lz = 0;
   std::vector<kcg::LzState> lz_host;
   unsigned long long solve_id = 0;     // cross-rank operations so far (identical on every rank)
+  long long nlaunch = 0;               // library kernel launches since the current entry point began
   cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
   std::vector<SysState> st_host;
   std::vector<double> resid_host;
@@ -483,6 +484,12 @@ kcg_status cuda_fail(kcg_ctx* c, cudaError_t e, const char* what) {
     cudaError_t _e = (call);                            \
     if (_e != cudaSuccess) return cuda_fail(c, _e, what); \
   } while (0)
+// a launch of one of the library's kernels (counted for report->kernel_launches)
+#define CKL(call, what) \
+  do {                  \
+    ++c->nlaunch;       \
+    CK(call, what);     \
+  } while (0)
 
 enum Route { ROUTE_KRON = 0, ROUTE_SYL = 1 };
 
@@ -533,9 +540,9 @@ kcg_status exchange_x_rows(kcg_ctx* c, const double* x_all, size_t x_rank_stride
     const RankState& R = c->R[j];
     double* up = R.rank > 0 ? peer_ptr<double>(c, R.rank - 1, c->L.xg_bot) : nullptr;
     double* dn = R.rank + 1 < c->nranks ? peer_ptr<double>(c, R.rank + 1, c->L.xg_top) : nullptr;
-    CK(kcg::launch_xghost(s, x_all + j * x_rank_stride, up, dn, c->P * c->k, geom_of(c, R)), "x ghost kernel");
+    CKL(kcg::launch_xghost(s, x_all + j * x_rank_stride, up, dn, c->P * c->k, geom_of(c, R)), "x ghost kernel");
   }
-  CK(kcg::launch_xrank_sync(s, xsync_of(c, tag)), "rendezvous kernel");
+  CKL(kcg::launch_xrank_sync(s, xsync_of(c, tag)), "rendezvous kernel");
   return KCG_OK;
 }
 
@@ -581,8 +588,8 @@ kcg_status solve_impl(kcg_ctx* c, Route route, const double* Y_in, double* mu_ou
     RankState& R = c->R[j];
     if (host_io) CK(cudaMemcpyAsync(R.Y_stage, Y_in + j * y_stride, y_stride * 8, cudaMemcpyHostToDevice, s), "H2D Y");
     if (inmode == IN_B_USER && R.y_rm)
-      CK(kcg::launch_permute(s, Y_in, R.y_rm, (size_t)P * k, c->side, false), "permute b");
-    CK(kcg::launch_rhs(k, s, Yr(j), bgiven ? nullptr : (kron ? R.E_kron : R.E_syl), R.hits, R.r[0], R.p[0], mur(j), P,
+      CKL(kcg::launch_permute(s, Y_in, R.y_rm, (size_t)P * k, c->side, false), "permute b");
+    CKL(kcg::launch_rhs(k, s, Yr(j), bgiven ? nullptr : (kron ? R.E_kron : R.E_syl), R.hits, R.r[0], R.p[0], mur(j), P,
                        nin, gin(R)),
        "rhs kernel");
   }
@@ -592,7 +599,7 @@ kcg_status solve_impl(kcg_ctx* c, Route route, const double* Y_in, double* mu_ou
       double *ur = nullptr, *up = nullptr, *dr = nullptr, *dp = nullptr;
       if (R.rank > 0) { ur = peer_ptr<double>(c, R.rank - 1, c->L.r0); up = peer_ptr<double>(c, R.rank - 1, c->L.p0); }
       if (R.rank + 1 < c->nranks) { dr = peer_ptr<double>(c, R.rank + 1, c->L.r0); dp = peer_ptr<double>(c, R.rank + 1, c->L.p0); }
-      CK(kcg::launch_ghost_fill(s, R.r[0], R.p[0], ur, up, dr, dp, P * k, geom_of(c, R)), "ghost fill kernel");
+      CKL(kcg::launch_ghost_fill(s, R.r[0], R.p[0], ur, up, dr, dp, P * k, geom_of(c, R)), "ghost fill kernel");
     }
   CK(cudaEventRecord(c->ev[1], s), "event");
 
@@ -645,18 +652,18 @@ kcg_status solve_impl(kcg_ctx* c, Route route, const double* Y_in, double* mu_ou
   if (c->slab) {
     Lx.nlocal = c->nlocal;
     Lx.ctas = kron ? c->grid_kron : c->grid_syl;
-    CK(kcg::launch_cg_slab(Kk, prec, s, Lx, kron ? c->smem_kron : c->smem_syl), "cg slab kernel");
+    CKL(kcg::launch_cg_slab(Kk, prec, s, Lx, kron ? c->smem_kron : c->smem_syl), "cg slab kernel");
   } else if (res.on) {
     CgArgs& a = Lx.a[0];
     a.tiles_per_sys = res.nstrip;
     if (c->d.history_cap > 0) CK(cudaMemsetAsync(a.history, 0, (size_t)c->d.history_cap * 8, s), "memset history");
-    CK(kcg::launch_cg_resident(Kk, prec, s, a, c->R[0].res_part, res.grid, res.smem), "cg kernel (resident)");
+    CKL(kcg::launch_cg_resident(Kk, prec, s, a, c->R[0].res_part, res.grid, res.smem), "cg kernel (resident)");
   } else if (c->d.cg_variant == KCG_CG_HS) {
-    CK(kcg::launch_cg_hs(Kk, prec, c->d.prior == KCG_PRIOR_D2, s, Lx.a[0], c->R[0].r[1], c->R[0].hs_part,
+    CKL(kcg::launch_cg_hs(Kk, prec, c->d.prior == KCG_PRIOR_D2, s, Lx.a[0], c->R[0].r[1], c->R[0].hs_part,
                          kron ? c->grid_kron : c->grid_syl, kron ? c->smem_kron : c->smem_syl),
        "cg kernel (HS variant)");
   } else {
-    CK(kcg::launch_cg(Kk, prec, c->d.prior == KCG_PRIOR_D2, s, Lx.a[0], Lx.m[0], kron ? c->grid_kron : c->grid_syl,
+    CKL(kcg::launch_cg(Kk, prec, c->d.prior == KCG_PRIOR_D2, s, Lx.a[0], Lx.m[0], kron ? c->grid_kron : c->grid_syl,
                       kron ? c->smem_kron : c->smem_syl),
        "cg kernel");
   }
@@ -665,10 +672,10 @@ kcg_status solve_impl(kcg_ctx* c, Route route, const double* Y_in, double* mu_ou
     RankState& R = c->R[j];
     if (res.on) {  // x written whole by the resident kernel
     } else if (c->d.cg_variant == KCG_CG_HS)
-      CK(kcg::launch_hs_xfix(Kk, s, R.state, R.p[0], R.p[1], mur(j), n_sys, c->side, c->pitch), "x fix-up kernel");
+      CKL(kcg::launch_hs_xfix(Kk, s, R.state, R.p[0], R.p[1], mur(j), n_sys, c->side, c->pitch), "x fix-up kernel");
     else if (KCG_X2)
-      CK(kcg::launch_xfix(Kk, s, R.state, R.p[0], R.p[1], mur(j), n_sys, geom_of(c, R)), "x fix-up kernel");
-    if (!kron) CK(kcg::launch_backtransform(k, s, R.W_dev, mur(j), P, N), "backtransform kernel");
+      CKL(kcg::launch_xfix(Kk, s, R.state, R.p[0], R.p[1], mur(j), n_sys, geom_of(c, R)), "x fix-up kernel");
+    if (!kron) CKL(kcg::launch_backtransform(k, s, R.W_dev, mur(j), P, N), "backtransform kernel");
   }
   // true residual ||b - G x|| / ||b|| (one apply pass; x boundary rows exchanged in slab mode)
   if (c->slab) {
@@ -676,13 +683,13 @@ kcg_status solve_impl(kcg_ctx* c, Route route, const double* Y_in, double* mu_ou
       const RankState& R = c->R[j];
       double* up = R.rank > 0 ? peer_ptr<double>(c, R.rank - 1, c->L.xg_bot) : nullptr;
       double* dn = R.rank + 1 < c->nranks ? peer_ptr<double>(c, R.rank + 1, c->L.xg_top) : nullptr;
-      CK(kcg::launch_xghost(s, mur(j), up, dn, P * k, geom_of(c, R)), "x ghost kernel");
+      CKL(kcg::launch_xghost(s, mur(j), up, dn, P * k, geom_of(c, R)), "x ghost kernel");
     }
-    CK(kcg::launch_xrank_sync(s, xsync_of(c, tag0 + kPostTag + 1)), "rendezvous kernel");
+    CKL(kcg::launch_xrank_sync(s, xsync_of(c, tag0 + kPostTag + 1)), "rendezvous kernel");
   }
   for (int j = 0; j < c->nlocal; ++j) {
     RankState& R = c->R[j];
-    CK(kcg::launch_resid(k, s, R.params_kron, mur(j), Yr(j), bgiven ? nullptr : R.E_kron, R.hits, R.resid_partials,
+    CKL(kcg::launch_resid(k, s, R.params_kron, mur(j), Yr(j), bgiven ? nullptr : R.E_kron, R.hits, R.resid_partials,
                          R.resid_out, P, nin, gin(R), c->slab ? R.xg_top : nullptr, c->slab ? R.xg_bot : nullptr),
        "residual kernel");
     if (c->slab) {
@@ -692,13 +699,13 @@ kcg_status solve_impl(kcg_ctx* c, Route route, const double* Y_in, double* mu_ou
       Pt.count = P * 2;
       Pt.rank = R.rank;
       Pt.nranks = c->nranks;
-      CK(kcg::launch_put(s, Pt), "put kernel");
+      CKL(kcg::launch_put(s, Pt), "put kernel");
     }
   }
-  if (c->slab) CK(kcg::launch_xrank_sync(s, xsync_of(c, tag0 + kPostTag + 2)), "rendezvous kernel");
+  if (c->slab) CKL(kcg::launch_xrank_sync(s, xsync_of(c, tag0 + kPostTag + 2)), "rendezvous kernel");
   for (int j = 0; j < c->nlocal; ++j)
     if (c->R[j].x_rm && inmode != IN_B_WORK)
-      CK(kcg::launch_permute(s, c->R[j].x_rm, muu(j), (size_t)P * k, c->side, true), "permute mu");
+      CKL(kcg::launch_permute(s, c->R[j].x_rm, muu(j), (size_t)P * k, c->side, true), "permute mu");
   c->st_host.resize(n_sys);
   const int nr = c->slab ? c->nranks : 1;
   c->resid_host.resize((size_t)nr * P * 2);
@@ -767,6 +774,7 @@ kcg_status solve_impl(kcg_ctx* c, Route route, const double* Y_in, double* mu_ou
         rep->loop_bytes += (double)passes * res.nstrip * (std::min(4, rs) + 4) * c->side * Kk * 16.0;
     }
     rep->peak_mem_bytes = c->ws_need;
+    rep->kernel_launches = c->nlaunch;
     rep->history_len = std::min(maxit, c->d.history_cap);
     if (rep->history && rep->history_len > 0) {
       cudaError_t e = cudaMemcpy(rep->history, c->R[0].history, (size_t)rep->history_len * 8, cudaMemcpyDeviceToHost);
@@ -805,7 +813,7 @@ kcg_status lanczos_impl(kcg_ctx* c, const double* Y_in, double* mu_out, bool hos
   CK(cudaEventRecord(c->ev[0], s), "event");
   if (host_io) CK(cudaMemcpyAsync(R.Y_stage, Y_in, (size_t)P * n * N * 8, cudaMemcpyHostToDevice, s), "H2D Y");
   SlabGeom g{c->side, c->side, 0, c->pitch, 0, 0, c->d.layout == KCG_LAYOUT_NESTED, c->d.prior == KCG_PRIOR_D2};
-  CK(kcg::launch_rhs(k, s, Yr, R.E_lz, nullptr, R.lz_V, nullptr, nullptr, P, n, g), "lanczos rhs kernel");
+  CKL(kcg::launch_rhs(k, s, Yr, R.E_lz, nullptr, R.lz_V, nullptr, nullptr, P, n, g), "lanczos rhs kernel");
   CK(cudaMemsetAsync(R.lz_st, 0, P * sizeof(kcg::LzState), s), "memset lanczos state");
   CK(cudaEventRecord(c->ev[1], s), "event");
   kcg::LzArgs a{};
@@ -832,14 +840,14 @@ kcg_status lanczos_impl(kcg_ctx* c, const double* Y_in, double* mu_out, bool hos
   a.store = c->d.lanczos_store;
   a.tol = tol;
   a.trace = R.trace;
-  CK(kcg::launch_lanczos(k, R.hits != nullptr, c->d.prior == KCG_PRIOR_D2, s, a, R.lz_map, c->grid_lz, c->smem_lz),
+  CKL(kcg::launch_lanczos(k, R.hits != nullptr, c->d.prior == KCG_PRIOR_D2, s, a, R.lz_map, c->grid_lz, c->smem_lz),
      "lanczos kernel");
-  if (a.store) CK(kcg::launch_lz_assemble(k, s, a), "lanczos assembly kernel");
+  if (a.store) CKL(kcg::launch_lz_assemble(k, s, a), "lanczos assembly kernel");
   CK(cudaEventRecord(c->ev[2], s), "event");
-  CK(kcg::launch_resid(k, s, R.params_kron, mur, Yr, R.E_kron, R.hits, R.resid_partials, R.resid_out, P, n,
+  CKL(kcg::launch_resid(k, s, R.params_kron, mur, Yr, R.E_kron, R.hits, R.resid_partials, R.resid_out, P, n,
                        geom_of(c, R), nullptr, nullptr),
      "residual kernel");
-  if (R.x_rm) CK(kcg::launch_permute(s, R.x_rm, muu, (size_t)P * k, c->side, true), "permute mu");
+  if (R.x_rm) CKL(kcg::launch_permute(s, R.x_rm, muu, (size_t)P * k, c->side, true), "permute mu");
   c->lz_host.resize(P);
   c->resid_host.resize((size_t)P * 2);
   CK(cudaMemcpyAsync(c->lz_host.data(), R.lz_st, P * sizeof(kcg::LzState), cudaMemcpyDeviceToHost, s), "D2H");
@@ -899,6 +907,7 @@ kcg_status lanczos_impl(kcg_ctx* c, const double* Y_in, double* mu_out, bool hos
     rep->system_iterations = sumit;
     rep->loop_bytes = bytes;
     rep->peak_mem_bytes = c->ws_need;
+    rep->kernel_launches = c->nlaunch;
     rep->history_len = 0;
   }
   c->err.clear();
@@ -928,7 +937,7 @@ kcg_status kohler_impl(kcg_ctx* c, const double* Y_in, double* mu_out, double to
   CgSlabLaunch* Lp = new CgSlabLaunch();
   std::unique_ptr<CgSlabLaunch> L_owner(Lp);
   for (int i = 0; i < k; ++i) {
-    CK(kcg::launch_kohler_rhs(k, s, Y_in, R.E_koh, R.R_koh, mur, R.hits, R.r[0], R.p[0], xcol, P, n, i, c->side,
+    CKL(kcg::launch_kohler_rhs(k, s, Y_in, R.E_koh, R.R_koh, mur, R.hits, R.r[0], R.p[0], xcol, P, n, i, c->side,
                               c->pitch, nested),
        "kohler rhs kernel");
     CgArgs& a = Lp->a[0];
@@ -966,24 +975,24 @@ kcg_status kohler_impl(kcg_ctx* c, const double* Y_in, double* mu_out, double to
     const int grid = std::max(1, std::min(c->grid_syl, P * a.tiles_per_sys));
     if (c->res_koh.on) {
       a.tiles_per_sys = c->res_koh.nstrip;
-      CK(kcg::launch_cg_resident(1, prec, s, a, R.res_part, c->res_koh.grid, c->res_koh.smem),
+      CKL(kcg::launch_cg_resident(1, prec, s, a, R.res_part, c->res_koh.grid, c->res_koh.smem),
          "cg kernel (kohler column, resident)");
     } else if (c->d.cg_variant == KCG_CG_HS) {
-      CK(kcg::launch_cg_hs(1, prec, d2, s, a, R.r[1], R.hs_part, grid, c->smem_syl), "cg kernel (kohler column, HS)");
-      CK(kcg::launch_hs_xfix(1, s, R.state, R.p[0], R.p[1], xcol, P, c->side, c->pitch), "x fix-up kernel");
+      CKL(kcg::launch_cg_hs(1, prec, d2, s, a, R.r[1], R.hs_part, grid, c->smem_syl), "cg kernel (kohler column, HS)");
+      CKL(kcg::launch_hs_xfix(1, s, R.state, R.p[0], R.p[1], xcol, P, c->side, c->pitch), "x fix-up kernel");
     } else {
-      CK(kcg::launch_cg(1, prec, d2, s, a, maps, grid, c->smem_syl), "cg kernel (kohler column)");
-      if (KCG_X2) CK(kcg::launch_xfix(1, s, R.state, R.p[0], R.p[1], xcol, P, geom_of(c, R)), "x fix-up kernel");
+      CKL(kcg::launch_cg(1, prec, d2, s, a, maps, grid, c->smem_syl), "cg kernel (kohler column)");
+      if (KCG_X2) CKL(kcg::launch_xfix(1, s, R.state, R.p[0], R.p[1], xcol, P, geom_of(c, R)), "x fix-up kernel");
     }
-    if (k > 1) CK(kcg::launch_column_copy(s, xcol, mur, P, k, i, N), "column copy kernel");
+    if (k > 1) CKL(kcg::launch_column_copy(s, xcol, mur, P, k, i, N), "column copy kernel");
     CK(cudaMemcpyAsync(st.data() + (size_t)i * P, R.state, P * sizeof(SysState), cudaMemcpyDeviceToHost, s), "D2H");
   }
-  CK(kcg::launch_backtransform(k, s, R.W_koh, mur, P, N), "backtransform kernel");
+  CKL(kcg::launch_backtransform(k, s, R.W_koh, mur, P, N), "backtransform kernel");
   CK(cudaEventRecord(c->ev[2], s), "event");
-  CK(kcg::launch_resid(k, s, R.params_kron, mur, Y_in, R.E_kron, R.hits, R.resid_partials, R.resid_out, P, n,
+  CKL(kcg::launch_resid(k, s, R.params_kron, mur, Y_in, R.E_kron, R.hits, R.resid_partials, R.resid_out, P, n,
                        geom_of(c, R), nullptr, nullptr),
      "residual kernel");
-  if (R.x_rm) CK(kcg::launch_permute(s, R.x_rm, mu_out, (size_t)P * k, c->side, true), "permute mu");
+  if (R.x_rm) CKL(kcg::launch_permute(s, R.x_rm, mu_out, (size_t)P * k, c->side, true), "permute mu");
   c->resid_host.resize((size_t)P * 2);
   CK(cudaMemcpyAsync(c->resid_host.data(), R.resid_out, (size_t)P * 2 * 8, cudaMemcpyDeviceToHost, s), "D2H");
   CK(cudaEventRecord(c->ev[3], s), "event");
@@ -1028,6 +1037,7 @@ kcg_status kohler_impl(kcg_ctx* c, const double* Y_in, double* mu_out, double to
     rep->system_iterations = sumit;
     rep->loop_bytes = (32.0 * (double)passes + 16.0 * (double)xpasses) * (double)N;
     rep->peak_mem_bytes = c->ws_need;
+    rep->kernel_launches = c->nlaunch;
     rep->history_len = 0;
   }
   c->err.clear();
@@ -1395,23 +1405,28 @@ kcg_status kron_cg_create_slab(const kcg_desc* d, const kcg_slab* slab, const do
 }
 
 kcg_status kron_cg_solve(kcg_ctx* c, const double* Y, double* mu, double tol, int max_iter, kcg_report* rep) {
+  if (c) c->nlaunch = 0;
   return solve_impl(c, ROUTE_KRON, Y, mu, false, tol, max_iter, rep);
 }
 kcg_status sylvester_solve(kcg_ctx* c, const double* Y, double* mu, double tol, int max_iter, kcg_report* rep) {
+  if (c) c->nlaunch = 0;
   return solve_impl(c, ROUTE_SYL, Y, mu, false, tol, max_iter, rep);
 }
 kcg_status sylvester_kohler_solve(kcg_ctx* c, const double* Y, double* mu, double tol, int max_iter,
                                   kcg_report* rep) {
+  if (c) c->nlaunch = 0;
   return kohler_impl(c, Y, mu, tol, max_iter, rep);
 }
 
 kcg_status kron_cg_solve_b(kcg_ctx* c, const double* b, double* x, double tol, int max_iter, kcg_report* rep) {
+  if (c) c->nlaunch = 0;
   return solve_impl(c, ROUTE_KRON, b, x, false, tol, max_iter, rep, IN_B_USER);
 }
 
 kcg_status posterior_variance(kcg_ctx* c, int n_probes, unsigned long long seed, double* var, double* scratch,
                               double tol, int max_iter, kcg_report* rep) {
   if (!c) return KCG_E_ARG;
+  c->nlaunch = 0;
   if (!var || !scratch) { c->err = "null var or scratch"; return KCG_E_ARG; }
   if (n_probes < 1) { c->err = "n_probes < 1"; return KCG_E_ARG; }
   if (c->slab) { c->err = "posterior_variance: no row slabs"; return KCG_E_CONFIG; }
@@ -1427,19 +1442,19 @@ kcg_status posterior_variance(kcg_ctx* c, int n_probes, unsigned long long seed,
   long long sumit = 0;
   std::vector<int> its_probe(c->P), its_max(c->P, 0);  // per-patch iterations: max over the probes
   for (int i = 0; i < n_probes; ++i) {
-    CK(kcg::launch_probe(s, z, c->P, c->k, c->side, c->d.layout == KCG_LAYOUT_NESTED, seed, i), "probe kernel");
+    CKL(kcg::launch_probe(s, z, c->P, c->k, c->side, c->d.layout == KCG_LAYOUT_NESTED, seed, i), "probe kernel");
     sub = kcg_report{};
     sub.iterations_per = its_probe.data();
     const kcg_status st = solve_impl(c, ROUTE_KRON, z, x, false, tol, max_iter, &sub, IN_B_WORK);
     if (st != KCG_OK && st != KCG_NOT_CONVERGED) return st;
     if (st == KCG_NOT_CONVERGED) worst = KCG_NOT_CONVERGED;
-    CK(kcg::launch_var_accum(s, z, x, acc, tot, i == 0, i == n_probes - 1 ? 1.0 / n_probes : 1.0), "accumulate kernel");
+    CKL(kcg::launch_var_accum(s, z, x, acc, tot, i == 0, i == n_probes - 1 ? 1.0 / n_probes : 1.0), "accumulate kernel");
     wall += sub.wall_time_s; loop += sub.loop_time_s; bytes += sub.loop_bytes;
     maxit = std::max(maxit, sub.iterations); sumit += sub.system_iterations;
     maxrel = std::max(maxrel, sub.rel_residual); maxtrue = std::max(maxtrue, sub.rel_residual_true);
     for (int p = 0; p < c->P; ++p) its_max[p] = std::max(its_max[p], its_probe[p]);
   }
-  if (R.y_rm) CK(kcg::launch_permute(s, R.y_rm, var, planes, c->side, true), "permute var");
+  if (R.y_rm) CKL(kcg::launch_permute(s, R.y_rm, var, planes, c->side, true), "permute var");
   CK(cudaStreamSynchronize(s), "posterior variance");
   if (rep) {
     all = sub;
@@ -1448,6 +1463,7 @@ kcg_status posterior_variance(kcg_ctx* c, int n_probes, unsigned long long seed,
     all.wall_time_s = wall; all.loop_time_s = loop; all.loop_bytes = bytes;
     all.iterations_per = rep->iterations_per; all.history = rep->history; all.history_len = 0;
     all.n_systems = c->P;
+    all.kernel_launches = c->nlaunch;
     if (all.iterations_per)
       for (int p = 0; p < c->P; ++p) all.iterations_per[p] = its_max[p];
     *rep = all;
@@ -1458,17 +1474,21 @@ kcg_status posterior_variance(kcg_ctx* c, int n_probes, unsigned long long seed,
 
 kcg_status sylvester_lanczos_solve(kcg_ctx* c, const double* Y, double* mu, double tol, int max_iter,
                                    kcg_report* rep) {
+  if (c) c->nlaunch = 0;
   return lanczos_impl(c, Y, mu, false, tol, max_iter, rep);
 }
 kcg_status sylvester_lanczos_solve_host(kcg_ctx* c, const double* Y, double* mu, double tol, int max_iter,
                                         kcg_report* rep) {
+  if (c) c->nlaunch = 0;
   return lanczos_impl(c, Y, mu, true, tol, max_iter, rep);
 }
 kcg_status kron_cg_solve_host(kcg_ctx* c, const double* Y, double* mu, double tol, int max_iter, kcg_report* rep) {
+  if (c) c->nlaunch = 0;
   return solve_impl(c, ROUTE_KRON, Y, mu, true, tol, max_iter, rep);
 }
 kcg_status sylvester_solve_host(kcg_ctx* c, const double* Y, double* mu, double tol, int max_iter,
                                 kcg_report* rep) {
+  if (c) c->nlaunch = 0;
   return solve_impl(c, ROUTE_SYL, Y, mu, true, tol, max_iter, rep);
 }
 
@@ -1487,18 +1507,18 @@ kcg_status kron_cg_apply(kcg_ctx* c, const double* x, double* y) {
     const double* xi = x + j * stride;
     double* yo = y + j * stride;
     if (R.x_rm) {  // NESTED: gather, apply in row-major, scatter
-      CK(kcg::launch_permute(c->stream, xi, R.x_rm, (size_t)c->P * c->k, c->side, false), "permute x");
+      CKL(kcg::launch_permute(c->stream, xi, R.x_rm, (size_t)c->P * c->k, c->side, false), "permute x");
       xi = R.x_rm;
       yo = R.y_rm;
     }
-    CK(kcg::launch_apply(c->k, c->stream, R.params_kron, xi, yo, R.hits, c->P, geom_of(c, R),
+    CKL(kcg::launch_apply(c->k, c->stream, R.params_kron, xi, yo, R.hits, c->P, geom_of(c, R),
                          c->slab ? R.xg_top : nullptr, c->slab ? R.xg_bot : nullptr),
        "apply kernel");
-    if (R.x_rm) CK(kcg::launch_permute(c->stream, R.y_rm, y + j * stride, (size_t)c->P * c->k, c->side, true), "permute y");
+    if (R.x_rm) CKL(kcg::launch_permute(c->stream, R.y_rm, y + j * stride, (size_t)c->P * c->k, c->side, true), "permute y");
   }
   if (c->slab) {  // nobody rewrites a neighbour's xg_* before everyone is done reading it
     const unsigned long long tag0 = c->solve_id << 32;
-    CK(kcg::launch_xrank_sync(c->stream, xsync_of(c, tag0 + kPostTag + 1)), "rendezvous kernel");
+    CKL(kcg::launch_xrank_sync(c->stream, xsync_of(c, tag0 + kPostTag + 1)), "rendezvous kernel");
   }
   CK(cudaStreamSynchronize(c->stream), "apply");
   return KCG_OK;
@@ -1512,10 +1532,10 @@ kcg_status kron_cg_rhs(kcg_ctx* c, const double* Y, double* b) {
     SlabGeom g{c->side, c->rows, R.row0, c->side, 0, c->ghost, c->d.layout == KCG_LAYOUT_NESTED,
                c->d.prior == KCG_PRIOR_D2};  // dense b
     double* bo = R.y_rm ? R.y_rm : b + j * (size_t)c->P * c->k * c->N;
-    CK(kcg::launch_rhs(c->k, c->stream, Y + j * (size_t)c->P * c->n * c->N, R.E_kron, R.hits, bo, nullptr, nullptr,
+    CKL(kcg::launch_rhs(c->k, c->stream, Y + j * (size_t)c->P * c->n * c->N, R.E_kron, R.hits, bo, nullptr, nullptr,
                        c->P, c->n, g),
        "rhs kernel");
-    if (R.y_rm) CK(kcg::launch_permute(c->stream, R.y_rm, b + j * (size_t)c->P * c->k * c->N, (size_t)c->P * c->k,
+    if (R.y_rm) CKL(kcg::launch_permute(c->stream, R.y_rm, b + j * (size_t)c->P * c->k * c->N, (size_t)c->P * c->k,
                                        c->side, true), "permute b");
   }
   CK(cudaStreamSynchronize(c->stream), "rhs");

@@ -48,7 +48,7 @@ class kcg_report(C.Structure):
                 ("wall_time_s", C.c_double), ("loop_time_s", C.c_double),
                 ("system_iterations", C.c_longlong), ("loop_bytes", C.c_double),
                 ("peak_mem_bytes", C.c_size_t), ("history", C.POINTER(C.c_double)),
-                ("history_len", C.c_int)]
+                ("history_len", C.c_int), ("kernel_launches", C.c_longlong)]
 
 
 _vp, _dp, _ip = C.c_void_p, C.POINTER(C.c_double), C.c_int
@@ -197,7 +197,8 @@ class KronCG:
                         wall_time_s=rep.wall_time_s, loop_time_s=rep.loop_time_s,
                         system_iterations=rep.system_iterations, loop_bytes=rep.loop_bytes,
                         peak_mem_bytes=rep.peak_mem_bytes,
-                        history=list(hist[:rep.history_len]) if hist is not None else [])
+                        history=list(hist[:rep.history_len]) if hist is not None else [],
+                        kernel_launches=rep.kernel_launches)
         return r
 
     def _solve(self, fn, Y, mu, tol, max_iter, n_sys, allow=(KCG_OK, KCG_NOT_CONVERGED)):

@@ -41,6 +41,24 @@ def test_d2_kron_vs_oracle(level, k, hits):
     assert rep["rel_residual_true"] <= 5 * TOL
 
 
+@pytest.mark.parametrize("level,k,hits", [(0, 1, None), (1, 2, None), (2, 3, "random"), (3, 4, None),
+                                          (5, 4, "random"), (6, 1, None), (7, 3, None)])
+def test_d2_variants_like_for_like(level, k, hits):
+    """Reading R9 like for like: the GPU's textbook HS variant against the oracle's HS-CG and the GPU's
+    single-pass kernel against the oracle's single-pass CG, each at +-2 iterations and 1e-8."""
+    ps = [_d2(level, k, 170 + s, hits=hits) for s in range(2)]
+    for variant, fn in (("hs", cg.cg_hs), ("single_pass", cg.cg_single_pass)):
+        ctx, Y = make_ctx(ps, cg_variant=variant)
+        mu, rep = ctx.solve(Y, tol=TOL, max_iter=200000)
+        mu = mu.cpu().numpy()
+        assert rep["converged"], rep
+        for i, p in enumerate(ps):
+            G, b = model.problem_system(p)
+            ref = fn(G, b, tol=TOL, max_iter=200000)
+            assert rel(mu[i], ref.x) <= 1e-8, (variant, i, rel(mu[i], ref.x))
+            assert abs(rep["iterations_per"][i] - ref.iterations) <= 2, (variant, rep["iterations_per"][i], ref.iterations)
+
+
 def test_d2_apply_matches_assembled():
     import torch
     ps = [_d2(6, 4, 180, hits="random"), _d2(6, 4, 181)]

@@ -3,9 +3,11 @@ printed noise precisions, phi = 1, Q0 = D^2 with kappa2 = 0,
 HEALPix NESTED pixel order -- all three routes through the C ABI against the oracle (assembled in
 NESTED numbering) and the direct sparse solve.
 
-cond(G) ~ 1e4-1e5 here (T ~ 1e6-3e7 against D^2), so CG iterates at tol 1e-10 sit up to cond * tol
-from the exact solution; CG parity is checked on the residual, the exact error bound and the
-oracle's iteration count, the Sylvester routes (well-conditioned shifted systems) to 1e-8."""
+cond(G) ~ 2e4 here (T ~ 1e6-3e7 against D^2), so CG iterates at tol 1e-10 sit up to cond * tol
+(~3e-7 measured) from the exact solution.  The GPU Kron-CG iterate is therefore compared element by
+element with the ORACLE's iterate (textbook HS-CG on the same assembled system) at the north-star bar
+1e-8, and its iteration count within +-2 (measured: 4e-14..2e-13 and equal counts at L = 5..7,
+profiles/r02/paper_kron_parity_probe.txt); the Sylvester routes to 1e-8 of the direct solve."""
 
 import numpy as np
 import pytest
@@ -48,8 +50,9 @@ def test_paper_workload_kron_and_sylvester(level):
         o = cg.cg_hs(G, b, tol=TOL)
         x = mu[i].reshape(-1)
         assert np.linalg.norm(G @ x - b) <= 5e-10 * np.linalg.norm(b)
-        assert rel(x, ref) <= 1e-5
-        assert abs(rep["iterations_per"][i] - o.iterations) <= max(2, o.iterations // 20)
+        assert rel(x, o.x) <= 1e-8, rel(x, o.x)  # the oracle's own iterate (measured 4e-14..2e-13)
+        assert abs(rep["iterations_per"][i] - o.iterations) <= 2, (rep["iterations_per"][i], o.iterations)
+        assert rel(x, ref) <= 1e-5  # inside the cond * tol bound of the exact solution (~3e-7 measured)
         assert rel(smu[i].reshape(-1), ref) <= 1e-8
 
 
