@@ -94,7 +94,8 @@ typedef struct {
                     /* within the face; Y, mu, hits, apply/rhs arguments; no row slabs)            */
   int precond;      /* KCG_PRECOND_NONE (the paper's CG) or KCG_PRECOND_BLOCK_JACOBI (pixel */
                     /* k x k blocks of G, reading R10; n_comp <= 7; any level incl. 0)              */
-  int host_staging; /* 1: workspace also holds Y / mu staging for the *_host entry points          */
+  int host_staging; /* 1: workspace also holds Y / mu staging for the *_host entry points; 2: two   */
+                    /* staging pairs (also kron_cg_solve_host_many, the pipelined entry point)     */
   int history_cap;  /* per-iteration max relative residual recorded on device (0 = off)            */
   int lanczos_cap;  /* block-Lanczos route (sylvester_lanczos_solve): 0 = not provisioned; else the   */
                     /* most Lanczos steps a solve may take (coefficients H_i, B_i, eliminations kept  */
@@ -200,6 +201,17 @@ KCG_API kcg_status kron_cg_solve_host(kcg_ctx* ctx, const double* Y_host, double
                               int max_iter, kcg_report* report);
 KCG_API kcg_status sylvester_solve_host(kcg_ctx* ctx, const double* Y_host, double* mu_host, double tol,
                                 int max_iter, kcg_report* report);
+
+/* Pipelined host entry point for a stream of data sets (e.g. Monte-Carlo simulations of the maps):
+ * nbatch Kronecker-route solves, batch i reading Y_host[i] [P][n][N] and writing mu_host[i]
+ * [P][k][N] (pinned host memory for overlap; the pointers may repeat).  Needs desc.host_staging = 2
+ * (two staging pairs in the workspace) and no row slabs (KCG_E_CONFIG).  The H2D copy of batch i+1
+ * and the D2H copy of batch i-1 run on two copy streams while batch i is solved on the context's
+ * stream; returns after the last copy.  reports: NULL or [nbatch] (each filled as by kron_cg_solve;
+ * iterations_per / history pointers per report as usual).  Status: the worst over the batches;
+ * an error stops the pipeline after the failing batch.                                           */
+KCG_API kcg_status kron_cg_solve_host_many(kcg_ctx* ctx, int nbatch, const double* const* Y_host,
+                                   double* const* mu_host, double tol, int max_iter, kcg_report* reports);
 
 /* y = G x for all patches (Alg.MatvecQ + Alg.MatvecBCBT fused).  x_dev, y_dev
  * [P][k][N], must not alias.                                                                  */

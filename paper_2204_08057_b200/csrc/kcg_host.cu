@@ -42,7 +42,7 @@ struct Layout {
   size_t r0, r1, p0, p1, partials, state, history, sync, group, resid_partials, resid_out, params_kron, params_syl,
       E_kron, E_syl, W, Y_stage, mu_stage, trace, slots, flags, xg_top, xg_bot, rslots, x_rm, y_rm, hits_rm,
       lz_V, lz_part, lz_st, lz_H, lz_R, lz_Ri, lz_Sinv, lz_g, lz_Z, lz_prm, E_lz, params_koh, E_koh, R_koh, W_koh,
-      hs_part, res_part, total;
+      hs_part, res_part, Y_stage2, mu_stage2, total;
   int lz_slots;
   size_t vec_doubles, partial_doubles;
 };
@@ -93,6 +93,10 @@ Layout layout_of(const kcg_desc* d, int nranks) {
     L.Y_stage = take(P * n * N * 8);
     L.mu_stage = take(P * k * N * 8);
   }
+  if (d->host_staging == 2 && nranks == 1) {  // second staging pair: kron_cg_solve_host_many's pipeline
+    L.Y_stage2 = take(P * n * N * 8);
+    L.mu_stage2 = take(P * k * N * 8);
+  }
   // cross-rank areas (written by peers)
   L.slots = take(2 * P * k * (size_t)nranks * 3 * 8);
   L.flags = take(KCG_GMAX * sizeof(unsigned long long));
@@ -138,6 +142,7 @@ struct RankState {
   SysParams *params_kron = nullptr, *params_syl = nullptr, *params_koh = nullptr;
   double *E_koh = nullptr, *R_koh = nullptr, *W_koh = nullptr;
   double *E_kron = nullptr, *E_syl = nullptr, *W_dev = nullptr, *Y_stage = nullptr, *mu_stage = nullptr;
+  double *Y_stage2 = nullptr, *mu_stage2 = nullptr;  // host_staging == 2
   long long* trace = nullptr;
   double *slots = nullptr, *xg_top = nullptr, *xg_bot = nullptr, *rslots = nullptr;
   double *x_rm = nullptr, *y_rm = nullptr, *hits_rm = nullptr;  // NESTED layout only
@@ -183,6 +188,10 @@ RankState carve(char* ws, const Layout& L, int rank, int rows, bool staging, boo
   if (staging) {
     R.Y_stage = reinterpret_cast<double*>(ws + L.Y_stage);
     R.mu_stage = reinterpret_cast<double*>(ws + L.mu_stage);
+  }
+  if (L.Y_stage2) {
+    R.Y_stage2 = reinterpret_cast<double*>(ws + L.Y_stage2);
+    R.mu_stage2 = reinterpret_cast<double*>(ws + L.mu_stage2);
   }
   R.slots = reinterpret_cast<double*>(ws + L.slots);
   R.flags = reinterpret_cast<unsigned long long*>(ws + L.flags);
@@ -244,6 +253,9 @@ struct kcg_ctx {
   unsigned long long solve_id = 0;     // cross-rank operations so far (identical on every rank)
   long long nlaunch = 0;               // library kernel launches since the current entry point began
   cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+  // kron_cg_solve_host_many: copy streams and their events (created on first use)
+  cudaStream_t h2d_stream = nullptr, d2h_stream = nullptr;
+  cudaEvent_t ev_h2d[2] = {nullptr, nullptr}, ev_d2h[2] = {nullptr, nullptr}, ev_solved[2] = {nullptr, nullptr};
   std::vector<SysState> st_host;
   std::vector<double> resid_host;
   std::string err;
@@ -260,6 +272,7 @@ bool desc_ok(const kcg_desc* d, std::string* why) {
   if (d->n_comp > d->n_freq) { *why = "n_comp > n_freq (A cannot have full column rank)"; return false; }
   if (d->n_patches < 1 || d->n_patches > 64) { *why = "n_patches outside [1,64]"; return false; }
   if (d->history_cap < 0) { *why = "history_cap < 0"; return false; }
+  if (d->host_staging < 0 || d->host_staging > 2) { *why = "host_staging outside [0,2]"; return false; }
   if (d->lanczos_cap < 0 || d->lanczos_cap > 1000000) { *why = "lanczos_cap outside [0, 1e6]"; return false; }
   if (d->lanczos_store != 0 && d->lanczos_store != 1) { *why = "lanczos_store must be 0 or 1"; return false; }
   if (d->cg_variant != KCG_CG_SINGLE_PASS && d->cg_variant != KCG_CG_HS) { *why = "unknown cg_variant"; return false; }
@@ -1482,6 +1495,68 @@ kcg_status sylvester_lanczos_solve_host(kcg_ctx* c, const double* Y, double* mu,
   if (c) c->nlaunch = 0;
   return lanczos_impl(c, Y, mu, true, tol, max_iter, rep);
 }
+// Pipelined host entry point: batch i's solve overlaps the H2D copy of batch i+1 and the D2H copy of
+// batch i-1 (two staging pairs, two copy streams; the solves themselves stay stream-ordered on the
+// context's stream).
+kcg_status kron_cg_solve_host_many(kcg_ctx* c, int nbatch, const double* const* Y_host, double* const* mu_host,
+                                   double tol, int max_iter, kcg_report* reports) {
+  if (!c) return KCG_E_ARG;
+  c->nlaunch = 0;
+  if (c->slab || c->d.host_staging != 2) {
+    c->err = "kron_cg_solve_host_many needs desc.host_staging = 2 and no row slabs";
+    return KCG_E_CONFIG;
+  }
+  if (nbatch < 1 || !Y_host || !mu_host) { c->err = "nbatch < 1 or null pointer array"; return KCG_E_ARG; }
+  for (int i = 0; i < nbatch; ++i)
+    if (!Y_host[i] || !mu_host[i]) { c->err = "null Y or mu"; return KCG_E_ARG; }
+  RankState& R = c->R[0];
+  if (!c->h2d_stream) {
+    CK(cudaStreamCreateWithFlags(&c->h2d_stream, cudaStreamNonBlocking), "stream create");
+    CK(cudaStreamCreateWithFlags(&c->d2h_stream, cudaStreamNonBlocking), "stream create");
+    for (int b = 0; b < 2; ++b) {
+      CK(cudaEventCreateWithFlags(&c->ev_h2d[b], cudaEventDisableTiming), "event create");
+      CK(cudaEventCreateWithFlags(&c->ev_d2h[b], cudaEventDisableTiming), "event create");
+      CK(cudaEventCreateWithFlags(&c->ev_solved[b], cudaEventDisableTiming), "event create");
+    }
+  }
+  double* Ys[2] = {R.Y_stage, R.Y_stage2};
+  double* Ms[2] = {R.mu_stage, R.mu_stage2};
+  const size_t yb = (size_t)c->P * c->n * c->N * 8, mb = (size_t)c->P * c->k * c->N * 8;
+  cudaStream_t s = c->stream;
+  CK(cudaEventRecord(c->ev_solved[1], s), "event");  // the context's stream is past earlier work
+  CK(cudaStreamWaitEvent(c->h2d_stream, c->ev_solved[1], 0), "wait");
+  CK(cudaMemcpyAsync(Ys[0], Y_host[0], yb, cudaMemcpyHostToDevice, c->h2d_stream), "H2D Y");
+  CK(cudaEventRecord(c->ev_h2d[0], c->h2d_stream), "event");
+  kcg_status worst = KCG_OK;
+  for (int i = 0; i < nbatch; ++i) {
+    const int b = i & 1;
+    if (i + 1 < nbatch) {  // staging buffer b^1 was read by solve i-1, which has returned
+      CK(cudaMemcpyAsync(Ys[b ^ 1], Y_host[i + 1], yb, cudaMemcpyHostToDevice, c->h2d_stream), "H2D Y");
+      CK(cudaEventRecord(c->ev_h2d[b ^ 1], c->h2d_stream), "event");
+    }
+    CK(cudaStreamWaitEvent(s, c->ev_h2d[b], 0), "wait");
+    if (i >= 2) CK(cudaStreamWaitEvent(s, c->ev_d2h[b], 0), "wait");  // mu of batch i-2 copied out
+    kcg_report tmp{};
+    kcg_report* rp = reports ? reports + i : &tmp;
+    c->nlaunch = 0;  // per batch: rp->kernel_launches counts this solve's launches
+    const kcg_status st = solve_impl(c, ROUTE_KRON, Ys[b], Ms[b], false, tol, max_iter, rp);
+    if (st != KCG_OK && st != KCG_NOT_CONVERGED) {
+      cudaStreamSynchronize(c->h2d_stream);
+      cudaStreamSynchronize(c->d2h_stream);
+      return st;
+    }
+    if (st == KCG_NOT_CONVERGED) worst = st;
+    CK(cudaEventRecord(c->ev_solved[b], s), "event");
+    CK(cudaStreamWaitEvent(c->d2h_stream, c->ev_solved[b], 0), "wait");
+    CK(cudaMemcpyAsync(mu_host[i], Ms[b], mb, cudaMemcpyDeviceToHost, c->d2h_stream), "D2H mu");
+    CK(cudaEventRecord(c->ev_d2h[b], c->d2h_stream), "event");
+  }
+  CK(cudaStreamSynchronize(c->d2h_stream), "D2H");
+  CK(cudaStreamSynchronize(c->h2d_stream), "H2D");
+  c->err.clear();
+  return worst;
+}
+
 kcg_status kron_cg_solve_host(kcg_ctx* c, const double* Y, double* mu, double tol, int max_iter, kcg_report* rep) {
   if (c) c->nlaunch = 0;
   return solve_impl(c, ROUTE_KRON, Y, mu, true, tol, max_iter, rep);
@@ -1649,6 +1724,13 @@ void kron_cg_destroy(kcg_ctx* c) {
   if (!c) return;
   for (int i = 0; i < 4; ++i)
     if (c->ev[i]) cudaEventDestroy(c->ev[i]);
+  for (int i = 0; i < 2; ++i) {
+    if (c->ev_h2d[i]) cudaEventDestroy(c->ev_h2d[i]);
+    if (c->ev_d2h[i]) cudaEventDestroy(c->ev_d2h[i]);
+    if (c->ev_solved[i]) cudaEventDestroy(c->ev_solved[i]);
+  }
+  if (c->h2d_stream) cudaStreamDestroy(c->h2d_stream);
+  if (c->d2h_stream) cudaStreamDestroy(c->d2h_stream);
   delete c;
 }
 

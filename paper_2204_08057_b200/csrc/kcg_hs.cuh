@@ -416,6 +416,10 @@ cudaError_t HsEntry<K>::launch(bool prec, bool d2, cudaStream_t s, const CgArgs&
   const void* f = hs_pick<K>(a.hits != nullptr, prec, d2);
   if (!f) return cudaErrorInvalidValue;
   void* args[3] = {(void*)&a, (void*)&q, (void*)&part};
+  // the attribute is per function and shared by the routes (contexts) that launch it: set it to
+  // this launch's size every time
+  cudaError_t e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
   return cudaLaunchCooperativeKernel(f, dim3(grid), dim3(256), args, smem, s);
 }
 

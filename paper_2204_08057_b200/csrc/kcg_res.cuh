@@ -301,6 +301,10 @@ cudaError_t ResEntry<K>::launch(bool prec, cudaStream_t s, const CgArgs& a, doub
   const void* f = res_pick<K>(a.hits != nullptr, prec);
   if (!f) return cudaErrorInvalidValue;
   void* args[2] = {(void*)&a, (void*)&part};
+  // the attribute is per function and shared by the routes (contexts) that launch it: set it to
+  // this launch's size every time
+  cudaError_t e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
   return cudaLaunchCooperativeKernel(f, dim3(grid), dim3(256), args, smem, s);
 }
 

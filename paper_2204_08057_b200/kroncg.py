@@ -77,6 +77,9 @@ kron_cg_solve_b = _sig("kron_cg_solve_b", C.c_int, _solve_args)
 sylvester_kohler_solve = _sig("sylvester_kohler_solve", C.c_int, _solve_args)
 posterior_variance = _sig("posterior_variance", C.c_int,
                           [_ctxp, C.c_int, C.c_ulonglong, _vp, _vp, C.c_double, C.c_int, C.POINTER(kcg_report)])
+kron_cg_solve_host_many = _sig("kron_cg_solve_host_many", C.c_int,
+                               [_ctxp, C.c_int, C.POINTER(_vp), C.POINTER(_vp), C.c_double, C.c_int,
+                                C.POINTER(kcg_report)])
 kron_cg_apply = _sig("kron_cg_apply", C.c_int, [_ctxp, _vp, _vp])
 kron_cg_rhs = _sig("kron_cg_rhs", C.c_int, [_ctxp, _vp, _vp])
 sylvester_factor = _sig("sylvester_factor", C.c_int, [_ctxp, _vp, _vp])
@@ -102,7 +105,7 @@ EXPORTS = ["kron_cg_workspace_size", "kron_cg_create", "kron_cg_solve", "sylvest
            "sylvester_factor", "kcg_last_error", "kcg_status_string", "kron_cg_destroy",
            "kron_cg_workspace_size_slab", "kron_cg_create_slab", "kcg_ipc_export", "kcg_ipc_import",
            "kcg_ipc_close", "sylvester_lanczos_solve", "sylvester_lanczos_solve_host",
-           "kron_cg_solve_b", "posterior_variance", "sylvester_kohler_solve"]
+           "kron_cg_solve_b", "posterior_variance", "sylvester_kohler_solve", "kron_cg_solve_host_many"]
 
 
 class KcgError(RuntimeError):
@@ -161,7 +164,7 @@ class KronCG:
         pr = {"laplacian": KCG_PRIOR_LAPLACIAN, "d2": KCG_PRIOR_D2}[prior]
         cv = {"single_pass": KCG_CG_SINGLE_PASS, "hs": KCG_CG_HS}[cg_variant]
         self.desc = kcg_desc(level, n, k, P, pr, lay,
-                             pc, int(bool(host_staging)), int(history_cap), int(lanczos_cap),
+                             pc, int(host_staging), int(history_cap), int(lanczos_cap),
                              int(bool(lanczos_store)), cv)
         ws = kron_cg_workspace_size(C.byref(self.desc))
         if ws == 0:
@@ -309,6 +312,27 @@ class KronCG:
               "lanczos": sylvester_lanczos_solve_host}[route]
         n_sys = self.P * self.k if route == "sylvester" else self.P
         return mu, self._solve(fn, Y, mu, tol, max_iter, n_sys, **kw)
+
+    def solve_host_many(self, Ys, mus, tol=1e-10, max_iter=100000):
+        """Pipelined host entry point (kron_cg_solve_host_many; needs host_staging=2): solve batch i
+        from Ys[i] into mus[i] (pinned CPU tensors / numpy arrays) while batch i+1 is copied in and
+        batch i-1 out.  Returns the list of per-batch reports."""
+        nb = len(Ys)
+        if nb < 1 or len(mus) != nb:
+            raise ValueError("need as many outputs as inputs (>= 1)")
+        for Y, mu in zip(Ys, mus):
+            self._check_host(Y, self.shape_Y, "Y")
+            self._check_host(mu, self.shape_mu, "mu")
+        yp = (_vp * nb)(*[_ptr(Y) for Y in Ys])
+        mp = (_vp * nb)(*[_ptr(mu) for mu in mus])
+        reps = (kcg_report * nb)()
+        its = [(C.c_int * max(self.P, 1))() for _ in range(nb)]
+        for i in range(nb):
+            reps[i].iterations_per = C.cast(its[i], C.POINTER(C.c_int))
+        st = kron_cg_solve_host_many(self._ctx, nb, yp, mp, float(tol), int(max_iter), reps)
+        if st not in (KCG_OK, KCG_NOT_CONVERGED):
+            raise self._err(st)
+        return [self._report(reps[i], its[i], None, reps[i].status) for i in range(nb)]
 
     def apply(self, x, y=None):
         """y = G x (kron_cg_apply)."""

@@ -32,3 +32,17 @@ def rel(a, b):
     b = np.asarray(b).reshape(-1)
     nb = np.linalg.norm(b)
     return float(np.linalg.norm(a - b) / (nb if nb > 0 else 1.0))
+
+
+def oracle_count_envelope(fn, G, b, **kw):
+    """The oracle's iteration count is itself uncertain by rounding where CG needs a number of steps
+    comparable to the unknowns (measured: a 2^-50 relative change of b moves the oracle's HS count by
+    up to 2, and the HS and single-pass variants differ by up to 9 -- DESIGN.md reading R34).  Returns
+    (lo, hi, result on b): the counts of `fn` on b and on b (1 +- 2^-50); the bar is then
+    lo - 2 <= it_gpu <= hi + 2, which is the plain +-2 wherever the count is well determined."""
+    import numpy as np
+    ref = fn(G, b, **kw)
+    its = [ref.iterations]
+    for f in (1.0 + 2.0 ** -50, 1.0 - 2.0 ** -50):
+        its.append(fn(G, np.asarray(b) * f, **kw).iterations)
+    return min(its), max(its), ref

@@ -5,7 +5,7 @@ assembly (D @ D) and the DCT-exact solve (D^2 -> lambda^2)."""
 import numpy as np
 import pytest
 
-from gpu_util import have_gpu, make_ctx, rel
+from gpu_util import have_gpu, make_ctx, oracle_count_envelope, rel
 from oracle import cg, exact, model, sylvester
 from synth import make_config, make_patch
 
@@ -45,7 +45,9 @@ def test_d2_kron_vs_oracle(level, k, hits):
                                           (5, 4, "random"), (6, 1, None), (7, 3, None)])
 def test_d2_variants_like_for_like(level, k, hits):
     """Reading R9 like for like: the GPU's textbook HS variant against the oracle's HS-CG and the GPU's
-    single-pass kernel against the oracle's single-pass CG, each at +-2 iterations and 1e-8."""
+    single-pass kernel against the oracle's single-pass CG, each at 1e-8 and +-2 iterations around the
+    oracle's rounding envelope (reading R34: at levels <= 3 CG needs almost as many steps as there
+    are unknowns and the oracle's own count moves by up to 2 under a 2^-50 change of b)."""
     ps = [_d2(level, k, 170 + s, hits=hits) for s in range(2)]
     for variant, fn in (("hs", cg.cg_hs), ("single_pass", cg.cg_single_pass)):
         ctx, Y = make_ctx(ps, cg_variant=variant)
@@ -54,9 +56,9 @@ def test_d2_variants_like_for_like(level, k, hits):
         assert rep["converged"], rep
         for i, p in enumerate(ps):
             G, b = model.problem_system(p)
-            ref = fn(G, b, tol=TOL, max_iter=200000)
+            lo, hi, ref = oracle_count_envelope(fn, G, b, tol=TOL, max_iter=200000)
             assert rel(mu[i], ref.x) <= 1e-8, (variant, i, rel(mu[i], ref.x))
-            assert abs(rep["iterations_per"][i] - ref.iterations) <= 2, (variant, rep["iterations_per"][i], ref.iterations)
+            assert lo - 2 <= rep["iterations_per"][i] <= hi + 2, (variant, rep["iterations_per"][i], lo, hi)
 
 
 def test_d2_apply_matches_assembled():

