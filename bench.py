@@ -771,7 +771,7 @@ def main():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--config", default="fullsky", choices=["tiny", "medium", "planck", "fullsky", "stress"])
     ap.add_argument("--route", default="kron", choices=["kron", "sylvester"])
-    ap.add_argument("--e2e-steps", type=int, default=4)
+    ap.add_argument("--e2e-steps", type=int, default=10)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-slab-probe", action="store_true")
     ap.add_argument("--no-lanczos", action="store_true", help="skip the block-Lanczos (Alg. SylvSolver) leg")

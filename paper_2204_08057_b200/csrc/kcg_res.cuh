@@ -42,7 +42,6 @@ __global__ void __launch_bounds__(256, 1) cg_resident_kernel(const CgArgs a, dou
   SysState* st = reinterpret_cast<SysState*>(Hb + (HITS ? BOX : 0));  // [n_sys]
   __shared__ double Msh[K * K + K + 4 * K * K];
   __shared__ double red[3][NW];
-  __shared__ int s_done;
   cg::grid_group grid = cg::this_grid();
 
   // ---------------------------------------------------------------- set-up: b and the constants
@@ -201,6 +200,29 @@ __global__ void __launch_bounds__(256, 1) cg_resident_kernel(const CgArgs a, dou
       }
       __threadfence();
       grid.sync();
+      // The next pass's halo rows (box rows 0, 1, RS + 2, RS + 3 of r and p, written by the
+      // neighbouring strips this pass) are loaded into registers in batches of HC per thread, their
+      // L2 latency overlapped with the reduction below; element e = ((f K + c) 4 + row) side + x.
+      constexpr int HC = 24;
+      const bool halo = z.status == ST_RUNNING;
+      const int nh = halo ? 8 * K * side : 0;
+      const double* rg = (q & 1) ? a.rbuf[0] : a.rbuf[1];
+      const double* pg = (q & 1) ? a.pbuf[0] : a.pbuf[1];
+      auto decode = [&](int e, int& so, size_t& go) {  // false: outside the face (stays 0)
+        const int gx = e % side, t4 = e / side, hr = t4 & 3, fc = t4 >> 2, c = fc % K, f = fc / K;
+        const int by = hr < 2 ? hr : RS + hr, gy = y0 - 2 + by;
+        so = (f * K + c) * BOX + by * BW + gx + 1;  // Pb = Rb + K * BOX
+        go = (size_t)(s * K + c) * ps + (size_t)gy * pitch + gx;
+        return gy >= 0 && gy < side;
+      };
+      double hv[HC];
+#pragma unroll
+      for (int j = 0; j < HC; ++j) {
+        const int e = j * NT + tid;
+        int so;
+        size_t go;
+        hv[j] = (e < nh && decode(e, so, go)) ? __ldcg(((e / (4 * side * K)) ? pg : rg) + go) : 0.0;
+      }
       // every CTA: every system's sums over its strips in strip order, then the CG scalar update
       const double* pq = part + (size_t)(q & 1) * ncta * 3;
       for (int t = warp; t < a.n_sys; t += NW) {
@@ -217,38 +239,48 @@ __global__ void __launch_bounds__(256, 1) cg_resident_kernel(const CgArgs a, dou
         w2 = warp_sum(w2);
         if (lane == 0) st[t] = cg_update(st[t], w0, w1, w2, it, a);
       }
-    } else if (tid == 0 && z.status == ST_RUNNING) {
-      double w0 = 0.0, w1 = 0.0, w2 = 0.0;
-      for (int w = 0; w < NW; ++w) { w0 += red[0][w]; w1 += red[1][w]; w2 += red[2][w]; }
-      st[s] = cg_update(st[s], w0, w1, w2, it, a);
-    }
-    __syncthreads();
-    if (tid == 0) {
-      int done = 1;
-      if (gmode) {
-        double m = 0.0;
-        for (int t = 0; t < a.n_sys; ++t) {
-          done &= st[t].status != ST_RUNNING;
-          m = fmax(m, st[t].rel);
+#pragma unroll
+      for (int j = 0; j < HC; ++j) {
+        const int e = j * NT + tid;
+        int so;
+        size_t go;
+        if (e < nh && decode(e, so, go)) rs_smem[so] = hv[j];
+      }
+      for (int e0 = HC * NT; e0 < nh; e0 += HC * NT) {  // wide faces: further batches
+#pragma unroll
+        for (int j = 0; j < HC; ++j) {
+          const int e = e0 + j * NT + tid;
+          int so;
+          size_t go;
+          hv[j] = (e < nh && decode(e, so, go)) ? __ldcg(((e / (4 * side * K)) ? pg : rg) + go) : 0.0;
         }
-        if (cta == 0 && it >= 0 && it < a.history_cap) a.history[it] = m;
-      } else {
-        done = st[s].status != ST_RUNNING;
-        if (it >= 0 && it < a.history_cap && z.status == ST_RUNNING)  // max over systems: positive doubles
+#pragma unroll
+        for (int j = 0; j < HC; ++j) {
+          const int e = e0 + j * NT + tid;
+          int so;
+          size_t go;
+          if (e < nh && decode(e, so, go)) rs_smem[so] = hv[j];
+        }
+      }
+      __syncthreads();
+      bool done = true;  // every thread reads the same states: uniform
+      double m = 0.0;
+      for (int t = 0; t < a.n_sys; ++t) {
+        done &= st[t].status != ST_RUNNING;
+        m = fmax(m, st[t].rel);
+      }
+      if (cta == 0 && tid == 0 && it >= 0 && it < a.history_cap) a.history[it] = m;
+      if (done) break;
+    } else {
+      if (tid == 0 && z.status == ST_RUNNING) {
+        double w0 = 0.0, w1 = 0.0, w2 = 0.0;
+        for (int w = 0; w < NW; ++w) { w0 += red[0][w]; w1 += red[1][w]; w2 += red[2][w]; }
+        st[s] = cg_update(st[s], w0, w1, w2, it, a);
+        if (it >= 0 && it < a.history_cap)  // max over the systems: positive doubles order as integers
           atomicMax(reinterpret_cast<unsigned long long*>(a.history + it), __double_as_longlong(st[s].rel));
       }
-      s_done = done;
-    }
-    __syncthreads();
-    if (s_done) break;
-    if (gmode && st[s].status == ST_RUNNING) {  // halo rows of the next pass from the neighbours
-      const double* rg = (q & 1) ? a.rbuf[0] : a.rbuf[1];
-      const double* pg = (q & 1) ? a.pbuf[0] : a.pbuf[1];
-      load_rows(Rb, rg, 0, 2);
-      load_rows(Rb, rg, RS + 2, BH);
-      load_rows(Pb, pg, 0, 2);
-      load_rows(Pb, pg, RS + 2, BH);
       __syncthreads();
+      if (st[s].status != ST_RUNNING) break;
     }
   }
   // x of the strip; the final states
