@@ -511,9 +511,14 @@ def _small_leg(dev, timed, args, clocks_dev):
         st = stack(ps)
         Y = torch.from_numpy(st["Y"]).to(dev)
         leg = {}
-        for mode in ("resident", "streaming"):
-            if mode == "streaming":
-                os.environ["KCG_RESIDENT"] = "0"
+        # default = the planner's choice (single-CTA resident kernel for tiny faces, the streaming
+        # kernel otherwise); "streaming" forces the latter, "strips" the opt-in row-strip resident mode
+        modes = {"default": None, "streaming": "0"}
+        if cfg == "medium":
+            modes["strips"] = "2"
+        for mode, env in modes.items():
+            if env is not None:
+                os.environ["KCG_RESIDENT"] = env
             try:
                 ctx = KronCG(ps[0].level, st["A"], st["noise_prec"], st["tau"], st["kappa2"], device=dev)
             finally:
@@ -527,16 +532,17 @@ def _small_leg(dev, timed, args, clocks_dev):
             clocks = clk.stop()
             it = reps[-1]["iterations"]
             lt = sum(r["loop_time_s"] for r in reps) / len(reps)
+            res = ctx.launch_config()["resident_kron"] > 0
             leg[mode] = {"value": len(reps) / t, "unit": "solves/s", "ms_per_step": t / len(reps) * 1e3,
                          "iterations": it, "us_per_iteration": lt / (it + 1) * 1e6,
                          "strips_per_face": ctx.launch_config()["resident_kron"],
                          "roofline": roof3(reps, ps[0].k, ps[0].N,
-                                           "cg_resident_kernel" if mode == "resident" else "cg_persistent_kernel",
-                                           bound="latency" if mode == "resident" else "hbm",
+                                           "cg_resident_kernel" if res else "cg_persistent_kernel",
+                                           bound="latency" if res else "hbm",
                                            note=("frac = iteration rate against the streaming algorithm's HBM "
                                                  "roofline (48 K N B per pass); the resident kernel keeps x, r, p "
                                                  "in shared memory, bytes_moved = its global (L2) traffic")
-                                           if mode == "resident" else None),
+                                           if res else None),
                          "clocks": clocks}
             del ctx
         leg["config"] = {"workload": cfg, "level": ps[0].level, "k": ps[0].k, "patches": len(ps)}

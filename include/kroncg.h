@@ -69,7 +69,7 @@ typedef enum {
   KCG_E_NONFINITE = 5,
   KCG_E_BREAKDOWN = 6,
   KCG_E_CUDA = 7,
-  KCG_E_NCCL = 8,
+  /* 8 is unassigned: the row-slab exchange uses peer memory, not NCCL (reading R35) */
   KCG_E_STATE = 9
 } kcg_status;
 

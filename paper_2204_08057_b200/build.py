@@ -12,7 +12,7 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "lib", "libkroncg.so")
 SOURCES = ["kcg_kernels.cu", "kcg_host.cu", "kcg_lanczos_a.cu", "kcg_lanczos_b.cu", "kcg_hs_a.cu", "kcg_hs_b.cu", "kcg_res_a.cu", "kcg_res_b.cu"] + [f"kcg_cg_k{K}.cu" for K in range(1, 9)]
-HEADERS = ["kcg_internal.h", "kcg_cg.cuh", "kcg_lanczos.cuh", "kcg_hs.cuh", "kcg_res.cuh", os.path.join("..", "..", "include", "kroncg.h")]
+HEADERS = ["kcg_internal.h", "kcg_cg.cuh", "kcg_march.cuh", "kcg_lanczos.cuh", "kcg_hs.cuh", "kcg_res.cuh", os.path.join("..", "..", "include", "kroncg.h")]
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",

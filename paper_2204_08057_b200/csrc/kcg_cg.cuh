@@ -21,6 +21,7 @@
 #include <cooperative_groups.h>
 
 #include <algorithm>
+#include <type_traits>
 
 namespace cg = cooperative_groups;
 
@@ -925,235 +926,6 @@ __device__ __forceinline__ void flush_tile_partial(const double (*tred)[NW], dou
   }
 }
 
-// ------------------------------------------------------------------------------ D2 prior tile
-// The paper's prior Q0 = D^2 + kappa2 I (reading R3 "d2"): (D v)_j = sum_{nbr} v - deg_j v_j
-// with D v := 0 outside the face, so (D^2 v)_j = sum_{nbr in face} (D v)_nbr - deg_j (D v)_j.
-// Single-pass recomputation with a radius-2 operator: r_new is needed on tile + 2-ring, so p_new on
-// tile + 4-ring (H = 4).  Generic point loops over the box (uniform trip counts), box pitch BW = 72:
-//   A   p_new = u + beta p (u = K^{-1} r) on the box; tile p_old saved (X2)
-//   B0  S = D p_new on tile + 3-ring
-//   B1  q = h M p_new + tau (kappa2 p_new + D S), r_new = r - alpha q on tile + 2-ring
-//   B'  U = K^{-1} r_new on tile + 2-ring (PREC)
-//   C0  S = D v on tile + 1-ring (v = U or r_new)
-//   C1  w = h M v + tau (kappa2 v + D S) on the tile; (r,r), (r,u), (w,u); x += xinc; stores
-// Block-Jacobi diag: diag(D^2)_jj = deg_j^2 + deg_j.
-template <int K, bool HITS, bool PREC, bool EDGE>
-__device__ __forceinline__ void cg_tile_d2(const CgArgs& a, const TileCtx& tc, double (*tred)[256 / 32]) {
-  constexpr int TY = d2_tile_y(K), TX = KCG_TX, H = KCG_HALO2, BW = d2_box_w(), BH = TY + 2 * H;
-  constexpr int PLANE = BW * BH, SPL = BW * (TY + 6), UPL = BW * (TY + 4);
-  constexpr int NT = 256;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int side = a.side;
-  const size_t N = (size_t)side * side;
-  const size_t ps = (size_t)a.pitch * side;
-  double* __restrict__ R = tc.R;
-  double* __restrict__ Pp = tc.Pp;
-  double* __restrict__ S = tc.S;
-  const int s = tc.s, y0 = tc.y0, x0 = tc.x0;
-  const double alpha = tc.alpha, beta = tc.beta, kappa2 = tc.kappa2, ap = tc.alpha_prev;
-  const double* __restrict__ Mg = tc.sp->M;
-  const double* __restrict__ Kinvg = &tc.sp->Kinv[0][0];
-  auto gyx = [&](int by, int bx, int& gy, int& gx) { gy = y0 - H + by; gx = x0 - H + bx; };
-  // interior tiles (EDGE = false: the box lies inside the face) skip every boundary test
-  auto in_face = [&](int gy, int gx) { return !EDGE || (gy >= 0 && gy < side && gx >= 0 && gx < side); };
-  auto degree_full = [&](int gy, int gx) { return 4 - (gy == 0) - (gy == side - 1) - (gx == 0) - (gx == side - 1); };
-  auto degree = [&](int gy, int gx) { return EDGE ? degree_full(gy, gx) : 4; };  // box rows/cols >= 1 only
-  auto hit = [&](int gy, int gx) { return HITS ? __ldg(tc.hp + (size_t)gy * side + gx) : 1.0; };
-  // K_j^{-1} r for PREC: Kinv holds (M + (kappa2 + d^2 + d) P)^{-1}, d = 2, 3, 4, 0 (host)
-  double tau[K];
-#pragma unroll
-  for (int c = 0; c < K; ++c) tau[c] = __ldg(&tc.sp->tau[c]);
-
-  mbar_wait(tc.bar, tc.phase);
-
-  // Phase A (pairs of box columns)
-  for (int e0 = 0; e0 < PLANE / 2; e0 += NT) {
-    const int e = e0 + tid;
-    if (e < PLANE / 2) {
-      const int by = e / (BW / 2), bx = 2 * (e - by * (BW / 2));
-      double r0[K], r1[K], u0[K], u1[K];
-#pragma unroll
-      for (int c = 0; c < K; ++c) {
-        const double2 r = reinterpret_cast<const double2*>(R + c * PLANE)[e];
-        r0[c] = r.x; r1[c] = r.y;
-      }
-      if (PREC) {
-        int gy, gx;
-        gyx(by, bx, gy, gx);
-        const bool f0 = in_face(gy, gx), f1 = in_face(gy, gx + 1);
-        // the outermost box ring may lie on the face boundary even for an interior tile
-        const int d0 = f0 ? degree_full(gy, gx) : 4, d1 = f1 ? degree_full(gy, gx + 1) : 4;
-        precond_pixel<K, HITS>(Kinvg, Mg, tau, kappa2, HITS && f0 ? hit(gy, gx) : 1.0, d0, r0, u0, true);
-        precond_pixel<K, HITS>(Kinvg, Mg, tau, kappa2, HITS && f1 ? hit(gy, gx + 1) : 1.0, d1, r1, u1, true);
-      } else {
-#pragma unroll
-        for (int c = 0; c < K; ++c) { u0[c] = r0[c]; u1[c] = r1[c]; }
-      }
-      const bool tile_px = tc.xpass && by >= H && by < H + TY && bx >= H && bx < H + TX;
-#pragma unroll
-      for (int c = 0; c < K; ++c) {
-        double2* pp = reinterpret_cast<double2*>(Pp + c * PLANE) + e;
-        const double2 po = *pp;
-        *pp = make_double2(fma(beta, po.x, u0[c]), fma(beta, po.y, u1[c]));
-        if (tile_px) *reinterpret_cast<double2*>(tc.pold + ((size_t)c * TY + (by - H)) * TX + (bx - H)) = po;
-      }
-    }
-  }
-  __syncwarp();
-  __syncthreads();
-
-  // D v at box point (by, bx) of plane c (v zero outside the face by construction)
-  auto Dat = [&](const double* V, int pl, int by, int bx, int deg) {
-    const double* v = V + pl + by * BW + bx;
-    return ((v[-BW] + v[BW]) + (v[-1] + v[1])) - deg * v[0];
-  };
-  // Phase B0: S = D p_new on box rows/cols [1, BH-1) (tile + 3-ring); zero outside the face
-  constexpr int B0W = TX + 6, B0H = TY + 6;
-  for (int e0 = 0; e0 < B0W * B0H; e0 += NT) {
-    const int e = e0 + tid;
-    if (e < B0W * B0H) {
-      const int by = 1 + e / B0W, bx = 1 + e % B0W;
-      int gy, gx;
-      gyx(by, bx, gy, gx);
-      const bool f = in_face(gy, gx);
-      const int deg = f ? degree(gy, gx) : 0;
-#pragma unroll
-      for (int c = 0; c < K; ++c) S[c * SPL + (by - 1) * BW + bx] = f ? Dat(Pp, c * PLANE, by, bx, deg) : 0.0;
-    }
-  }
-  __syncwarp();
-  __syncthreads();
-
-  // Phase B1: r_new = r - alpha (h M p + tau (kappa2 p + D S)) on box rows/cols [2, BH-2)
-  constexpr int B1W = TX + 4, B1H = TY + 4;
-  const double* __restrict__ Msh = tc.Ms;
-  double Mr[K * K];  // the mixing matrix in registers (not K^2 shared loads per point)
-#pragma unroll
-  for (int e2 = 0; e2 < K * K; ++e2) Mr[e2] = Msh[e2];
-  for (int e0 = 0; e0 < B1W * B1H; e0 += NT) {
-    const int e = e0 + tid;
-    if (e < B1W * B1H) {
-      const int by = 2 + e / B1W, bx = 2 + e % B1W;
-      int gy, gx;
-      gyx(by, bx, gy, gx);
-      if (in_face(gy, gx)) {
-        const int deg = degree(gy, gx);
-        const double h = hit(gy, gx);
-        double pc[K];
-#pragma unroll
-        for (int c = 0; c < K; ++c) pc[c] = Pp[c * PLANE + by * BW + bx];
-#pragma unroll
-        for (int c = 0; c < K; ++c) {
-          double mix = 0.0;
-#pragma unroll
-          for (int d = 0; d < K; ++d) mix = fma(Mr[c * K + d], pc[d], mix);
-          const double d2p = Dat(S, c * SPL - BW, by, bx, deg);  // S row = box row - 1
-          const double q = fma(h, mix, tau[c] * fma(kappa2, pc[c], d2p));
-          double* rp = R + c * PLANE + by * BW + bx;
-          *rp = fma(-alpha, q, *rp);
-        }
-      }
-    }
-  }
-  __syncwarp();
-  __syncthreads();
-
-  // Phase B' (PREC): U = K^{-1} r_new on box rows/cols [2, BH-2) (U row = box row - 2)
-  if (PREC) {
-    for (int e0 = 0; e0 < B1W * B1H; e0 += NT) {
-      const int e = e0 + tid;
-      if (e < B1W * B1H) {
-        const int by = 2 + e / B1W, bx = 2 + e % B1W;
-        int gy, gx;
-        gyx(by, bx, gy, gx);
-        double r[K], u[K];
-#pragma unroll
-        for (int c = 0; c < K; ++c) r[c] = R[c * PLANE + by * BW + bx];
-        if (in_face(gy, gx)) {
-          precond_pixel<K, HITS>(Msh + K * K + K, Msh, tau, kappa2, hit(gy, gx), degree(gy, gx), r, u, true);
-        } else {
-#pragma unroll
-          for (int c = 0; c < K; ++c) u[c] = 0.0;
-        }
-#pragma unroll
-        for (int c = 0; c < K; ++c) tc.U[c * UPL + (by - 2) * BW + bx] = u[c];
-      }
-    }
-    __syncwarp();
-    __syncthreads();
-  }
-  // v = U (PREC) or r_new, addressed with box rows: V + pl + by * BW
-  const double* __restrict__ V = PREC ? tc.U - 2 * BW : R;
-  constexpr int VPL = PREC ? UPL : PLANE;
-
-  // Phase C0: S = D v on box rows/cols [H-1, H+T+1) (tile + 1-ring); zero outside the face
-  constexpr int C0W = TX + 2, C0H = TY + 2;
-  for (int e0 = 0; e0 < C0W * C0H; e0 += NT) {
-    const int e = e0 + tid;
-    if (e < C0W * C0H) {
-      const int by = H - 1 + e / C0W, bx = H - 1 + e % C0W;
-      int gy, gx;
-      gyx(by, bx, gy, gx);
-      const bool f = in_face(gy, gx);
-      const int deg = f ? degree(gy, gx) : 0;
-#pragma unroll
-      for (int c = 0; c < K; ++c) S[c * SPL + (by - 1) * BW + bx] = f ? Dat(V, c * VPL, by, bx, deg) : 0.0;
-    }
-  }
-  __syncwarp();
-  __syncthreads();
-
-  // Phase C1: tile points (consecutive threads along a row: coalesced stores)
-  double rr = 0.0, ru = 0.0, wu = 0.0;
-  for (int e0 = 0; e0 < TY * TX; e0 += NT) {
-    const int e = e0 + tid;
-    const int ty = e / TX, tx = e - ty * TX;
-    const int by = H + ty, bx = H + tx;
-    const int gy = y0 + ty, gx = x0 + tx;
-    if (e < TY * TX && (!EDGE || (gy < side && gx < side))) {
-      const int deg = degree(gy, gx);
-      const double h = hit(gy, gx);
-      double vc[K];
-#pragma unroll
-      for (int c = 0; c < K; ++c) vc[c] = V[c * VPL + by * BW + bx];
-      double* xp = a.x + ((size_t)s * K * side + gy) * side + gx;
-      double xo[K];  // x loads issued before the point's arithmetic (L2 latency overlapped)
-#pragma unroll
-      for (int c = 0; c < K; ++c) xo[c] = tc.xpass ? __ldcg(xp + c * N) : 0.0;
-      const size_t ro = ((size_t)s * K) * ps + (size_t)gy * a.pitch + gx;
-      double* rout = (tc.par ? a.rbuf[0] : a.rbuf[1]) + ro;
-      double* pout = (tc.par ? a.pbuf[0] : a.pbuf[1]) + ro;
-#pragma unroll
-      for (int c = 0; c < K; ++c) {
-        double mix = 0.0;
-#pragma unroll
-        for (int d = 0; d < K; ++d) mix = fma(Mr[c * K + d], vc[d], mix);
-        const double d2v = Dat(S, c * SPL - BW, by, bx, deg);
-        const double w = fma(h, mix, tau[c] * fma(kappa2, vc[c], d2v));
-        const double rn = R[c * PLANE + by * BW + bx];
-        const double pn = Pp[c * PLANE + by * BW + bx];
-        rr = fma(rn, rn, rr);
-        if (PREC) ru = fma(rn, vc[c], ru);
-        wu = fma(w, vc[c], wu);
-        if (tc.xpass) {
-          const double po = tc.pold[((size_t)c * TY + ty) * TX + tx];
-          xp[c * N] = xo[c] + fma(alpha, pn, ap * po);
-        }
-        rout[c * ps] = rn;
-        pout[c * ps] = pn;
-      }
-    }
-  }
-  rr = warp_sum(rr);
-  wu = warp_sum(wu);
-  if (PREC) ru = warp_sum(ru);
-  if (lane == 0) {
-    tred[0][warp] = rr;
-    if (PREC) { tred[1][warp] = ru; tred[2][warp] = wu; }
-    else tred[1][warp] = wu;
-  }
-}
-
 // The persistent CG iteration of one CTA group: `cta` of `ncta` CTAs working on the systems of
 // `a` (the whole grid without slabs; one rank's group in row-slab mode, where the launch may carry
 // several emulated ranks).
@@ -1333,10 +1105,7 @@ __device__ __forceinline__ void cg_body(const CgArgs& a, const CgMaps& maps, con
       const int gy0 = (SLAB ? a.row0 : 0) + tc.y0;
       const bool interior = tc.x0 >= H && tc.x0 + TX + H <= a.side && gy0 >= H && gy0 + TY + H <= a.side &&
                             tc.y0 + TY <= (SLAB ? a.rows : a.side);
-      if constexpr (D2) {
-        if (interior) cg_tile_d2<K, HITS, PREC, false>(a, tc, tred[i & 1]);
-        else cg_tile_d2<K, HITS, PREC, true>(a, tc, tred[i & 1]);
-      } else if (cg_xtma(K) && xtma) {
+      if (cg_xtma(K) && xtma) {
         if (interior) cg_tile<K, false, HITS, cg_xtma(K), PREC, SLAB>(a, tc, tred[i & 1]);
         else cg_tile<K, true, HITS, cg_xtma(K), PREC, SLAB>(a, tc, tred[i & 1]);
       } else {
@@ -1391,6 +1160,10 @@ __global__ void __launch_bounds__(cg_threads(K), cg_min_blocks(K)) cg_slab_kerne
 }
 
 
+}  // namespace kcg
+#include "kcg_march.cuh"
+namespace kcg {
+
 // --------------------------------------------------------------------------- per-K entry points
 // Defined here, explicitly instantiated once per K in kcg_cg_k<K>.cu; the dispatchers in
 // kcg_kernels.cu see them as extern templates.
@@ -1409,16 +1182,24 @@ constexpr size_t cg_dyn_smem_fixed() {
             : cg_stages(K) * (size_t)cg_stage_bytes(K) + (PREC ? (size_t)cg_ubox_bytes(K) : 0);
 }
 
-template <int K, bool HITS, bool PREC, bool D2>
-static cudaError_t cg_config_t(bool slab, int n_sys, int* max_grid, size_t* smem) {
-  const size_t sm = cg_dyn_smem_fixed<K, PREC, D2>() + (size_t)n_sys * (sizeof(SysState) + sizeof(int));
+template <int K, bool HITS, bool PREC>
+static cudaError_t cg_config_t(bool slab, bool d2, int n_sys, int* max_grid, size_t* smem) {
   const void* kern = nullptr;
-  if constexpr (D2) kern = (const void*)cg_persistent_kernel<K, HITS, PREC, true>;
-  else kern = slab ? (const void*)cg_slab_kernel<K, HITS, PREC> : (const void*)cg_persistent_kernel<K, HITS, PREC, false>;
+  size_t sm = (size_t)n_sys * (sizeof(SysState) + sizeof(int));
+  int nt = cg_threads(K);
+  if (d2) {  // the row-march kernel (kcg_march.cuh)
+    if constexpr (K <= 4) kern = (const void*)cg_march_kernel<K, HITS, PREC>;
+    sm += (size_t)m_groups(K) * m_group_doubles(K) * 8;
+    nt = m_threads(K);
+  } else {
+    kern = slab ? (const void*)cg_slab_kernel<K, HITS, PREC> : (const void*)cg_persistent_kernel<K, HITS, PREC, false>;
+    sm += cg_dyn_smem_fixed<K, PREC, false>();
+  }
+  if (!kern) return cudaErrorInvalidValue;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
   if (e != cudaSuccess) return e;
   int nb = 0, dev = 0, nsm = 0;
-  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, threads_of(K, D2), sm);
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, nt, sm);
   if (e != cudaSuccess) return e;
   e = cudaGetDevice(&dev);
   if (e != cudaSuccess) return e;
@@ -1429,27 +1210,18 @@ static cudaError_t cg_config_t(bool slab, int n_sys, int* max_grid, size_t* smem
   return nb > 0 ? cudaSuccess : cudaErrorInvalidConfiguration;
 }
 
-// Built: PREC for K <= 7 (u box), the D2 prior for K <= 4 without slabs (halo-4 boxes).
+// Built: PREC for K <= 7 (u box), the D2 prior (row-march kernel) for K <= 4 without slabs.
 template <int K>
 cudaError_t CgEntry<K>::config(bool hits, bool prec, bool slab, bool d2, int n_sys, int* max_grid, size_t* smem) {
-  if (d2) {
-    if constexpr (K <= 4) {
-      if (slab) return cudaErrorInvalidValue;
-      if (prec) return hits ? cg_config_t<K, true, true, true>(false, n_sys, max_grid, smem)
-                            : cg_config_t<K, false, true, true>(false, n_sys, max_grid, smem);
-      return hits ? cg_config_t<K, true, false, true>(false, n_sys, max_grid, smem)
-                  : cg_config_t<K, false, false, true>(false, n_sys, max_grid, smem);
-    }
-    return cudaErrorInvalidValue;
-  }
+  if (d2 && (K > 4 || slab)) return cudaErrorInvalidValue;
   if (prec) {
     if constexpr (K <= 7)
-      return hits ? cg_config_t<K, true, true, false>(slab, n_sys, max_grid, smem)
-                  : cg_config_t<K, false, true, false>(slab, n_sys, max_grid, smem);
+      return hits ? cg_config_t<K, true, true>(slab, d2, n_sys, max_grid, smem)
+                  : cg_config_t<K, false, true>(slab, d2, n_sys, max_grid, smem);
     return cudaErrorInvalidValue;
   }
-  return hits ? cg_config_t<K, true, false, false>(slab, n_sys, max_grid, smem)
-              : cg_config_t<K, false, false, false>(slab, n_sys, max_grid, smem);
+  return hits ? cg_config_t<K, true, false>(slab, d2, n_sys, max_grid, smem)
+              : cg_config_t<K, false, false>(slab, d2, n_sys, max_grid, smem);
 }
 
 template <int K>
@@ -1460,8 +1232,8 @@ cudaError_t CgEntry<K>::launch(bool prec, bool d2, cudaStream_t s, const CgArgs&
   const void* f = nullptr;
   if (d2) {
     if constexpr (K <= 4) {
-      if (prec) f = hits ? (const void*)cg_persistent_kernel<K, true, true, true> : (const void*)cg_persistent_kernel<K, false, true, true>;
-      else f = hits ? (const void*)cg_persistent_kernel<K, true, false, true> : (const void*)cg_persistent_kernel<K, false, false, true>;
+      if (prec) f = hits ? (const void*)cg_march_kernel<K, true, true> : (const void*)cg_march_kernel<K, false, true>;
+      else f = hits ? (const void*)cg_march_kernel<K, true, false> : (const void*)cg_march_kernel<K, false, false>;
     }
   } else if (prec) {
     if constexpr (K <= 7) f = hits ? (const void*)cg_persistent_kernel<K, true, true, false> : (const void*)cg_persistent_kernel<K, false, true, false>;
@@ -1469,7 +1241,7 @@ cudaError_t CgEntry<K>::launch(bool prec, bool d2, cudaStream_t s, const CgArgs&
     f = hits ? (const void*)cg_persistent_kernel<K, true, false, false> : (const void*)cg_persistent_kernel<K, false, false, false>;
   }
   if (!f) return cudaErrorInvalidValue;
-  return cudaLaunchCooperativeKernel(f, dim3(grid), dim3(threads_of(K, d2)), args, smem, s);
+  return cudaLaunchCooperativeKernel(f, dim3(grid), dim3(d2 ? m_threads(K) : cg_threads(K)), args, smem, s);
 }
 
 template <int K>

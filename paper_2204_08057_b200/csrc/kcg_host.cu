@@ -47,9 +47,27 @@ struct Layout {
   size_t vec_doubles, partial_doubles;
 };
 
-int tiles_x(int side, int K) { return (side + KCG_TX - 1) / KCG_TX; }
+// Work geometry of the single-pass CG kernels: CTA tiles (Laplacian prior) or, for the D2 prior, the
+// row-march kernel's strips (x) and 16-row partial-sum blocks (y).
+int tiles_x(int side, int K, bool d2 = false) { return d2 ? kcg::m_strips(side) : (side + KCG_TX - 1) / KCG_TX; }
 int tiles_y(int rows, int K, bool d2 = false) {
-  return (rows + kcg::tile_y_of(K, d2) - 1) / kcg::tile_y_of(K, d2);
+  return d2 ? kcg::m_blocks(rows) : (rows + kcg::tile_y_of(K, false) - 1) / kcg::tile_y_of(K, false);
+}
+
+// D2 row-march kernel: rows per work unit (a multiple of the partial block KCG_MPB) minimising the
+// estimated pass time ceil(units / warps) * (seg + 8 warm-up rows + ~4 rows of pipeline fill), all
+// n_sys systems active.
+int march_seg(int side, int n_sys, int warps) {
+  if (side <= KCG_MPB) return KCG_MPB;
+  const long strips = kcg::m_strips(side);
+  int best = side;
+  double bt = 1e300;
+  for (int seg = KCG_MPB; seg < side + KCG_MPB; seg += KCG_MPB) {
+    const long units = (long)n_sys * strips * ((side + seg - 1) / seg);
+    const double t = (double)((units + warps - 1) / std::max(warps, 1)) * (std::min(seg, side) + 2 * KCG_MHALO + 4);
+    if (t < bt) { bt = t; best = seg; }
+  }
+  return best;
 }
 
 // One rank's layout: `rows` local rows (side / nranks), r/p buffers with `ghost` ghost rows.
@@ -63,8 +81,8 @@ Layout layout_of(const kcg_desc* d, int nranks) {
   const size_t P = d->n_patches, n = d->n_freq, k = d->n_comp;
   L.vec_doubles = P * k * (size_t)pitch * (rows + 2 * ghost);
   const bool d2 = d->prior == KCG_PRIOR_D2;
-  const size_t tk = (size_t)tiles_x(side, (int)k) * tiles_y(rows, (int)k, d2);
-  const size_t ts = (size_t)tiles_x(side, 1) * tiles_y(rows, 1, d2);
+  const size_t tk = (size_t)tiles_x(side, (int)k, d2) * tiles_y(rows, (int)k, d2) * (d2 ? k : 1);  // (D2: per plane)
+  const size_t ts = (size_t)tiles_x(side, 1, d2) * tiles_y(rows, 1, d2);
   L.partial_doubles = 2 * std::max(P * tk, P * k * ts) * 3;  // [2 parities][systems][tiles][<= 3]
   size_t off = 0;
   auto take = [&](size_t bytes) { size_t o = off; off += align_up(bytes); return o; };
@@ -422,8 +440,9 @@ PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
 
 bool encode_map(CUtensorMap* m, double* base, int side, int buf_rows, int pitch, size_t planes, int K, bool d2,
                 std::string* why) {
-  const int bx = KCG_TX + 2 * kcg::halo_of(d2);
-  const int by = kcg::tile_y_of(K, d2) + 2 * kcg::halo_of(d2);
+  // box: the CTA tile + halo, or (D2) one row-march chunk of 32 columns x KCG_MCH rows
+  const int bx = d2 ? 32 : KCG_TX + 2 * KCG_HALO;
+  const int by = d2 ? KCG_MCH : kcg::tile_y_of(K, false) + 2 * KCG_HALO;
   auto enc = get_encode();
   if (!enc) { *why = "cuTensorMapEncodeTiled unavailable"; return false; }
   cuuint64_t dims[3] = {(cuuint64_t)side, (cuuint64_t)buf_rows, (cuuint64_t)planes};
@@ -448,7 +467,7 @@ bool encode_xmap(CUtensorMap* m, double* base, int side, int rows, size_t planes
   if (!enc) { *why = "cuTensorMapEncodeTiled unavailable"; return false; }
   cuuint64_t dims[3] = {(cuuint64_t)side, (cuuint64_t)rows, (cuuint64_t)planes};
   cuuint64_t strides[2] = {(cuuint64_t)side * 8, (cuuint64_t)side * rows * 8};
-  cuuint32_t box[3] = {(cuuint32_t)KCG_TX, (cuuint32_t)kcg::tile_y_of(K, d2), (cuuint32_t)K};
+  cuuint32_t box[3] = {(cuuint32_t)(d2 ? 32 : KCG_TX), (cuuint32_t)(d2 ? KCG_MCH : kcg::tile_y_of(K, false)), (cuuint32_t)K};
   cuuint32_t es[3] = {1, 1, 1};
   CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, base, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
                    CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
@@ -641,7 +660,8 @@ kcg_status solve_impl(kcg_ctx* c, Route route, const double* Y_in, double* mu_ou
     a.n_sys = n_sys;
     a.tiles_x = kron ? c->tiles_x_kron : c->tiles_x_syl;
     a.tiles_y = kron ? c->tiles_y_kron : c->tiles_y_syl;
-    a.tiles_per_sys = a.tiles_x * a.tiles_y;
+    const bool march = c->d.prior == KCG_PRIOR_D2 && c->d.cg_variant == KCG_CG_SINGLE_PASS;
+    a.tiles_per_sys = a.tiles_x * a.tiles_y * (march ? Kk : 1);  // row-march kernel: partials per plane
     a.max_iter = max_iter;
     a.tol2 = tol * tol;
     a.trace = R.trace;
@@ -657,6 +677,10 @@ kcg_status solve_impl(kcg_ctx* c, Route route, const double* Y_in, double* mu_ou
         return KCG_E_CUDA;
       }
       a.x_tma = 1;
+    }
+    if (march) {  // row-march kernel: segment rows, hits by TMA
+      a.h_tma = (R.hits && c->side >= 2) ? 1 : 0;
+      a.seg = march_seg(c->side, n_sys, (kron ? c->grid_kron : c->grid_syl) * kcg::m_groups(Kk));
     }
     Lx.m[j] = maps;
     CK(cudaMemsetAsync(R.sync, 0, 4 * sizeof(unsigned), s), "memset sync");
@@ -986,6 +1010,10 @@ kcg_status kohler_impl(kcg_ctx* c, const double* Y_in, double* mu_out, double to
     }
     CK(cudaMemsetAsync(R.sync, 0, 4 * sizeof(unsigned), s), "memset sync");
     const int grid = std::max(1, std::min(c->grid_syl, P * a.tiles_per_sys));
+    if (d2) {
+      a.h_tma = (R.hits && c->side >= 2) ? 1 : 0;
+      a.seg = march_seg(c->side, P, grid * kcg::m_groups(1));
+    }
     if (c->res_koh.on) {
       a.tiles_per_sys = c->res_koh.nstrip;
       CKL(kcg::launch_cg_resident(1, prec, s, a, R.res_part, c->res_koh.grid, c->res_koh.smem),
@@ -1064,14 +1092,20 @@ namespace {
 // system ("single": the face's K N values are few) or strips of RS >= 2 rows, at most one CTA per SM.
 ResPlan plan_resident(int K, int side, int n_sys, bool hits, bool prec, int nsm) {
   ResPlan P;
-  if (const char* ev = std::getenv("KCG_RESIDENT"))
-    if (std::atoi(ev) == 0) return P;
+  // KCG_RESIDENT: 0 = never, 2 = also the row-strip (grid-barrier) mode.  Default: single-CTA faces
+  // only -- the strip mode measured slower than the streaming kernel (medium, L = 8, K = 3: 9.8 vs
+  // 7.6 us per iteration; profiles/r02/res_trace_medium.txt), so it is an opt-in experiment.
+  int mode = 1;
+  if (const char* ev = std::getenv("KCG_RESIDENT")) mode = std::atoi(ev);
+  if (mode == 0) return P;
   if (prec && K > 7) return P;
   const size_t lim = 220 * 1024;  // dynamic smem budget (static: ~3 KB)
   int best_rs = 0;
   if ((size_t)K * side * side <= 8192 && kcg::res_smem(K, side, side, hits, prec, n_sys) <= lim && n_sys <= nsm)
     best_rs = side;
-  for (int rs = 2; !best_rs && rs <= side; rs *= 2) {
+  int rs0 = 2;  // experiments: KCG_RES_RS = the smallest strip height to consider
+  if (const char* ev = std::getenv("KCG_RES_RS")) rs0 = std::max(2, std::atoi(ev));
+  for (int rs = rs0; mode == 2 && !best_rs && rs <= side; rs *= 2) {
     const long long grid = (long long)n_sys * (side / rs);
     if (grid <= nsm && grid <= KCG_RES_CTA_MAX && kcg::res_smem(K, rs, side, hits, prec, n_sys) <= lim) best_rs = rs;
   }
@@ -1303,6 +1337,12 @@ kcg_status create_impl(const kcg_desc* d, const kcg_slab* sl, const double* A_ho
           !encode_map(&R.maps_syl.p[i], R.p[i], c->side, buf_rows, c->pitch, planes, 1, d2, &why))
         return fail(KCG_E_CUDA, why);
     }
+    // D2 row-march kernel: the hits planes [P][side][side], one chunk of 32 x KCG_MCH per box
+    if (d2 && R.hits && c->side >= 2) {
+      if (!encode_xmap(&R.maps_kron.h, const_cast<double*>(R.hits), c->side, c->side, (size_t)P, 1, true, &why))
+        return fail(KCG_E_CUDA, why);
+      R.maps_syl.h = R.maps_kron.h;
+    }
   }
   if (c->L.lz_slots > 0) {  // block-Lanczos constants: Lemma 2 factor, E = T A P^{-1} (Y^ = Y E)
     std::vector<kcg::LzFace> lf(P);
@@ -1347,9 +1387,9 @@ kcg_status create_impl(const kcg_desc* d, const kcg_slab* sl, const double* A_ho
     }
   }
   CKC(cudaStreamSynchronize(c->stream), "create sync");
-  c->tiles_x_kron = tiles_x(c->side, k);
+  c->tiles_x_kron = tiles_x(c->side, k, d2);
   c->tiles_y_kron = tiles_y(c->rows, k, d2);
-  c->tiles_x_syl = tiles_x(c->side, 1);
+  c->tiles_x_syl = tiles_x(c->side, 1, d2);
   c->tiles_y_syl = tiles_y(c->rows, 1, d2);
   int mg = 0;
   const bool prec = d->precond == KCG_PRECOND_BLOCK_JACOBI;
@@ -1362,6 +1402,7 @@ kcg_status create_impl(const kcg_desc* d, const kcg_slab* sl, const double* A_ho
     c->res_koh = plan_resident(1, c->side, P, hits_dev != nullptr, prec, nsm);
   }
   if (d->cg_variant == KCG_CG_HS) {  // textbook CG variant: its own tile geometry and grid
+    c->tiles_x_kron = c->tiles_x_syl = tiles_x(c->side, 1);
     c->tiles_y_kron = (c->rows + kcg::hs_tile_y(k) - 1) / kcg::hs_tile_y(k);
     c->tiles_y_syl = (c->rows + kcg::hs_tile_y(1) - 1) / kcg::hs_tile_y(1);
     CKC(kcg::hs_kernel_config(k, hits_dev != nullptr, prec, d2, P, &mg, &c->smem_kron), "hs kernel config (kron)");
@@ -1373,10 +1414,12 @@ kcg_status create_impl(const kcg_desc* d, const kcg_slab* sl, const double* A_ho
     return KCG_OK;
   }
   CKC(kcg::cg_kernel_config(k, hits_dev != nullptr, prec, c->slab, d2, P, &mg, &c->smem_kron), "cg kernel config (kron)");
-  c->grid_kron = std::max(1, std::min(mg / c->nlocal, P * c->tiles_x_kron * c->tiles_y_kron));
+  // (D2 row-march kernel: m_groups(K) warp groups per CTA, each a work unit of >= one strip x 16 rows)
+  const int wdk = d2 ? kcg::m_groups(k) : 1, wds = d2 ? kcg::m_groups(1) : 1;
+  c->grid_kron = std::max(1, std::min(mg / c->nlocal, (P * c->tiles_x_kron * c->tiles_y_kron + wdk - 1) / wdk));
   CKC(kcg::cg_kernel_config(1, hits_dev != nullptr, prec, c->slab, d2, P * k, &mg, &c->smem_syl),
       "cg kernel config (sylvester)");
-  c->grid_syl = std::max(1, std::min(mg / c->nlocal, P * k * c->tiles_x_syl * c->tiles_y_syl));
+  c->grid_syl = std::max(1, std::min(mg / c->nlocal, (P * k * c->tiles_x_syl * c->tiles_y_syl + wds - 1) / wds));
   if (mg < c->nlocal) return fail(KCG_E_CONFIG, "slab: more emulated ranks than co-resident CTAs");
   for (int i = 0; i < 4; ++i) CKC(cudaEventCreate(&c->ev[i]), "event create");
 #undef CKC
@@ -1675,7 +1718,6 @@ const char* kcg_status_string(int s) {
     case KCG_E_NONFINITE: return "KCG_E_NONFINITE";
     case KCG_E_BREAKDOWN: return "KCG_E_BREAKDOWN";
     case KCG_E_CUDA: return "KCG_E_CUDA";
-    case KCG_E_NCCL: return "KCG_E_NCCL";
     case KCG_E_STATE: return "KCG_E_STATE";
     default: return "KCG_UNKNOWN";
   }

@@ -78,6 +78,25 @@ __host__ __device__ constexpr int d2_stage_bytes(int K) { return 2 * K * (d2_til
 __host__ __device__ constexpr int d2_sbox_bytes(int K) { return K * (d2_tile_y(K) + 6) * d2_box_w() * 8; }
 __host__ __device__ constexpr int d2_pold_bytes(int K) { return K * d2_tile_y(K) * KCG_TX * 8; }
 __host__ __device__ constexpr int d2_ubox_bytes(int K) { return K * (d2_tile_y(K) + 4) * d2_box_w() * 8; }
+// ---- D2 prior: the row-march CG kernel (kcg_march.cuh).  A GROUP of K warps (warp c = component
+// plane c) marches a strip of KCG_MOUT output columns (32 lanes = the strip + a 4-column halo each
+// side) down a segment of rows; rows of r, p, x, hits are TMA-staged one row per stage into a
+// per-group ring of m_stages(K) stages; the planes meet only in the k x k mixing (shared rows).
+#define KCG_MOUT 24
+#define KCG_MHALO 4
+#define KCG_MCH 1           // rows per TMA stage
+#define KCG_MPB 16          // rows per partial-sum block (fixed reduction order)
+__host__ __device__ constexpr int m_groups(int K) { return K == 1 ? 16 : (K == 2 ? 8 : (K == 3 ? 5 : 4)); }
+__host__ __device__ constexpr int m_threads(int K) { return m_groups(K) * K * 32; }
+__host__ __device__ constexpr int m_stages(int K) { return 8; }
+__host__ __device__ constexpr int m_stage_doubles(int K) { return (3 * K + 1) * 32; }
+// doubles of one group's shared memory: the stage ring + 3 exchange rings [4 rows][K][32]
+__host__ __device__ constexpr int m_group_doubles(int K) { return m_stages(K) * m_stage_doubles(K) + 3 * 4 * K * 32; }
+__host__ __device__ constexpr int m_strips(int side) { return (side + KCG_MOUT - 1) / KCG_MOUT; }
+__host__ __device__ constexpr int m_blocks(int side) { return (side + KCG_MPB - 1) / KCG_MPB; }
+// partial slots per system: strips x 16-row blocks x planes
+__host__ __device__ constexpr int m_slots(int side, int K) { return m_strips(side) * m_blocks(side) * K; }
+
 // geometry by prior
 __host__ __device__ constexpr int tile_y_of(int K, bool d2) { return d2 ? d2_tile_y(K) : cg_tile_y(K); }
 __host__ __device__ constexpr int halo_of(bool d2) { return d2 ? KCG_HALO2 : KCG_HALO; }
@@ -120,6 +139,7 @@ struct CgMaps {              // TMA descriptors of rbuf[0..1], pbuf[0..1] (box =
   CUtensorMap r[2];
   CUtensorMap p[2];
   CUtensorMap x;             // the solution buffer, box = {TX, TY, K}; re-encoded per solve
+  CUtensorMap h;             // D2 march kernel: the hits planes [P][side][side], box = {32, KCG_MCH, 1}
 };
 
 struct CgArgs {
@@ -138,6 +158,8 @@ struct CgArgs {
   int n_sys, tiles_x, tiles_y, tiles_per_sys;
   int max_iter;
   int x_tma;                 // 1: CgMaps::x describes `x` (TMA needs side >= 2): staged (K <= 3) or L2-prefetched
+  int h_tma;                 // D2 march kernel: 1 = CgMaps::h describes the hits planes (side >= 2)
+  int seg;                   // D2 march kernel: rows per work unit (a multiple of KCG_MPB)
   long long* trace;          // KCG_TRACE builds only: per-iteration %globaltimer stamps
   unsigned* sync;            // [2..3] tile-claim counters of the two pass parities (zeroed per launch)
   double tol2;

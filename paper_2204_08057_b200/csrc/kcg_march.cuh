@@ -1,0 +1,380 @@
+#pragma once
+// sm_100a fp64: the single-pass CG iteration for the paper's own prior Q0 = D^2 + kappa2 I
+// (reading R3 "d2"; Alg.MatvecD P:L128-138 applied twice) as a ROW MARCH in registers.
+//
+// Why not the CTA tiles of the Laplacian kernel: with a radius-2 operator the single-pass recompute
+// needs p on the tile + 4 rings, so a 64 x 8 tile staged a 72 x 16 box (2.25x) and evaluated five
+// shared-memory stencil phases over it -- the round-1 kernel was shared-memory-wavefront and barrier
+// bound (ncu: smem pipe ~58% busy, issue active 25%, 0.22 of HBM).  Here:
+//
+//   * a GROUP of K warps owns a strip of 24 output columns (lane l = box column x0 - 4 + l, 4-column
+//     halo each side), warp c of the group component plane c, and marches DOWN a segment of rows;
+//     everything a pixel needs from its vertical neighbours sits in small per-lane register rings
+//     (3 rows per quantity), its horizontal neighbours come from the adjacent lanes by shuffles --
+//     no shared-memory stencil at all; the planes meet only in the k x k mixing, through 4-row
+//     shared rings of p_new / r_new (/ u_new) and one named barrier of the group per row, no CTA
+//     barrier inside a pass (one plane per warp: ~60 registers, 16 warps per SM);
+//   * the rows of r, p (and x on x passes, hits with N_h) are staged by TMA one row (32 columns x K
+//     planes) per stage into a per-warp ring of m_stages(K) shared-memory stages (own mbarriers),
+//     prefetched continuously across the warp's units (zero fill outside the face = the free
+//     boundary); a stage is held until its r feeds r_old two rows later;
+//   * per input row y the warp evaluates, pipelined by one row per phase,
+//         A   p_new(y)   = u(y) + beta p(y)          (u = r, or K^{-1} r with block-Jacobi)
+//         B0  S1(y-1)    = D p_new                   (0 outside the face)
+//         B1  r_new(y-2) = r - alpha (h M p_new + tau (kappa2 p_new + D S1))
+//         C0  S2(y-3)    = D u_new                   (u_new = r_new, or K^{-1} r_new)
+//         C1  w(y-4)     = h M u_new + tau (kappa2 u_new + D S2);  (r,r), (r,u), (w,u)
+//     p_new, x (+= alpha_prev p_old + alpha p_new on x passes) and r_new are final when computed and
+//     are stored at once (valid columns / segment rows only);
+//   * work unit = (system, strip, segment of `seg` rows), claimed dynamically per warp; the segment
+//     starts 4 rows early (warm-up: the halo rows are recomputed -- bitwise identical to the
+//     neighbouring unit's values, so the iterate does not depend on the decomposition);
+//   * partials per (system, strip, 16-row block, plane): the reduction order is fixed by the face
+//     geometry, independent of the segment length, the grid and the batch composition.
+//   * block-Jacobi: u = K^{-1} r mixes the planes too -- A reads every plane of r from the stage;
+//     u_new is formed one row later from the shared r_new ring (C0 / C1 one row further behind).
+// Global traffic per pass = the Laplacian kernel's (r, p read + written, x every other pass) plus
+// the re-read halo columns (L2) and 8 warm-up rows per segment.
+// Edge cases: faces narrower than a strip (one strip, masked lanes), level 0 (deg 0), x / hits
+// without a TMA descriptor (side 1: direct loads).
+
+namespace kcg {
+
+__device__ __forceinline__ void group_bar(int id, int nthreads) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
+
+template <int K, bool HITS, bool PREC>
+__global__ void __launch_bounds__(m_threads(K), 1) cg_march_kernel(const CgArgs a, const __grid_constant__ CgMaps maps) {
+  constexpr int NG = m_groups(K), NT = m_threads(K), NW = NT / 32, NS = m_stages(K), SD = m_stage_doubles(K);
+  constexpr int XR = 4 * K * 32, GD = m_group_doubles(K);
+  constexpr int MO = KCG_MOUT, MH = KCG_MHALO, PB = KCG_MPB;
+  constexpr int NP = PREC ? 3 : 2;
+  constexpr int DL = PREC ? 5 : 4;  // row of C1 behind the input row
+  constexpr int MSZ = K * K + K + (PREC ? 4 * K * K : 0);
+  constexpr unsigned FULL = 0xffffffffu;
+  static_assert((NS & (NS - 1)) == 0 && NS >= 4 && KCG_MCH == 1 && (K == 1 || NG <= 15), "geometry");
+
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  SysState* st = reinterpret_cast<SysState*>(smem_raw + (size_t)NG * GD * 8);
+  int* act = reinterpret_cast<int*>(st + a.n_sys);
+  __shared__ __align__(8) uint64_t mbar[NG][NS];
+  __shared__ double rs[KCG_RB][3][NW];
+  __shared__ double Mw[NW][MSZ];  // per-warp constants of the system being marched
+  __shared__ int uq[NG][4];       // units claimed by each group's issuing warp, in order
+  __shared__ int s_nact;
+
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int g = warp / K, c = warp - g * K;  // group, plane
+  const bool issuer = c == 0;                // the group's TMA / claim warp
+  const int cta = blockIdx.x, ncta = gridDim.x;
+  const int side = a.side, pitch = a.pitch, seg = a.seg;
+  const int nstrips = a.tiles_x, tps = a.tiles_per_sys;
+  const int nsegs = (side + seg - 1) / seg, ups = nstrips * nsegs;  // units per system
+  const size_t N = (size_t)side * side, ps = (size_t)pitch * side;
+  double* gsm = reinterpret_cast<double*>(smem_raw) + (size_t)g * GD;
+  double* stg = gsm;                 // [NS][SD]: r [K][32], p [K][32], x [K][32], hits [32]
+  double* PX = gsm + NS * SD;        // [4][K][32] p_new rows
+  double* RX = PX + XR;              // [4][K][32] r_new rows
+  double* UX = RX + XR;              // [4][K][32] u_new rows (block-Jacobi)
+  auto gsync = [&]() {
+    if constexpr (K == 1) __syncwarp();
+    else group_bar(1 + g, K * 32);
+  };
+
+  if (tid == 0) {  // the launch must provide the dynamic shared memory this layout assumes
+    unsigned dyn;
+    asm volatile("mov.u32 %0, %%dynamic_smem_size;" : "=r"(dyn));
+    if ((size_t)dyn < (size_t)NG * GD * 8 + (size_t)a.n_sys * (sizeof(SysState) + sizeof(int))) __trap();
+  }
+  for (int s = tid; s < a.n_sys; s += NT) {
+    SysState z;
+    z.bnorm2 = 0.0; z.gamma = 0.0; z.alpha = 0.0; z.beta = 0.0; z.rel = 1.0;
+    z.iters = 0; z.status = ST_RUNNING; z.parity = 0; z.pad = 0; z.alpha_last = 0.0;
+    st[s] = z;
+  }
+  if (tid == 0) {
+    for (int w = 0; w < NG; ++w)
+      for (int i = 0; i < NS; ++i) mbar_init(&mbar[w][i], 1);
+    fence_mbar_init();
+  }
+  // r_old of a unit's first two rows reads stages of the previous unit (masked): keep them finite
+  for (int e = tid; e < NG * GD; e += NT) reinterpret_cast<double*>(smem_raw)[e] = 0.0;
+  __syncthreads();
+
+  auto xpass_of = [](int q) { return KCG_X2 ? (q >= 2 && (q & 1) == 0) : (q >= 1); };
+  struct Unit { int s, x0, ys, ye, nsteps, par, hpl; };
+  auto unit_of = [&](int u) {  // a unit's geometry from its index in the pass's active-unit list
+    Unit U;
+    const int i = u / ups, rem = u - i * ups, sg = rem / nstrips;
+    U.s = act[i];
+    U.x0 = (rem - sg * nstrips) * MO;
+    U.ys = sg * seg;
+    U.ye = min(side, U.ys + seg);
+    U.nsteps = (U.ye - U.ys + MH + DL + 2) / 3 * 3;  // rows ys-4 .. >= ye-1+DL, a multiple of the ring period
+    U.par = st[U.s].parity;
+    U.hpl = HITS ? (int)__ldg(&a.params[U.s].hits_plane) : 0;
+    return U;
+  };
+
+  // per-group stage sequence numbers (uniform in the group): issued / waited for / freed
+  uint32_t gi = 0, gr = 0, gf = 0;
+  int it = -1;
+  unsigned gepoch = 0;
+  while (true) {
+    if (tid == 0) {
+      int n = 0;
+      for (int s = 0; s < a.n_sys; ++s)
+        if (st[s].status == ST_RUNNING) act[n++] = s;
+      s_nact = n;
+    }
+    __syncthreads();
+    const int nact = s_nact;
+    if (nact == 0) break;
+    const int units = nact * ups;
+    const int par_out = (it + 1) & 1;
+    const bool xpass = xpass_of(it + 1);
+    const bool xl = xpass && a.x_tma;  // x rows staged with r and p
+    const bool hl = HITS && a.h_tma;
+    const uint32_t tx_bytes = (2 * K + (xl ? K : 0) + (hl ? 1 : 0)) * 32 * 8;
+    unsigned* ctr = a.sync + 2 + par_out;
+    const int ngt = ncta * NG;
+
+    // ---- the group's row stream (issuing warp only): unit iu, next row ic; claims published in uq
+    int iu = cta * NG + g, ic = 0, kq = 0;
+    Unit I{};
+    if (issuer && iu < units) I = unit_of(iu);
+    auto advance_issue = [&]() {
+      if (iu >= units) return;
+      if (ic == I.nsteps) {  // the issuing unit is exhausted: claim the next one
+        unsigned cl = 0;
+        if (lane == 0) cl = atomicAdd(ctr, 1u);
+        iu = ngt + (int)__shfl_sync(FULL, cl, 0);
+        ic = 0;
+        ++kq;
+        if (lane == 0) uq[g][kq & 3] = iu;
+        if (iu >= units) return;
+        I = unit_of(iu);
+      }
+      if (lane == 0) {
+        const int slot = gi & (NS - 1);
+        double* d = stg + slot * SD;
+        uint64_t* bar = &mbar[g][slot];
+        const int r0 = I.ys - MH + ic, c0 = I.x0 - MH;
+        mbar_arrive_expect_tx(bar, tx_bytes);
+        tma_load_3d(d, &maps.r[I.par], bar, c0, r0, I.s * K);
+        tma_load_3d(d + K * 32, &maps.p[I.par], bar, c0, r0, I.s * K);
+        if (xl) tma_load_3d(d + 2 * K * 32, &maps.x, bar, c0, r0, I.s * K);
+        if (hl) tma_load_3d(d + 3 * K * 32, &maps.h, bar, c0, r0, I.hpl);
+      }
+      ++ic;
+      ++gi;
+    };
+    if (issuer)
+      for (int j = 0; j < NS; ++j) advance_issue();
+
+    int cu = cta * NG + g, ku = 0;
+    while (cu < units) {
+      const Unit C = unit_of(cu);
+      const SysParams* sp = a.params + C.s;
+      __syncwarp();
+      for (int e = lane; e < MSZ; e += 32)
+        Mw[warp][e] = e < K * K ? __ldg(&sp->M[e]) : (e < K * K + K ? __ldg(&sp->tau[e - K * K]) : __ldg(&sp->Kinv[0][0] + (e - K * K - K)));
+      __syncwarp();
+      double Mrow[K];  // row c of M
+#pragma unroll
+      for (int d = 0; d < K; ++d) Mrow[d] = Mw[warp][c * K + d];
+      const double tau_c = Mw[warp][K * K + c];
+      const SysState z = st[C.s];
+      const double alpha = z.alpha, beta = z.beta, ap = KCG_X2 ? z.alpha_last : 0.0;
+      const double kappa2 = __ldg(&sp->kappa2);
+      const double* hp = HITS ? a.hits + (size_t)C.hpl * N : nullptr;
+      const int gx = C.x0 - MH + lane;
+      const bool colin = gx >= 0 && gx < side;
+      const bool outc = lane >= MH && lane < MH + MO && gx < side;
+      const int degx = 4 - (gx == 0) - (gx == side - 1);
+      const size_t pc = ((size_t)C.s * K + c);  // this warp's plane
+      double* rout = (C.par ? a.rbuf[0] : a.rbuf[1]) + pc * ps + gx;  // select, not a dynamic index
+      double* pout = (C.par ? a.pbuf[0] : a.pbuf[1]) + pc * ps + gx;
+      double* xo = a.x + pc * N + gx;
+      const int strip = C.x0 / MO;
+      double* part = a.partials + ((size_t)par_out * a.n_sys + C.s) * tps * NP + ((size_t)strip * K + c) * NP;
+      // the full K x K block-Jacobi solve of a pixel (block-Jacobi): every plane of v, plane c of K^{-1} v
+      auto prec_c = [&](const double (&v)[K], double h, double dg) {
+        double u[K];
+        double tau[K];
+#pragma unroll
+        for (int d = 0; d < K; ++d) tau[d] = Mw[warp][K * K + d];
+        precond_pixel<K, HITS>(&Mw[warp][K * K + K], &Mw[warp][0], tau, kappa2, h, (int)dg, v, u, true);
+        double uc = u[0];
+#pragma unroll
+        for (int d = 1; d < K; ++d) uc = d == c ? u[d] : uc;
+        return uc;
+      };
+
+      // register rings of this plane (slot of row y = (y - ys + 4) mod 3)
+      double pn[3] = {0.0, 0.0, 0.0}, s1[3] = {0.0, 0.0, 0.0}, rn[3] = {0.0, 0.0, 0.0}, s2[3] = {0.0, 0.0, 0.0};
+      double un[3] = {0.0, 0.0, 0.0};
+      // per-row values of rows y-1 .. y-5, shifted by one every step: in-face flag, degree, hits
+      bool f1 = false, f2 = false, f3 = false, f4 = false, f5 = false;
+      double dg1 = 0.0, dg2 = 0.0, dg3 = 0.0, dg4 = 0.0, dg5 = 0.0;
+      double h1 = 1.0, h2 = 1.0, h3 = 1.0, h4 = 1.0, h5 = 1.0;
+      double prr = 0.0, pru = 0.0, pwu = 0.0;  // partials of the current 16-row block
+      const uint32_t q0 = gr;                 // the unit's first stage
+      auto free_stage = [&]() {               // issuing warp: the oldest held stage is consumed, refill it
+        ++gf;
+        if (lane == 0) fence_proxy_async_smem();
+        advance_issue();
+      };
+      auto xr = [&](const double* X, int row, int d) { return X[((row & 3) * K + d) * 32 + lane]; };
+
+      // one input row: y = ys - 4 + t, ring period 3 (J = t mod 3 at compile time)
+      auto step = [&](auto Jc, int t) {
+        constexpr int J = decltype(Jc)::value, J1 = (J + 2) % 3, J2 = (J + 1) % 3;  // rows y-1 | y-4, y-2 | y-5
+        const int y = C.ys - MH + t;
+        const uint32_t q = gr++;
+        const int slot = q & (NS - 1);
+        mbar_wait(&mbar[g][slot], (q / NS) & 1u);
+        const double* sg = stg + slot * SD + lane;
+        const double r_c = sg[c * 32], p_c = sg[(K + c) * 32];
+        const double ro_c = stg[((q - 2) & (NS - 1)) * SD + c * 32 + lane];  // r_old of row y - 2
+        const bool f0 = colin && (unsigned)y < (unsigned)side;
+        const double dg0 = (double)(degx - (y == 0) - (y == side - 1));
+        const bool vA = outc && y >= C.ys && y < C.ye;
+        double xv = 0.0;
+        if (xpass) xv = xl ? sg[(2 * K + c) * 32] : (vA ? __ldcg(xo + (size_t)y * side) : 0.0);
+        double h0 = 1.0;
+        if (HITS) h0 = hl ? sg[3 * K * 32] : (f0 ? __ldg(hp + (size_t)y * side + gx) : 1.0);
+        // A: p_new(y)
+        double u_c = r_c;
+        if (PREC) {
+          double rv[K];
+#pragma unroll
+          for (int d = 0; d < K; ++d) rv[d] = sg[d * 32];
+          u_c = f0 ? prec_c(rv, h0, dg0) : 0.0;
+        }
+        pn[J] = fma(beta, p_c, u_c);
+        if (K > 1) PX[((y & 3) * K + c) * 32 + lane] = pn[J];
+        if (vA) {
+          pout[(size_t)y * pitch] = pn[J];
+          if (xpass) xo[(size_t)y * side] = xv + fma(alpha, pn[J], ap * p_c);
+        }
+        // B0: S1(y-1) = D p_new
+        {
+          const double v = pn[J1];
+          const double L = __shfl_up_sync(FULL, v, 1), R = __shfl_down_sync(FULL, v, 1);
+          s1[J1] = f1 ? fma(-dg1, v, (pn[J2] + pn[J]) + (L + R)) : 0.0;
+        }
+        // B1: r_new(y-2)
+        {
+          const double v = s1[J2];
+          const double L = __shfl_up_sync(FULL, v, 1), R = __shfl_down_sync(FULL, v, 1);
+          const double d2p = fma(-dg2, v, (s1[J] + s1[J1]) + (L + R));
+          double mix = 0.0;
+#pragma unroll
+          for (int d = 0; d < K; ++d) mix = fma(Mrow[d], d == c ? pn[J2] : xr(PX, y - 2, d), mix);
+          const double qv = fma(h2, mix, tau_c * fma(kappa2, pn[J2], d2p));
+          rn[J2] = f2 ? fma(-alpha, qv, ro_c) : 0.0;
+          if (K > 1 || PREC) RX[(((y - 2) & 3) * K + c) * 32 + lane] = rn[J2];
+          const int y2 = y - 2;
+          if (outc && y2 >= C.ys && y2 < C.ye) rout[(size_t)y2 * pitch] = rn[J2];
+        }
+        // B' (block-Jacobi): u_new(y-3) = K^{-1} r_new from the shared r_new row
+        if (PREC) {
+          double rv[K];
+#pragma unroll
+          for (int d = 0; d < K; ++d) rv[d] = d == c ? rn[J] : xr(RX, y - 3, d);
+          un[J] = f3 ? prec_c(rv, h3, dg3) : 0.0;
+          if (K > 1) UX[(((y - 3) & 3) * K + c) * 32 + lane] = un[J];
+        }
+        // C0: S2 = D u_new at row y-3 (u = r_new) or y-4 (block-Jacobi)
+        if (!PREC) {
+          const double v = rn[J];
+          const double L = __shfl_up_sync(FULL, v, 1), R = __shfl_down_sync(FULL, v, 1);
+          s2[J] = f3 ? fma(-dg3, v, (rn[J1] + rn[J2]) + (L + R)) : 0.0;
+        } else {  // u_new rows: y-3 -> J, y-4 -> J1, y-5 -> J2; S2 row y-4 -> J1
+          const double v = un[J1];
+          const double L = __shfl_up_sync(FULL, v, 1), R = __shfl_down_sync(FULL, v, 1);
+          s2[J1] = f4 ? fma(-dg4, v, (un[J2] + un[J]) + (L + R)) : 0.0;
+        }
+        // C1: w at row yc = y - DL and the partials
+        {
+          const int yc = y - DL;
+          double w, uc, rc;
+          if (!PREC) {  // S2 rows y-5 (J2), y-4 (J1), y-3 (J); u = r_new row y-4 (J1)
+            const double v = s2[J1];
+            const double L = __shfl_up_sync(FULL, v, 1), R = __shfl_down_sync(FULL, v, 1);
+            const double d2v = fma(-dg4, v, (s2[J2] + s2[J]) + (L + R));
+            double mix = 0.0;
+#pragma unroll
+            for (int d = 0; d < K; ++d) mix = fma(Mrow[d], d == c ? rn[J1] : xr(RX, yc, d), mix);
+            uc = rn[J1];
+            rc = uc;
+            w = fma(h4, mix, tau_c * fma(kappa2, uc, d2v));
+          } else {      // S2 rows y-6 (J), y-5 (J2), y-4 (J1); u_new row y-5 (J2); r_new row y-5 (RX)
+            const double v = s2[J2];
+            const double L = __shfl_up_sync(FULL, v, 1), R = __shfl_down_sync(FULL, v, 1);
+            const double d2v = fma(-dg5, v, (s2[J] + s2[J1]) + (L + R));
+            double mix = 0.0;
+#pragma unroll
+            for (int d = 0; d < K; ++d) mix = fma(Mrow[d], d == c ? un[J2] : xr(UX, yc, d), mix);
+            uc = un[J2];
+            rc = xr(RX, yc, c);
+            w = fma(h5, mix, tau_c * fma(kappa2, uc, d2v));
+          }
+          const bool inc = yc >= C.ys && yc < C.ye;
+          if (outc && inc) {
+            prr = fma(rc, rc, prr);
+            if (PREC) pru = fma(rc, uc, pru);
+            pwu = fma(w, uc, pwu);
+          }
+          // the 16-row block of yc ends (or the segment does): flush this plane's partials
+          if (inc && (((yc + 1) % PB) == 0 || yc == C.ye - 1)) {
+            const double sr = warp_sum(prr), sw = warp_sum(pwu), su = PREC ? warp_sum(pru) : 0.0;
+            if (lane == 0) {
+              double* o = part + (size_t)(yc / PB) * nstrips * K * NP;
+              o[0] = sr;
+              if (PREC) { o[1] = su; o[2] = sw; }
+              else o[1] = sw;
+            }
+            prr = 0.0; pru = 0.0; pwu = 0.0;
+          }
+        }
+        // shift the per-row values
+        f5 = f4; f4 = f3; f3 = f2; f2 = f1; f1 = f0;
+        dg5 = dg4; dg4 = dg3; dg3 = dg2; dg2 = dg1; dg1 = dg0;
+        if (HITS) { h5 = h4; h4 = h3; h3 = h2; h2 = h1; h1 = h0; }
+        // Group barrier: the shared rows of this step are written, stage y-2 is read by every warp.
+        // (A barrier every other step -- enough for the read distances without block-Jacobi --
+        // measured 5% slower: the issuing warp then refills two stages at once.)
+        gsync();
+        if (issuer && q >= q0 + 2) free_stage();
+      };
+      for (int t = 0; t < C.nsteps; t += 3) {
+        step(std::integral_constant<int, 0>{}, t);
+        step(std::integral_constant<int, 1>{}, t + 1);
+        step(std::integral_constant<int, 2>{}, t + 2);
+      }
+      gsync();  // every warp is done with the unit's stages
+      if (issuer)
+        while (gf < q0 + C.nsteps) free_stage();  // the unit's last held stages
+      gsync();  // uq of the next unit is published
+      cu = uq[g][++ku & 3];
+    }
+    __syncwarp();
+
+    iteration_reduce<NT, NP, false>(a, st, act, nact, par_out, it, rs, cta, ncta, gepoch, [&]() {
+      if (cta == 0) *ctr = 0u;  // quiescent now; next used two passes later
+    });
+    if (cta == 0 && tid == 0 && it >= 0 && it < a.history_cap) {
+      double m = 0.0;
+      for (int ii = 0; ii < nact; ++ii) m = fmax(m, st[act[ii]].rel);
+      a.history[it] = m;
+    }
+    ++it;
+  }
+  if (cta == 0)
+    for (int s = tid; s < a.n_sys; s += NT) a.state_out[s] = st[s];
+}
+
+}  // namespace kcg

@@ -28,6 +28,7 @@ __global__ void __launch_bounds__(256, 1) cg_resident_kernel(const CgArgs a, dou
   const int BW = side + 2, BH = RS + 4;
   const int cta = blockIdx.x, ncta = gridDim.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int s = cta / nstrip, strip = cta - s * nstrip, y0 = strip * RS;
+  const int lside = 31 - __clz(side);  // side = 2^L
   const bool gmode = nstrip > 1;
   const size_t N = (size_t)side * side, ps = (size_t)pitch * side;
   const int BOX = BH * BW, UBOX = (RS + 2) * BW;
@@ -40,6 +41,7 @@ __global__ void __launch_bounds__(256, 1) cg_resident_kernel(const CgArgs a, dou
   double* Xb = Ub + (PREC ? K * UBOX : 0);  // [K][RS][side]: x
   double* Hb = Xb + K * RS * side;         // [BH][BW]: hits (HITS)
   SysState* st = reinterpret_cast<SysState*>(Hb + (HITS ? BOX : 0));  // [n_sys]
+  double* Pq = reinterpret_cast<double*>(st + a.n_sys);  // grid mode: every CTA's partials [ncta][3]
   __shared__ double Msh[K * K + K + 4 * K * K];
   __shared__ double red[3][NW];
   cg::grid_group grid = cg::this_grid();
@@ -86,8 +88,16 @@ __global__ void __launch_bounds__(256, 1) cg_resident_kernel(const CgArgs a, dou
     hi = min(b1, side - y0 + 2);
   };
 
+  // KCG_TRACE builds: per pass q, [0] CTA 0 start, [1..3] after phases A, B, C (+ halo publish),
+  // [4] after the grid barrier, [5] after the reduction, [6 + b] CTA b at the barrier
+  const bool trc = KCG_TRACE == 1 && a.trace != nullptr;
+  auto stamp = [&](int q, int col) {
+    if (trc && q < KCG_TRACE_ITERS && tid == 0 && (cta == 0 || col >= 6) && col < KCG_TRACE_COLS)
+      a.trace[(size_t)q * KCG_TRACE_COLS + col] = globaltimer();
+  };
   for (int it = -1;; ++it) {
     const int q = it + 1;  // pass number; writes ping-pong buffer (q + 1) & 1
+    stamp(q, 0);
     const SysState z = st[s];
     double v[3] = {0.0, 0.0, 0.0};  // (r, r), (r, u), (w, u)
     if (z.status == ST_RUNNING) {
@@ -109,6 +119,7 @@ __global__ void __launch_bounds__(256, 1) cg_resident_kernel(const CgArgs a, dou
         for (int c = 0; c < K; ++c) Pb[c * BOX + o] = fma(beta, Pb[c * BOX + o], u[c]);
       }
       __syncthreads();
+      stamp(q, 1);
       // Phase B: q = G p, r -= alpha q on strip + 1 row
       rows_in(1, BH - 1, lo, hi);
       for (int e = tid; e < (hi - lo) * side; e += NT) {
@@ -129,6 +140,7 @@ __global__ void __launch_bounds__(256, 1) cg_resident_kernel(const CgArgs a, dou
         }
       }
       __syncthreads();
+      stamp(q, 2);
       if (PREC) {  // Phase B': u = K^{-1} r_new on strip + 1 row (U row = box row - 1)
         for (int e = tid; e < (hi - lo) * side; e += NT) {
           const int by = lo + e / side, gx = e - (e / side) * side;
@@ -198,8 +210,10 @@ __global__ void __launch_bounds__(256, 1) cg_resident_kernel(const CgArgs a, dou
         for (int w = 0; w < NW; ++w) acc += red[tid][w];
         part[((size_t)(q & 1) * ncta + cta) * 3 + tid] = acc;
       }
-      __threadfence();
+      stamp(q, 3);  // (grid.sync orders the halo / partial stores of every thread before it)
+      stamp(q, 6 + cta);
       grid.sync();
+      stamp(q, 4);
       // The next pass's halo rows (box rows 0, 1, RS + 2, RS + 3 of r and p, written by the
       // neighbouring strips this pass) are loaded into registers in batches of HC per thread, their
       // L2 latency overlapped with the reduction below; element e = ((f K + c) 4 + row) side + x.
@@ -209,7 +223,7 @@ __global__ void __launch_bounds__(256, 1) cg_resident_kernel(const CgArgs a, dou
       const double* rg = (q & 1) ? a.rbuf[0] : a.rbuf[1];
       const double* pg = (q & 1) ? a.pbuf[0] : a.pbuf[1];
       auto decode = [&](int e, int& so, size_t& go) {  // false: outside the face (stays 0)
-        const int gx = e % side, t4 = e / side, hr = t4 & 3, fc = t4 >> 2, c = fc % K, f = fc / K;
+        const int gx = e & (side - 1), t4 = e >> lside, hr = t4 & 3, fc = t4 >> 2, c = fc % K, f = fc / K;
         const int by = hr < 2 ? hr : RS + hr, gy = y0 - 2 + by;
         so = (f * K + c) * BOX + by * BW + gx + 1;  // Pb = Rb + K * BOX
         go = (size_t)(s * K + c) * ps + (size_t)gy * pitch + gx;
@@ -223,16 +237,32 @@ __global__ void __launch_bounds__(256, 1) cg_resident_kernel(const CgArgs a, dou
         size_t go;
         hv[j] = (e < nh && decode(e, so, go)) ? __ldcg(((e / (4 * side * K)) ? pg : rg) + go) : 0.0;
       }
-      // every CTA: every system's sums over its strips in strip order, then the CG scalar update
+      // every CTA: every system's sums over its strips in strip order, then the CG scalar update.
+      // All partials come in ONE round of loads (batches of PC per thread) into shared memory.
       const double* pq = part + (size_t)(q & 1) * ncta * 3;
+      constexpr int PC = 12;
+      for (int e0 = 0; e0 < ncta * 3; e0 += PC * NT) {
+        double pv[PC];
+#pragma unroll
+        for (int j = 0; j < PC; ++j) {
+          const int e = e0 + j * NT + tid;
+          pv[j] = e < ncta * 3 ? __ldcg(pq + e) : 0.0;
+        }
+#pragma unroll
+        for (int j = 0; j < PC; ++j) {
+          const int e = e0 + j * NT + tid;
+          if (e < ncta * 3) Pq[e] = pv[j];
+        }
+      }
+      __syncthreads();
       for (int t = warp; t < a.n_sys; t += NW) {
         if (st[t].status != ST_RUNNING) continue;
         double w0 = 0.0, w1 = 0.0, w2 = 0.0;
         for (int b = lane; b < nstrip; b += 32) {
-          const double* p3 = pq + ((size_t)t * nstrip + b) * 3;
-          w0 += __ldcg(p3);
-          w1 += __ldcg(p3 + 1);
-          w2 += __ldcg(p3 + 2);
+          const double* p3 = Pq + ((size_t)t * nstrip + b) * 3;
+          w0 += p3[0];
+          w1 += p3[1];
+          w2 += p3[2];
         }
         w0 = warp_sum(w0);
         w1 = warp_sum(w1);
@@ -263,6 +293,7 @@ __global__ void __launch_bounds__(256, 1) cg_resident_kernel(const CgArgs a, dou
         }
       }
       __syncthreads();
+      stamp(q, 5);
       bool done = true;  // every thread reads the same states: uniform
       double m = 0.0;
       for (int t = 0; t < a.n_sys; ++t) {
@@ -299,7 +330,7 @@ __global__ void __launch_bounds__(256, 1) cg_resident_kernel(const CgArgs a, dou
 __host__ __device__ constexpr size_t res_smem_bytes(int K, int RS, int side, bool hits, bool prec, int n_sys) {
   return 8 * ((size_t)2 * K * (RS + 4) * (side + 2) + (prec ? (size_t)K * (RS + 2) * (side + 2) : 0) +
               (size_t)K * RS * side + (hits ? (size_t)(RS + 4) * (side + 2) : 0)) +
-         (size_t)n_sys * sizeof(SysState);
+         (size_t)n_sys * sizeof(SysState) + (RS < side ? (size_t)n_sys * (side / RS) * 3 * 8 : 0);
 }
 
 template <int K>

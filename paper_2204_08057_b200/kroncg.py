@@ -27,7 +27,7 @@ _lib = C.CDLL(LIB_PATH)
 
 # status codes (kcg_status)
 KCG_OK, KCG_NOT_CONVERGED, KCG_E_ARG, KCG_E_SHAPE, KCG_E_CONFIG = 0, 1, 2, 3, 4
-KCG_E_NONFINITE, KCG_E_BREAKDOWN, KCG_E_CUDA, KCG_E_NCCL, KCG_E_STATE = 5, 6, 7, 8, 9
+KCG_E_NONFINITE, KCG_E_BREAKDOWN, KCG_E_CUDA, KCG_E_STATE = 5, 6, 7, 9
 KCG_PRIOR_LAPLACIAN, KCG_PRIOR_D2 = 0, 1
 KCG_LAYOUT_ROW_MAJOR, KCG_LAYOUT_NESTED = 0, 1
 KCG_PRECOND_NONE, KCG_PRECOND_BLOCK_JACOBI = 0, 1

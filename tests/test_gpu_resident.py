@@ -24,8 +24,18 @@ def _streaming_ctx(ps, **kw):
         del os.environ["KCG_RESIDENT"]
 
 
+def _strips_ctx(ps, **kw):
+    """The row-strip (grid-barrier) mode is opt-in (KCG_RESIDENT=2): slower than streaming at the
+    sizes measured, kept as a tested experiment."""
+    os.environ["KCG_RESIDENT"] = "2"
+    try:
+        return make_ctx(ps, **kw)
+    finally:
+        del os.environ["KCG_RESIDENT"]
+
+
 def _check(ps, precond=None, expect_strips=None):
-    ctx, Y = make_ctx(ps, precond=precond or "none")
+    ctx, Y = _strips_ctx(ps, precond=precond or "none")
     cfg = ctx.launch_config()
     assert cfg["resident_kron"] > 0, cfg
     if expect_strips is not None:
@@ -33,23 +43,32 @@ def _check(ps, precond=None, expect_strips=None):
     mu, rep = ctx.solve(Y, tol=TOL)
     mu = mu.cpu().numpy()
     assert rep["converged"], rep["status_name"]
+    width = []
     for i, p in enumerate(ps):
         G, b = model.problem_system(p)
         K = cg.block_jacobi_precond(p.level, p.A, p.noise_prec, p.tau, p.kappa2, p.hits) if precond else None
         lo, hi, ref = oracle_count_envelope(cg.cg_hs, G, b, tol=TOL, precond=K)
         assert rel(mu[i], ref.x) <= 1e-8, (i, rel(mu[i], ref.x))
         assert lo - 2 <= rep["iterations_per"][i] <= hi + 2, (i, rep["iterations_per"][i], lo, hi)
+        width.append(hi - lo)
     assert rep["rel_residual_true"] <= 5 * TOL
     # the streaming kernel: same iteration
     c2, _ = _streaming_ctx(ps, precond=precond or "none")
     assert c2.launch_config()["resident_kron"] == 0
     mu2, rep2 = c2.solve(Y, tol=TOL)
     assert rel(mu, mu2.cpu().numpy()) <= 1e-8
-    assert all(abs(a - b) <= 1 for a, b in zip(rep["iterations_per"], rep2["iterations_per"]))
+    # the two kernels sum the partials in different orders, so their counts differ like the oracle's
+    # own count under a 2^-50 perturbation of b (reading R34): +-2 beyond that envelope's width
+    its, its2 = rep["iterations_per"], rep2["iterations_per"]
+    assert all(abs(a - b) <= 2 + w for a, b, w in zip(its, its2, width)), (its, its2, width)
     return ctx, Y, mu, rep
 
 
 def test_resident_tiny_single_cta():
+    ctx, _ = make_ctx(make_config("tiny"))
+    assert ctx.launch_config()["resident_kron"] == 1  # the default planner picks the single-CTA mode
+    c2, _ = make_ctx(make_config("medium"))
+    assert c2.launch_config()["resident_kron"] == 0   # and keeps medium on the streaming kernel
     _, _, mu, _ = _check(make_config("tiny"), expect_strips=1)
     assert rel(mu[0], exact.problem_dct_exact(make_config("tiny")[0])) <= 1e-8
 
@@ -74,7 +93,7 @@ def test_resident_block_jacobi(level, k, hits):
 
 def test_resident_sylvester_and_kohler_medium():
     ps = make_config("medium")
-    ctx, Y = make_ctx(ps)
+    ctx, Y = _strips_ctx(ps)
     cfg = ctx.launch_config()
     assert cfg["resident_syl"] > 0 and cfg["resident_kohler"] > 0, cfg
     mu, rep = ctx.sylvester(Y, tol=TOL)
@@ -111,7 +130,7 @@ def test_resident_zero_rhs_max_iter_nonfinite_and_determinism():
     from paper_2204_08057_b200.kroncg import KcgError
     for level in (4, 7):  # single-CTA and strip modes
         ps = [make_patch(level, 9, 3, seed=1)]
-        ctx, Y = make_ctx(ps)
+        ctx, Y = _strips_ctx(ps)
         assert ctx.launch_config()["resident_kron"] > 0
         mu, rep = ctx.solve(torch.zeros_like(Y), tol=TOL)
         assert rep["iterations"] == 0 and rep["converged"] and not mu.any()
