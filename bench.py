@@ -573,6 +573,9 @@ def run_b200(args):
     world, rank, local = _dist()
     if args.gpus != world and world > 1:
         print(f"warning: --gpus {args.gpus} but WORLD_SIZE {world}", file=sys.stderr)
+    # more ranks than GPUs (the multi-process test of the face-shard path, KCG_BENCH_BACKEND=gloo):
+    # ranks share devices round-robin; nothing on this path waits on another rank's kernels
+    local = local % max(1, torch.cuda.device_count())
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     backend = os.environ.get("KCG_BENCH_BACKEND", "nccl")

@@ -270,6 +270,15 @@ KCG_API kcg_status kcg_ipc_import(const unsigned char handle[64], size_t offset,
 KCG_API kcg_status kcg_ipc_close(void* base);
 
 /* Release host-side state.  Does not free the caller's workspace. */
+/* Row-slab plumbing check (diagnostic; no kernel waits on another rank, so several ranks may share
+ * one GPU): kcg_slab_probe_put stores value + rank into slot [rank] of every rank's workspace
+ * (peer stores through the kcg_ipc_import mappings) and synchronises the stream; after a host-side
+ * barrier of all ranks, kcg_slab_probe_get copies this process's first local rank's nranks slots
+ * to out_host (double[nranks]).  KCG_E_STATE on a non-slab context.  The slots are scratch of the
+ * true-residual sum: call between solves only.                                                  */
+KCG_API kcg_status kcg_slab_probe_put(kcg_ctx* ctx, double value);
+KCG_API kcg_status kcg_slab_probe_get(kcg_ctx* ctx, double* out_host);
+
 KCG_API void kron_cg_destroy(kcg_ctx* ctx);
 
 #ifdef __cplusplus

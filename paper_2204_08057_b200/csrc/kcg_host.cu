@@ -1754,6 +1754,36 @@ KCG_API int kcg_debug_config(const kcg_ctx* c, long long* out) {
   return 8;
 }
 
+// Row-slab plumbing check without any waiting kernel (safe with several ranks on one GPU): each
+// local rank stores value + rank into slot [rank] of EVERY rank's rslots area (peer stores through
+// the IPC-mapped workspaces), then -- after the caller's host barrier -- kcg_slab_probe_get copies
+// this process's first local rank's slots [0, nranks) to the host.
+kcg_status kcg_slab_probe_put(kcg_ctx* c, double value) {
+  if (!c || !c->slab) return KCG_E_STATE;
+  cudaStream_t s = c->stream;
+  std::vector<double> v(c->nlocal);
+  for (int j = 0; j < c->nlocal; ++j) {
+    RankState& R = c->R[j];
+    v[j] = value + R.rank;
+    CK(cudaMemcpyAsync(R.resid_out, &v[j], 8, cudaMemcpyHostToDevice, s), "H2D");
+    kcg::XrankPut Pt{};
+    for (int g = 0; g < c->nranks; ++g) Pt.dst[g] = peer_ptr<double>(c, g, c->L.rslots);
+    Pt.src = R.resid_out;
+    Pt.count = 1;
+    Pt.rank = R.rank;
+    Pt.nranks = c->nranks;
+    CKL(kcg::launch_put(s, Pt), "put kernel");
+  }
+  CK(cudaStreamSynchronize(s), "probe sync");
+  return KCG_OK;
+}
+
+kcg_status kcg_slab_probe_get(kcg_ctx* c, double* out_host) {
+  if (!c || !c->slab || !out_host) return KCG_E_STATE;
+  CK(cudaMemcpy(out_host, c->R[0].rslots, (size_t)c->nranks * 8, cudaMemcpyDeviceToHost), "D2H");
+  return KCG_OK;
+}
+
 // Diagnostic (not part of the ABI header): copy the phase trace of the last solve (KCG_TRACE builds).
 KCG_API int kcg_debug_trace(kcg_ctx* c, long long* out, int max_iters) {
   if (!c || !c->R[0].trace || !out) return 0;

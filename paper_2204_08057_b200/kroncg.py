@@ -97,6 +97,8 @@ kron_cg_create_slab = _sig("kron_cg_create_slab", C.c_int,
 kcg_ipc_export = _sig("kcg_ipc_export", C.c_int, [_vp, C.c_char_p, C.POINTER(C.c_size_t)])
 kcg_ipc_import = _sig("kcg_ipc_import", C.c_int, [C.c_char_p, C.c_size_t, C.POINTER(_vp), C.POINTER(_vp)])
 kcg_ipc_close = _sig("kcg_ipc_close", C.c_int, [_vp])
+kcg_slab_probe_put = _sig("kcg_slab_probe_put", C.c_int, [_ctxp, C.c_double])
+kcg_slab_probe_get = _sig("kcg_slab_probe_get", C.c_int, [_ctxp, C.POINTER(C.c_double)])
 kcg_status_string = _sig("kcg_status_string", C.c_char_p, [C.c_int])
 kron_cg_destroy = _sig("kron_cg_destroy", None, [_ctxp])
 
@@ -104,7 +106,7 @@ EXPORTS = ["kron_cg_workspace_size", "kron_cg_create", "kron_cg_solve", "sylvest
            "kron_cg_solve_host", "sylvester_solve_host", "kron_cg_apply", "kron_cg_rhs",
            "sylvester_factor", "kcg_last_error", "kcg_status_string", "kron_cg_destroy",
            "kron_cg_workspace_size_slab", "kron_cg_create_slab", "kcg_ipc_export", "kcg_ipc_import",
-           "kcg_ipc_close", "sylvester_lanczos_solve", "sylvester_lanczos_solve_host",
+           "kcg_ipc_close", "kcg_slab_probe_put", "kcg_slab_probe_get", "sylvester_lanczos_solve", "sylvester_lanczos_solve_host",
            "kron_cg_solve_b", "posterior_variance", "sylvester_kohler_solve", "kron_cg_solve_host_many"]
 
 
@@ -547,6 +549,20 @@ class KronCGSlab(KronCG):
         if not emulate:
             import torch.distributed as dist
             dist.barrier(group)  # every rank's context (zeroed flags, ghost rows) exists before solves
+
+    def probe_put(self, value: float):
+        """Diagnostic: peer-store value + rank into every rank's probe slot (kcg_slab_probe_put)."""
+        st = kcg_slab_probe_put(self._ctx, float(value))
+        if st != KCG_OK:
+            raise self._err(st)
+
+    def probe_get(self) -> list:
+        """Diagnostic: this process's probe slots of all ranks (kcg_slab_probe_get)."""
+        out = (C.c_double * self.nranks)()
+        st = kcg_slab_probe_get(self._ctx, out)
+        if st != KCG_OK:
+            raise self._err(st)
+        return list(out)
 
     def close(self):
         super().close()
