@@ -285,21 +285,6 @@ __device__ __forceinline__ void spin_geq_u32(const unsigned* p, unsigned target)
   while (ld_acquire_gpu_u32(p) < target)
     if (clock64() - t0 > (1LL << 34)) __trap();
 }
-// Barrier over the ncta CTAs of one group: generation `epoch` (1, 2, ...) completes when the counter
-// reaches epoch * ncta.
-// The fence is system scope: it also publishes (cumulatively, after the CTA barrier) the CTA's
-// peer stores of ghost rows before the rank's CTA 0 raises its cross-rank flag.
-__device__ __forceinline__ void group_sync(unsigned* ctr, int ncta, unsigned epoch) {
-  __syncwarp();
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    __threadfence_system();
-    atomicAdd(ctr, 1u);
-    spin_geq_u32(ctr, epoch * (unsigned)ncta);
-    __threadfence();
-  }
-  __syncthreads();
-}
 __device__ __forceinline__ unsigned long long ld_relaxed_sys_u64(const unsigned long long* p) {
   unsigned long long v;
   asm volatile("ld.relaxed.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
@@ -316,11 +301,19 @@ __device__ __forceinline__ void xrank_signal(const CgArgs& a, unsigned long long
   __threadfence_system();
   for (int q = 0; q < a.nranks; ++q) st_relaxed_sys_u64(a.flags[q] + a.rank, tag);
 }
+// The G flags are loaded together each round (one memory round trip per poll, not G).
 __device__ __forceinline__ void xrank_wait(const CgArgs& a, unsigned long long tag) {
   const long long t0 = clock64();
-  for (int q = 0; q < a.nranks; ++q)
-    while (ld_relaxed_sys_u64(a.my_flags + q) < tag)
-      if (clock64() - t0 > (1LL << 34)) __trap();
+  while (true) {
+    unsigned long long f[KCG_GMAX];
+#pragma unroll
+    for (int q = 0; q < KCG_GMAX; ++q) f[q] = q < a.nranks ? ld_relaxed_sys_u64(a.my_flags + q) : tag;
+    bool ok = true;
+#pragma unroll
+    for (int q = 0; q < KCG_GMAX; ++q) ok &= f[q] >= tag;
+    if (ok) break;
+    if (clock64() - t0 > (1LL << 34)) __trap();
+  }
   __threadfence_system();
 }
 
@@ -328,11 +321,11 @@ __device__ __forceinline__ void xrank_wait(const CgArgs& a, unsigned long long t
 //  REDUNDANT  (nact <= KCG_RB and nact*tps <= KCG_RED_MAX): one grid barrier, then every CTA reduces
 //             every active system itself -- no second barrier, no state broadcast.
 //  DISTRIBUTED grid barrier; CTA b reduces systems b, b+grid, ...; second grid barrier; pull.
-//  SLAB       (row-slab decomposition, the exchange step of SURVEY 8(e)): group barrier of the
-//             rank's CTAs; its CTA 0 reduces every active system over the rank's tiles (canonical
-//             order) and stores the sums into slot [par][s][rank] of EVERY rank (peer stores), then
-//             releases its flag on every rank; every CTA acquires all ranks' flags and adds the
-//             ranks' sums in rank order (the same on every rank) before the scalar update.
+//  SLAB       (row-slab decomposition, the exchange step of SURVEY 8(e)): the rank's last-arriving
+//             CTA reduces every active system over the rank's tiles (canonical order) and stores
+//             the sums into slot [par][s][rank] of EVERY rank (peer stores), then releases its flag
+//             on every rank; every CTA acquires all ranks' flags (one poll round trip for all G) and
+//             adds the ranks' sums in rank order (the same on every rank) before the scalar update.
 // `after_count` runs on thread 0 once every CTA's stores of the pass are visible (the speculative
 // TMA of the next pass).
 template <int NT, int NP, bool SLAB, typename F>
@@ -344,8 +337,21 @@ __device__ __forceinline__ void iteration_reduce(const CgArgs& a, SysState* st, 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int G = a.nranks;
     const unsigned long long tag = a.tag0 + (unsigned long long)(it + 2);
-    group_sync(a.group, ncta, ++gepoch);
-    if (cta == 0) {
+    // The LAST CTA of the rank to arrive reduces (no group barrier: the others go straight to the
+    // cross-rank flags).  Arrival = system fence (publishes the CTA's ghost-row peer stores and tile
+    // partials) + one atomic on the rank's counter; the last arrival acquires every partial.
+    __shared__ int s_last;
+    __syncwarp();
+    __syncthreads();
+    if (tid == 0) {
+      __threadfence_system();
+      const unsigned old = atomicAdd(a.group, 1u);
+      ++gepoch;
+      s_last = old == gepoch * (unsigned)ncta - 1u;
+      if (s_last) __threadfence();
+    }
+    __syncthreads();
+    if (s_last) {
       const int tps = a.tiles_per_sys;
       for (int first = 0; first < nact; first += KCG_RB) {
         const int nb = min(KCG_RB, nact - first);

@@ -61,29 +61,66 @@ def shard_for_rank(costs: Sequence[float], world: int, rank: int) -> List[int]:
 # counts 89-319), ranks are grouped: a group of g ranks splits each of its faces into g row slabs
 # (kron_cg_create_slab) and faces are assigned to groups by LPT.  A single face
 # (planck, stress) is split over all ranks.
-# Modelled per-pass cost of the cross-rank exchange (halo rows + scalar sum), in units of one full
-# face's CG pass (~40 us on a B200 for N = 4^10, k = 4; the exchange is a few us over NVLink).
-SLAB_PASS_OVERHEAD = 0.15
+# Per-pass cost of the cross-rank exchange (halo rows + scalar sum) in units of one full face's CG
+# pass (~40 us on a B200 for N = 4^10, k = 4), MEASURED in the one-launch emulation (planck face,
+# bench.py "slab_emulation" / scripts/probes/slab_probe.py, profiles/r02/slab_probe_r02.txt):
+# +7.9 / +7.4 / +12.5 us per pass for g = 2 / 4 / 8.  Over NVLink add ~1-2 us of link latency.
+SLAB_PASS_OVERHEAD = {2: 0.20, 4: 0.19, 8: 0.31}
+
+
+def _ovh(g: int) -> float:
+    return 0.0 if g == 1 else SLAB_PASS_OVERHEAD.get(g, max(SLAB_PASS_OVERHEAD.values()))
 
 
 def plan_groups(costs: Sequence[float], world: int):
     """Choose the group size g (a power of two dividing world, <= 8) minimising the modelled
-    makespan  max_group(sum cost) / g + SLAB_PASS_OVERHEAD * max_group(max cost) [g > 1]
-    (faces of a group iterate together in one batch; converged faces drop out, so the group's
-    passes = its slowest face's).  Ties -> smaller g.  Returns (g, faces_per_group) with
-    faces_per_group[j] the faces of group j (ranks j*g .. j*g+g-1)."""
+    makespan  max_group(sum cost) / g + overhead(g) * max_group(max cost)  (faces of a group iterate
+    together in one batch; converged faces drop out, so the group's passes = its slowest face's).
+    Ties -> smaller g.  Returns (g, faces_per_group) with faces_per_group[j] the faces of group j
+    (ranks j*g .. j*g+g-1)."""
     best = None
     g = 1
     while g <= min(world, 8):
         if world % g == 0:
             plan = assign_lpt(costs, world // g)
-            t = makespan(costs, plan) / g
-            if g > 1:
-                t += SLAB_PASS_OVERHEAD * max(max(costs[i] for i in part) for part in plan if part)
+            t = uniform_makespan(costs, plan, g)
             if best is None or t < best[0] - 1e-12:
                 best = (t, g, plan)
         g *= 2
     return best[1], best[2]
+
+
+def uniform_makespan(costs: Sequence[float], plan: List[List[int]], g: int) -> float:
+    """Modelled time of a uniform plan: groups of g ranks, faces of group j split g ways."""
+    return max((sum(costs[i] for i in part) / g + _ovh(g) * max(costs[i] for i in part)) if part else 0.0
+               for part in plan)
+
+
+def mixed_plan(costs: Sequence[float], world: int, g: int = 2):
+    """The survey's alternative for more ranks than faces can balance (e.g. 12 faces on 8 GPUs:
+    8 whole faces + 4 faces half-split): every rank runs a whole-face context AND its share of a
+    g-split context (two launches per step).  The s most expensive faces are split (s chosen by
+    the model), the split faces LPT over world/g groups, the whole faces LPT over the ranks on top
+    of the split loads.  Returns (modelled makespan, split faces per group, whole faces per rank)."""
+    best = None
+    order = sorted(range(len(costs)), key=lambda i: (-costs[i], i))
+    for s in range(0, len(costs) + 1):
+        split, whole = order[:s], order[s:]
+        groups = assign_lpt([costs[i] for i in split], world // g) if s else [[] for _ in range(world // g)]
+        groups = [[split[i] for i in grp] for grp in groups]
+        load = []
+        for r in range(world):
+            part = groups[r // g]
+            load.append((sum(costs[i] for i in part) / g + _ovh(g) * max(costs[i] for i in part)) if part else 0.0)
+        per_rank = [[] for _ in range(world)]
+        for i in whole:  # LPT on top of the split loads
+            r = min(range(world), key=lambda j: (load[j], j))
+            per_rank[r].append(i)
+            load[r] += costs[i]
+        t = max(load)
+        if best is None or t < best[0] - 1e-12:
+            best = (t, groups, [sorted(p) for p in per_rank])
+    return best
 
 
 def rank_role(costs: Sequence[float], world: int, rank: int):

@@ -122,6 +122,30 @@ def test_plan_groups_slabs_only_where_faces_cannot_balance():
     assert all(r[3] == plan8[r[1]] for r in roles)
 
 
+def test_mixed_plan_model():
+    """The survey's mixed plan (whole faces + a few split faces per rank) against the uniform group
+    plans under the measured per-pass exchange costs (sharding.SLAB_PASS_OVERHEAD)."""
+    from paper_2204_08057_b200.sharding import assign_lpt, mixed_plan, plan_groups, uniform_makespan
+    rng = np.random.default_rng(1)
+    costs = list(rng.uniform(9, 18, 12))
+    costs[0] = 30.0                                # one slow face (the fullsky face 0 pattern)
+    for world in (2, 4, 8):
+        g, plan = plan_groups(costs, world)
+        tu = uniform_makespan(costs, plan, g)
+        assert tu == min(uniform_makespan(costs, assign_lpt(costs, world // gg), gg)
+                         for gg in (1, 2, 4, 8) if world % gg == 0 and gg <= world)
+        for gm in (2, 4):
+            if world % gm:
+                continue
+            t, groups, whole = mixed_plan(costs, world, gm)
+            faces = sorted([i for grp in groups for i in grp] + [i for w in whole for i in w])
+            assert faces == list(range(12))            # every face exactly once
+            assert t <= uniform_makespan(costs, assign_lpt(costs, world), 1) + 1e-9  # s = 0 is a candidate
+            assert t >= sum(costs) / world - 1e-9      # never below the perfect split
+    t8, groups8, _ = mixed_plan(costs, 8, 4)
+    assert 0 in groups8[0] + groups8[1]                 # the slow face is the one split
+
+
 def _slab_worker(rank, world, port, out):
     """Row-slab single-pass CG on CPU (gloo): each rank holds rows [rank R, (rank+1) R) of x, r, p
     plus 2 ghost rows of r and p per side, exchanged every iteration (send/recv), and the three
