@@ -184,6 +184,15 @@ KCG_API kcg_status sylvester_kohler_solve(kcg_ctx* ctx, const double* Y_dev, dou
 KCG_API kcg_status kron_cg_solve_b(kcg_ctx* ctx, const double* b_dev, double* x_dev, double tol, int max_iter,
                            kcg_report* report);
 
+/* Warm start (reading R37; SURVEY 5 "warm start"): kron_cg_solve from a given initial guess
+ * x0_dev [P][k][N] (user layout; may alias mu_dev) instead of 0 -- r_0 = b - G x_0 (one apply and
+ * one residual pass before the CG kernel), stop on ||r_j|| <= tol ||b|| as usual (||r_0|| when
+ * b = 0); a x_0 that already satisfies the rule returns after 0 iterations.  Kronecker route,
+ * single-pass variant, no row slabs (KCG_E_CONFIG otherwise); the D2 prior, hits, NESTED and
+ * block-Jacobi are supported.                                                                  */
+KCG_API kcg_status kron_cg_solve_x0(kcg_ctx* ctx, const double* Y_dev, const double* x0_dev, double* mu_dev,
+                                    double tol, int max_iter, kcg_report* report);
+
 /* Posterior variances diag(Q^{-1}) = diag(G^{-1}) ("of most importance ... the main
  * diagonal") by Hutchinson's estimator with n_probes Rademacher probes:
  *   var = (1/s) sum_i z_i (.) G^{-1} z_i,   z_i[p][c][j] = +1 or -1 = sign bit of

@@ -31,14 +31,27 @@ class CGResult:
     status: str = "ok"           # ok | not_converged | breakdown | nonfinite
 
 
-def cg_hs(G, b, tol=1e-10, max_iter=10000, precond=None, callback=None) -> CGResult:
-    """Textbook (preconditioned) Hestenes-Stiefel CG, x0 = 0 (Saad Alg. 6.18 / 9.1)."""
+def cg_hs(G, b, tol=1e-10, max_iter=10000, precond=None, callback=None, x0=None) -> CGResult:
+    """Textbook (preconditioned) Hestenes-Stiefel CG (Saad Alg. 6.18 / 9.1), x0 = 0 by default.
+
+    x0 given (warm start, reading R37): Saad's r_0 = b - A x_0; the stopping rule stays
+    ||r_j|| <= tol ||b|| (||r_0|| when b = 0), tested before the first step too (x_0 may already
+    satisfy it: 0 iterations)."""
     b = np.asarray(b, dtype=np.float64)
-    x = np.zeros_like(b)
     bnorm = float(np.sqrt(b @ b))
-    if bnorm == 0.0:
-        return CGResult(x, 0, True, 0.0, [])
-    r = b.copy()
+    if x0 is None:
+        x = np.zeros_like(b)
+        if bnorm == 0.0:
+            return CGResult(x, 0, True, 0.0, [])
+        r = b.copy()
+    else:
+        x = np.array(x0, dtype=np.float64).reshape(b.shape)
+        r = b - G @ x
+        r0 = float(np.sqrt(r @ r))
+        if bnorm == 0.0:
+            bnorm = r0
+        if r0 <= tol * bnorm:
+            return CGResult(x, 0, True, r0 / bnorm if bnorm > 0 else 0.0, [])
     z = r if precond is None else precond(r)
     p = z.copy()
     rz = float(r @ z)

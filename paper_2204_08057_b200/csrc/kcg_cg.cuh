@@ -151,13 +151,18 @@ __global__ void __launch_bounds__(256) rhs_kernel(const double* __restrict__ Y, 
 // w = G u (u = r, ru = rr without a preconditioner).  The start pass (it < 0) gives ||b||^2,
 // gamma_0 = (b,u_0) and alpha_0 = gamma_0/delta_0; afterwards beta = gamma'/gamma,
 // alpha = gamma'/(delta - beta gamma'/alpha); stop on ||r|| <= tol ||b|| (reading R8).
-__device__ __forceinline__ SysState cg_update(SysState z, double rr, double ru, double wu, int it, const CgArgs& a) {
+// Warm start (a.bnorm2 != nullptr, reading R37): the start pass sees r_0 = b - G x_0, so ||b||^2 of
+// system s comes from the host-launched residual kernel (a.bnorm2[2 s + 1]); the stopping rule
+// stays ||r_j|| <= tol ||b|| (||r_0|| when b = 0), and x_0 may already satisfy it (0 iterations).
+__device__ __forceinline__ SysState cg_update(SysState z, double rr, double ru, double wu, int it, const CgArgs& a,
+                                              int s) {
   if (it < 0) {
-    z.bnorm2 = rr;
+    const double b2 = a.bnorm2 ? a.bnorm2[2 * s + 1] : rr;
+    z.bnorm2 = b2 > 0.0 ? b2 : rr;
     z.gamma = ru;
-    z.rel = rr > 0.0 ? 1.0 : 0.0;
+    z.rel = z.bnorm2 > 0.0 ? sqrt(rr / z.bnorm2) : 0.0;
     if (!isfinite(rr) || !isfinite(ru) || !isfinite(wu)) z.status = ST_NONFINITE;
-    else if (rr == 0.0) z.status = ST_CONVERGED;
+    else if (rr == 0.0 || (a.bnorm2 && rr <= a.tol2 * z.bnorm2)) z.status = ST_CONVERGED;
     else if (!(wu > 0.0) || !(ru > 0.0)) z.status = ST_BREAKDOWN;
     else if (a.max_iter <= 0) z.status = ST_MAXIT;
     else { z.alpha = ru / wu; z.beta = 0.0; }
@@ -199,8 +204,8 @@ __device__ __forceinline__ void load_partial(const double* base, int t, double (
 
 // Scalar update from the NP reduced sums (without a preconditioner ru = rr, wu = wr).
 template <int NP>
-__device__ __forceinline__ SysState update_from(SysState z, const double (&v)[3], int it, const CgArgs& a) {
-  return NP == 2 ? cg_update(z, v[0], v[0], v[1], it, a) : cg_update(z, v[0], v[1], v[2], it, a);
+__device__ __forceinline__ SysState update_from(SysState z, const double (&v)[3], int it, const CgArgs& a, int s) {
+  return NP == 2 ? cg_update(z, v[0], v[0], v[1], it, a, s) : cg_update(z, v[0], v[1], v[2], it, a, s);
 }
 
 // The CTA reduces systems act[ii], ii = ii0, ii0 + step, ... and applies the CG scalar update.
@@ -241,7 +246,7 @@ __device__ __forceinline__ void reduce_systems_cta(const CgArgs& a, SysState* st
       for (int w = 0; w < NW; ++w)
 #pragma unroll
         for (int q = 0; q < NP; ++q) v[q] += rs[tid][q][w];
-      const SysState z = update_from<NP>(st[s], v, it, a);
+      const SysState z = update_from<NP>(st[s], v, it, a, s);
       if (to_global) a.state_out[s] = z;
       else st[s] = z;
     }
@@ -399,7 +404,7 @@ __device__ __forceinline__ void iteration_reduce(const CgArgs& a, SysState* st, 
       for (int g = 0; g < G; ++g)
 #pragma unroll
         for (int q = 0; q < NP; ++q) v[q] += __ldcg(src + g * NP + q);
-      st[s] = update_from<NP>(st[s], v, it, a);
+      st[s] = update_from<NP>(st[s], v, it, a, s);
     }
     __syncthreads();
     return;

@@ -11,6 +11,7 @@
 // rank).  Each rank's state lives in its own workspace (RankState); the non-slab context is the
 // one-rank case with no ghost rows.
 #include <cudaTypedefs.h>
+#include <nvtx3/nvToolsExt.h>  // header-only (NVTX3): ranges cost nothing without a profiler attached
 
 #include <algorithm>
 #include <cmath>
@@ -32,6 +33,15 @@ using kcg::SysParams;
 using kcg::SysState;
 
 namespace {
+
+// NVTX range over a host-side scope (the entry points and the phases of a solve), for nsys / ncu
+// timelines: "kcg:<route>" around a call, "kcg:rhs" / "kcg:cg" / "kcg:post" inside.
+struct Nvtx {
+  explicit Nvtx(const char* name) { nvtxRangePushA(name); }
+  ~Nvtx() { nvtxRangePop(); }
+  Nvtx(const Nvtx&) = delete;
+  Nvtx& operator=(const Nvtx&) = delete;
+};
 
 const size_t kAlign = 256;
 size_t align_up(size_t x) { return (x + kAlign - 1) / kAlign * kAlign; }
@@ -584,8 +594,13 @@ kcg_status exchange_x_rows(kcg_ctx* c, const double* x_all, size_t x_rank_stride
 enum InputMode { IN_Y = 0, IN_B_USER = 1, IN_B_WORK = 2 };
 
 kcg_status solve_impl(kcg_ctx* c, Route route, const double* Y_in, double* mu_out, bool host_io, double tol,
-                      int max_iter, kcg_report* rep, InputMode inmode = IN_Y) {
+                      int max_iter, kcg_report* rep, InputMode inmode = IN_Y, const double* x0 = nullptr) {
+  Nvtx nv_(route == ROUTE_KRON ? "kcg:kron_cg_solve" : "kcg:sylvester_solve");
   if (!c) return KCG_E_ARG;
+  if (x0 && (route != ROUTE_KRON || host_io || c->slab || inmode != IN_Y || c->d.cg_variant != KCG_CG_SINGLE_PASS)) {
+    c->err = "warm start: Kronecker route, device buffers, single-pass CG, no row slabs";
+    return KCG_E_CONFIG;
+  }
   if (inmode != IN_Y && (route != ROUTE_KRON || host_io || c->slab)) {
     c->err = "a given right-hand side b needs the Kronecker route, device buffers and no row slabs";
     return KCG_E_CONFIG;
@@ -621,9 +636,20 @@ kcg_status solve_impl(kcg_ctx* c, Route route, const double* Y_in, double* mu_ou
     if (host_io) CK(cudaMemcpyAsync(R.Y_stage, Y_in + j * y_stride, y_stride * 8, cudaMemcpyHostToDevice, s), "H2D Y");
     if (inmode == IN_B_USER && R.y_rm)
       CKL(kcg::launch_permute(s, Y_in, R.y_rm, (size_t)P * k, c->side, false), "permute b");
-    CKL(kcg::launch_rhs(k, s, Yr(j), bgiven ? nullptr : (kron ? R.E_kron : R.E_syl), R.hits, R.r[0], R.p[0], mur(j), P,
-                       nin, gin(R)),
+    // (warm start: x is not zeroed -- x_0 may alias mu; it is copied in below)
+    CKL(kcg::launch_rhs(k, s, Yr(j), bgiven ? nullptr : (kron ? R.E_kron : R.E_syl), R.hits, R.r[0], R.p[0],
+                       x0 ? nullptr : mur(j), P, nin, gin(R)),
        "rhs kernel");
+    if (x0) {  // warm start (reading R37): x = x_0, r_0 = b - G x_0, (||r_0||^2, ||b||^2) per system
+      if (R.x_rm) CKL(kcg::launch_permute(s, x0, R.x_rm, (size_t)P * k, c->side, false), "permute x0");
+      else if (x0 != mur(j)) CK(cudaMemcpyAsync(mur(j), x0, mu_stride * 8, cudaMemcpyDeviceToDevice, s), "D2D x0");
+      CKL(kcg::launch_resid(k, s, R.params_kron, mur(j), Yr(j), R.E_kron, R.hits, R.resid_partials, R.resid_out, P, n,
+                           gin(R), nullptr, nullptr),
+         "residual kernel (x0)");
+      CKL(kcg::launch_apply(k, s, R.params_kron, mur(j), R.r[1], R.hits, P, geom_of(c, R), nullptr, nullptr),
+         "apply kernel (x0)");
+      CKL(kcg::launch_sub_pitched(s, R.r[0], R.r[1], (size_t)P * k, c->side, c->pitch), "r0 = b - G x0");
+    }
   }
   if (c->slab)
     for (int j = 0; j < c->nlocal; ++j) {
@@ -664,6 +690,7 @@ kcg_status solve_impl(kcg_ctx* c, Route route, const double* Y_in, double* mu_ou
     a.tiles_per_sys = a.tiles_x * a.tiles_y * (march ? Kk : 1);  // row-march kernel: partials per plane
     a.max_iter = max_iter;
     a.tol2 = tol * tol;
+    a.bnorm2 = x0 ? R.resid_out : nullptr;
     a.trace = R.trace;
     a.sync = R.sync;
     a.tag0 = tag0;
@@ -828,6 +855,7 @@ kcg_status solve_impl(kcg_ctx* c, Route route, const double* Y_in, double* mu_ou
 // the assembly kernel; then the true residual of G mu = b as for CG.
 kcg_status lanczos_impl(kcg_ctx* c, const double* Y_in, double* mu_out, bool host_io, double tol, int max_iter,
                         kcg_report* rep) {
+  Nvtx nv_("kcg:sylvester_lanczos_solve");
   if (!c) return KCG_E_ARG;
   if (c->L.lz_slots <= 0 || c->slab) {
     c->err = c->slab ? "block-Lanczos route: no row slabs" : "block-Lanczos route needs desc.lanczos_cap > 0";
@@ -955,6 +983,7 @@ kcg_status lanczos_impl(kcg_ctx* c, const double* Y_in, double* mu_out, bool hos
 // column i's right-hand side carrying the Schur coupling to the columns already solved; each column
 // is one batched launch of the CG kernel over the P patches (K = 1 systems, shift R_ii).
 kcg_status kohler_impl(kcg_ctx* c, const double* Y_in, double* mu_out, double tol, int max_iter, kcg_report* rep) {
+  Nvtx nv_("kcg:sylvester_kohler_solve");
   if (!c) return KCG_E_ARG;
   if (c->slab) { c->err = "Alg. Kohler route: no row slabs"; return KCG_E_CONFIG; }
   if (!Y_in || !mu_out) { c->err = "null Y or mu"; return KCG_E_ARG; }
@@ -1126,6 +1155,7 @@ ResPlan plan_resident(int K, int side, int n_sys, bool hits, bool prec, int nsm)
 kcg_status create_impl(const kcg_desc* d, const kcg_slab* sl, const double* A_host, const double* T_host,
                        const double* phi_host, const double* kappa2_host, const double* hits_dev, void* workspace_dev,
                        size_t ws_bytes, void* stream, kcg_ctx** out) {
+  Nvtx nv_("kcg:create");
   if (!out) return KCG_E_ARG;
   *out = nullptr;
   kcg_ctx* c = new kcg_ctx();
@@ -1474,6 +1504,13 @@ kcg_status sylvester_kohler_solve(kcg_ctx* c, const double* Y, double* mu, doubl
   return kohler_impl(c, Y, mu, tol, max_iter, rep);
 }
 
+kcg_status kron_cg_solve_x0(kcg_ctx* c, const double* Y, const double* x0, double* mu, double tol, int max_iter,
+                            kcg_report* rep) {
+  if (c) c->nlaunch = 0;
+  if (c && !x0) { c->err = "null x0"; return KCG_E_ARG; }
+  return solve_impl(c, ROUTE_KRON, Y, mu, false, tol, max_iter, rep, IN_Y, x0);
+}
+
 kcg_status kron_cg_solve_b(kcg_ctx* c, const double* b, double* x, double tol, int max_iter, kcg_report* rep) {
   if (c) c->nlaunch = 0;
   return solve_impl(c, ROUTE_KRON, b, x, false, tol, max_iter, rep, IN_B_USER);
@@ -1481,6 +1518,7 @@ kcg_status kron_cg_solve_b(kcg_ctx* c, const double* b, double* x, double tol, i
 
 kcg_status posterior_variance(kcg_ctx* c, int n_probes, unsigned long long seed, double* var, double* scratch,
                               double tol, int max_iter, kcg_report* rep) {
+  Nvtx nv_("kcg:posterior_variance");
   if (!c) return KCG_E_ARG;
   c->nlaunch = 0;
   if (!var || !scratch) { c->err = "null var or scratch"; return KCG_E_ARG; }
@@ -1543,6 +1581,7 @@ kcg_status sylvester_lanczos_solve_host(kcg_ctx* c, const double* Y, double* mu,
 // context's stream).
 kcg_status kron_cg_solve_host_many(kcg_ctx* c, int nbatch, const double* const* Y_host, double* const* mu_host,
                                    double tol, int max_iter, kcg_report* reports) {
+  Nvtx nv_("kcg:kron_cg_solve_host_many");
   if (!c) return KCG_E_ARG;
   c->nlaunch = 0;
   if (c->slab || c->d.host_staging != 2) {
@@ -1611,6 +1650,7 @@ kcg_status sylvester_solve_host(kcg_ctx* c, const double* Y, double* mu, double 
 }
 
 kcg_status kron_cg_apply(kcg_ctx* c, const double* x, double* y) {
+  Nvtx nv_("kcg:kron_cg_apply");
   if (!c) return KCG_E_ARG;
   if (!x || !y) { c->err = "null x or y"; return KCG_E_ARG; }
   if (x == y) { c->err = "x and y must not alias"; return KCG_E_ARG; }

@@ -157,6 +157,7 @@ struct CgArgs {
                              // buffers above and below (row-slab mode; else side, 0, 0)
   int n_sys, tiles_x, tiles_y, tiles_per_sys;
   int max_iter;
+  const double* bnorm2;      // warm start (reading R37): (||b - G x0||^2, ||b||^2) per system, else nullptr
   int x_tma;                 // 1: CgMaps::x describes `x` (TMA needs side >= 2): staged (K <= 3) or L2-prefetched
   int h_tma;                 // D2 march kernel: 1 = CgMaps::h describes the hits planes (side >= 2)
   int seg;                   // D2 march kernel: rows per work unit (a multiple of KCG_MPB)
@@ -279,6 +280,7 @@ cudaError_t launch_resid(int K, cudaStream_t s, const SysParams* params, const d
 cudaError_t launch_xfix(int K, cudaStream_t s, const SysState* st, const double* p0, const double* p1, double* x,
                         int n_sys, const SlabGeom& g);
 cudaError_t launch_backtransform(int K, cudaStream_t s, const double* W, double* x, int P, size_t N);
+cudaError_t launch_sub_pitched(cudaStream_t s, double* r, const double* v, size_t planes, int side, int pitch);
 cudaError_t launch_ghost_fill(cudaStream_t s, const double* r0, const double* p0, double* up_r, double* up_p,
                               double* dn_r, double* dn_p, int planes, const SlabGeom& g);
 cudaError_t launch_xghost(cudaStream_t s, const double* x, double* up_xg_bot, double* dn_xg_top, int planes,

@@ -377,6 +377,21 @@ cudaError_t launch_resid(int K, cudaStream_t s, const SysParams* params, const d
   return cudaGetLastError();
 }
 
+// r[plane][y pitch + x] -= v[plane][y side + x] (warm start: r_0 = b - G x_0 in the pitched r buffer)
+__global__ void __launch_bounds__(256) sub_pitched_kernel(double* __restrict__ r, const double* __restrict__ v,
+                                                          size_t planes, int side, int pitch) {
+  const size_t N = (size_t)side * side, tot = planes * N;
+  for (size_t e = (size_t)blockIdx.x * blockDim.x + threadIdx.x; e < tot; e += (size_t)gridDim.x * blockDim.x) {
+    const size_t pl = e / N, j = e - pl * N, y = j / side, x = j - y * side;
+    r[pl * pitch * side + y * pitch + x] -= v[e];
+  }
+}
+
+cudaError_t launch_sub_pitched(cudaStream_t s, double* r, const double* v, size_t planes, int side, int pitch) {
+  sub_pitched_kernel<<<grid_for(planes * (size_t)side * side), 256, 0, s>>>(r, v, planes, side, pitch);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_xfix(int K, cudaStream_t s, const SysState* st, const double* p0, const double* p1, double* x,
                         int n_sys, const SlabGeom& g) {
   const size_t N = (size_t)g.rows * g.side;

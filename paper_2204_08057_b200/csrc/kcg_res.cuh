@@ -71,6 +71,9 @@ __global__ void __launch_bounds__(256, 1) cg_resident_kernel(const CgArgs a, dou
       }
   };
   load_rows(Rb, a.rbuf[0], 0, BH);
+  if (a.bnorm2)  // warm start: the strip's x starts at x_0 (a.x holds it), not at 0
+    for (int c = 0; c < K; ++c)
+      for (int e = tid; e < RS * side; e += NT) Xb[c * RS * side + e] = a.x[(s * K + c) * N + (size_t)y0 * side + e];
   if (HITS)
     for (int e = tid; e < BH * side; e += NT) {
       const int by = e / side, gx = e - by * side, gy = y0 - 2 + by;
@@ -267,7 +270,7 @@ __global__ void __launch_bounds__(256, 1) cg_resident_kernel(const CgArgs a, dou
         w0 = warp_sum(w0);
         w1 = warp_sum(w1);
         w2 = warp_sum(w2);
-        if (lane == 0) st[t] = cg_update(st[t], w0, w1, w2, it, a);
+        if (lane == 0) st[t] = cg_update(st[t], w0, w1, w2, it, a, t);
       }
 #pragma unroll
       for (int j = 0; j < HC; ++j) {
@@ -306,7 +309,7 @@ __global__ void __launch_bounds__(256, 1) cg_resident_kernel(const CgArgs a, dou
       if (tid == 0 && z.status == ST_RUNNING) {
         double w0 = 0.0, w1 = 0.0, w2 = 0.0;
         for (int w = 0; w < NW; ++w) { w0 += red[0][w]; w1 += red[1][w]; w2 += red[2][w]; }
-        st[s] = cg_update(st[s], w0, w1, w2, it, a);
+        st[s] = cg_update(st[s], w0, w1, w2, it, a, s);
         if (it >= 0 && it < a.history_cap)  // max over the systems: positive doubles order as integers
           atomicMax(reinterpret_cast<unsigned long long*>(a.history + it), __double_as_longlong(st[s].rel));
       }

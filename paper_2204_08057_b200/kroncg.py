@@ -74,6 +74,7 @@ sylvester_solve_host = _sig("sylvester_solve_host", C.c_int, _solve_args)
 sylvester_lanczos_solve = _sig("sylvester_lanczos_solve", C.c_int, _solve_args)
 sylvester_lanczos_solve_host = _sig("sylvester_lanczos_solve_host", C.c_int, _solve_args)
 kron_cg_solve_b = _sig("kron_cg_solve_b", C.c_int, _solve_args)
+kron_cg_solve_x0 = _sig("kron_cg_solve_x0", C.c_int, [_ctxp, _vp, _vp, _vp, C.c_double, C.c_int, C.POINTER(kcg_report)])
 sylvester_kohler_solve = _sig("sylvester_kohler_solve", C.c_int, _solve_args)
 posterior_variance = _sig("posterior_variance", C.c_int,
                           [_ctxp, C.c_int, C.c_ulonglong, _vp, _vp, C.c_double, C.c_int, C.POINTER(kcg_report)])
@@ -107,7 +108,8 @@ EXPORTS = ["kron_cg_workspace_size", "kron_cg_create", "kron_cg_solve", "sylvest
            "sylvester_factor", "kcg_last_error", "kcg_status_string", "kron_cg_destroy",
            "kron_cg_workspace_size_slab", "kron_cg_create_slab", "kcg_ipc_export", "kcg_ipc_import",
            "kcg_ipc_close", "kcg_slab_probe_put", "kcg_slab_probe_get", "sylvester_lanczos_solve", "sylvester_lanczos_solve_host",
-           "kron_cg_solve_b", "posterior_variance", "sylvester_kohler_solve", "kron_cg_solve_host_many"]
+           "kron_cg_solve_b", "posterior_variance", "sylvester_kohler_solve", "kron_cg_solve_host_many",
+           "kron_cg_solve_x0"]
 
 
 class KcgError(RuntimeError):
@@ -248,12 +250,17 @@ class KronCG:
             raise ValueError(f"{name} must be a C-contiguous host float64 array/tensor of shape {shape}")
 
     # ------------------------------------------------------------------ API
-    def solve(self, Y, mu=None, tol=1e-10, max_iter=100000, **kw):
-        """Kronecker route (kron_cg_solve). Y: CUDA [P][n][side][side] -> (mu, report)."""
+    def solve(self, Y, mu=None, tol=1e-10, max_iter=100000, x0=None, **kw):
+        """Kronecker route (kron_cg_solve). Y: CUDA [P][n][side][side] -> (mu, report).
+        x0: optional warm start [P][k][side][side] (kron_cg_solve_x0; may be mu itself)."""
         self._check_dev(Y, self.shape_Y, "Y")
         mu = self._out(mu)
         self._check_dev(mu, self.shape_mu, "mu")
-        return mu, self._solve(kron_cg_solve, Y, mu, tol, max_iter, self.P, **kw)
+        if x0 is None:
+            return mu, self._solve(kron_cg_solve, Y, mu, tol, max_iter, self.P, **kw)
+        self._check_dev(x0, self.shape_mu, "x0")
+        fn = lambda ctx, y, m, t, mi, rep: kron_cg_solve_x0(ctx, y, _ptr(x0), m, t, mi, rep)
+        return mu, self._solve(fn, Y, mu, tol, max_iter, self.P, **kw)
 
     def sylvester(self, Y, mu=None, tol=1e-10, max_iter=100000, **kw):
         """Sylvester route (sylvester_solve). Y: CUDA [P][n][side][side] -> (mu, report)."""

@@ -177,3 +177,31 @@ def test_cg_d2_prior_small(prior):
     assert res.converged
     assert rel(res.x, exact.problem_dct_exact(p)) <= 1e-8
     assert rel(res.x, exact.dense_solve(G, b)) <= 1e-8
+
+
+def test_warm_start_pins(tiny):
+    """Warm start (reading R37), pinned to the plain definitions: x0 = 0 is the cold start bit for
+    bit; x0 = the dense solution stops before the first step; any x0 reaches the dense solution
+    within the tolerance's reach; CG from x0 on (b) equals CG from 0 on b - G x0 shifted by x0 (the
+    textbook identity behind r_0 = b - G x_0)."""
+    _, G, b = tiny
+    x_star = exact.dense_solve(G, b)
+    cold = cg.cg_hs(G, b, tol=1e-10)
+    zero = cg.cg_hs(G, b, tol=1e-10, x0=np.zeros_like(b))
+    assert zero.iterations == cold.iterations and np.array_equal(zero.x, cold.x)
+    at = cg.cg_hs(G, b, tol=1e-10, x0=x_star)
+    assert at.iterations == 0 and at.converged and np.array_equal(at.x, x_star)
+    rng = np.random.default_rng(3)
+    x0 = x_star + 1e-3 * np.linalg.norm(x_star) / np.sqrt(b.size) * rng.standard_normal(b.size)
+    w = cg.cg_hs(G, b, tol=1e-10, x0=x0)
+    assert w.converged and np.linalg.norm(G @ w.x - b) <= 1.5e-10 * np.linalg.norm(b)
+    assert np.linalg.norm(w.x - x_star) <= 1e-6 * np.linalg.norm(x_star)
+    assert w.iterations < cold.iterations               # a good guess saves steps
+    # shifted system: same iterates up to rounding, same counts (the rule is relative to ||b||)
+    d = b - G @ x0
+    sh = cg.cg_hs(G, d, tol=1e-10 * np.linalg.norm(b) / np.linalg.norm(d))
+    assert abs(sh.iterations - w.iterations) <= 1
+    assert np.linalg.norm((x0 + sh.x) - w.x) <= 1e-9 * np.linalg.norm(x_star)
+    # b = 0: the rule falls back to ||r_0|| and CG drives x0 to the solution 0
+    z = cg.cg_hs(G, np.zeros_like(b), tol=1e-8, x0=x0)
+    assert z.converged and np.linalg.norm(z.x) <= 1e-6 * np.linalg.norm(x0)
