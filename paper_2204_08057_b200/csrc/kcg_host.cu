@@ -91,7 +91,7 @@ Layout layout_of(const kcg_desc* d, int nranks) {
   const size_t P = d->n_patches, n = d->n_freq, k = d->n_comp;
   L.vec_doubles = P * k * (size_t)pitch * (rows + 2 * ghost);
   const bool d2 = d->prior == KCG_PRIOR_D2;
-  const size_t tk = (size_t)tiles_x(side, (int)k, d2) * tiles_y(rows, (int)k, d2) * (d2 ? k : 1);  // (D2: per plane)
+  const size_t tk = (size_t)tiles_x(side, (int)k, d2) * tiles_y(rows, (int)k, d2) * (d2 ? k : 1);  // (D2: <= per plane)
   const size_t ts = (size_t)tiles_x(side, 1, d2) * tiles_y(rows, 1, d2);
   L.partial_doubles = 2 * std::max(P * tk, P * k * ts) * 3;  // [2 parities][systems][tiles][<= 3]
   size_t off = 0;
@@ -687,7 +687,7 @@ kcg_status solve_impl(kcg_ctx* c, Route route, const double* Y_in, double* mu_ou
     a.tiles_x = kron ? c->tiles_x_kron : c->tiles_x_syl;
     a.tiles_y = kron ? c->tiles_y_kron : c->tiles_y_syl;
     const bool march = c->d.prior == KCG_PRIOR_D2 && c->d.cg_variant == KCG_CG_SINGLE_PASS;
-    a.tiles_per_sys = a.tiles_x * a.tiles_y * (march ? Kk : 1);  // row-march kernel: partials per plane
+    a.tiles_per_sys = a.tiles_x * a.tiles_y * (march ? kcg::m_gw(Kk) : 1);  // row-march: partials per group warp
     a.max_iter = max_iter;
     a.tol2 = tol * tol;
     a.bnorm2 = x0 ? R.resid_out : nullptr;

@@ -86,16 +86,23 @@ __host__ __device__ constexpr int d2_ubox_bytes(int K) { return K * (d2_tile_y(K
 #define KCG_MHALO 4
 #define KCG_MCH 1           // rows per TMA stage
 #define KCG_MPB 16          // rows per partial-sum block (fixed reduction order)
-__host__ __device__ constexpr int m_groups(int K) { return K == 1 ? 16 : (K == 2 ? 8 : (K == 3 ? 5 : 4)); }
-__host__ __device__ constexpr int m_threads(int K) { return m_groups(K) * K * 32; }
-__host__ __device__ constexpr int m_stages(int K) { return 8; }
+#ifndef KCG_MKP4
+#define KCG_MKP4 2          // K = 4: component planes per warp (2 warps per group)
+#endif
+__host__ __device__ constexpr int m_kp(int K) { return K == 4 ? KCG_MKP4 : 1; }  // planes per warp
+__host__ __device__ constexpr int m_gw(int K) { return K / m_kp(K); }            // warps per group
+__host__ __device__ constexpr int m_groups(int K) {
+  return K == 1 ? 16 : (K == 2 ? 8 : (K == 3 ? 5 : (m_kp(K) == 1 ? 4 : (m_kp(K) == 2 ? 6 : 8))));
+}
+__host__ __device__ constexpr int m_threads(int K) { return m_groups(K) * m_gw(K) * 32; }
+__host__ __device__ constexpr int m_stages(int K) { return m_kp(K) == 2 ? 4 : 8; }  // (6 groups x 8 stages > smem)
 __host__ __device__ constexpr int m_stage_doubles(int K) { return (3 * K + 1) * 32; }
 // doubles of one group's shared memory: the stage ring + 3 exchange rings [4 rows][K][32]
 __host__ __device__ constexpr int m_group_doubles(int K) { return m_stages(K) * m_stage_doubles(K) + 3 * 4 * K * 32; }
 __host__ __device__ constexpr int m_strips(int side) { return (side + KCG_MOUT - 1) / KCG_MOUT; }
 __host__ __device__ constexpr int m_blocks(int side) { return (side + KCG_MPB - 1) / KCG_MPB; }
-// partial slots per system: strips x 16-row blocks x planes
-__host__ __device__ constexpr int m_slots(int side, int K) { return m_strips(side) * m_blocks(side) * K; }
+// partial slots per system: strips x 16-row blocks x warps of a group
+__host__ __device__ constexpr int m_slots(int side, int K) { return m_strips(side) * m_blocks(side) * m_gw(K); }
 
 // geometry by prior
 __host__ __device__ constexpr int tile_y_of(int K, bool d2) { return d2 ? d2_tile_y(K) : cg_tile_y(K); }

@@ -47,13 +47,14 @@ __device__ __forceinline__ void group_bar(int id, int nthreads) {
 template <int K, bool HITS, bool PREC>
 __global__ void __launch_bounds__(m_threads(K), 1) cg_march_kernel(const CgArgs a, const __grid_constant__ CgMaps maps) {
   constexpr int NG = m_groups(K), NT = m_threads(K), NW = NT / 32, NS = m_stages(K), SD = m_stage_doubles(K);
+  constexpr int KP = m_kp(K), GW = m_gw(K);  // planes per warp, warps per group
   constexpr int XR = 4 * K * 32, GD = m_group_doubles(K);
   constexpr int MO = KCG_MOUT, MH = KCG_MHALO, PB = KCG_MPB;
   constexpr int NP = PREC ? 3 : 2;
   constexpr int DL = PREC ? 5 : 4;  // row of C1 behind the input row
   constexpr int MSZ = K * K + K + (PREC ? 4 * K * K : 0);
   constexpr unsigned FULL = 0xffffffffu;
-  static_assert((NS & (NS - 1)) == 0 && NS >= 4 && KCG_MCH == 1 && (K == 1 || NG <= 15), "geometry");
+  static_assert((NS & (NS - 1)) == 0 && NS >= 4 && KCG_MCH == 1 && (GW == 1 || NG <= 15) && GW * KP == K, "geometry");
 
   extern __shared__ __align__(128) unsigned char smem_raw[];
   SysState* st = reinterpret_cast<SysState*>(smem_raw + (size_t)NG * GD * 8);
@@ -65,8 +66,8 @@ __global__ void __launch_bounds__(m_threads(K), 1) cg_march_kernel(const CgArgs 
   __shared__ int s_nact;
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int g = warp / K, c = warp - g * K;  // group, plane
-  const bool issuer = c == 0;                // the group's TMA / claim warp
+  const int g = warp / GW, wg = warp - g * GW, c0 = wg * KP;  // group, warp in the group, its first plane
+  const bool issuer = wg == 0;                                 // the group's TMA / claim warp
   const int cta = blockIdx.x, ncta = gridDim.x;
   const int side = a.side, pitch = a.pitch, seg = a.seg;
   const int nstrips = a.tiles_x, tps = a.tiles_per_sys;
@@ -78,8 +79,8 @@ __global__ void __launch_bounds__(m_threads(K), 1) cg_march_kernel(const CgArgs 
   double* RX = PX + XR;              // [4][K][32] r_new rows
   double* UX = RX + XR;              // [4][K][32] u_new rows (block-Jacobi)
   auto gsync = [&]() {
-    if constexpr (K == 1) __syncwarp();
-    else group_bar(1 + g, K * 32);
+    if constexpr (GW == 1) __syncwarp();
+    else group_bar(1 + g, GW * 32);
   };
 
   if (tid == 0) {  // the launch must provide the dynamic shared memory this layout assumes
@@ -181,10 +182,13 @@ __global__ void __launch_bounds__(m_threads(K), 1) cg_march_kernel(const CgArgs 
       for (int e = lane; e < MSZ; e += 32)
         Mw[warp][e] = e < K * K ? __ldg(&sp->M[e]) : (e < K * K + K ? __ldg(&sp->tau[e - K * K]) : __ldg(&sp->Kinv[0][0] + (e - K * K - K)));
       __syncwarp();
-      double Mrow[K];  // row c of M
+      double Mrow[KP][K], tau_c[KP];  // rows c0 .. c0+KP-1 of M, their prior scales
 #pragma unroll
-      for (int d = 0; d < K; ++d) Mrow[d] = Mw[warp][c * K + d];
-      const double tau_c = Mw[warp][K * K + c];
+      for (int i = 0; i < KP; ++i) {
+#pragma unroll
+        for (int d = 0; d < K; ++d) Mrow[i][d] = Mw[warp][(c0 + i) * K + d];
+        tau_c[i] = Mw[warp][K * K + c0 + i];
+      }
       const SysState z = st[C.s];
       const double alpha = z.alpha, beta = z.beta, ap = KCG_X2 ? z.alpha_last : 0.0;
       const double kappa2 = __ldg(&sp->kappa2);
@@ -193,28 +197,34 @@ __global__ void __launch_bounds__(m_threads(K), 1) cg_march_kernel(const CgArgs 
       const bool colin = gx >= 0 && gx < side;
       const bool outc = lane >= MH && lane < MH + MO && gx < side;
       const int degx = 4 - (gx == 0) - (gx == side - 1);
-      const size_t pc = ((size_t)C.s * K + c);  // this warp's plane
+      const size_t pc = ((size_t)C.s * K + c0);  // this warp's first plane
       double* rout = (C.par ? a.rbuf[0] : a.rbuf[1]) + pc * ps + gx;  // select, not a dynamic index
       double* pout = (C.par ? a.pbuf[0] : a.pbuf[1]) + pc * ps + gx;
       double* xo = a.x + pc * N + gx;
       const int strip = C.x0 / MO;
-      double* part = a.partials + ((size_t)par_out * a.n_sys + C.s) * tps * NP + ((size_t)strip * K + c) * NP;
-      // the full K x K block-Jacobi solve of a pixel (block-Jacobi): every plane of v, plane c of K^{-1} v
-      auto prec_c = [&](const double (&v)[K], double h, double dg) {
+      double* part = a.partials + ((size_t)par_out * a.n_sys + C.s) * tps * NP + ((size_t)strip * GW + wg) * NP;
+      // the full K x K block-Jacobi solve of a pixel: every plane of v, planes c0.. of K^{-1} v
+      auto prec_w = [&](const double (&v)[K], double h, double dg, double (&uo)[KP]) {
         double u[K];
         double tau[K];
 #pragma unroll
         for (int d = 0; d < K; ++d) tau[d] = Mw[warp][K * K + d];
         precond_pixel<K, HITS>(&Mw[warp][K * K + K], &Mw[warp][0], tau, kappa2, h, (int)dg, v, u, true);
-        double uc = u[0];
 #pragma unroll
-        for (int d = 1; d < K; ++d) uc = d == c ? u[d] : uc;
-        return uc;
+        for (int i = 0; i < KP; ++i) {
+          double ui = u[0];
+#pragma unroll
+          for (int d = 1; d < K; ++d) ui = d == c0 + i ? u[d] : ui;
+          uo[i] = ui;
+        }
       };
 
-      // register rings of this plane (slot of row y = (y - ys + 4) mod 3)
-      double pn[3] = {0.0, 0.0, 0.0}, s1[3] = {0.0, 0.0, 0.0}, rn[3] = {0.0, 0.0, 0.0}, s2[3] = {0.0, 0.0, 0.0};
-      double un[3] = {0.0, 0.0, 0.0};
+      // register rings of this warp's planes (slot of row y = (y - ys + 4) mod 3)
+      double pn[3][KP], s1[3][KP], rn[3][KP], s2[3][KP], un[3][KP];
+#pragma unroll
+      for (int j = 0; j < 3; ++j)
+#pragma unroll
+        for (int i = 0; i < KP; ++i) { pn[j][i] = 0.0; s1[j][i] = 0.0; rn[j][i] = 0.0; s2[j][i] = 0.0; un[j][i] = 0.0; }
       // per-row values of rows y-1 .. y-5, shifted by one every step: in-face flag, degree, hits
       bool f1 = false, f2 = false, f3 = false, f4 = false, f5 = false;
       double dg1 = 0.0, dg2 = 0.0, dg3 = 0.0, dg4 = 0.0, dg5 = 0.0;
@@ -236,103 +246,153 @@ __global__ void __launch_bounds__(m_threads(K), 1) cg_march_kernel(const CgArgs 
         const int slot = q & (NS - 1);
         mbar_wait(&mbar[g][slot], (q / NS) & 1u);
         const double* sg = stg + slot * SD + lane;
-        const double r_c = sg[c * 32], p_c = sg[(K + c) * 32];
-        const double ro_c = stg[((q - 2) & (NS - 1)) * SD + c * 32 + lane];  // r_old of row y - 2
+        const double* sg2 = stg + ((q - 2) & (NS - 1)) * SD + lane;  // row y - 2 (held)
+        double r_c[KP], p_c[KP], ro_c[KP];
+#pragma unroll
+        for (int i = 0; i < KP; ++i) {
+          r_c[i] = sg[(c0 + i) * 32];
+          p_c[i] = sg[(K + c0 + i) * 32];
+          ro_c[i] = sg2[(c0 + i) * 32];
+        }
         const bool f0 = colin && (unsigned)y < (unsigned)side;
         const double dg0 = (double)(degx - (y == 0) - (y == side - 1));
         const bool vA = outc && y >= C.ys && y < C.ye;
-        double xv = 0.0;
-        if (xpass) xv = xl ? sg[(2 * K + c) * 32] : (vA ? __ldcg(xo + (size_t)y * side) : 0.0);
+        double xv[KP];
+#pragma unroll
+        for (int i = 0; i < KP; ++i) xv[i] = 0.0;
+        if (xpass)
+#pragma unroll
+          for (int i = 0; i < KP; ++i)
+            xv[i] = xl ? sg[(2 * K + c0 + i) * 32] : (vA ? __ldcg(xo + i * N + (size_t)y * side) : 0.0);
         double h0 = 1.0;
         if (HITS) h0 = hl ? sg[3 * K * 32] : (f0 ? __ldg(hp + (size_t)y * side + gx) : 1.0);
         // A: p_new(y)
-        double u_c = r_c;
+        double u_c[KP];
+#pragma unroll
+        for (int i = 0; i < KP; ++i) u_c[i] = r_c[i];
         if (PREC) {
           double rv[K];
 #pragma unroll
           for (int d = 0; d < K; ++d) rv[d] = sg[d * 32];
-          u_c = f0 ? prec_c(rv, h0, dg0) : 0.0;
+          if (f0) prec_w(rv, h0, dg0, u_c);
+          else
+#pragma unroll
+            for (int i = 0; i < KP; ++i) u_c[i] = 0.0;
         }
-        pn[J] = fma(beta, p_c, u_c);
-        if (K > 1) PX[((y & 3) * K + c) * 32 + lane] = pn[J];
+#pragma unroll
+        for (int i = 0; i < KP; ++i) {
+          pn[J][i] = fma(beta, p_c[i], u_c[i]);
+          if (GW > 1) PX[((y & 3) * K + c0 + i) * 32 + lane] = pn[J][i];
+        }
         if (vA) {
-          pout[(size_t)y * pitch] = pn[J];
-          if (xpass) xo[(size_t)y * side] = xv + fma(alpha, pn[J], ap * p_c);
+#pragma unroll
+          for (int i = 0; i < KP; ++i) {
+            pout[i * ps + (size_t)y * pitch] = pn[J][i];
+            if (xpass) xo[i * N + (size_t)y * side] = xv[i] + fma(alpha, pn[J][i], ap * p_c[i]);
+          }
         }
         // B0: S1(y-1) = D p_new
-        {
-          const double v = pn[J1];
+#pragma unroll
+        for (int i = 0; i < KP; ++i) {
+          const double v = pn[J1][i];
           const double L = __shfl_up_sync(FULL, v, 1), R = __shfl_down_sync(FULL, v, 1);
-          s1[J1] = f1 ? fma(-dg1, v, (pn[J2] + pn[J]) + (L + R)) : 0.0;
+          s1[J1][i] = f1 ? fma(-dg1, v, (pn[J2][i] + pn[J][i]) + (L + R)) : 0.0;
         }
         // B1: r_new(y-2)
         {
-          const double v = s1[J2];
-          const double L = __shfl_up_sync(FULL, v, 1), R = __shfl_down_sync(FULL, v, 1);
-          const double d2p = fma(-dg2, v, (s1[J] + s1[J1]) + (L + R));
-          double mix = 0.0;
+          double pv[K];  // p_new of row y-2, every plane
 #pragma unroll
-          for (int d = 0; d < K; ++d) mix = fma(Mrow[d], d == c ? pn[J2] : xr(PX, y - 2, d), mix);
-          const double qv = fma(h2, mix, tau_c * fma(kappa2, pn[J2], d2p));
-          rn[J2] = f2 ? fma(-alpha, qv, ro_c) : 0.0;
-          if (K > 1 || PREC) RX[(((y - 2) & 3) * K + c) * 32 + lane] = rn[J2];
+          for (int d = 0; d < K; ++d) pv[d] = GW == 1 ? pn[J2][GW == 1 ? d : 0] : xr(PX, y - 2, d);
           const int y2 = y - 2;
-          if (outc && y2 >= C.ys && y2 < C.ye) rout[(size_t)y2 * pitch] = rn[J2];
+          const bool st2 = outc && y2 >= C.ys && y2 < C.ye;
+#pragma unroll
+          for (int i = 0; i < KP; ++i) {
+            const double v = s1[J2][i];
+            const double L = __shfl_up_sync(FULL, v, 1), R = __shfl_down_sync(FULL, v, 1);
+            const double d2p = fma(-dg2, v, (s1[J][i] + s1[J1][i]) + (L + R));
+            double mix = 0.0;
+#pragma unroll
+            for (int d = 0; d < K; ++d) mix = fma(Mrow[i][d], pv[d], mix);
+            const double qv = fma(h2, mix, tau_c[i] * fma(kappa2, pn[J2][i], d2p));
+            rn[J2][i] = f2 ? fma(-alpha, qv, ro_c[i]) : 0.0;
+            if (GW > 1 || PREC) RX[(((y - 2) & 3) * K + c0 + i) * 32 + lane] = rn[J2][i];
+            if (st2) rout[i * ps + (size_t)y2 * pitch] = rn[J2][i];
+          }
         }
         // B' (block-Jacobi): u_new(y-3) = K^{-1} r_new from the shared r_new row
         if (PREC) {
           double rv[K];
 #pragma unroll
-          for (int d = 0; d < K; ++d) rv[d] = d == c ? rn[J] : xr(RX, y - 3, d);
-          un[J] = f3 ? prec_c(rv, h3, dg3) : 0.0;
-          if (K > 1) UX[(((y - 3) & 3) * K + c) * 32 + lane] = un[J];
+          for (int d = 0; d < K; ++d) rv[d] = GW == 1 ? rn[J][GW == 1 ? d : 0] : xr(RX, y - 3, d);
+          double uo[KP];
+          if (f3) prec_w(rv, h3, dg3, uo);
+          else
+#pragma unroll
+            for (int i = 0; i < KP; ++i) uo[i] = 0.0;
+#pragma unroll
+          for (int i = 0; i < KP; ++i) {
+            un[J][i] = uo[i];
+            if (GW > 1) UX[(((y - 3) & 3) * K + c0 + i) * 32 + lane] = un[J][i];
+          }
         }
         // C0: S2 = D u_new at row y-3 (u = r_new) or y-4 (block-Jacobi)
-        if (!PREC) {
-          const double v = rn[J];
-          const double L = __shfl_up_sync(FULL, v, 1), R = __shfl_down_sync(FULL, v, 1);
-          s2[J] = f3 ? fma(-dg3, v, (rn[J1] + rn[J2]) + (L + R)) : 0.0;
-        } else {  // u_new rows: y-3 -> J, y-4 -> J1, y-5 -> J2; S2 row y-4 -> J1
-          const double v = un[J1];
-          const double L = __shfl_up_sync(FULL, v, 1), R = __shfl_down_sync(FULL, v, 1);
-          s2[J1] = f4 ? fma(-dg4, v, (un[J2] + un[J]) + (L + R)) : 0.0;
+#pragma unroll
+        for (int i = 0; i < KP; ++i) {
+          if (!PREC) {
+            const double v = rn[J][i];
+            const double L = __shfl_up_sync(FULL, v, 1), R = __shfl_down_sync(FULL, v, 1);
+            s2[J][i] = f3 ? fma(-dg3, v, (rn[J1][i] + rn[J2][i]) + (L + R)) : 0.0;
+          } else {  // u_new rows: y-3 -> J, y-4 -> J1, y-5 -> J2; S2 row y-4 -> J1
+            const double v = un[J1][i];
+            const double L = __shfl_up_sync(FULL, v, 1), R = __shfl_down_sync(FULL, v, 1);
+            s2[J1][i] = f4 ? fma(-dg4, v, (un[J2][i] + un[J][i]) + (L + R)) : 0.0;
+          }
         }
         // C1: w at row yc = y - DL and the partials
         {
           const int yc = y - DL;
-          double w, uc, rc;
-          if (!PREC) {  // S2 rows y-5 (J2), y-4 (J1), y-3 (J); u = r_new row y-4 (J1)
-            const double v = s2[J1];
-            const double L = __shfl_up_sync(FULL, v, 1), R = __shfl_down_sync(FULL, v, 1);
-            const double d2v = fma(-dg4, v, (s2[J2] + s2[J]) + (L + R));
-            double mix = 0.0;
+          double uv[K];  // u_new of row yc, every plane
 #pragma unroll
-            for (int d = 0; d < K; ++d) mix = fma(Mrow[d], d == c ? rn[J1] : xr(RX, yc, d), mix);
-            uc = rn[J1];
-            rc = uc;
-            w = fma(h4, mix, tau_c * fma(kappa2, uc, d2v));
-          } else {      // S2 rows y-6 (J), y-5 (J2), y-4 (J1); u_new row y-5 (J2); r_new row y-5 (RX)
-            const double v = s2[J2];
-            const double L = __shfl_up_sync(FULL, v, 1), R = __shfl_down_sync(FULL, v, 1);
-            const double d2v = fma(-dg5, v, (s2[J] + s2[J1]) + (L + R));
-            double mix = 0.0;
+          for (int d = 0; d < K; ++d) {
+            const int i = GW == 1 ? d : 0;  // (GW == 1: every plane is this warp's, c0 = 0)
+            uv[d] = GW == 1 ? (PREC ? un[J2][i] : rn[J1][i]) : xr(PREC ? UX : RX, yc, d);
+          }
+          double lrr = 0.0, lru = 0.0, lwu = 0.0;
 #pragma unroll
-            for (int d = 0; d < K; ++d) mix = fma(Mrow[d], d == c ? un[J2] : xr(UX, yc, d), mix);
-            uc = un[J2];
-            rc = xr(RX, yc, c);
-            w = fma(h5, mix, tau_c * fma(kappa2, uc, d2v));
+          for (int i = 0; i < KP; ++i) {
+            double w, uc, rc;
+            if (!PREC) {  // S2 rows y-5 (J2), y-4 (J1), y-3 (J); u = r_new row y-4 (J1)
+              const double v = s2[J1][i];
+              const double L = __shfl_up_sync(FULL, v, 1), R = __shfl_down_sync(FULL, v, 1);
+              const double d2v = fma(-dg4, v, (s2[J2][i] + s2[J][i]) + (L + R));
+              double mix = 0.0;
+#pragma unroll
+              for (int d = 0; d < K; ++d) mix = fma(Mrow[i][d], uv[d], mix);
+              uc = rn[J1][i];
+              rc = uc;
+              w = fma(h4, mix, tau_c[i] * fma(kappa2, uc, d2v));
+            } else {      // S2 rows y-6 (J), y-5 (J2), y-4 (J1); u_new row y-5 (J2); r_new row y-5 (RX)
+              const double v = s2[J2][i];
+              const double L = __shfl_up_sync(FULL, v, 1), R = __shfl_down_sync(FULL, v, 1);
+              const double d2v = fma(-dg5, v, (s2[J][i] + s2[J1][i]) + (L + R));
+              double mix = 0.0;
+#pragma unroll
+              for (int d = 0; d < K; ++d) mix = fma(Mrow[i][d], uv[d], mix);
+              uc = un[J2][i];
+              rc = xr(RX, yc, c0 + i);
+              w = fma(h5, mix, tau_c[i] * fma(kappa2, uc, d2v));
+            }
+            lrr = fma(rc, rc, lrr);
+            if (PREC) lru = fma(rc, uc, lru);
+            lwu = fma(w, uc, lwu);
           }
           const bool inc = yc >= C.ys && yc < C.ye;
-          if (outc && inc) {
-            prr = fma(rc, rc, prr);
-            if (PREC) pru = fma(rc, uc, pru);
-            pwu = fma(w, uc, pwu);
-          }
-          // the 16-row block of yc ends (or the segment does): flush this plane's partials
+          if (outc && inc) { prr += lrr; pru += lru; pwu += lwu; }
+          // the 16-row block of yc ends (or the segment does): flush this warp's partials
           if (inc && (((yc + 1) % PB) == 0 || yc == C.ye - 1)) {
             const double sr = warp_sum(prr), sw = warp_sum(pwu), su = PREC ? warp_sum(pru) : 0.0;
             if (lane == 0) {
-              double* o = part + (size_t)(yc / PB) * nstrips * K * NP;
+              double* o = part + (size_t)(yc / PB) * nstrips * GW * NP;
               o[0] = sr;
               if (PREC) { o[1] = su; o[2] = sw; }
               else o[1] = sw;
