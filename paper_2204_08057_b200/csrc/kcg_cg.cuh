@@ -518,8 +518,6 @@ struct TileCtx {
   uint32_t phase;
   double* part_out;
   double* dump;       // KCG_TRACE == 2 diagnostic builds: smem snapshots of one tile (else nullptr)
-  double* S;          // D2: scratch box of D p / D r (tile + 3-ring rows, box pitch)
-  double* pold;       // D2: p_old of the tile [K][TY][TX] (X2 x update)
 };
 
 // KCG_TRACE == 2: copy n doubles of shared memory to dst (all threads; barrier after)
@@ -940,26 +938,22 @@ __device__ __forceinline__ void flush_tile_partial(const double (*tred)[NW], dou
 // The persistent CG iteration of one CTA group: `cta` of `ncta` CTAs working on the systems of
 // `a` (the whole grid without slabs; one rank's group in row-slab mode, where the launch may carry
 // several emulated ranks).
-template <int K, bool HITS, bool PREC, bool SLAB, bool D2>
+template <int K, bool HITS, bool PREC, bool SLAB>
 __device__ __forceinline__ void cg_body(const CgArgs& a, const CgMaps& maps, const int cta, const int ncta) {
-  constexpr int TY = tile_y_of(K, D2), TX = KCG_TX, H = halo_of(D2);
+  constexpr int TY = cg_tile_y(K), TX = KCG_TX, H = KCG_HALO;
   constexpr int BW = TX + 2 * H, BH = TY + 2 * H;
   constexpr int FIELD = K * BW * BH;  // doubles of one field box
-  constexpr int XBYTES = D2 ? 0 : cg_xstage_bytes(K);  // x block, TMA-staged with the boxes (0 if disabled)
+  constexpr int XBYTES = cg_xstage_bytes(K);  // x block, TMA-staged with the boxes (0 if disabled)
   constexpr int STAGE_BYTES = 2 * FIELD * 8 + XBYTES;
-  constexpr int UBYTES = PREC ? (D2 ? d2_ubox_bytes(K) : cg_ubox_bytes(K)) : 0;
-  constexpr int EXTRA = D2 ? d2_sbox_bytes(K) + d2_pold_bytes(K) : 0;  // D2 scratch boxes
-  constexpr int NT = threads_of(K, D2), NW = NT / 32, NS = cg_stages(K);
+  constexpr int UBYTES = PREC ? cg_ubox_bytes(K) : 0;
+  constexpr int NT = cg_threads(K), NW = NT / 32, NS = cg_stages(K);
   constexpr int NP = PREC ? 3 : 2;  // partials per tile
   constexpr int MSZ = K * K + K + (PREC ? 4 * K * K : 0);
-  static_assert(D2 || STAGE_BYTES == cg_stage_bytes(K), "stage size");
-  static_assert(!D2 || STAGE_BYTES == d2_stage_bytes(K), "stage size (D2)");
+  static_assert(STAGE_BYTES == cg_stage_bytes(K), "stage size");
 
   extern __shared__ __align__(128) unsigned char smem_raw[];
   double* ubox = reinterpret_cast<double*>(smem_raw + NS * STAGE_BYTES);
-  double* sbox = reinterpret_cast<double*>(smem_raw + NS * STAGE_BYTES + UBYTES);  // D2 only
-  double* pold = reinterpret_cast<double*>(smem_raw + NS * STAGE_BYTES + UBYTES + (D2 ? d2_sbox_bytes(K) : 0));
-  SysState* st = reinterpret_cast<SysState*>(smem_raw + NS * STAGE_BYTES + UBYTES + EXTRA);
+  SysState* st = reinterpret_cast<SysState*>(smem_raw + NS * STAGE_BYTES + UBYTES);
   int* act = reinterpret_cast<int*>(st + a.n_sys);
   __shared__ __align__(8) uint64_t mbar[2];
   __shared__ double tred[2][3][NW];  // per-warp tile partials, double-buffered by tile parity
@@ -974,12 +968,12 @@ __device__ __forceinline__ void cg_body(const CgArgs& a, const CgMaps& maps, con
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int tps = a.tiles_per_sys;
-  const bool xtma = !D2 && cg_xtma(K) && a.x_tma != 0;
+  const bool xtma = cg_xtma(K) && a.x_tma != 0;
 
   if (tid == 0) {  // the launch must provide the dynamic shared memory this layout assumes
     unsigned dyn;
     asm volatile("mov.u32 %0, %%dynamic_smem_size;" : "=r"(dyn));
-    if ((size_t)dyn < (size_t)NS * STAGE_BYTES + UBYTES + EXTRA + (size_t)a.n_sys * (sizeof(SysState) + sizeof(int)))
+    if ((size_t)dyn < (size_t)NS * STAGE_BYTES + UBYTES + (size_t)a.n_sys * (sizeof(SysState) + sizeof(int)))
       __trap();
   }
   for (int s = tid; s < a.n_sys; s += NT) {
@@ -1086,15 +1080,13 @@ __device__ __forceinline__ void cg_body(const CgArgs& a, const CgMaps& maps, con
       else if (tid < K * K + K) Ms[tid] = __ldg(&sp->tau[tid - K * K]);
       else if (PREC && tid < MSZ) Ms[tid] = __ldg(&sp->Kinv[0][0] + (tid - K * K - K));
 #if KCG_PREC_SMEM_A
-      if constexpr (PREC && !D2) __syncthreads();  // phase A of the PCG tile reads the shared copy
+      if constexpr (PREC) __syncthreads();  // phase A of the PCG tile reads the shared copy
 #endif
       TileCtx tc;
       tc.R = reinterpret_cast<double*>(smem_raw + sidx * STAGE_BYTES);
       tc.Pp = tc.R + FIELD;
       tc.xs = tc.R + 2 * FIELD;
       tc.U = ubox;
-      tc.S = sbox;
-      tc.pold = pold;
       tc.Ms = Ms;
       tc.sp = sp;
       tc.s = s;
@@ -1157,17 +1149,17 @@ __device__ __forceinline__ void cg_body(const CgArgs& a, const CgMaps& maps, con
     for (int s = tid; s < a.n_sys; s += NT) a.state_out[s] = st[s];
 }
 
-template <int K, bool HITS, bool PREC, bool D2>
-__global__ void __launch_bounds__(threads_of(K, D2), min_blocks_of(K, D2))
+template <int K, bool HITS, bool PREC>
+__global__ void __launch_bounds__(cg_threads(K), cg_min_blocks(K))
     cg_persistent_kernel(const CgArgs a, const __grid_constant__ CgMaps maps) {
-  cg_body<K, HITS, PREC, false, D2>(a, maps, blockIdx.x, gridDim.x);
+  cg_body<K, HITS, PREC, false>(a, maps, blockIdx.x, gridDim.x);
 }
 
 // Row-slab mode: CTA group r (blocks [r ctas, (r+1) ctas)) runs local rank r of the launch.
 template <int K, bool HITS, bool PREC>
 __global__ void __launch_bounds__(cg_threads(K), cg_min_blocks(K)) cg_slab_kernel(const __grid_constant__ CgSlabLaunch L) {
   const int rl = blockIdx.x / L.ctas;
-  cg_body<K, HITS, PREC, true, false>(L.a[rl], L.m[rl], blockIdx.x - rl * L.ctas, L.ctas);
+  cg_body<K, HITS, PREC, true>(L.a[rl], L.m[rl], blockIdx.x - rl * L.ctas, L.ctas);
 }
 
 
@@ -1186,11 +1178,10 @@ struct CgEntry {
   static cudaError_t launch_slab(bool prec, cudaStream_t s, const CgSlabLaunch& L, size_t smem);
 };
 
-// Dynamic shared memory of one CTA: two stages, the PREC u box, the D2 scratch boxes, the states.
-template <int K, bool PREC, bool D2>
+// Dynamic shared memory of one CTA (Laplacian tile kernel): two stages, the PREC u box (+ the states).
+template <int K, bool PREC>
 constexpr size_t cg_dyn_smem_fixed() {
-  return D2 ? 2 * (size_t)d2_stage_bytes(K) + (PREC ? (size_t)d2_ubox_bytes(K) : 0) + d2_sbox_bytes(K) + d2_pold_bytes(K)
-            : cg_stages(K) * (size_t)cg_stage_bytes(K) + (PREC ? (size_t)cg_ubox_bytes(K) : 0);
+  return cg_stages(K) * (size_t)cg_stage_bytes(K) + (PREC ? (size_t)cg_ubox_bytes(K) : 0);
 }
 
 template <int K, bool HITS, bool PREC>
@@ -1203,8 +1194,8 @@ static cudaError_t cg_config_t(bool slab, bool d2, int n_sys, int* max_grid, siz
     sm += (size_t)m_groups(K) * m_group_doubles(K) * 8;
     nt = m_threads(K);
   } else {
-    kern = slab ? (const void*)cg_slab_kernel<K, HITS, PREC> : (const void*)cg_persistent_kernel<K, HITS, PREC, false>;
-    sm += cg_dyn_smem_fixed<K, PREC, false>();
+    kern = slab ? (const void*)cg_slab_kernel<K, HITS, PREC> : (const void*)cg_persistent_kernel<K, HITS, PREC>;
+    sm += cg_dyn_smem_fixed<K, PREC>();
   }
   if (!kern) return cudaErrorInvalidValue;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
@@ -1247,9 +1238,9 @@ cudaError_t CgEntry<K>::launch(bool prec, bool d2, cudaStream_t s, const CgArgs&
       else f = hits ? (const void*)cg_march_kernel<K, true, false> : (const void*)cg_march_kernel<K, false, false>;
     }
   } else if (prec) {
-    if constexpr (K <= 7) f = hits ? (const void*)cg_persistent_kernel<K, true, true, false> : (const void*)cg_persistent_kernel<K, false, true, false>;
+    if constexpr (K <= 7) f = hits ? (const void*)cg_persistent_kernel<K, true, true> : (const void*)cg_persistent_kernel<K, false, true>;
   } else {
-    f = hits ? (const void*)cg_persistent_kernel<K, true, false, false> : (const void*)cg_persistent_kernel<K, false, false, false>;
+    f = hits ? (const void*)cg_persistent_kernel<K, true, false> : (const void*)cg_persistent_kernel<K, false, false>;
   }
   if (!f) return cudaErrorInvalidValue;
   return cudaLaunchCooperativeKernel(f, dim3(grid), dim3(d2 ? m_threads(K) : cg_threads(K)), args, smem, s);

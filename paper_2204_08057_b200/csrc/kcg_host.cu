@@ -61,7 +61,7 @@ struct Layout {
 // row-march kernel's strips (x) and 16-row partial-sum blocks (y).
 int tiles_x(int side, int K, bool d2 = false) { return d2 ? kcg::m_strips(side) : (side + KCG_TX - 1) / KCG_TX; }
 int tiles_y(int rows, int K, bool d2 = false) {
-  return d2 ? kcg::m_blocks(rows) : (rows + kcg::tile_y_of(K, false) - 1) / kcg::tile_y_of(K, false);
+  return d2 ? kcg::m_blocks(rows) : (rows + kcg::cg_tile_y(K) - 1) / kcg::cg_tile_y(K);
 }
 
 // D2 row-march kernel: rows per work unit (a multiple of the partial block KCG_MPB) minimising the
@@ -452,7 +452,7 @@ bool encode_map(CUtensorMap* m, double* base, int side, int buf_rows, int pitch,
                 std::string* why) {
   // box: the CTA tile + halo, or (D2) one row-march chunk of 32 columns x KCG_MCH rows
   const int bx = d2 ? 32 : KCG_TX + 2 * KCG_HALO;
-  const int by = d2 ? KCG_MCH : kcg::tile_y_of(K, false) + 2 * KCG_HALO;
+  const int by = d2 ? KCG_MCH : kcg::cg_tile_y(K) + 2 * KCG_HALO;
   auto enc = get_encode();
   if (!enc) { *why = "cuTensorMapEncodeTiled unavailable"; return false; }
   cuuint64_t dims[3] = {(cuuint64_t)side, (cuuint64_t)buf_rows, (cuuint64_t)planes};
@@ -477,7 +477,7 @@ bool encode_xmap(CUtensorMap* m, double* base, int side, int rows, size_t planes
   if (!enc) { *why = "cuTensorMapEncodeTiled unavailable"; return false; }
   cuuint64_t dims[3] = {(cuuint64_t)side, (cuuint64_t)rows, (cuuint64_t)planes};
   cuuint64_t strides[2] = {(cuuint64_t)side * 8, (cuuint64_t)side * rows * 8};
-  cuuint32_t box[3] = {(cuuint32_t)(d2 ? 32 : KCG_TX), (cuuint32_t)(d2 ? KCG_MCH : kcg::tile_y_of(K, false)), (cuuint32_t)K};
+  cuuint32_t box[3] = {(cuuint32_t)(d2 ? 32 : KCG_TX), (cuuint32_t)(d2 ? KCG_MCH : kcg::cg_tile_y(K)), (cuuint32_t)K};
   cuuint32_t es[3] = {1, 1, 1};
   CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, base, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
                    CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);

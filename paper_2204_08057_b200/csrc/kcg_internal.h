@@ -68,16 +68,6 @@ __host__ __device__ constexpr int cg_stage_bytes(int K) {
   return 2 * K * (cg_tile_y(K) + 2 * KCG_HALO) * (KCG_TX + 2 * KCG_HALO) * 8 + cg_xstage_bytes(K);
 }
 
-// ---- D2 prior (the paper's phi D^2 + kappa2 I, radius-2 stencil): single-pass recomputation
-// needs a 4-pixel halo.  Generic point loops (tile 64 x TY2, 256 threads), no x staging; scratch
-// boxes for D p (tile + 3-ring), D r / D u (tile + 1-ring) and p_old of the tile (X2).
-#define KCG_HALO2 4
-__host__ __device__ constexpr int d2_tile_y(int K) { return K == 1 ? 16 : 8; }
-__host__ __device__ constexpr int d2_box_w() { return KCG_TX + 2 * KCG_HALO2; }
-__host__ __device__ constexpr int d2_stage_bytes(int K) { return 2 * K * (d2_tile_y(K) + 2 * KCG_HALO2) * d2_box_w() * 8; }
-__host__ __device__ constexpr int d2_sbox_bytes(int K) { return K * (d2_tile_y(K) + 6) * d2_box_w() * 8; }
-__host__ __device__ constexpr int d2_pold_bytes(int K) { return K * d2_tile_y(K) * KCG_TX * 8; }
-__host__ __device__ constexpr int d2_ubox_bytes(int K) { return K * (d2_tile_y(K) + 4) * d2_box_w() * 8; }
 // ---- D2 prior: the row-march CG kernel (kcg_march.cuh).  A GROUP of K warps (warp c = component
 // plane c) marches a strip of KCG_MOUT output columns (32 lanes = the strip + a 4-column halo each
 // side) down a segment of rows; rows of r, p, x, hits are TMA-staged one row per stage into a
@@ -104,11 +94,6 @@ __host__ __device__ constexpr int m_blocks(int side) { return (side + KCG_MPB - 
 // partial slots per system: strips x 16-row blocks x warps of a group
 __host__ __device__ constexpr int m_slots(int side, int K) { return m_strips(side) * m_blocks(side) * m_gw(K); }
 
-// geometry by prior
-__host__ __device__ constexpr int tile_y_of(int K, bool d2) { return d2 ? d2_tile_y(K) : cg_tile_y(K); }
-__host__ __device__ constexpr int halo_of(bool d2) { return d2 ? KCG_HALO2 : KCG_HALO; }
-__host__ __device__ constexpr int threads_of(int K, bool d2) { return d2 ? 256 : cg_threads(K); }
-__host__ __device__ constexpr int min_blocks_of(int K, bool d2) { return d2 ? 1 : cg_min_blocks(K); }
 
 // Per-system constant parameters of the operator  q_c = h sum_d M[c][d] p_d + tau_c (kappa2 p_c + (L p_c)).
 // Kronecker route: one system per patch, K = k, M = A^T T A, tau = prior scales.
