@@ -491,7 +491,7 @@ def _paper_leg(dev, timed, args, level=10, faces=12):
                      "iterations_per_system": reps[-1]["iterations_per"],
                      "true_rel_residual": reps[-1]["rel_residual_true"]}
         if name != "lanczos":
-            out[name]["roofline"] = roof3(reps, k if name == "kron" else 1, N, "cg_persistent_kernel (D2)",
+            out[name]["roofline"] = roof3(reps, k if name == "kron" else 1, N, "cg_march_kernel (D2 row march)",
                                           traffic_key=f"paper/{name}")
     del ctx, Y, mu, hits
     torch.cuda.empty_cache()
