@@ -59,7 +59,7 @@ struct Layout {
 
 // Work geometry of the single-pass CG kernels: CTA tiles (Laplacian prior) or, for the D2 prior, the
 // row-march kernel's strips (x) and 16-row partial-sum blocks (y).
-int tiles_x(int side, int K, bool d2 = false) { return d2 ? kcg::m_strips(side) : (side + KCG_TX - 1) / KCG_TX; }
+int tiles_x(int side, int K, bool d2 = false) { return d2 ? kcg::m_strips(side, K) : (side + KCG_TX - 1) / KCG_TX; }
 int tiles_y(int rows, int K, bool d2 = false) {
   return d2 ? kcg::m_blocks(rows) : (rows + kcg::cg_tile_y(K) - 1) / kcg::cg_tile_y(K);
 }
@@ -67,9 +67,9 @@ int tiles_y(int rows, int K, bool d2 = false) {
 // D2 row-march kernel: rows per work unit (a multiple of the partial block KCG_MPB) minimising the
 // estimated pass time ceil(units / warps) * (seg + 8 warm-up rows + ~4 rows of pipeline fill), all
 // n_sys systems active.
-int march_seg(int side, int n_sys, int warps) {
+int march_seg(int side, int K, int n_sys, int warps) {
   if (side <= KCG_MPB) return KCG_MPB;
-  const long strips = kcg::m_strips(side);
+  const long strips = kcg::m_strips(side, K);
   int best = side;
   double bt = 1e300;
   for (int seg = KCG_MPB; seg < side + KCG_MPB; seg += KCG_MPB) {
@@ -450,8 +450,8 @@ PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
 
 bool encode_map(CUtensorMap* m, double* base, int side, int buf_rows, int pitch, size_t planes, int K, bool d2,
                 std::string* why) {
-  // box: the CTA tile + halo, or (D2) one row-march chunk of 32 columns x KCG_MCH rows
-  const int bx = d2 ? 32 : KCG_TX + 2 * KCG_HALO;
+  // box: the CTA tile + halo, or (D2) one row-march stage of 32 m_cp(K) columns x KCG_MCH rows
+  const int bx = d2 ? 32 * kcg::m_cp(K) : KCG_TX + 2 * KCG_HALO;
   const int by = d2 ? KCG_MCH : kcg::cg_tile_y(K) + 2 * KCG_HALO;
   auto enc = get_encode();
   if (!enc) { *why = "cuTensorMapEncodeTiled unavailable"; return false; }
@@ -477,13 +477,34 @@ bool encode_xmap(CUtensorMap* m, double* base, int side, int rows, size_t planes
   if (!enc) { *why = "cuTensorMapEncodeTiled unavailable"; return false; }
   cuuint64_t dims[3] = {(cuuint64_t)side, (cuuint64_t)rows, (cuuint64_t)planes};
   cuuint64_t strides[2] = {(cuuint64_t)side * 8, (cuuint64_t)side * rows * 8};
-  cuuint32_t box[3] = {(cuuint32_t)(d2 ? 32 : KCG_TX), (cuuint32_t)(d2 ? KCG_MCH : kcg::cg_tile_y(K)), (cuuint32_t)K};
+  cuuint32_t box[3] = {(cuuint32_t)(d2 ? 32 * kcg::m_cp(K) : KCG_TX), (cuuint32_t)(d2 ? KCG_MCH : kcg::cg_tile_y(K)),
+                       (cuuint32_t)K};
   cuuint32_t es[3] = {1, 1, 1};
   CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, base, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
                    CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) {
     char buf[128];
     snprintf(buf, sizeof buf, "cuTensorMapEncodeTiled (x) failed (%d)", (int)r);
+    *why = buf;
+    return false;
+  }
+  return true;
+}
+
+// TMA descriptor of the hits planes [planes][side][side] for the D2 row-march kernel: box {32 cp, 1, 1}.
+bool encode_hmap(CUtensorMap* m, const double* base, int side, size_t planes, int cp, std::string* why) {
+  auto enc = get_encode();
+  if (!enc) { *why = "cuTensorMapEncodeTiled unavailable"; return false; }
+  cuuint64_t dims[3] = {(cuuint64_t)side, (cuuint64_t)side, (cuuint64_t)planes};
+  cuuint64_t strides[2] = {(cuuint64_t)side * 8, (cuuint64_t)side * side * 8};
+  cuuint32_t box[3] = {(cuuint32_t)(32 * cp), (cuuint32_t)KCG_MCH, 1};
+  cuuint32_t es[3] = {1, 1, 1};
+  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<double*>(base), dims, strides, box, es,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    char buf[128];
+    snprintf(buf, sizeof buf, "cuTensorMapEncodeTiled (hits) failed (%d)", (int)r);
     *why = buf;
     return false;
   }
@@ -707,7 +728,7 @@ kcg_status solve_impl(kcg_ctx* c, Route route, const double* Y_in, double* mu_ou
     }
     if (march) {  // row-march kernel: segment rows, hits by TMA
       a.h_tma = (R.hits && c->side >= 2) ? 1 : 0;
-      a.seg = march_seg(c->side, n_sys, (kron ? c->grid_kron : c->grid_syl) * kcg::m_groups(Kk));
+      a.seg = march_seg(c->side, Kk, n_sys, (kron ? c->grid_kron : c->grid_syl) * kcg::m_groups(Kk));
     }
     Lx.m[j] = maps;
     CK(cudaMemsetAsync(R.sync, 0, 4 * sizeof(unsigned), s), "memset sync");
@@ -1041,7 +1062,7 @@ kcg_status kohler_impl(kcg_ctx* c, const double* Y_in, double* mu_out, double to
     const int grid = std::max(1, std::min(c->grid_syl, P * a.tiles_per_sys));
     if (d2) {
       a.h_tma = (R.hits && c->side >= 2) ? 1 : 0;
-      a.seg = march_seg(c->side, P, grid * kcg::m_groups(1));
+      a.seg = march_seg(c->side, 1, P, grid * kcg::m_groups(1));
     }
     if (c->res_koh.on) {
       a.tiles_per_sys = c->res_koh.nstrip;
@@ -1368,10 +1389,10 @@ kcg_status create_impl(const kcg_desc* d, const kcg_slab* sl, const double* A_ho
         return fail(KCG_E_CUDA, why);
     }
     // D2 row-march kernel: the hits planes [P][side][side], one chunk of 32 x KCG_MCH per box
-    if (d2 && R.hits && c->side >= 2) {
-      if (!encode_xmap(&R.maps_kron.h, const_cast<double*>(R.hits), c->side, c->side, (size_t)P, 1, true, &why))
+    if (d2 && R.hits && c->side >= 2) {  // box {32 m_cp(K), 1, 1}: the Kronecker and the K = 1 strips differ
+      if (!encode_hmap(&R.maps_kron.h, R.hits, c->side, (size_t)P, kcg::m_cp(k), &why) ||
+          !encode_hmap(&R.maps_syl.h, R.hits, c->side, (size_t)P, kcg::m_cp(1), &why))
         return fail(KCG_E_CUDA, why);
-      R.maps_syl.h = R.maps_kron.h;
     }
   }
   if (c->L.lz_slots > 0) {  // block-Lanczos constants: Lemma 2 factor, E = T A P^{-1} (Y^ = Y E)

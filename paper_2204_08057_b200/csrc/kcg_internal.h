@@ -68,31 +68,38 @@ __host__ __device__ constexpr int cg_stage_bytes(int K) {
   return 2 * K * (cg_tile_y(K) + 2 * KCG_HALO) * (KCG_TX + 2 * KCG_HALO) * 8 + cg_xstage_bytes(K);
 }
 
-// ---- D2 prior: the row-march CG kernel (kcg_march.cuh).  A GROUP of K warps (warp c = component
-// plane c) marches a strip of KCG_MOUT output columns (32 lanes = the strip + a 4-column halo each
-// side) down a segment of rows; rows of r, p, x, hits are TMA-staged one row per stage into a
+// ---- D2 prior: the row-march CG kernel (kcg_march.cuh).  A GROUP of warps (m_kp(K) component
+// planes per warp) marches a strip of m_out(K) output columns (32 lanes x m_cp(K) columns = the strip
+// + a 4-column halo each side) down a segment of rows; rows of r, p, x, hits are TMA-staged one row per stage into a
 // per-group ring of m_stages(K) stages; the planes meet only in the k x k mixing (shared rows).
-#define KCG_MOUT 24
 #define KCG_MHALO 4
 #define KCG_MCH 1           // rows per TMA stage
 #define KCG_MPB 16          // rows per partial-sum block (fixed reduction order)
 #ifndef KCG_MKP4
 #define KCG_MKP4 2          // K = 4: component planes per warp (2 warps per group)
 #endif
+#ifndef KCG_MCP1
+#define KCG_MCP1 2          // K = 1: face columns per lane (a 64-column box, 56 output columns)
+#endif
 __host__ __device__ constexpr int m_kp(int K) { return K == 4 ? KCG_MKP4 : 1; }  // planes per warp
 __host__ __device__ constexpr int m_gw(int K) { return K / m_kp(K); }            // warps per group
+__host__ __device__ constexpr int m_cp(int K) { return K == 1 ? KCG_MCP1 : 1; }  // columns per lane
+__host__ __device__ constexpr int m_out(int K) { return 32 * m_cp(K) - 2 * KCG_MHALO; }  // output columns
 __host__ __device__ constexpr int m_groups(int K) {
-  return K == 1 ? 16 : (K == 2 ? 8 : (K == 3 ? 5 : (m_kp(K) == 1 ? 4 : (m_kp(K) == 2 ? 6 : 8))));
+  return K == 1 ? (m_cp(K) == 2 ? 12 : 16)
+                : (K == 2 ? 8 : (K == 3 ? 5 : (m_kp(K) == 1 ? 4 : (m_kp(K) == 2 ? 6 : 8))));
 }
 __host__ __device__ constexpr int m_threads(int K) { return m_groups(K) * m_gw(K) * 32; }
-__host__ __device__ constexpr int m_stages(int K) { return m_kp(K) == 2 ? 4 : 8; }  // (6 groups x 8 stages > smem)
-__host__ __device__ constexpr int m_stage_doubles(int K) { return (3 * K + 1) * 32; }
-// doubles of one group's shared memory: the stage ring + 3 exchange rings [4 rows][K][32]
-__host__ __device__ constexpr int m_group_doubles(int K) { return m_stages(K) * m_stage_doubles(K) + 3 * 4 * K * 32; }
-__host__ __device__ constexpr int m_strips(int side) { return (side + KCG_MOUT - 1) / KCG_MOUT; }
+__host__ __device__ constexpr int m_stages(int K) { return (m_kp(K) == 2 || m_cp(K) == 2) ? 4 : 8; }  // (smem)
+__host__ __device__ constexpr int m_stage_doubles(int K) { return (3 * K + 1) * 32 * m_cp(K); }
+// doubles of one group's shared memory: the stage ring + 3 exchange rings [4 rows][K][32 cp]
+__host__ __device__ constexpr int m_group_doubles(int K) {
+  return m_stages(K) * m_stage_doubles(K) + 3 * 4 * K * 32 * m_cp(K);
+}
+__host__ __device__ constexpr int m_strips(int side, int K) { return (side + m_out(K) - 1) / m_out(K); }
 __host__ __device__ constexpr int m_blocks(int side) { return (side + KCG_MPB - 1) / KCG_MPB; }
 // partial slots per system: strips x 16-row blocks x warps of a group
-__host__ __device__ constexpr int m_slots(int side, int K) { return m_strips(side) * m_blocks(side) * m_gw(K); }
+__host__ __device__ constexpr int m_slots(int side, int K) { return m_strips(side, K) * m_blocks(side) * m_gw(K); }
 
 
 // Per-system constant parameters of the operator  q_c = h sum_d M[c][d] p_d + tau_c (kappa2 p_c + (L p_c)).

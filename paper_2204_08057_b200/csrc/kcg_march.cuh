@@ -47,9 +47,10 @@ __device__ __forceinline__ void group_bar(int id, int nthreads) {
 template <int K, bool HITS, bool PREC>
 __global__ void __launch_bounds__(m_threads(K), 1) cg_march_kernel(const CgArgs a, const __grid_constant__ CgMaps maps) {
   constexpr int NG = m_groups(K), NT = m_threads(K), NW = NT / 32, NS = m_stages(K), SD = m_stage_doubles(K);
-  constexpr int KP = m_kp(K), GW = m_gw(K);  // planes per warp, warps per group
-  constexpr int XR = 4 * K * 32, GD = m_group_doubles(K);
-  constexpr int MO = KCG_MOUT, MH = KCG_MHALO, PB = KCG_MPB;
+  constexpr int KP = m_kp(K), GW = m_gw(K), CP = m_cp(K);  // planes per warp, warps per group, columns per lane
+  constexpr int BW = 32 * CP;                                 // box width (one stage row of a plane)
+  constexpr int XR = 4 * K * BW, GD = m_group_doubles(K);
+  constexpr int MO = m_out(K), MH = KCG_MHALO, PB = KCG_MPB;
   constexpr int NP = PREC ? 3 : 2;
   constexpr int DL = PREC ? 5 : 4;  // row of C1 behind the input row
   constexpr int MSZ = K * K + K + (PREC ? 4 * K * K : 0);
@@ -74,10 +75,10 @@ __global__ void __launch_bounds__(m_threads(K), 1) cg_march_kernel(const CgArgs 
   const int nsegs = (side + seg - 1) / seg, ups = nstrips * nsegs;  // units per system
   const size_t N = (size_t)side * side, ps = (size_t)pitch * side;
   double* gsm = reinterpret_cast<double*>(smem_raw) + (size_t)g * GD;
-  double* stg = gsm;                 // [NS][SD]: r [K][32], p [K][32], x [K][32], hits [32]
-  double* PX = gsm + NS * SD;        // [4][K][32] p_new rows
-  double* RX = PX + XR;              // [4][K][32] r_new rows
-  double* UX = RX + XR;              // [4][K][32] u_new rows (block-Jacobi)
+  double* stg = gsm;                 // [NS][SD]: r [K][BW], p [K][BW], x [K][BW], hits [BW]
+  double* PX = gsm + NS * SD;        // [4][K][BW] p_new rows
+  double* RX = PX + XR;              // [4][K][BW] r_new rows
+  double* UX = RX + XR;              // [4][K][BW] u_new rows (block-Jacobi)
   auto gsync = [&]() {
     if constexpr (GW == 1) __syncwarp();
     else group_bar(1 + g, GW * 32);
@@ -137,7 +138,7 @@ __global__ void __launch_bounds__(m_threads(K), 1) cg_march_kernel(const CgArgs 
     const bool xpass = xpass_of(it + 1);
     const bool xl = xpass && a.x_tma;  // x rows staged with r and p
     const bool hl = HITS && a.h_tma;
-    const uint32_t tx_bytes = (2 * K + (xl ? K : 0) + (hl ? 1 : 0)) * 32 * 8;
+    const uint32_t tx_bytes = (2 * K + (xl ? K : 0) + (hl ? 1 : 0)) * BW * 8;
     unsigned* ctr = a.sync + 2 + par_out;
     const int ngt = ncta * NG;
 
@@ -164,9 +165,9 @@ __global__ void __launch_bounds__(m_threads(K), 1) cg_march_kernel(const CgArgs 
         const int r0 = I.ys - MH + ic, c0 = I.x0 - MH;
         mbar_arrive_expect_tx(bar, tx_bytes);
         tma_load_3d(d, &maps.r[I.par], bar, c0, r0, I.s * K);
-        tma_load_3d(d + K * 32, &maps.p[I.par], bar, c0, r0, I.s * K);
-        if (xl) tma_load_3d(d + 2 * K * 32, &maps.x, bar, c0, r0, I.s * K);
-        if (hl) tma_load_3d(d + 3 * K * 32, &maps.h, bar, c0, r0, I.hpl);
+        tma_load_3d(d + K * BW, &maps.p[I.par], bar, c0, r0, I.s * K);
+        if (xl) tma_load_3d(d + 2 * K * BW, &maps.x, bar, c0, r0, I.s * K);
+        if (hl) tma_load_3d(d + 3 * K * BW, &maps.h, bar, c0, r0, I.hpl);
       }
       ++ic;
       ++gi;
@@ -193,10 +194,18 @@ __global__ void __launch_bounds__(m_threads(K), 1) cg_march_kernel(const CgArgs 
       const double alpha = z.alpha, beta = z.beta, ap = KCG_X2 ? z.alpha_last : 0.0;
       const double kappa2 = __ldg(&sp->kappa2);
       const double* hp = HITS ? a.hits + (size_t)C.hpl * N : nullptr;
-      const int gx = C.x0 - MH + lane;
-      const bool colin = gx >= 0 && gx < side;
-      const bool outc = lane >= MH && lane < MH + MO && gx < side;
-      const int degx = 4 - (gx == 0) - (gx == side - 1);
+      // this lane's CP face columns gx + cc (CP = 2: a double2 in the stage rows and the stores)
+      const int gx = C.x0 - MH + CP * lane;
+      bool colin[CP], outc[CP];
+      int degx[CP];
+#pragma unroll
+      for (int cc = 0; cc < CP; ++cc) {
+        const int xx = gx + cc, l = CP * lane + cc;
+        colin[cc] = xx >= 0 && xx < side;
+        outc[cc] = l >= MH && l < MH + MO && xx < side;
+        degx[cc] = 4 - (xx == 0) - (xx == side - 1);
+      }
+      const bool pair_out = CP == 2 && outc[0] && outc[CP - 1];  // both columns stored (aligned double2)
       const size_t pc = ((size_t)C.s * K + c0);  // this warp's first plane
       double* rout = (C.par ? a.rbuf[0] : a.rbuf[1]) + pc * ps + gx;  // select, not a dynamic index
       double* pout = (C.par ? a.pbuf[0] : a.pbuf[1]) + pc * ps + gx;
@@ -218,17 +227,46 @@ __global__ void __launch_bounds__(m_threads(K), 1) cg_march_kernel(const CgArgs 
           uo[i] = ui;
         }
       };
+      // left + right neighbours of this lane's CP columns of a row (shuffles across lanes)
+      auto lr = [&](const double (&v)[CP], double (&o)[CP]) {
+        if constexpr (CP == 1) {
+          o[0] = __shfl_up_sync(FULL, v[0], 1) + __shfl_down_sync(FULL, v[0], 1);
+        } else {
+          const double L = __shfl_up_sync(FULL, v[CP - 1], 1), R = __shfl_down_sync(FULL, v[0], 1);
+          o[0] = L + v[1];
+          o[CP - 1] = v[0] + R;
+        }
+      };
+      // row `row` of a shared ring, plane d, this lane's columns
+      auto xr = [&](const double* X, int row, int d, int cc) { return X[((row & 3) * K + d) * BW + CP * lane + cc]; };
+      auto ld = [&](const double* src, double (&v)[CP]) {  // this lane's columns of a stage / ring row
+        if constexpr (CP == 1) v[0] = src[lane];
+        else { const double2 t = reinterpret_cast<const double2*>(src)[lane]; v[0] = t.x; v[CP - 1] = t.y; }
+      };
+      auto stv = [&](double* dst, const double (&v)[CP]) {  // store this lane's columns (valid ones)
+        if (CP == 2 && pair_out) *reinterpret_cast<double2*>(dst) = make_double2(v[0], v[CP - 1]);
+        else
+#pragma unroll
+          for (int cc = 0; cc < CP; ++cc)
+            if (outc[cc]) dst[cc] = v[cc];
+      };
 
-      // register rings of this warp's planes (slot of row y = (y - ys + 4) mod 3)
-      double pn[3][KP], s1[3][KP], rn[3][KP], s2[3][KP], un[3][KP];
+      // register rings of this warp's planes and columns (slot of row y = (y - ys + 4) mod 3)
+      double pn[3][KP][CP], s1[3][KP][CP], rn[3][KP][CP], s2[3][KP][CP], un[3][KP][CP];
 #pragma unroll
       for (int j = 0; j < 3; ++j)
 #pragma unroll
-        for (int i = 0; i < KP; ++i) { pn[j][i] = 0.0; s1[j][i] = 0.0; rn[j][i] = 0.0; s2[j][i] = 0.0; un[j][i] = 0.0; }
-      // per-row values of rows y-1 .. y-5, shifted by one every step: in-face flag, degree, hits
-      bool f1 = false, f2 = false, f3 = false, f4 = false, f5 = false;
-      double dg1 = 0.0, dg2 = 0.0, dg3 = 0.0, dg4 = 0.0, dg5 = 0.0;
-      double h1 = 1.0, h2 = 1.0, h3 = 1.0, h4 = 1.0, h5 = 1.0;
+        for (int i = 0; i < KP; ++i)
+#pragma unroll
+          for (int cc = 0; cc < CP; ++cc) {
+            pn[j][i][cc] = 0.0; s1[j][i][cc] = 0.0; rn[j][i][cc] = 0.0; s2[j][i][cc] = 0.0; un[j][i][cc] = 0.0;
+          }
+      // per-row values of rows y-1 .. y-5, shifted by one every step: in-face row, degree offset, hits
+      bool r1 = false, r2 = false, r3 = false, r4 = false, r5 = false;
+      int e1 = 0, e2 = 0, e3 = 0, e4 = 0, e5 = 0;  // -(row == 0) - (row == side - 1)
+      double h1[CP], h2[CP], h3[CP], h4[CP], h5[CP];
+#pragma unroll
+      for (int cc = 0; cc < CP; ++cc) { h1[cc] = 1.0; h2[cc] = 1.0; h3[cc] = 1.0; h4[cc] = 1.0; h5[cc] = 1.0; }
       double prr = 0.0, pru = 0.0, pwu = 0.0;  // partials of the current 16-row block
       const uint32_t q0 = gr;                 // the unit's first stage
       auto free_stage = [&]() {               // issuing warp: the oldest held stage is consumed, refill it
@@ -236,7 +274,6 @@ __global__ void __launch_bounds__(m_threads(K), 1) cg_march_kernel(const CgArgs 
         if (lane == 0) fence_proxy_async_smem();
         advance_issue();
       };
-      auto xr = [&](const double* X, int row, int d) { return X[((row & 3) * K + d) * 32 + lane]; };
 
       // one input row: y = ys - 4 + t, ring period 3 (J = t mod 3 at compile time)
       auto step = [&](auto Jc, int t) {
@@ -245,149 +282,180 @@ __global__ void __launch_bounds__(m_threads(K), 1) cg_march_kernel(const CgArgs 
         const uint32_t q = gr++;
         const int slot = q & (NS - 1);
         mbar_wait(&mbar[g][slot], (q / NS) & 1u);
-        const double* sg = stg + slot * SD + lane;
-        const double* sg2 = stg + ((q - 2) & (NS - 1)) * SD + lane;  // row y - 2 (held)
-        double r_c[KP], p_c[KP], ro_c[KP];
+        const double* sg = stg + slot * SD;
+        const double* sg2 = stg + ((q - 2) & (NS - 1)) * SD;  // row y - 2 (held)
+        double r_c[KP][CP], p_c[KP][CP], ro_c[KP][CP];
 #pragma unroll
         for (int i = 0; i < KP; ++i) {
-          r_c[i] = sg[(c0 + i) * 32];
-          p_c[i] = sg[(K + c0 + i) * 32];
-          ro_c[i] = sg2[(c0 + i) * 32];
+          ld(sg + (c0 + i) * BW, r_c[i]);
+          ld(sg + (K + c0 + i) * BW, p_c[i]);
+          ld(sg2 + (c0 + i) * BW, ro_c[i]);
         }
-        const bool f0 = colin && (unsigned)y < (unsigned)side;
-        const double dg0 = (double)(degx - (y == 0) - (y == side - 1));
-        const bool vA = outc && y >= C.ys && y < C.ye;
-        double xv[KP];
+        const bool r0 = (unsigned)y < (unsigned)side;
+        const int e0 = -(y == 0) - (y == side - 1);
+        const bool vA = y >= C.ys && y < C.ye;
+        double xv[KP][CP];
 #pragma unroll
-        for (int i = 0; i < KP; ++i) xv[i] = 0.0;
-        if (xpass)
+        for (int i = 0; i < KP; ++i)
 #pragma unroll
-          for (int i = 0; i < KP; ++i)
-            xv[i] = xl ? sg[(2 * K + c0 + i) * 32] : (vA ? __ldcg(xo + i * N + (size_t)y * side) : 0.0);
-        double h0 = 1.0;
-        if (HITS) h0 = hl ? sg[3 * K * 32] : (f0 ? __ldg(hp + (size_t)y * side + gx) : 1.0);
-        // A: p_new(y)
-        double u_c[KP];
-#pragma unroll
-        for (int i = 0; i < KP; ++i) u_c[i] = r_c[i];
-        if (PREC) {
-          double rv[K];
-#pragma unroll
-          for (int d = 0; d < K; ++d) rv[d] = sg[d * 32];
-          if (f0) prec_w(rv, h0, dg0, u_c);
-          else
-#pragma unroll
-            for (int i = 0; i < KP; ++i) u_c[i] = 0.0;
-        }
-#pragma unroll
-        for (int i = 0; i < KP; ++i) {
-          pn[J][i] = fma(beta, p_c[i], u_c[i]);
-          if (GW > 1) PX[((y & 3) * K + c0 + i) * 32 + lane] = pn[J][i];
-        }
-        if (vA) {
+          for (int cc = 0; cc < CP; ++cc) xv[i][cc] = 0.0;
+        if (xpass) {
 #pragma unroll
           for (int i = 0; i < KP; ++i) {
-            pout[i * ps + (size_t)y * pitch] = pn[J][i];
-            if (xpass) xo[i * N + (size_t)y * side] = xv[i] + fma(alpha, pn[J][i], ap * p_c[i]);
+            if (xl) ld(sg + (2 * K + c0 + i) * BW, xv[i]);
+            else
+#pragma unroll
+              for (int cc = 0; cc < CP; ++cc)
+                xv[i][cc] = (vA && outc[cc]) ? __ldcg(xo + i * N + (size_t)y * side + cc) : 0.0;
+          }
+        }
+        double h0[CP];
+#pragma unroll
+        for (int cc = 0; cc < CP; ++cc) h0[cc] = 1.0;
+        if (HITS) {
+          if (hl) ld(sg + 3 * K * BW, h0);
+          else
+#pragma unroll
+            for (int cc = 0; cc < CP; ++cc) h0[cc] = (colin[cc] && r0) ? __ldg(hp + (size_t)y * side + gx + cc) : 1.0;
+        }
+        // A: p_new(y)
+#pragma unroll
+        for (int cc = 0; cc < CP; ++cc) {
+          double u_c[KP];
+#pragma unroll
+          for (int i = 0; i < KP; ++i) u_c[i] = r_c[i][cc];
+          if (PREC) {
+            double rv[K];
+#pragma unroll
+            for (int d = 0; d < K; ++d) rv[d] = sg[d * BW + CP * lane + cc];
+            if (colin[cc] && r0) prec_w(rv, h0[cc], (double)(degx[cc] + e0), u_c);
+            else
+#pragma unroll
+              for (int i = 0; i < KP; ++i) u_c[i] = 0.0;
+          }
+#pragma unroll
+          for (int i = 0; i < KP; ++i) pn[J][i][cc] = fma(beta, p_c[i][cc], u_c[i]);
+        }
+#pragma unroll
+        for (int i = 0; i < KP; ++i) {
+          if (GW > 1)
+#pragma unroll
+            for (int cc = 0; cc < CP; ++cc) PX[((y & 3) * K + c0 + i) * BW + CP * lane + cc] = pn[J][i][cc];
+          if (vA) {
+            stv(pout + i * ps + (size_t)y * pitch, pn[J][i]);
+            if (xpass) {
+              double xn[CP];
+#pragma unroll
+              for (int cc = 0; cc < CP; ++cc) xn[cc] = xv[i][cc] + fma(alpha, pn[J][i][cc], ap * p_c[i][cc]);
+              stv(xo + i * N + (size_t)y * side, xn);
+            }
           }
         }
         // B0: S1(y-1) = D p_new
 #pragma unroll
         for (int i = 0; i < KP; ++i) {
-          const double v = pn[J1][i];
-          const double L = __shfl_up_sync(FULL, v, 1), R = __shfl_down_sync(FULL, v, 1);
-          s1[J1][i] = f1 ? fma(-dg1, v, (pn[J2][i] + pn[J][i]) + (L + R)) : 0.0;
+          double o[CP];
+          lr(pn[J1][i], o);
+#pragma unroll
+          for (int cc = 0; cc < CP; ++cc)
+            s1[J1][i][cc] = (r1 && colin[cc]) ? fma(-(double)(degx[cc] + e1), pn[J1][i][cc], (pn[J2][i][cc] + pn[J][i][cc]) + o[cc])
+                                                : 0.0;
         }
         // B1: r_new(y-2)
         {
-          double pv[K];  // p_new of row y-2, every plane
-#pragma unroll
-          for (int d = 0; d < K; ++d) pv[d] = GW == 1 ? pn[J2][GW == 1 ? d : 0] : xr(PX, y - 2, d);
           const int y2 = y - 2;
-          const bool st2 = outc && y2 >= C.ys && y2 < C.ye;
+          const bool st2 = y2 >= C.ys && y2 < C.ye;
 #pragma unroll
           for (int i = 0; i < KP; ++i) {
-            const double v = s1[J2][i];
-            const double L = __shfl_up_sync(FULL, v, 1), R = __shfl_down_sync(FULL, v, 1);
-            const double d2p = fma(-dg2, v, (s1[J][i] + s1[J1][i]) + (L + R));
-            double mix = 0.0;
+            double o[CP];
+            lr(s1[J2][i], o);
 #pragma unroll
-            for (int d = 0; d < K; ++d) mix = fma(Mrow[i][d], pv[d], mix);
-            const double qv = fma(h2, mix, tau_c[i] * fma(kappa2, pn[J2][i], d2p));
-            rn[J2][i] = f2 ? fma(-alpha, qv, ro_c[i]) : 0.0;
-            if (GW > 1 || PREC) RX[(((y - 2) & 3) * K + c0 + i) * 32 + lane] = rn[J2][i];
-            if (st2) rout[i * ps + (size_t)y2 * pitch] = rn[J2][i];
+            for (int cc = 0; cc < CP; ++cc) {
+              const double d2p = fma(-(double)(degx[cc] + e2), s1[J2][i][cc], (s1[J][i][cc] + s1[J1][i][cc]) + o[cc]);
+              double mix = 0.0;
+#pragma unroll
+              for (int d = 0; d < K; ++d)  // p_new of row y-2, plane d (GW == 1: every plane is this warp's)
+                mix = fma(Mrow[i][d], GW == 1 ? pn[J2][GW == 1 ? d : 0][cc] : xr(PX, y2, d, cc), mix);
+              const double qv = fma(h2[cc], mix, tau_c[i] * fma(kappa2, pn[J2][i][cc], d2p));
+              rn[J2][i][cc] = (r2 && colin[cc]) ? fma(-alpha, qv, ro_c[i][cc]) : 0.0;
+              if (GW > 1 || PREC) RX[((y2 & 3) * K + c0 + i) * BW + CP * lane + cc] = rn[J2][i][cc];
+            }
+            if (st2) stv(rout + i * ps + (size_t)y2 * pitch, rn[J2][i]);
           }
         }
         // B' (block-Jacobi): u_new(y-3) = K^{-1} r_new from the shared r_new row
         if (PREC) {
-          double rv[K];
 #pragma unroll
-          for (int d = 0; d < K; ++d) rv[d] = GW == 1 ? rn[J][GW == 1 ? d : 0] : xr(RX, y - 3, d);
-          double uo[KP];
-          if (f3) prec_w(rv, h3, dg3, uo);
-          else
+          for (int cc = 0; cc < CP; ++cc) {
+            double rv[K];
 #pragma unroll
-            for (int i = 0; i < KP; ++i) uo[i] = 0.0;
+            for (int d = 0; d < K; ++d) rv[d] = GW == 1 ? rn[J][GW == 1 ? d : 0][cc] : xr(RX, y - 3, d, cc);
+            double uo[KP];
+            if (r3 && colin[cc]) prec_w(rv, h3[cc], (double)(degx[cc] + e3), uo);
+            else
 #pragma unroll
-          for (int i = 0; i < KP; ++i) {
-            un[J][i] = uo[i];
-            if (GW > 1) UX[(((y - 3) & 3) * K + c0 + i) * 32 + lane] = un[J][i];
+              for (int i = 0; i < KP; ++i) uo[i] = 0.0;
+#pragma unroll
+            for (int i = 0; i < KP; ++i) {
+              un[J][i][cc] = uo[i];
+              if (GW > 1) UX[(((y - 3) & 3) * K + c0 + i) * BW + CP * lane + cc] = uo[i];
+            }
           }
         }
         // C0: S2 = D u_new at row y-3 (u = r_new) or y-4 (block-Jacobi)
 #pragma unroll
         for (int i = 0; i < KP; ++i) {
+          double o[CP];
           if (!PREC) {
-            const double v = rn[J][i];
-            const double L = __shfl_up_sync(FULL, v, 1), R = __shfl_down_sync(FULL, v, 1);
-            s2[J][i] = f3 ? fma(-dg3, v, (rn[J1][i] + rn[J2][i]) + (L + R)) : 0.0;
+            lr(rn[J][i], o);
+#pragma unroll
+            for (int cc = 0; cc < CP; ++cc)
+              s2[J][i][cc] = (r3 && colin[cc]) ? fma(-(double)(degx[cc] + e3), rn[J][i][cc], (rn[J1][i][cc] + rn[J2][i][cc]) + o[cc])
+                                               : 0.0;
           } else {  // u_new rows: y-3 -> J, y-4 -> J1, y-5 -> J2; S2 row y-4 -> J1
-            const double v = un[J1][i];
-            const double L = __shfl_up_sync(FULL, v, 1), R = __shfl_down_sync(FULL, v, 1);
-            s2[J1][i] = f4 ? fma(-dg4, v, (un[J2][i] + un[J][i]) + (L + R)) : 0.0;
+            lr(un[J1][i], o);
+#pragma unroll
+            for (int cc = 0; cc < CP; ++cc)
+              s2[J1][i][cc] = (r4 && colin[cc]) ? fma(-(double)(degx[cc] + e4), un[J1][i][cc], (un[J2][i][cc] + un[J][i][cc]) + o[cc])
+                                                : 0.0;
           }
         }
         // C1: w at row yc = y - DL and the partials
         {
           const int yc = y - DL;
-          double uv[K];  // u_new of row yc, every plane
-#pragma unroll
-          for (int d = 0; d < K; ++d) {
-            const int i = GW == 1 ? d : 0;  // (GW == 1: every plane is this warp's, c0 = 0)
-            uv[d] = GW == 1 ? (PREC ? un[J2][i] : rn[J1][i]) : xr(PREC ? UX : RX, yc, d);
-          }
           double lrr = 0.0, lru = 0.0, lwu = 0.0;
 #pragma unroll
           for (int i = 0; i < KP; ++i) {
-            double w, uc, rc;
-            if (!PREC) {  // S2 rows y-5 (J2), y-4 (J1), y-3 (J); u = r_new row y-4 (J1)
-              const double v = s2[J1][i];
-              const double L = __shfl_up_sync(FULL, v, 1), R = __shfl_down_sync(FULL, v, 1);
-              const double d2v = fma(-dg4, v, (s2[J2][i] + s2[J][i]) + (L + R));
-              double mix = 0.0;
+            double o[CP];
+            lr(PREC ? s2[J2][i] : s2[J1][i], o);
 #pragma unroll
-              for (int d = 0; d < K; ++d) mix = fma(Mrow[i][d], uv[d], mix);
-              uc = rn[J1][i];
-              rc = uc;
-              w = fma(h4, mix, tau_c[i] * fma(kappa2, uc, d2v));
-            } else {      // S2 rows y-6 (J), y-5 (J2), y-4 (J1); u_new row y-5 (J2); r_new row y-5 (RX)
-              const double v = s2[J2][i];
-              const double L = __shfl_up_sync(FULL, v, 1), R = __shfl_down_sync(FULL, v, 1);
-              const double d2v = fma(-dg5, v, (s2[J][i] + s2[J1][i]) + (L + R));
+            for (int cc = 0; cc < CP; ++cc) {
+              double w, uc, rc;
               double mix = 0.0;
+              if (!PREC) {  // S2 rows y-5 (J2), y-4 (J1), y-3 (J); u = r_new row y-4 (J1)
+                const double d2v = fma(-(double)(degx[cc] + e4), s2[J1][i][cc], (s2[J2][i][cc] + s2[J][i][cc]) + o[cc]);
 #pragma unroll
-              for (int d = 0; d < K; ++d) mix = fma(Mrow[i][d], uv[d], mix);
-              uc = un[J2][i];
-              rc = xr(RX, yc, c0 + i);
-              w = fma(h5, mix, tau_c[i] * fma(kappa2, uc, d2v));
+                for (int d = 0; d < K; ++d) mix = fma(Mrow[i][d], GW == 1 ? rn[J1][GW == 1 ? d : 0][cc] : xr(RX, yc, d, cc), mix);
+                uc = rn[J1][i][cc];
+                rc = uc;
+                w = fma(h4[cc], mix, tau_c[i] * fma(kappa2, uc, d2v));
+              } else {      // S2 rows y-6 (J), y-5 (J2), y-4 (J1); u_new row y-5 (J2); r_new row y-5 (RX)
+                const double d2v = fma(-(double)(degx[cc] + e5), s2[J2][i][cc], (s2[J][i][cc] + s2[J1][i][cc]) + o[cc]);
+#pragma unroll
+                for (int d = 0; d < K; ++d) mix = fma(Mrow[i][d], GW == 1 ? un[J2][GW == 1 ? d : 0][cc] : xr(UX, yc, d, cc), mix);
+                uc = un[J2][i][cc];
+                rc = xr(RX, yc, c0 + i, cc);
+                w = fma(h5[cc], mix, tau_c[i] * fma(kappa2, uc, d2v));
+              }
+              if (outc[cc]) {
+                lrr = fma(rc, rc, lrr);
+                if (PREC) lru = fma(rc, uc, lru);
+                lwu = fma(w, uc, lwu);
+              }
             }
-            lrr = fma(rc, rc, lrr);
-            if (PREC) lru = fma(rc, uc, lru);
-            lwu = fma(w, uc, lwu);
           }
           const bool inc = yc >= C.ys && yc < C.ye;
-          if (outc && inc) { prr += lrr; pru += lru; pwu += lwu; }
+          if (inc) { prr += lrr; pru += lru; pwu += lwu; }
           // the 16-row block of yc ends (or the segment does): flush this warp's partials
           if (inc && (((yc + 1) % PB) == 0 || yc == C.ye - 1)) {
             const double sr = warp_sum(prr), sw = warp_sum(pwu), su = PREC ? warp_sum(pru) : 0.0;
@@ -401,9 +469,11 @@ __global__ void __launch_bounds__(m_threads(K), 1) cg_march_kernel(const CgArgs 
           }
         }
         // shift the per-row values
-        f5 = f4; f4 = f3; f3 = f2; f2 = f1; f1 = f0;
-        dg5 = dg4; dg4 = dg3; dg3 = dg2; dg2 = dg1; dg1 = dg0;
-        if (HITS) { h5 = h4; h4 = h3; h3 = h2; h2 = h1; h1 = h0; }
+        r5 = r4; r4 = r3; r3 = r2; r2 = r1; r1 = r0;
+        e5 = e4; e4 = e3; e3 = e2; e2 = e1; e1 = e0;
+        if (HITS)
+#pragma unroll
+          for (int cc = 0; cc < CP; ++cc) { h5[cc] = h4[cc]; h4[cc] = h3[cc]; h3[cc] = h2[cc]; h2[cc] = h1[cc]; h1[cc] = h0[cc]; }
         // Group barrier: the shared rows of this step are written, stage y-2 is read by every warp.
         // (A barrier every other step -- enough for the read distances without block-Jacobi --
         // measured 5% slower: the issuing warp then refills two stages at once.)
