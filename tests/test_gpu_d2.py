@@ -102,3 +102,43 @@ def test_d2_limits():
     with pytest.raises(KcgError) as e:
         make_ctx([_d2(4, 5, 1)])
     assert e.value.status == 4
+
+
+@pytest.mark.parametrize("level,k", [(5, 4), (6, 2), (7, 3)])
+def test_d2_block_jacobi_with_hits(level, k):
+    """The row-march kernel's block-Jacobi path with per-pixel Cholesky (hits): u = K^{-1} r over every
+    plane of the stage (A) and over the shared r_new rows (B'), C0 / C1 one row further behind --
+    Kronecker route (K = 4: two planes per warp, K = 2 / 3: one) and the Sylvester columns (K = 1:
+    two face columns per lane) against the oracle's preconditioned CG (reading R10)."""
+    ps = [_d2(level, k, 860 + s, hits="random") for s in range(2)]
+    ctx, Y = make_ctx(ps, precond="block_jacobi")
+    mu, rep = ctx.solve(Y, tol=TOL, max_iter=200000)
+    mu = mu.cpu().numpy()
+    assert rep["converged"], rep["status_name"]
+    for i, p in enumerate(ps):
+        G, b = model.problem_system(p)
+        K = cg.block_jacobi_precond(p.level, p.A, p.noise_prec, p.tau, p.kappa2, p.hits, prior="d2")
+        lo, hi, ref = oracle_count_envelope(cg.cg_hs, G, b, tol=TOL, precond=K, max_iter=200000)
+        assert rel(mu[i], ref.x) <= 1e-8, (i, rel(mu[i], ref.x))
+        sp = cg.cg_single_pass(G, b, tol=TOL, max_iter=200000, precond=K)
+        assert min(lo, sp.iterations) - 2 <= rep["iterations_per"][i] <= max(hi, sp.iterations) + 2
+    smu, srep = ctx.sylvester(Y, tol=TOL, max_iter=200000)
+    smu = smu.cpu().numpy()
+    assert srep["converged"]
+    for i, p in enumerate(ps):
+        ref = sylvester.problem_solve(p, tol=TOL, max_iter=200000, precond="jacobi")
+        assert rel(smu[i], ref.x) <= 1e-8, (i, rel(smu[i], ref.x))
+
+
+def test_d2_march_ragged_strips_and_segments():
+    """Face widths that are not multiples of the strips (24 columns for K = 4, 56 for K = 1) and a
+    Sylvester route with several segments per strip: level 8 (256 = 10 x 24 + 16 = 4 x 56 + 32)."""
+    p = _d2(8, 4, 880)
+    ctx, Y = make_ctx([p])
+    mu, rep = ctx.solve(Y, tol=TOL, max_iter=200000)
+    xe = exact.problem_dct_exact(p)
+    assert rep["converged"] and rel(mu.cpu().numpy()[0], xe) <= 1e-8
+    smu, srep = ctx.sylvester(Y, tol=TOL, max_iter=200000)
+    assert srep["converged"] and rel(smu.cpu().numpy()[0], xe) <= 1e-8
+    kmu, krep = ctx.kohler(Y, tol=TOL, max_iter=200000)
+    assert krep["converged"] and rel(kmu.cpu().numpy()[0], xe) <= 1e-8
