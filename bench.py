@@ -649,6 +649,9 @@ def run_b200(args):
     clk = ClockSampler(local)
     t_main, reps = timed(main_fn, args.steps)
     clocks = clk.stop()
+    # this rank's own busy time of the main leg (the max over ranks is t_main): per-GPU busy time and
+    # the sharding's makespan bound go into the line for N > 1
+    t_busy_local = sum(r["loop_time_s"] for r in reps)
     for _ in range(max(1, args.warmup // 2)):
         other_fn()
     t_other, reps_other = timed(other_fn, args.steps)
@@ -706,6 +709,13 @@ def run_b200(args):
 
     g_main = agg(reps)
     g_other = agg(reps_other)
+    if world > 1:
+        tb = torch.tensor([t_busy_local, float(sum(costs[i] for i in mine)) / g], dtype=torch.float64,
+                          device="cpu" if cpu_coll else dev)
+        tbs = [torch.zeros_like(tb) for _ in range(world)]
+        dist.all_gather(tbs, tb)
+        busy = [float(v[0].item()) for v in tbs]
+        load = [float(v[1].item()) for v in tbs]
     io = torch.tensor([float(Y_host.numel() * 8), float(mu_host[0].numel() * 8)], dtype=torch.float64,
                       device="cpu" if cpu_coll else dev)
     if world > 1:
@@ -753,6 +763,14 @@ def run_b200(args):
         "true_rel_residual": reps[-1]["rel_residual_true"],
     }
     line.update(extra)
+    if world > 1:  # per-GPU busy time of the CG loop (all steps) next to the cost model's makespan bound
+        line["sharding"] = {
+            "faces_per_group": len(mine), "group_size": g,
+            "cg_loop_busy_s_per_rank": busy,
+            "modelled_load_per_rank": load,
+            "modelled_speedup_bound": sum(costs) / max(max(load), 1e-30),
+            "note": "load = the sqrt(cond) cost of the faces a rank's group holds / g (row slabs); bound = "
+                    "total cost / the largest rank load (the cost model's makespan, exchange not counted)"}
     if world == 1 and not args.no_slab_probe:
         line["slab_emulation"] = _slab_probe(dev)
     if world == 1 and not args.no_cpu_baseline:
