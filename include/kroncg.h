@@ -143,7 +143,9 @@ KCG_API kcg_status kron_cg_create(const kcg_desc* desc, const double* A_host, co
                           const double* hits_dev, void* workspace_dev, size_t ws_bytes,
                           void* stream, kcg_ctx** out);
 
-/* Kronecker route: CG on G (Sec. 3.2).  Y_dev [P][n][N] -> mu_dev [P][k][N].                   */
+/* Kronecker route: CG on G (Sec. 3.2).  Y_dev [P][n][N] -> mu_dev [P][k][N].  Every device mu_dev
+ * (all routes) must be 16-byte aligned (cudaMalloc / torch give 256): the kernels store the
+ * solution as pixel pairs -- KCG_E_ARG otherwise.                                               */
 KCG_API kcg_status kron_cg_solve(kcg_ctx* ctx, const double* Y_dev, double* mu_dev, double tol,
                          int max_iter, kcg_report* report);
 

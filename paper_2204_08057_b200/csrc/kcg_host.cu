@@ -627,6 +627,10 @@ kcg_status solve_impl(kcg_ctx* c, Route route, const double* Y_in, double* mu_ou
     return KCG_E_CONFIG;
   }
   if (!Y_in || !mu_out) { c->err = "null Y or mu"; return KCG_E_ARG; }
+  if (!host_io && (reinterpret_cast<uintptr_t>(mu_out) & 15)) {  // the kernels store x as double2
+    c->err = "mu must be 16-byte aligned";
+    return KCG_E_ARG;
+  }
   if (!(tol > 0.0) || !std::isfinite(tol)) { c->err = "tol must be finite and > 0"; return KCG_E_ARG; }
   if (max_iter < 0) { c->err = "max_iter < 0"; return KCG_E_ARG; }
   if (host_io && !c->d.host_staging) { c->err = "host entry point needs desc.host_staging = 1"; return KCG_E_CONFIG; }
@@ -883,6 +887,10 @@ kcg_status lanczos_impl(kcg_ctx* c, const double* Y_in, double* mu_out, bool hos
     return KCG_E_CONFIG;
   }
   if (!Y_in || !mu_out) { c->err = "null Y or mu"; return KCG_E_ARG; }
+  if (!host_io && (reinterpret_cast<uintptr_t>(mu_out) & 15)) {  // the kernels store x as double2
+    c->err = "mu must be 16-byte aligned";
+    return KCG_E_ARG;
+  }
   if (!(tol > 0.0) || !std::isfinite(tol)) { c->err = "tol must be finite and > 0"; return KCG_E_ARG; }
   if (max_iter < 0) { c->err = "max_iter < 0"; return KCG_E_ARG; }
   if (host_io && !c->d.host_staging) { c->err = "host entry point needs desc.host_staging = 1"; return KCG_E_CONFIG; }
@@ -1008,6 +1016,10 @@ kcg_status kohler_impl(kcg_ctx* c, const double* Y_in, double* mu_out, double to
   if (!c) return KCG_E_ARG;
   if (c->slab) { c->err = "Alg. Kohler route: no row slabs"; return KCG_E_CONFIG; }
   if (!Y_in || !mu_out) { c->err = "null Y or mu"; return KCG_E_ARG; }
+  if ((reinterpret_cast<uintptr_t>(mu_out) & 15)) {  // the kernels store x as double2
+    c->err = "mu must be 16-byte aligned";
+    return KCG_E_ARG;
+  }
   if (!(tol > 0.0) || !std::isfinite(tol)) { c->err = "tol must be finite and > 0"; return KCG_E_ARG; }
   if (max_iter < 0) { c->err = "max_iter < 0"; return KCG_E_ARG; }
   cudaStream_t s = c->stream;

@@ -243,8 +243,10 @@ __global__ void __launch_bounds__(m_threads(K), 1) cg_march_kernel(const CgArgs 
         if constexpr (CP == 1) v[0] = src[lane];
         else { const double2 t = reinterpret_cast<const double2*>(src)[lane]; v[0] = t.x; v[CP - 1] = t.y; }
       };
-      auto stv = [&](double* dst, const double (&v)[CP]) {  // store this lane's columns (valid ones)
-        if (CP == 2 && pair_out) *reinterpret_cast<double2*>(dst) = make_double2(v[0], v[CP - 1]);
+      // x is the caller's buffer: double2 stores only if it is 16-byte aligned (r / p: the workspace)
+      const bool x16 = (reinterpret_cast<uintptr_t>(a.x) & 15) == 0;
+      auto stv = [&](double* dst, const double (&v)[CP], bool al = true) {  // this lane's valid columns
+        if (CP == 2 && pair_out && al) *reinterpret_cast<double2*>(dst) = make_double2(v[0], v[CP - 1]);
         else
 #pragma unroll
           for (int cc = 0; cc < CP; ++cc)
@@ -347,7 +349,7 @@ __global__ void __launch_bounds__(m_threads(K), 1) cg_march_kernel(const CgArgs 
               double xn[CP];
 #pragma unroll
               for (int cc = 0; cc < CP; ++cc) xn[cc] = xv[i][cc] + fma(alpha, pn[J][i][cc], ap * p_c[i][cc]);
-              stv(xo + i * N + (size_t)y * side, xn);
+              stv(xo + i * N + (size_t)y * side, xn, x16);
             }
           }
         }

@@ -88,3 +88,20 @@ def test_posterior_variance_reports_iterations_per_patch():
             z = variance.rademacher(5, q, len(ps), p.k, p.N)[i].reshape(-1)
             counts.append(cg.cg_hs(G, z, tol=TOL).iterations)
         assert abs(its[i] - max(counts)) <= 2, (its[i], counts)
+
+
+def test_misaligned_mu_rejected():
+    """Device solutions are stored as pixel pairs (double2): a mu that is not 16-byte aligned is an
+    argument error (kroncg.h), never a misaligned store."""
+    import torch
+    from gpu_util import make_ctx
+    from paper_2204_08057_b200.kroncg import KcgError
+    from synth import make_patch
+    ps = [make_patch(4, 9, 3, seed=1)]
+    ctx, Y = make_ctx(ps)
+    buf = torch.zeros(ctx.shape_mu[0] * 3 * 16 * 16 + 1, dtype=torch.float64, device="cuda")
+    mu = buf[1:].view(ctx.shape_mu)  # offset by one double: 8-byte aligned only
+    for fn in (ctx.solve, ctx.sylvester, ctx.kohler):
+        with pytest.raises(KcgError) as e:
+            fn(Y, mu)
+        assert e.value.status == 2
