@@ -596,7 +596,7 @@ __device__ __forceinline__ void cg_tile(const CgArgs& a, const TileCtx& tc, doub
     const double ap = tc.alpha_prev;
 #pragma unroll
     for (int j = 0; j < RPW; ++j) {
-      const int ly = warp + j * NW;
+      const int ly = KCG_ROWMAP ? warp * RPW + j : warp + j * NW;
       const int e0 = ((ly + H) * BW + H) / 2 + lane;
       if constexpr (!PREC) {
 #pragma unroll
@@ -689,10 +689,19 @@ __device__ __forceinline__ void cg_tile(const CgArgs& a, const TileCtx& tc, doub
 #pragma unroll
     for (int c = 0; c < K; ++c) tau[c] = M[K * K + c];
 
-  // Phase B1: tile rows, pairs
+  // Phase B1: tile rows, pairs.  With consecutive rows per warp (KCG_ROWMAP) the centre rows of all
+  // RPW rows are loaded once and serve as the up / down neighbours of the adjacent rows.
+  double2 pcs[KCG_ROWMAP ? RPW : 1][K];
+  if (KCG_ROWMAP)
+#pragma unroll
+    for (int j = 0; j < RPW; ++j)
+#pragma unroll
+      for (int c = 0; c < K; ++c)
+        pcs[KCG_ROWMAP ? j : 0][c] =
+            reinterpret_cast<const double2*>(Pp + c * PLANE + (warp * RPW + j + H) * BW)[1 + lane];
 #pragma unroll
   for (int j = 0; j < RPW; ++j) {
-    const int ly = warp + j * NW;            // local tile row
+    const int ly = KCG_ROWMAP ? warp * RPW + j : warp + j * NW;  // local tile row
     const int by = ly + H;                   // box row
     const int gyg = row0 + y0 + ly;
     bool in0 = true, in1 = true;
@@ -715,12 +724,15 @@ __device__ __forceinline__ void cg_tile(const CgArgs& a, const TileCtx& tc, doub
     const double h0 = HITS && up0 ? hit(y0 + ly, gx) : 1.0, h1 = HITS && up1 ? hit(y0 + ly, gx + 1) : 1.0;
     double2 pc[K];
 #pragma unroll
-    for (int c = 0; c < K; ++c) pc[c] = reinterpret_cast<const double2*>(Pp + c * PLANE + by * BW)[1 + lane];
+    for (int c = 0; c < K; ++c)
+      pc[c] = KCG_ROWMAP ? pcs[KCG_ROWMAP ? j : 0][c] : reinterpret_cast<const double2*>(Pp + c * PLANE + by * BW)[1 + lane];
 #pragma unroll
     for (int c = 0; c < K; ++c) {
       const double* row = Pp + c * PLANE + by * BW;
-      const double2 up = reinterpret_cast<const double2*>(row - BW)[1 + lane];
-      const double2 dn = reinterpret_cast<const double2*>(row + BW)[1 + lane];
+      const double2 up = (KCG_ROWMAP && j > 0) ? pcs[KCG_ROWMAP ? j - 1 : 0][c]
+                                                : reinterpret_cast<const double2*>(row - BW)[1 + lane];
+      const double2 dn = (KCG_ROWMAP && j + 1 < RPW) ? pcs[KCG_ROWMAP ? j + 1 : 0][c]
+                                                      : reinterpret_cast<const double2*>(row + BW)[1 + lane];
       const double el = row[H - 1], er = row[H + TX];  // broadcast loads, no branch
       double left = __shfl_up_sync(0xffffffffu, pc[c].y, 1);
       double right = __shfl_down_sync(0xffffffffu, pc[c].x, 1);
@@ -812,9 +824,17 @@ __device__ __forceinline__ void cg_tile(const CgArgs& a, const TileCtx& tc, doub
   const double* __restrict__ S = USEU ? tc.U - BW : R;
   constexpr int SPLANE = USEU ? UPLANE : PLANE;
   double rr = 0.0, ru = 0.0, wu = 0.0;
+  double2 scs[KCG_ROWMAP ? RPW : 1][K];  // (KCG_ROWMAP) the S centre rows of all RPW rows, loaded once
+  if (KCG_ROWMAP)
+#pragma unroll
+    for (int j = 0; j < RPW; ++j)
+#pragma unroll
+      for (int c = 0; c < K; ++c)
+        scs[KCG_ROWMAP ? j : 0][c] =
+            reinterpret_cast<const double2*>(S + c * SPLANE + (warp * RPW + j + H) * BW)[1 + lane];
 #pragma unroll
   for (int j = 0; j < RPW; ++j) {
-    const int ly = warp + j * NW;
+    const int ly = KCG_ROWMAP ? warp * RPW + j : warp + j * NW;
     const int by = ly + H;
     const int gyg = row0 + y0 + ly;
     bool in0 = true, in1 = true;
@@ -845,8 +865,15 @@ __device__ __forceinline__ void cg_tile(const CgArgs& a, const TileCtx& tc, doub
     double2 rc[K], sc[K];
 #pragma unroll
     for (int c = 0; c < K; ++c) {
-      rc[c] = reinterpret_cast<const double2*>(R + c * PLANE + by * BW)[1 + lane];
-      sc[c] = USEU ? reinterpret_cast<const double2*>(S + c * SPLANE + by * BW)[1 + lane] : rc[c];
+      if (KCG_ROWMAP && !USEU) {
+        rc[c] = scs[KCG_ROWMAP ? j : 0][c];
+        sc[c] = rc[c];
+      } else {
+        rc[c] = reinterpret_cast<const double2*>(R + c * PLANE + by * BW)[1 + lane];
+        sc[c] = USEU ? (KCG_ROWMAP ? scs[KCG_ROWMAP ? j : 0][c]
+                                   : reinterpret_cast<const double2*>(S + c * SPLANE + by * BW)[1 + lane])
+                     : rc[c];
+      }
     }
     const size_t ro = ((size_t)s * K) * ps + (size_t)(y0 + ly + ghost) * a.pitch + gx;
     double* rout = (tc.par ? a.rbuf[0] : a.rbuf[1]) + ro;  // select, not a dynamic param index
@@ -854,8 +881,10 @@ __device__ __forceinline__ void cg_tile(const CgArgs& a, const TileCtx& tc, doub
 #pragma unroll
     for (int c = 0; c < K; ++c) {
       const double* row = S + c * SPLANE + by * BW;
-      const double2 up = reinterpret_cast<const double2*>(row - BW)[1 + lane];
-      const double2 dn = reinterpret_cast<const double2*>(row + BW)[1 + lane];
+      const double2 up = (KCG_ROWMAP && j > 0) ? scs[KCG_ROWMAP ? j - 1 : 0][c]
+                                                : reinterpret_cast<const double2*>(row - BW)[1 + lane];
+      const double2 dn = (KCG_ROWMAP && j + 1 < RPW) ? scs[KCG_ROWMAP ? j + 1 : 0][c]
+                                                      : reinterpret_cast<const double2*>(row + BW)[1 + lane];
       const double el = row[H - 1], er = row[H + TX];
       double left = __shfl_up_sync(0xffffffffu, sc[c].y, 1);
       double right = __shfl_down_sync(0xffffffffu, sc[c].x, 1);

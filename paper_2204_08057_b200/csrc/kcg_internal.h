@@ -45,6 +45,9 @@ namespace kcg {
 #ifndef KCG_XPF
 #define KCG_XPF 1           // prefetch the next tile's x block into L2 (TMA prefetch) when not staged
 #endif
+#ifndef KCG_ROWMAP
+#define KCG_ROWMAP 1        // warp w owns tile rows w RPW .. w RPW + RPW - 1 (consecutive: shared up / down rows)
+#endif
 #ifndef KCG_PREC_SMEM_A
 #define KCG_PREC_SMEM_A 0   // 1: PCG phase A reads the block-Jacobi inverses from shared memory (extra barrier)
 #endif
