@@ -1048,8 +1048,8 @@ __device__ __forceinline__ void cg_body(const CgArgs& a, const CgMaps& maps, con
     __syncthreads();
   }
 
-  // pass q = it + 1 updates x iff xpass_of(q) (KCG_X2: even passes >= 2; else every pass >= 1)
-  auto xpass_of = [](int q) { return KCG_X2 ? (q >= 2 && (q & 1) == 0) : (q >= 1); };
+  // pass q = it + 1 updates x on tile `tile` iff cg_xpass(q, tile) (KCG_X2 + KCG_XMIX: the tile class
+  // tile & 1 picks the even or the odd passes; without KCG_X2 every pass >= 1)
   // Thread 0: TMA of (physical) tile t into stage sidx (parity flipped for the speculative load of
   // the next pass) and its coordinates into s_info[sidx] for all threads.  On x passes the x block
   // comes with the boxes (XTMA) or is prefetched into L2 (read by phase C).  r/p buffers carry
@@ -1061,7 +1061,7 @@ __device__ __forceinline__ void cg_body(const CgArgs& a, const CgMaps& maps, con
     s_info[sidx][0] = s; s_info[sidx][1] = tile; s_info[sidx][2] = ty; s_info[sidx][3] = tx;
     const int par = st[s].parity ^ flip;
     double* dst = reinterpret_cast<double*>(smem_raw + sidx * STAGE_BYTES);
-    const bool xp = xpass_of(it + 1 + flip);
+    const bool xp = cg_xpass(it + 1 + flip, cg_xclass(ty, tx, a.tiles_x));
     const bool xl = xtma && xp;
     mbar_arrive_expect_tx(&mbar[sidx], xl ? STAGE_BYTES : 2 * FIELD * 8);
     if (xl) tma_load_3d(dst + 2 * FIELD, &maps.x, &mbar[sidx], tx * TX, ty * TY, s * K);
@@ -1142,7 +1142,7 @@ __device__ __forceinline__ void cg_body(const CgArgs& a, const CgMaps& maps, con
       tc.par = st[s].parity;
       tc.alpha = st[s].alpha;
       tc.beta = st[s].beta;
-      tc.xpass = xpass_of(it + 1);
+      tc.xpass = cg_xpass(it + 1, cg_xclass(ty, tx, a.tiles_x));
       tc.alpha_prev = KCG_X2 ? st[s].alpha_last : 0.0;
       tc.kappa2 = __ldg(&sp->kappa2);
       tc.hp = HITS ? a.hits + (size_t)__ldg(&sp->hits_plane) * ((size_t)(SLAB ? a.rows + 2 * a.ghost : a.side) * a.side)

@@ -556,6 +556,14 @@ kcg_status cuda_fail(kcg_ctx* c, cudaError_t e, const char* what) {
 
 enum Route { ROUTE_KRON = 0, ROUTE_SYL = 1 };
 
+// fraction of a system's tiles in x class 1 (kcg::cg_xclass)
+static double kcg_xclass1_frac(int tiles_x, int tiles_y) {
+  long long n1 = 0;
+  for (int ty = 0; ty < tiles_y; ++ty)
+    for (int tx = 0; tx < tiles_x; ++tx) n1 += kcg::cg_xclass(ty, tx, tiles_x);
+  return tiles_x * tiles_y > 0 ? (double)n1 / ((double)tiles_x * tiles_y) : 0.0;
+}
+
 SlabGeom geom_of(const kcg_ctx* c, const RankState& R) {
   return SlabGeom{c->side, c->rows, R.row0, c->pitch, c->ghost, c->ghost, c->d.layout == KCG_LAYOUT_NESTED,
                   c->d.prior == KCG_PRIOR_D2};
@@ -763,7 +771,9 @@ kcg_status solve_impl(kcg_ctx* c, Route route, const double* Y_in, double* mu_ou
     } else if (c->d.cg_variant == KCG_CG_HS)
       CKL(kcg::launch_hs_xfix(Kk, s, R.state, R.p[0], R.p[1], mur(j), n_sys, c->side, c->pitch), "x fix-up kernel");
     else if (KCG_X2)
-      CKL(kcg::launch_xfix(Kk, s, R.state, R.p[0], R.p[1], mur(j), n_sys, geom_of(c, R)), "x fix-up kernel");
+      CKL(kcg::launch_xfix(Kk, c->d.prior == KCG_PRIOR_D2 ? 0 : kcg::cg_tile_y(Kk), s, R.state, R.p[0], R.p[1],
+                           mur(j), n_sys, geom_of(c, R)),
+          "x fix-up kernel");
     if (!kron) CKL(kcg::launch_backtransform(k, s, R.W_dev, mur(j), P, N), "backtransform kernel");
   }
   // true residual ||b - G x|| / ||b|| (one apply pass; x boundary rows exchanged in slab mode)
@@ -810,14 +820,20 @@ kcg_status solve_impl(kcg_ctx* c, Route route, const double* Y_in, double* mu_ou
 
   // report (every rank holds the same scalars; residual sums added over ranks in rank order)
   int worst = KCG_OK, maxit = 0, allconv = 1;
-  long long sumit = 0, passes = 0, xpasses = 0;
+  long long sumit = 0, passes = 0;
+  double xpasses = 0.0;
+  // tiles of class 1 (odd index) of the tile kernel's mixed x schedule (KCG_XMIX), per system
+  const bool xmix = KCG_X2 && KCG_XMIX && c->d.prior != KCG_PRIOR_D2;
+  const double frac1 = xmix ? kcg_xclass1_frac(kron ? c->tiles_x_kron : c->tiles_x_syl,
+                                               kron ? c->tiles_y_kron : c->tiles_y_syl) : 0.0;
   double maxrel = 0.0;
   for (int i = 0; i < n_sys; ++i) {
     const SysState& z = c->st_host[i];
     maxit = std::max(maxit, z.iters);
     sumit += z.iters;
     passes += z.iters + 1;
-    xpasses += KCG_X2 ? z.iters / 2 : z.iters;
+    // x passes: class 0 the even q in [2, iters], class 1 the odd q in [1, iters]
+    xpasses += KCG_X2 ? (1.0 - frac1) * (z.iters / 2) + frac1 * ((z.iters + 1) / 2) : (double)z.iters;
     maxrel = std::max(maxrel, z.rel);
     if (z.status != kcg::ST_CONVERGED) allconv = 0;
     int code = KCG_OK;
@@ -1085,7 +1101,9 @@ kcg_status kohler_impl(kcg_ctx* c, const double* Y_in, double* mu_out, double to
       CKL(kcg::launch_hs_xfix(1, s, R.state, R.p[0], R.p[1], xcol, P, c->side, c->pitch), "x fix-up kernel");
     } else {
       CKL(kcg::launch_cg(1, prec, d2, s, a, maps, grid, c->smem_syl), "cg kernel (kohler column)");
-      if (KCG_X2) CKL(kcg::launch_xfix(1, s, R.state, R.p[0], R.p[1], xcol, P, geom_of(c, R)), "x fix-up kernel");
+      if (KCG_X2)
+        CKL(kcg::launch_xfix(1, d2 ? 0 : kcg::cg_tile_y(1), s, R.state, R.p[0], R.p[1], xcol, P, geom_of(c, R)),
+            "x fix-up kernel");
     }
     if (k > 1) CKL(kcg::launch_column_copy(s, xcol, mur, P, k, i, N), "column copy kernel");
     CK(cudaMemcpyAsync(st.data() + (size_t)i * P, R.state, P * sizeof(SysState), cudaMemcpyDeviceToHost, s), "D2H");
@@ -1101,13 +1119,15 @@ kcg_status kohler_impl(kcg_ctx* c, const double* Y_in, double* mu_out, double to
   CK(cudaEventRecord(c->ev[3], s), "event");
   CK(cudaStreamSynchronize(s), "kohler solve");
   int worst = KCG_OK, maxit = 0, allconv = 1;
-  long long sumit = 0, passes = 0, xpasses = 0;
+  long long sumit = 0, passes = 0;
+  double xpasses = 0.0;
+  const double frac1 = KCG_X2 && KCG_XMIX && !d2 ? kcg_xclass1_frac(c->tiles_x_syl, c->tiles_y_syl) : 0.0;  // K = 1
   double maxrel = 0.0;
   for (const SysState& z : st) {
     maxit = std::max(maxit, z.iters);
     sumit += z.iters;
     passes += z.iters + 1;
-    xpasses += KCG_X2 ? z.iters / 2 : z.iters;
+    xpasses += KCG_X2 ? (1.0 - frac1) * (z.iters / 2) + frac1 * ((z.iters + 1) / 2) : (double)z.iters;
     maxrel = std::max(maxrel, z.rel);
     if (z.status != kcg::ST_CONVERGED) allconv = 0;
     int code = KCG_OK;

@@ -54,6 +54,23 @@ namespace kcg {
 #ifndef KCG_X2
 #define KCG_X2 1            // update x every other pass (x += a_{q-1} p_{q-1} + a_q p_q): 40kN B/iter
 #endif
+#ifndef KCG_XMIX
+#define KCG_XMIX 0          // 1 / 2: X2 with the x updates of tile class 1 (index / row parity) on the odd passes (measured slower)
+#endif
+// X2 schedule of the tile CG kernel: a tile of class (tile & 1) (KCG_XMIX; else class 0) updates x on
+// the passes q >= 1 with (q & 1) == class, q >= 2 for class 0, so each pass carries half of the x
+// traffic instead of every other pass carrying all of it.  After the last pass q = iters, a tile's
+// pending alpha_q p_q is the one of a pass that was not its x pass (xfix_kernel).
+// tile class: KCG_XMIX 1 = tile index parity, 2 = tile-row parity, 0 = class 0 everywhere
+__host__ __device__ constexpr int cg_xclass(int ty, int tx, int tiles_x) {
+  return KCG_XMIX == 1 ? ((ty * tiles_x + tx) & 1) : KCG_XMIX == 2 ? (ty & 1) : 0;
+}
+__host__ __device__ constexpr bool cg_xpass(int q, int cls) {
+  return KCG_X2 ? (cls ? (q & 1) == 1 : (q >= 2 && (q & 1) == 0)) : q >= 1;
+}
+__host__ __device__ constexpr bool cg_xpending(int iters, int cls) {
+  return KCG_X2 && iters > 0 && !cg_xpass(iters, cls);
+}
 __host__ __device__ constexpr int cg_tile_y(int K) { return K == 1 ? KCG_TY1 : (K <= 3 ? 16 : (K == 4 ? KCG_TY4 : 8)); }
 __host__ __device__ constexpr int cg_threads(int K) { return K == 1 ? 256 : (K <= 3 ? 512 : (K == 4 ? KCG_NT4 : 256)); }
 __host__ __device__ constexpr int cg_stages(int K) { return 2; }
@@ -279,7 +296,7 @@ cudaError_t launch_resid(int K, cudaStream_t s, const SysParams* params, const d
                          const double* Y, const double* E, const double* hits, double* partials,
                          double* out, int n_sys, int n, const SlabGeom& g, const double* xg_top,
                          const double* xg_bot);
-cudaError_t launch_xfix(int K, cudaStream_t s, const SysState* st, const double* p0, const double* p1, double* x,
+cudaError_t launch_xfix(int K, int tile_y, cudaStream_t s, const SysState* st, const double* p0, const double* p1, double* x,
                         int n_sys, const SlabGeom& g);
 cudaError_t launch_backtransform(int K, cudaStream_t s, const double* W, double* x, int P, size_t N);
 cudaError_t launch_sub_pitched(cudaStream_t s, double* r, const double* v, size_t planes, int side, int pitch);

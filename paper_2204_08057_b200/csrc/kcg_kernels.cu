@@ -180,15 +180,20 @@ __global__ void __launch_bounds__(256) reduce_pairs_kernel(const double* __restr
 }
 
 // --------------------------------------------------------------------------- X2 fix-up
-// x += alpha_last p for every system whose last pass left its x increment pending (odd `iters`,
-// KCG_X2); p = the system's current p planes (buffer `parity`, row pitch `pitch`).
+// x += alpha_last p for every pixel whose tile's last pass left its x increment pending
+// (cg_xpending, KCG_X2); p = the system's current p planes (buffer `parity`, row pitch `pitch`).
+// tile_y > 0: the tile CG kernel's per-tile schedule (tiles KCG_TX x tile_y, local rows; KCG_XMIX);
+// tile_y = 0: every pixel in class 0 (the row-march kernel's uniform schedule).
 template <int K>
 __global__ void __launch_bounds__(256) xfix_kernel(const SysState* __restrict__ st, const double* __restrict__ p0,
                                                    const double* __restrict__ p1, double* __restrict__ x, int side,
-                                                   int rows, int pitch, int ghost) {
+                                                   int rows, int pitch, int ghost, int tile_y) {
   const int s = blockIdx.y;
   const SysState z = st[s];
-  if (!KCG_X2 || (z.iters & 1) == 0) return;
+  if (!KCG_X2 || z.iters == 0) return;
+  const bool pend0 = cg_xpending(z.iters, 0), pend1 = cg_xpending(z.iters, 1);
+  if (!pend0 && !(tile_y > 0 && pend1)) return;
+  const int tiles_x = (side + KCG_TX - 1) / KCG_TX;
   const double al = z.alpha_last;
   const size_t ps = (size_t)pitch * (rows + 2 * ghost);
   const double* p = (z.parity ? p1 : p0) + (size_t)s * K * ps + (size_t)ghost * pitch;
@@ -196,6 +201,8 @@ __global__ void __launch_bounds__(256) xfix_kernel(const SysState* __restrict__ 
   double* xs = x + (size_t)s * K * N;
   for (size_t j = (size_t)blockIdx.x * blockDim.x + threadIdx.x; j < N; j += (size_t)gridDim.x * blockDim.x) {
     const size_t gy = j / side, gx = j - gy * side;
+    const int cls = tile_y > 0 ? cg_xclass((int)(gy / tile_y), (int)(gx / KCG_TX), tiles_x) : 0;
+    if (!(cls ? pend1 : pend0)) continue;
 #pragma unroll
     for (int c = 0; c < K; ++c) xs[c * N + j] = fma(al, p[(size_t)c * ps + gy * pitch + gx], xs[c * N + j]);
   }
@@ -392,11 +399,11 @@ cudaError_t launch_sub_pitched(cudaStream_t s, double* r, const double* v, size_
   return cudaGetLastError();
 }
 
-cudaError_t launch_xfix(int K, cudaStream_t s, const SysState* st, const double* p0, const double* p1, double* x,
-                        int n_sys, const SlabGeom& g) {
+cudaError_t launch_xfix(int K, int tile_y, cudaStream_t s, const SysState* st, const double* p0, const double* p1,
+                        double* x, int n_sys, const SlabGeom& g) {
   const size_t N = (size_t)g.rows * g.side;
   dim3 gr(grid_for(N), n_sys);
-  KCG_DISPATCH(K, (xfix_kernel<KK><<<gr, 256, 0, s>>>(st, p0, p1, x, g.side, g.rows, g.pitch, g.ghost)));
+  KCG_DISPATCH(K, (xfix_kernel<KK><<<gr, 256, 0, s>>>(st, p0, p1, x, g.side, g.rows, g.pitch, g.ghost, tile_y)));
   return cudaGetLastError();
 }
 
