@@ -1238,7 +1238,7 @@ static cudaError_t cg_config_t(bool slab, bool d2, int n_sys, int* max_grid, siz
   int nt = cg_threads(K);
   if (d2) {  // the row-march kernel (kcg_march.cuh)
     if constexpr (K <= 4) kern = (const void*)cg_march_kernel<K, HITS, PREC>;
-    sm += (size_t)m_groups(K) * m_group_doubles(K) * 8;
+    sm += (size_t)m_groups(K) * m_group_doubles(K, PREC) * 8;
     nt = m_threads(K);
   } else {
     kern = slab ? (const void*)cg_slab_kernel<K, HITS, PREC> : (const void*)cg_persistent_kernel<K, HITS, PREC>;

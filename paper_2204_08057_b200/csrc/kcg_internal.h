@@ -105,16 +105,30 @@ __host__ __device__ constexpr int m_kp(int K) { return K == 4 ? KCG_MKP4 : 1; } 
 __host__ __device__ constexpr int m_gw(int K) { return K / m_kp(K); }            // warps per group
 __host__ __device__ constexpr int m_cp(int K) { return K == 1 ? KCG_MCP1 : 1; }  // columns per lane
 __host__ __device__ constexpr int m_out(int K) { return 32 * m_cp(K) - 2 * KCG_MHALO; }  // output columns
+#ifndef KCG_MG4
+#define KCG_MG4 6           // K = 4 (two planes per warp): groups per CTA
+#endif
+#ifndef KCG_MST4
+#define KCG_MST4 4          // K = 4 (two planes per warp): TMA row stages per group (power of 2)
+#endif
+#ifndef KCG_MG1
+#define KCG_MG1 12          // K = 1 (two columns per lane): groups per CTA
+#endif
+#ifndef KCG_MST1
+#define KCG_MST1 4          // K = 1 (two columns per lane): TMA row stages per group (power of 2)
+#endif
 __host__ __device__ constexpr int m_groups(int K) {
-  return K == 1 ? (m_cp(K) == 2 ? 12 : 16)
-                : (K == 2 ? 8 : (K == 3 ? 5 : (m_kp(K) == 1 ? 4 : (m_kp(K) == 2 ? 6 : 8))));
+  return K == 1 ? (m_cp(K) == 2 ? KCG_MG1 : 16)
+                : (K == 2 ? 8 : (K == 3 ? 5 : (m_kp(K) == 1 ? 4 : (m_kp(K) == 2 ? KCG_MG4 : 8))));
 }
 __host__ __device__ constexpr int m_threads(int K) { return m_groups(K) * m_gw(K) * 32; }
-__host__ __device__ constexpr int m_stages(int K) { return (m_kp(K) == 2 || m_cp(K) == 2) ? 4 : 8; }  // (smem)
+__host__ __device__ constexpr int m_stages(int K) {  // (shared memory)
+  return m_kp(K) == 2 ? KCG_MST4 : (m_cp(K) == 2 ? KCG_MST1 : 8);
+}
 __host__ __device__ constexpr int m_stage_doubles(int K) { return (3 * K + 1) * 32 * m_cp(K); }
 // doubles of one group's shared memory: the stage ring + 3 exchange rings [4 rows][K][32 cp]
-__host__ __device__ constexpr int m_group_doubles(int K) {
-  return m_stages(K) * m_stage_doubles(K) + 3 * 4 * K * 32 * m_cp(K);
+__host__ __device__ constexpr int m_group_doubles(int K, bool prec) {  // (u_new ring with block-Jacobi only)
+  return m_stages(K) * m_stage_doubles(K) + (prec ? 3 : 2) * 4 * K * 32 * m_cp(K);
 }
 __host__ __device__ constexpr int m_strips(int side, int K) { return (side + m_out(K) - 1) / m_out(K); }
 __host__ __device__ constexpr int m_blocks(int side) { return (side + KCG_MPB - 1) / KCG_MPB; }

@@ -49,7 +49,7 @@ __global__ void __launch_bounds__(m_threads(K), 1) cg_march_kernel(const CgArgs 
   constexpr int NG = m_groups(K), NT = m_threads(K), NW = NT / 32, NS = m_stages(K), SD = m_stage_doubles(K);
   constexpr int KP = m_kp(K), GW = m_gw(K), CP = m_cp(K);  // planes per warp, warps per group, columns per lane
   constexpr int BW = 32 * CP;                                 // box width (one stage row of a plane)
-  constexpr int XR = 4 * K * BW, GD = m_group_doubles(K);
+  constexpr int XR = 4 * K * BW, GD = m_group_doubles(K, PREC);
   constexpr int MO = m_out(K), MH = KCG_MHALO, PB = KCG_MPB;
   constexpr int NP = PREC ? 3 : 2;
   constexpr int DL = PREC ? 5 : 4;  // row of C1 behind the input row
