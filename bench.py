@@ -458,6 +458,12 @@ def _variance_leg(ctx, timed, args, K, N, n_probes=4):
     roof["avg_launch_ms"] /= n_probes
     roof["algorithmic_bytes_per_launch"] /= n_probes
     roof["bytes_moved"]["per_launch"] /= n_probes
+    tr = _traffic(f"{args.config}/variance")  # DRAM bytes of one probe solve's CG launch (ncu)
+    if tr:
+        tl = roof["avg_launch_ms"] * 1e-3
+        roof["traffic"] = tr
+        roof["ncu_dram"] = {"per_launch": tr, "achieved": tr / tl / 1e9, "frac": tr / tl / 1e9 / roof["peak"],
+                            "source": f"profiles/ncu_traffic.json[{args.config}/variance]"}
     return {"value": len(reps) * n_probes / t, "unit": "probe solves/s (all faces of the rank per probe)",
             "probes_per_step": n_probes, "ms_per_step": t / len(reps) * 1e3,
             "face_iterations_per_probe": reps[-1]["system_iterations"] / n_probes,
