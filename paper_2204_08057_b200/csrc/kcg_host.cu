@@ -18,6 +18,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <functional>
 #include <memory>
 #include <string>
 #include <vector>
@@ -623,7 +624,8 @@ kcg_status exchange_x_rows(kcg_ctx* c, const double* x_all, size_t x_rank_stride
 enum InputMode { IN_Y = 0, IN_B_USER = 1, IN_B_WORK = 2 };
 
 kcg_status solve_impl(kcg_ctx* c, Route route, const double* Y_in, double* mu_out, bool host_io, double tol,
-                      int max_iter, kcg_report* rep, InputMode inmode = IN_Y, const double* x0 = nullptr) {
+                      int max_iter, kcg_report* rep, InputMode inmode = IN_Y, const double* x0 = nullptr,
+                      const std::function<kcg_status()>* after_launch = nullptr) {
   Nvtx nv_(route == ROUTE_KRON ? "kcg:kron_cg_solve" : "kcg:sylvester_solve");
   if (!c) return KCG_E_ARG;
   if (x0 && (route != ROUTE_KRON || host_io || c->slab || inmode != IN_Y || c->d.cg_variant != KCG_CG_SINGLE_PASS)) {
@@ -805,6 +807,12 @@ kcg_status solve_impl(kcg_ctx* c, Route route, const double* Y_in, double* mu_ou
   for (int j = 0; j < c->nlocal; ++j)
     if (c->R[j].x_rm && inmode != IN_B_WORK)
       CKL(kcg::launch_permute(s, c->R[j].x_rm, muu(j), (size_t)P * k, c->side, true), "permute mu");
+  // the solve's device work is queued: the caller's hook (kron_cg_solve_host_many: the next batch's H2D
+  // and the previous batch's D2H) goes in now, so a host-blocking copy call cannot delay these kernels
+  if (after_launch) {
+    const kcg_status e = (*after_launch)();
+    if (e != KCG_OK) return e;
+  }
   c->st_host.resize(n_sys);
   const int nr = c->slab ? c->nranks : 1;
   c->resid_host.resize((size_t)nr * P * 2);
@@ -1663,18 +1671,34 @@ kcg_status kron_cg_solve_host_many(kcg_ctx* c, int nbatch, const double* const* 
   CK(cudaMemcpyAsync(Ys[0], Y_host[0], yb, cudaMemcpyHostToDevice, c->h2d_stream), "H2D Y");
   CK(cudaEventRecord(c->ev_h2d[0], c->h2d_stream), "event");
   kcg_status worst = KCG_OK;
+  // D2H of batch j's mu on the copy stream, after its solve (event ev_solved[j & 1])
+  auto d2h = [&](int j) -> kcg_status {
+    CK(cudaStreamWaitEvent(c->d2h_stream, c->ev_solved[j & 1], 0), "wait");
+    CK(cudaMemcpyAsync(mu_host[j], Ms[j & 1], mb, cudaMemcpyDeviceToHost, c->d2h_stream), "D2H mu");
+    CK(cudaEventRecord(c->ev_d2h[j & 1], c->d2h_stream), "event");
+    return KCG_OK;
+  };
   for (int i = 0; i < nbatch; ++i) {
     const int b = i & 1;
-    if (i + 1 < nbatch) {  // staging buffer b^1 was read by solve i-1, which has returned
-      CK(cudaMemcpyAsync(Ys[b ^ 1], Y_host[i + 1], yb, cudaMemcpyHostToDevice, c->h2d_stream), "H2D Y");
-      CK(cudaEventRecord(c->ev_h2d[b ^ 1], c->h2d_stream), "event");
-    }
     CK(cudaStreamWaitEvent(s, c->ev_h2d[b], 0), "wait");
     if (i >= 2) CK(cudaStreamWaitEvent(s, c->ev_d2h[b], 0), "wait");  // mu of batch i-2 copied out
     kcg_report tmp{};
     kcg_report* rp = reports ? reports + i : &tmp;
     c->nlaunch = 0;  // per batch: rp->kernel_launches counts this solve's launches
-    const kcg_status st = solve_impl(c, ROUTE_KRON, Ys[b], Ms[b], false, tol, max_iter, rp);
+    // once solve i is queued: batch i-1's D2H, then batch i+1's H2D into staging buffer b^1 (read by
+    // solve i-1, which has returned)
+    const std::function<kcg_status()> hook = [&]() -> kcg_status {
+      if (i >= 1) {
+        const kcg_status e = d2h(i - 1);
+        if (e != KCG_OK) return e;
+      }
+      if (i + 1 < nbatch) {
+        CK(cudaMemcpyAsync(Ys[b ^ 1], Y_host[i + 1], yb, cudaMemcpyHostToDevice, c->h2d_stream), "H2D Y");
+        CK(cudaEventRecord(c->ev_h2d[b ^ 1], c->h2d_stream), "event");
+      }
+      return KCG_OK;
+    };
+    const kcg_status st = solve_impl(c, ROUTE_KRON, Ys[b], Ms[b], false, tol, max_iter, rp, IN_Y, nullptr, &hook);
     if (st != KCG_OK && st != KCG_NOT_CONVERGED) {
       cudaStreamSynchronize(c->h2d_stream);
       cudaStreamSynchronize(c->d2h_stream);
@@ -1682,9 +1706,10 @@ kcg_status kron_cg_solve_host_many(kcg_ctx* c, int nbatch, const double* const* 
     }
     if (st == KCG_NOT_CONVERGED) worst = st;
     CK(cudaEventRecord(c->ev_solved[b], s), "event");
-    CK(cudaStreamWaitEvent(c->d2h_stream, c->ev_solved[b], 0), "wait");
-    CK(cudaMemcpyAsync(mu_host[i], Ms[b], mb, cudaMemcpyDeviceToHost, c->d2h_stream), "D2H mu");
-    CK(cudaEventRecord(c->ev_d2h[b], c->d2h_stream), "event");
+  }
+  {
+    const kcg_status e = d2h(nbatch - 1);
+    if (e != KCG_OK) return e;
   }
   CK(cudaStreamSynchronize(c->d2h_stream), "D2H");
   CK(cudaStreamSynchronize(c->h2d_stream), "H2D");

@@ -105,3 +105,27 @@ def test_misaligned_mu_rejected():
         with pytest.raises(KcgError) as e:
             fn(Y, mu)
         assert e.value.status == 2
+
+
+@pytest.mark.parametrize("nb", [1, 2, 5])
+def test_solve_host_many_pipeline(nb):
+    """kron_cg_solve_host_many (two staging pairs, copies queued after each solve's kernels): batch i's
+    mu from Ys[i] equals the device-resident solve of the same Y bit for bit (the same kernels on the
+    same data), with the same iteration counts; every batch has its own input, output and report; the
+    first batch is also checked against the oracle."""
+    import torch
+    ps = [make_patch(5, 9, 3, seed=60 + s, tau="loguniform") for s in range(3)]
+    ctx, Y = make_ctx(ps, host_staging=2)
+    Ys = [(Y.cpu() * (1.0 + 0.25 * i)).pin_memory() for i in range(nb)]
+    mus = [torch.full(tuple(ctx.shape_mu), float("nan"), dtype=torch.float64).pin_memory() for _ in range(nb)]
+    reps = ctx.solve_host_many(Ys, mus, tol=TOL)
+    assert len(reps) == nb
+    for i in range(nb):
+        mu_d, rep_d = ctx.solve(Ys[i].cuda(), tol=TOL)
+        assert reps[i]["converged"] and reps[i]["iterations_per"] == rep_d["iterations_per"], (i, reps[i], rep_d)
+        assert torch.equal(mus[i], mu_d.cpu()), i
+    for j, p in enumerate(ps):
+        G, b = model.problem_system(p)
+        ref = cg.cg_hs(G, b, tol=TOL)
+        assert rel(mus[0][j].numpy(), ref.x) <= 1e-8
+        assert abs(reps[0]["iterations_per"][j] - ref.iterations) <= 2
