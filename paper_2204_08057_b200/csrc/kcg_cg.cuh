@@ -755,6 +755,35 @@ __device__ __forceinline__ void cg_tile(const CgArgs& a, const TileCtx& tc, doub
       *rp = rv;
     }
   }
+  // x of tile row j (x passes; phase C): TMA-staged (XTMA), else from L2 (prefetched there by the issue)
+  auto load_x = [&](int j, double2 (&xj)[K]) {
+    const int ly = KCG_ROWMAP ? warp * RPW + j : warp + j * NW;
+    bool in0 = true, in1 = true;
+    if (EDGE) {
+      const bool rin = y0 + ly < rows;
+      in0 = rin && gx < side;
+      in1 = rin && gx + 1 < side;
+    }
+    const double* xp = a.x + ((size_t)s * K * rows + y0 + ly) * side + gx;
+#pragma unroll
+    for (int c = 0; c < K; ++c) {
+      if (XTMA) {
+        xj[c] = reinterpret_cast<const double2*>(tc.xs + ((size_t)c * TY + ly) * TX)[lane];
+      } else if (!EDGE || (in0 && in1)) {
+        xj[c] = __ldcg(reinterpret_cast<const double2*>(xp + c * N));
+      } else {
+        xj[c].x = in0 ? __ldcg(xp + c * N) : 0.0;
+        xj[c].y = in1 ? __ldcg(xp + c * N + 1) : 0.0;
+      }
+    }
+  };
+  // KCG_XEARLY (L2 x only): rows 0 .. XE-1 of x are requested before the phase-B barrier, so their L2
+  // latency overlaps the ring phase and the barrier instead of stalling phase C
+  constexpr int XE = XTMA ? 0 : (KCG_XEARLY >= 2 ? RPW : KCG_XEARLY);
+  double2 xe[XE > 0 ? XE : 1][K];
+  if (XE > 0 && tc.xpass)
+#pragma unroll
+    for (int j = 0; j < XE; ++j) load_x(j, xe[j]);
   // Phase B2: the 1-pixel ring around the tile (scalars).  Ring pixels outside the face are
   // skipped (their r stays 0); in slab mode ring rows beyond the slab are real (ghost) pixels.
   for (int t0 = 0; t0 < RP; t0 += NT) {
@@ -850,16 +879,11 @@ __device__ __forceinline__ void cg_tile(const CgArgs& a, const TileCtx& tc, doub
     double* xp = a.x + ((size_t)s * K * rows + y0 + ly) * side + gx;
     double2 xj[K];
     if (tc.xpass) {
+      if (j < XE) {
 #pragma unroll
-      for (int c = 0; c < K; ++c) {
-        if (XTMA) {
-          xj[c] = reinterpret_cast<const double2*>(tc.xs + ((size_t)c * TY + ly) * TX)[lane];
-        } else if (!EDGE || (in0 && in1)) {
-          xj[c] = __ldcg(reinterpret_cast<const double2*>(xp + c * N));
-        } else {
-          xj[c].x = in0 ? __ldcg(xp + c * N) : 0.0;
-          xj[c].y = in1 ? __ldcg(xp + c * N + 1) : 0.0;
-        }
+        for (int c = 0; c < K; ++c) xj[c] = xe[j < XE ? j : 0][c];
+      } else {
+        load_x(j, xj);
       }
     }
     double2 rc[K], sc[K];

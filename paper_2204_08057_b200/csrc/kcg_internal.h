@@ -54,6 +54,9 @@ namespace kcg {
 #ifndef KCG_X2
 #define KCG_X2 1            // update x every other pass (x += a_{q-1} p_{q-1} + a_q p_q): 40kN B/iter
 #endif
+#ifndef KCG_XEARLY
+#define KCG_XEARLY 0        // tile kernel, x from L2: rows of x requested before the phase-B barrier (1: row 0, 2: all)
+#endif
 #ifndef KCG_XMIX
 #define KCG_XMIX 0          // 1 / 2: X2 with the x updates of tile class 1 (index / row parity) on the odd passes (measured slower)
 #endif
