@@ -600,7 +600,9 @@ def run_b200(args):
     from paper_2204_08057_b200.kroncg import KronCG
     from synth.problems import stack
 
-    problems, mine, costs, g, slab = _patches_for(args.config, world, rank, args.shard_only)
+    from synth import CONFIGS
+    whole = args.shard_only or (not args.row_slabs and len(CONFIGS[args.config]["seeds"]) >= world)
+    problems, mine, costs, g, slab = _patches_for(args.config, world, rank, whole)
     st = stack(problems)
     K, N = problems[0].k, problems[0].N
     if g == 1:
@@ -817,6 +819,11 @@ def main():
     ap.add_argument("--no-small", action="store_true", help="skip the tiny / medium (resident kernel) legs")
     ap.add_argument("--shard-only", action="store_true",
                     help="N > 1: whole faces per rank only (no row-slab groups), e.g. several ranks on one GPU")
+    ap.add_argument("--row-slabs", action="store_true",
+                    help="N > 1 with at least as many faces as ranks: let the planner split faces into row slabs "
+                         "(sharding.plan_groups).  Off by default: the cross-GPU slab solve (kernels spinning on "
+                         "each other's flags over NVLink) cannot run on this one-GPU pool, and on fullsky the model "
+                         "gains 2%% at 8 ranks (32.2 vs 32.9 face-passes).  Single-face configs always use slabs")
     ap.add_argument("--lanczos-cap", type=int, default=128,
                     help="Lanczos steps provisioned (HBM-resident basis: P k N 8 (cap + 1) bytes)")
     ap.add_argument("--ref-iters", type=int, default=2, help="oracle CG iterations per face per reference step")
