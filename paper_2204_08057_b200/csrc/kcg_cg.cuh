@@ -555,6 +555,8 @@ __device__ __forceinline__ void cg_tile(const CgArgs& a, const TileCtx& tc, doub
   constexpr int NT = cg_threads(K), NW = NT / 32, RPW = TY / NW;
   constexpr int RP = 2 * (TX + 2) + 2 * TY;  // ring points
   static_assert(TX == 64 && RPW * NW == TY, "pair mapping needs TX = 64 and NW | TY");
+  constexpr bool FUSE = cg_fuse(K, PREC);  // phases A and B fused, r_new into the U box (KCG_FUSEAB)
+  static_assert(!FUSE || KCG_ROWMAP, "the fused phases need consecutive rows per warp");
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int side = a.side, rows = SLAB ? a.rows : side, row0 = SLAB ? a.row0 : 0, ghost = SLAB ? a.ghost : 0;
   const size_t N = (size_t)rows * side;                   // pixels of one local plane
@@ -586,10 +588,183 @@ __device__ __forceinline__ void cg_tile(const CgArgs& a, const TileCtx& tc, doub
 #pragma unroll
     for (int c = 0; c < K; ++c) tau[c] = KCG_PREC_SMEM_A ? tc.Ms[K * K + c] : __ldg(&tc.sp->tau[c]);
 
+  // x of tile row j (x passes; phase C): TMA-staged (XTMA), else from L2 (prefetched there by the issue)
+  auto load_x = [&](int j, double2 (&xj)[K]) {
+    const int ly = KCG_ROWMAP ? warp * RPW + j : warp + j * NW;
+    bool in0 = true, in1 = true;
+    if (EDGE) {
+      const bool rin = y0 + ly < rows;
+      in0 = rin && gx < side;
+      in1 = rin && gx + 1 < side;
+    }
+    const double* xp = a.x + ((size_t)s * K * rows + y0 + ly) * side + gx;
+#pragma unroll
+    for (int c = 0; c < K; ++c) {
+      if (XTMA) {
+        xj[c] = reinterpret_cast<const double2*>(tc.xs + ((size_t)c * TY + ly) * TX)[lane];
+      } else if (!EDGE || (in0 && in1)) {
+        xj[c] = __ldcg(reinterpret_cast<const double2*>(xp + c * N));
+      } else {
+        xj[c].x = in0 ? __ldcg(xp + c * N) : 0.0;
+        xj[c].y = in1 ? __ldcg(xp + c * N + 1) : 0.0;
+      }
+    }
+  };
+  // KCG_XEARLY (L2 x only): rows 0 .. XE-1 of x are requested before the phase-B barrier, so their L2
+  // latency overlaps the ring phase and the barrier instead of stalling phase C
+  constexpr int XE = XTMA ? 0 : (KCG_XEARLY >= 2 ? RPW : KCG_XEARLY);
+  double2 xe[XE > 0 ? XE : 1][K];
+  double2 xinc[RPW][K];
+  if constexpr (FUSE) {
+    // ---- Phase AB (KCG_FUSEAB, no preconditioner; no CTA barrier between A and B): warp w owns the
+    // tile rows ly = w RPW + j.  p_new = r + beta p of its rows and of the rows just above / below (the
+    // neighbour warps' rows, recomputed) sits in registers, the edge columns -1 / TX come from broadcast
+    // loads; r_new of its rows goes to the U box (tile + 1 ring, row pitch BW, U row = tile row + 1)
+    // -- the R and P boxes stay read-only, so the ring phase below can form p_new itself; p_new is
+    // final here and is stored at once; the x increment waits in registers for phase C.
+    const double* __restrict__ Mg = tc.sp->M;  // (the shared copy is written per tile without a barrier)
+    double taug[K];
+#pragma unroll
+    for (int c = 0; c < K; ++c) taug[c] = __ldg(&tc.sp->tau[c]);
+    const double ap = tc.alpha_prev;
+    const double2* R2 = reinterpret_cast<const double2*>(R);
+    const double2* P2 = reinterpret_cast<const double2*>(Pp);
+    double2* U2 = reinterpret_cast<double2*>(tc.U);
+    double2 pr[RPW + 2][K];  // p_new of box rows warp RPW + H - 1 + i
+#pragma unroll
+    for (int i = 0; i < RPW + 2; ++i) {
+      const int by = warp * RPW + H - 1 + i;
+#pragma unroll
+      for (int c = 0; c < K; ++c) {
+        const int e = by * (BW / 2) + 1 + lane + c * (PLANE / 2);
+        const double2 r = R2[e], po = P2[e];
+        pr[i][c] = make_double2(fma(beta, po.x, r.x), fma(beta, po.y, r.y));
+        if (i >= 1 && i <= RPW) {
+          xinc[i - 1 < RPW ? i - 1 : 0][c] = make_double2(fma(alpha, pr[i][c].x, ap * po.x), fma(alpha, pr[i][c].y, ap * po.y));
+        }
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < RPW; ++j) {
+      const int ly = warp * RPW + j;  // local tile row
+      const int by = ly + H;          // box row
+      const int gyg = row0 + y0 + ly;
+      bool in0 = true, in1 = true;
+      double kd0 = kappa2 + 4.0, kd1 = kappa2 + 4.0;
+      if (EDGE) {
+        const bool rin = y0 + ly < rows;
+        in0 = rin && gx < side;
+        in1 = rin && gx + 1 < side;
+        kd0 = kappa2 + degree(gyg, gx);
+        kd1 = kappa2 + degree(gyg, gx + 1);
+      }
+      bool up0 = in0, up1 = in1;
+      if (EDGE && SLAB) {
+        const bool rin1 = y0 + ly <= rows;
+        up0 = rin1 && in_face(gyg, gx);
+        up1 = rin1 && in_face(gyg, gx + 1);
+      }
+      const double h0 = HITS && up0 ? hit(y0 + ly, gx) : 1.0, h1 = HITS && up1 ? hit(y0 + ly, gx + 1) : 1.0;
+      const size_t ro = ((size_t)s * K) * ps + (size_t)(y0 + ly + ghost) * a.pitch + gx;
+      double* pout = (tc.par ? a.pbuf[0] : a.pbuf[1]) + ro;
+#pragma unroll
+      for (int c = 0; c < K; ++c) {
+        const double2 pc = pr[j + 1][c], up = pr[j][c], dn = pr[j + 2][c];
+        const double* rowR = R + c * PLANE + by * BW;
+        const double* rowP = Pp + c * PLANE + by * BW;
+        const double el = fma(beta, rowP[H - 1], rowR[H - 1]), er = fma(beta, rowP[H + TX], rowR[H + TX]);
+        double left = __shfl_up_sync(0xffffffffu, pc.y, 1);
+        double right = __shfl_down_sync(0xffffffffu, pc.x, 1);
+        left = lane == 0 ? el : left;
+        right = lane == 31 ? er : right;
+        const double nb0 = (up.x + dn.x) + (left + pc.y);
+        const double nb1 = (up.y + dn.y) + (pc.x + right);
+        double mix0 = 0.0, mix1 = 0.0;
+#pragma unroll
+        for (int d = 0; d < K; ++d) {
+          const double m = __ldg(&Mg[c * K + d]);
+          mix0 = fma(m, pr[j + 1][d].x, mix0);
+          mix1 = fma(m, pr[j + 1][d].y, mix1);
+        }
+        const double q0 = op_point<HITS>(h0, mix0, taug[c], kd0, pc.x, nb0);
+        const double q1 = op_point<HITS>(h1, mix1, taug[c], kd1, pc.y, nb1);
+        const double2 r = R2[by * (BW / 2) + 1 + lane + c * (PLANE / 2)];
+        double2 rn = r;
+        if (up0) rn.x = fma(-alpha, q0, r.x);
+        if (up1) rn.y = fma(-alpha, q1, r.y);
+        U2[(ly + 1) * (BW / 2) + 1 + lane + c * (UPLANE / 2)] = rn;
+        if constexpr (SLAB) {  // boundary rows of p_new also land in the neighbour's ghost rows
+          const int lyy = y0 + ly;
+          const int bsel = tc.par ? 0 : 1;
+          const size_t so = ((size_t)s * K + c) * ps + gx;
+#pragma unroll
+          for (int dir = 0; dir < 2; ++dir) {
+            if (a.nb_p[dir][bsel] == nullptr) continue;
+            const int nrow = dir == 0 ? rows + ghost + lyy : lyy - (rows - ghost);
+            if (dir == 0 ? lyy >= ghost : lyy < rows - ghost) continue;
+            double* npp = a.nb_p[dir][bsel] + so + (size_t)nrow * a.pitch;
+            if (!EDGE || (in0 && in1)) {
+              *reinterpret_cast<double2*>(npp) = pc;
+            } else {
+              if (in0) npp[0] = pc.x;
+              if (in1) npp[1] = pc.y;
+            }
+          }
+        }
+        if (!EDGE || (in0 && in1)) {
+          *reinterpret_cast<double2*>(pout + c * ps) = pc;
+        } else {
+          if (in0) pout[c * ps] = pc.x;
+          if (in1) pout[c * ps + 1] = pc.y;
+        }
+      }
+    }
+    if (XE > 0 && tc.xpass)
+#pragma unroll
+      for (int j = 0; j < XE; ++j) load_x(j, xe[j]);
+    // Phase B2 (fused form): r_new on the 1-pixel ring into the U box; p_new of a ring point and of
+    // its four neighbours formed from the read-only R and P boxes.  Ring pixels outside the face get 0.
+    for (int t0 = 0; t0 < RP; t0 += NT) {
+      const int t = t0 + tid;
+      if (t >= RP) continue;
+      int by, bx;
+      if (t < TX + 2) { by = H - 1; bx = H - 1 + t; }
+      else if (t < 2 * (TX + 2)) { by = H + TY; bx = H - 1 + (t - (TX + 2)); }
+      else { const int u = t - 2 * (TX + 2); by = H + (u >> 1); bx = (u & 1) ? H + TX : H - 1; }
+      const int ly = y0 - H + by, gxr = x0 - H + bx, gyg = row0 + ly;
+      double* uo = tc.U + (by - 1) * BW + bx;
+      double kd = kappa2 + 4.0;
+      if (EDGE) {
+        if (!in_face(gyg, gxr)) {
+#pragma unroll
+          for (int c = 0; c < K; ++c) uo[c * UPLANE] = 0.0;
+          continue;
+        }
+        kd = kappa2 + degree(gyg, gxr);
+      }
+      const double h = HITS ? hit(ly, gxr) : 1.0;
+      const int o = by * BW + bx;
+      auto pnew = [&](int c, int off) { return fma(beta, Pp[c * PLANE + o + off], R[c * PLANE + o + off]); };
+      double pcs[K];
+#pragma unroll
+      for (int c = 0; c < K; ++c) pcs[c] = pnew(c, 0);
+#pragma unroll
+      for (int c = 0; c < K; ++c) {
+        const double nb = (pnew(c, -BW) + pnew(c, BW)) + (pnew(c, -1) + pnew(c, 1));
+        double mix = 0.0;
+#pragma unroll
+        for (int d = 0; d < K; ++d) mix = fma(__ldg(&Mg[c * K + d]), pcs[d], mix);
+        uo[c * UPLANE] = fma(-alpha, op_point<HITS>(h, mix, taug[c], kd, pcs[c], nb), R[c * PLANE + o]);
+      }
+    }
+    __syncwarp();
+    __syncthreads();
+#pragma unroll
+    for (int c = 0; c < K; ++c) tau[c] = M[K * K + c];
+  } else {
   // Phase A.  Interior pairs in the pair mapping (the thread keeps its pairs' x increment
   //   xinc = alpha_prev p_old + alpha p_new   (X2: x is updated every other pass)
   // in registers); the 2-pixel frame of the box as a flat loop over double2 units (pixel pairs).
-  double2 xinc[RPW][K];
   {
     double2* P2 = reinterpret_cast<double2*>(Pp);
     const double2* R2 = reinterpret_cast<const double2*>(R);
@@ -755,32 +930,6 @@ __device__ __forceinline__ void cg_tile(const CgArgs& a, const TileCtx& tc, doub
       *rp = rv;
     }
   }
-  // x of tile row j (x passes; phase C): TMA-staged (XTMA), else from L2 (prefetched there by the issue)
-  auto load_x = [&](int j, double2 (&xj)[K]) {
-    const int ly = KCG_ROWMAP ? warp * RPW + j : warp + j * NW;
-    bool in0 = true, in1 = true;
-    if (EDGE) {
-      const bool rin = y0 + ly < rows;
-      in0 = rin && gx < side;
-      in1 = rin && gx + 1 < side;
-    }
-    const double* xp = a.x + ((size_t)s * K * rows + y0 + ly) * side + gx;
-#pragma unroll
-    for (int c = 0; c < K; ++c) {
-      if (XTMA) {
-        xj[c] = reinterpret_cast<const double2*>(tc.xs + ((size_t)c * TY + ly) * TX)[lane];
-      } else if (!EDGE || (in0 && in1)) {
-        xj[c] = __ldcg(reinterpret_cast<const double2*>(xp + c * N));
-      } else {
-        xj[c].x = in0 ? __ldcg(xp + c * N) : 0.0;
-        xj[c].y = in1 ? __ldcg(xp + c * N + 1) : 0.0;
-      }
-    }
-  };
-  // KCG_XEARLY (L2 x only): rows 0 .. XE-1 of x are requested before the phase-B barrier, so their L2
-  // latency overlaps the ring phase and the barrier instead of stalling phase C
-  constexpr int XE = XTMA ? 0 : (KCG_XEARLY >= 2 ? RPW : KCG_XEARLY);
-  double2 xe[XE > 0 ? XE : 1][K];
   if (XE > 0 && tc.xpass)
 #pragma unroll
     for (int j = 0; j < XE; ++j) load_x(j, xe[j]);
@@ -816,6 +965,7 @@ __device__ __forceinline__ void cg_tile(const CgArgs& a, const TileCtx& tc, doub
   }
   __syncwarp();
   __syncthreads();
+  }  // FUSE
 
   if (KCG_TRACE == 2) dump_smem(tc.dump ? tc.dump + 8192 : nullptr, R, K * PLANE);
   // Phase B' (PREC): u_new = K^{-1} r_new on tile + ring into U (row by of the R box = U row by-1).
@@ -849,7 +999,7 @@ __device__ __forceinline__ void cg_tile(const CgArgs& a, const TileCtx& tc, doub
     if (PREC) dump_smem(tc.dump ? tc.dump + 3 * 8192 : nullptr, tc.U, K * UPLANE);
   }
   // Phase C.  Stencil source S = r_new (R box) or u_new (U box, same indexing: U = S + BW).
-  constexpr bool USEU = PREC;
+  constexpr bool USEU = PREC || FUSE;  // (FUSE: the U box holds r_new itself)
   const double* __restrict__ S = USEU ? tc.U - BW : R;
   constexpr int SPLANE = USEU ? UPLANE : PLANE;
   double rr = 0.0, ru = 0.0, wu = 0.0;
@@ -889,7 +1039,7 @@ __device__ __forceinline__ void cg_tile(const CgArgs& a, const TileCtx& tc, doub
     double2 rc[K], sc[K];
 #pragma unroll
     for (int c = 0; c < K; ++c) {
-      if (KCG_ROWMAP && !USEU) {
+      if (KCG_ROWMAP && (!USEU || FUSE)) {
         rc[c] = scs[KCG_ROWMAP ? j : 0][c];
         sc[c] = rc[c];
       } else {
@@ -924,7 +1074,8 @@ __device__ __forceinline__ void cg_tile(const CgArgs& a, const TileCtx& tc, doub
       }
       const double w0 = op_point<HITS>(h0, mix0, tau[c], kd0, sc[c].x, nb0);
       const double w1 = op_point<HITS>(h1, mix1, tau[c], kd1, sc[c].y, nb1);
-      const double2 pn = reinterpret_cast<const double2*>(Pp + c * PLANE + by * BW)[1 + lane];
+      const double2 pn = FUSE ? make_double2(0.0, 0.0)  // (FUSE: p_new stored in phase AB)
+                              : reinterpret_cast<const double2*>(Pp + c * PLANE + by * BW)[1 + lane];
       double2 xn;
       xn.x = xj[c].x + xinc[j][c].x;
       xn.y = xj[c].y + xinc[j][c].y;
@@ -952,27 +1103,27 @@ __device__ __forceinline__ void cg_tile(const CgArgs& a, const TileCtx& tc, doub
           double* npp = a.nb_p[dir][bsel] + so + (size_t)nrow * a.pitch;
           if (!EDGE || (in0 && in1)) {
             *reinterpret_cast<double2*>(nrp) = rc[c];
-            *reinterpret_cast<double2*>(npp) = pn;
+            if (!FUSE) *reinterpret_cast<double2*>(npp) = pn;
           } else {
-            if (in0) { nrp[0] = rc[c].x; npp[0] = pn.x; }
-            if (in1) { nrp[1] = rc[c].y; npp[1] = pn.y; }
+            if (in0) { nrp[0] = rc[c].x; if (!FUSE) npp[0] = pn.x; }
+            if (in1) { nrp[1] = rc[c].y; if (!FUSE) npp[1] = pn.y; }
           }
         }
       }
       if (!EDGE || (in0 && in1)) {
         if (tc.xpass) *reinterpret_cast<double2*>(xp + c * N) = xn;
         *reinterpret_cast<double2*>(rout + c * ps) = rc[c];
-        *reinterpret_cast<double2*>(pout + c * ps) = pn;
+        if (!FUSE) *reinterpret_cast<double2*>(pout + c * ps) = pn;
       } else {
         if (in0) {
           if (tc.xpass) xp[c * N] = xn.x;
           rout[c * ps] = rc[c].x;
-          pout[c * ps] = pn.x;
+          if (!FUSE) pout[c * ps] = pn.x;
         }
         if (in1) {
           if (tc.xpass) xp[c * N + 1] = xn.y;
           rout[c * ps + 1] = rc[c].y;
-          pout[c * ps + 1] = pn.y;
+          if (!FUSE) pout[c * ps + 1] = pn.y;
         }
       }
     }
@@ -1016,7 +1167,7 @@ __device__ __forceinline__ void cg_body(const CgArgs& a, const CgMaps& maps, con
   constexpr int FIELD = K * BW * BH;  // doubles of one field box
   constexpr int XBYTES = cg_xstage_bytes(K);  // x block, TMA-staged with the boxes (0 if disabled)
   constexpr int STAGE_BYTES = 2 * FIELD * 8 + XBYTES;
-  constexpr int UBYTES = PREC ? cg_ubox_bytes(K) : 0;
+  constexpr int UBYTES = (PREC || cg_fuse(K, PREC)) ? cg_ubox_bytes(K) : 0;
   constexpr int NT = cg_threads(K), NW = NT / 32, NS = cg_stages(K);
   constexpr int NP = PREC ? 3 : 2;  // partials per tile
   constexpr int MSZ = K * K + K + (PREC ? 4 * K * K : 0);
@@ -1252,7 +1403,7 @@ struct CgEntry {
 // Dynamic shared memory of one CTA (Laplacian tile kernel): two stages, the PREC u box (+ the states).
 template <int K, bool PREC>
 constexpr size_t cg_dyn_smem_fixed() {
-  return cg_stages(K) * (size_t)cg_stage_bytes(K) + (PREC ? (size_t)cg_ubox_bytes(K) : 0);
+  return cg_stages(K) * (size_t)cg_stage_bytes(K) + ((PREC || cg_fuse(K, PREC)) ? (size_t)cg_ubox_bytes(K) : 0);
 }
 
 template <int K, bool HITS, bool PREC>

@@ -54,6 +54,12 @@ namespace kcg {
 #ifndef KCG_X2
 #define KCG_X2 1            // update x every other pass (x += a_{q-1} p_{q-1} + a_q p_q): 40kN B/iter
 #endif
+#ifndef KCG_FUSEAB
+#define KCG_FUSEAB 1        // tile kernel without a preconditioner: phases A and B fused (no barrier between)
+#endif
+// the fused tile phases: no preconditioner, the r_new box must fit next to the two stages (K <= 6), and
+// K = 1 keeps its two CTAs per SM (the box would cost one)
+__host__ __device__ constexpr bool cg_fuse(int K, bool prec) { return KCG_FUSEAB && !prec && K >= 2 && K <= 6; }
 #ifndef KCG_XEARLY
 #define KCG_XEARLY 0        // tile kernel, x from L2: rows of x requested before the phase-B barrier (1: row 0, 2: all)
 #endif
