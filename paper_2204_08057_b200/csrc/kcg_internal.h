@@ -60,6 +60,9 @@ namespace kcg {
 // the fused tile phases: no preconditioner, the r_new box must fit next to the two stages (K <= 6), and
 // K = 1 keeps its two CTAs per SM (the box would cost one)
 __host__ __device__ constexpr bool cg_fuse(int K, bool prec) { return KCG_FUSEAB && !prec && K >= 2 && K <= 6; }
+#ifndef KCG_MFENCE
+#define KCG_MFENCE 0        // D2 row march: async-proxy fence before every stage refill (only WAR: not needed)
+#endif
 #ifndef KCG_XEARLY
 #define KCG_XEARLY 0        // tile kernel, x from L2: rows of x requested before the phase-B barrier (1: row 0, 2: all)
 #endif

@@ -172,8 +172,13 @@ __global__ void __launch_bounds__(m_threads(K), 1) cg_march_kernel(const CgArgs 
       ++ic;
       ++gi;
     };
-    if (issuer)
+    if (issuer) {
+      // generic-proxy writes to the stages (the zero fill at kernel start) before the async-proxy
+      // TMA writes; afterwards the stages are only read by the generic proxy, and a stage is
+      // refilled after the group barrier that follows its last reads (WAR: no proxy fence needed)
+      if (lane == 0) fence_proxy_async_smem();
       for (int j = 0; j < NS; ++j) advance_issue();
+    }
 
     int cu = cta * NG + g, ku = 0;
     while (cu < units) {
@@ -273,7 +278,7 @@ __global__ void __launch_bounds__(m_threads(K), 1) cg_march_kernel(const CgArgs 
       const uint32_t q0 = gr;                 // the unit's first stage
       auto free_stage = [&]() {               // issuing warp: the oldest held stage is consumed, refill it
         ++gf;
-        if (lane == 0) fence_proxy_async_smem();
+        if (KCG_MFENCE && lane == 0) fence_proxy_async_smem();
         advance_issue();
       };
 
