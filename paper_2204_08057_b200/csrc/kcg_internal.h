@@ -59,7 +59,12 @@ namespace kcg {
 #endif
 // the fused tile phases: no preconditioner, the r_new box must fit next to the two stages (K <= 6), and
 // K = 1 keeps its two CTAs per SM (the box would cost one)
-__host__ __device__ constexpr bool cg_fuse(int K, bool prec) { return KCG_FUSEAB && !prec && K >= 2 && K <= 6; }
+#ifndef KCG_FUSE1
+#define KCG_FUSE1 0         // also fuse K = 1 (then one CTA per SM: use with KCG_NT1 = 512, KCG_MINB1 = 1)
+#endif
+__host__ __device__ constexpr bool cg_fuse(int K, bool prec) {
+  return KCG_FUSEAB && !prec && (K >= 2 || KCG_FUSE1) && K <= 6;
+}
 #ifndef KCG_MFENCE
 #define KCG_MFENCE 0        // D2 row march: async-proxy fence before every stage refill (only WAR: not needed)
 #endif
@@ -83,13 +88,25 @@ __host__ __device__ constexpr bool cg_xpass(int q, int cls) {
 __host__ __device__ constexpr bool cg_xpending(int iters, int cls) {
   return KCG_X2 && iters > 0 && !cg_xpass(iters, cls);
 }
-__host__ __device__ constexpr int cg_tile_y(int K) { return K == 1 ? KCG_TY1 : (K <= 3 ? 16 : (K == 4 ? KCG_TY4 : 8)); }
-__host__ __device__ constexpr int cg_threads(int K) { return K == 1 ? 256 : (K <= 3 ? 512 : (K == 4 ? KCG_NT4 : 256)); }
+#ifndef KCG_TY23
+#define KCG_TY23 16         // tile rows, K = 2, 3 (two rows per warp; profiles/r02/ab_k23_tile_geometry.txt)
+#endif
+#ifndef KCG_NT23
+#define KCG_NT23 256        // threads, K = 2, 3
+#endif
+__host__ __device__ constexpr int cg_tile_y(int K) { return K == 1 ? KCG_TY1 : (K <= 3 ? KCG_TY23 : (K == 4 ? KCG_TY4 : 8)); }
+#ifndef KCG_NT1
+#define KCG_NT1 256         // threads, K = 1
+#endif
+#ifndef KCG_MINB1
+#define KCG_MINB1 2         // resident CTAs per SM, K = 1
+#endif
+__host__ __device__ constexpr int cg_threads(int K) { return K == 1 ? KCG_NT1 : (K <= 3 ? KCG_NT23 : (K == 4 ? KCG_NT4 : 256)); }
 __host__ __device__ constexpr int cg_stages(int K) { return 2; }
 #ifndef KCG_MINB4
 #define KCG_MINB4 1         // resident CTAs per SM, K = 4
 #endif
-__host__ __device__ constexpr int cg_min_blocks(int K) { return K == 1 ? 2 : (K == 4 ? KCG_MINB4 : 1); }
+__host__ __device__ constexpr int cg_min_blocks(int K) { return K == 1 ? KCG_MINB1 : (K == 4 ? KCG_MINB4 : 1); }
 __host__ __device__ constexpr bool cg_xtma(int K) { return K <= KCG_XTMA_MAXK && K <= 6; }  // K>=7: smem
 // Bytes of the x block staged with a tile.
 __host__ __device__ constexpr int cg_xstage_bytes(int K) { return cg_xtma(K) ? K * cg_tile_y(K) * KCG_TX * 8 : 0; }
