@@ -57,14 +57,12 @@ namespace kcg {
 #ifndef KCG_FUSEAB
 #define KCG_FUSEAB 1        // tile kernel without a preconditioner: phases A and B fused (no barrier between)
 #endif
-// the fused tile phases: no preconditioner, the r_new box must fit next to the two stages (K <= 6), and
-// K = 1 keeps its two CTAs per SM (the box would cost one)
+// the fused tile phases (cg_fuse, after the tile geometry below): no preconditioner, the r_new box must
+// fit next to the two stages (K <= 6), and K = 1 keeps its two CTAs per SM (the box would cost one)
 #ifndef KCG_FUSE1
 #define KCG_FUSE1 0         // also fuse K = 1 (then one CTA per SM: use with KCG_NT1 = 512, KCG_MINB1 = 1)
 #endif
-__host__ __device__ constexpr bool cg_fuse(int K, bool prec) {
-  return KCG_FUSEAB && !prec && (K >= 2 || KCG_FUSE1) && K <= 6;
-}
+
 #ifndef KCG_MFENCE
 #define KCG_MFENCE 0        // D2 row march: async-proxy fence before every stage refill (only WAR: not needed)
 #endif
@@ -107,6 +105,11 @@ __host__ __device__ constexpr int cg_stages(int K) { return 2; }
 #define KCG_MINB4 1         // resident CTAs per SM, K = 4
 #endif
 __host__ __device__ constexpr int cg_min_blocks(int K) { return K == 1 ? KCG_MINB1 : (K == 4 ? KCG_MINB4 : 1); }
+// fused phases only with two or more rows per warp (one row per warp, k >= 5: the two recomputed
+// neighbour rows triple the p_new work -- stress 2.66 vs 2.82 solves/s)
+__host__ __device__ constexpr bool cg_fuse(int K, bool prec) {
+  return KCG_FUSEAB && !prec && (K >= 2 || KCG_FUSE1) && K <= 6 && cg_tile_y(K) >= 2 * (cg_threads(K) / 32);
+}
 __host__ __device__ constexpr bool cg_xtma(int K) { return K <= KCG_XTMA_MAXK && K <= 6; }  // K>=7: smem
 // Bytes of the x block staged with a tile.
 __host__ __device__ constexpr int cg_xstage_bytes(int K) { return cg_xtma(K) ? K * cg_tile_y(K) * KCG_TX * 8 : 0; }
