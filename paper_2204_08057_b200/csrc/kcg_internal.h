@@ -133,12 +133,18 @@ __host__ __device__ constexpr int cg_stage_bytes(int K) {
 #ifndef KCG_MCP1
 #define KCG_MCP1 2          // K = 1: face columns per lane (a 64-column box, 56 output columns)
 #endif
+#ifndef KCG_MCP4
+#define KCG_MCP4 1          // K = 4: face columns per lane
+#endif
 __host__ __device__ constexpr int m_kp(int K) { return K == 4 ? KCG_MKP4 : 1; }  // planes per warp
 __host__ __device__ constexpr int m_gw(int K) { return K / m_kp(K); }            // warps per group
-__host__ __device__ constexpr int m_cp(int K) { return K == 1 ? KCG_MCP1 : 1; }  // columns per lane
+__host__ __device__ constexpr int m_cp(int K) { return K == 1 ? KCG_MCP1 : (K == 4 ? KCG_MCP4 : 1); }  // columns per lane
 __host__ __device__ constexpr int m_out(int K) { return 32 * m_cp(K) - 2 * KCG_MHALO; }  // output columns
 #ifndef KCG_MG4
 #define KCG_MG4 6           // K = 4 (two planes per warp): groups per CTA
+#endif
+#ifndef KCG_MG4W
+#define KCG_MG4W 4          // K = 4 (one plane per warp): groups per CTA
 #endif
 #ifndef KCG_MST4
 #define KCG_MST4 4          // K = 4 (two planes per warp): TMA row stages per group (power of 2)
@@ -151,7 +157,7 @@ __host__ __device__ constexpr int m_out(int K) { return 32 * m_cp(K) - 2 * KCG_M
 #endif
 __host__ __device__ constexpr int m_groups(int K) {
   return K == 1 ? (m_cp(K) == 2 ? KCG_MG1 : 16)
-                : (K == 2 ? 8 : (K == 3 ? 5 : (m_kp(K) == 1 ? 4 : (m_kp(K) == 2 ? KCG_MG4 : 8))));
+                : (K == 2 ? 8 : (K == 3 ? 5 : (m_kp(K) == 1 ? KCG_MG4W : (m_kp(K) == 2 ? KCG_MG4 : 8))));
 }
 __host__ __device__ constexpr int m_threads(int K) { return m_groups(K) * m_gw(K) * 32; }
 __host__ __device__ constexpr int m_stages(int K) {  // (shared memory)

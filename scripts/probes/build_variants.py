@@ -10,6 +10,10 @@ VARIANTS = {
     "b8x256x2": ["KCG_TY4=8", "KCG_MINB4=2"],
     "c8x128x2": ["KCG_TY4=8", "KCG_NT4=128", "KCG_MINB4=2"],
     "d16x128": ["KCG_NT4=128"],
+    # D2 row march, K = 4: two face columns per lane (64-column boxes, 56 output columns)
+    "m4c2k2g4": ["KCG_MKP4=2", "KCG_MCP4=2", "KCG_MG4=4"],
+    "m4c2k1g3": ["KCG_MKP4=1", "KCG_MCP4=2", "KCG_MG4W=3"],
+    "m4c2k1g4": ["KCG_MKP4=1", "KCG_MCP4=2", "KCG_MG4W=4"],
 }
 names = sys.argv[1:] or list(VARIANTS)
 out = os.path.join(ROOT, "paper_2204_08057_b200", "lib", "variants")
