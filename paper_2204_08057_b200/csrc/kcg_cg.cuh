@@ -1413,8 +1413,8 @@ static cudaError_t cg_config_t(bool slab, bool d2, int n_sys, int* max_grid, siz
   int nt = cg_threads(K);
   if (d2) {  // the row-march kernel (kcg_march.cuh)
     if constexpr (K <= 4) kern = (const void*)cg_march_kernel<K, HITS, PREC>;
-    sm += (size_t)m_groups(K) * m_group_doubles(K, PREC) * 8;
-    nt = m_threads(K);
+    sm += (size_t)m_groups(K, HITS) * m_group_doubles(K, PREC, HITS) * 8;
+    nt = m_threads(K, HITS);
   } else {
     kern = slab ? (const void*)cg_slab_kernel<K, HITS, PREC> : (const void*)cg_persistent_kernel<K, HITS, PREC>;
     sm += cg_dyn_smem_fixed<K, PREC>();
@@ -1465,7 +1465,7 @@ cudaError_t CgEntry<K>::launch(bool prec, bool d2, cudaStream_t s, const CgArgs&
     f = hits ? (const void*)cg_persistent_kernel<K, true, false> : (const void*)cg_persistent_kernel<K, false, false>;
   }
   if (!f) return cudaErrorInvalidValue;
-  return cudaLaunchCooperativeKernel(f, dim3(grid), dim3(d2 ? m_threads(K) : cg_threads(K)), args, smem, s);
+  return cudaLaunchCooperativeKernel(f, dim3(grid), dim3(d2 ? m_threads(K, hits) : cg_threads(K)), args, smem, s);
 }
 
 template <int K>

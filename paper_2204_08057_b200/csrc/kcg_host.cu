@@ -722,7 +722,7 @@ kcg_status solve_impl(kcg_ctx* c, Route route, const double* Y_in, double* mu_ou
     a.tiles_x = kron ? c->tiles_x_kron : c->tiles_x_syl;
     a.tiles_y = kron ? c->tiles_y_kron : c->tiles_y_syl;
     const bool march = c->d.prior == KCG_PRIOR_D2 && c->d.cg_variant == KCG_CG_SINGLE_PASS;
-    a.tiles_per_sys = a.tiles_x * a.tiles_y * (march ? kcg::m_gw(Kk) : 1);  // row-march: partials per group warp
+    a.tiles_per_sys = a.tiles_x * a.tiles_y * (march ? kcg::m_gw(Kk, R.hits != nullptr) : 1);  // row-march: partials per group warp
     a.max_iter = max_iter;
     a.tol2 = tol * tol;
     a.bnorm2 = x0 ? R.resid_out : nullptr;
@@ -742,7 +742,7 @@ kcg_status solve_impl(kcg_ctx* c, Route route, const double* Y_in, double* mu_ou
     }
     if (march) {  // row-march kernel: segment rows, hits by TMA
       a.h_tma = (R.hits && c->side >= 2) ? 1 : 0;
-      a.seg = march_seg(c->side, Kk, n_sys, (kron ? c->grid_kron : c->grid_syl) * kcg::m_groups(Kk));
+      a.seg = march_seg(c->side, Kk, n_sys, (kron ? c->grid_kron : c->grid_syl) * kcg::m_groups(Kk, R.hits != nullptr));
     }
     Lx.m[j] = maps;
     CK(cudaMemsetAsync(R.sync, 0, 4 * sizeof(unsigned), s), "memset sync");
@@ -1098,7 +1098,7 @@ kcg_status kohler_impl(kcg_ctx* c, const double* Y_in, double* mu_out, double to
     const int grid = std::max(1, std::min(c->grid_syl, P * a.tiles_per_sys));
     if (d2) {
       a.h_tma = (R.hits && c->side >= 2) ? 1 : 0;
-      a.seg = march_seg(c->side, 1, P, grid * kcg::m_groups(1));
+      a.seg = march_seg(c->side, 1, P, grid * kcg::m_groups(1, R.hits != nullptr));
     }
     if (c->res_koh.on) {
       a.tiles_per_sys = c->res_koh.nstrip;
@@ -1505,8 +1505,8 @@ kcg_status create_impl(const kcg_desc* d, const kcg_slab* sl, const double* A_ho
     return KCG_OK;
   }
   CKC(kcg::cg_kernel_config(k, hits_dev != nullptr, prec, c->slab, d2, P, &mg, &c->smem_kron), "cg kernel config (kron)");
-  // (D2 row-march kernel: m_groups(K) warp groups per CTA, each a work unit of >= one strip x 16 rows)
-  const int wdk = d2 ? kcg::m_groups(k) : 1, wds = d2 ? kcg::m_groups(1) : 1;
+  // (D2 row-march kernel: m_groups(K, hits) warp groups per CTA, each a work unit of >= one strip x 16 rows)
+  const int wdk = d2 ? kcg::m_groups(k, hits_dev != nullptr) : 1, wds = d2 ? kcg::m_groups(1, hits_dev != nullptr) : 1;
   c->grid_kron = std::max(1, std::min(mg / c->nlocal, (P * c->tiles_x_kron * c->tiles_y_kron + wdk - 1) / wdk));
   CKC(kcg::cg_kernel_config(1, hits_dev != nullptr, prec, c->slab, d2, P * k, &mg, &c->smem_syl),
       "cg kernel config (sylvester)");

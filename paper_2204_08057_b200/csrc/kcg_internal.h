@@ -127,27 +127,35 @@ __host__ __device__ constexpr int cg_stage_bytes(int K) {
 #define KCG_MHALO 4
 #define KCG_MCH 1           // rows per TMA stage
 #define KCG_MPB 16          // rows per partial-sum block (fixed reduction order)
+// K = 4 (round 2): two face columns per lane (64-column boxes, 56 output columns: 12.5 % halo lanes
+// instead of 25 %); without hits one plane per warp in 3 groups of 4 warps (fullsky-d2 63.1 vs 73.0 us per
+// face-pass), with hits two planes per warp in 4 groups of 2 warps (the hits ring would spill the
+// one-plane warp: paper workload 38.3 vs 45.0 ms) -- profiles/r02/ab_march_k4_columns_per_lane.txt.
+// The geometry therefore depends on HITS (H) for K = 4; the strip width (m_cp) does not.
 #ifndef KCG_MKP4
-#define KCG_MKP4 2          // K = 4: component planes per warp (2 warps per group)
+#define KCG_MKP4 1          // K = 4 without hits: component planes per warp
+#endif
+#ifndef KCG_MKP4H
+#define KCG_MKP4H 2         // K = 4 with hits: component planes per warp
 #endif
 #ifndef KCG_MCP1
 #define KCG_MCP1 2          // K = 1: face columns per lane (a 64-column box, 56 output columns)
 #endif
 #ifndef KCG_MCP4
-#define KCG_MCP4 1          // K = 4: face columns per lane
+#define KCG_MCP4 2          // K = 4: face columns per lane
 #endif
-__host__ __device__ constexpr int m_kp(int K) { return K == 4 ? KCG_MKP4 : 1; }  // planes per warp
-__host__ __device__ constexpr int m_gw(int K) { return K / m_kp(K); }            // warps per group
+__host__ __device__ constexpr int m_kp(int K, bool H) { return K == 4 ? (H ? KCG_MKP4H : KCG_MKP4) : 1; }  // planes per warp
+__host__ __device__ constexpr int m_gw(int K, bool H) { return K / m_kp(K, H); }                           // warps per group
 __host__ __device__ constexpr int m_cp(int K) { return K == 1 ? KCG_MCP1 : (K == 4 ? KCG_MCP4 : 1); }  // columns per lane
 __host__ __device__ constexpr int m_out(int K) { return 32 * m_cp(K) - 2 * KCG_MHALO; }  // output columns
 #ifndef KCG_MG4
-#define KCG_MG4 6           // K = 4 (two planes per warp): groups per CTA
+#define KCG_MG4 4           // K = 4 (two planes per warp): groups per CTA
 #endif
 #ifndef KCG_MG4W
-#define KCG_MG4W 4          // K = 4 (one plane per warp): groups per CTA
+#define KCG_MG4W 3          // K = 4 (one plane per warp): groups per CTA
 #endif
 #ifndef KCG_MST4
-#define KCG_MST4 4          // K = 4 (two planes per warp): TMA row stages per group (power of 2)
+#define KCG_MST4 4          // K = 4: TMA row stages per group (power of 2)
 #endif
 #ifndef KCG_MG1
 #define KCG_MG1 12          // K = 1 (two columns per lane): groups per CTA
@@ -155,23 +163,23 @@ __host__ __device__ constexpr int m_out(int K) { return 32 * m_cp(K) - 2 * KCG_M
 #ifndef KCG_MST1
 #define KCG_MST1 4          // K = 1 (two columns per lane): TMA row stages per group (power of 2)
 #endif
-__host__ __device__ constexpr int m_groups(int K) {
+__host__ __device__ constexpr int m_groups(int K, bool H) {
   return K == 1 ? (m_cp(K) == 2 ? KCG_MG1 : 16)
-                : (K == 2 ? 8 : (K == 3 ? 5 : (m_kp(K) == 1 ? KCG_MG4W : (m_kp(K) == 2 ? KCG_MG4 : 8))));
+                : (K == 2 ? 8 : (K == 3 ? 5 : (m_kp(K, H) == 1 ? (m_cp(K) == 2 ? KCG_MG4W : 4) : (m_kp(K, H) == 2 ? KCG_MG4 : 8))));
 }
-__host__ __device__ constexpr int m_threads(int K) { return m_groups(K) * m_gw(K) * 32; }
-__host__ __device__ constexpr int m_stages(int K) {  // (shared memory)
-  return m_kp(K) == 2 ? KCG_MST4 : (m_cp(K) == 2 ? KCG_MST1 : 8);
+__host__ __device__ constexpr int m_threads(int K, bool H) { return m_groups(K, H) * m_gw(K, H) * 32; }
+__host__ __device__ constexpr int m_stages(int K, bool H) {  // (shared memory)
+  return K == 4 && (m_kp(K, H) == 2 || m_cp(K) == 2) ? KCG_MST4 : (m_cp(K) == 2 ? KCG_MST1 : 8);
 }
 __host__ __device__ constexpr int m_stage_doubles(int K) { return (3 * K + 1) * 32 * m_cp(K); }
 // doubles of one group's shared memory: the stage ring + 3 exchange rings [4 rows][K][32 cp]
-__host__ __device__ constexpr int m_group_doubles(int K, bool prec) {  // (u_new ring with block-Jacobi only)
-  return m_stages(K) * m_stage_doubles(K) + (prec ? 3 : 2) * 4 * K * 32 * m_cp(K);
+__host__ __device__ constexpr int m_group_doubles(int K, bool prec, bool H) {  // (u_new ring with block-Jacobi only)
+  return m_stages(K, H) * m_stage_doubles(K) + (prec ? 3 : 2) * 4 * K * 32 * m_cp(K);
 }
 __host__ __device__ constexpr int m_strips(int side, int K) { return (side + m_out(K) - 1) / m_out(K); }
 __host__ __device__ constexpr int m_blocks(int side) { return (side + KCG_MPB - 1) / KCG_MPB; }
 // partial slots per system: strips x 16-row blocks x warps of a group
-__host__ __device__ constexpr int m_slots(int side, int K) { return m_strips(side, K) * m_blocks(side) * m_gw(K); }
+__host__ __device__ constexpr int m_slots(int side, int K, bool H) { return m_strips(side, K) * m_blocks(side) * m_gw(K, H); }
 
 
 // Per-system constant parameters of the operator  q_c = h sum_d M[c][d] p_d + tau_c (kappa2 p_c + (L p_c)).

@@ -15,7 +15,7 @@
 //     shared rings of p_new / r_new (/ u_new) and one named barrier of the group per row, no CTA
 //     barrier inside a pass (one plane per warp: ~60 registers, 16 warps per SM);
 //   * the rows of r, p (and x on x passes, hits with N_h) are staged by TMA one row (32 columns x K
-//     planes) per stage into a per-warp ring of m_stages(K) shared-memory stages (own mbarriers),
+//     planes) per stage into a per-group ring of m_stages(K, HITS) shared-memory stages (own mbarriers),
 //     prefetched continuously across the warp's units (zero fill outside the face = the free
 //     boundary); a stage is held until its r feeds r_old two rows later;
 //   * per input row y the warp evaluates, pipelined by one row per phase,
@@ -45,11 +45,11 @@ __device__ __forceinline__ void group_bar(int id, int nthreads) {
 }
 
 template <int K, bool HITS, bool PREC>
-__global__ void __launch_bounds__(m_threads(K), 1) cg_march_kernel(const CgArgs a, const __grid_constant__ CgMaps maps) {
-  constexpr int NG = m_groups(K), NT = m_threads(K), NW = NT / 32, NS = m_stages(K), SD = m_stage_doubles(K);
-  constexpr int KP = m_kp(K), GW = m_gw(K), CP = m_cp(K);  // planes per warp, warps per group, columns per lane
+__global__ void __launch_bounds__(m_threads(K, HITS), 1) cg_march_kernel(const CgArgs a, const __grid_constant__ CgMaps maps) {
+  constexpr int NG = m_groups(K, HITS), NT = m_threads(K, HITS), NW = NT / 32, NS = m_stages(K, HITS), SD = m_stage_doubles(K);
+  constexpr int KP = m_kp(K, HITS), GW = m_gw(K, HITS), CP = m_cp(K);  // planes per warp, warps per group, columns per lane
   constexpr int BW = 32 * CP;                                 // box width (one stage row of a plane)
-  constexpr int XR = 4 * K * BW, GD = m_group_doubles(K, PREC);
+  constexpr int XR = 4 * K * BW, GD = m_group_doubles(K, PREC, HITS);
   constexpr int MO = m_out(K), MH = KCG_MHALO, PB = KCG_MPB;
   constexpr int NP = PREC ? 3 : 2;
   constexpr int DL = PREC ? 5 : 4;  // row of C1 behind the input row

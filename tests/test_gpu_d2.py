@@ -131,7 +131,7 @@ def test_d2_block_jacobi_with_hits(level, k):
 
 
 def test_d2_march_ragged_strips_and_segments():
-    """Face widths that are not multiples of the strips (24 columns for K = 4, 56 for K = 1) and a
+    """Face widths that are not multiples of the strips (56 output columns for K = 4 and K = 1) and a
     Sylvester route with several segments per strip: level 8 (256 = 10 x 24 + 16 = 4 x 56 + 32)."""
     p = _d2(8, 4, 880)
     ctx, Y = make_ctx([p])
