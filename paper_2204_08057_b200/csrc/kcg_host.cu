@@ -65,20 +65,18 @@ int tiles_y(int rows, int K, bool d2 = false) {
   return d2 ? kcg::m_blocks(rows) : (rows + kcg::cg_tile_y(K) - 1) / kcg::cg_tile_y(K);
 }
 
-// D2 row-march kernel: rows per work unit (a multiple of the partial block KCG_MPB) minimising the
-// estimated pass time ceil(units / warps) * (seg + 8 warm-up rows + ~4 rows of pipeline fill), all
-// n_sys systems active.
-int march_seg(int side, int K, int n_sys, int warps) {
-  if (side <= KCG_MPB) return KCG_MPB;
-  const long strips = kcg::m_strips(side, K);
-  int best = side;
-  double bt = 1e300;
-  for (int seg = KCG_MPB; seg < side + KCG_MPB; seg += KCG_MPB) {
-    const long units = (long)n_sys * strips * ((side + seg - 1) / seg);
-    const double t = (double)((units + warps - 1) / std::max(warps, 1)) * (std::min(seg, side) + 2 * KCG_MHALO + 4);
-    if (t < bt) { bt = t; best = seg; }
+// D2 row-march kernel: rows per work unit, planned for every number of running systems (seg = 0 and
+// the table: the kernel picks each pass's plan; entry KCG_MSEGTAB - 1 serves every nact >= KCG_MSEGTAB
+// and is planned for all n_sys); KCG_MSEG (diagnostics) fixes it.
+void march_seg(kcg::CgArgs* a, int side, int K, int n_sys, int groups) {
+  a->seg = 0;
+  if (const char* ev = std::getenv("KCG_MSEG"))
+    a->seg = std::max(KCG_MPB, (std::atoi(ev) + KCG_MPB - 1) / KCG_MPB * KCG_MPB);
+  const int strips = kcg::m_strips(side, K);
+  for (int i = 0; i < KCG_MSEGTAB; ++i) {
+    const int n = i + 1 < KCG_MSEGTAB ? std::min(i + 1, n_sys) : std::max(n_sys, KCG_MSEGTAB);
+    a->seg_tab[i] = (unsigned short)kcg::m_seg_model(side, strips, n, groups);
   }
-  return best;
 }
 
 // One rank's layout: `rows` local rows (side / nranks), r/p buffers with `ghost` ghost rows.
@@ -742,7 +740,7 @@ kcg_status solve_impl(kcg_ctx* c, Route route, const double* Y_in, double* mu_ou
     }
     if (march) {  // row-march kernel: segment rows, hits by TMA
       a.h_tma = (R.hits && c->side >= 2) ? 1 : 0;
-      a.seg = march_seg(c->side, Kk, n_sys, (kron ? c->grid_kron : c->grid_syl) * kcg::m_groups(Kk, R.hits != nullptr));
+      march_seg(&a, c->side, Kk, n_sys, (kron ? c->grid_kron : c->grid_syl) * kcg::m_groups(Kk, R.hits != nullptr));
     }
     Lx.m[j] = maps;
     CK(cudaMemsetAsync(R.sync, 0, 4 * sizeof(unsigned), s), "memset sync");
@@ -1098,7 +1096,7 @@ kcg_status kohler_impl(kcg_ctx* c, const double* Y_in, double* mu_out, double to
     const int grid = std::max(1, std::min(c->grid_syl, P * a.tiles_per_sys));
     if (d2) {
       a.h_tma = (R.hits && c->side >= 2) ? 1 : 0;
-      a.seg = march_seg(c->side, 1, P, grid * kcg::m_groups(1, R.hits != nullptr));
+      march_seg(&a, c->side, 1, P, grid * kcg::m_groups(1, R.hits != nullptr));
     }
     if (c->res_koh.on) {
       a.tiles_per_sys = c->res_koh.nstrip;

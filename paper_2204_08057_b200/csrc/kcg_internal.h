@@ -127,6 +127,7 @@ __host__ __device__ constexpr int cg_stage_bytes(int K) {
 #define KCG_MHALO 4
 #define KCG_MCH 1           // rows per TMA stage
 #define KCG_MPB 16          // rows per partial-sum block (fixed reduction order)
+#define KCG_MSEGTAB 64      // per-pass segment plans for 1 .. 64 running systems (the last one: all n_sys)
 // K = 4 (round 2): two face columns per lane (64-column boxes, 56 output columns: 12.5 % halo lanes
 // instead of 25 %); without hits one plane per warp in 3 groups of 4 warps (fullsky-d2 63.1 vs 73.0 us per
 // face-pass), with hits two planes per warp in 4 groups of 2 warps (the hits ring would spill the
@@ -177,6 +178,22 @@ __host__ __device__ constexpr int m_group_doubles(int K, bool prec, bool H) {  /
   return m_stages(K, H) * m_stage_doubles(K) + (prec ? 3 : 2) * 4 * K * 32 * m_cp(K);
 }
 __host__ __device__ constexpr int m_strips(int side, int K) { return (side + m_out(K) - 1) / m_out(K); }
+// rows per work unit (a multiple of KCG_MPB) minimising the estimated pass time
+// ceil(units / groups) * (seg + 8 warm-up rows + ~4 rows of pipeline fill) for n_sys active systems;
+// the host plans it for every possible number of running systems (CgArgs::seg_tab), the march
+// kernel picks the plan of each pass
+__host__ __device__ inline int m_seg_model(int side, int strips, int n_sys, int groups) {
+  if (side <= KCG_MPB) return KCG_MPB;
+  int best = side;
+  long long bt = -1;
+  for (int seg = KCG_MPB; seg < side + KCG_MPB; seg += KCG_MPB) {
+    const long long units = (long long)n_sys * strips * ((side + seg - 1) / seg);
+    const long long g = groups > 0 ? groups : 1;
+    const long long t = (units + g - 1) / g * ((seg < side ? seg : side) + 2 * KCG_MHALO + 4);
+    if (bt < 0 || t < bt) { bt = t; best = seg; }
+  }
+  return best;
+}
 __host__ __device__ constexpr int m_blocks(int side) { return (side + KCG_MPB - 1) / KCG_MPB; }
 // partial slots per system: strips x 16-row blocks x warps of a group
 __host__ __device__ constexpr int m_slots(int side, int K, bool H) { return m_strips(side, K) * m_blocks(side) * m_gw(K, H); }
@@ -239,7 +256,9 @@ struct CgArgs {
   const double* bnorm2;      // warm start (reading R37): (||b - G x0||^2, ||b||^2) per system, else nullptr
   int x_tma;                 // 1: CgMaps::x describes `x` (TMA needs side >= 2): staged (K <= 3) or L2-prefetched
   int h_tma;                 // D2 march kernel: 1 = CgMaps::h describes the hits planes (side >= 2)
-  int seg;                   // D2 march kernel: rows per work unit (a multiple of KCG_MPB)
+  int seg;                   // D2 march kernel: rows per work unit (a multiple of KCG_MPB); 0 = per pass from seg_tab
+  unsigned short seg_tab[KCG_MSEGTAB];  // D2 march kernel, seg == 0: rows per unit with nact systems running
+                             // = seg_tab[min(nact, KCG_MSEGTAB) - 1] (host-planned, kcg::m_seg_model)
   long long* trace;          // KCG_TRACE builds only: per-iteration %globaltimer stamps
   unsigned* sync;            // [2..3] tile-claim counters of the two pass parities (zeroed per launch)
   double tol2;

@@ -26,7 +26,8 @@
 //         C1  w(y-4)     = h M u_new + tau (kappa2 u_new + D S2);  (r,r), (r,u), (w,u)
 //     p_new, x (+= alpha_prev p_old + alpha p_new on x passes) and r_new are final when computed and
 //     are stored at once (valid columns / segment rows only);
-//   * work unit = (system, strip, segment of `seg` rows), claimed dynamically per warp; the segment
+//   * work unit = (system, strip, segment of `seg` rows, re-planned every pass from the number of
+//     systems still running), claimed dynamically per warp group; the segment
 //     starts 4 rows early (warm-up: the halo rows are recomputed -- bitwise identical to the
 //     neighbouring unit's values, so the iterate does not depend on the decomposition);
 //   * partials per (system, strip, 16-row block, plane): the reduction order is fixed by the face
@@ -64,15 +65,15 @@ __global__ void __launch_bounds__(m_threads(K, HITS), 1) cg_march_kernel(const C
   __shared__ double rs[KCG_RB][3][NW];
   __shared__ double Mw[NW][MSZ];  // per-warp constants of the system being marched
   __shared__ int uq[NG][4];       // units claimed by each group's issuing warp, in order
-  __shared__ int s_nact;
+  __shared__ int s_nact, s_seg;
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int g = warp / GW, wg = warp - g * GW, c0 = wg * KP;  // group, warp in the group, its first plane
   const bool issuer = wg == 0;                                 // the group's TMA / claim warp
   const int cta = blockIdx.x, ncta = gridDim.x;
-  const int side = a.side, pitch = a.pitch, seg = a.seg;
+  const int side = a.side, pitch = a.pitch;
   const int nstrips = a.tiles_x, tps = a.tiles_per_sys;
-  const int nsegs = (side + seg - 1) / seg, ups = nstrips * nsegs;  // units per system
+  int seg = a.seg, nsegs = 1, ups = 1;  // rows per unit (planned per pass), segments and units per system
   const size_t N = (size_t)side * side, ps = (size_t)pitch * side;
   double* gsm = reinterpret_cast<double*>(smem_raw) + (size_t)g * GD;
   double* stg = gsm;                 // [NS][SD]: r [K][BW], p [K][BW], x [K][BW], hits [BW]
@@ -129,10 +130,15 @@ __global__ void __launch_bounds__(m_threads(K, HITS), 1) cg_march_kernel(const C
       for (int s = 0; s < a.n_sys; ++s)
         if (st[s].status == ST_RUNNING) act[n++] = s;
       s_nact = n;
+      // the partials are per 16-row block, so the segment length never changes the iterate
+      s_seg = a.seg > 0 ? a.seg : (int)a.seg_tab[min(n, KCG_MSEGTAB) - 1];
     }
     __syncthreads();
     const int nact = s_nact;
     if (nact == 0) break;
+    seg = s_seg;  // (nact > 0 here, so the table index is valid)
+    nsegs = (side + seg - 1) / seg;
+    ups = nstrips * nsegs;
     const int units = nact * ups;
     const int par_out = (it + 1) & 1;
     const bool xpass = xpass_of(it + 1);

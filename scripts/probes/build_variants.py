@@ -14,6 +14,10 @@ VARIANTS = {
     "m4c2k2g4": ["KCG_MKP4=2", "KCG_MCP4=2", "KCG_MG4=4"],
     "m4c2k1g3": ["KCG_MKP4=1", "KCG_MCP4=2", "KCG_MG4W=3"],
     "m4c2k1g4": ["KCG_MKP4=1", "KCG_MCP4=2", "KCG_MG4W=4"],
+    # after the change: K = 4 with hits (two planes per warp), groups per CTA
+    "m4hg5": ["KCG_MG4=5"],
+    "m4hg3": ["KCG_MG4=3"],
+    "m4hs8g3": ["KCG_MG4=3", "KCG_MST4=8"],
 }
 names = sys.argv[1:] or list(VARIANTS)
 out = os.path.join(ROOT, "paper_2204_08057_b200", "lib", "variants")

@@ -142,3 +142,25 @@ def test_d2_march_ragged_strips_and_segments():
     assert srep["converged"] and rel(smu.cpu().numpy()[0], xe) <= 1e-8
     kmu, krep = ctx.kohler(Y, tol=TOL, max_iter=200000)
     assert krep["converged"] and rel(kmu.cpu().numpy()[0], xe) <= 1e-8
+
+
+@pytest.mark.parametrize("k,hits", [(4, None), (4, "random"), (1, None)])
+def test_d2_march_batch_independent_bitwise(k, hits):
+    """The row march re-plans its segment length every pass from the number of systems still running
+    (kcg::m_seg_model), and its partials are per (strip, 16-row block), so a face's iterate must not
+    depend on the batch it is solved in: face 0 alone (one system: short segments) and inside a batch
+    of four faces of different conditioning (longer segments, faces leaving at different passes) agree
+    bit for bit, and both equal the oracle at 1e-8."""
+    ps = [_d2(8, k, 510 + s, hits=hits) for s in range(4)]
+    ctx1, Y1 = make_ctx(ps[:1])
+    mu1, rep1 = ctx1.solve(Y1, tol=TOL, max_iter=200000)
+    ctx4, Y4 = make_ctx(ps)
+    mu4, rep4 = ctx4.solve(Y4, tol=TOL, max_iter=200000)
+    assert rep1["converged"] and rep4["converged"]
+    assert len(set(rep4["iterations_per"])) > 1, rep4["iterations_per"]  # faces leave at different passes
+    a, b = mu1.cpu().numpy()[0], mu4.cpu().numpy()[0]
+    assert rep1["iterations_per"][0] == rep4["iterations_per"][0]
+    assert np.array_equal(a, b), float(np.abs(a - b).max())
+    G, bb = model.problem_system(ps[0])
+    ref = cg.cg_hs(G, bb, tol=TOL, max_iter=200000)
+    assert rel(a, ref.x) <= 1e-8
