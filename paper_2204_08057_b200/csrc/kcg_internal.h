@@ -155,6 +155,9 @@ __host__ __device__ constexpr int m_out(int K) { return 32 * m_cp(K) - 2 * KCG_M
 #ifndef KCG_MG4W
 #define KCG_MG4W 3          // K = 4 (one plane per warp): groups per CTA
 #endif
+#ifndef KCG_MG4Q
+#define KCG_MG4Q 8          // K = 4 (all four planes in one warp, no group barrier): groups (= warps) per CTA
+#endif
 #ifndef KCG_MST4
 #define KCG_MST4 4          // K = 4: TMA row stages per group (power of 2)
 #endif
@@ -166,7 +169,7 @@ __host__ __device__ constexpr int m_out(int K) { return 32 * m_cp(K) - 2 * KCG_M
 #endif
 __host__ __device__ constexpr int m_groups(int K, bool H) {
   return K == 1 ? (m_cp(K) == 2 ? KCG_MG1 : 16)
-                : (K == 2 ? 8 : (K == 3 ? 5 : (m_kp(K, H) == 1 ? (m_cp(K) == 2 ? KCG_MG4W : 4) : (m_kp(K, H) == 2 ? KCG_MG4 : 8))));
+                : (K == 2 ? 8 : (K == 3 ? 5 : (m_kp(K, H) == 1 ? (m_cp(K) == 2 ? KCG_MG4W : 4) : (m_kp(K, H) == 2 ? KCG_MG4 : KCG_MG4Q))));
 }
 __host__ __device__ constexpr int m_threads(int K, bool H) { return m_groups(K, H) * m_gw(K, H) * 32; }
 __host__ __device__ constexpr int m_stages(int K, bool H) {  // (shared memory)

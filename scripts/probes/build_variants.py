@@ -18,6 +18,11 @@ VARIANTS = {
     "m4hg5": ["KCG_MG4=5"],
     "m4hg3": ["KCG_MG4=3"],
     "m4hs8g3": ["KCG_MG4=3", "KCG_MST4=8"],
+    # K = 4 with hits, one column per lane (24-column strips): more, thinner warps
+    "m4hc1k2g6": ["KCG_MCP4=1", "KCG_MKP4H=2", "KCG_MG4=6"],
+    "m4hc1k2g7": ["KCG_MCP4=1", "KCG_MKP4H=2", "KCG_MG4=7"],
+    "m4hc1k2g8": ["KCG_MCP4=1", "KCG_MKP4H=2", "KCG_MG4=8"],
+    "m4hc1k4g8": ["KCG_MCP4=1", "KCG_MKP4H=4", "KCG_MG4Q=8"],
 }
 names = sys.argv[1:] or list(VARIANTS)
 out = os.path.join(ROOT, "paper_2204_08057_b200", "lib", "variants")
