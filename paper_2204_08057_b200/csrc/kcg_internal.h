@@ -173,7 +173,7 @@ __host__ __device__ constexpr int m_groups(int K, bool H) {
 }
 __host__ __device__ constexpr int m_threads(int K, bool H) { return m_groups(K, H) * m_gw(K, H) * 32; }
 __host__ __device__ constexpr int m_stages(int K, bool H) {  // (shared memory)
-  return K == 4 && (m_kp(K, H) == 2 || m_cp(K) == 2) ? KCG_MST4 : (m_cp(K) == 2 ? KCG_MST1 : 8);
+  return K == 4 && (m_kp(K, H) >= 2 || m_cp(K) == 2) ? KCG_MST4 : (m_cp(K) == 2 ? KCG_MST1 : 8);
 }
 __host__ __device__ constexpr int m_stage_doubles(int K) { return (3 * K + 1) * 32 * m_cp(K); }
 // doubles of one group's shared memory: the stage ring + 3 exchange rings [4 rows][K][32 cp]

@@ -257,11 +257,14 @@ __global__ void __launch_bounds__(m_threads(K, HITS), 1) cg_march_kernel(const C
       // x is the caller's buffer: double2 stores only if it is 16-byte aligned (r / p: the workspace)
       const bool x16 = (reinterpret_cast<uintptr_t>(a.x) & 15) == 0;
       auto stv = [&](double* dst, const double (&v)[CP], bool al = true) {  // this lane's valid columns
-        if (CP == 2 && pair_out && al) *reinterpret_cast<double2*>(dst) = make_double2(v[0], v[CP - 1]);
-        else
-#pragma unroll
-          for (int cc = 0; cc < CP; ++cc)
-            if (outc[cc]) dst[cc] = v[cc];
+        if constexpr (CP == 2) {  // outc[1] implies outc[0] (even halo, even box start): one test per store
+          if (pair_out) {
+            if (al) *reinterpret_cast<double2*>(dst) = make_double2(v[0], v[CP - 1]);
+            else { dst[0] = v[0]; dst[CP - 1] = v[CP - 1]; }
+          } else if (outc[0]) dst[0] = v[0];  // (side 1 only)
+        } else {
+          if (outc[0]) dst[0] = v[0];
+        }
       };
 
       // register rings of this warp's planes and columns (slot of row y = (y - ys + 4) mod 3)
