@@ -155,6 +155,9 @@ __host__ __device__ constexpr int m_out(int K) { return 32 * m_cp(K) - 2 * KCG_M
 #ifndef KCG_MG4W
 #define KCG_MG4W 3          // K = 4 (one plane per warp): groups per CTA
 #endif
+#ifndef KCG_MINT
+#define KCG_MINT 0          // 1: interior work units (no face border in reach) run a step without border masks
+#endif
 #ifndef KCG_MG4Q
 #define KCG_MG4Q 8          // K = 4 (all four planes in one warp, no group barrier): groups (= warps) per CTA
 #endif

@@ -292,8 +292,13 @@ __global__ void __launch_bounds__(m_threads(K, HITS), 1) cg_march_kernel(const C
       };
 
       // one input row: y = ys - 4 + t, ring period 3 (J = t mod 3 at compile time)
-      auto step = [&](auto Jc, int t) {
+      // IN (KCG_MINT): every row and column the unit touches lies strictly inside the face (degree 4,
+      // no border masks); the rows before the warm-up then hold finite values no valid output reads
+      auto step = [&](auto Jc, auto INc, int t) {
         constexpr int J = decltype(Jc)::value, J1 = (J + 2) % 3, J2 = (J + 1) % 3;  // rows y-1 | y-4, y-2 | y-5
+        constexpr bool IN = decltype(INc)::value;
+        auto on = [&](bool row, int cc) { return IN || (row && colin[cc]); };       // pixel inside the face
+        auto mdeg = [&](int cc, int e) { return IN ? -4.0 : -(double)(degx[cc] + e); };  // -(degree)
         const int y = C.ys - MH + t;
         const uint32_t q = gr++;
         const int slot = q & (NS - 1);
@@ -307,8 +312,8 @@ __global__ void __launch_bounds__(m_threads(K, HITS), 1) cg_march_kernel(const C
           ld(sg + (K + c0 + i) * BW, p_c[i]);
           ld(sg2 + (c0 + i) * BW, ro_c[i]);
         }
-        const bool r0 = (unsigned)y < (unsigned)side;
-        const int e0 = -(y == 0) - (y == side - 1);
+        const bool r0 = IN || (unsigned)y < (unsigned)side;
+        const int e0 = IN ? 0 : -(y == 0) - (y == side - 1);
         const bool vA = y >= C.ys && y < C.ye;
         double xv[KP][CP];
 #pragma unroll
@@ -332,7 +337,7 @@ __global__ void __launch_bounds__(m_threads(K, HITS), 1) cg_march_kernel(const C
           if (hl) ld(sg + 3 * K * BW, h0);
           else
 #pragma unroll
-            for (int cc = 0; cc < CP; ++cc) h0[cc] = (colin[cc] && r0) ? __ldg(hp + (size_t)y * side + gx + cc) : 1.0;
+            for (int cc = 0; cc < CP; ++cc) h0[cc] = on(r0, cc) ? __ldg(hp + (size_t)y * side + gx + cc) : 1.0;
         }
         // A: p_new(y)
 #pragma unroll
@@ -344,7 +349,7 @@ __global__ void __launch_bounds__(m_threads(K, HITS), 1) cg_march_kernel(const C
             double rv[K];
 #pragma unroll
             for (int d = 0; d < K; ++d) rv[d] = sg[d * BW + CP * lane + cc];
-            if (colin[cc] && r0) prec_w(rv, h0[cc], (double)(degx[cc] + e0), u_c);
+            if (on(r0, cc)) prec_w(rv, h0[cc], -mdeg(cc, e0), u_c);
             else
 #pragma unroll
               for (int i = 0; i < KP; ++i) u_c[i] = 0.0;
@@ -374,7 +379,7 @@ __global__ void __launch_bounds__(m_threads(K, HITS), 1) cg_march_kernel(const C
           lr(pn[J1][i], o);
 #pragma unroll
           for (int cc = 0; cc < CP; ++cc)
-            s1[J1][i][cc] = (r1 && colin[cc]) ? fma(-(double)(degx[cc] + e1), pn[J1][i][cc], (pn[J2][i][cc] + pn[J][i][cc]) + o[cc])
+            s1[J1][i][cc] = on(r1, cc) ? fma(mdeg(cc, e1), pn[J1][i][cc], (pn[J2][i][cc] + pn[J][i][cc]) + o[cc])
                                                 : 0.0;
         }
         // B1: r_new(y-2)
@@ -387,13 +392,13 @@ __global__ void __launch_bounds__(m_threads(K, HITS), 1) cg_march_kernel(const C
             lr(s1[J2][i], o);
 #pragma unroll
             for (int cc = 0; cc < CP; ++cc) {
-              const double d2p = fma(-(double)(degx[cc] + e2), s1[J2][i][cc], (s1[J][i][cc] + s1[J1][i][cc]) + o[cc]);
+              const double d2p = fma(mdeg(cc, e2), s1[J2][i][cc], (s1[J][i][cc] + s1[J1][i][cc]) + o[cc]);
               double mix = 0.0;
 #pragma unroll
               for (int d = 0; d < K; ++d)  // p_new of row y-2, plane d (GW == 1: every plane is this warp's)
                 mix = fma(Mrow[i][d], GW == 1 ? pn[J2][GW == 1 ? d : 0][cc] : xr(PX, y2, d, cc), mix);
               const double qv = fma(h2[cc], mix, tau_c[i] * fma(kappa2, pn[J2][i][cc], d2p));
-              rn[J2][i][cc] = (r2 && colin[cc]) ? fma(-alpha, qv, ro_c[i][cc]) : 0.0;
+              rn[J2][i][cc] = on(r2, cc) ? fma(-alpha, qv, ro_c[i][cc]) : 0.0;
               if (GW > 1 || PREC) RX[((y2 & 3) * K + c0 + i) * BW + CP * lane + cc] = rn[J2][i][cc];
             }
             if (st2) stv(rout + i * ps + (size_t)y2 * pitch, rn[J2][i]);
@@ -407,7 +412,7 @@ __global__ void __launch_bounds__(m_threads(K, HITS), 1) cg_march_kernel(const C
 #pragma unroll
             for (int d = 0; d < K; ++d) rv[d] = GW == 1 ? rn[J][GW == 1 ? d : 0][cc] : xr(RX, y - 3, d, cc);
             double uo[KP];
-            if (r3 && colin[cc]) prec_w(rv, h3[cc], (double)(degx[cc] + e3), uo);
+            if (on(r3, cc)) prec_w(rv, h3[cc], -mdeg(cc, e3), uo);
             else
 #pragma unroll
               for (int i = 0; i < KP; ++i) uo[i] = 0.0;
@@ -426,13 +431,13 @@ __global__ void __launch_bounds__(m_threads(K, HITS), 1) cg_march_kernel(const C
             lr(rn[J][i], o);
 #pragma unroll
             for (int cc = 0; cc < CP; ++cc)
-              s2[J][i][cc] = (r3 && colin[cc]) ? fma(-(double)(degx[cc] + e3), rn[J][i][cc], (rn[J1][i][cc] + rn[J2][i][cc]) + o[cc])
+              s2[J][i][cc] = on(r3, cc) ? fma(mdeg(cc, e3), rn[J][i][cc], (rn[J1][i][cc] + rn[J2][i][cc]) + o[cc])
                                                : 0.0;
           } else {  // u_new rows: y-3 -> J, y-4 -> J1, y-5 -> J2; S2 row y-4 -> J1
             lr(un[J1][i], o);
 #pragma unroll
             for (int cc = 0; cc < CP; ++cc)
-              s2[J1][i][cc] = (r4 && colin[cc]) ? fma(-(double)(degx[cc] + e4), un[J1][i][cc], (un[J2][i][cc] + un[J][i][cc]) + o[cc])
+              s2[J1][i][cc] = on(r4, cc) ? fma(mdeg(cc, e4), un[J1][i][cc], (un[J2][i][cc] + un[J][i][cc]) + o[cc])
                                                 : 0.0;
           }
         }
@@ -449,14 +454,14 @@ __global__ void __launch_bounds__(m_threads(K, HITS), 1) cg_march_kernel(const C
               double w, uc, rc;
               double mix = 0.0;
               if (!PREC) {  // S2 rows y-5 (J2), y-4 (J1), y-3 (J); u = r_new row y-4 (J1)
-                const double d2v = fma(-(double)(degx[cc] + e4), s2[J1][i][cc], (s2[J2][i][cc] + s2[J][i][cc]) + o[cc]);
+                const double d2v = fma(mdeg(cc, e4), s2[J1][i][cc], (s2[J2][i][cc] + s2[J][i][cc]) + o[cc]);
 #pragma unroll
                 for (int d = 0; d < K; ++d) mix = fma(Mrow[i][d], GW == 1 ? rn[J1][GW == 1 ? d : 0][cc] : xr(RX, yc, d, cc), mix);
                 uc = rn[J1][i][cc];
                 rc = uc;
                 w = fma(h4[cc], mix, tau_c[i] * fma(kappa2, uc, d2v));
               } else {      // S2 rows y-6 (J), y-5 (J2), y-4 (J1); u_new row y-5 (J2); r_new row y-5 (RX)
-                const double d2v = fma(-(double)(degx[cc] + e5), s2[J2][i][cc], (s2[J][i][cc] + s2[J1][i][cc]) + o[cc]);
+                const double d2v = fma(mdeg(cc, e5), s2[J2][i][cc], (s2[J][i][cc] + s2[J1][i][cc]) + o[cc]);
 #pragma unroll
                 for (int d = 0; d < K; ++d) mix = fma(Mrow[i][d], GW == 1 ? un[J2][GW == 1 ? d : 0][cc] : xr(UX, yc, d, cc), mix);
                 uc = un[J2][i][cc];
@@ -496,10 +501,20 @@ __global__ void __launch_bounds__(m_threads(K, HITS), 1) cg_march_kernel(const C
         gsync();
         if (issuer && q >= q0 + 2) free_stage();
       };
-      for (int t = 0; t < C.nsteps; t += 3) {
-        step(std::integral_constant<int, 0>{}, t);
-        step(std::integral_constant<int, 1>{}, t + 1);
-        step(std::integral_constant<int, 2>{}, t + 2);
+      const bool interior = KCG_MINT && C.x0 - MH >= 1 && C.x0 - MH + BW <= side - 1 && C.ys - MH >= 1 &&
+                            C.ys - MH + C.nsteps <= side - 1;
+      if (KCG_MINT && interior) {
+        for (int t = 0; t < C.nsteps; t += 3) {
+          step(std::integral_constant<int, 0>{}, std::true_type{}, t);
+          step(std::integral_constant<int, 1>{}, std::true_type{}, t + 1);
+          step(std::integral_constant<int, 2>{}, std::true_type{}, t + 2);
+        }
+      } else {
+        for (int t = 0; t < C.nsteps; t += 3) {
+          step(std::integral_constant<int, 0>{}, std::false_type{}, t);
+          step(std::integral_constant<int, 1>{}, std::false_type{}, t + 1);
+          step(std::integral_constant<int, 2>{}, std::false_type{}, t + 2);
+        }
       }
       gsync();  // every warp is done with the unit's stages
       if (issuer)
