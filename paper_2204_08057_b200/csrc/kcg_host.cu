@@ -104,7 +104,7 @@ Layout layout_of(const kcg_desc* d, int nranks) {
   L.history = take((size_t)std::max(d->history_cap, 1) * 8);
   L.sync = take(4 * sizeof(unsigned));
   L.group = take(4 * sizeof(unsigned));
-  L.resid_partials = take(P * (size_t)kcg::apply_tiles_per_sys(rows, side) * 2 * 8);
+  L.resid_partials = take(P * (size_t)kcg::apply_tiles_per_sys(rows, side, d2) * 2 * 8);
   L.resid_out = take(P * 2 * 8);
   L.params_kron = take(P * sizeof(SysParams));
   L.params_syl = take(P * k * sizeof(SysParams));

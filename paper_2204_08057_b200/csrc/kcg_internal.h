@@ -393,7 +393,7 @@ cudaError_t launch_put(cudaStream_t s, const XrankPut& P);
 cudaError_t launch_xrank_sync(cudaStream_t s, const XrankSync& X);
 // dst[plane][nest(x,y)] = src[plane][y side + x] (to_nested) or the inverse gather.
 cudaError_t launch_permute(cudaStream_t s, const double* src, double* dst, size_t planes, int side, bool to_nested);
-int apply_tiles_per_sys(int rows, int side);
+int apply_tiles_per_sys(int rows, int side, bool d2);
 // Posterior variances (Hutchinson): z[p][c][pixel] = Rademacher(seed, probe, p, c, j) in the working
 // row-major layout, j = the pixel's index in the user layout; var (=|+=) z * x, times scale.
 cudaError_t launch_probe(cudaStream_t s, double* z, int P, int K, int side, bool nested, unsigned long long seed,

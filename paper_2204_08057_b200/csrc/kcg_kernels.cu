@@ -15,13 +15,17 @@ extern template struct CgEntry<7>;
 extern template struct CgEntry<8>;
 
 // --------------------------------------------------------------------------- apply / residual
-constexpr int AP_TY = 16, AP_TX = 64, AP_NT = 256;
+constexpr int AP_TX = 64, AP_NT = 256;
+#ifndef KCG_AP_TYD2
+#define KCG_AP_TYD2 8   // apply / residual tile rows with the D2 prior (two boxes in shared memory per block: 52 KB at 8 rows, 4 blocks per SM; 16 rows: 87 KB, 2 blocks -- paper workload residual pass 0.43 ms slower)
+#endif
+constexpr int ap_ty(bool d2) { return d2 ? KCG_AP_TYD2 : 16; }
 #ifndef KCG_AP_MINB
 #define KCG_AP_MINB 4  // resident blocks per SM for apply_kernel, K <= 4 (64 registers: 2.8x faster than 1 under ncu); 2 above
 #endif
 
-int apply_tiles_per_sys(int rows, int side) {
-  return ((rows + AP_TY - 1) / AP_TY) * ((side + AP_TX - 1) / AP_TX);
+int apply_tiles_per_sys(int rows, int side, bool d2) {
+  return ((rows + ap_ty(d2) - 1) / ap_ty(d2)) * ((side + AP_TX - 1) / AP_TX);
 }
 
 // RESID = false: y = G x.   RESID = true: partials[s][tile] = (||b - G x||^2, ||b||^2) over the
@@ -38,7 +42,7 @@ __global__ void __launch_bounds__(AP_NT, (K <= 4 ? KCG_AP_MINB : 2)) apply_kerne
                                                       int row0, int ghost, int nested,
                                                       const double* __restrict__ xg_top,
                                                       const double* __restrict__ xg_bot) {
-  constexpr int HA = D2 ? 2 : 1;
+  constexpr int HA = D2 ? 2 : 1, AP_TY = ap_ty(D2);
   constexpr int BW = AP_TX + 2 * HA, BH = AP_TY + 2 * HA, PLANE = BW * BH;
   extern __shared__ double xs[];  // [K][BH][BW], then (D2) D x [K][BH][BW], then E [n][K] if RESID
   __shared__ double red[2][AP_NT / 32];
@@ -354,11 +358,11 @@ static cudaError_t apply_t(cudaStream_t s, const SysParams* params, const double
                            const double* E, const double* hits, double* partials, int n_sys, int n, const SlabGeom& g,
                            const double* xg_top, const double* xg_bot) {
   constexpr int HA = D2 ? 2 : 1;
-  const size_t plane = (size_t)(AP_TX + 2 * HA) * (AP_TY + 2 * HA);
+  const size_t plane = (size_t)(AP_TX + 2 * HA) * (ap_ty(D2) + 2 * HA);
   const size_t sm = ((D2 ? 2 : 1) * (size_t)K * plane + (R ? (size_t)n * K : 0)) * sizeof(double);
   cudaError_t e = cudaFuncSetAttribute(apply_kernel<K, R, D2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
   if (e != cudaSuccess) return e;
-  dim3 gr(apply_tiles_per_sys(g.rows, g.side), n_sys);
+  dim3 gr(apply_tiles_per_sys(g.rows, g.side, D2), n_sys);
   apply_kernel<K, R, D2><<<gr, AP_NT, sm, s>>>(params, x, y, Y, E, hits, partials, n, g.side, g.rows, g.row0,
                                                g.hits_ghost, g.nested, xg_top, xg_bot);
   return cudaGetLastError();
@@ -380,7 +384,7 @@ cudaError_t launch_resid(int K, cudaStream_t s, const SysParams* params, const d
   if (g.d2) { KCG_DISPATCH(K, e = (apply_t<KK, true, true>(s, params, x, nullptr, Y, E, hits, partials, n_sys, n, g, xg_top, xg_bot))); }
   else { KCG_DISPATCH(K, e = (apply_t<KK, true, false>(s, params, x, nullptr, Y, E, hits, partials, n_sys, n, g, xg_top, xg_bot))); }
   if (e != cudaSuccess) return e;
-  reduce_pairs_kernel<<<n_sys, 256, 0, s>>>(partials, out, apply_tiles_per_sys(g.rows, g.side));
+  reduce_pairs_kernel<<<n_sys, 256, 0, s>>>(partials, out, apply_tiles_per_sys(g.rows, g.side, g.d2));
   return cudaGetLastError();
 }
 

@@ -24,6 +24,8 @@ VARIANTS = {
     "m4hc1k2g8": ["KCG_MCP4=1", "KCG_MKP4H=2", "KCG_MG4=8"],
     "m4hc1k4g8": ["KCG_MCP4=1", "KCG_MKP4H=4", "KCG_MG4Q=8"],
     "mint": ["KCG_MINT=1"],
+    "apty8": ["KCG_AP_TYD2=8"],
+    "apty4": ["KCG_AP_TYD2=4"],
     "m4hc1k4g9": ["KCG_MCP4=1", "KCG_MKP4H=4", "KCG_MG4Q=9"],
 }
 names = sys.argv[1:] or list(VARIANTS)
